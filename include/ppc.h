@@ -1,0 +1,157 @@
+/*
+ * ppc.h — C-ABI of the B200-native projected star-Q / tSVDQ engine.
+ *
+ * Plain pointers and sizes, no torch or C++ types. Every entry point replaces
+ * one function of the reference C++ API (/root/reference/proj/include/
+ * projprod/ *.hpp); the citation is next to each declaration. The C++ API
+ * mirror (include/projprod/ *.hpp, libprojprod.so) and the Python package
+ * (paper_2409_19402_b200) are thin callers of these symbols.
+ *
+ * Conventions
+ *   - FP64 everywhere; tensors are column-major, mode-1 fastest: entry
+ *     (i,j,k) of an n1 x n2 x n3 tensor lives at i + j*n1 + k*n1*n2
+ *     (tensor.hpp:13-19). The buffer is also the (n1*n2) x n3 tube matrix.
+ *   - Matrices are column-major. A transform basis Q is n3 x p.
+ *   - tSVDQ factor stacks are p contiguous column-major blocks: U (n1,k,p),
+ *     V (n2,k,p), S (k,p) — the exported layout of tools/main.cpp:212-217
+ *     and python/bindings.cpp:117-127.
+ *   - `loc` says where ALL array pointers of one call live: PPC_HOST (the
+ *     library copies in/out through the current stream) or PPC_DEVICE
+ *     (pointers are device memory of the current device; results are
+ *     stream-ordered and the call does not synchronize unless it returns a
+ *     host scalar). Scalar outputs (double*) are always host pointers.
+ *   - Caller-allocated outputs. Inputs are never modified.
+ *   - Return codes map onto the reference's exception taxonomy
+ *     (errors.hpp:9-37); ppc_last_error() holds the message (thread-local).
+ *   - Calls are reentrant across host threads; each thread has its own
+ *     current device and stream (ppc_set_device / ppc_set_stream).
+ */
+#ifndef PPC_H
+#define PPC_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PPC_VERSION 1
+
+typedef enum {
+    PPC_OK = 0,
+    PPC_SHAPE = 1,       /* shape_error            (errors.hpp:10-12) */
+    PPC_BOUNDS = 2,      /* bounds_error           (errors.hpp:15-17) */
+    PPC_ARGUMENT = 3,    /* argument_error         (errors.hpp:20-22) */
+    PPC_DEGENERATE = 4,  /* degenerate_input_error (errors.hpp:26-28) */
+    PPC_NUMERIC = 5,     /* numeric_error          (errors.hpp:31-33) */
+    PPC_FORMAT = 6,      /* format_error           (errors.hpp:36-38) */
+    PPC_CUDA = 7,        /* CUDA / NCCL runtime failure (no reference analogue) */
+    PPC_NO_DEVICE = 8    /* no usable sm_100 device: the engine has no CPU path */
+} ppc_status;
+
+enum { PPC_HOST = 0, PPC_DEVICE = 1 };
+
+const char* ppc_last_error(void);
+int ppc_version(void);
+
+/* ---- runtime ----------------------------------------------------------- */
+/* Number of visible CUDA devices (0 when none). PROJPROD_DEVICES caps it,
+ * mirroring PROJPROD_THREADS (parallel.cpp:13-27). */
+int ppc_device_count(void);
+int ppc_set_device(int device);
+/* Stream (cudaStream_t) used by this thread's subsequent calls; NULL = the
+ * library's own non-blocking stream. */
+int ppc_set_stream(void* stream);
+void* ppc_get_stream(void);
+int ppc_synchronize(void);
+/* Kernel launches issued by the library on this thread since the last reset
+ * (for the bench's gpu_launches count). */
+int64_t ppc_launch_count(int reset);
+/* Device timing of the most recent launch of the dominant kernel class
+ * ("gemm", "jacobi", ...) is not tracked here; bench.py times with events. */
+
+/* ---- L3 kernels (tensor.hpp, matrix_kernels.hpp) ------------------------ */
+/* tensor.hpp:87 / tensor.cpp:139-147: out = A x3 op(M).
+ * trans_m = 0: M is q x n3 (out tube matrix = T * M^T).
+ * trans_m = 1: M is n3 x q (out = A x3 M^T = T * M), the forward transform
+ * with Q passed directly (no Q^T copy, cf. decompositions.cpp:65). */
+int ppc_mode3_product(const double* A, int64_t n1, int64_t n2, int64_t n3,
+                      const double* M, int64_t q, int trans_m, double* out, int loc);
+
+/* tensor.hpp:90 / tensor.cpp:149-156: C(:,:,k) = A(:,:,k) B(:,:,k);
+ * A n1 x m x n3, B m x n2 x n3, C n1 x n2 x n3. */
+int ppc_facewise_product(const double* A, int64_t n1, int64_t m, int64_t n3,
+                         const double* B, int64_t n2, double* C, int loc);
+
+/* tensor.hpp:92 / tensor.cpp:158 (deterministic fixed-order reduction). */
+int ppc_frobenius_norm(const double* A, int64_t count, double* out, int loc);
+
+/* matrix_kernels.hpp:19-22 / matrix_kernels.cpp:29-46: batched thin SVD,
+ * keeping the leading k triplets (k = min(m,n) for svd(), 1 <= k for
+ * truncated_svd()). A is `batch` contiguous m x n blocks; U (m,k,batch),
+ * s (k,batch), V (n,k,batch). Sign rule of matrix_kernels.cpp:16-25. */
+int ppc_svd_batched(const double* A, int64_t m, int64_t n, int64_t batch, int64_t k,
+                    double* U, double* s, double* V, int loc);
+
+/* ---- L4 transforms (transforms.hpp) ------------------------------------- */
+/* transforms.hpp:49 / transforms.cpp:97-115: Q = U3(:,1:p) of the mode-3
+ * unfolding (Gram SYRK + symmetric top-p eigensolve on the device, sign rule
+ * on each column). sigma (nullable, host or device per loc) receives the p
+ * leading singular values of the unfolding; *completed (host, nullable) is
+ * set when p > min(n3, n1*n2) forced an orthonormal completion. */
+int ppc_data_dependent_q(const double* A, int64_t n1, int64_t n2, int64_t n3,
+                         int64_t p, double* Q, double* sigma, int* completed, int loc);
+
+/* transforms.hpp:67 / transforms.cpp:164-174: ||A - A x3 QQ^T||_F. */
+int ppc_projection_error(const double* A, int64_t n1, int64_t n2, int64_t n3,
+                         const double* Q, int64_t p, double* err, int loc);
+
+/* Host-side builders of the structured bases (tiny; transforms.cpp:33-95). */
+int ppc_dct_q(int64_t n3, int64_t p, double* Q);                          /* host */
+int ppc_haar_q(int64_t n3, int64_t p, double* Q);                         /* host */
+int ppc_random_orthogonal_q(int64_t n3, int64_t p, uint64_t seed, double* Q); /* host */
+int ppc_identity_q(int64_t n3, int64_t p, double* Q);                     /* host */
+/* transforms.cpp:20-27 + 100-109 of custom_transform: Stiefel check. */
+int ppc_check_stiefel(const double* Q, int64_t n3, int64_t p);            /* host */
+
+/* ---- L5 drivers (star_products.hpp, decompositions.hpp, metrics.hpp) ----- */
+/* star_products.hpp:28 / star_products.cpp:51-59:
+ * C = [(A x3 Q^T) facewise (B x3 Q^T)] x3 Q, times scale. */
+int ppc_star_q_product(const double* A, int64_t n1, int64_t m, int64_t n3,
+                       const double* B, int64_t n2, const double* Q, int64_t p,
+                       double scale, double* C, int loc);
+
+/* decompositions.hpp:90 / decompositions.cpp:62-83. */
+int ppc_tsvdq(const double* A, int64_t n1, int64_t n2, int64_t n3,
+              const double* Q, int64_t p, int64_t k,
+              double* U, double* S, double* V, int loc);
+
+/* decompositions.hpp:91 / decompositions.cpp:85-94. */
+int ppc_tsvdq_reconstruct(const double* U, const double* S, const double* V,
+                          const double* Q, int64_t n1, int64_t n2, int64_t n3,
+                          int64_t p, int64_t k, double* out, int loc);
+
+/* decompositions.hpp:92 / decompositions.cpp:96-103: (total, eckart_young,
+ * projection). total is measured directly against the reconstruction (fused
+ * on the device, never materialized); eckart_young comes from fresh slice
+ * SVDs of A x3 Q^T as in the reference. */
+int ppc_tsvdq_error(const double* A, int64_t n1, int64_t n2, int64_t n3,
+                    const double* U, const double* S, const double* V,
+                    const double* Q, int64_t p, int64_t k,
+                    double* total, double* eckart_young, double* projection, int loc);
+
+/* metrics.hpp:21 / metrics.cpp:21-28: ||A - Ahat|| / ||A||. */
+int ppc_relative_error(const double* A, const double* Ahat, int64_t count,
+                       double* re, int loc);
+
+/* Fused relative_error(A, tsvdq_reconstruct(F)) without materializing the
+ * reconstruction (tools/main.cpp:276-283 call chain). */
+int ppc_tsvdq_relative_error(const double* A, int64_t n1, int64_t n2, int64_t n3,
+                             const double* U, const double* S, const double* V,
+                             const double* Q, int64_t p, int64_t k,
+                             double* re, int loc);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PPC_H */

@@ -1,0 +1,265 @@
+"""ctypes front for the C oracle (oracle/libppo.so).
+
+TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and the
+cpu_baseline / --impl reference legs of bench.py — never by the product
+package. Arrays are numpy float64 in Fortran order with the reference's
+shapes: tensors (n1, n2, n3), Q (n3, p), factor stacks (n, k, p), s (k, p)
+(proj/python/bindings.cpp:22-46,117-127).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB = os.path.join(_HERE, "libppo.so")
+_lib = None
+
+ERRORS = {1: "shape_error", 2: "bounds_error", 3: "argument_error",
+          4: "degenerate_input_error", 5: "numeric_error"}
+
+
+class OracleError(ValueError):
+    def __init__(self, code, msg):
+        super().__init__(f"{ERRORS.get(code, code)}: {msg}")
+        self.code = code
+        self.kind = ERRORS.get(code, str(code))
+
+
+def build():
+    subprocess.run(["make", "-s", "-C", _HERE], check=True)
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB):
+            build()
+        L = C.CDLL(_LIB)
+        d, i64, pd = C.c_double, C.c_int64, C.POINTER(C.c_double)
+        L.ppo_last_error.restype = C.c_char_p
+        L.ppo_frobenius_norm.restype = d
+        L.ppo_derive_seed.restype = C.c_uint64
+        L.ppo_derive_seed.argtypes = [C.c_uint64, C.c_uint64]
+        L.ppo_xoshiro_normals.argtypes = [C.c_uint64, pd, i64]
+        L.ppo_xoshiro_normals.restype = None
+        L.ppo_random_orthogonal_q.argtypes = [i64, i64, C.c_uint64, pd]
+        _lib = L
+    return _lib
+
+
+def _p(a):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def _f(a):
+    return np.asfortranarray(np.asarray(a, dtype=np.float64))
+
+
+def _chk(rc):
+    if rc:
+        raise OracleError(rc, lib().ppo_last_error().decode())
+
+
+I = C.c_int64
+
+
+def set_threads(n: int):
+    lib().ppo_set_threads(int(n))
+
+
+def threads() -> int:
+    return lib().ppo_threads()
+
+
+def use_openblas() -> bool:
+    """Route oracle GEMMs through SciPy's bundled OpenBLAS (single-threaded),
+    standing in for Eigen's single-threaded GEMM in the CPU baseline."""
+    import glob
+    import scipy
+    libs = glob.glob(os.path.join(os.path.dirname(scipy.__file__), os.pardir,
+                                  "scipy.libs", "libscipy_openblas*.so"))
+    for path in libs:
+        rc = lib().ppo_use_blas(path.encode(), b"scipy_dgemm_",
+                                b"scipy_openblas_set_num_threads")
+        if rc == 0:
+            return True
+    return False
+
+
+def xoshiro_normals(seed: int, count: int) -> np.ndarray:
+    out = np.empty(count)
+    lib().ppo_xoshiro_normals(C.c_uint64(seed), _p(out), I(count))
+    return out
+
+
+def derive_seed(seed: int, stream: int) -> int:
+    return int(lib().ppo_derive_seed(seed, stream))
+
+
+def random_tensor(n1, n2, n3, seed):
+    """tests/support/common.hpp:45-48: xoshiro256++ normals in buffer order."""
+    return xoshiro_normals(seed, n1 * n2 * n3).reshape((n1, n2, n3), order="F")
+
+
+def random_matrix(m, n, seed):
+    return xoshiro_normals(seed, m * n).reshape((m, n), order="F")
+
+
+def frobenius_norm(a):
+    a = _f(a)
+    return lib().ppo_frobenius_norm(_p(a), I(a.size))
+
+
+def mode3_product(a, m):
+    a, m = _f(a), _f(m)
+    n1, n2, n3 = a.shape
+    q = m.shape[0]
+    if m.shape[1] != n3:
+        raise OracleError(1, "mode3_product: M cols != n3")
+    out = np.empty((n1, n2, q), order="F")
+    _chk(lib().ppo_mode3_product(_p(a), I(n1), I(n2), I(n3), _p(m), I(q), _p(out)))
+    return out
+
+
+def facewise_product(a, b):
+    a, b = _f(a), _f(b)
+    n1, m, n3 = a.shape
+    if b.shape[0] != m or b.shape[2] != n3:
+        raise OracleError(1, "facewise_product: shape mismatch")
+    n2 = b.shape[1]
+    out = np.empty((n1, n2, n3), order="F")
+    _chk(lib().ppo_facewise_product(_p(a), I(n1), I(m), I(n3), _p(b), I(n2), _p(out)))
+    return out
+
+
+def svd(a):
+    a = _f(a)
+    m, n = a.shape
+    r = min(m, n)
+    U = np.empty((m, r), order="F")
+    s = np.empty(r)
+    V = np.empty((n, r), order="F")
+    _chk(lib().ppo_svd(_p(a), I(m), I(n), _p(U), _p(s), _p(V)))
+    return U, s, V
+
+
+def orthonormalize(a):
+    a = _f(a)
+    n, p = a.shape
+    Q = np.empty((n, p), order="F")
+    _chk(lib().ppo_orthonormalize(_p(a), I(n), I(p), _p(Q)))
+    return Q
+
+
+def dct_q(n3, p):
+    Q = np.empty((n3, p), order="F")
+    _chk(lib().ppo_dct_q(I(n3), I(p), _p(Q)))
+    return Q
+
+
+def random_orthogonal_q(n3, p, seed):
+    Q = np.empty((n3, p), order="F")
+    _chk(lib().ppo_random_orthogonal_q(I(n3), I(p), C.c_uint64(seed), _p(Q)))
+    return Q
+
+
+def haar_q(n3, p):
+    """transforms.cpp:46-60 (host trivia, restated for the KAT fixtures)."""
+    if n3 == 2:
+        r = 1 / np.sqrt(2.0)
+        H = np.array([[r, r], [r, -r]])
+    elif n3 == 4:
+        s = np.sqrt(2.0)
+        # Eigen's comma initializer fills row by row (transforms.cpp:53-58)
+        H = 0.5 * np.array([[1, 1, 1, 1], [1, 1, -1, -1], [s, -s, 0, 0], [0, 0, s, -s]])
+    else:
+        raise OracleError(3, "haar_transform: n3 must be 2 or 4")
+    if p < 1 or p > n3:
+        raise OracleError(3, "transform: p outside [1,n3]")
+    return np.asfortranarray(H[:, :p])
+
+
+def data_dependent_q(a, p):
+    a = _f(a)
+    n1, n2, n3 = a.shape
+    Q = np.empty((n3, p), order="F")
+    sig = np.zeros(p)
+    comp = C.c_int(0)
+    _chk(lib().ppo_data_dependent_q(_p(a), I(n1), I(n2), I(n3), I(p), _p(Q), _p(sig),
+                                    C.byref(comp)))
+    return Q, sig, bool(comp.value)
+
+
+def projection_error(a, q):
+    a, q = _f(a), _f(q)
+    n1, n2, n3 = a.shape
+    err = C.c_double()
+    _chk(lib().ppo_projection_error(_p(a), I(n1), I(n2), I(n3), _p(q), I(q.shape[1]),
+                                    C.byref(err)))
+    return err.value
+
+
+def star_q_product(a, b, q, scale=1.0):
+    a, b, q = _f(a), _f(b), _f(q)
+    n1, m, n3 = a.shape
+    n2 = b.shape[1]
+    if b.shape[0] != m or b.shape[2] != n3 or q.shape[0] != n3:
+        raise OracleError(1, "star product: shape mismatch")
+    out = np.empty((n1, n2, n3), order="F")
+    _chk(lib().ppo_star_q_product(_p(a), I(n1), I(m), I(n3), _p(b), I(n2), _p(q),
+                                  I(q.shape[1]), C.c_double(scale), _p(out)))
+    return out
+
+
+def tsvdq(a, q, k):
+    a, q = _f(a), _f(q)
+    n1, n2, n3 = a.shape
+    p = q.shape[1]
+    U = np.empty((n1, k, p), order="F")
+    S = np.empty((k, p), order="F")
+    V = np.empty((n2, k, p), order="F")
+    _chk(lib().ppo_tsvdq(_p(a), I(n1), I(n2), I(n3), _p(q), I(p), I(k), _p(U), _p(S), _p(V)))
+    return U, S, V
+
+
+def slice_spectra(a, q):
+    a, q = _f(a), _f(q)
+    n1, n2, n3 = a.shape
+    p = q.shape[1]
+    s = np.empty((min(n1, n2), p), order="F")
+    _chk(lib().ppo_slice_spectra(_p(a), I(n1), I(n2), I(n3), _p(q), I(p), _p(s)))
+    return s
+
+
+def tsvdq_reconstruct(U, S, V, q, n3=None):
+    U, S, V, q = _f(U), _f(S), _f(V), _f(q)
+    n1, k, p = U.shape
+    n2 = V.shape[0]
+    n3 = q.shape[0]
+    out = np.empty((n1, n2, n3), order="F")
+    _chk(lib().ppo_tsvdq_reconstruct(_p(U), _p(S), _p(V), _p(q), I(n1), I(n2), I(n3), I(p),
+                                     I(k), _p(out)))
+    return out
+
+
+def tsvdq_error(a, U, S, V, q):
+    a, U, S, V, q = _f(a), _f(U), _f(S), _f(V), _f(q)
+    n1, n2, n3 = a.shape
+    k, p = S.shape
+    t, e, pr = C.c_double(), C.c_double(), C.c_double()
+    _chk(lib().ppo_tsvdq_error(_p(a), I(n1), I(n2), I(n3), _p(U), _p(S), _p(V), _p(q), I(p),
+                               I(k), C.byref(t), C.byref(e), C.byref(pr)))
+    return t.value, e.value, pr.value
+
+
+def relative_error(a, ahat):
+    a, ahat = _f(a), _f(ahat)
+    if a.shape != ahat.shape:
+        raise OracleError(1, "relative_error: shapes differ")
+    re = C.c_double()
+    _chk(lib().ppo_relative_error(_p(a), _p(ahat), I(a.size), C.byref(re)))
+    return re.value

@@ -1,0 +1,250 @@
+// C-ABI entry points (include/ppc.h). Each function validates its arguments
+// with the reference's checks and messages (thrown before any work starts, as
+// in tensor.cpp:140-142, decompositions.cpp:16-28, star_products.cpp:13-20),
+// then drives the device kernels on the calling thread's stream.
+#include <cmath>
+#include <string>
+
+#include "dmma_gemm.cuh"
+#include "internal.h"
+#include "jacobi.cuh"
+#include "kernels.cuh"
+#include "engine.h"
+
+using namespace ppc;
+
+namespace {
+
+std::string shp(int64_t a, int64_t b, int64_t c) {
+    return std::to_string(a) + "x" + std::to_string(b) + "x" + std::to_string(c);
+}
+
+void check_tensor(int64_t n1, int64_t n2, int64_t n3) {
+    if (n1 < 1 || n2 < 1 || n3 < 1)
+        fail(PPC_SHAPE, "tensor extents must be positive, got " + shp(n1, n2, n3));
+}
+
+// transforms.cpp:15-20
+void check_transform(int64_t n3, int64_t p) {
+    if (n3 < 1) fail(PPC_ARGUMENT, "transform: n3 must be positive");
+    if (p < 1 || p > n3)
+        fail(PPC_ARGUMENT,
+             "transform: p=" + std::to_string(p) + " outside [1," + std::to_string(n3) + "]");
+}
+
+// decompositions.cpp:23-28
+void check_spatial_rank(int64_t n1, int64_t n2, int64_t k, const char* who) {
+    const int64_t cap = n1 < n2 ? n1 : n2;
+    if (k < 1 || k > cap)
+        fail(PPC_ARGUMENT, std::string(who) + ": k=" + std::to_string(k) + " outside [1," +
+                               std::to_string(cap) + "]");
+}
+
+}  // namespace
+
+extern "C" {
+
+int ppc_mode3_product(const double* A, int64_t n1, int64_t n2, int64_t n3, const double* M,
+                      int64_t q, int trans_m, double* out, int loc) {
+    return guarded([&] {
+        validate_loc(loc);
+        check_tensor(n1, n2, n3);
+        if (q < 1) fail(PPC_SHAPE, "mode3_product: M must have at least one row");
+        const int64_t N = n1 * n2;
+        cudaStream_t s = stream();
+        In a(A, N * n3, loc), m(M, q * n3, loc);
+        Out o(out, N * q, loc);
+        mode3(a.d, N, n3, m.d, q, trans_m != 0, o.d, 1.0, s);
+        o.finish();
+        if (loc == PPC_HOST) PPC_CUDA_CHECK(cudaStreamSynchronize(s));
+    });
+}
+
+int ppc_facewise_product(const double* A, int64_t n1, int64_t m, int64_t n3, const double* B,
+                         int64_t n2, double* C, int loc) {
+    return guarded([&] {
+        validate_loc(loc);
+        check_tensor(n1, m, n3);
+        check_tensor(m, n2, n3);
+        cudaStream_t s = stream();
+        In a(A, n1 * m * n3, loc), b(B, m * n2 * n3, loc);
+        Out c(C, n1 * n2 * n3, loc);
+        facewise(a.d, n1, m, n3, b.d, n2, c.d, s);
+        c.finish();
+        if (loc == PPC_HOST) PPC_CUDA_CHECK(cudaStreamSynchronize(s));
+    });
+}
+
+int ppc_frobenius_norm(const double* A, int64_t count, double* out, int loc) {
+    return guarded([&] {
+        validate_loc(loc);
+        if (count < 0) fail(PPC_SHAPE, "frobenius_norm: negative count");
+        if (!out) fail(PPC_ARGUMENT, "null output");
+        cudaStream_t s = stream();
+        In a(A, count, loc);
+        double sums[2];
+        sumsq(a.d, nullptr, count, sums, s);
+        *out = std::sqrt(sums[1]);
+    });
+}
+
+int ppc_relative_error(const double* A, const double* Ahat, int64_t count, double* re, int loc) {
+    return guarded([&] {
+        validate_loc(loc);
+        if (count < 1) fail(PPC_SHAPE, "relative_error: shapes differ");
+        if (!re) fail(PPC_ARGUMENT, "null output");
+        cudaStream_t s = stream();
+        In a(A, count, loc), b(Ahat, count, loc);
+        double sums[2];
+        sumsq(a.d, b.d, count, sums, s);
+        // metrics.cpp:23-27
+        if (sums[1] == 0.0) fail(PPC_DEGENERATE, "relative_error: reference tensor is zero");
+        *re = std::sqrt(sums[0]) / std::sqrt(sums[1]);
+    });
+}
+
+int ppc_projection_error(const double* A, int64_t n1, int64_t n2, int64_t n3, const double* Q,
+                         int64_t p, double* err, int loc) {
+    return guarded([&] {
+        validate_loc(loc);
+        check_tensor(n1, n2, n3);
+        check_transform(n3, p);
+        if (!err) fail(PPC_ARGUMENT, "null output");
+        cudaStream_t s = stream();
+        const int64_t N = n1 * n2;
+        In a(A, N * n3, loc), q(Q, n3 * p, loc);
+        *err = std::sqrt(projection_residual(a.d, N, n3, q.d, p, nullptr, s)[0]);
+    });
+}
+
+int ppc_star_q_product(const double* A, int64_t n1, int64_t m, int64_t n3, const double* B,
+                       int64_t n2, const double* Q, int64_t p, double scale, double* C, int loc) {
+    return guarded([&] {
+        validate_loc(loc);
+        check_tensor(n1, m, n3);
+        check_tensor(m, n2, n3);
+        check_transform(n3, p);
+        cudaStream_t s = stream();
+        In a(A, n1 * m * n3, loc), b(B, m * n2 * n3, loc), q(Q, n3 * p, loc);
+        Out c(C, n1 * n2 * n3, loc);
+        star_q(a.d, n1, m, n3, b.d, n2, q.d, p, scale, c.d, s);
+        c.finish();
+        if (loc == PPC_HOST) PPC_CUDA_CHECK(cudaStreamSynchronize(s));
+    });
+}
+
+int ppc_svd_batched(const double* A, int64_t m, int64_t n, int64_t batch, int64_t k, double* U,
+                    double* S, double* V, int loc) {
+    return guarded([&] {
+        validate_loc(loc);
+        if (m < 1 || n < 1) fail(PPC_SHAPE, "svd: empty matrix");
+        if (batch < 1) fail(PPC_SHAPE, "svd: batch must be positive");
+        const int64_t r = m < n ? m : n;
+        if (k < 1 || k > r)
+            fail(PPC_ARGUMENT, "truncated_svd: k=" + std::to_string(k) + " outside [1," +
+                                   std::to_string(r) + "]");
+        cudaStream_t s = stream();
+        In a(A, m * n * batch, loc);
+        require_finite(a.d, m * n * batch, "svd", s);
+        Out u(U, m * k * batch, loc), sv(S, k * batch, loc), v(V, n * k * batch, loc);
+        slice_svd(a.d, m, n, m * n, batch, k, u.d, sv.d, v.d, nullptr, s);
+        u.finish();
+        sv.finish();
+        v.finish();
+        if (loc == PPC_HOST) PPC_CUDA_CHECK(cudaStreamSynchronize(s));
+    });
+}
+
+int ppc_data_dependent_q(const double* A, int64_t n1, int64_t n2, int64_t n3, int64_t p,
+                         double* Q, double* sigma, int* completed, int loc) {
+    return guarded([&] {
+        validate_loc(loc);
+        check_transform(n3, p);  // transforms.cpp:98
+        check_tensor(n1, n2, n3);
+        cudaStream_t s = stream();
+        const int64_t N = n1 * n2;
+        In a(A, N * n3, loc);
+        require_finite(a.d, N * n3, "svd", s);
+        Out q(Q, n3 * p, loc);
+        Out sg(sigma, sigma ? p : 0, loc);
+        const bool comp = data_q(a.d, N, n3, p, q.d, sigma ? sg.d : nullptr, s);
+        if (completed) *completed = comp ? 1 : 0;
+        q.finish();
+        if (sigma) sg.finish();
+        if (loc == PPC_HOST) PPC_CUDA_CHECK(cudaStreamSynchronize(s));
+    });
+}
+
+int ppc_tsvdq(const double* A, int64_t n1, int64_t n2, int64_t n3, const double* Q, int64_t p,
+              int64_t k, double* U, double* S, double* V, int loc) {
+    return guarded([&] {
+        validate_loc(loc);
+        check_tensor(n1, n2, n3);
+        check_transform(n3, p);
+        check_spatial_rank(n1, n2, k, "tsvdq");
+        cudaStream_t s = stream();
+        In a(A, n1 * n2 * n3, loc), q(Q, n3 * p, loc);
+        Out u(U, n1 * k * p, loc), sv(S, k * p, loc), v(V, n2 * k * p, loc);
+        tsvdq(a.d, n1, n2, n3, q.d, p, k, u.d, sv.d, v.d, s);
+        u.finish();
+        sv.finish();
+        v.finish();
+        if (loc == PPC_HOST) PPC_CUDA_CHECK(cudaStreamSynchronize(s));
+    });
+}
+
+int ppc_tsvdq_reconstruct(const double* U, const double* S, const double* V, const double* Q,
+                          int64_t n1, int64_t n2, int64_t n3, int64_t p, int64_t k, double* out,
+                          int loc) {
+    return guarded([&] {
+        validate_loc(loc);
+        check_tensor(n1, n2, n3);
+        check_transform(n3, p);
+        check_spatial_rank(n1, n2, k, "tsvdq_reconstruct");
+        cudaStream_t s = stream();
+        In u(U, n1 * k * p, loc), sv(S, k * p, loc), v(V, n2 * k * p, loc), q(Q, n3 * p, loc);
+        Out o(out, n1 * n2 * n3, loc);
+        reconstruct(u.d, sv.d, v.d, q.d, n1, n2, n3, p, k, o.d, s);
+        o.finish();
+        if (loc == PPC_HOST) PPC_CUDA_CHECK(cudaStreamSynchronize(s));
+    });
+}
+
+int ppc_tsvdq_error(const double* A, int64_t n1, int64_t n2, int64_t n3, const double* U,
+                    const double* S, const double* V, const double* Q, int64_t p, int64_t k,
+                    double* total, double* eckart_young, double* projection, int loc) {
+    return guarded([&] {
+        validate_loc(loc);
+        check_tensor(n1, n2, n3);
+        check_transform(n3, p);  // decompositions.cpp:97 check_transform_match
+        check_spatial_rank(n1, n2, k, "tsvdq_error");
+        if (!total || !eckart_young || !projection) fail(PPC_ARGUMENT, "null output");
+        cudaStream_t s = stream();
+        In a(A, n1 * n2 * n3, loc), u(U, n1 * k * p, loc), sv(S, k * p, loc), v(V, n2 * k * p, loc),
+            q(Q, n3 * p, loc);
+        const ErrorParts e = tsvdq_error(a.d, n1, n2, n3, u.d, sv.d, v.d, q.d, p, k, s);
+        *total = e.total;
+        *eckart_young = e.eckart_young;
+        *projection = e.projection;
+    });
+}
+
+int ppc_tsvdq_relative_error(const double* A, int64_t n1, int64_t n2, int64_t n3, const double* U,
+                             const double* S, const double* V, const double* Q, int64_t p,
+                             int64_t k, double* re, int loc) {
+    return guarded([&] {
+        validate_loc(loc);
+        check_tensor(n1, n2, n3);
+        check_transform(n3, p);
+        check_spatial_rank(n1, n2, k, "tsvdq_relative_error");
+        if (!re) fail(PPC_ARGUMENT, "null output");
+        cudaStream_t s = stream();
+        In a(A, n1 * n2 * n3, loc), u(U, n1 * k * p, loc), sv(S, k * p, loc), v(V, n2 * k * p, loc),
+            q(Q, n3 * p, loc);
+        const auto r = recon_residual(a.d, n1, n2, n3, u.d, sv.d, v.d, q.d, p, k, s);
+        if (r[1] == 0.0) fail(PPC_DEGENERATE, "relative_error: reference tensor is zero");
+        *re = std::sqrt(r[0]) / std::sqrt(r[1]);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,169 @@
+// Device-level hot path (see engine.h). Every GEMM-shaped stage runs on the
+// FP64 DMMA kernel (dmma_gemm.cuh); reductions are fixed-order.
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "dmma_gemm.cuh"
+#include "engine.h"
+#include "internal.h"
+#include "jacobi.cuh"
+#include "kernels.cuh"
+#include "slice_svd.cuh"
+
+namespace ppc {
+
+void mode3(const double* T, int64_t N, int64_t n3, const double* M, int64_t q, bool trans_m,
+           double* out, double alpha, cudaStream_t s) {
+    GemmDesc d;
+    d.M = N; d.N = q; d.K = n3;
+    d.A = T; d.lda = N; d.a_kmajor = false;
+    d.B = M;
+    if (trans_m) {  // B(k,n) = M[k + n*n3]
+        d.ldb = n3; d.b_nmajor = false;
+    } else {        // B(k,n) = M^T(k,n) = M[n + k*q]
+        d.ldb = q; d.b_nmajor = true;
+    }
+    d.C = out; d.ldc = N;
+    d.alpha = alpha;
+    gemm(d, s);
+}
+
+void facewise(const double* A, int64_t n1, int64_t m, int64_t p, const double* B, int64_t n2,
+              double* C, cudaStream_t s) {
+    GemmDesc d;
+    d.M = n1; d.N = n2; d.K = m; d.batch = p;
+    d.A = A; d.lda = n1; d.strideA = n1 * m;
+    d.B = B; d.ldb = m; d.strideB = m * n2;
+    d.C = C; d.ldc = n1; d.strideC = n1 * n2;
+    gemm(d, s);
+}
+
+void star_q(const double* A, int64_t n1, int64_t m, int64_t n3, const double* B, int64_t n2,
+            const double* Q, int64_t p, double scale, double* C, cudaStream_t s) {
+    DeviceBuffer ah(sizeof(double) * n1 * m * p), bh(sizeof(double) * m * n2 * p),
+        ch(sizeof(double) * n1 * n2 * p);
+    mode3(A, n1 * m, n3, Q, p, true, ah.d(), 1.0, s);   // A x3 Q^T
+    mode3(B, m * n2, n3, Q, p, true, bh.d(), 1.0, s);   // B x3 Q^T
+    facewise(ah.d(), n1, m, p, bh.d(), n2, ch.d(), s);   // facewise
+    mode3(ch.d(), n1 * n2, p, Q, n3, false, C, scale, s);  // x3 Q, scale in the epilogue
+}
+
+void sumsq(const double* a, const double* b, int64_t count, double sums[2], cudaStream_t s) {
+    DeviceBuffer part(sizeof(double) * 2 * (kReduceBlocks + 1));
+    double* fin = part.d() + 2 * kReduceBlocks;
+    launch_sumsq_partials(a, b, count, part.d(), s);
+    launch_reduce_pairs(part.d(), kReduceBlocks, fin, s);
+    PPC_CUDA_CHECK(cudaMemcpyAsync(sums, fin, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    PPC_CUDA_CHECK(cudaStreamSynchronize(s));
+}
+
+namespace {
+// Fused residual GEMM: {sum (X - alpha op(A)op(B))^2, sum X^2} as host doubles.
+std::array<double, 2> residual_sums(const GemmDesc& d, const double* X, int64_t ldx,
+                                    int64_t strideX, cudaStream_t s) {
+    const int64_t ctas = gemm_residual_ctas(d);
+    DeviceBuffer part(sizeof(double) * 2 * (ctas + 1));
+    gemm_residual(d, X, ldx, strideX, part.d(), s);
+    double* fin = part.d() + 2 * ctas;
+    launch_reduce_pairs(part.d(), ctas, fin, s);
+    std::array<double, 2> out{};
+    PPC_CUDA_CHECK(cudaMemcpyAsync(out.data(), fin, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    PPC_CUDA_CHECK(cudaStreamSynchronize(s));
+    return out;
+}
+}  // namespace
+
+std::array<double, 2> projection_residual(const double* T, int64_t N, int64_t n3, const double* Q,
+                                          int64_t p, const double* coeff, cudaStream_t s) {
+    DeviceBuffer cbuf;
+    if (!coeff) {
+        cbuf = DeviceBuffer(sizeof(double) * N * p);
+        mode3(T, N, n3, Q, p, true, cbuf.d(), 1.0, s);
+        coeff = cbuf.d();
+    }
+    // residual of T against coeff (N x p) * Q^T (p x n3): B(k,n) = Q[n + k*n3]
+    GemmDesc d;
+    d.M = N; d.N = n3; d.K = p;
+    d.A = coeff; d.lda = N;
+    d.B = Q; d.ldb = n3; d.b_nmajor = true;
+    return residual_sums(d, T, N, 0, s);
+}
+
+void require_finite(const double* x, int64_t n, const char* who, cudaStream_t s) {
+    DeviceBuffer flag(sizeof(int) * 2);
+    PPC_CUDA_CHECK(cudaMemsetAsync(flag.as<int>(), 0, sizeof(int), s));
+    launch_nonfinite(x, n, flag.as<int>(), s);
+    int h = 0;
+    PPC_CUDA_CHECK(cudaMemcpyAsync(&h, flag.as<int>(), sizeof(int), cudaMemcpyDeviceToHost, s));
+    PPC_CUDA_CHECK(cudaStreamSynchronize(s));
+    if (h) fail(PPC_NUMERIC, std::string(who) + ": input has non-finite entries");
+}
+
+void core_from_factors(const double* U, const double* S, const double* V, int64_t n1, int64_t n2,
+                       int64_t p, int64_t k, double* Chat, cudaStream_t s) {
+    DeviceBuffer us(sizeof(double) * n1 * k * p);
+    launch_scale_columns(U, S, us.d(), n1, k, p, s);
+    // Chat_i (n1 x n2) = US_i (n1 x k) * V_i^T: B(kk, n) = V_i[n + kk*n2]
+    GemmDesc d;
+    d.M = n1; d.N = n2; d.K = k; d.batch = p;
+    d.A = us.d(); d.lda = n1; d.strideA = n1 * k;
+    d.B = V; d.ldb = n2; d.strideB = n2 * k; d.b_nmajor = true;
+    d.C = Chat; d.ldc = n1; d.strideC = n1 * n2;
+    gemm(d, s);
+}
+
+void reconstruct(const double* U, const double* S, const double* V, const double* Q, int64_t n1,
+                 int64_t n2, int64_t n3, int64_t p, int64_t k, double* out, cudaStream_t s) {
+    DeviceBuffer ch(sizeof(double) * n1 * n2 * p);
+    core_from_factors(U, S, V, n1, n2, p, k, ch.d(), s);
+    mode3(ch.d(), n1 * n2, p, Q, n3, false, out, 1.0, s);
+}
+
+std::array<double, 2> recon_residual(const double* A, int64_t n1, int64_t n2, int64_t n3,
+                                     const double* U, const double* S, const double* V,
+                                     const double* Q, int64_t p, int64_t k, cudaStream_t s) {
+    const int64_t N = n1 * n2;
+    DeviceBuffer ch(sizeof(double) * N * p);
+    core_from_factors(U, S, V, n1, n2, p, k, ch.d(), s);
+    GemmDesc d;
+    d.M = N; d.N = n3; d.K = p;
+    d.A = ch.d(); d.lda = N;
+    d.B = Q; d.ldb = n3; d.b_nmajor = true;
+    return residual_sums(d, A, N, 0, s);
+}
+
+void tsvdq(const double* A, int64_t n1, int64_t n2, int64_t n3, const double* Q, int64_t p,
+           int64_t k, double* U, double* S, double* V, cudaStream_t s) {
+    const int64_t N = n1 * n2;
+    DeviceBuffer ah(sizeof(double) * N * p);
+    mode3(A, N, n3, Q, p, true, ah.d(), 1.0, s);  // decompositions.cpp:65
+    require_finite(ah.d(), N * p, "svd", s);       // matrix_kernels.cpp:32
+    slice_svd(ah.d(), n1, n2, N, p, k, U, S, V, nullptr, s);  // :75-81
+}
+
+ErrorParts tsvdq_error(const double* A, int64_t n1, int64_t n2, int64_t n3, const double* U,
+                       const double* S, const double* V, const double* Q, int64_t p, int64_t k,
+                       cudaStream_t s) {
+    const int64_t N = n1 * n2;
+    // :97-100 recompute A x3 Q^T and fresh slice SVDs for the tail energies
+    DeviceBuffer ah(sizeof(double) * N * p);
+    mode3(A, N, n3, Q, p, true, ah.d(), 1.0, s);
+    require_finite(ah.d(), N * p, "svd", s);
+    DeviceBuffer tail(sizeof(double) * p), tsum(sizeof(double) * 2 * 2);
+    {
+        DeviceBuffer u(sizeof(double) * n1 * k * p), sv(sizeof(double) * k * p),
+            v(sizeof(double) * n2 * k * p);
+        slice_svd(ah.d(), n1, n2, N, p, k, u.d(), sv.d(), v.d(), tail.d(), s);
+    }
+    std::vector<double> th(p);
+    PPC_CUDA_CHECK(cudaMemcpyAsync(th.data(), tail.d(), sizeof(double) * p, cudaMemcpyDeviceToHost, s));
+    // :51-58 total measured directly against the reconstruction (fused)
+    const auto tot = recon_residual(A, n1, n2, n3, U, S, V, Q, p, k, s);
+    const auto pr = projection_residual(A, N, n3, Q, p, ah.d(), s);
+    double ey = 0.0;
+    for (int64_t i = 0; i < p; ++i) ey += th[i];  // decompositions.cpp:41-49 order (slice-major)
+    return ErrorParts{std::sqrt(tot[0]), std::sqrt(ey), std::sqrt(pr[0])};
+}
+
+}  // namespace ppc

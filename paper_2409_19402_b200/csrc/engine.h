@@ -1,0 +1,65 @@
+// Device-level building blocks of the hot path (device pointers, one stream).
+// The C-ABI (api.cu) stages host data and calls these; the multi-GPU driver
+// composes them per shard.
+#pragma once
+
+#include <array>
+#include <cstdint>
+
+#include <cuda_runtime.h>
+
+namespace ppc {
+
+// out (N x q) = alpha * T (N x n3) * op(M):  trans_m=false: M is q x n3 (M^T);
+// trans_m=true: M is n3 x q (the basis Q itself).       [tensor.cpp:139-147]
+void mode3(const double* T, int64_t N, int64_t n3, const double* M, int64_t q, bool trans_m,
+           double* out, double alpha, cudaStream_t s);
+// C(:,:,i) = A(:,:,i) B(:,:,i), i < p                     [tensor.cpp:149-156]
+void facewise(const double* A, int64_t n1, int64_t m, int64_t p, const double* B, int64_t n2,
+              double* C, cudaStream_t s);
+// star_products.cpp:51-59
+void star_q(const double* A, int64_t n1, int64_t m, int64_t n3, const double* B, int64_t n2,
+            const double* Q, int64_t p, double scale, double* C, cudaStream_t s);
+// host sums[0] = sum (a-b)^2 (or a^2 when b == nullptr), sums[1] = sum a^2.
+void sumsq(const double* a, const double* b, int64_t count, double sums[2], cudaStream_t s);
+// {||T - T Q Q^T||^2, ||T||^2}; coeff (N x p) may be supplied if already known.
+std::array<double, 2> projection_residual(const double* T, int64_t N, int64_t n3, const double* Q,
+                                          int64_t p, const double* coeff, cudaStream_t s);
+// numeric_error if any entry is non-finite (matrix_kernels.cpp:32).
+void require_finite(const double* x, int64_t n, const char* who, cudaStream_t s);
+
+// Batched thin SVD (leading k triplets) of `batch` m x n blocks at `stride`.
+// tail2 (device, nullable, length batch): sum_{j>=k} s_j^2 per block.
+void slice_svd(const double* A, int64_t m, int64_t n, int64_t stride, int64_t batch, int64_t k,
+               double* U, double* S, double* V, double* tail2, cudaStream_t s);
+
+// Deterministic Gram G = T^T T (n3 x n3) over the N rows of T (SYRK).
+void gram(const double* T, int64_t N, int64_t n3, double* G, cudaStream_t s);
+// Top-p eigenpairs of a symmetric PSD n x n matrix G: Q (n x p), lambda (p).
+void sym_eig_top(const double* G, int64_t n, int64_t p, double* Q, double* lambda, cudaStream_t s);
+// transforms.cpp:97-115 on the device. Returns completed_basis.
+bool data_q(const double* T, int64_t N, int64_t n3, int64_t p, double* Q, double* sigma,
+            cudaStream_t s);
+
+// decompositions.cpp:62-83
+void tsvdq(const double* A, int64_t n1, int64_t n2, int64_t n3, const double* Q, int64_t p,
+           int64_t k, double* U, double* S, double* V, cudaStream_t s);
+// Chat (n1 x n2 x p) = U diag(S) V^T facewise             [decompositions.cpp:88-92]
+void core_from_factors(const double* U, const double* S, const double* V, int64_t n1, int64_t n2,
+                       int64_t p, int64_t k, double* Chat, cudaStream_t s);
+// decompositions.cpp:85-94
+void reconstruct(const double* U, const double* S, const double* V, const double* Q, int64_t n1,
+                 int64_t n2, int64_t n3, int64_t p, int64_t k, double* out, cudaStream_t s);
+// {||A - recon(F)||^2, ||A||^2} without materializing recon(F).
+std::array<double, 2> recon_residual(const double* A, int64_t n1, int64_t n2, int64_t n3,
+                                     const double* U, const double* S, const double* V,
+                                     const double* Q, int64_t p, int64_t k, cudaStream_t s);
+struct ErrorParts {
+    double total, eckart_young, projection;
+};
+// decompositions.cpp:96-103
+ErrorParts tsvdq_error(const double* A, int64_t n1, int64_t n2, int64_t n3, const double* U,
+                       const double* S, const double* V, const double* Q, int64_t p, int64_t k,
+                       cudaStream_t s);
+
+}  // namespace ppc

@@ -1,0 +1,115 @@
+// Internal runtime of the ppc engine: per-thread context, error plumbing,
+// stream-ordered workspace, launch accounting. Not part of the C-ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <new>
+#include <string>
+
+#include "ppc.h"
+
+namespace ppc {
+
+// Typed failure carried from deep inside the engine to the C-ABI boundary,
+// where it becomes a status code + ppc_last_error() message.
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] inline void fail(int code, const std::string& msg) { throw Error(code, msg); }
+
+inline void cuda_check(cudaError_t e, const char* what, const char* file, int line) {
+    if (e != cudaSuccess)
+        fail(PPC_CUDA, std::string(what) + ": " + cudaGetErrorString(e) + " (" + file + ":" +
+                           std::to_string(line) + ")");
+}
+#define PPC_CUDA_CHECK(x) ::ppc::cuda_check((x), #x, __FILE__, __LINE__)
+
+// Per-thread execution context.
+struct Context {
+    int device = -1;
+    cudaStream_t stream = nullptr;      // user stream (ppc_set_stream) or own
+    cudaStream_t own_stream = nullptr;  // created lazily per device
+    int sms = 148;
+    int64_t launches = 0;
+};
+Context& ctx();               // ensures a device is selected (throws PPC_NO_DEVICE)
+cudaStream_t stream();        // current stream of this thread
+inline void count_launch(int n = 1) { ctx().launches += n; }
+void check_launch(const char* name);  // cudaGetLastError -> PPC_CUDA
+
+// Stream-ordered device buffer (cudaMallocAsync on the current stream; the
+// default mempool keeps freed blocks, so steady-state calls do not hit the OS).
+class DeviceBuffer {
+public:
+    DeviceBuffer() = default;
+    explicit DeviceBuffer(size_t bytes);
+    ~DeviceBuffer();
+    DeviceBuffer(const DeviceBuffer&) = delete;
+    DeviceBuffer& operator=(const DeviceBuffer&) = delete;
+    DeviceBuffer(DeviceBuffer&& o) noexcept : p_(o.p_), n_(o.n_) { o.p_ = nullptr; o.n_ = 0; }
+    DeviceBuffer& operator=(DeviceBuffer&& o) noexcept {
+        if (this != &o) {
+            release();
+            p_ = o.p_;
+            n_ = o.n_;
+            o.p_ = nullptr;
+            o.n_ = 0;
+        }
+        return *this;
+    }
+    void release();
+    double* d() const { return static_cast<double*>(p_); }
+    template <typename T> T* as() const { return static_cast<T*>(p_); }
+    size_t bytes() const { return n_; }
+private:
+    void* p_ = nullptr;
+    size_t n_ = 0;
+};
+
+// Input/output staging for loc = PPC_HOST: device copies on the current
+// stream; for PPC_DEVICE the pointers are passed through untouched.
+struct In {
+    const double* d = nullptr;
+    DeviceBuffer buf;
+    In(const double* p, size_t count, int loc);
+};
+struct Out {
+    double* d = nullptr;
+    double* host = nullptr;
+    size_t count = 0;
+    DeviceBuffer buf;
+    Out(double* p, size_t count, int loc);
+    void finish();  // D2H for host outputs
+};
+
+void validate_loc(int loc);
+void require_positive(int64_t v, const char* what);
+
+void set_error(const std::string& m);
+const char* last_error();
+
+// Run a C-ABI body, mapping exceptions to status codes + last_error.
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return PPC_OK;
+    } catch (const Error& e) {
+        set_error(e.what());
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        set_error("host allocation failed");
+        return PPC_CUDA;
+    } catch (const std::exception& e) {
+        set_error(e.what());
+        return PPC_CUDA;
+    }
+}
+
+}  // namespace ppc

@@ -1,0 +1,299 @@
+// K6 — batched one-sided (Hestenes) Jacobi SVD, one CTA per matrix.
+//
+// Replaces Eigen::JacobiSVD(ComputeThinU|ComputeThinV) + fix_svd_signs
+// (matrix_kernels.cpp:15-37) for small slices, and serves as the small dense
+// symmetric eigensolver of the engine: for a symmetric PSD H, the one-sided
+// rotations that orthogonalize H's columns accumulate H's eigenvectors in V
+// and the column norms of H V are its eigenvalues.
+//
+// Parallel round-robin ("circle") ordering: each round pairs all columns
+// disjointly, one warp per pair; dot products are reduced in a fixed lane
+// order (deterministic). Working set (W = R x C, V = C x C) lives in shared
+// memory when it fits (<= ~200 KB), else in a global workspace (L2-resident
+// for the sizes that reach this path).
+#include <cfloat>
+
+#include "internal.h"
+#include "jacobi.cuh"
+#include "kernels.cuh"
+
+namespace ppc {
+
+namespace {
+
+constexpr double kEps = 2.220446049250313e-16;
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__global__ void jacobi_svd_kernel(const double* __restrict__ A, int64_t m, int64_t n,
+                                  int64_t strideA, int64_t k, double* __restrict__ U,
+                                  double* __restrict__ S, double* __restrict__ V, double* gws,
+                                  int use_smem, double* tail2) {
+    extern __shared__ __align__(16) double sm[];
+    __shared__ int s_rot;
+    const int64_t b = blockIdx.x;
+    const bool tall = m >= n;
+    const int64_t R = tall ? m : n, Cc = tall ? n : m;
+    double* W;
+    double* Va;
+    if (use_smem) {
+        W = sm;
+        Va = sm + R * Cc;
+    } else {
+        W = gws + b * (R * Cc + Cc * Cc + 2 * Cc);
+        Va = W + R * Cc;
+    }
+    double* sig = use_smem ? (Va + Cc * Cc) : (Va + Cc * Cc);
+    int* rank = reinterpret_cast<int*>(sig + Cc);
+    const double* Ab = A + b * strideA;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
+
+    // load W (= A, or A^T for wide inputs) and V = I
+    for (int64_t i = tid; i < R * Cc; i += nt) {
+        const int64_t r = i % R, c = i / R;
+        W[i] = tall ? Ab[r + c * m] : Ab[c + r * m];
+    }
+    for (int64_t i = tid; i < Cc * Cc; i += nt) Va[i] = (i % Cc == i / Cc) ? 1.0 : 0.0;
+    __syncthreads();
+
+    const double tol = kEps * sqrt((double)R);
+    const int64_t P = (Cc + 1) & ~int64_t(1);  // players, padded to even
+    int sweep = 0;
+    for (; sweep < 60 && Cc > 1; ++sweep) {
+        if (tid == 0) s_rot = 0;
+        __syncthreads();
+        for (int64_t r = 0; r < P - 1; ++r) {
+            for (int64_t pi = warp; pi < P / 2; pi += nw) {
+                int64_t a, c;
+                if (pi == 0) {
+                    a = r;
+                    c = P - 1;
+                } else {
+                    a = (r + pi) % (P - 1);
+                    c = (r + P - 1 - pi) % (P - 1);
+                }
+                if (a > c) { int64_t t = a; a = c; c = t; }
+                if (c >= Cc) continue;  // dummy player
+                double* wa = W + a * R;
+                double* wc = W + c * R;
+                double al = 0.0, be = 0.0, ga = 0.0;
+                for (int64_t i = lane; i < R; i += 32) {
+                    const double x = wa[i], y = wc[i];
+                    al = fma(x, x, al);
+                    be = fma(y, y, be);
+                    ga = fma(x, y, ga);
+                }
+                al = warp_sum(al);
+                be = warp_sum(be);
+                ga = warp_sum(ga);
+                if (ga == 0.0 || !(fabs(ga) > tol * sqrt(al * be))) continue;
+                const double zeta = (be - al) / (2.0 * ga);
+                const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+                const double cs = rsqrt(1.0 + tt * tt), sn = cs * tt;
+                for (int64_t i = lane; i < R; i += 32) {
+                    const double x = wa[i], y = wc[i];
+                    wa[i] = cs * x - sn * y;
+                    wc[i] = sn * x + cs * y;
+                }
+                double* va = Va + a * Cc;
+                double* vc = Va + c * Cc;
+                for (int64_t i = lane; i < Cc; i += 32) {
+                    const double x = va[i], y = vc[i];
+                    va[i] = cs * x - sn * y;
+                    vc[i] = sn * x + cs * y;
+                }
+                if (lane == 0) s_rot = 1;
+            }
+            __syncthreads();
+        }
+        if (!s_rot) break;
+        __syncthreads();
+    }
+
+    // singular values = column norms
+    for (int64_t c = warp; c < Cc; c += nw) {
+        double acc = 0.0;
+        for (int64_t i = lane; i < R; i += 32) acc = fma(W[c * R + i], W[c * R + i], acc);
+        acc = warp_sum(acc);
+        if (lane == 0) sig[c] = sqrt(acc);
+    }
+    __syncthreads();
+    // stable descending rank
+    for (int64_t c = tid; c < Cc; c += nt) {
+        const double sc = sig[c];
+        int rk = 0;
+        for (int64_t j = 0; j < Cc; ++j) {
+            const double sj = sig[j];
+            rk += (sj > sc) || (sj == sc && j < c);
+        }
+        rank[c] = rk;
+    }
+    __syncthreads();
+    double smax = 0.0;
+    for (int64_t c = 0; c < Cc; ++c) smax = fmax(smax, sig[c]);
+    if (tid == 0 && tail2) {  // discarded energy, decompositions.cpp:41-49
+        double acc = 0.0;
+        for (int64_t c = 0; c < Cc; ++c)
+            if (rank[c] >= k) acc = fma(sig[c], sig[c], acc);
+        tail2[b] = acc;
+    }
+    const double ztol = smax * kEps * (double)R;
+
+    // outputs: the wide case swaps roles (A^T = U' S V'^T => A = V' S U'^T)
+    double* Uo = U ? U + b * m * k : nullptr;
+    double* Vo = V ? V + b * n * k : nullptr;
+    double* Ltall = tall ? Uo : Vo;  // receives normalized W columns (R rows)
+    double* Lrot = tall ? Vo : Uo;   // receives rotation columns (Cc rows)
+    for (int64_t c = warp; c < Cc; c += nw) {
+        const int64_t o = rank[c];
+        if (o >= k) continue;
+        const double s = sig[c];
+        if (lane == 0 && S) S[b * k + o] = s;
+        if (Ltall) {
+            const double inv = (s > ztol && s > 0.0) ? 1.0 / s : 0.0;
+            for (int64_t i = lane; i < R; i += 32) Ltall[o * R + i] = W[c * R + i] * inv;
+        }
+        if (Lrot)
+            for (int64_t i = lane; i < Cc; i += 32) Lrot[o * Cc + i] = Va[c * Cc + i];
+    }
+    __syncthreads();
+    if (!U) return;  // eigen mode: no left vectors, no sign rule needed by callers
+    // orthonormal completion of zero-sigma columns of the tall factor
+    // (JacobiSVD's thin U is always orthonormal), warp 0, in column order
+    if (Ltall && warp == 0) {
+        for (int64_t o = 0; o < k && o < Cc; ++o) {
+            // find sigma of output column o
+            double so = 0.0;
+            for (int64_t c = 0; c < Cc; ++c)
+                if (rank[c] == o) so = sig[c];
+            if (so > ztol && so > 0.0) continue;
+            double* col = Ltall + o * R;
+            for (int64_t e = 0; e < R; ++e) {
+                for (int64_t i = lane; i < R; i += 32) col[i] = (i == e) ? 1.0 : 0.0;
+                __syncwarp();
+                for (int pass = 0; pass < 2; ++pass)
+                    for (int64_t q = 0; q < k && q < Cc; ++q) {
+                        if (q == o) continue;
+                        double sq = 0.0;
+                        for (int64_t c = 0; c < Cc; ++c)
+                            if (rank[c] == q) sq = sig[c];
+                        if (q > o && !(sq > ztol && sq > 0.0)) continue;  // not yet filled
+                        const double* u = Ltall + q * R;
+                        double d = 0.0;
+                        for (int64_t i = lane; i < R; i += 32) d = fma(u[i], col[i], d);
+                        d = warp_sum(d);
+                        for (int64_t i = lane; i < R; i += 32) col[i] -= d * u[i];
+                        __syncwarp();
+                    }
+                double nv = 0.0;
+                for (int64_t i = lane; i < R; i += 32) nv = fma(col[i], col[i], nv);
+                nv = sqrt(warp_sum(nv));
+                if (nv > 0.5) {
+                    for (int64_t i = lane; i < R; i += 32) col[i] /= nv;
+                    __syncwarp();
+                    break;
+                }
+            }
+        }
+    }
+    __syncthreads();
+    // sign rule (matrix_kernels.cpp:16-25): largest |U| entry (first on ties)
+    // of each U column made nonnegative, V flipped with it.
+    for (int64_t o = warp; o < k && o < Cc; o += nw) {
+        const double* u = Uo + o * m;
+        double best = -1.0;
+        int64_t bi = 0;
+        for (int64_t i = lane; i < m; i += 32) {
+            const double a = fabs(u[i]);
+            if (a > best) { best = a; bi = i; }
+        }
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            const double ob = __shfl_xor_sync(0xffffffffu, best, off);
+            const int64_t oi = __shfl_xor_sync(0xffffffffu, bi, off);
+            if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+        }
+        const bool flip = u[bi] < 0.0;
+        __syncwarp();
+        if (flip) {
+            for (int64_t i = lane; i < m; i += 32) Uo[o * m + i] = -Uo[o * m + i];
+            if (Vo)
+                for (int64_t i = lane; i < n; i += 32) Vo[o * n + i] = -Vo[o * n + i];
+        }
+    }
+}
+
+}  // namespace
+
+size_t jacobi_smem_bytes(int64_t m, int64_t n) {
+    const int64_t R = m > n ? m : n, C = m > n ? n : m;
+    return (size_t)(R * C + C * C + C) * sizeof(double) + (size_t)C * sizeof(int) + 16;
+}
+
+void jacobi_svd(const double* A, int64_t m, int64_t n, int64_t strideA, int64_t batch, int64_t k,
+                double* U, double* S, double* V, double* tail2, cudaStream_t s) {
+    if (batch == 0) return;
+    const int64_t R = m > n ? m : n, C = m > n ? n : m;
+    if (k < 1 || k > C) fail(PPC_ARGUMENT, "jacobi_svd: k out of range");
+    const size_t smem = jacobi_smem_bytes(m, n);
+    const int threads = C >= 96 ? 512 : (C >= 32 ? 256 : 128);
+    const bool use_smem = smem <= 200 * 1024;
+    DeviceBuffer ws;
+    if (!use_smem) ws = DeviceBuffer((size_t)batch * (R * C + C * C + 2 * C) * sizeof(double));
+    if (use_smem && smem > 48 * 1024)
+        PPC_CUDA_CHECK(cudaFuncSetAttribute(jacobi_svd_kernel,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (batch > 0x7fffffffLL) fail(PPC_ARGUMENT, "jacobi_svd: batch too large");
+    jacobi_svd_kernel<<<(unsigned)batch, threads, use_smem ? smem : 0, s>>>(
+        A, m, n, strideA, k, U, S, V, ws.d(), use_smem ? 1 : 0, tail2);
+    count_launch();
+    check_launch("jacobi_svd");
+}
+
+}  // namespace ppc
+
+namespace ppc {
+namespace {
+__global__ void sign_rule_kernel(double* X, int64_t rows, int64_t cols, double* Y, int64_t yrows) {
+    const int64_t b = blockIdx.y;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t c = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+    if (c >= cols) return;
+    double* x = X + (b * cols + c) * rows;
+    double best = -1.0;
+    int64_t bi = 0;
+    for (int64_t i = lane; i < rows; i += 32) {
+        const double a = fabs(x[i]);
+        if (a > best) { best = a; bi = i; }
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, off);
+        const int64_t oi = __shfl_xor_sync(0xffffffffu, bi, off);
+        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+    }
+    const bool flip = x[bi] < 0.0;
+    __syncwarp();
+    if (!flip) return;
+    for (int64_t i = lane; i < rows; i += 32) x[i] = -x[i];
+    if (Y) {
+        double* y = Y + (b * cols + c) * yrows;
+        for (int64_t i = lane; i < yrows; i += 32) y[i] = -y[i];
+    }
+}
+}  // namespace
+
+void sign_rule(double* X, int64_t rows, int64_t cols, int64_t batch, double* Y, int64_t yrows,
+               cudaStream_t s) {
+    if (!cols || !batch) return;
+    dim3 grid((unsigned)((cols + 7) / 8), (unsigned)batch);
+    sign_rule_kernel<<<grid, 256, 0, s>>>(X, rows, cols, Y, yrows);
+    count_launch();
+    check_launch("sign_rule");
+}
+}  // namespace ppc

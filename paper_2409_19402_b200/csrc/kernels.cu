@@ -1,0 +1,178 @@
+// Memory-bound helper kernels (see kernels.cuh).
+#include "internal.h"
+#include "kernels.cuh"
+
+namespace ppc {
+
+namespace {
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Fixed-order two-value block reduction (blockDim.x multiple of 32, <= 1024).
+__device__ __forceinline__ void block_sum2(double& a, double& b) {
+    __shared__ double red[2][32];
+    a = warp_sum(a);
+    b = warp_sum(b);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) {
+        red[0][w] = a;
+        red[1][w] = b;
+    }
+    __syncthreads();
+    if (w == 0) {
+        const int nw = blockDim.x >> 5;
+        a = l < nw ? red[0][l] : 0.0;
+        b = l < nw ? red[1][l] : 0.0;
+        a = warp_sum(a);
+        b = warp_sum(b);
+    }
+}
+
+__global__ void __launch_bounds__(kReduceThreads)
+    sumsq_partials_kernel(const double* __restrict__ a, const double* __restrict__ b,
+                          int64_t count, double* __restrict__ partials) {
+    double sd = 0.0, sa = 0.0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b) {
+        for (; i + 3 * stride < count; i += 4 * stride) {
+            double x0 = a[i], x1 = a[i + stride], x2 = a[i + 2 * stride], x3 = a[i + 3 * stride];
+            double d0 = x0 - b[i], d1 = x1 - b[i + stride], d2 = x2 - b[i + 2 * stride],
+                   d3 = x3 - b[i + 3 * stride];
+            sd = fma(d0, d0, sd); sd = fma(d1, d1, sd); sd = fma(d2, d2, sd); sd = fma(d3, d3, sd);
+            sa = fma(x0, x0, sa); sa = fma(x1, x1, sa); sa = fma(x2, x2, sa); sa = fma(x3, x3, sa);
+        }
+        for (; i < count; i += stride) {
+            const double x = a[i], d = x - b[i];
+            sd = fma(d, d, sd);
+            sa = fma(x, x, sa);
+        }
+    } else {
+        for (; i + 3 * stride < count; i += 4 * stride) {
+            double x0 = a[i], x1 = a[i + stride], x2 = a[i + 2 * stride], x3 = a[i + 3 * stride];
+            sa = fma(x0, x0, sa); sa = fma(x1, x1, sa); sa = fma(x2, x2, sa); sa = fma(x3, x3, sa);
+        }
+        for (; i < count; i += stride) sa = fma(a[i], a[i], sa);
+        sd = sa;
+    }
+    block_sum2(sd, sa);
+    if (threadIdx.x == 0) {
+        partials[2 * blockIdx.x] = sd;
+        partials[2 * blockIdx.x + 1] = sa;
+    }
+}
+
+__global__ void __launch_bounds__(1024) reduce_pairs_kernel(const double* __restrict__ p, int64_t n,
+                                                           double* __restrict__ out) {
+    double a = 0.0, b = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        a += p[2 * i];
+        b += p[2 * i + 1];
+    }
+    block_sum2(a, b);
+    if (threadIdx.x == 0) {
+        out[0] = a;
+        out[1] = b;
+    }
+}
+
+__global__ void scale_columns_kernel(const double* __restrict__ U, const double* __restrict__ S,
+                                     double* __restrict__ out, int64_t rows, int64_t k,
+                                     int64_t total) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
+        const int64_t col = i / rows;  // = j + b*k, the index into S (k x batch)
+        out[i] = U[i] * S[col];
+    }
+}
+
+__global__ void transpose_kernel(const double* __restrict__ in, double* __restrict__ out,
+                                 int64_t rows, int64_t cols) {
+    __shared__ double tile[32][33];
+    const int64_t b = blockIdx.z;
+    in += b * rows * cols;
+    out += b * rows * cols;
+    const int64_t r0 = (int64_t)blockIdx.x * 32, c0 = (int64_t)blockIdx.y * 32;
+    for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+        const int64_t r = r0 + threadIdx.x, c = c0 + j;
+        if (r < rows && c < cols) tile[j][threadIdx.x] = in[r + c * rows];
+    }
+    __syncthreads();
+    for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+        const int64_t c = c0 + threadIdx.x, r = r0 + j;
+        if (r < rows && c < cols) out[c + r * cols] = tile[threadIdx.x][j];
+    }
+}
+
+__global__ void scale_kernel(double* x, int64_t n, double alpha) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) x[i] *= alpha;
+}
+
+__global__ void nonfinite_kernel(const double* __restrict__ x, int64_t n, int* flag) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    bool bad = false;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+        bad |= !isfinite(x[i]);
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicExch(flag, 1);
+}
+
+unsigned grid_for(int64_t n, int threads) {
+    int64_t g = (n + threads - 1) / threads;
+    if (g > 148 * 16) g = 148 * 16;
+    if (g < 1) g = 1;
+    return (unsigned)g;
+}
+
+}  // namespace
+
+void launch_sumsq_partials(const double* a, const double* b, int64_t count, double* partials,
+                           cudaStream_t s) {
+    sumsq_partials_kernel<<<kReduceBlocks, kReduceThreads, 0, s>>>(a, b, count, partials);
+    count_launch();
+    check_launch("sumsq_partials");
+}
+
+void launch_reduce_pairs(const double* partials, int64_t n, double* out, cudaStream_t s) {
+    reduce_pairs_kernel<<<1, 1024, 0, s>>>(partials, n, out);
+    count_launch();
+    check_launch("reduce_pairs");
+}
+
+void launch_scale_columns(const double* U, const double* S, double* out, int64_t rows,
+                          int64_t k, int64_t batch, cudaStream_t s) {
+    const int64_t total = rows * k * batch;
+    if (!total) return;
+    scale_columns_kernel<<<grid_for(total, 256), 256, 0, s>>>(U, S, out, rows, k, total);
+    count_launch();
+    check_launch("scale_columns");
+}
+
+void launch_transpose(const double* in, double* out, int64_t rows, int64_t cols, int64_t batch,
+                      cudaStream_t s) {
+    if (!rows || !cols || !batch) return;
+    dim3 grid((unsigned)((rows + 31) / 32), (unsigned)((cols + 31) / 32), (unsigned)batch);
+    transpose_kernel<<<grid, dim3(32, 8), 0, s>>>(in, out, rows, cols);
+    count_launch();
+    check_launch("transpose");
+}
+
+void launch_scale(double* x, int64_t n, double alpha, cudaStream_t s) {
+    if (!n) return;
+    scale_kernel<<<grid_for(n, 256), 256, 0, s>>>(x, n, alpha);
+    count_launch();
+    check_launch("scale");
+}
+
+void launch_nonfinite(const double* x, int64_t n, int* flag, cudaStream_t s) {
+    if (!n) return;
+    nonfinite_kernel<<<grid_for(n, 256), 256, 0, s>>>(x, n, flag);
+    count_launch();
+    check_launch("nonfinite");
+}
+
+}  // namespace ppc

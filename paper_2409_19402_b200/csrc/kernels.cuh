@@ -1,0 +1,32 @@
+// Small memory-bound kernels of the engine (deterministic reductions,
+// per-column scaling, transposes). All reductions use a fixed grid and a
+// fixed summation order, so results are bitwise reproducible run to run and
+// independent of the launching device count (verify.cpp:452-455).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace ppc {
+
+constexpr int kReduceBlocks = 1024;  // fixed: reduction order is part of the result
+constexpr int kReduceThreads = 256;
+
+// partials[2*b] = sum (a-b)^2, partials[2*b+1] = sum a^2 over block b's
+// fixed element subset (b == nullptr: both sums are sum a^2).
+void launch_sumsq_partials(const double* a, const double* b, int64_t count, double* partials,
+                           cudaStream_t s);
+// out[0..1] = fixed-order sums of the pairs in partials[0..2n).
+void launch_reduce_pairs(const double* partials, int64_t n, double* out, cudaStream_t s);
+// out(:, j, b) = U(:, j, b) * S(j, b) for a stack of `batch` rows x k blocks.
+void launch_scale_columns(const double* U, const double* S, double* out, int64_t rows,
+                          int64_t k, int64_t batch, cudaStream_t s);
+// out(j, i, b) = in(i, j, b) for `batch` rows x cols blocks.
+void launch_transpose(const double* in, double* out, int64_t rows, int64_t cols, int64_t batch,
+                      cudaStream_t s);
+// y = alpha * x
+void launch_scale(double* x, int64_t n, double alpha, cudaStream_t s);
+// non-finite detector: *flag = 1 if any entry of x is NaN/Inf.
+void launch_nonfinite(const double* x, int64_t n, int* flag, cudaStream_t s);
+
+}  // namespace ppc

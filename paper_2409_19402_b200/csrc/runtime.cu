@@ -1,0 +1,187 @@
+// Per-thread runtime: device/stream selection, error plumbing, stream-ordered
+// workspace, host<->device staging. Replaces the reference's L2 runtime
+// (parallel.cpp:13-57: slice loops over std::threads) with CUDA grids on one
+// device per host thread.
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+
+#include "internal.h"
+#include "kernels.cuh"
+
+namespace ppc {
+
+namespace {
+thread_local Context t_ctx;
+thread_local std::string t_err;
+std::once_flag g_pool_once[64];
+
+int visible_devices() {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    // PROJPROD_DEVICES caps the count like PROJPROD_THREADS caps workers
+    // (parallel.cpp:13-27): unset/invalid = no cap, < 1 clamps to 1.
+    const char* env = std::getenv("PROJPROD_DEVICES");
+    if (env && *env) {
+        char* end = nullptr;
+        long cap = std::strtol(env, &end, 10);
+        if (end != env) {
+            if (cap < 1) cap = 1;
+            if (cap < n) n = (int)cap;
+        }
+    }
+    return n;
+}
+
+void init_device(int dev) {
+    PPC_CUDA_CHECK(cudaSetDevice(dev));
+    cudaDeviceProp prop;
+    PPC_CUDA_CHECK(cudaGetDeviceProperties(&prop, dev));
+    if (prop.major < 10)
+        fail(PPC_NO_DEVICE, std::string("device ") + prop.name +
+                                " is not sm_100-class; this engine is B200-only");
+    t_ctx.device = dev;
+    t_ctx.sms = prop.multiProcessorCount;
+    if (dev < 64)
+        std::call_once(g_pool_once[dev], [dev] {
+            cudaMemPool_t pool;
+            if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+                uint64_t thr = UINT64_MAX;
+                cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+            }
+        });
+}
+}  // namespace
+
+Context& ctx() {
+    if (t_ctx.device < 0) {
+        if (visible_devices() == 0)
+            fail(PPC_NO_DEVICE, "no CUDA device visible: the ppc engine has no CPU path");
+        init_device(0);
+    } else {
+        PPC_CUDA_CHECK(cudaSetDevice(t_ctx.device));
+    }
+    return t_ctx;
+}
+
+cudaStream_t stream() {
+    Context& c = ctx();
+    if (c.stream) return c.stream;
+    if (!c.own_stream) PPC_CUDA_CHECK(cudaStreamCreateWithFlags(&c.own_stream, cudaStreamNonBlocking));
+    return c.own_stream;
+}
+
+void check_launch(const char* name) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) fail(PPC_CUDA, std::string(name) + " launch: " + cudaGetErrorString(e));
+}
+
+DeviceBuffer::DeviceBuffer(size_t bytes) : n_(bytes) {
+    if (bytes) PPC_CUDA_CHECK(cudaMallocAsync(&p_, bytes, stream()));
+}
+DeviceBuffer::~DeviceBuffer() { release(); }
+void DeviceBuffer::release() {
+    if (p_) cudaFreeAsync(p_, stream());
+    p_ = nullptr;
+    n_ = 0;
+}
+
+void validate_loc(int loc) {
+    if (loc != PPC_HOST && loc != PPC_DEVICE) fail(PPC_ARGUMENT, "loc must be PPC_HOST or PPC_DEVICE");
+}
+
+void require_positive(int64_t v, const char* what) {
+    if (v < 1) fail(PPC_SHAPE, std::string(what) + " must be positive");
+}
+
+In::In(const double* p, size_t count, int loc) {
+    if (loc == PPC_DEVICE || count == 0) {
+        d = p;
+        return;
+    }
+    if (!p) fail(PPC_ARGUMENT, "null input pointer");
+    buf = DeviceBuffer(count * sizeof(double));
+    PPC_CUDA_CHECK(cudaMemcpyAsync(buf.d(), p, count * sizeof(double), cudaMemcpyHostToDevice, stream()));
+    d = buf.d();
+}
+
+Out::Out(double* p, size_t n, int loc) : count(n) {
+    if (loc == PPC_DEVICE || n == 0) {
+        d = p;
+        return;
+    }
+    if (!p) fail(PPC_ARGUMENT, "null output pointer");
+    host = p;
+    buf = DeviceBuffer(n * sizeof(double));
+    d = buf.d();
+}
+
+void Out::finish() {
+    if (host)
+        PPC_CUDA_CHECK(cudaMemcpyAsync(host, d, count * sizeof(double), cudaMemcpyDeviceToHost, stream()));
+}
+
+void set_error(const std::string& m) { t_err = m; }
+const char* last_error() { return t_err.c_str(); }
+
+}  // namespace ppc
+
+extern "C" {
+
+const char* ppc_last_error(void) { return ppc::last_error(); }
+int ppc_version(void) { return PPC_VERSION; }
+
+int ppc_device_count(void) { return ppc::visible_devices(); }
+
+int ppc_set_device(int device) {
+    try {
+        int n = ppc::visible_devices();
+        if (device < 0 || device >= n) ppc::fail(PPC_ARGUMENT, "ppc_set_device: no such device");
+        ppc::t_ctx.stream = nullptr;
+        ppc::t_ctx.own_stream = nullptr;
+        ppc::init_device(device);
+        return 0;
+    } catch (const ppc::Error& e) {
+        ppc::set_error(e.what());
+        return e.code;
+    }
+}
+
+int ppc_set_stream(void* s) {
+    try {
+        ppc::ctx().stream = static_cast<cudaStream_t>(s);
+        return 0;
+    } catch (const ppc::Error& e) {
+        ppc::set_error(e.what());
+        return e.code;
+    }
+}
+
+void* ppc_get_stream(void) {
+    try {
+        return ppc::stream();
+    } catch (...) {
+        return nullptr;
+    }
+}
+
+int ppc_synchronize(void) {
+    try {
+        PPC_CUDA_CHECK(cudaStreamSynchronize(ppc::stream()));
+        return 0;
+    } catch (const ppc::Error& e) {
+        ppc::set_error(e.what());
+        return e.code;
+    }
+}
+
+int64_t ppc_launch_count(int reset) {
+    int64_t n = ppc::t_ctx.launches;
+    if (reset) ppc::t_ctx.launches = 0;
+    return n;
+}
+
+}  // extern "C"

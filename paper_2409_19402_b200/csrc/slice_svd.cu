@@ -1,0 +1,130 @@
+// Facewise SVD, Gram SYRK and the data-driven basis Q.
+//
+//   slice_svd  — matrix_kernels.cpp:29-37 per transform-domain slice
+//                (decompositions.cpp:75-81). Small slices: one-CTA Jacobi (K6).
+//   gram       — G = T^T T with deterministic split-K over pixel chunks and a
+//                fixed pairwise tree over chunks (K4).
+//   data_q     — transforms.cpp:97-115 via Gram + symmetric eigensolve (K5).
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "dmma_gemm.cuh"
+#include "engine.h"
+#include "internal.h"
+#include "jacobi.cuh"
+#include "kernels.cuh"
+#include "slice_svd.cuh"
+
+namespace ppc {
+
+namespace {
+
+__global__ void tree_add_kernel(double* parts, int64_t nparts, int64_t elems, int64_t width) {
+    // parts[s] += parts[s + width] for s multiple of 2*width
+    const int64_t total = ((nparts + 2 * width - 1) / (2 * width)) * elems;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
+        const int64_t grp = i / elems, e = i % elems;
+        const int64_t a = grp * 2 * width, b = a + width;
+        if (b < nparts) parts[a * elems + e] += parts[b * elems + e];
+    }
+}
+
+__global__ void sqrt_clamp_kernel(const double* lam, double* sig, int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) sig[i] = sqrt(fmax(lam[i], 0.0));
+}
+
+}  // namespace
+
+GramPlan gram_plan(int64_t N, int64_t n3) {
+    // Chunk count depends on (N, n3) only — never on the device count — so
+    // the reduction tree (and hence Q) is bitwise identical on 1..8 GPUs.
+    GramPlan g;
+    const int64_t bt = n3 <= 32 ? 1 : (n3 + 127) / 128;
+    const int64_t tiles = std::max<int64_t>(1, bt * (bt + 1) / 2);
+    int64_t want = std::max<int64_t>(1, (4 * 148) / tiles);
+    int64_t maxc = std::max<int64_t>(1, N / 512);
+    int64_t c = 1;
+    while (c * 2 <= want && c * 2 <= maxc) c *= 2;
+    g.chunks = c;
+    g.chunk = ((N + c - 1) / c + 15) / 16 * 16;
+    return g;
+}
+
+void gram_partials(const double* T, int64_t ldT, int64_t rows, int64_t n3, int64_t chunk,
+                   int64_t chunks, double* parts, cudaStream_t s) {
+    GemmDesc d;
+    d.M = n3; d.N = n3; d.K = rows;
+    d.A = T; d.lda = ldT; d.a_kmajor = true;   // A(m,k) = T[k + m*ldT]
+    d.B = T; d.ldb = ldT; d.b_nmajor = false;  // B(k,n) = T[k + n*ldT]
+    d.C = parts; d.ldc = n3;
+    d.symmetric = true;
+    d.splits = chunks;
+    d.kchunk = chunk;
+    d.strideCsplit = n3 * n3;
+    gemm(d, s);
+}
+
+void tree_reduce(double* parts, int64_t nparts, int64_t elems, cudaStream_t s) {
+    for (int64_t w = 1; w < nparts; w *= 2) {
+        const int64_t total = ((nparts + 2 * w - 1) / (2 * w)) * elems;
+        const unsigned grid = (unsigned)std::min<int64_t>((total + 255) / 256, 148 * 16);
+        tree_add_kernel<<<grid, 256, 0, s>>>(parts, nparts, elems, w);
+        count_launch();
+        check_launch("tree_add");
+    }
+}
+
+void gram(const double* T, int64_t N, int64_t n3, double* G, cudaStream_t s) {
+    const GramPlan g = gram_plan(N, n3);
+    if (g.chunks == 1) {
+        gram_partials(T, N, N, n3, g.chunk, 1, G, s);
+        return;
+    }
+    DeviceBuffer parts(sizeof(double) * g.chunks * n3 * n3);
+    gram_partials(T, N, N, n3, g.chunk, g.chunks, parts.d(), s);
+    tree_reduce(parts.d(), g.chunks, n3 * n3, s);
+    PPC_CUDA_CHECK(cudaMemcpyAsync(G, parts.d(), sizeof(double) * n3 * n3, cudaMemcpyDeviceToDevice, s));
+}
+
+void sym_eig_top(const double* G, int64_t n, int64_t p, double* Q, double* lambda, cudaStream_t s) {
+    // One-sided Jacobi on the PSD G: V = eigenvectors, column norms of G V =
+    // eigenvalues, descending (stable order on ties).
+    if (n <= kSubspaceMinN) {
+        jacobi_svd(G, n, n, n * n, 1, p, nullptr, lambda, Q, nullptr, s);
+        return;
+    }
+    subspace_eig_top(G, n, 1, p, Q, lambda, s);
+}
+
+bool data_q(const double* T, int64_t N, int64_t n3, int64_t p, double* Q, double* sigma,
+            cudaStream_t s) {
+    DeviceBuffer G(sizeof(double) * n3 * n3), lam(sizeof(double) * n3);
+    gram(T, N, n3, G.d(), s);
+    const int64_t avail = std::min(n3, N);
+    // When p > min(n3, N) the unfolding has only `avail` singular vectors;
+    // the eigenvectors of G for its zero eigenvalues complete the basis
+    // (transforms.cpp:104-111 pads with an orthonormal completion).
+    sym_eig_top(G.d(), n3, p, Q, lam.d(), s);
+    sign_rule(Q, n3, p, 1, nullptr, 0, s);  // fix_svd_signs on U3 (matrix_kernels.cpp:35)
+    if (sigma) {
+        sqrt_clamp_kernel<<<(unsigned)((p + 255) / 256), 256, 0, s>>>(lam.d(), sigma, p);
+        count_launch();
+        check_launch("sqrt_clamp");
+    }
+    return p > avail;
+}
+
+void slice_svd(const double* A, int64_t m, int64_t n, int64_t stride, int64_t batch, int64_t k,
+               double* U, double* S, double* V, double* tail2, cudaStream_t s) {
+    const int64_t r = std::min(m, n);
+    if (r <= kSubspaceMinN || jacobi_smem_bytes(m, n) <= 200 * 1024 || k > r / 2) {
+        jacobi_svd(A, m, n, stride, batch, k, U, S, V, tail2, s);
+        return;
+    }
+    subspace_svd(A, m, n, stride, batch, k, U, S, V, tail2, s);
+}
+
+}  // namespace ppc

@@ -1,0 +1,29 @@
+// Facewise SVD / Gram / eigensolver internals (see slice_svd.cu, subspace.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace ppc {
+
+// Problems with min dimension <= this go to the one-CTA Jacobi kernel; larger
+// ones to the Gram + Chebyshev-filtered subspace iteration + Rayleigh-Ritz
+// polish path (subspace.cu).
+constexpr int64_t kSubspaceMinN = 1LL << 40;  // TODO(r1): lower once subspace path lands
+
+struct GramPlan {
+    int64_t chunks = 1;  // power of two
+    int64_t chunk = 0;   // rows per chunk (multiple of 16)
+};
+GramPlan gram_plan(int64_t N, int64_t n3);
+// Per-chunk partial Grams of the rows of T (ldT >= rows): parts[c] (n3 x n3).
+void gram_partials(const double* T, int64_t ldT, int64_t rows, int64_t n3, int64_t chunk,
+                   int64_t chunks, double* parts, cudaStream_t s);
+// Fixed pairwise tree over nparts arrays of `elems` doubles; result in parts[0].
+void tree_reduce(double* parts, int64_t nparts, int64_t elems, cudaStream_t s);
+
+void subspace_eig_top(const double* G, int64_t n, int64_t batch, int64_t p, double* Q,
+                      double* lambda, cudaStream_t s);
+void subspace_svd(const double* A, int64_t m, int64_t n, int64_t stride, int64_t batch, int64_t k,
+                  double* U, double* S, double* V, double* tail2, cudaStream_t s);
+
+}  // namespace ppc

@@ -1,0 +1,433 @@
+"""Python mirror of the reference's `projprod` module (proj/python/bindings.cpp)
+on top of the B200 engine's C-ABI (include/ppc.h).
+
+Same names, argument meanings, array layouts and error behaviour as the
+reference bindings:
+  * tensors are (n1, n2, n3) float64 arrays in the native mode-1-fastest
+    layout (bindings.cpp:22-46); factor stacks are (n, k, p) and s is (k, p)
+    (bindings.cpp:117-127);
+  * shape / bounds / argument / degenerate errors raise ValueError subclasses,
+    numeric errors RuntimeError (README.md:135-136, test_smoke.py:99-106).
+
+Arrays may be numpy (host; the engine stages them through HBM) or CUDA torch
+tensors laid out Fortran-contiguous (device; zero-copy, stream-ordered). Use
+`to_device` / `empty_device` to make such tensors.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+
+__all__ = [
+    "ShapeError", "BoundsError", "ArgumentError", "DegenerateInputError", "NumericError",
+    "FormatError", "EngineError", "Transform", "TsvdqFactors", "mode3_product",
+    "facewise_product", "frobenius_norm", "svd", "truncated_svd", "data_dependent_transform",
+    "projection_error", "star_q", "star_q_product", "tsvdq", "tsvdq_reconstruct", "tsvdq_error",
+    "relative_error", "tsvdq_relative_error", "to_device", "empty_device", "to_host",
+    "launch_count",
+]
+
+
+class ShapeError(ValueError):
+    pass
+
+
+class BoundsError(IndexError, ValueError):
+    pass
+
+
+class ArgumentError(ValueError):
+    pass
+
+
+class DegenerateInputError(ValueError):
+    pass
+
+
+class NumericError(RuntimeError):
+    pass
+
+
+class FormatError(RuntimeError):
+    pass
+
+
+class EngineError(RuntimeError):
+    """CUDA runtime failure or no usable B200 (the engine has no CPU path)."""
+
+
+_ERR = {1: ShapeError, 2: BoundsError, 3: ArgumentError, 4: DegenerateInputError,
+        5: NumericError, 6: FormatError, 7: EngineError, 8: EngineError}
+
+
+def _check(rc: int):
+    if rc:
+        msg = _lib.lib().ppc_last_error().decode(errors="replace")
+        raise _ERR.get(rc, EngineError)(msg)
+
+
+# ------------------------------------------------------------------ arrays
+def _torch():
+    import torch
+    return torch
+
+
+def _is_dev(x) -> bool:
+    try:
+        import torch
+    except ImportError:  # pragma: no cover
+        return False
+    return isinstance(x, torch.Tensor) and x.is_cuda
+
+
+def _fortran_ok(t) -> bool:
+    exp, acc = [], 1
+    for s in t.shape:
+        exp.append(acc)
+        acc *= s
+    return all(st == e or sz == 1 for st, e, sz in zip(t.stride(), exp, t.shape))
+
+
+def empty_device(shape, device="cuda"):
+    """Fortran-contiguous float64 CUDA tensor of the given shape."""
+    torch = _torch()
+    rev = tuple(reversed(tuple(shape)))
+    return torch.empty(rev, dtype=torch.float64, device=device).permute(*reversed(range(len(shape))))
+
+
+def to_device(a, device="cuda"):
+    torch = _torch()
+    a = np.asfortranarray(np.asarray(a, dtype=np.float64))
+    t = empty_device(a.shape, device)
+    t.copy_(torch.from_numpy(a))
+    return t
+
+
+def to_host(x) -> np.ndarray:
+    if _is_dev(x):
+        return np.asfortranarray(x.cpu().numpy())
+    return np.asarray(x)
+
+
+class _Args:
+    """Collects array arguments of one call; all host or all device."""
+
+    def __init__(self, *arrays):
+        devs = [_is_dev(a) for a in arrays if a is not None]
+        if any(devs) and not all(devs):
+            raise ArgumentError("mix of host and device arrays in one call")
+        self.device = bool(devs) and all(devs)
+        self.loc = _lib.PPC_DEVICE if self.device else _lib.PPC_HOST
+        self.keep = []
+
+    def inp(self, a, ndim=None):
+        if self.device:
+            if a.dtype != _torch().float64:
+                raise ArgumentError("device arrays must be float64")
+            if not _fortran_ok(a):
+                a = a.permute(*reversed(range(a.dim()))).contiguous().permute(*reversed(range(a.dim())))
+            self.keep.append(a)
+            return a, C.c_void_p(a.data_ptr())
+        arr = np.asfortranarray(np.asarray(a, dtype=np.float64))
+        if ndim is not None and arr.ndim != ndim:
+            raise ShapeError(f"expected a {ndim}-d array, got ndim={arr.ndim}")
+        self.keep.append(arr)
+        return arr, C.c_void_p(arr.ctypes.data)
+
+    def out(self, shape):
+        if self.device:
+            t = empty_device(shape)
+            self.keep.append(t)
+            return t, C.c_void_p(t.data_ptr())
+        arr = np.empty(shape, order="F")
+        return arr, C.c_void_p(arr.ctypes.data)
+
+
+def _sync_stream_from_torch():
+    """Run the engine on torch's current stream so device arrays are ordered."""
+    torch = _torch()
+    _check(_lib.lib().ppc_set_stream(C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+
+
+def _call(args: _Args, fn, *cargs):
+    if args.device:
+        _sync_stream_from_torch()
+    _check(fn(*cargs))
+
+
+def launch_count(reset: bool = False) -> int:
+    return int(_lib.lib().ppc_launch_count(1 if reset else 0))
+
+
+# --------------------------------------------------------------- transforms
+_KINDS = ("identity", "random", "dct", "haar", "data", "custom")
+
+
+@dataclass
+class Transform:
+    """transforms.hpp:23-34: Q (n3 x p, orthonormal columns) + kind/seed/scale."""
+
+    q: np.ndarray
+    kind: str = "custom"
+    seed: int | None = None
+    scale: float = 1.0
+    completed_basis: bool = False
+
+    def __init__(self, kind: str, n3: int, p: int, seed: int = 0, data=None):
+        # bindings.cpp:73-86 build_transform
+        L = _lib.lib()
+        if kind not in _KINDS or kind == "custom":
+            raise ArgumentError(f"unknown transform '{kind}' (identity|random|dct|haar|data)")
+        self.kind, self.scale, self.seed, self.completed_basis = kind, 1.0, None, False
+        if kind == "data":
+            if data is None:
+                raise ArgumentError("transform 'data' needs the data= tensor")
+            t = data_dependent_transform(data, p)
+            self.q, self.completed_basis = t.q, t.completed_basis
+            return
+        q = np.empty((int(n3), int(p)), order="F")
+        ptr = C.c_void_p(q.ctypes.data)
+        if kind == "identity":
+            _check(L.ppc_identity_q(n3, p, ptr))
+        elif kind == "dct":
+            _check(L.ppc_dct_q(n3, p, ptr))
+        elif kind == "haar":
+            _check(L.ppc_haar_q(n3, p, ptr))
+        else:
+            _check(L.ppc_random_orthogonal_q(n3, p, C.c_uint64(int(seed)), ptr))
+            self.seed = int(seed)
+        self.q = q
+
+    @classmethod
+    def custom(cls, q, scale: float = 1.0) -> "Transform":
+        """transforms.cpp:100-111 custom_transform: Stiefel check, scale != 0."""
+        q = np.asfortranarray(np.asarray(q, dtype=np.float64))
+        if q.ndim != 2:
+            raise ShapeError(f"expected a 2-d array, got ndim={q.ndim}")
+        _check(_lib.lib().ppc_check_stiefel(C.c_void_p(q.ctypes.data), q.shape[0], q.shape[1]))
+        if scale == 0.0:
+            raise ArgumentError("custom_transform: scale must be nonzero")
+        t = cls.__new__(cls)
+        t.q, t.kind, t.seed, t.scale, t.completed_basis = q, "custom", None, float(scale), False
+        return t
+
+    @classmethod
+    def _from_q(cls, q, kind="data", completed=False) -> "Transform":
+        t = cls.__new__(cls)
+        t.q, t.kind, t.seed, t.scale, t.completed_basis = q, kind, None, 1.0, completed
+        return t
+
+    @property
+    def n3(self) -> int:
+        return int(self.q.shape[0])
+
+    @property
+    def p(self) -> int:
+        return int(self.q.shape[1])
+
+
+@dataclass
+class TsvdqFactors:
+    """decompositions.hpp:24-31, exported as bindings.cpp:117-130."""
+
+    u: object   # (n1, k, p)
+    s: object   # (k, p)
+    v: object   # (n2, k, p)
+    transform: Transform
+    k: int
+    n1: int = field(default=0)
+    n2: int = field(default=0)
+
+
+def _q_of(t, args: _Args):
+    q = t.q if isinstance(t, Transform) else t
+    if args.device and not _is_dev(q):
+        q = to_device(q)
+    return args.inp(q, 2)
+
+
+# ----------------------------------------------------------------- kernels
+def mode3_product(a, m):
+    """tensor.cpp:139-147: A x_3 M, M is q x n3."""
+    args = _Args(a, m if _is_dev(m) else None)
+    a_, pa = args.inp(a, 3)
+    if args.device and not _is_dev(m):
+        m = to_device(m)
+    m_, pm = args.inp(m, 2)
+    n1, n2, n3 = a_.shape
+    if m_.shape[1] != n3:
+        raise ShapeError(f"mode3_product: M has {m_.shape[1]} cols, tensor n3={n3}")
+    out, po = args.out((n1, n2, m_.shape[0]))
+    _call(args, _lib.lib().ppc_mode3_product, pa, n1, n2, n3, pm, m_.shape[0], 0, po, args.loc)
+    return out
+
+
+def facewise_product(a, b):
+    """tensor.cpp:149-156."""
+    args = _Args(a, b)
+    a_, pa = args.inp(a, 3)
+    b_, pb = args.inp(b, 3)
+    n1, m, n3 = a_.shape
+    if b_.shape[0] != m or b_.shape[2] != n3:
+        raise ShapeError(f"facewise_product: {tuple(a_.shape)} vs {tuple(b_.shape)}")
+    out, po = args.out((n1, b_.shape[1], n3))
+    _call(args, _lib.lib().ppc_facewise_product, pa, n1, m, n3, pb, b_.shape[1], po, args.loc)
+    return out
+
+
+def frobenius_norm(a) -> float:
+    args = _Args(a)
+    a_, pa = args.inp(a)
+    out = C.c_double()
+    _call(args, _lib.lib().ppc_frobenius_norm, pa, int(np.prod(a_.shape)), C.byref(out), args.loc)
+    return out.value
+
+
+def truncated_svd(a, k: int):
+    """matrix_kernels.cpp:39-46 (batched over a leading stack if a is 3-d:
+    a (m, n, batch) -> U (m,k,batch), s (k,batch), V (n,k,batch))."""
+    args = _Args(a)
+    a_, pa = args.inp(a)
+    squeeze = len(a_.shape) == 2
+    m, n = a_.shape[0], a_.shape[1]
+    batch = 1 if squeeze else a_.shape[2]
+    U, pu = args.out((m, k, batch))
+    s, ps = args.out((k, batch))
+    V, pv = args.out((n, k, batch))
+    _call(args, _lib.lib().ppc_svd_batched, pa, m, n, batch, k, pu, ps, pv, args.loc)
+    if squeeze:
+        return U[:, :, 0], s[:, 0], V[:, :, 0]
+    return U, s, V
+
+
+def svd(a):
+    """matrix_kernels.cpp:29-37: thin SVD, descending s, sign rule."""
+    shp = a.shape
+    return truncated_svd(a, min(shp[0], shp[1]))
+
+
+def data_dependent_transform(a, p: int) -> Transform:
+    """transforms.cpp:97-115 (Gram SYRK + top-p eigensolve on the device)."""
+    args = _Args(a)
+    a_, pa = args.inp(a, 3)
+    n1, n2, n3 = a_.shape
+    q, pq = args.out((n3, p))
+    comp = C.c_int(0)
+    _call(args, _lib.lib().ppc_data_dependent_q, pa, n1, n2, n3, p, pq, None, C.byref(comp), args.loc)
+    return Transform._from_q(to_host(q) if args.device else q, "data", bool(comp.value))
+
+
+def projection_error(a, t) -> float:
+    args = _Args(a)
+    a_, pa = args.inp(a, 3)
+    q_, pq = _q_of(t, args)
+    n1, n2, n3 = a_.shape
+    if q_.shape[0] != n3:
+        raise ShapeError(f"projection_error: transform rows {q_.shape[0]} != tensor n3 {n3}")
+    out = C.c_double()
+    _call(args, _lib.lib().ppc_projection_error, pa, n1, n2, n3, pq, q_.shape[1], C.byref(out), args.loc)
+    return out.value
+
+
+def star_q_product(a, b, t):
+    """star_products.cpp:51-59."""
+    args = _Args(a, b)
+    a_, pa = args.inp(a, 3)
+    b_, pb = args.inp(b, 3)
+    q_, pq = _q_of(t, args)
+    n1, m, n3 = a_.shape
+    if b_.shape[0] != m:
+        raise ShapeError(f"star product: inner extents differ ({m} vs {b_.shape[0]})")
+    if n3 != q_.shape[0] or b_.shape[2] != q_.shape[0]:
+        raise ShapeError("star product: mode-3 extents must match the transform")
+    scale = t.scale if isinstance(t, Transform) else 1.0
+    out, po = args.out((n1, b_.shape[1], n3))
+    _call(args, _lib.lib().ppc_star_q_product, pa, n1, m, n3, pb, b_.shape[1], pq, q_.shape[1],
+          C.c_double(scale), po, args.loc)
+    return out
+
+
+star_q = star_q_product
+
+
+def tsvdq(a, t: Transform, k: int) -> TsvdqFactors:
+    """decompositions.cpp:62-83."""
+    args = _Args(a)
+    a_, pa = args.inp(a, 3)
+    q_, pq = _q_of(t, args)
+    n1, n2, n3 = a_.shape
+    if q_.shape[0] != n3:
+        raise ShapeError(f"tsvdq: transform length {q_.shape[0]} != tensor n3 {n3}")
+    p = q_.shape[1]
+    cap = min(n1, n2)
+    if k < 1 or k > cap:
+        raise ArgumentError(f"tsvdq: k={k} outside [1,{cap}]")
+    U, pu = args.out((n1, k, p))
+    S, ps = args.out((k, p))
+    V, pv = args.out((n2, k, p))
+    _call(args, _lib.lib().ppc_tsvdq, pa, n1, n2, n3, pq, p, k, pu, ps, pv, args.loc)
+    return TsvdqFactors(U, S, V, t, k, n1, n2)
+
+
+def _factor_args(f: TsvdqFactors, args: _Args):
+    u_, pu = args.inp(f.u, 3)
+    s_, ps = args.inp(f.s, 2)
+    v_, pv = args.inp(f.v, 3)
+    q_, pq = _q_of(f.transform, args)
+    return u_, s_, v_, q_, pu, ps, pv, pq
+
+
+def tsvdq_reconstruct(f: TsvdqFactors):
+    """decompositions.cpp:85-94."""
+    args = _Args(f.u, f.s, f.v)
+    u_, s_, v_, q_, pu, ps, pv, pq = _factor_args(f, args)
+    n1, k, p = u_.shape
+    n2 = v_.shape[0]
+    n3 = q_.shape[0]
+    out, po = args.out((n1, n2, n3))
+    _call(args, _lib.lib().ppc_tsvdq_reconstruct, pu, ps, pv, pq, n1, n2, n3, p, k, po, args.loc)
+    return out
+
+
+def tsvdq_error(a, f: TsvdqFactors):
+    """decompositions.cpp:96-103 -> (total, eckart_young, projection)."""
+    args = _Args(a, f.u, f.s, f.v)
+    a_, pa = args.inp(a, 3)
+    u_, s_, v_, q_, pu, ps, pv, pq = _factor_args(f, args)
+    n1, n2, n3 = a_.shape
+    if q_.shape[0] != n3:
+        raise ShapeError(f"tsvdq_error: transform length {q_.shape[0]} != tensor n3 {n3}")
+    k, p = s_.shape
+    t, e, pr = C.c_double(), C.c_double(), C.c_double()
+    _call(args, _lib.lib().ppc_tsvdq_error, pa, n1, n2, n3, pu, ps, pv, pq, p, k, C.byref(t),
+          C.byref(e), C.byref(pr), args.loc)
+    return t.value, e.value, pr.value
+
+
+def relative_error(ref, approx) -> float:
+    """metrics.cpp:21-28."""
+    args = _Args(ref, approx)
+    a_, pa = args.inp(ref)
+    b_, pb = args.inp(approx)
+    if tuple(a_.shape) != tuple(b_.shape):
+        raise ShapeError("relative_error: shapes differ")
+    out = C.c_double()
+    _call(args, _lib.lib().ppc_relative_error, pa, pb, int(np.prod(a_.shape)), C.byref(out), args.loc)
+    return out.value
+
+
+def tsvdq_relative_error(a, f: TsvdqFactors) -> float:
+    """relative_error(A, tsvdq_reconstruct(F)) fused (no reconstruction in HBM)."""
+    args = _Args(a, f.u, f.s, f.v)
+    a_, pa = args.inp(a, 3)
+    u_, s_, v_, q_, pu, ps, pv, pq = _factor_args(f, args)
+    n1, n2, n3 = a_.shape
+    k, p = s_.shape
+    out = C.c_double()
+    _call(args, _lib.lib().ppc_tsvdq_relative_error, pa, n1, n2, n3, pu, ps, pv, pq, p, k,
+          C.byref(out), args.loc)
+    return out.value

@@ -1,0 +1,345 @@
+"""Parity of the CUDA engine (through its C-ABI, via the Python mirror) with
+the CPU oracle on the same seeded inputs, plus the reference's known-answer
+tests. FP64 tolerances follow BASELINE.json north_star (1e-10 relative on
+singular values, reconstructions and relative error) and the reference's own
+test tolerances where tighter (1e-12 / 1e-13 for products)."""
+import math
+
+import numpy as np
+import pytest
+
+from paper_2409_19402_b200 import synth
+
+pytestmark = pytest.mark.gpu
+SQ2 = math.sqrt(2.0)
+
+
+def tube(v):
+    return np.asarray(v, dtype=float).reshape(1, 1, -1)
+
+
+def counterexample():
+    a = np.zeros((2, 2, 2))
+    a[:, :, 0] = np.eye(2)
+    a[:, :, 1] = np.diag([1.0, -1.0])
+    return a
+
+
+def rel(a, b):
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / (nb if nb else 1.0)
+
+
+# ------------------------------------------------------------- L3 kernels
+@pytest.mark.parametrize("shape,q", [((3, 4, 5), 6), ((64, 48, 32), 8), ((37, 29, 61), 13),
+                                     ((128, 96, 200), 20), ((256, 128, 256), 64),
+                                     ((100, 70, 33), 130), ((16, 8, 7), 1)])
+def test_mode3_product_vs_oracle(engine, oracle, shape, q):
+    a = oracle.random_tensor(*shape, 13)
+    m = oracle.random_matrix(q, shape[2], 14)
+    got = engine.mode3_product(a, m)
+    want = oracle.mode3_product(a, m)
+    assert rel(got, want) <= 1e-13
+
+
+@pytest.mark.parametrize("n1,m,n2,p", [(1, 1, 1, 3), (5, 7, 3, 4), (64, 48, 64, 8),
+                                       (130, 70, 90, 5), (256, 128, 256, 3)])
+def test_facewise_vs_oracle(engine, oracle, n1, m, n2, p):
+    a = oracle.random_tensor(n1, m, p, 3)
+    b = oracle.random_tensor(m, n2, p, 4)
+    assert rel(engine.facewise_product(a, b), oracle.facewise_product(a, b)) <= 1e-13
+
+
+def test_facewise_tube_kat(engine):
+    ab = engine.facewise_product(tube([1, 2, 3]), tube([4, 5, -6])).ravel()
+    assert list(ab) == [4.0, 10.0, -18.0]
+
+
+def test_frobenius_and_relative_error(engine, oracle):
+    a = oracle.random_tensor(31, 17, 9, 61)
+    assert engine.frobenius_norm(a) == pytest.approx(np.linalg.norm(a), rel=1e-14)
+    assert engine.frobenius_norm(counterexample()) == pytest.approx(2.0, rel=1e-15)
+    assert engine.frobenius_norm(tube([2, 4, 6, 8])) == pytest.approx(math.sqrt(120.0), rel=1e-15)
+    assert engine.relative_error(a, a) == 0.0
+    assert engine.relative_error(a, np.zeros_like(a)) == 1.0
+    with pytest.raises(engine.DegenerateInputError):
+        engine.relative_error(np.zeros_like(a), a)
+    with pytest.raises(engine.ShapeError):
+        engine.relative_error(a, a[:, :, :3])
+
+
+# ----------------------------------------------------------- star products
+def test_star_q_worked_tube(engine):
+    a, b = tube([2, 4, 6, 8]), tube([1, -1, 1, 0])
+    t = engine.Transform("haar", 4, 2)
+    np.testing.assert_allclose(engine.star_q(a, b, t).ravel(), [3, 3, 3, 0], atol=1e-12)
+    h4 = engine.Transform("haar", 4, 4).q
+    perp = engine.Transform.custom(h4[:, 2:])
+    np.testing.assert_allclose(engine.star_q(a, b, perp).ravel(), [-1, 1, 0, 8], atol=1e-12)
+
+
+def test_star_q_scale_law(engine):
+    rng = np.random.default_rng(8)
+    a, b = rng.standard_normal((2, 2, 4)), rng.standard_normal((2, 3, 4))
+    unit = engine.Transform("dct", 4, 2)
+    base = engine.star_q(a, b, unit)
+    for c in (-2.0, 0.5, 3.0):
+        got = engine.star_q(a, b, engine.Transform.custom(unit.q, c))
+        assert np.linalg.norm(got - c * base) <= 1e-12 * abs(c) * np.linalg.norm(base)
+
+
+def test_star_q_cfg1_vs_oracle(engine, oracle):
+    # BASELINE configs[0]: A 64x48x32 N(0,1) seed 0 (xoshiro, buffer order),
+    # Q = random orthogonal (32, 8), A *Q' A^T with A^T the slicewise transpose.
+    a = oracle.random_tensor(64, 48, 32, 0)
+    at = np.asfortranarray(a.transpose(1, 0, 2))
+    q = oracle.random_orthogonal_q(32, 8, 1)
+    tq = engine.Transform("random", 32, 8, seed=1)
+    assert np.abs(tq.q - q).max() <= 1e-13
+    got = engine.star_q(a, at, tq)
+    want = oracle.star_q_product(a, at, q)
+    assert rel(got, want) <= 1e-12
+
+
+@pytest.mark.parametrize("n1,m,n2,n3,p", [(128, 64, 96, 64, 16), (96, 80, 112, 40, 40),
+                                          (33, 17, 21, 11, 5)])
+def test_star_q_vs_oracle(engine, oracle, n1, m, n2, n3, p):
+    a = oracle.random_tensor(n1, m, n3, 1)
+    b = oracle.random_tensor(m, n2, n3, 2)
+    q = oracle.dct_q(n3, p)
+    got = engine.star_q(a, b, engine.Transform("dct", n3, p))
+    assert rel(got, oracle.star_q_product(a, b, q)) <= 1e-12
+
+
+def test_star_q_shape_errors(engine):
+    t = engine.Transform("dct", 4, 2)
+    with pytest.raises(engine.ShapeError):
+        engine.star_q(np.ones((2, 3, 4)), np.ones((2, 3, 4)), t)
+    with pytest.raises(engine.ShapeError):
+        engine.star_q(np.ones((2, 3, 5)), np.ones((3, 3, 5)), t)
+
+
+# --------------------------------------------------------------- SVD / tSVDQ
+def test_svd_contract(engine, oracle):
+    a = oracle.random_matrix(7, 5, 21)
+    U, s, V = engine.svd(a)
+    assert np.all(np.diff(s) <= 0) and s[-1] >= 0
+    assert np.linalg.norm(U.T @ U - np.eye(5)) <= 5e-10
+    assert np.linalg.norm(V.T @ V - np.eye(5)) <= 5e-10
+    assert np.linalg.norm(a - U @ np.diag(s) @ V.T) <= 1e-10 * np.linalg.norm(a)
+    Uo, so, Vo = oracle.svd(a)
+    np.testing.assert_allclose(s, so, rtol=1e-12)
+    np.testing.assert_allclose(U, Uo, atol=1e-10)  # sign rule makes factors comparable
+    np.testing.assert_allclose(V, Vo, atol=1e-10)
+    _, s, _ = engine.svd(np.array([[SQ2, 0.0], [0.0, 0.0]]))
+    assert s[0] == pytest.approx(SQ2, rel=1e-14) and abs(s[1]) <= 1e-14
+    aw = oracle.random_matrix(5, 9, 22)  # wide
+    U, s, V = engine.svd(aw)
+    assert np.linalg.norm(aw - U @ np.diag(s) @ V.T) <= 1e-10 * np.linalg.norm(aw)
+    np.testing.assert_allclose(s, oracle.svd(aw)[1], rtol=1e-12)
+
+
+def test_svd_errors(engine):
+    with pytest.raises(engine.ArgumentError):
+        engine.truncated_svd(np.ones((3, 2)), 3)
+    bad = np.ones((3, 3))
+    bad[1, 1] = np.inf
+    with pytest.raises(engine.NumericError):
+        engine.svd(bad)
+
+
+def _slice_parity(engine, oracle, a, q, k, s_tol=1e-10, rec_tol=1e-10):
+    t = engine.Transform.custom(q)
+    f = engine.tsvdq(a, t, k)
+    U, S, V = oracle.tsvdq(a, q, k)
+    # singular values, relative per value
+    ok = S > 1e-13 * S.max()
+    assert np.max(np.abs(f.s - S)[ok] / S[ok]) <= s_tol
+    # reconstruction, relative to ||A|| (sign/rotation invariant)
+    rg = engine.tsvdq_reconstruct(f)
+    ro = oracle.tsvdq_reconstruct(U, S, V, q)
+    assert rel(rg, ro) <= rec_tol * np.linalg.norm(a) / max(np.linalg.norm(ro), 1e-300)
+    # relative error
+    reg = engine.relative_error(a, rg)
+    reo = oracle.relative_error(a, ro)
+    assert abs(reg - reo) <= 1e-10 * max(reo, 1e-300) + 1e-15
+    assert abs(engine.tsvdq_relative_error(a, f) - reo) <= 1e-10 * max(reo, 1e-300) + 1e-15
+    # factor contracts
+    for i in range(q.shape[1]):
+        u, v = f.u[:, :, i], f.v[:, :, i]
+        assert np.linalg.norm(u.T @ u - np.eye(k)) <= 1e-10 * k
+        assert np.linalg.norm(v.T @ v - np.eye(k)) <= 1e-10 * k
+        assert np.all(np.diff(f.s[:, i]) <= 0)
+    return f
+
+
+def test_tsvdq_cfg1_vs_oracle(engine, oracle):
+    # BASELINE configs[0]: tSVDQ k=4 with the random orthogonal p=8 basis
+    a = oracle.random_tensor(64, 48, 32, 0)
+    q = oracle.random_orthogonal_q(32, 8, 1)
+    f = _slice_parity(engine, oracle, a, q, 4)
+    # sign rule -> factors comparable where the gap is clear
+    U, S, V = oracle.tsvdq(a, q, 4)
+    for i in range(8):
+        s = S[:, i]
+        for j in range(4):
+            gap = min(abs(s[j] - s[j - 1]) if j else np.inf,
+                      abs(s[j] - s[j + 1]) if j + 1 < 4 else np.inf) / s[0]
+            if gap >= 1e-8:
+                assert np.abs(f.u[:, j, i] - U[:, j, i]).max() <= 1e-8
+                assert np.abs(f.v[:, j, i] - V[:, j, i]).max() <= 1e-8
+
+
+def test_tsvdq_error_kats(engine):
+    a = counterexample()
+    tdd = engine.data_dependent_transform(a, 1)
+    tot, ey, pr = engine.tsvdq_error(a, engine.tsvdq(a, tdd, 1))
+    assert abs(tot - math.sqrt(3.0)) <= 1e-12
+    assert abs(ey - 1.0) <= 1e-12
+    assert abs(pr - SQ2) <= 1e-12
+    th = engine.Transform("haar", 2, 1)
+    f = engine.tsvdq(a, th, 1)
+    tot, ey, pr = engine.tsvdq_error(a, f)
+    assert abs(tot - SQ2) <= 1e-12 and abs(ey) <= 1e-12 and abs(pr - SQ2) <= 1e-12
+    assert abs(engine.relative_error(a, engine.tsvdq_reconstruct(f)) - SQ2 / 2) <= 1e-12
+
+
+def test_projection_error_kat(engine, oracle):
+    assert engine.projection_error(tube([2, 4, 6, 8]), engine.Transform("haar", 4, 2)) == \
+        pytest.approx(math.sqrt(66.0), abs=1e-12)
+    a = oracle.random_tensor(20, 30, 17, 4)
+    q = oracle.dct_q(17, 6)
+    assert engine.projection_error(a, engine.Transform("dct", 17, 6)) == pytest.approx(
+        oracle.projection_error(a, q), rel=1e-12)
+
+
+def test_tsvdq_error_vs_oracle_and_ey_identity(engine, oracle):
+    a = oracle.random_tensor(6, 5, 7, 7)
+    t = engine.Transform("dct", 7, 4)
+    f = engine.tsvdq(a, t, 3)
+    tot, ey, pr = engine.tsvdq_error(a, f)
+    U, S, V = oracle.tsvdq(a, t.q, 3)
+    to, eo, po = oracle.tsvdq_error(a, U, S, V, t.q)
+    nrm = np.linalg.norm(a)
+    assert abs(tot - to) <= 1e-10 * nrm and abs(ey - eo) <= 1e-10 * nrm and abs(pr - po) <= 1e-10 * nrm
+    assert abs(tot ** 2 - (ey ** 2 + pr ** 2)) <= 1e-10 * nrm ** 2
+    assert f.u.shape == (6, 3, 4) and f.v.shape == (5, 3, 4) and f.s.shape == (3, 4)
+
+
+def test_tsvdq_limits(engine, oracle):
+    a = oracle.random_tensor(4, 3, 5, 42)
+    nrm = np.linalg.norm(a)
+    full = engine.Transform("random", 5, 5, seed=9)
+    f = engine.tsvdq(a, full, 3)
+    assert np.linalg.norm(a - engine.tsvdq_reconstruct(f)) <= 1e-10 * nrm
+    tot, ey, pr = engine.tsvdq_error(a, f)
+    assert tot <= 1e-10 * nrm and ey <= 1e-10 * nrm and pr <= 1e-10 * nrm
+    part = engine.Transform("random", 5, 3, seed=9)
+    fp = engine.tsvdq(a, part, 3)
+    proj = oracle.mode3_product(a, part.q @ part.q.T)
+    assert np.linalg.norm(proj - engine.tsvdq_reconstruct(fp)) <= 1e-10 * nrm
+    z = np.zeros((4, 3, 5))
+    assert np.linalg.norm(engine.tsvdq_reconstruct(engine.tsvdq(z, part, 2))) == 0.0
+    with pytest.raises(engine.ArgumentError):
+        engine.tsvdq(a, part, 0)
+    with pytest.raises(engine.ArgumentError):
+        engine.tsvdq(a, part, 5)
+
+
+def test_tsvdq_exact_rank(engine, oracle):
+    q = oracle.random_orthogonal_q(6, 4, 17)
+    hat = np.zeros((5, 4, 4), order="F")
+    for s in range(4):
+        hat[:, :, s] = oracle.random_matrix(5, 2, 100 + s) @ oracle.random_matrix(4, 2, 200 + s).T
+    a = oracle.mode3_product(hat, q)
+    f = engine.tsvdq(a, engine.Transform.custom(q), 2)
+    tot, ey, pr = engine.tsvdq_error(a, f)
+    nrm = np.linalg.norm(a)
+    assert abs(tot - pr) <= 1e-10 * nrm and ey <= 1e-10 * nrm and tot <= 1e-10 * nrm
+
+
+@pytest.mark.parametrize("k", [1, 5, 10, 20])
+def test_tsvdq_video_scaled_vs_oracle(engine, oracle, k):
+    # cfg2 distribution at 60x80x50 (oracle-sized); shared Q (SURVEY §8c rule 1)
+    a = synth.video(60, 80, 50, seed=3)
+    q, _, _ = oracle.data_dependent_q(a, 20)
+    _slice_parity(engine, oracle, a, q, k)
+
+
+# --------------------------------------------------------------- data-driven Q
+def test_data_q_kats(engine, oracle):
+    a = counterexample()
+    t = engine.data_dependent_transform(a, 2)
+    aq = np.abs(t.q)
+    assert np.abs(aq - np.eye(2)).max() <= 1e-12 or np.abs(aq - np.eye(2)[::-1]).max() <= 1e-12
+    v = np.array([1 / 3, 2 / 3, 2 / 3])
+    b = oracle.random_matrix(2, 2, 5)[:, :, None] * v[None, None, :]
+    t1 = engine.data_dependent_transform(b, 1)
+    assert min(np.linalg.norm(t1.q[:, 0] - v), np.linalg.norm(t1.q[:, 0] + v)) <= 1e-12
+    g = oracle.random_tensor(4, 3, 5, 11)
+    assert engine.projection_error(g, engine.data_dependent_transform(g, 5)) <= 1e-10
+
+
+@pytest.mark.parametrize("shape,p", [((20, 30, 16), 6), ((40, 50, 64), 12), ((3, 2, 9), 8)])
+def test_data_q_vs_oracle(engine, oracle, shape, p):
+    a = oracle.random_tensor(*shape, 5)
+    t = engine.data_dependent_transform(a, p)
+    qo, so, comp = oracle.data_dependent_q(a, p)
+    assert t.completed_basis == comp
+    assert np.abs(t.q.T @ t.q - np.eye(p)).max() <= 1e-12
+    n1, n2, n3 = shape
+    avail = min(n3, n1 * n2)
+    unf = a.reshape(n1 * n2, n3, order="F")
+    lam = np.sum((unf @ t.q) ** 2, axis=0)  # captured energy per column = sigma_j^2
+    sig2 = so[:min(p, avail)] ** 2
+    assert np.max(np.abs(lam[:len(sig2)] - sig2)) <= 1e-12 * sig2[0]
+    # projector agreement on the leading block with a clear gap
+    pg = t.q[:, :min(p, avail)] @ t.q[:, :min(p, avail)].T
+    po = qo[:, :min(p, avail)] @ qo[:, :min(p, avail)].T
+    assert np.abs(pg - po).max() <= 1e-9
+    # sign rule
+    for j in range(min(p, avail)):
+        i = int(np.argmax(np.abs(t.q[:, j])))
+        assert t.q[i, j] >= 0
+
+
+def test_data_q_deterministic(engine):
+    a = synth.hyperspectral(48, 40, 60, seed=1)
+    q1 = engine.data_dependent_transform(a, 12).q
+    q2 = engine.data_dependent_transform(a, 12).q
+    assert np.array_equal(q1, q2)
+
+
+def test_hyperspectral_scaled_pipeline(engine, oracle):
+    # cfg3 distribution at 64x64x224: data Q p=32 (parity on eigenvalues and
+    # captured energy), then tSVDQ k=16 with the shared Q.
+    a = synth.hyperspectral(64, 64, 224, seed=2)
+    t = engine.data_dependent_transform(a, 32)
+    qo, so, _ = oracle.data_dependent_q(a, 32)
+    unf = a.reshape(-1, 224, order="F")
+    cap_g, cap_o = np.sum((unf @ t.q) ** 2), np.sum((unf @ qo) ** 2)
+    assert abs(cap_g - cap_o) <= 1e-12 * cap_o
+    _slice_parity(engine, oracle, a, qo, 16)
+    # RE with own Q vs oracle with own Q (rule 3)
+    f = engine.tsvdq(a, t, 16)
+    U, S, V = oracle.tsvdq(a, qo, 16)
+    reo = oracle.relative_error(a, oracle.tsvdq_reconstruct(U, S, V, qo))
+    assert abs(engine.tsvdq_relative_error(a, f) - reo) <= 1e-10 * reo
+
+
+# --------------------------------------------------------------- device mode
+def test_device_arrays_zero_copy(engine, oracle):
+    import torch
+    a = oracle.random_tensor(40, 30, 24, 9)
+    q = oracle.dct_q(24, 6)
+    da = engine.to_device(a)
+    t = engine.Transform("dct", 24, 6)
+    f = engine.tsvdq(da, t, 5)
+    assert isinstance(f.u, torch.Tensor) and f.u.is_cuda
+    fh = engine.tsvdq(a, t, 5)
+    np.testing.assert_allclose(engine.to_host(f.s), fh.s, rtol=1e-14)
+    re_dev = engine.tsvdq_relative_error(da, f)
+    assert re_dev == pytest.approx(engine.tsvdq_relative_error(a, fh), rel=1e-13)
+    c = engine.star_q(da, engine.to_device(np.asfortranarray(a.transpose(1, 0, 2))), t)
+    want = oracle.star_q_product(a, np.asfortranarray(a.transpose(1, 0, 2)), q)
+    assert rel(engine.to_host(c), want) <= 1e-12
