@@ -1,0 +1,515 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 projected star-Q / tSVDQ engine (BASELINE.json metric:
+"tSVDQ input GB/s and star-Q product TFLOP/s (FP64) vs roofline").
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg5|cfg4|cfg3|cfg2]
+                  [--impl ours|reference]
+
+Workloads (BASELINE.json configs, synthetic inputs of the named shapes):
+  cfg5  2048x2048x1024 rank-50 CP + noise; data-driven Q (p=128) + tSVDQ k=32
+        + fused reconstruction relative error.  metric: tSVDQ input GB/s.
+  cfg4  star-Q product A 1024x512x256 * B 512x1024x256, DCT p=64.  metric: TFLOP/s.
+  cfg3  512x512x224 hyperspectral, data Q p=32, k=16.  cfg2  240x320x200 video, p=20, k=10.
+
+One step = one pass of the hot path over one input already resident in HBM
+(`value`); `e2e` repeats it through the C-ABI with pinned HOST buffers, the
+H2D of the inputs and the D2H of the result inside the timed region.
+Under torchrun (N>1) every rank runs its own instance of the workload
+(independent tensors, no data-path collective): weak scaling.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import math
+import os
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FP64_PEAK_FALLBACK = 36.914  # TFLOP/s, MEASURED_FP64.json (DMMA m8n8k4, this pool)
+
+
+def load_peaks():
+    peaks = {"hbm_gbs": 6540.5, "fp64_tflops": FP64_PEAK_FALLBACK,
+             "hbm_src": "MEASURED_PEAKS.json", "fp64_src": "MEASURED_FP64.json"}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks["hbm_gbs"] = float(json.load(f)["hbm_gbs"])
+    except Exception:
+        peaks["hbm_gbs"], peaks["hbm_src"] = 6650.0, "fallback (B200_PROFILING.md)"
+    try:
+        with open(os.path.join(ROOT, "MEASURED_FP64.json")) as f:
+            d = json.load(f)
+        peaks["fp64_tflops"] = float(d["dmma_m8n8k4_tflops"])
+    except Exception:
+        peaks["fp64_src"] = "constant from MEASURED_FP64.json (r01)"
+    return peaks
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms while running."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                rows.append(parts)
+        os.unlink(self.path)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = sorted(float(r[1]) for r in rows if r[1].replace(".", "").isdigit())
+        mx = max(float(r[2]) for r in rows if r[2].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx,
+                "reasons": reasons, "samples": len(rows)}
+
+
+# --------------------------------------------------------------- helpers
+def sync_all(dist_on):
+    import torch
+    torch.cuda.synchronize()
+    if dist_on:
+        import torch.distributed as dist
+        dist.barrier()
+        torch.cuda.synchronize()
+
+
+def max_over_ranks(x, dist_on):
+    if not dist_on:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def timing_report(L, reset=True):
+    buf = C.create_string_buffer(1 << 16)
+    rc = L.ppc_timing_report(buf, len(buf), 1 if reset else 0)
+    if rc:
+        raise RuntimeError(L.ppc_last_error().decode())
+    return json.loads(buf.value.decode())
+
+
+def ptr(t):
+    return C.c_void_p(t.data_ptr())
+
+
+def flat_host(t):
+    """Pinned host copy of a Fortran-laid-out device tensor (mode-1 fastest)."""
+    return t.permute(*reversed(range(t.dim()))).contiguous().reshape(-1).cpu().pin_memory()
+
+
+# --------------------------------------------------------------- workloads
+class StarQ:
+    """cfg4: C = [(A x3 Q^T) facewise (B x3 Q^T)] x3 Q (star_products.cpp:51-59)."""
+
+    name = "cfg4"
+    metric, unit = "starq_tflops", "TFLOP/s"
+
+    def __init__(self, n1=1024, m=512, n2=1024, n3=256, p=64, seed=0):
+        import torch
+        import paper_2409_19402_b200 as pp
+        from paper_2409_19402_b200 import synth
+        self.dims = (n1, m, n2, n3, p)
+        self.A = synth.gaussian_device(n1, m, n3, seed, 1)
+        self.B = synth.gaussian_device(m, n2, n3, seed, 2)
+        self.Q = pp.to_device(pp.Transform("dct", n3, p).q)
+        self.Cout = pp.empty_device((n1, n2, n3))
+        self.flops = 2.0 * p * (n1 * m * n3 + m * n2 * n3 + n1 * m * n2 + n1 * n2 * n3)
+        self.in_bytes = 8.0 * (n1 * m * n3 + m * n2 * n3)
+        self.torch = torch
+
+    def config(self):
+        n1, m, n2, n3, p = self.dims
+        return {"workload": "cfg4 star-Q product", "A": [n1, m, n3], "B": [m, n2, n3], "p": p,
+                "transform": "dct", "l2": "inputs (2 GiB) > L2; no flush needed"}
+
+    def step(self, L):
+        n1, m, n2, n3, p = self.dims
+        rc = L.ppc_star_q_product(ptr(self.A), n1, m, n3, ptr(self.B), n2, ptr(self.Q), p,
+                                  C.c_double(1.0), ptr(self.Cout), 1)
+        if rc:
+            raise RuntimeError(L.ppc_last_error().decode())
+
+    def value(self, sec):
+        return self.flops / sec / 1e12
+
+    def dominant(self, stages):
+        return "facewise", "tensor"
+
+    def e2e_setup(self):
+        torch = self.torch
+        n1, m, n2, n3, p = self.dims
+        self.hA = flat_host(self.A)
+        self.hB = flat_host(self.B)
+        self.hQ = flat_host(self.Q)
+        self.hC = torch.empty(n1 * n2 * n3, dtype=torch.float64).pin_memory()
+        self.h2d = 8 * (n1 * m * n3 + m * n2 * n3 + n3 * p)
+        self.d2h = 8 * n1 * n2 * n3
+
+    def e2e_step(self, L):
+        n1, m, n2, n3, p = self.dims
+        rc = L.ppc_star_q_product(ptr(self.hA), n1, m, n3, ptr(self.hB), n2, ptr(self.hQ), p,
+                                  C.c_double(1.0), ptr(self.hC), 0)
+        if rc:
+            raise RuntimeError(L.ppc_last_error().decode())
+
+    def cpu_sample(self, ppo, threads):
+        """Bounded sample: the same product with n1 and n2 cut to 128 (p, m, n3 kept)."""
+        import numpy as np
+        n1, m, n2, n3, p = 128, 512, 128, 256, 64
+        rng = np.random.default_rng(0)
+        a = np.asfortranarray(rng.standard_normal((n1, m, n3)))
+        b = np.asfortranarray(rng.standard_normal((m, n2, n3)))
+        q = ppo.dct_q(n3, p)
+        flops = 2.0 * p * (n1 * m * n3 + m * n2 * n3 + n1 * m * n2 + n1 * n2 * n3)
+        t0 = time.perf_counter()
+        reps = 0
+        while True:
+            ppo.star_q_product(a, b, q)
+            reps += 1
+            if time.perf_counter() - t0 > 10.0 or reps >= 50:
+                break
+        sec = (time.perf_counter() - t0) / reps
+        return flops / sec / 1e12, f"star_q_product A {n1}x{m}x{n3}, B {m}x{n2}x{n3}, p={p} (n1,n2 cut 8x), {reps} reps"
+
+
+class Tsvdq:
+    """cfg2/3/5: data-driven Q (transforms.cpp:97-115) + tsvdq (decompositions.cpp:62-83)
+    + relative_error(A, tsvdq_reconstruct(F)) fused (tools/main.cpp:276-283 chain)."""
+
+    metric, unit = "tsvdq_input_GBps", "GB/s"
+
+    def __init__(self, name, n1, n2, n3, p, k, seed=0):
+        import torch
+        import paper_2409_19402_b200 as pp
+        from paper_2409_19402_b200 import synth
+        self.name = name
+        self.dims = (n1, n2, n3, p, k)
+        self.torch = torch
+        if name == "cfg5":
+            self.A = synth.cp_tensor_device(n1, n2, n3, rank=50, noise=1e-3, seed=seed)
+        elif name == "cfg3":
+            self.A = pp.to_device(synth.hyperspectral(n1, n2, n3, seed=seed))
+        else:
+            self.A = pp.to_device(synth.video(n1, n2, n3, seed=seed))
+        self.Q = pp.empty_device((n3, p))
+        self.U = pp.empty_device((n1, k, p))
+        self.S = pp.empty_device((k, p))
+        self.V = pp.empty_device((n2, k, p))
+        self.in_bytes = 8.0 * n1 * n2 * n3
+        self.re = None
+
+    def config(self):
+        n1, n2, n3, p, k = self.dims
+        desc = {"cfg5": "cfg5 rank-50 CP + N(0,1e-3^2) noise", "cfg3": "cfg3 hyperspectral",
+                "cfg2": "cfg2 video"}[self.name]
+        return {"workload": desc + " tSVDQ with data-driven Q", "shape": [n1, n2, n3], "p": p,
+                "k": k, "step": "data_dependent_transform + tsvdq + relative_error(A, recon)",
+                "l2": "input > L2" if self.in_bytes > 126e6 else "input < L2 (resident)"}
+
+    def step(self, L):
+        n1, n2, n3, p, k = self.dims
+        comp = C.c_int(0)
+        for rc in (L.ppc_data_dependent_q(ptr(self.A), n1, n2, n3, p, ptr(self.Q), None, C.byref(comp), 1),
+                   L.ppc_tsvdq(ptr(self.A), n1, n2, n3, ptr(self.Q), p, k, ptr(self.U), ptr(self.S),
+                               ptr(self.V), 1)):
+            if rc:
+                raise RuntimeError(L.ppc_last_error().decode())
+        re = C.c_double()
+        rc = L.ppc_tsvdq_relative_error(ptr(self.A), n1, n2, n3, ptr(self.U), ptr(self.S), ptr(self.V),
+                                        ptr(self.Q), p, k, C.byref(re), 1)
+        if rc:
+            raise RuntimeError(L.ppc_last_error().decode())
+        self.re = re.value
+
+    def value(self, sec):
+        return self.in_bytes / sec / 1e9
+
+    def dominant(self, stages):
+        best = max(stages.items(), key=lambda kv: kv[1]["ms"])[0] if stages else "gram_syrk"
+        return best, "tensor"
+
+    def e2e_setup(self):
+        torch = self.torch
+        n1, n2, n3, p, k = self.dims
+        self.hA = flat_host(self.A)
+        self.hQ = torch.empty(n3 * p, dtype=torch.float64).pin_memory()
+        self.hU = torch.empty(n1 * k * p, dtype=torch.float64).pin_memory()
+        self.hS = torch.empty(k * p, dtype=torch.float64).pin_memory()
+        self.hV = torch.empty(n2 * k * p, dtype=torch.float64).pin_memory()
+        # inputs once per step; results (Q + factors) back once; the RE call
+        # re-stages A (it is a separate public call taking host buffers).
+        self.h2d = 8 * (2 * n1 * n2 * n3 + (n1 + n2 + 1) * k * p + n3 * p)
+        self.d2h = 8 * (n3 * p + (n1 + n2 + 1) * k * p) + 8
+
+    def e2e_step(self, L):
+        n1, n2, n3, p, k = self.dims
+        comp = C.c_int(0)
+        re = C.c_double()
+        for rc in (
+            L.ppc_data_dependent_q(ptr(self.hA), n1, n2, n3, p, ptr(self.hQ), None, C.byref(comp), 0),
+            L.ppc_tsvdq(ptr(self.hA), n1, n2, n3, ptr(self.hQ), p, k, ptr(self.hU), ptr(self.hS),
+                        ptr(self.hV), 0),
+            L.ppc_tsvdq_relative_error(ptr(self.hA), n1, n2, n3, ptr(self.hU), ptr(self.hS),
+                                       ptr(self.hV), ptr(self.hQ), p, k, C.byref(re), 0)):
+            if rc:
+                raise RuntimeError(L.ppc_last_error().decode())
+
+    def cpu_sample(self, ppo, threads):
+        """Bounded sample of the same pipeline on the oracle (reference algorithm
+        restated, OpenBLAS GEMMs): n1 cut so the sample takes ~10-30 s."""
+        import numpy as np
+        from paper_2409_19402_b200 import synth
+        n1, n2, n3, p, k = self.dims
+        if self.name == "cfg5":
+            s1, s2 = 256, 256
+            a = synth.cp_tensor(s1, s2, n3, rank=50, noise=1e-3, seed=1)
+        elif self.name == "cfg3":
+            s1, s2 = 128, 128
+            a = synth.hyperspectral(s1, s2, n3, seed=1)
+        else:
+            s1, s2 = n1, n2
+            a = synth.video(n1, n2, n3, seed=1)
+        t0 = time.perf_counter()
+        q, _, _ = ppo.data_dependent_q(a, p)
+        U, S, V = ppo.tsvdq(a, q, k)
+        re = ppo.relative_error(a, ppo.tsvdq_reconstruct(U, S, V, q))
+        sec = time.perf_counter() - t0
+        return (8.0 * s1 * s2 * n3) / sec / 1e9, (f"oracle data Q + tsvdq + RE on a {s1}x{s2}x{n3} "
+                                                  f"tensor of the same distribution (p={p}, k={k}), 1 rep")
+
+
+def make_workload(name):
+    if name == "cfg4":
+        return StarQ()
+    dims = {"cfg5": (2048, 2048, 1024, 128, 32), "cfg3": (512, 512, 224, 32, 16),
+            "cfg2": (240, 320, 200, 20, 10)}[name]
+    return Tsvdq(name, *dims)
+
+
+# --------------------------------------------------------------- reference arm
+def run_reference(args, rank, world):
+    """--impl reference: the reference algorithm (oracle port; the C++/Eigen
+    reference cannot be built here — no Eigen) timed on the host cores."""
+    if rank != 0:
+        return
+    from oracle import ppo
+    ppo.use_openblas()
+    threads = os.cpu_count() or 1
+    ppo.set_threads(threads)
+    wl_cls = {"cfg4": StarQ}.get(args.workload)
+    vals = []
+
+    class _Shim:  # cpu_sample needs only dims/name
+        pass
+
+    if args.workload == "cfg4":
+        sample_fn = StarQ.cpu_sample
+        shim = _Shim()
+        metric, unit = StarQ.metric, StarQ.unit
+    else:
+        dims = {"cfg5": (2048, 2048, 1024, 128, 32), "cfg3": (512, 512, 224, 32, 16),
+                "cfg2": (240, 320, 200, 20, 10)}[args.workload]
+        shim = _Shim()
+        shim.name, shim.dims = args.workload, dims
+        sample_fn = Tsvdq.cpu_sample
+        metric, unit = Tsvdq.metric, Tsvdq.unit
+    desc = ""
+    for _ in range(args.warmup if args.workload == "cfg4" else 0):
+        sample_fn(shim, ppo, threads)
+    for _ in range(args.steps):
+        v, desc = sample_fn(shim, ppo, threads)
+        vals.append(v)
+    vals.sort()
+    v = vals[len(vals) // 2]
+    line = {"impl": "reference", "metric": metric, "value": v, "unit": unit, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.workload, "sample": desc},
+            "cpu_baseline": {"value": v, "unit": unit, "cores": threads, "kind": "port",
+                             "sample": desc + "; reference algorithm restated in C (oracle/ppo.c), "
+                                              "GEMMs on OpenBLAS 1 thread, slice loops on all cores"},
+            "e2e": {"value": v, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default=os.environ.get("PPC_BENCH_WORKLOAD", "cfg4"),
+                    choices=["cfg5", "cfg4", "cfg3", "cfg2"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    dist_on = world > 1
+    torch.cuda.set_device(local)
+    if dist_on:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_2409_19402_b200 as pp  # noqa: F401
+    from paper_2409_19402_b200 import _lib
+    L = _lib.lib()
+    if L.ppc_set_device(local):
+        raise RuntimeError(L.ppc_last_error().decode())
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    L.ppc_set_stream(C.c_void_p(stream.cuda_stream))
+
+    peaks = load_peaks()
+    wl = make_workload(args.workload)
+    torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        wl.step(L)
+    sync_all(dist_on)
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    L.ppc_launch_count(1)
+    timing_report(L, reset=True)
+    L.ppc_timing_enable(1)
+    sync_all(dist_on)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        wl.step(L)
+    e1.record(stream)
+    sync_all(dist_on)
+    L.ppc_timing_enable(0)
+    ms = e0.elapsed_time(e1)
+    launches = int(L.ppc_launch_count(1))
+    stages = timing_report(L, reset=True)
+    clk = clocks.stop()
+    ms = max_over_ranks(ms, dist_on)
+    ms_step = ms / args.steps
+    value_rank = wl.value(ms_step / 1e3)
+    value = value_rank * world  # every rank processes its own instance (weak)
+
+    # dominant kernel roofline (algorithmic flops or bytes per launch / avg launch time)
+    dom, bound = wl.dominant(stages)
+    st = stages.get(dom, {"ms": float("nan"), "n": 1, "flops": 0.0, "bytes": 0.0})
+    avg_ms = st["ms"] / max(1, st["n"])
+    if bound == "tensor":
+        achieved = (st["flops"] / max(1, st["n"])) / (avg_ms / 1e3) / 1e12
+        roof = {"bound": "tensor", "achieved": achieved, "peak": peaks["fp64_tflops"],
+                "unit": "TFLOP/s", "frac": achieved / peaks["fp64_tflops"], "traffic": None,
+                "kernel": dom, "peak_source": peaks["fp64_src"] + " (FP64 DMMA; no tcgen05 f64 kind)"}
+    else:
+        achieved = (st["bytes"] / max(1, st["n"])) / (avg_ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / peaks["hbm_gbs"], "traffic": None, "kernel": dom,
+                "peak_source": peaks["hbm_src"]}
+    stage_summary = {}
+    for name, s in stages.items():
+        a_ms = s["ms"] / max(1, s["n"])
+        stage_summary[name] = {"ms_per_launch": round(a_ms, 4), "launches": s["n"],
+                               "share": round(s["ms"] / ms, 4) if ms > 0 else None}
+        if s["flops"]:
+            stage_summary[name]["tflops"] = round(s["flops"] / s["n"] / (a_ms / 1e3) / 1e12, 3)
+        if s["bytes"]:
+            stage_summary[name]["gbs"] = round(s["bytes"] / s["n"] / (a_ms / 1e3) / 1e9, 1)
+
+    # end-to-end through the C-ABI with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        wl.e2e_setup()
+        wl.e2e_step(L)  # warm
+        sync_all(dist_on)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            wl.e2e_step(L)
+        torch.cuda.synchronize()
+        sec = max_over_ranks((time.perf_counter() - t0) / args.steps, dist_on)
+        e2e = {"value": wl.value(sec) * world, "unit": wl.unit, "h2d_bytes_per_step": wl.h2d,
+               "d2h_bytes_per_step": wl.d2h, "ms_per_step": sec * 1e3}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            from oracle import ppo
+            ppo.use_openblas()
+            threads = os.cpu_count() or 1
+            ppo.set_threads(threads)
+            v, desc = wl.cpu_sample(ppo, threads)
+            cpu = {"value": v, "unit": wl.unit, "cores": threads, "kind": "port",
+                   "sample": desc + "; reference algorithm restated in C (oracle/ppo.c; Eigen "
+                                    "reference unbuildable here), OpenBLAS 1-thread GEMMs, slice loops on all cores"}
+        except Exception as ex:  # pragma: no cover
+            cpu = {"value": None, "unit": wl.unit, "cores": 0, "kind": "port", "sample": f"failed: {ex}"}
+
+    if rank == 0:
+        cfg = wl.config()
+        cfg["parallelism"] = f"replicas{world}" if world > 1 else "single"
+        line = {"metric": wl.metric, "value": value, "unit": wl.unit, "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic", "config": cfg, "roofline": roof, "cpu_baseline": cpu,
+                "e2e": e2e, "gpu_launches": launches, "clocks": clk, "stages": stage_summary}
+        if getattr(wl, "re", None) is not None:
+            line["result_check"] = {"relative_error": wl.re}
+        print(json.dumps(line), flush=True)
+
+    if dist_on:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -67,8 +67,11 @@ int ppc_synchronize(void);
 /* Kernel launches issued by the library on this thread since the last reset
  * (for the bench's gpu_launches count). */
 int64_t ppc_launch_count(int reset);
-/* Device timing of the most recent launch of the dominant kernel class
- * ("gemm", "jacobi", ...) is not tracked here; bench.py times with events. */
+/* Per-stage device timing with CUDA events recorded on the launching stream
+ * (off by default). ppc_timing_report writes a JSON object
+ * {"stage": {"ms", "n", "flops", "bytes"}} (algorithmic flops/bytes). */
+int ppc_timing_enable(int on);
+int ppc_timing_report(char* buf, int64_t cap, int reset);
 
 /* ---- L3 kernels (tensor.hpp, matrix_kernels.hpp) ------------------------ */
 /* tensor.hpp:87 / tensor.cpp:139-147: out = A x3 op(M).

@@ -15,6 +15,8 @@ namespace ppc {
 
 void mode3(const double* T, int64_t N, int64_t n3, const double* M, int64_t q, bool trans_m,
            double* out, double alpha, cudaStream_t s) {
+    StageTimer tm(trans_m ? "mode3_fwd" : "mode3_inv", s, 2.0 * N * n3 * q,
+                  8.0 * (N * n3 + N * q + n3 * q));
     GemmDesc d;
     d.M = N; d.N = q; d.K = n3;
     d.A = T; d.lda = N; d.a_kmajor = false;
@@ -31,6 +33,7 @@ void mode3(const double* T, int64_t N, int64_t n3, const double* M, int64_t q, b
 
 void facewise(const double* A, int64_t n1, int64_t m, int64_t p, const double* B, int64_t n2,
               double* C, cudaStream_t s) {
+    StageTimer tm("facewise", s, 2.0 * n1 * m * n2 * p, 8.0 * p * (n1 * m + m * n2 + n1 * n2));
     GemmDesc d;
     d.M = n1; d.N = n2; d.K = m; d.batch = p;
     d.A = A; d.lda = n1; d.strideA = n1 * m;
@@ -124,6 +127,7 @@ std::array<double, 2> recon_residual(const double* A, int64_t n1, int64_t n2, in
                                      const double* U, const double* S, const double* V,
                                      const double* Q, int64_t p, int64_t k, cudaStream_t s) {
     const int64_t N = n1 * n2;
+    StageTimer tm("recon_residual", s, 2.0 * p * N * k + 2.0 * N * p * n3, 8.0 * N * (p + n3));
     DeviceBuffer ch(sizeof(double) * N * p);
     core_from_factors(U, S, V, n1, n2, p, k, ch.d(), s);
     GemmDesc d;
@@ -139,7 +143,11 @@ void tsvdq(const double* A, int64_t n1, int64_t n2, int64_t n3, const double* Q,
     DeviceBuffer ah(sizeof(double) * N * p);
     mode3(A, N, n3, Q, p, true, ah.d(), 1.0, s);  // decompositions.cpp:65
     require_finite(ah.d(), N * p, "svd", s);       // matrix_kernels.cpp:32
-    slice_svd(ah.d(), n1, n2, N, p, k, U, S, V, nullptr, s);  // :75-81
+    {
+        StageTimer tm("slice_svd", s, (double)p * std::min(n1, n2) * std::min(n1, n2) * std::max(n1, n2) +
+                                          4.0 * p * N * k, 8.0 * p * N);
+        slice_svd(ah.d(), n1, n2, N, p, k, U, S, V, nullptr, s);  // :75-81
+    }
 }
 
 ErrorParts tsvdq_error(const double* A, int64_t n1, int64_t n2, int64_t n3, const double* U,

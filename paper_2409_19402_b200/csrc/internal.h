@@ -88,6 +88,21 @@ struct Out {
     void finish();  // D2H for host outputs
 };
 
+// Optional per-stage device timing (CUDA events on the launching stream),
+// enabled by ppc_timing_enable(); used by bench.py for the roofline.
+class StageTimer {
+public:
+    StageTimer(const char* name, cudaStream_t s, double flops = 0.0, double bytes = 0.0);
+    ~StageTimer();
+    StageTimer(const StageTimer&) = delete;
+    StageTimer& operator=(const StageTimer&) = delete;
+private:
+    const char* name_;
+    cudaStream_t s_;
+    double flops_, bytes_;
+    cudaEvent_t e0_ = nullptr;
+};
+
 void validate_loc(int loc);
 void require_positive(int64_t v, const char* what);
 

@@ -4,7 +4,9 @@
 // device per host thread.
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <vector>
 
 #include "internal.h"
 #include "kernels.cuh"
@@ -124,6 +126,35 @@ void Out::finish() {
         PPC_CUDA_CHECK(cudaMemcpyAsync(host, d, count * sizeof(double), cudaMemcpyDeviceToHost, stream()));
 }
 
+// ---------------------------------------------------------- stage timing
+namespace {
+struct StageRec {
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev;
+    double flops = 0.0, bytes = 0.0;
+    int64_t launches = 0;
+};
+thread_local bool t_timing = false;
+thread_local std::map<std::string, StageRec> t_stages;
+}  // namespace
+
+StageTimer::StageTimer(const char* name, cudaStream_t s, double flops, double bytes)
+    : name_(name), s_(s), flops_(flops), bytes_(bytes) {
+    if (!t_timing) return;
+    cudaEventCreate(&e0_);
+    cudaEventRecord(e0_, s_);
+}
+StageTimer::~StageTimer() {
+    if (!e0_) return;
+    cudaEvent_t e1;
+    cudaEventCreate(&e1);
+    cudaEventRecord(e1, s_);
+    StageRec& r = t_stages[name_];
+    r.ev.emplace_back(e0_, e1);
+    r.flops += flops_;
+    r.bytes += bytes_;
+    r.launches += 1;
+}
+
 void set_error(const std::string& m) { t_err = m; }
 const char* last_error() { return t_err.c_str(); }
 
@@ -176,6 +207,46 @@ int ppc_synchronize(void) {
         ppc::set_error(e.what());
         return e.code;
     }
+}
+
+int ppc_timing_enable(int on) {
+    ppc::t_timing = on != 0;
+    return 0;
+}
+
+// JSON object {"stage": {"ms": total, "n": launches, "flops": F, "bytes": B}, ...}
+// of everything recorded since the last reset; synchronizes the events.
+int ppc_timing_report(char* buf, int64_t cap, int reset) {
+    return ppc::guarded([&] {
+        std::string out = "{";
+        bool first = true;
+        for (auto& kv : ppc::t_stages) {
+            double ms = 0.0;
+            for (auto& pr : kv.second.ev) {
+                PPC_CUDA_CHECK(cudaEventSynchronize(pr.second));
+                float t = 0.f;
+                PPC_CUDA_CHECK(cudaEventElapsedTime(&t, pr.first, pr.second));
+                ms += t;
+            }
+            char tmp[256];
+            snprintf(tmp, sizeof tmp, "%s\"%s\": {\"ms\": %.6f, \"n\": %lld, \"flops\": %.6e, \"bytes\": %.6e}",
+                     first ? "" : ", ", kv.first.c_str(), ms, (long long)kv.second.launches,
+                     kv.second.flops, kv.second.bytes);
+            out += tmp;
+            first = false;
+        }
+        out += "}";
+        if ((int64_t)out.size() + 1 > cap) ppc::fail(PPC_ARGUMENT, "timing report buffer too small");
+        memcpy(buf, out.c_str(), out.size() + 1);
+        if (reset) {
+            for (auto& kv : ppc::t_stages)
+                for (auto& pr : kv.second.ev) {
+                    cudaEventDestroy(pr.first);
+                    cudaEventDestroy(pr.second);
+                }
+            ppc::t_stages.clear();
+        }
+    });
 }
 
 int64_t ppc_launch_count(int reset) {

@@ -78,6 +78,7 @@ void tree_reduce(double* parts, int64_t nparts, int64_t elems, cudaStream_t s) {
 }
 
 void gram(const double* T, int64_t N, int64_t n3, double* G, cudaStream_t s) {
+    StageTimer tm("gram_syrk", s, (double)N * n3 * n3, 8.0 * N * n3);
     const GramPlan g = gram_plan(N, n3);
     if (g.chunks == 1) {
         gram_partials(T, N, N, n3, g.chunk, 1, G, s);
@@ -107,7 +108,10 @@ bool data_q(const double* T, int64_t N, int64_t n3, int64_t p, double* Q, double
     // When p > min(n3, N) the unfolding has only `avail` singular vectors;
     // the eigenvectors of G for its zero eigenvalues complete the basis
     // (transforms.cpp:104-111 pads with an orthonormal completion).
-    sym_eig_top(G.d(), n3, p, Q, lam.d(), s);
+    {
+        StageTimer tm("eig_q", s);
+        sym_eig_top(G.d(), n3, p, Q, lam.d(), s);
+    }
     sign_rule(Q, n3, p, 1, nullptr, 0, s);  // fix_svd_signs on U3 (matrix_kernels.cpp:35)
     if (sigma) {
         sqrt_clamp_kernel<<<(unsigned)((p + 255) / 256), 256, 0, s>>>(lam.d(), sigma, p);
