@@ -8,7 +8,7 @@ namespace ppc {
 // Problems with min dimension <= this go to the one-CTA Jacobi kernel; larger
 // ones to the Gram + Chebyshev-filtered subspace iteration + Rayleigh-Ritz
 // polish path (subspace.cu).
-constexpr int64_t kSubspaceMinN = 1LL << 40;  // TODO(r1): lower once subspace path lands
+constexpr int64_t kSubspaceMinN = 160;
 
 struct GramPlan {
     int64_t chunks = 1;  // power of two
@@ -23,6 +23,9 @@ void tree_reduce(double* parts, int64_t nparts, int64_t elems, cudaStream_t s);
 
 void subspace_eig_top(const double* G, int64_t n, int64_t batch, int64_t p, double* Q,
                       double* lambda, cudaStream_t s);
+void slice_tail_energy(const double* A, int64_t m, int64_t n, int64_t stride, int64_t batch,
+                       int64_t k, const double* U, const double* S, const double* V, double* tail2,
+                       cudaStream_t s);
 void subspace_svd(const double* A, int64_t m, int64_t n, int64_t stride, int64_t batch, int64_t k,
                   double* U, double* S, double* V, double* tail2, cudaStream_t s);
 

@@ -1,14 +1,472 @@
-// Large-problem eigensolver / slice SVD (Gram + Chebyshev-filtered subspace
-// iteration + Rayleigh-Ritz polish). Placeholder until the path lands.
+// K5/K7 — top-k symmetric eigensolver and large-slice SVD.
+//
+// For slices too large for the one-CTA Jacobi kernel (K6) the facewise SVD
+// (matrix_kernels.cpp:29-37 applied per slice, decompositions.cpp:75-81)
+// runs as:
+//   1. batched Gram SYRK  G_i = A_i^T A_i  (or A_i A_i^T when wide)   [DMMA]
+//   2. top-k eigenvectors of every G_i by Chebyshev-filtered subspace
+//      iteration with Rayleigh-Ritz, prefix locking and operator deflation
+//      (G - X_L Theta_L X_L^T), a per-slice polynomial degree that bounds the
+//      amplification spread inside the active block, and CholQR2 (with a
+//      shift on the first pass) for orthonormalization            [DMMA]
+//   3. Rayleigh-Ritz polish on A itself: W = A V_k, one-sided Jacobi SVD of
+//      W -> U, sigma and the k x k rotation of V_k. This restores singular
+//      values to ~eps * sigma_1 absolute accuracy (the Gram route alone loses
+//      relative accuracy as (sigma_1/sigma_j)^2).
+// Every GEMM-shaped step is a batched call of the FP64 DMMA GEMM; the small
+// per-slice dense work (Cholesky + triangular inverse, b x b eigensolve) runs
+// one CTA per slice. The host drives the iteration and reads back only the
+// b Ritz values and residual norms per slice per iteration.
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "dmma_gemm.cuh"
+#include "engine.h"
 #include "internal.h"
+#include "jacobi.cuh"
+#include "kernels.cuh"
 #include "slice_svd.cuh"
 
 namespace ppc {
-void subspace_eig_top(const double*, int64_t, int64_t, int64_t, double*, double*, cudaStream_t) {
-    fail(PPC_ARGUMENT, "subspace_eig_top: not available yet");
+
+namespace {
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
 }
-void subspace_svd(const double*, int64_t, int64_t, int64_t, int64_t, int64_t, double*, double*,
-                  double*, double*, cudaStream_t) {
-    fail(PPC_ARGUMENT, "subspace_svd: not available yet");
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z += 0x9e3779b97f4a7c15ULL;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
 }
+
+// Deterministic N(0,1) start block (counter-based, Box-Muller).
+__global__ void randn_kernel(double* X, int64_t n, uint64_t seed) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+        const uint64_t a = mix64(seed ^ (2 * (uint64_t)i)), b = mix64(seed ^ (2 * (uint64_t)i + 1));
+        const double u1 = ((a >> 11) + 1) * 0x1.0p-53, u2 = (b >> 11) * 0x1.0p-53;
+        X[i] = sqrt(-2.0 * log(u1)) * cos(6.283185307179586 * u2);
+    }
+}
+
+// Y_next = a*Z + b*Y + c*Yp with per-slice coefficients coef[3*slice + {0,1,2}].
+__global__ void cheb_kernel(double* __restrict__ Yn, const double* __restrict__ Z,
+                            const double* __restrict__ Y, const double* __restrict__ Yp,
+                            const double* __restrict__ coef, int64_t per_slice, int64_t total) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
+        const int64_t s = i / per_slice;
+        const double a = coef[3 * s], b = coef[3 * s + 1], c = coef[3 * s + 2];
+        double v = a * Z[i] + b * Y[i];
+        if (c != 0.0) v += c * Yp[i];
+        Yn[i] = v;
+    }
+}
+
+// P(i, j, s) *= w(i, s)   (rows of the b x b block scaled: Theta_L mask)
+__global__ void scale_rows_kernel(double* P, const double* w, int64_t b, int64_t total) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
+        const int64_t row = i % b, s = i / (b * b);
+        P[i] *= w[row + s * b];
+    }
+}
+
+// Y(:, j, s) = X(:, j, s) for j < nlock[s]; then normalize every column of Y.
+__global__ void restore_normalize_kernel(double* Y, const double* X, const int* nlock, int64_t r,
+                                         int64_t b) {
+    const int64_t s = blockIdx.y;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t j = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+    if (j >= b) return;
+    double* y = Y + (s * b + j) * r;
+    if (j < nlock[s]) {
+        const double* x = X + (s * b + j) * r;
+        for (int64_t i = lane; i < r; i += 32) y[i] = x[i];
+        return;
+    }
+    double acc = 0.0;
+    for (int64_t i = lane; i < r; i += 32) acc = fma(y[i], y[i], acc);
+    acc = warp_sum(acc);
+    const double inv = acc > 0.0 ? rsqrt(acc) : 0.0;
+    for (int64_t i = lane; i < r; i += 32) y[i] *= inv;
+}
+
+// res(j, s) = || GX(:, j, s) - theta(j, s) X(:, j, s) ||
+__global__ void residual_kernel(const double* GX, const double* X, const double* theta,
+                                double* res, int64_t r, int64_t b) {
+    const int64_t s = blockIdx.y;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t j = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
+    if (j >= b) return;
+    const double* g = GX + (s * b + j) * r;
+    const double* x = X + (s * b + j) * r;
+    const double th = theta[s * b + j];
+    double acc = 0.0;
+    for (int64_t i = lane; i < r; i += 32) {
+        const double d = g[i] - th * x[i];
+        acc = fma(d, d, acc);
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) res[s * b + j] = sqrt(acc);
+}
+
+// One CTA per slice: R = chol(S + shift*I) (upper, S = R^T R), then R^{-1}
+// in place (LAPACK trti2 order, one row per thread), written out as a full
+// b x b column-major block with zeros below the diagonal. b <= 160 (smem).
+__global__ void chol_inv_kernel(const double* __restrict__ S, double* __restrict__ Rinv, int64_t b,
+                                int shift_pass, int* fail) {
+    extern __shared__ __align__(16) double M[];
+    __shared__ double piv;
+    __shared__ int bad;
+    const int64_t s = blockIdx.x;
+    const double* Sin = S + s * b * b;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    for (int64_t i = tid; i < b * b; i += nt) M[i] = Sin[i];
+    if (tid == 0) bad = 0;
+    __syncthreads();
+    if (shift_pass) {  // shifted CholQR (Fukaya et al.): tiny diagonal shift ~ u * trace
+        if (tid == 0) {
+            double t = 0.0;
+            for (int64_t i = 0; i < b; ++i) t += M[i + i * b];
+            piv = t;
+        }
+        __syncthreads();
+        const double sh = 1e-15 * piv;
+        __syncthreads();
+        for (int64_t i = tid; i < b; i += nt) M[i + i * b] += sh;
+        __syncthreads();
+    }
+    for (int64_t k = 0; k < b; ++k) {
+        if (tid == 0) {
+            const double d = M[k + k * b];
+            if (!(d > 0.0)) bad = 1;
+            piv = d > 0.0 ? sqrt(d) : 1.0;
+            M[k + k * b] = piv;
+        }
+        __syncthreads();
+        for (int64_t j = k + 1 + tid; j < b; j += nt) M[k + j * b] /= piv;
+        __syncthreads();
+        const int64_t rem = b - k - 1;
+        for (int64_t t = tid; t < rem * rem; t += nt) {
+            const int64_t i = k + 1 + t % rem, j = k + 1 + t / rem;
+            if (i <= j) M[i + j * b] -= M[k + i * b] * M[k + j * b];
+        }
+        __syncthreads();
+    }
+    for (int64_t j = 0; j < b; ++j) {
+        if (tid == 0) M[j + j * b] = 1.0 / M[j + j * b];
+        __syncthreads();
+        double y = 0.0;
+        if (tid < j)
+            for (int64_t l = tid; l < j; ++l) y = fma(M[tid + l * b], M[l + j * b], y);
+        __syncthreads();
+        if (tid < j) M[tid + j * b] = -y * M[j + j * b];
+        __syncthreads();
+    }
+    double* out = Rinv + s * b * b;
+    for (int64_t t = tid; t < b * b; t += nt) {
+        const int64_t i = t % b, j = t / b;
+        out[t] = (i <= j) ? M[t] : 0.0;
+    }
+    if (tid == 0 && bad && fail) atomicExch(fail, 1);
+}
+
+// tail2[z] = sum of the pairs' first components of CTA partials in group z.
+__global__ void group_sum_kernel(const double* part, int64_t per_group, double* out) {
+    const int64_t z = blockIdx.x;
+    double a = 0.0;
+    for (int64_t i = threadIdx.x; i < per_group; i += blockDim.x) a += part[2 * (z * per_group + i)];
+    __shared__ double red[32];
+    a = warp_sum(a);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        a = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+        a = warp_sum(a);
+        if (threadIdx.x == 0) out[z] = a;
+    }
+}
+
+unsigned grid1(int64_t n) {
+    int64_t g = (n + 255) / 256;
+    return (unsigned)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 16));
+}
+
+// ---------------------------------------------------------------- GEMM glue
+// C_s (rows x cols) = alpha * X_s^T (rows x m)^T ... helpers for the batched
+// r x b panels (column-major, per-slice strides).
+void g_AtB(const double* A, const double* B, double* C, int64_t m, int64_t ra, int64_t rb,
+           int64_t batch, int64_t sA, int64_t sB, cudaStream_t s) {
+    // C (ra x rb) = A^T (ra x m) * B (m x rb); A is m x ra, B is m x rb
+    GemmDesc d;
+    d.M = ra; d.N = rb; d.K = m; d.batch = batch;
+    d.A = A; d.lda = m; d.strideA = sA; d.a_kmajor = true;
+    d.B = B; d.ldb = m; d.strideB = sB;
+    d.C = C; d.ldc = ra; d.strideC = ra * rb;
+    gemm(d, s);
+}
+
+void g_AB(const double* A, const double* B, double* C, int64_t m, int64_t kk, int64_t n,
+          int64_t batch, int64_t sA, int64_t sB, double alpha, const double* Cin, double beta,
+          cudaStream_t s) {
+    // C (m x n) = alpha * A (m x kk) * B (kk x n) + beta * Cin
+    GemmDesc d;
+    d.M = m; d.N = n; d.K = kk; d.batch = batch;
+    d.A = A; d.lda = m; d.strideA = sA;
+    d.B = B; d.ldb = kk; d.strideB = sB;
+    d.C = C; d.ldc = m; d.strideC = m * n;
+    d.alpha = alpha;
+    d.Cin = Cin; d.ldcin = m; d.strideCin = m * n; d.beta = beta;
+    gemm(d, s);
+}
+
+struct Work {
+    int64_t r, b, batch;
+    DeviceBuffer X, Y, Yp, Yn, Z, W, P, S, Rinv, Hv, th, res, coef, wmask, nlock, fail;
+    Work(int64_t r_, int64_t b_, int64_t batch_)
+        : r(r_), b(b_), batch(batch_),
+          X(sizeof(double) * r_ * b_ * batch_), Y(sizeof(double) * r_ * b_ * batch_),
+          Yp(sizeof(double) * r_ * b_ * batch_), Yn(sizeof(double) * r_ * b_ * batch_),
+          Z(sizeof(double) * r_ * b_ * batch_), W(sizeof(double) * r_ * b_ * batch_),
+          P(sizeof(double) * b_ * b_ * batch_), S(sizeof(double) * b_ * b_ * batch_),
+          Rinv(sizeof(double) * b_ * b_ * batch_), Hv(sizeof(double) * b_ * b_ * batch_),
+          th(sizeof(double) * b_ * batch_), res(sizeof(double) * b_ * batch_),
+          coef(sizeof(double) * 3 * batch_), wmask(sizeof(double) * b_ * batch_),
+          nlock(sizeof(int) * batch_), fail(sizeof(int) * 2) {}
+};
+
+// Orthonormalize the columns of Y (r x b per slice) into X via CholQR2.
+void cholqr2(Work& w, double* Yin, double* Xout, cudaStream_t s) {
+    const int64_t r = w.r, b = w.b, batch = w.batch;
+    const size_t smem = (size_t)b * b * sizeof(double);
+    if (smem > 200 * 1024) fail(PPC_ARGUMENT, "subspace: block too wide for the CholQR kernel");
+    if (smem > 48 * 1024)
+        PPC_CUDA_CHECK(cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)smem));
+    double* src = Yin;
+    for (int pass = 0; pass < 2; ++pass) {
+        g_AtB(src, src, w.S.d(), r, b, b, batch, r * b, r * b, s);  // S = Y^T Y
+        chol_inv_kernel<<<(unsigned)batch, 256, smem, s>>>(w.S.d(), w.Rinv.d(), b, pass == 0 ? 1 : 0,
+                                                            w.fail.as<int>());
+        count_launch();
+        check_launch("chol_inv");
+        double* dst = (pass == 0) ? w.Yn.d() : Xout;
+        g_AB(src, w.Rinv.d(), dst, r, b, b, batch, r * b, b * b, 1.0, nullptr, 0.0, s);
+        src = dst;
+    }
+}
+
+// Rayleigh-Ritz on the orthonormal Xn: X = Xn Z, theta, W = G X, res.
+void rayleigh_ritz(Work& w, const double* G, int64_t sG, double* Xn, cudaStream_t s) {
+    const int64_t r = w.r, b = w.b, batch = w.batch;
+    g_AB(G, Xn, w.Z.d(), r, r, b, batch, sG, r * b, 1.0, nullptr, 0.0, s);  // Z = G Xn
+    g_AtB(Xn, w.Z.d(), w.S.d(), r, b, b, batch, r * b, r * b, s);          // H = Xn^T G Xn
+    // eigen-decomposition of H (PSD) by one-sided Jacobi: V = eigvecs, S = eigvals
+    jacobi_svd(w.S.d(), b, b, b * b, batch, b, nullptr, w.th.d(), w.Hv.d(), nullptr, s);
+    g_AB(Xn, w.Hv.d(), w.X.d(), r, b, b, batch, r * b, b * b, 1.0, nullptr, 0.0, s);   // X
+    g_AB(w.Z.d(), w.Hv.d(), w.W.d(), r, b, b, batch, r * b, b * b, 1.0, nullptr, 0.0, s);  // G X
+    dim3 grid((unsigned)((b + 7) / 8), (unsigned)batch);
+    residual_kernel<<<grid, 256, 0, s>>>(w.W.d(), w.X.d(), w.th.d(), w.res.d(), r, b);
+    count_launch();
+    check_launch("residual");
+}
+
+}  // namespace
+
+// tail2[z] = ||A_z - U_z diag(S_z) V_z^T||_F^2 (= the discarded energy sum_{j>=k} s_j^2
+// of slice z by Eckart-Young), via the fused residual GEMM.
+void slice_tail_energy(const double* A, int64_t m, int64_t n, int64_t stride, int64_t batch,
+                       int64_t k, const double* U, const double* S, const double* V, double* tail2,
+                       cudaStream_t s) {
+    DeviceBuffer us(sizeof(double) * m * k * batch);
+    launch_scale_columns(U, S, us.d(), m, k, batch, s);
+    GemmDesc d;
+    d.M = m; d.N = n; d.K = k; d.batch = batch;
+    d.A = us.d(); d.lda = m; d.strideA = m * k;
+    d.B = V; d.ldb = n; d.strideB = n * k; d.b_nmajor = true;
+    const int64_t ctas = gemm_residual_ctas(d);
+    DeviceBuffer part(sizeof(double) * 2 * ctas);
+    gemm_residual(d, A, m, stride, part.d(), s);
+    group_sum_kernel<<<(unsigned)batch, 256, 0, s>>>(part.d(), ctas / batch, tail2);
+    count_launch();
+    check_launch("group_sum");
+}
+
+// Top-k eigenpairs of `batch` symmetric PSD r x r matrices G (stride r*r).
+// Xout (r, k, batch), lambda (k, batch). Deterministic.
+void subspace_eig_top(const double* G, int64_t r, int64_t batch, int64_t k, double* Xout,
+                      double* lambda, cudaStream_t s) {
+    int64_t b = k + std::max<int64_t>(k, 16);
+    b = (b + 7) / 8 * 8;
+    if (b >= r || r <= 8) {
+        // the block would cover the space: full Jacobi eigendecomposition
+        jacobi_svd(G, r, r, r * r, batch, k, nullptr, lambda, Xout, nullptr, s);
+        return;
+    }
+    b = std::min<int64_t>(b, 160);
+    if (k > b) fail(PPC_ARGUMENT, "subspace_eig_top: k too large for the block");
+    Work w(r, b, batch);
+    const int64_t per = r * b;
+    PPC_CUDA_CHECK(cudaMemsetAsync(w.fail.d(), 0, 2 * sizeof(int), s));
+    randn_kernel<<<grid1(per * batch), 256, 0, s>>>(w.Y.d(), per * batch, 0x5eed5eedULL + (uint64_t)r * 131 + b);
+    count_launch();
+    cholqr2(w, w.Y.d(), w.Yp.d(), s);
+    rayleigh_ritz(w, G, r * r, w.Yp.d(), s);
+
+    std::vector<double> th(b * batch), res(b * batch), coef(3 * batch), wm(b * batch);
+    std::vector<int> nlock(batch, 0);
+    const double tol = 1e-13;
+    const int max_iter = 80;
+    for (int it = 0; it < max_iter; ++it) {
+        PPC_CUDA_CHECK(cudaMemcpyAsync(th.data(), w.th.d(), sizeof(double) * b * batch, cudaMemcpyDeviceToHost, s));
+        PPC_CUDA_CHECK(cudaMemcpyAsync(res.data(), w.res.d(), sizeof(double) * b * batch, cudaMemcpyDeviceToHost, s));
+        PPC_CUDA_CHECK(cudaStreamSynchronize(s));
+        bool all_done = true;
+        int dmax = 0;
+        double gscale = 0.0;
+        for (int64_t sl = 0; sl < batch; ++sl) gscale = std::max(gscale, th[sl * b]);
+        std::vector<int> deg(batch, 0);
+        std::vector<double> cc(batch), ee(batch);
+        for (int64_t sl = 0; sl < batch; ++sl) {
+            const double* t = &th[sl * b];
+            const double* rr = &res[sl * b];
+            const double scale = std::max(t[0], 1e-300);
+            // lock a converged prefix: residual small against the largest
+            // eigenvalue of the whole batch (the tensor's scale) or, for
+            // sigma parity, 1e-10 of this slice's own top eigenvalue
+            const double thr = std::max(tol * gscale, 1e-10 * scale);
+            int L = 0;
+            while (L < k && rr[L] <= thr) ++L;  // locked prefix
+            nlock[sl] = L;
+            for (int64_t j = 0; j < b; ++j) wm[sl * b + j] = (j < L) ? t[j] : 0.0;
+            if (L >= k || t[0] <= 0.0) {
+                deg[sl] = 0;
+                continue;
+            }
+            all_done = false;
+            // Chebyshev interval [0, ub]: damp everything below the smallest Ritz value
+            const double ub = std::max(t[b - 1], 0.0);
+            const double c = 0.5 * ub, e = std::max(0.5 * ub, 1e-300 * scale);
+            cc[sl] = c;
+            ee[sl] = e;
+            const double xt = std::max(1.0, (t[L] - c) / e), xk = std::max(1.0, (t[k - 1] - c) / e);
+            const double spread = std::acosh(xt) - std::acosh(xk);
+            int d = 10;
+            if (spread > 0) d = (int)std::min<double>(10.0, std::max(1.0, std::log(1e6) / spread));
+            if (xk <= 1.0 + 1e-12) d = std::min(d, 2);  // no separation yet: gentle
+            deg[sl] = d;
+            dmax = std::max(dmax, d);
+        }
+        if (all_done) break;
+        PPC_CUDA_CHECK(cudaMemcpyAsync(w.wmask.d(), wm.data(), sizeof(double) * b * batch, cudaMemcpyHostToDevice, s));
+        PPC_CUDA_CHECK(cudaMemcpyAsync(w.nlock.d(), nlock.data(), sizeof(int) * batch, cudaMemcpyHostToDevice, s));
+        // filter: Y_0 = X; Y_{j+1} from the deflated operator G - X_L Theta_L X_L^T
+        PPC_CUDA_CHECK(cudaMemcpyAsync(w.Y.d(), w.X.d(), sizeof(double) * per * batch, cudaMemcpyDeviceToDevice, s));
+        double* Y = w.Y.d();
+        double* Yp = w.Yp.d();
+        double* Yn = w.Yn.d();
+        for (int j = 0; j < dmax; ++j) {
+            g_AB(G, Y, w.Z.d(), r, r, b, batch, r * r, per, 1.0, nullptr, 0.0, s);  // Z = G Y
+            g_AtB(w.X.d(), Y, w.P.d(), r, b, b, batch, per, per, s);              // P = X^T Y
+            scale_rows_kernel<<<grid1(b * b * batch), 256, 0, s>>>(w.P.d(), w.wmask.d(), b, b * b * batch);
+            count_launch();
+            g_AB(w.X.d(), w.P.d(), w.Z.d(), r, b, b, batch, per, b * b, -1.0, w.Z.d(), 1.0, s);  // Z -= X P
+            for (int64_t sl = 0; sl < batch; ++sl) {
+                double* cf = &coef[3 * sl];
+                if (j >= deg[sl]) {
+                    cf[0] = 0.0; cf[1] = 1.0; cf[2] = 0.0;  // frozen: Y_{j+1} = Y_j
+                } else if (j == 0) {
+                    cf[0] = 1.0 / ee[sl]; cf[1] = -cc[sl] / ee[sl]; cf[2] = 0.0;
+                } else {
+                    cf[0] = 2.0 / ee[sl]; cf[1] = -2.0 * cc[sl] / ee[sl]; cf[2] = -1.0;
+                }
+            }
+            PPC_CUDA_CHECK(cudaMemcpyAsync(w.coef.d(), coef.data(), sizeof(double) * 3 * batch, cudaMemcpyHostToDevice, s));
+            cheb_kernel<<<grid1(per * batch), 256, 0, s>>>(Yn, w.Z.d(), Y, Yp, w.coef.d(), per, per * batch);
+            count_launch();
+            check_launch("cheb");
+            // rotate buffers: (Yp, Y, Yn) <- (Y, Yn, Yp)
+            double* t = Yp;
+            Yp = Y;
+            Y = Yn;
+            Yn = t;
+            // keep the host coefficient buffer alive until the copy ran
+            PPC_CUDA_CHECK(cudaStreamSynchronize(s));
+        }
+        // locked columns back, normalize, CholQR2, Rayleigh-Ritz
+        dim3 grid((unsigned)((b + 7) / 8), (unsigned)batch);
+        restore_normalize_kernel<<<grid, 256, 0, s>>>(Y, w.X.d(), w.nlock.as<int>(), r, b);
+        count_launch();
+        check_launch("restore_normalize");
+        // CholQR2 writes through w.Yn; make sure Y is not aliased with it
+        if (Y == w.Yn.d()) {
+            PPC_CUDA_CHECK(cudaMemcpyAsync(w.Yp.d(), Y, sizeof(double) * per * batch, cudaMemcpyDeviceToDevice, s));
+            Y = w.Yp.d();
+        }
+        double* Xn = (Y == w.Y.d()) ? w.Yp.d() : w.Y.d();
+        cholqr2(w, Y, Xn, s);
+        rayleigh_ritz(w, G, r * r, Xn, s);
+    }
+    // outputs: leading k Ritz pairs
+    PPC_CUDA_CHECK(cudaMemcpy2DAsync(Xout, sizeof(double) * r * k, w.X.d(), sizeof(double) * per,
+                                     sizeof(double) * r * k, batch, cudaMemcpyDeviceToDevice, s));
+    PPC_CUDA_CHECK(cudaMemcpy2DAsync(lambda, sizeof(double) * k, w.th.d(), sizeof(double) * b,
+                                     sizeof(double) * k, batch, cudaMemcpyDeviceToDevice, s));
+}
+
+void subspace_svd(const double* A, int64_t m, int64_t n, int64_t stride, int64_t batch, int64_t k,
+                  double* U, double* S, double* V, double* tail2, cudaStream_t s) {
+    const bool tall = m >= n;
+    const int64_t r = tall ? n : m;  // Gram dimension
+    DeviceBuffer G(sizeof(double) * r * r * batch);
+    {
+        GemmDesc d;
+        d.M = r; d.N = r; d.batch = batch; d.symmetric = true;
+        d.C = G.d(); d.ldc = r; d.strideC = r * r;
+        d.A = A; d.B = A; d.strideA = stride; d.strideB = stride;
+        if (tall) {  // G = A^T A: A(mm,kk) = A[kk + mm*m], B(kk,nn) = A[kk + nn*m]
+            d.K = m; d.lda = m; d.a_kmajor = true; d.ldb = m; d.b_nmajor = false;
+        } else {     // G = A A^T: A(mm,kk) = A[mm + kk*m], B(kk,nn) = A[nn + kk*m]
+            d.K = n; d.lda = m; d.a_kmajor = false; d.ldb = m; d.b_nmajor = true;
+        }
+        gemm(d, s);
+    }
+    DeviceBuffer Xk(sizeof(double) * r * k * batch), lam(sizeof(double) * k * batch);
+    subspace_eig_top(G.d(), r, batch, k, Xk.d(), lam.d(), s);
+    // polish: W = A Xk (tall: m x k) or A^T Xk (wide: n x k)
+    const int64_t o = tall ? m : n;
+    DeviceBuffer Wb(sizeof(double) * o * k * batch), Us(sizeof(double) * o * k * batch),
+        Vs(sizeof(double) * k * k * batch);
+    {
+        GemmDesc d;
+        d.M = o; d.N = k; d.K = r; d.batch = batch;
+        d.A = A; d.strideA = stride;
+        d.lda = m;
+        d.a_kmajor = !tall;  // wide: A^T (n x m): A(mm,kk) = A[kk + mm*m]
+        d.B = Xk.d(); d.ldb = r; d.strideB = r * k;
+        d.C = Wb.d(); d.ldc = o; d.strideC = o * k;
+        gemm(d, s);
+    }
+    // W = P diag(sigma) R^T (one-sided Jacobi; R k x k)
+    jacobi_svd(Wb.d(), o, k, o * k, batch, k, Us.d(), S, Vs.d(), nullptr, s);
+    if (tall) {
+        // A ~ U sigma (Xk R)^T: U = P, V = Xk R
+        PPC_CUDA_CHECK(cudaMemcpyAsync(U, Us.d(), sizeof(double) * m * k * batch, cudaMemcpyDeviceToDevice, s));
+        g_AB(Xk.d(), Vs.d(), V, n, k, k, batch, n * k, k * k, 1.0, nullptr, 0.0, s);
+    } else {
+        // A^T ~ P sigma (Xk R)^T  =>  A ~ (Xk R) sigma P^T: U = Xk R, V = P
+        g_AB(Xk.d(), Vs.d(), U, m, k, k, batch, m * k, k * k, 1.0, nullptr, 0.0, s);
+        PPC_CUDA_CHECK(cudaMemcpyAsync(V, Us.d(), sizeof(double) * n * k * batch, cudaMemcpyDeviceToDevice, s));
+        sign_rule(U, m, k, batch, V, n, s);
+    }
+    if (tail2) slice_tail_energy(A, m, n, stride, batch, k, U, S, V, tail2, s);
+}
+
 }  // namespace ppc

@@ -343,3 +343,65 @@ def test_device_arrays_zero_copy(engine, oracle):
     c = engine.star_q(da, engine.to_device(np.asfortranarray(a.transpose(1, 0, 2))), t)
     want = oracle.star_q_product(a, np.asfortranarray(a.transpose(1, 0, 2)), q)
     assert rel(engine.to_host(c), want) <= 1e-12
+
+
+# ------------------------------------------- large slices (Gram + subspace)
+def _numpy_rank_k(a, k):
+    u, s, vt = np.linalg.svd(a, full_matrices=False)
+    return s, (u[:, :k] * s[:k]) @ vt[:k]
+
+
+@pytest.mark.parametrize("m,n,k,kind", [(300, 260, 10, "noise"), (256, 256, 16, "spiked"),
+                                        (200, 420, 12, "noise"), (512, 384, 32, "lowrank")])
+def test_large_slice_svd_vs_lapack(engine, m, n, k, kind):
+    rng = np.random.default_rng(m + n + k)
+    batch = 3
+    a = rng.standard_normal((m, n, batch))
+    if kind == "spiked":
+        a += 3.0
+    if kind == "lowrank":
+        a = np.einsum("ir,jr,b->ijb", rng.standard_normal((m, 40)), rng.standard_normal((n, 40)),
+                      np.ones(batch)) + 1e-3 * a
+    a = np.asfortranarray(a)
+    U, s, V = engine.truncated_svd(a, k)
+    for z in range(batch):
+        sn, ak = _numpy_rank_k(a[:, :, z], k)
+        np.testing.assert_allclose(s[:, z], sn[:k], rtol=1e-10)
+        rec = (U[:, :, z] * s[:, z]) @ V[:, :, z].T
+        assert np.linalg.norm(rec - ak) <= 1e-10 * np.linalg.norm(a[:, :, z])
+        assert np.linalg.norm(U[:, :, z].T @ U[:, :, z] - np.eye(k)) <= 1e-10 * k
+        assert np.linalg.norm(V[:, :, z].T @ V[:, :, z] - np.eye(k)) <= 1e-10 * k
+        for j in range(k):
+            i = int(np.argmax(np.abs(U[:, j, z])))
+            assert U[i, j, z] >= 0
+
+
+@pytest.mark.parametrize("k", [1, 10, 20])
+def test_tsvdq_video_large_slices_vs_oracle(engine, oracle, k):
+    # full cfg2 frame size 240x320 (Gram + subspace path), 40 frames
+    a = synth.video(240, 320, 40, seed=4)
+    q, _, _ = oracle.data_dependent_q(a, 12)
+    _slice_parity(engine, oracle, a, q, k)
+
+
+def test_tsvdq_error_large_slices(engine, oracle):
+    a = synth.video(240, 320, 24, seed=5)
+    t = engine.Transform("dct", 24, 6)
+    f = engine.tsvdq(a, t, 8)
+    tot, ey, pr = engine.tsvdq_error(a, f)
+    U, S, V = oracle.tsvdq(a, t.q, 8)
+    to, eo, po = oracle.tsvdq_error(a, U, S, V, t.q)
+    nrm = np.linalg.norm(a)
+    assert abs(tot - to) <= 1e-10 * nrm and abs(ey - eo) <= 1e-10 * nrm and abs(pr - po) <= 1e-10 * nrm
+
+
+def test_data_q_large_n3_vs_oracle(engine, oracle):
+    # n3 = 200 > Jacobi limit: Gram + subspace eigensolver for Q (cfg2 p=20)
+    a = synth.video(60, 80, 200, seed=6)
+    t = engine.data_dependent_transform(a, 20)
+    qo, so, _ = oracle.data_dependent_q(a, 20)
+    unf = a.reshape(-1, 200, order="F")
+    lam = np.sum((unf @ t.q) ** 2, axis=0)
+    assert np.max(np.abs(lam - so ** 2)) <= 1e-12 * so[0] ** 2
+    assert abs(lam.sum() - (so ** 2).sum()) <= 1e-12 * (so ** 2).sum()
+    assert np.abs(t.q.T @ t.q - np.eye(20)).max() <= 1e-12
