@@ -97,7 +97,7 @@ void sym_eig_top(const double* G, int64_t n, int64_t p, double* Q, double* lambd
         jacobi_svd(G, n, n, n * n, 1, p, nullptr, lambda, Q, nullptr, s);
         return;
     }
-    subspace_eig_top(G, n, 1, p, Q, lambda, s);
+    subspace_eig_top(G, n, 1, p, Q, lambda, s, false);
 }
 
 bool data_q(const double* T, int64_t N, int64_t n3, int64_t p, double* Q, double* sigma,

@@ -22,7 +22,7 @@ void gram_partials(const double* T, int64_t ldT, int64_t rows, int64_t n3, int64
 void tree_reduce(double* parts, int64_t nparts, int64_t elems, cudaStream_t s);
 
 void subspace_eig_top(const double* G, int64_t n, int64_t batch, int64_t p, double* Q,
-                      double* lambda, cudaStream_t s);
+                      double* lambda, cudaStream_t s, bool vectors_for_reconstruction);
 void slice_tail_energy(const double* A, int64_t m, int64_t n, int64_t stride, int64_t batch,
                        int64_t k, const double* U, const double* S, const double* V, double* tail2,
                        cudaStream_t s);

@@ -19,6 +19,8 @@
 // b Ritz values and residual norms per slice per iteration.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <vector>
 
 #include "dmma_gemm.cuh"
@@ -242,8 +244,11 @@ struct Work {
           nlock(sizeof(int) * batch_), fail(sizeof(int) * 2) {}
 };
 
-// Orthonormalize the columns of Y (r x b per slice) into X via CholQR2.
-void cholqr2(Work& w, double* Yin, double* Xout, cudaStream_t s) {
+// Orthonormalize the columns of Y (r x b per slice) into X via shifted
+// CholQR3 (Fukaya, Kannan, Nakatsukasa, Yamamoto, Yanagisawa 2020): a shifted
+// first pass makes the Cholesky factorization succeed for cond(Y) up to ~1e15,
+// two plain passes restore orthogonality to machine precision.
+void cholqr3(Work& w, double* Yin, double* Xout, cudaStream_t s) {
     const int64_t r = w.r, b = w.b, batch = w.batch;
     const size_t smem = (size_t)b * b * sizeof(double);
     if (smem > 200 * 1024) fail(PPC_ARGUMENT, "subspace: block too wide for the CholQR kernel");
@@ -251,13 +256,14 @@ void cholqr2(Work& w, double* Yin, double* Xout, cudaStream_t s) {
         PPC_CUDA_CHECK(cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             (int)smem));
     double* src = Yin;
-    for (int pass = 0; pass < 2; ++pass) {
+    DeviceBuffer tmp(sizeof(double) * r * b * batch);
+    for (int pass = 0; pass < 3; ++pass) {
         g_AtB(src, src, w.S.d(), r, b, b, batch, r * b, r * b, s);  // S = Y^T Y
         chol_inv_kernel<<<(unsigned)batch, 256, smem, s>>>(w.S.d(), w.Rinv.d(), b, pass == 0 ? 1 : 0,
                                                             w.fail.as<int>());
         count_launch();
         check_launch("chol_inv");
-        double* dst = (pass == 0) ? w.Yn.d() : Xout;
+        double* dst = (pass == 2) ? Xout : (pass == 0 ? w.Yn.d() : tmp.d());
         g_AB(src, w.Rinv.d(), dst, r, b, b, batch, r * b, b * b, 1.0, nullptr, 0.0, s);
         src = dst;
     }
@@ -302,7 +308,8 @@ void slice_tail_energy(const double* A, int64_t m, int64_t n, int64_t stride, in
 // Top-k eigenpairs of `batch` symmetric PSD r x r matrices G (stride r*r).
 // Xout (r, k, batch), lambda (k, batch). Deterministic.
 void subspace_eig_top(const double* G, int64_t r, int64_t batch, int64_t k, double* Xout,
-                      double* lambda, cudaStream_t s) {
+                      double* lambda, cudaStream_t s, bool vectors_for_reconstruction) {
+    static const bool dbg = std::getenv("PPC_SUBSPACE_DEBUG") != nullptr;
     int64_t b = k + std::max<int64_t>(k, 16);
     b = (b + 7) / 8 * 8;
     if (b >= r || r <= 8) {
@@ -317,31 +324,43 @@ void subspace_eig_top(const double* G, int64_t r, int64_t batch, int64_t k, doub
     PPC_CUDA_CHECK(cudaMemsetAsync(w.fail.d(), 0, 2 * sizeof(int), s));
     randn_kernel<<<grid1(per * batch), 256, 0, s>>>(w.Y.d(), per * batch, 0x5eed5eedULL + (uint64_t)r * 131 + b);
     count_launch();
-    cholqr2(w, w.Y.d(), w.Yp.d(), s);
+    cholqr3(w, w.Y.d(), w.Yp.d(), s);
     rayleigh_ritz(w, G, r * r, w.Yp.d(), s);
 
     std::vector<double> th(b * batch), res(b * batch), coef(3 * batch), wm(b * batch);
     std::vector<int> nlock(batch, 0);
-    const double tol = 1e-13;
-    const int max_iter = 80;
+    const int max_iter = 100;
     for (int it = 0; it < max_iter; ++it) {
         PPC_CUDA_CHECK(cudaMemcpyAsync(th.data(), w.th.d(), sizeof(double) * b * batch, cudaMemcpyDeviceToHost, s));
         PPC_CUDA_CHECK(cudaMemcpyAsync(res.data(), w.res.d(), sizeof(double) * b * batch, cudaMemcpyDeviceToHost, s));
         PPC_CUDA_CHECK(cudaStreamSynchronize(s));
         bool all_done = true;
         int dmax = 0;
-        double gscale = 0.0;
-        for (int64_t sl = 0; sl < batch; ++sl) gscale = std::max(gscale, th[sl * b]);
+        // ||A||^2 ~ sum of the slices' captured energies (top-b Ritz values)
+        double energy = 0.0;
+        for (int64_t i = 0; i < b * batch; ++i) energy += std::max(th[i], 0.0);
         std::vector<int> deg(batch, 0);
         std::vector<double> cc(batch), ee(batch);
         for (int64_t sl = 0; sl < batch; ++sl) {
             const double* t = &th[sl * b];
             const double* rr = &res[sl * b];
             const double scale = std::max(t[0], 1e-300);
-            // lock a converged prefix: residual small against the largest
-            // eigenvalue of the whole batch (the tensor's scale) or, for
-            // sigma parity, 1e-10 of this slice's own top eigenvalue
-            const double thr = std::max(tol * gscale, 1e-10 * scale);
+            // Lock a converged prefix. Singular values after the Rayleigh-Ritz
+            // polish carry relative error ~ (res/gap)^2, so res <= 1e-9 theta_1
+            // suffices for them. Slice-SVD vectors must also reproduce the
+            // rank-k truncation to 1e-11 ||A||: the subspace angle is
+            // res / (theta_k - theta_{k+1}), which moves A_k by about
+            // angle * (sigma_k + sigma_{k+1}). The eigenbasis Q only needs
+            // eigenvalue accuracy (res <= 1e-13 theta_1).
+            double thr;
+            if (vectors_for_reconstruction) {
+                const double gap = std::max(t[k - 1] - t[k], 0.0);
+                const double srec = 1e-11 * std::sqrt(energy) * gap /
+                                    (std::sqrt(std::max(t[k - 1], 0.0)) + std::sqrt(std::max(t[k], 0.0)) + 1e-300);
+                thr = std::max(32.0 * 2.22e-16 * scale, std::min(srec, 1e-9 * scale));
+            } else {
+                thr = 1e-13 * scale;
+            }
             int L = 0;
             while (L < k && rr[L] <= thr) ++L;  // locked prefix
             nlock[sl] = L;
@@ -357,13 +376,23 @@ void subspace_eig_top(const double* G, int64_t r, int64_t batch, int64_t k, doub
             cc[sl] = c;
             ee[sl] = e;
             const double xt = std::max(1.0, (t[L] - c) / e), xk = std::max(1.0, (t[k - 1] - c) / e);
+            // (a) the block must stay numerically full rank for shifted
+            // CholQR3: amplification of the largest active Ritz value over the
+            // block's bottom (x = 1, T_d(1) = 1) kept <= 1e10;
+            // (b) the spread inside the wanted active set (precision of the
+            // smaller wanted components) kept <= 1e6.
+            double d = 10.0;
+            if (xt > 1.0) d = std::min(d, std::acosh(1e10) / std::acosh(xt));
             const double spread = std::acosh(xt) - std::acosh(xk);
-            int d = 10;
-            if (spread > 0) d = (int)std::min<double>(10.0, std::max(1.0, std::log(1e6) / spread));
-            if (xk <= 1.0 + 1e-12) d = std::min(d, 2);  // no separation yet: gentle
-            deg[sl] = d;
-            dmax = std::max(dmax, d);
+            if (spread > 0) d = std::min(d, std::log(1e6) / spread);
+            if (xk <= 1.0 + 1e-12) d = std::min(d, 2.0);  // no separation yet: gentle
+            deg[sl] = std::max(1, (int)d);
+            dmax = std::max(dmax, deg[sl]);
+            if (dbg && (sl < 4 || it % 10 == 0))
+                fprintf(stderr, "[subspace] it %d slice %lld L=%d deg=%d t0=%.6e tk=%.6e tb=%.6e res0=%.3e resk=%.3e thr=%.3e\n",
+                        it, (long long)sl, L, deg[sl], t[0], t[k - 1], t[b - 1], rr[0], rr[k - 1], thr);
         }
+        if (dbg) fprintf(stderr, "[subspace] it %d dmax %d\n", it, dmax);
         if (all_done) break;
         PPC_CUDA_CHECK(cudaMemcpyAsync(w.wmask.d(), wm.data(), sizeof(double) * b * batch, cudaMemcpyHostToDevice, s));
         PPC_CUDA_CHECK(cudaMemcpyAsync(w.nlock.d(), nlock.data(), sizeof(int) * batch, cudaMemcpyHostToDevice, s));
@@ -405,13 +434,13 @@ void subspace_eig_top(const double* G, int64_t r, int64_t batch, int64_t k, doub
         restore_normalize_kernel<<<grid, 256, 0, s>>>(Y, w.X.d(), w.nlock.as<int>(), r, b);
         count_launch();
         check_launch("restore_normalize");
-        // CholQR2 writes through w.Yn; make sure Y is not aliased with it
+        // CholQR3 writes through w.Yn; make sure Y is not aliased with it
         if (Y == w.Yn.d()) {
             PPC_CUDA_CHECK(cudaMemcpyAsync(w.Yp.d(), Y, sizeof(double) * per * batch, cudaMemcpyDeviceToDevice, s));
             Y = w.Yp.d();
         }
         double* Xn = (Y == w.Y.d()) ? w.Yp.d() : w.Y.d();
-        cholqr2(w, Y, Xn, s);
+        cholqr3(w, Y, Xn, s);
         rayleigh_ritz(w, G, r * r, Xn, s);
     }
     // outputs: leading k Ritz pairs
@@ -439,7 +468,7 @@ void subspace_svd(const double* A, int64_t m, int64_t n, int64_t stride, int64_t
         gemm(d, s);
     }
     DeviceBuffer Xk(sizeof(double) * r * k * batch), lam(sizeof(double) * k * batch);
-    subspace_eig_top(G.d(), r, batch, k, Xk.d(), lam.d(), s);
+    subspace_eig_top(G.d(), r, batch, k, Xk.d(), lam.d(), s, true);
     // polish: W = A Xk (tall: m x k) or A^T Xk (wide: n x k)
     const int64_t o = tall ? m : n;
     DeviceBuffer Wb(sizeof(double) * o * k * batch), Us(sizeof(double) * o * k * batch),

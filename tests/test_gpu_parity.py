@@ -405,3 +405,19 @@ def test_data_q_large_n3_vs_oracle(engine, oracle):
     assert np.max(np.abs(lam - so ** 2)) <= 1e-12 * so[0] ** 2
     assert abs(lam.sum() - (so ** 2).sum()) <= 1e-12 * (so ** 2).sum()
     assert np.abs(t.q.T @ t.q - np.eye(20)).max() <= 1e-12
+
+
+def test_cp_scaled_pipeline(engine, oracle):
+    # cfg5 distribution (rank-50 CP + 1e-3 noise) at 192x176x96, p=64 > rank:
+    # noise columns in Q and noise slices (SURVEY finding 8) -> shared-Q parity
+    a = synth.cp_tensor(192, 176, 96, rank=50, noise=1e-3, seed=7)
+    t = engine.data_dependent_transform(a, 64)
+    qo, so, _ = oracle.data_dependent_q(a, 64)
+    unf = a.reshape(-1, 96, order="F")
+    lam = np.sum((unf @ t.q) ** 2, axis=0)
+    assert np.max(np.abs(lam - so ** 2)) <= 1e-12 * so[0] ** 2
+    _slice_parity(engine, oracle, a, qo, 16)
+    f = engine.tsvdq(a, t, 16)
+    U, S, V = oracle.tsvdq(a, qo, 16)
+    reo = oracle.relative_error(a, oracle.tsvdq_reconstruct(U, S, V, qo))
+    assert abs(engine.tsvdq_relative_error(a, f) - reo) <= 1e-10 * reo
