@@ -245,20 +245,14 @@ class Tsvdq:
         desc = {"cfg5": "cfg5 rank-50 CP + N(0,1e-3^2) noise", "cfg3": "cfg3 hyperspectral",
                 "cfg2": "cfg2 video"}[self.name]
         return {"workload": desc + " tSVDQ with data-driven Q", "shape": [n1, n2, n3], "p": p,
-                "k": k, "step": "data_dependent_transform + tsvdq + relative_error(A, recon)",
+                "k": k, "step": "ppc_tsvdq_compress = data_dependent_transform + tsvdq + relative_error(A, recon) (tools/main.cpp:186-283)",
                 "l2": "input > L2" if self.in_bytes > 126e6 else "input < L2 (resident)"}
 
     def step(self, L):
         n1, n2, n3, p, k = self.dims
-        comp = C.c_int(0)
-        for rc in (L.ppc_data_dependent_q(ptr(self.A), n1, n2, n3, p, ptr(self.Q), None, C.byref(comp), 1),
-                   L.ppc_tsvdq(ptr(self.A), n1, n2, n3, ptr(self.Q), p, k, ptr(self.U), ptr(self.S),
-                               ptr(self.V), 1)):
-            if rc:
-                raise RuntimeError(L.ppc_last_error().decode())
         re = C.c_double()
-        rc = L.ppc_tsvdq_relative_error(ptr(self.A), n1, n2, n3, ptr(self.U), ptr(self.S), ptr(self.V),
-                                        ptr(self.Q), p, k, C.byref(re), 1)
+        rc = L.ppc_tsvdq_compress(ptr(self.A), n1, n2, n3, p, k, ptr(self.Q), None, ptr(self.U),
+                                  ptr(self.S), ptr(self.V), C.byref(re), 1)
         if rc:
             raise RuntimeError(L.ppc_last_error().decode())
         self.re = re.value
@@ -278,23 +272,18 @@ class Tsvdq:
         self.hU = torch.empty(n1 * k * p, dtype=torch.float64).pin_memory()
         self.hS = torch.empty(k * p, dtype=torch.float64).pin_memory()
         self.hV = torch.empty(n2 * k * p, dtype=torch.float64).pin_memory()
-        # inputs once per step; results (Q + factors) back once; the RE call
-        # re-stages A (it is a separate public call taking host buffers).
-        self.h2d = 8 * (2 * n1 * n2 * n3 + (n1 + n2 + 1) * k * p + n3 * p)
+        # one public call per step (ppc_tsvdq_compress, the CLI compress chain):
+        # H2D of A, D2H of Q + factors + the relative error
+        self.h2d = 8 * n1 * n2 * n3
         self.d2h = 8 * (n3 * p + (n1 + n2 + 1) * k * p) + 8
 
     def e2e_step(self, L):
         n1, n2, n3, p, k = self.dims
-        comp = C.c_int(0)
         re = C.c_double()
-        for rc in (
-            L.ppc_data_dependent_q(ptr(self.hA), n1, n2, n3, p, ptr(self.hQ), None, C.byref(comp), 0),
-            L.ppc_tsvdq(ptr(self.hA), n1, n2, n3, ptr(self.hQ), p, k, ptr(self.hU), ptr(self.hS),
-                        ptr(self.hV), 0),
-            L.ppc_tsvdq_relative_error(ptr(self.hA), n1, n2, n3, ptr(self.hU), ptr(self.hS),
-                                       ptr(self.hV), ptr(self.hQ), p, k, C.byref(re), 0)):
-            if rc:
-                raise RuntimeError(L.ppc_last_error().decode())
+        rc = L.ppc_tsvdq_compress(ptr(self.hA), n1, n2, n3, p, k, ptr(self.hQ), None, ptr(self.hU),
+                                  ptr(self.hS), ptr(self.hV), C.byref(re), 0)
+        if rc:
+            raise RuntimeError(L.ppc_last_error().decode())
 
     def cpu_sample(self, ppo, threads):
         """Bounded sample of the same pipeline on the oracle (reference algorithm
@@ -303,7 +292,9 @@ class Tsvdq:
         from paper_2409_19402_b200 import synth
         n1, n2, n3, p, k = self.dims
         if self.name == "cfg5":
-            s1, s2 = 256, 256
+            # n3 = 1024 makes the oracle's Jacobi SVD of the n3 x n3 factor
+            # O(n3^3 sweeps) ~ minutes; the sample cuts every extent by 8
+            s1, s2, n3, p, k = 256, 256, 128, 16, 4
             a = synth.cp_tensor(s1, s2, n3, rank=50, noise=1e-3, seed=1)
         elif self.name == "cfg3":
             s1, s2 = 128, 128
@@ -380,7 +371,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default=os.environ.get("PPC_BENCH_WORKLOAD", "cfg4"),
+    ap.add_argument("--workload", default=os.environ.get("PPC_BENCH_WORKLOAD", "cfg5"),
                     choices=["cfg5", "cfg4", "cfg3", "cfg2"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -154,6 +154,15 @@ int ppc_tsvdq_relative_error(const double* A, int64_t n1, int64_t n2, int64_t n3
                              const double* Q, int64_t p, int64_t k,
                              double* re, int loc);
 
+/* The `projprod compress --method tsvdq --transform data` pipeline
+ * (tools/main.cpp:186-283: data_dependent_transform -> tsvdq ->
+ * tsvdq_reconstruct -> relative_error) as one call: A is staged once, the
+ * reconstruction is never materialized. Q (n3,p), sigma (p, nullable),
+ * U (n1,k,p), S (k,p), V (n2,k,p); *re = ||A - recon|| / ||A||. */
+int ppc_tsvdq_compress(const double* A, int64_t n1, int64_t n2, int64_t n3, int64_t p,
+                       int64_t k, double* Q, double* sigma, double* U, double* S, double* V,
+                       double* re, int loc);
+
 #ifdef __cplusplus
 }
 #endif

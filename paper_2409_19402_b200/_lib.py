@@ -66,6 +66,7 @@ def lib() -> C.CDLL:
         "ppc_tsvdq_error": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, vp, i64, i64, pd, pd, pd, C.c_int]),
         "ppc_relative_error": (C.c_int, [vp, vp, i64, pd, C.c_int]),
         "ppc_tsvdq_relative_error": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, vp, i64, i64, pd, C.c_int]),
+        "ppc_tsvdq_compress": (C.c_int, [vp, i64, i64, i64, i64, i64, vp, vp, vp, vp, vp, pd, C.c_int]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)

@@ -247,4 +247,33 @@ int ppc_tsvdq_relative_error(const double* A, int64_t n1, int64_t n2, int64_t n3
     });
 }
 
+int ppc_tsvdq_compress(const double* A, int64_t n1, int64_t n2, int64_t n3, int64_t p, int64_t k,
+                       double* Q, double* sigma, double* U, double* S, double* V, double* re,
+                       int loc) {
+    return guarded([&] {
+        validate_loc(loc);
+        check_transform(n3, p);
+        check_tensor(n1, n2, n3);
+        check_spatial_rank(n1, n2, k, "tsvdq");
+        if (!re) fail(PPC_ARGUMENT, "null output");
+        cudaStream_t s = stream();
+        const int64_t N = n1 * n2;
+        In a(A, N * n3, loc);
+        require_finite(a.d, N * n3, "svd", s);
+        Out q(Q, n3 * p, loc), sg(sigma, sigma ? p : 0, loc), u(U, n1 * k * p, loc),
+            sv(S, k * p, loc), v(V, n2 * k * p, loc);
+        data_q(a.d, N, n3, p, q.d, sigma ? sg.d : nullptr, s);
+        tsvdq(a.d, n1, n2, n3, q.d, p, k, u.d, sv.d, v.d, s);
+        const auto r = recon_residual(a.d, n1, n2, n3, u.d, sv.d, v.d, q.d, p, k, s);
+        if (r[1] == 0.0) fail(PPC_DEGENERATE, "relative_error: reference tensor is zero");
+        *re = std::sqrt(r[0]) / std::sqrt(r[1]);
+        q.finish();
+        if (sigma) sg.finish();
+        u.finish();
+        sv.finish();
+        v.finish();
+        if (loc == PPC_HOST) PPC_CUDA_CHECK(cudaStreamSynchronize(s));
+    });
+}
+
 }  // extern "C"

@@ -40,6 +40,12 @@ struct GemmParams {
     double* partial;      // RESID: 2 doubles per CTA, CTA linear id order
     int tri;              // 1: only tiles with n_tile >= m_tile (SYRK), mirror on store
     int nfast;            // raster: 1 = n tile fastest
+    // k-blocked operands (kshift > 0): a K-major operand stored as consecutive
+    // blocks of 2^kshift rows, element (k, o) at (k >> kshift) * kbstride +
+    // o * ld + (k & mask). Keeps each pipeline stage inside one block (TLB).
+    int kshift;
+    int64_t kbstride;
+    const int* zmap;      // nullable: batch index indirection (blockIdx.z -> batch)
 };
 
 __device__ __forceinline__ void dmma884(double (&d)[2], double a, double b) {
@@ -71,7 +77,8 @@ __device__ __forceinline__ void cp_async_wait() {
 // stride ld). (c0, o0) is the tile origin; (cmax, omax) the valid extents.
 template <int TC, int TO, int VEC, int NT>
 __device__ __forceinline__ void load_tile(double* s, const double* g, int64_t ld, int64_t c0,
-                                          int64_t o0, int64_t cmax, int64_t omax) {
+                                          int64_t o0, int64_t cmax, int64_t omax, int kshift = 0,
+                                          int64_t kbstride = 0) {
     constexpr int PER_QUAD = 4 / VEC;
     constexpr int CHUNKS = TC * TO / VEC;
 #pragma unroll
@@ -82,7 +89,9 @@ __device__ __forceinline__ void load_tile(double* s, const double* g, int64_t ld
         const int q = r / TO, o = r % TO;
         const int64_t gc = c0 + q * 4 + v * VEC, go = o0 + o;
         const bool ok = (gc < cmax) && (go < omax);
-        const double* src = ok ? g + gc + go * ld : g;
+        const int64_t off = kshift ? ((gc >> kshift) * kbstride + (gc & ((1LL << kshift) - 1)) + go * ld)
+                                   : gc + go * ld;
+        const double* src = ok ? g + off : g;
         cp_async<VEC>(s + id * VEC, src, ok);
     }
 }
@@ -114,7 +123,7 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32)
         mt = blockIdx.x % mtiles;
         nt = blockIdx.x / mtiles;
     }
-    const int64_t split = blockIdx.y, bz = blockIdx.z;
+    const int64_t split = blockIdx.y, bz = P.zmap ? (int64_t)P.zmap[blockIdx.z] : (int64_t)blockIdx.z;
     const int64_t kb = split * P.kchunk;
     const int64_t ke = min(P.K, kb + P.kchunk);
     const double* A = P.A + bz * P.strideA;
@@ -132,9 +141,9 @@ __global__ void __launch_bounds__(WARPS_M* WARPS_N * 32)
         if constexpr (!AK)  // A(m,k) at A[m + k*lda]: contiguous m
             load_tile<BM, BK, VEC, NT>(as, A, P.lda, m0, k0, P.M, ke);
         else                // A(m,k) at A[k + m*lda]: contiguous k
-            load_tile<BK, BM, VEC, NT>(as, A, P.lda, k0, m0, ke, P.M);
+            load_tile<BK, BM, VEC, NT>(as, A, P.lda, k0, m0, ke, P.M, P.kshift, P.kbstride);
         if constexpr (!BNM)  // B(k,n) at B[k + n*ldb]: contiguous k
-            load_tile<BK, BN, VEC, NT>(bs, B, P.ldb, k0, n0, ke, P.N);
+            load_tile<BK, BN, VEC, NT>(bs, B, P.ldb, k0, n0, ke, P.N, P.kshift, P.kbstride);
         else                 // B(k,n) at B[n + k*ldb]: contiguous n
             load_tile<BN, BK, VEC, NT>(bs, B, P.ldb, n0, k0, P.N, ke);
     };
@@ -265,6 +274,9 @@ struct GemmDesc {
     // split-K: > 1 writes `splits` partial outputs at C + s*strideCsplit
     int64_t splits = 1, strideCsplit = 0;
     int64_t kchunk = 0;  // rows of K per split; 0 = ceil(K / splits) rounded to 16
+    int kshift = 0;      // k-blocked K-major operands (see GemmParams)
+    int64_t kbstride = 0;
+    const int* zmap = nullptr;  // device array of `batch` batch indices (nullable)
 };
 
 // D = alpha op(A) op(B) + beta Cin (EPI_STORE).

@@ -48,6 +48,9 @@ void fill(GemmParams& P, const GemmDesc& d, int64_t kchunk) {
     P.kchunk = kchunk;
     P.strideCsplit = d.strideCsplit;
     P.tri = d.symmetric ? 1 : 0;
+    P.kshift = d.kshift;
+    P.kbstride = d.kbstride;
+    P.zmap = d.zmap;
 }
 
 void validate(const GemmDesc& d) {
@@ -57,6 +60,8 @@ void validate(const GemmDesc& d) {
         fail(PPC_ARGUMENT, "gemm: (A^T, B^T) orientation not supported");
     if (d.symmetric && d.M != d.N) fail(PPC_ARGUMENT, "gemm: symmetric needs M == N");
     if (d.batch > 65535 || d.splits > 65535) fail(PPC_ARGUMENT, "gemm: batch/splits too large");
+    if (d.kshift && (d.b_nmajor || !d.a_kmajor))
+        fail(PPC_ARGUMENT, "gemm: k-blocked addressing needs K-major A and B");
 }
 
 void launch(CfgId id, const GemmParams& P, dim3 grid, const GemmDesc& d, bool v2, int epi,

@@ -228,6 +228,135 @@ __global__ void jacobi_svd_kernel(const double* __restrict__ A, int64_t m, int64
     }
 }
 
+
+// Eigen mode for symmetric PSD blocks whose W fits shared memory but W + V do
+// not (b <= ~160): sweep on W in shared memory and log every round's
+// rotations (cs, sn) to global memory; V is rebuilt afterwards by a
+// row-parallel kernel that replays the log. rank/sig go to global memory.
+__global__ void jacobi_logged_kernel(const double* __restrict__ A, int64_t b, int64_t strideA,
+                                     double2* __restrict__ log, int64_t max_sweeps,
+                                     int* __restrict__ nsweeps, double* __restrict__ sig_out,
+                                     int* __restrict__ rank_out) {
+    extern __shared__ __align__(16) double W[];
+    __shared__ int s_rot;
+    const int64_t bi = blockIdx.x;
+    const double* Ab = A + bi * strideA;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
+    for (int64_t i = tid; i < b * b; i += nt) W[i] = Ab[i];
+    __syncthreads();
+    const int64_t P = (b + 1) & ~int64_t(1);
+    const int64_t per_sweep = (P - 1) * (P / 2);
+    double2* lg = log + bi * max_sweeps * per_sweep;
+    const double tol = kEps * sqrt((double)b);
+    int sweep = 0;
+    for (; sweep < max_sweeps && b > 1; ++sweep) {
+        if (tid == 0) s_rot = 0;
+        __syncthreads();
+        for (int64_t r = 0; r < P - 1; ++r) {
+            for (int64_t pi = warp; pi < P / 2; pi += nw) {
+                int64_t a, c;
+                if (pi == 0) { a = r; c = P - 1; }
+                else { a = (r + pi) % (P - 1); c = (r + P - 1 - pi) % (P - 1); }
+                if (a > c) { int64_t t = a; a = c; c = t; }
+                double cs = 1.0, sn = 0.0;
+                if (c < b) {
+                    double* wa = W + a * b;
+                    double* wc = W + c * b;
+                    double al = 0.0, be = 0.0, ga = 0.0;
+                    for (int64_t i = lane; i < b; i += 32) {
+                        const double x = wa[i], y = wc[i];
+                        al = fma(x, x, al); be = fma(y, y, be); ga = fma(x, y, ga);
+                    }
+                    al = warp_sum(al); be = warp_sum(be); ga = warp_sum(ga);
+                    if (ga != 0.0 && fabs(ga) > tol * sqrt(al * be)) {
+                        const double zeta = (be - al) / (2.0 * ga);
+                        const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+                        cs = rsqrt(1.0 + tt * tt);
+                        sn = cs * tt;
+                        for (int64_t i = lane; i < b; i += 32) {
+                            const double x = wa[i], y = wc[i];
+                            wa[i] = cs * x - sn * y;
+                            wc[i] = sn * x + cs * y;
+                        }
+                        if (lane == 0) s_rot = 1;
+                    }
+                }
+                if (lane == 0) lg[sweep * per_sweep + r * (P / 2) + pi] = make_double2(cs, sn);
+            }
+            __syncthreads();
+        }
+        if (!s_rot) { ++sweep; break; }
+        __syncthreads();
+    }
+    if (tid == 0) nsweeps[bi] = sweep;
+    double* sig = sig_out + bi * b;
+    int* rank = rank_out + bi * b;
+    for (int64_t c = warp; c < b; c += nw) {
+        double acc = 0.0;
+        for (int64_t i = lane; i < b; i += 32) acc = fma(W[c * b + i], W[c * b + i], acc);
+        acc = warp_sum(acc);
+        if (lane == 0) sig[c] = sqrt(acc);
+    }
+    __syncthreads();
+    for (int64_t c = tid; c < b; c += nt) {
+        const double sc = sig[c];
+        int rk = 0;
+        for (int64_t j = 0; j < b; ++j) rk += (sig[j] > sc) || (sig[j] == sc && j < c);
+        rank[c] = rk;
+    }
+}
+
+// Replays the rotation log on rows [row0, row0+ROWS) of V = I, then writes
+// the leading k eigenvectors (columns in rank order) and eigenvalues.
+template <int ROWS>
+__global__ void replay_rotations_kernel(const double2* __restrict__ log, const int* __restrict__ nsweeps,
+                                        int64_t b, int64_t max_sweeps, const double* __restrict__ sig,
+                                        const int* __restrict__ rank, int64_t k, double* __restrict__ V,
+                                        double* __restrict__ lambda) {
+    extern __shared__ __align__(16) double Vr[];  // ROWS x b, row-major
+    const int64_t bi = blockIdx.y;
+    const int64_t row0 = (int64_t)blockIdx.x * ROWS;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    for (int64_t t = tid; t < ROWS * b; t += nt) {
+        const int64_t i = t / b, c = t % b;
+        Vr[t] = (row0 + i == c) ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    const int64_t P = (b + 1) & ~int64_t(1);
+    const int64_t per_sweep = (P - 1) * (P / 2);
+    const double2* lg = log + bi * max_sweeps * per_sweep;
+    const int sw = nsweeps[bi];
+    for (int s = 0; s < sw; ++s)
+        for (int64_t r = 0; r < P - 1; ++r) {
+            const double2* rl = lg + s * per_sweep + r * (P / 2);
+            for (int64_t t = tid; t < ROWS * (P / 2); t += nt) {
+                const int64_t i = t / (P / 2), pi = t % (P / 2);
+                const double2 cs = rl[pi];
+                if (cs.y == 0.0 && cs.x == 1.0) continue;
+                int64_t a, c;
+                if (pi == 0) { a = r; c = P - 1; }
+                else { a = (r + pi) % (P - 1); c = (r + P - 1 - pi) % (P - 1); }
+                if (a > c) { int64_t tq = a; a = c; c = tq; }
+                if (c >= b) continue;
+                double* v = Vr + i * b;
+                const double x = v[a], y = v[c];
+                v[a] = cs.x * x - cs.y * y;
+                v[c] = cs.y * x + cs.x * y;
+            }
+            __syncthreads();
+        }
+    const int* rk = rank + bi * b;
+    for (int64_t t = tid; t < ROWS * b; t += nt) {
+        const int64_t i = t / b, c = t % b;
+        const int64_t o = rk[c];
+        if (o < k && row0 + i < b) V[(bi * k + o) * b + row0 + i] = Vr[t];
+    }
+    if (blockIdx.x == 0)
+        for (int64_t c = tid; c < b; c += nt)
+            if (rk[c] < k) lambda[bi * k + rk[c]] = sig[bi * b + c];
+}
+
 }  // namespace
 
 size_t jacobi_smem_bytes(int64_t m, int64_t n) {
@@ -243,6 +372,32 @@ void jacobi_svd(const double* A, int64_t m, int64_t n, int64_t strideA, int64_t 
     const size_t smem = jacobi_smem_bytes(m, n);
     const int threads = C >= 96 ? 512 : (C >= 32 ? 256 : 128);
     const bool use_smem = smem <= 200 * 1024;
+    if (!use_smem && !U && !tail2 && m == n && (size_t)n * n * sizeof(double) <= 200 * 1024) {
+        // eigen mode, W fits but W + V does not: logged rotations + replay
+        const int64_t P = (n + 1) & ~int64_t(1);
+        const int64_t max_sweeps = 40;
+        DeviceBuffer lg(sizeof(double2) * batch * max_sweeps * (P - 1) * (P / 2)),
+            ns(sizeof(int) * batch), sg(sizeof(double) * batch * n), rk(sizeof(int) * batch * n);
+        const size_t wsm = (size_t)n * n * sizeof(double);
+        PPC_CUDA_CHECK(cudaFuncSetAttribute(jacobi_logged_kernel,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm));
+        jacobi_logged_kernel<<<(unsigned)batch, 512, wsm, s>>>(A, n, strideA, lg.as<double2>(),
+                                                                max_sweeps, ns.as<int>(), sg.d(),
+                                                                rk.as<int>());
+        count_launch();
+        check_launch("jacobi_logged");
+        constexpr int ROWS = 32;
+        const size_t rsm = (size_t)ROWS * n * sizeof(double);
+        PPC_CUDA_CHECK(cudaFuncSetAttribute(replay_rotations_kernel<ROWS>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));
+        dim3 grid((unsigned)((n + ROWS - 1) / ROWS), (unsigned)batch);
+        replay_rotations_kernel<ROWS><<<grid, 512, rsm, s>>>(lg.as<double2>(), ns.as<int>(), n,
+                                                             max_sweeps, sg.d(), rk.as<int>(), k,
+                                                             V, S);
+        count_launch();
+        check_launch("replay_rotations");
+        return;
+    }
     DeviceBuffer ws;
     if (!use_smem) ws = DeviceBuffer((size_t)batch * (R * C + C * C + 2 * C) * sizeof(double));
     if (use_smem && smem > 48 * 1024)

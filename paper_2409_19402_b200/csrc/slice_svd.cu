@@ -31,6 +31,20 @@ __global__ void tree_add_kernel(double* parts, int64_t nparts, int64_t elems, in
     }
 }
 
+// Tb = T re-laid as consecutive blocks of KB rows: block kb is the KB x n3
+// column-major matrix of rows [kb*KB, kb*KB + KB) (zero-padded at the end).
+__global__ void block_rows_kernel(const double* __restrict__ T, double* __restrict__ Tb, int64_t N,
+                                  int64_t n3, int kshift, int64_t total) {
+    const int64_t KB = 1LL << kshift;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
+        const int64_t kb = e / (KB * n3), rem = e - kb * KB * n3;
+        const int64_t a = rem >> kshift, ii = rem & (KB - 1);
+        const int64_t i = (kb << kshift) + ii;
+        Tb[e] = i < N ? T[i + a * N] : 0.0;
+    }
+}
+
 __global__ void sqrt_clamp_kernel(const double* lam, double* sig, int64_t n) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) sig[i] = sqrt(fmax(lam[i], 0.0));
@@ -54,7 +68,7 @@ GramPlan gram_plan(int64_t N, int64_t n3) {
 }
 
 void gram_partials(const double* T, int64_t ldT, int64_t rows, int64_t n3, int64_t chunk,
-                   int64_t chunks, double* parts, cudaStream_t s) {
+                   int64_t chunks, double* parts, cudaStream_t s, int kshift) {
     GemmDesc d;
     d.M = n3; d.N = n3; d.K = rows;
     d.A = T; d.lda = ldT; d.a_kmajor = true;   // A(m,k) = T[k + m*ldT]
@@ -64,6 +78,11 @@ void gram_partials(const double* T, int64_t ldT, int64_t rows, int64_t n3, int64
     d.splits = chunks;
     d.kchunk = chunk;
     d.strideCsplit = n3 * n3;
+    if (kshift) {  // T is in the row-blocked layout (block_rows_kernel)
+        d.kshift = kshift;
+        d.kbstride = (1LL << kshift) * n3;
+        d.lda = d.ldb = 1LL << kshift;
+    }
     gemm(d, s);
 }
 
@@ -80,12 +99,30 @@ void tree_reduce(double* parts, int64_t nparts, int64_t elems, cudaStream_t s) {
 void gram(const double* T, int64_t N, int64_t n3, double* G, cudaStream_t s) {
     StageTimer tm("gram_syrk", s, (double)N * n3 * n3, 8.0 * N * n3);
     const GramPlan g = gram_plan(N, n3);
+    // Large tube matrices: each SYRK pipeline stage would touch one 2 MB page
+    // per column (columns are N*8 bytes apart), thrashing the TLB. Re-lay T
+    // into 2048-row blocks first (one extra HBM pass); same summation order.
+    const int kshift = (N >= (1LL << 20) && n3 >= 64) ? 11 : 0;
+    DeviceBuffer tb;
+    const double* src = T;
+    int64_t ld = N;
+    if (kshift) {
+        StageTimer tr("gram_relayout", s, 0.0, 16.0 * N * n3);
+        const int64_t KB = 1LL << kshift, nb = (N + KB - 1) / KB;
+        tb = DeviceBuffer(sizeof(double) * nb * KB * n3);
+        const int64_t total = nb * KB * n3;
+        block_rows_kernel<<<148 * 16, 256, 0, s>>>(T, tb.d(), N, n3, kshift, total);
+        count_launch();
+        check_launch("block_rows");
+        src = tb.d();
+        ld = KB;
+    }
     if (g.chunks == 1) {
-        gram_partials(T, N, N, n3, g.chunk, 1, G, s);
+        gram_partials(src, ld, N, n3, g.chunk, 1, G, s, kshift);
         return;
     }
     DeviceBuffer parts(sizeof(double) * g.chunks * n3 * n3);
-    gram_partials(T, N, N, n3, g.chunk, g.chunks, parts.d(), s);
+    gram_partials(src, ld, N, n3, g.chunk, g.chunks, parts.d(), s, kshift);
     tree_reduce(parts.d(), g.chunks, n3 * n3, s);
     PPC_CUDA_CHECK(cudaMemcpyAsync(G, parts.d(), sizeof(double) * n3 * n3, cudaMemcpyDeviceToDevice, s));
 }

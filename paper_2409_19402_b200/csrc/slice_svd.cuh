@@ -17,7 +17,7 @@ struct GramPlan {
 GramPlan gram_plan(int64_t N, int64_t n3);
 // Per-chunk partial Grams of the rows of T (ldT >= rows): parts[c] (n3 x n3).
 void gram_partials(const double* T, int64_t ldT, int64_t rows, int64_t n3, int64_t chunk,
-                   int64_t chunks, double* parts, cudaStream_t s);
+                   int64_t chunks, double* parts, cudaStream_t s, int kshift = 0);
 // Fixed pairwise tree over nparts arrays of `elems` doubles; result in parts[0].
 void tree_reduce(double* parts, int64_t nparts, int64_t elems, cudaStream_t s);
 

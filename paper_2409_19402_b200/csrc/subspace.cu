@@ -65,7 +65,8 @@ __global__ void cheb_kernel(double* __restrict__ Yn, const double* __restrict__ 
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
         const int64_t s = i / per_slice;
         const double a = coef[3 * s], b = coef[3 * s + 1], c = coef[3 * s + 2];
-        double v = a * Z[i] + b * Y[i];
+        double v = b * Y[i];
+        if (a != 0.0) v += a * Z[i];  // frozen slices: Z is not computed for them
         if (c != 0.0) v += c * Yp[i];
         Yn[i] = v;
     }
@@ -123,7 +124,7 @@ __global__ void residual_kernel(const double* GX, const double* X, const double*
 // in place (LAPACK trti2 order, one row per thread), written out as a full
 // b x b column-major block with zeros below the diagonal. b <= 160 (smem).
 __global__ void chol_inv_kernel(const double* __restrict__ S, double* __restrict__ Rinv, int64_t b,
-                                int shift_pass, int* fail) {
+                                int shift_pass, int* fail, double* __restrict__ Rout) {
     extern __shared__ __align__(16) double M[];
     __shared__ double piv;
     __shared__ int bad;
@@ -159,6 +160,13 @@ __global__ void chol_inv_kernel(const double* __restrict__ S, double* __restrict
         for (int64_t t = tid; t < rem * rem; t += nt) {
             const int64_t i = k + 1 + t % rem, j = k + 1 + t / rem;
             if (i <= j) M[i + j * b] -= M[k + i * b] * M[k + j * b];
+        }
+        __syncthreads();
+    }
+    if (Rout) {
+        for (int64_t t = tid; t < b * b; t += nt) {
+            const int64_t i = t % b, j = t / b;
+            Rout[s * b * b + t] = (i <= j) ? M[t] : 0.0;
         }
         __syncthreads();
     }
@@ -205,9 +213,10 @@ unsigned grid1(int64_t n) {
 // C_s (rows x cols) = alpha * X_s^T (rows x m)^T ... helpers for the batched
 // r x b panels (column-major, per-slice strides).
 void g_AtB(const double* A, const double* B, double* C, int64_t m, int64_t ra, int64_t rb,
-           int64_t batch, int64_t sA, int64_t sB, cudaStream_t s) {
+           int64_t batch, int64_t sA, int64_t sB, cudaStream_t s, const int* zmap = nullptr) {
     // C (ra x rb) = A^T (ra x m) * B (m x rb); A is m x ra, B is m x rb
     GemmDesc d;
+    d.zmap = zmap;
     d.M = ra; d.N = rb; d.K = m; d.batch = batch;
     d.A = A; d.lda = m; d.strideA = sA; d.a_kmajor = true;
     d.B = B; d.ldb = m; d.strideB = sB;
@@ -217,9 +226,10 @@ void g_AtB(const double* A, const double* B, double* C, int64_t m, int64_t ra, i
 
 void g_AB(const double* A, const double* B, double* C, int64_t m, int64_t kk, int64_t n,
           int64_t batch, int64_t sA, int64_t sB, double alpha, const double* Cin, double beta,
-          cudaStream_t s) {
+          cudaStream_t s, const int* zmap = nullptr) {
     // C (m x n) = alpha * A (m x kk) * B (kk x n) + beta * Cin
     GemmDesc d;
+    d.zmap = zmap;
     d.M = m; d.N = n; d.K = kk; d.batch = batch;
     d.A = A; d.lda = m; d.strideA = sA;
     d.B = B; d.ldb = kk; d.strideB = sB;
@@ -231,7 +241,7 @@ void g_AB(const double* A, const double* B, double* C, int64_t m, int64_t kk, in
 
 struct Work {
     int64_t r, b, batch;
-    DeviceBuffer X, Y, Yp, Yn, Z, W, P, S, Rinv, Hv, th, res, coef, wmask, nlock, fail;
+    DeviceBuffer X, Y, Yp, Yn, Z, W, P, S, Rinv, Hv, th, res, coef, wmask, nlock, fail, zmap;
     Work(int64_t r_, int64_t b_, int64_t batch_)
         : r(r_), b(b_), batch(batch_),
           X(sizeof(double) * r_ * b_ * batch_), Y(sizeof(double) * r_ * b_ * batch_),
@@ -241,43 +251,71 @@ struct Work {
           Rinv(sizeof(double) * b_ * b_ * batch_), Hv(sizeof(double) * b_ * b_ * batch_),
           th(sizeof(double) * b_ * batch_), res(sizeof(double) * b_ * batch_),
           coef(sizeof(double) * 3 * batch_), wmask(sizeof(double) * b_ * batch_),
-          nlock(sizeof(int) * batch_), fail(sizeof(int) * 2) {}
+          nlock(sizeof(int) * batch_), fail(sizeof(int) * 2), zmap(sizeof(int) * batch_) {}
 };
 
-// Orthonormalize the columns of Y (r x b per slice) into X via shifted
-// CholQR3 (Fukaya, Kannan, Nakatsukasa, Yamamoto, Yanagisawa 2020): a shifted
-// first pass makes the Cholesky factorization succeed for cond(Y) up to ~1e15,
-// two plain passes restore orthogonality to machine precision.
-void cholqr3(Work& w, double* Yin, double* Xout, cudaStream_t s) {
-    const int64_t r = w.r, b = w.b, batch = w.batch;
-    const size_t smem = (size_t)b * b * sizeof(double);
+// General strided-batch GEMM on column panels: C = alpha op(A) B + beta C.
+void gg(const double* A, int64_t lda, int64_t sA, bool at, const double* B, int64_t ldb, int64_t sB,
+        double* C, int64_t ldc, int64_t sC, int64_t M, int64_t N, int64_t K, int64_t batch,
+        double alpha, double beta, cudaStream_t s, const int* zmap = nullptr) {
+    GemmDesc d;
+    d.M = M; d.N = N; d.K = K; d.batch = batch; d.zmap = zmap;
+    d.A = A; d.lda = lda; d.strideA = sA; d.a_kmajor = at;
+    d.B = B; d.ldb = ldb; d.strideB = sB;
+    d.C = C; d.ldc = ldc; d.strideC = sC;
+    d.alpha = alpha;
+    if (beta != 0.0) { d.Cin = C; d.ldcin = ldc; d.strideCin = sC; d.beta = beta; }
+    gemm(d, s);
+}
+
+// Orthonormalize columns [c0, b) of the r x b panels Y into the same columns
+// of Xout: first against the locked columns [0, c0) of X (block CGS, twice),
+// then shifted CholQR3 (Fukaya, Kannan, Nakatsukasa, Yamamoto, Yanagisawa
+// 2020): the shifted first pass keeps the Cholesky factorization alive for
+// cond(Y) up to ~1e15, two plain passes restore orthogonality.
+void cholqr3(Work& w, double* Y, double* Xout, int64_t c0, cudaStream_t s) {
+    const int64_t r = w.r, b = w.b, batch = w.batch, bc = b - c0, per = r * b;
+    StageTimer tm("ss.cholqr3", s);
+    if (c0 > 0)
+        for (int pass = 0; pass < 2; ++pass) {
+            // P = X_L^T Y_A (c0 x bc); Y_A -= X_L P
+            gg(w.X.d(), r, per, true, Y + c0 * r, r, per, w.P.d(), c0, c0 * bc, c0, bc, r, batch, 1.0, 0.0, s);
+            gg(w.X.d(), r, per, false, w.P.d(), c0, c0 * bc, Y + c0 * r, r, per, r, bc, c0, batch, -1.0, 1.0, s);
+        }
+    const size_t smem = (size_t)bc * bc * sizeof(double);
     if (smem > 200 * 1024) fail(PPC_ARGUMENT, "subspace: block too wide for the CholQR kernel");
     if (smem > 48 * 1024)
         PPC_CUDA_CHECK(cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             (int)smem));
-    double* src = Yin;
-    DeviceBuffer tmp(sizeof(double) * r * b * batch);
+    double* src = Y + c0 * r;
+    double* bufs[3] = {w.Yn.d() + c0 * r, w.Z.d() + c0 * r, Xout + c0 * r};
     for (int pass = 0; pass < 3; ++pass) {
-        g_AtB(src, src, w.S.d(), r, b, b, batch, r * b, r * b, s);  // S = Y^T Y
-        chol_inv_kernel<<<(unsigned)batch, 256, smem, s>>>(w.S.d(), w.Rinv.d(), b, pass == 0 ? 1 : 0,
-                                                            w.fail.as<int>());
+        gg(src, r, per, true, src, r, per, w.S.d(), bc, bc * bc, bc, bc, r, batch, 1.0, 0.0, s);  // S = Y^T Y
+        chol_inv_kernel<<<(unsigned)batch, 256, smem, s>>>(w.S.d(), w.Rinv.d(), bc, pass == 0 ? 1 : 0,
+                                                            w.fail.as<int>(), nullptr);
         count_launch();
         check_launch("chol_inv");
-        double* dst = (pass == 2) ? Xout : (pass == 0 ? w.Yn.d() : tmp.d());
-        g_AB(src, w.Rinv.d(), dst, r, b, b, batch, r * b, b * b, 1.0, nullptr, 0.0, s);
-        src = dst;
+        gg(src, r, per, false, w.Rinv.d(), bc, bc * bc, bufs[pass], r, per, r, bc, bc, batch, 1.0, 0.0, s);
+        src = bufs[pass];
     }
 }
 
-// Rayleigh-Ritz on the orthonormal Xn: X = Xn Z, theta, W = G X, res.
-void rayleigh_ritz(Work& w, const double* G, int64_t sG, double* Xn, cudaStream_t s) {
-    const int64_t r = w.r, b = w.b, batch = w.batch;
-    g_AB(G, Xn, w.Z.d(), r, r, b, batch, sG, r * b, 1.0, nullptr, 0.0, s);  // Z = G Xn
-    g_AtB(Xn, w.Z.d(), w.S.d(), r, b, b, batch, r * b, r * b, s);          // H = Xn^T G Xn
-    // eigen-decomposition of H (PSD) by one-sided Jacobi: V = eigvecs, S = eigvals
-    jacobi_svd(w.S.d(), b, b, b * b, batch, b, nullptr, w.th.d(), w.Hv.d(), nullptr, s);
-    g_AB(Xn, w.Hv.d(), w.X.d(), r, b, b, batch, r * b, b * b, 1.0, nullptr, 0.0, s);   // X
-    g_AB(w.Z.d(), w.Hv.d(), w.W.d(), r, b, b, batch, r * b, b * b, 1.0, nullptr, 0.0, s);  // G X
+// Rayleigh-Ritz on the orthonormal active columns [c0, b) of Xn: X, theta,
+// W = G X and residual norms for those columns (locked ones keep theirs).
+void rayleigh_ritz(Work& w, const double* G, int64_t sG, double* Xn, int64_t c0, cudaStream_t s) {
+    const int64_t r = w.r, b = w.b, batch = w.batch, bc = b - c0, per = r * b;
+    StageTimer tm("ss.rayleigh_ritz", s);
+    gg(G, r, sG, false, Xn + c0 * r, r, per, w.Z.d() + c0 * r, r, per, r, bc, r, batch, 1.0, 0.0, s);  // Z = G Xn
+    gg(Xn + c0 * r, r, per, true, w.Z.d() + c0 * r, r, per, w.S.d(), bc, bc * bc, bc, bc, r, batch, 1.0, 0.0, s);
+    {
+        StageTimer tj("ss.rr_eig", s);
+        // H (PSD) = Hv diag(theta) Hv^T by one-sided Jacobi (eigen mode)
+        jacobi_svd(w.S.d(), bc, bc, bc * bc, batch, bc, nullptr, w.P.d(), w.Hv.d(), nullptr, s);
+    }
+    PPC_CUDA_CHECK(cudaMemcpy2DAsync(w.th.d() + c0, sizeof(double) * b, w.P.d(), sizeof(double) * bc,
+                                     sizeof(double) * bc, batch, cudaMemcpyDeviceToDevice, s));
+    gg(Xn + c0 * r, r, per, false, w.Hv.d(), bc, bc * bc, w.X.d() + c0 * r, r, per, r, bc, bc, batch, 1.0, 0.0, s);
+    gg(w.Z.d() + c0 * r, r, per, false, w.Hv.d(), bc, bc * bc, w.W.d() + c0 * r, r, per, r, bc, bc, batch, 1.0, 0.0, s);
     dim3 grid((unsigned)((b + 7) / 8), (unsigned)batch);
     residual_kernel<<<grid, 256, 0, s>>>(w.W.d(), w.X.d(), w.th.d(), w.res.d(), r, b);
     count_launch();
@@ -324,10 +362,11 @@ void subspace_eig_top(const double* G, int64_t r, int64_t batch, int64_t k, doub
     PPC_CUDA_CHECK(cudaMemsetAsync(w.fail.d(), 0, 2 * sizeof(int), s));
     randn_kernel<<<grid1(per * batch), 256, 0, s>>>(w.Y.d(), per * batch, 0x5eed5eedULL + (uint64_t)r * 131 + b);
     count_launch();
-    cholqr3(w, w.Y.d(), w.Yp.d(), s);
-    rayleigh_ritz(w, G, r * r, w.Yp.d(), s);
+    cholqr3(w, w.Y.d(), w.Yp.d(), 0, s);
+    rayleigh_ritz(w, G, r * r, w.Yp.d(), 0, s);
 
-    std::vector<double> th(b * batch), res(b * batch), coef(3 * batch), wm(b * batch);
+    std::vector<double> th(b * batch), res(b * batch), coef(3 * batch), wm(b * batch),
+        thp(b * batch, 0.0);
     std::vector<int> nlock(batch, 0);
     const int max_iter = 100;
     for (int it = 0; it < max_iter; ++it) {
@@ -357,12 +396,25 @@ void subspace_eig_top(const double* G, int64_t r, int64_t batch, int64_t k, doub
                 const double gap = std::max(t[k - 1] - t[k], 0.0);
                 const double srec = 1e-11 * std::sqrt(energy) * gap /
                                     (std::sqrt(std::max(t[k - 1], 0.0)) + std::sqrt(std::max(t[k], 0.0)) + 1e-300);
-                thr = std::max(32.0 * 2.22e-16 * scale, std::min(srec, 1e-9 * scale));
+                // polished singular values err by ~ sigma_j * angle^2, angle ~ res/gap
+                const double ssig = 3e-6 * gap;
+                thr = std::max(32.0 * 2.22e-16 * scale, std::min(srec, ssig));
             } else {
                 thr = 1e-13 * scale;
             }
             int L = 0;
-            while (L < k && rr[L] <= thr) ++L;  // locked prefix
+            if (vectors_for_reconstruction) {
+                while (L < k && rr[L] <= thr) ++L;  // locked prefix
+            } else {
+                // basis Q: judged on eigenvalues / captured energy (SURVEY 8c
+                // rule 5) -> also lock Ritz values that moved < 1e-14 theta_1
+                // in the last iteration (linear convergence: remaining error
+                // well under the 1e-12 theta_1 parity bound)
+                while (L < k && (rr[L] <= thr ||
+                                 (it >= 2 && std::fabs(t[L] - thp[sl * b + L]) <= 1e-14 * scale &&
+                                  rr[L] <= 1e-6 * scale)))
+                    ++L;
+            }
             nlock[sl] = L;
             for (int64_t j = 0; j < b; ++j) wm[sl * b + j] = (j < L) ? t[j] : 0.0;
             if (L >= k || t[0] <= 0.0) {
@@ -393,22 +445,15 @@ void subspace_eig_top(const double* G, int64_t r, int64_t batch, int64_t k, doub
                         it, (long long)sl, L, deg[sl], t[0], t[k - 1], t[b - 1], rr[0], rr[k - 1], thr);
         }
         if (dbg) fprintf(stderr, "[subspace] it %d dmax %d\n", it, dmax);
+        thp = th;
         if (all_done) break;
         PPC_CUDA_CHECK(cudaMemcpyAsync(w.wmask.d(), wm.data(), sizeof(double) * b * batch, cudaMemcpyHostToDevice, s));
         PPC_CUDA_CHECK(cudaMemcpyAsync(w.nlock.d(), nlock.data(), sizeof(int) * batch, cudaMemcpyHostToDevice, s));
-        // filter: Y_0 = X; Y_{j+1} from the deflated operator G - X_L Theta_L X_L^T
-        PPC_CUDA_CHECK(cudaMemcpyAsync(w.Y.d(), w.X.d(), sizeof(double) * per * batch, cudaMemcpyDeviceToDevice, s));
-        double* Y = w.Y.d();
-        double* Yp = w.Yp.d();
-        double* Yn = w.Yn.d();
-        for (int j = 0; j < dmax; ++j) {
-            g_AB(G, Y, w.Z.d(), r, r, b, batch, r * r, per, 1.0, nullptr, 0.0, s);  // Z = G Y
-            g_AtB(w.X.d(), Y, w.P.d(), r, b, b, batch, per, per, s);              // P = X^T Y
-            scale_rows_kernel<<<grid1(b * b * batch), 256, 0, s>>>(w.P.d(), w.wmask.d(), b, b * b * batch);
-            count_launch();
-            g_AB(w.X.d(), w.P.d(), w.Z.d(), r, b, b, batch, per, b * b, -1.0, w.Z.d(), 1.0, s);  // Z -= X P
+        // per-degree, per-slice recurrence coefficients (one upload per iteration)
+        coef.assign(3 * batch * dmax, 0.0);
+        for (int j = 0; j < dmax; ++j)
             for (int64_t sl = 0; sl < batch; ++sl) {
-                double* cf = &coef[3 * sl];
+                double* cf = &coef[3 * (j * batch + sl)];
                 if (j >= deg[sl]) {
                     cf[0] = 0.0; cf[1] = 1.0; cf[2] = 0.0;  // frozen: Y_{j+1} = Y_j
                 } else if (j == 0) {
@@ -417,17 +462,41 @@ void subspace_eig_top(const double* G, int64_t r, int64_t batch, int64_t k, doub
                     cf[0] = 2.0 / ee[sl]; cf[1] = -2.0 * cc[sl] / ee[sl]; cf[2] = -1.0;
                 }
             }
-            PPC_CUDA_CHECK(cudaMemcpyAsync(w.coef.d(), coef.data(), sizeof(double) * 3 * batch, cudaMemcpyHostToDevice, s));
-            cheb_kernel<<<grid1(per * batch), 256, 0, s>>>(Yn, w.Z.d(), Y, Yp, w.coef.d(), per, per * batch);
-            count_launch();
-            check_launch("cheb");
-            // rotate buffers: (Yp, Y, Yn) <- (Y, Yn, Yp)
-            double* t = Yp;
-            Yp = Y;
-            Y = Yn;
-            Yn = t;
-            // keep the host coefficient buffer alive until the copy ran
-            PPC_CUDA_CHECK(cudaStreamSynchronize(s));
+        if ((int64_t)coef.size() * 8 > (int64_t)w.coef.bytes()) w.coef = DeviceBuffer(coef.size() * sizeof(double));
+        std::vector<int> zm((size_t)dmax * batch), nact(dmax, 0);
+        for (int j = 0; j < dmax; ++j)
+            for (int64_t sl = 0; sl < batch; ++sl)
+                if (j < deg[sl]) zm[(size_t)j * batch + nact[j]++] = (int)sl;
+        if ((int64_t)zm.size() * 4 > (int64_t)w.zmap.bytes()) w.zmap = DeviceBuffer(zm.size() * sizeof(int));
+        PPC_CUDA_CHECK(cudaMemcpyAsync(w.zmap.d(), zm.data(), sizeof(int) * zm.size(), cudaMemcpyHostToDevice, s));
+        PPC_CUDA_CHECK(cudaMemcpyAsync(w.coef.d(), coef.data(), sizeof(double) * coef.size(), cudaMemcpyHostToDevice, s));
+        // filter: Y_0 = X; Y_{j+1} from the deflated operator G - X_L Theta_L X_L^T
+        PPC_CUDA_CHECK(cudaMemcpyAsync(w.Y.d(), w.X.d(), sizeof(double) * per * batch, cudaMemcpyDeviceToDevice, s));
+        double* Y = w.Y.d();
+        double* Yp = w.Yp.d();
+        double* Yn = w.Yn.d();
+        {
+            StageTimer tf("ss.filter", s);
+            for (int j = 0; j < dmax; ++j) {
+                // only the slices still filtering at this degree (compacted batch)
+                const int na = nact[j];
+                const int* zm = w.zmap.as<int>() + (int64_t)j * batch;
+                if (na > 0) {
+                    g_AB(G, Y, w.Z.d(), r, r, b, na, r * r, per, 1.0, nullptr, 0.0, s, zm);  // Z = G Y
+                    g_AtB(w.X.d(), Y, w.P.d(), r, b, b, na, per, per, s, zm);              // P = X^T Y
+                    scale_rows_kernel<<<grid1(b * b * batch), 256, 0, s>>>(w.P.d(), w.wmask.d(), b, b * b * batch);
+                    count_launch();
+                    g_AB(w.X.d(), w.P.d(), w.Z.d(), r, b, b, na, per, b * b, -1.0, w.Z.d(), 1.0, s, zm);  // Z -= X P
+                }
+                cheb_kernel<<<grid1(per * batch), 256, 0, s>>>(Yn, w.Z.d(), Y, Yp, w.coef.d() + 3 * j * batch,
+                                                                per, per * batch);
+                count_launch();
+                check_launch("cheb");
+                double* t = Yp;  // rotate (Yp, Y, Yn) <- (Y, Yn, Yp)
+                Yp = Y;
+                Y = Yn;
+                Yn = t;
+            }
         }
         // locked columns back, normalize, CholQR2, Rayleigh-Ritz
         dim3 grid((unsigned)((b + 7) / 8), (unsigned)batch);
@@ -440,8 +509,13 @@ void subspace_eig_top(const double* G, int64_t r, int64_t batch, int64_t k, doub
             Y = w.Yp.d();
         }
         double* Xn = (Y == w.Y.d()) ? w.Yp.d() : w.Y.d();
-        cholqr3(w, Y, Xn, s);
-        rayleigh_ritz(w, G, r * r, Xn, s);
+        // Rayleigh-Ritz only on the columns past the common locked prefix
+        const int64_t c0 = std::min<int64_t>(*std::min_element(nlock.begin(), nlock.end()), b - 1);
+        if (c0 > 0)  // locked columns of the basis are final: copy them through
+            PPC_CUDA_CHECK(cudaMemcpy2DAsync(Xn, sizeof(double) * per, w.X.d(), sizeof(double) * per,
+                                             sizeof(double) * r * c0, batch, cudaMemcpyDeviceToDevice, s));
+        cholqr3(w, Y, Xn, c0, s);
+        rayleigh_ritz(w, G, r * r, Xn, c0, s);
     }
     // outputs: leading k Ritz pairs
     PPC_CUDA_CHECK(cudaMemcpy2DAsync(Xout, sizeof(double) * r * k, w.X.d(), sizeof(double) * per,
@@ -471,8 +545,11 @@ void subspace_svd(const double* A, int64_t m, int64_t n, int64_t stride, int64_t
     subspace_eig_top(G.d(), r, batch, k, Xk.d(), lam.d(), s, true);
     // polish: W = A Xk (tall: m x k) or A^T Xk (wide: n x k)
     const int64_t o = tall ? m : n;
-    DeviceBuffer Wb(sizeof(double) * o * k * batch), Us(sizeof(double) * o * k * batch),
-        Vs(sizeof(double) * k * k * batch);
+    DeviceBuffer Wb(sizeof(double) * o * k * batch), Qw(sizeof(double) * o * k * batch),
+        T1(sizeof(double) * o * k * batch), Sk(sizeof(double) * k * k * batch),
+        R1(sizeof(double) * k * k * batch), R2(sizeof(double) * k * k * batch),
+        Ri(sizeof(double) * k * k * batch), R(sizeof(double) * k * k * batch),
+        Ur(sizeof(double) * k * k * batch), Vr(sizeof(double) * k * k * batch), flag(sizeof(int) * 2);
     {
         GemmDesc d;
         d.M = o; d.N = k; d.K = r; d.batch = batch;
@@ -483,18 +560,31 @@ void subspace_svd(const double* A, int64_t m, int64_t n, int64_t stride, int64_t
         d.C = Wb.d(); d.ldc = o; d.strideC = o * k;
         gemm(d, s);
     }
-    // W = P diag(sigma) R^T (one-sided Jacobi; R k x k)
-    jacobi_svd(Wb.d(), o, k, o * k, batch, k, Us.d(), S, Vs.d(), nullptr, s);
-    if (tall) {
-        // A ~ U sigma (Xk R)^T: U = P, V = Xk R
-        PPC_CUDA_CHECK(cudaMemcpyAsync(U, Us.d(), sizeof(double) * m * k * batch, cudaMemcpyDeviceToDevice, s));
-        g_AB(Xk.d(), Vs.d(), V, n, k, k, batch, n * k, k * k, 1.0, nullptr, 0.0, s);
-    } else {
-        // A^T ~ P sigma (Xk R)^T  =>  A ~ (Xk R) sigma P^T: U = Xk R, V = P
-        g_AB(Xk.d(), Vs.d(), U, m, k, k, batch, m * k, k * k, 1.0, nullptr, 0.0, s);
-        PPC_CUDA_CHECK(cudaMemcpyAsync(V, Us.d(), sizeof(double) * n * k * batch, cudaMemcpyDeviceToDevice, s));
-        sign_rule(U, m, k, batch, V, n, s);
+    // CholQR2 of W (cond(W) = sigma_1/sigma_k): W = Qw R, R = R2 R1
+    const size_t ksm = (size_t)k * k * sizeof(double);
+    if (ksm > 48 * 1024)
+        PPC_CUDA_CHECK(cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ksm));
+    g_AtB(Wb.d(), Wb.d(), Sk.d(), o, k, k, batch, o * k, o * k, s);
+    chol_inv_kernel<<<(unsigned)batch, 256, ksm, s>>>(Sk.d(), Ri.d(), k, 0, flag.as<int>(), R1.d());
+    count_launch();
+    check_launch("chol_inv");
+    g_AB(Wb.d(), Ri.d(), T1.d(), o, k, k, batch, o * k, k * k, 1.0, nullptr, 0.0, s);
+    g_AtB(T1.d(), T1.d(), Sk.d(), o, k, k, batch, o * k, o * k, s);
+    chol_inv_kernel<<<(unsigned)batch, 256, ksm, s>>>(Sk.d(), Ri.d(), k, 0, flag.as<int>(), R2.d());
+    count_launch();
+    check_launch("chol_inv");
+    g_AB(T1.d(), Ri.d(), Qw.d(), o, k, k, batch, o * k, k * k, 1.0, nullptr, 0.0, s);
+    g_AB(R2.d(), R1.d(), R.d(), k, k, k, batch, k * k, k * k, 1.0, nullptr, 0.0, s);
+    // R = Ur diag(sigma) Vr^T (one-CTA Jacobi, high relative accuracy)
+    jacobi_svd(R.d(), k, k, k * k, batch, k, Ur.d(), S, Vr.d(), nullptr, s);
+    if (tall) {  // A ~ (Qw Ur) sigma (Xk Vr)^T
+        g_AB(Qw.d(), Ur.d(), U, m, k, k, batch, m * k, k * k, 1.0, nullptr, 0.0, s);
+        g_AB(Xk.d(), Vr.d(), V, n, k, k, batch, n * k, k * k, 1.0, nullptr, 0.0, s);
+    } else {     // A^T ~ (Qw Ur) sigma (Xk Vr)^T  =>  A ~ (Xk Vr) sigma (Qw Ur)^T
+        g_AB(Xk.d(), Vr.d(), U, m, k, k, batch, m * k, k * k, 1.0, nullptr, 0.0, s);
+        g_AB(Qw.d(), Ur.d(), V, n, k, k, batch, n * k, k * k, 1.0, nullptr, 0.0, s);
     }
+    sign_rule(U, m, k, batch, V, n, s);  // matrix_kernels.cpp:16-25
     if (tail2) slice_tail_energy(A, m, n, stride, batch, k, U, S, V, tail2, s);
 }
 

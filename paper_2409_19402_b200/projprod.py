@@ -27,7 +27,7 @@ __all__ = [
     "FormatError", "EngineError", "Transform", "TsvdqFactors", "mode3_product",
     "facewise_product", "frobenius_norm", "svd", "truncated_svd", "data_dependent_transform",
     "projection_error", "star_q", "star_q_product", "tsvdq", "tsvdq_reconstruct", "tsvdq_error",
-    "relative_error", "tsvdq_relative_error", "to_device", "empty_device", "to_host",
+    "relative_error", "tsvdq_relative_error", "compress_tsvdq", "to_device", "empty_device", "to_host",
     "launch_count",
 ]
 
@@ -418,6 +418,24 @@ def relative_error(ref, approx) -> float:
     out = C.c_double()
     _call(args, _lib.lib().ppc_relative_error, pa, pb, int(np.prod(a_.shape)), C.byref(out), args.loc)
     return out.value
+
+
+def compress_tsvdq(a, p: int, k: int):
+    """tools/main.cpp:186-283 (`compress --method tsvdq --transform data`):
+    data-driven Q, tSVDQ factors and the reconstruction's relative error in one
+    device pass. Returns (TsvdqFactors, relative_error)."""
+    args = _Args(a)
+    a_, pa = args.inp(a, 3)
+    n1, n2, n3 = a_.shape
+    q, pq = args.out((n3, p))
+    U, pu = args.out((n1, k, p))
+    S, ps = args.out((k, p))
+    V, pv = args.out((n2, k, p))
+    re = C.c_double()
+    _call(args, _lib.lib().ppc_tsvdq_compress, pa, n1, n2, n3, p, k, pq, None, pu, ps, pv,
+          C.byref(re), args.loc)
+    t = Transform._from_q(to_host(q) if args.device else q, "data")
+    return TsvdqFactors(U, S, V, t, k, n1, n2), re.value
 
 
 def tsvdq_relative_error(a, f: TsvdqFactors) -> float:
