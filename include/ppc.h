@@ -114,6 +114,8 @@ int ppc_dct_q(int64_t n3, int64_t p, double* Q);                          /* hos
 int ppc_haar_q(int64_t n3, int64_t p, double* Q);                         /* host */
 int ppc_random_orthogonal_q(int64_t n3, int64_t p, uint64_t seed, double* Q); /* host */
 int ppc_identity_q(int64_t n3, int64_t p, double* Q);                     /* host */
+/* matrix_kernels.cpp:48-78 orthonormalize (rank gate, Householder QR, sign rule). */
+int ppc_orthonormalize(const double* A, int64_t n, int64_t p, double* Q);    /* host */
 /* transforms.cpp:20-27 + 100-109 of custom_transform: Stiefel check. */
 int ppc_check_stiefel(const double* Q, int64_t n3, int64_t p);            /* host */
 

@@ -60,6 +60,7 @@ def lib() -> C.CDLL:
         "ppc_random_orthogonal_q": (C.c_int, [i64, i64, C.c_uint64, vp]),
         "ppc_identity_q": (C.c_int, [i64, i64, vp]),
         "ppc_check_stiefel": (C.c_int, [vp, i64, i64]),
+        "ppc_orthonormalize": (C.c_int, [vp, i64, i64, vp]),
         "ppc_star_q_product": (C.c_int, [vp, i64, i64, i64, vp, i64, vp, i64, C.c_double, vp, C.c_int]),
         "ppc_tsvdq": (C.c_int, [vp, i64, i64, i64, vp, i64, i64, vp, vp, vp, C.c_int]),
         "ppc_tsvdq_reconstruct": (C.c_int, [vp, vp, vp, vp, i64, i64, i64, i64, i64, vp, C.c_int]),

@@ -207,6 +207,19 @@ int ppc_random_orthogonal_q(int64_t n3, int64_t p, uint64_t seed, double* Q) {
     });
 }
 
+int ppc_orthonormalize(const double* A, int64_t n, int64_t p, double* Q) {
+    return guarded([&] {
+        if (p < 1 || p > n)
+            fail(PPC_ARGUMENT, "orthonormalize: need 1 <= cols <= rows, got " + std::to_string(n) + "x" +
+                                   std::to_string(p));
+        std::vector<double> a(A, A + n * p);
+        for (double x : a)
+            if (!std::isfinite(x)) fail(PPC_NUMERIC, "orthonormalize: input has non-finite entries");
+        const auto q = orthonormalize(a, n, p);
+        for (int64_t i = 0; i < n * p; ++i) Q[i] = q[i];
+    });
+}
+
 // transforms.cpp:20-27 (+ non-finite check of custom_transform :100-103)
 int ppc_check_stiefel(const double* Q, int64_t n3, int64_t p) {
     return guarded([&] {

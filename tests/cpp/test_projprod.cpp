@@ -1,0 +1,194 @@
+// C++ API drop-in test: the reference's own test cases (proj/tests/*.cpp,
+// restated without doctest/Eigen) run against libprojprod.so -> libppc.so.
+// Exit code 0 = all passed. Needs a B200.
+#include <cmath>
+#include <cstdio>
+#include <functional>
+#include <string>
+#include <vector>
+
+#include "projprod/decompositions.hpp"
+#include "projprod/errors.hpp"
+#include "projprod/metrics.hpp"
+#include "projprod/star_products.hpp"
+
+using namespace projprod;
+
+static int g_fail = 0, g_checks = 0;
+#define CHECK(c)                                                                   \
+    do {                                                                           \
+        ++g_checks;                                                                \
+        if (!(c)) {                                                                \
+            ++g_fail;                                                              \
+            std::fprintf(stderr, "FAIL %s:%d: %s\n", __FILE__, __LINE__, #c);      \
+        }                                                                          \
+    } while (0)
+template <class E, class F>
+static void check_throws(F f, const char* what) {
+    ++g_checks;
+    try {
+        f();
+    } catch (const E&) {
+        return;
+    } catch (...) {
+    }
+    ++g_fail;
+    std::fprintf(stderr, "FAIL: expected exception: %s\n", what);
+}
+
+static Tensor3 make_tube(std::vector<double> v) {
+    Tensor3 t(1, 1, (Index)v.size());
+    for (Index k = 0; k < t.n3(); ++k) t(0, 0, k) = v[(size_t)k];
+    return t;
+}
+static Tensor3 counterexample() {  // tests/support/common.hpp:15-22
+    Tensor3 A(2, 2, 2);
+    A(0, 0, 0) = 1; A(1, 1, 0) = 1; A(0, 0, 1) = 1; A(1, 1, 1) = -1;
+    return A;
+}
+static Tensor3 seeded(Index n1, Index n2, Index n3, unsigned s) {
+    Tensor3 A(n1, n2, n3);
+    unsigned x = s * 2654435761u + 1;
+    for (Index i = 0; i < A.size(); ++i) {
+        x = x * 1664525u + 1013904223u;
+        A.data()[i] = ((x >> 8) * (1.0 / 16777216.0)) - 0.5;
+    }
+    return A;
+}
+
+int main() {
+    const double s2 = std::sqrt(2.0);
+    // test_star_products.cpp:70-78 — worked projected products
+    {
+        Tensor3 a = make_tube({2, 4, 6, 8}), b = make_tube({1, -1, 1, 0});
+        StarContext ctx(haar_transform(4, 2));
+        Tensor3 ab = star_q_product(a, b, ctx);
+        const double w[4] = {3, 3, 3, 0};
+        for (int k = 0; k < 4; ++k) CHECK(std::fabs(ab(0, 0, k) - w[k]) <= 1e-12);
+        Matrix H4 = haar_transform(4, 4).Q;
+        StarContext perp(custom_transform(H4.rightCols(2)));
+        Tensor3 c = star_q_product(a, b, perp);
+        const double w2[4] = {-1, 1, 0, 8};
+        for (int k = 0; k < 4; ++k) CHECK(std::fabs(c(0, 0, k) - w2[k]) <= 1e-12);
+        // identity acts as projection: [3,3,6,0]
+        Tensor3 ia = star_q_product(star_q_identity(1, ctx), a, ctx);
+        const double w3[4] = {3, 3, 6, 0};
+        for (int k = 0; k < 4; ++k) CHECK(std::fabs(ia(0, 0, k) - w3[k]) <= 1e-12);
+    }
+    // test_tensor.cpp:101-121 — mode-3 product KAT
+    {
+        Tensor3 a = make_tube({2, 4, 6, 8});
+        Matrix Q = haar_transform(4, 2).Q;
+        Tensor3 ah = mode3_product(a, Q.transpose());
+        CHECK(std::fabs(ah(0, 0, 0) - (3 + 3 * s2)) <= 1e-14 * (3 + 3 * s2));
+        CHECK(std::fabs(ah(0, 0, 1) - (3 - 3 * s2)) <= 1e-13);
+        check_throws<shape_error>([&] { mode3_product(a, Matrix::Identity(3, 3)); }, "mode3 shape");
+    }
+    // test_tensor.cpp:144-149 — facewise tube
+    {
+        Tensor3 ab = facewise_product(make_tube({1, 2, 3}), make_tube({4, 5, -6}));
+        CHECK(ab(0, 0, 0) == 4.0 && ab(0, 0, 1) == 10.0 && ab(0, 0, 2) == -18.0);
+        check_throws<shape_error>([&] { facewise_product(counterexample(), Tensor3(3, 2, 2)); }, "facewise");
+    }
+    // test_tensor.cpp:160-165 — Frobenius norm
+    CHECK(std::fabs(frobenius_norm(counterexample()) - 2.0) <= 1e-15 * 2);
+    CHECK(frobenius_norm(Tensor3(3, 3, 3)) == 0.0);
+    // test_decompositions.cpp:61-78 — error splits
+    {
+        Tensor3 A = counterexample();
+        Transform Tdd = data_dependent_transform(A, 1);
+        ApproxError e1 = tsvdq_error(A, tsvdq(A, Tdd, 1));
+        CHECK(std::fabs(e1.total - std::sqrt(3.0)) <= 1e-12);
+        CHECK(std::fabs(e1.eckart_young - 1.0) <= 1e-12);
+        CHECK(std::fabs(e1.projection - s2) <= 1e-12);
+        Transform Th = haar_transform(2, 1);
+        TsvdqFactors F = tsvdq(A, Th, 1);
+        ApproxError e2 = tsvdq_error(A, F);
+        CHECK(std::fabs(e2.total - s2) <= 1e-12);
+        CHECK(std::fabs(e2.eckart_young) <= 1e-12);
+        CHECK(std::fabs(e2.projection - s2) <= 1e-12);
+        // test_metrics.cpp:19-24
+        CHECK(std::fabs(relative_error(A, tsvdq_reconstruct(F)) - s2 / 2) <= 1e-12);
+        CHECK(std::fabs(tsvdq_relative_error(A, F) - s2 / 2) <= 1e-12);
+        check_throws<degenerate_input_error>([&] { relative_error(Tensor3(2, 2, 2), A); }, "zero ref");
+    }
+    // test_transforms.cpp:112-121 — projection error
+    CHECK(std::fabs(projection_error(make_tube({2, 4, 6, 8}), haar_transform(4, 2)) - std::sqrt(66.0)) <= 1e-12);
+    // test_decompositions.cpp:27-59 — factor contracts and sigma-form reconstruction
+    {
+        Tensor3 A = seeded(5, 4, 6, 41);
+        Transform T = dct_transform(6, 3);
+        TsvdqFactors F = tsvdq(A, T, 3);
+        CHECK(F.Uhat.size() == 3 && F.Vhat.size() == 3);
+        for (size_t i = 0; i < 3; ++i) {
+            const Matrix& U = F.Uhat[i];
+            CHECK((U.transpose() * U - Matrix::Identity(3, 3)).norm() <= 1e-10 * 3);
+            const Vector& s = F.shat[i];
+            for (Index j = 0; j + 1 < s.size(); ++j) CHECK(s(j) >= s(j + 1));
+        }
+        Tensor3 hat(5, 4, 3);
+        for (Index i = 0; i < 3; ++i) {
+            const auto u = (size_t)i;
+            Matrix US = F.Uhat[u];
+            for (Index j = 0; j < 3; ++j)
+                for (Index r = 0; r < 5; ++r) US(r, j) *= F.shat[u](j);
+            hat.set_slice(i, US * F.Vhat[u].transpose());
+        }
+        Tensor3 recon = tsvdq_reconstruct(F);
+        CHECK(frobenius_norm(mode3_product(hat, T.Q) - recon) <= 1e-12 * frobenius_norm(recon));
+        check_throws<argument_error>([&] { tsvdq(A, T, 0); }, "k=0");
+        check_throws<argument_error>([&] { tsvdq(A, T, 5); }, "k=5");
+    }
+    // test_decompositions.cpp:80-103 — limits
+    {
+        Tensor3 A = seeded(4, 3, 5, 42);
+        Transform full = random_orthogonal_transform(5, 5, 9);
+        TsvdqFactors Ff = tsvdq(A, full, 3);
+        CHECK(frobenius_norm(A - tsvdq_reconstruct(Ff)) <= 1e-10 * frobenius_norm(A));
+        Transform part = random_orthogonal_transform(5, 3, 9);
+        Tensor3 proj = mode3_product(A, part.Q * part.Q.transpose());
+        CHECK(frobenius_norm(proj - tsvdq_reconstruct(tsvdq(A, part, 3))) <= 1e-10 * frobenius_norm(A));
+    }
+    // test_star_products.cpp:90-102 — scale law
+    {
+        Tensor3 A = seeded(2, 2, 4, 8), B = seeded(2, 3, 4, 9);
+        Transform unit = dct_transform(4, 2);
+        Tensor3 base = star_q_product(A, B, StarContext(unit));
+        for (double c : {-2.0, 0.5, 3.0}) {
+            Tensor3 got = star_q_product(A, B, StarContext(custom_transform(unit.Q, c)));
+            CHECK(frobenius_norm(got - c * base) <= 1e-12 * std::fabs(c) * frobenius_norm(base));
+        }
+    }
+    // test_star_products.cpp:185-206 — transpose rule
+    {
+        Tensor3 A = seeded(3, 2, 5, 10), B = seeded(2, 4, 5, 11);
+        StarContext ctx(random_orthogonal_transform(5, 3, 13));
+        Tensor3 lhs = star_q_transpose(star_q_product(A, B, ctx), ctx);
+        Tensor3 rhs = star_q_product(star_q_transpose(B, ctx), star_q_transpose(A, ctx), ctx);
+        CHECK(lhs.n1() == 4 && lhs.n2() == 3);
+        CHECK(frobenius_norm(lhs - rhs) <= 1e-12 * frobenius_norm(lhs));
+    }
+    // test_decompositions.cpp:118-124 — star_q_rank
+    CHECK(star_q_rank(counterexample(), identity_transform(2, 2)) == 2);
+    CHECK(star_q_rank(counterexample(), haar_transform(2, 1)) == 1);
+    CHECK(star_q_rank(Tensor3(3, 3, 4), dct_transform(4, 2)) == 0);
+    // test_matrix_kernels.cpp:11-35 — SVD contract and pins
+    {
+        Matrix A(2, 2);
+        A(0, 0) = s2;
+        SvdResult d = svd(A);
+        CHECK(std::fabs(d.s(0) - s2) <= 1e-14 * s2 && std::fabs(d.s(1)) <= 1e-14);
+        SvdResult di = svd(Matrix::Identity(3, 3));
+        for (Index j = 0; j < 3; ++j) CHECK(std::fabs(di.s(j) - 1.0) <= 1e-14);
+        check_throws<argument_error>([&] { truncated_svd(A, 3); }, "truncated k");
+        Matrix Q = orthonormalize(Matrix::Identity(4, 2) + 0.1 * Matrix::Identity(4, 2));
+        CHECK((Q.transpose() * Q - Matrix::Identity(2, 2)).norm() <= 1e-12);
+    }
+    // errors: argument / shape / degenerate
+    check_throws<argument_error>([&] { identity_transform(4, 9); }, "p > n3");
+    check_throws<argument_error>([&] { haar_transform(3, 2); }, "haar n3");
+    check_throws<shape_error>([&] { Tensor3(0, 3, 5); }, "extent");
+    check_throws<degenerate_input_error>([&] { custom_transform(Matrix(4, 2)); }, "stiefel");
+    std::printf("%d/%d checks passed\n", g_checks - g_fail, g_checks);
+    return g_fail ? 1 : 0;
+}
