@@ -156,6 +156,28 @@ int ppc_tsvdq_relative_error(const double* A, int64_t n1, int64_t n2, int64_t n3
                              const double* Q, int64_t p, int64_t k,
                              double* re, int loc);
 
+/* ---- shard-level building blocks (multi-GPU driver, dist.py) ------------ */
+/* Deterministic Gram plan for a tube matrix of N rows and n3 columns: the
+ * number of row chunks (a power of two) and the chunk length. Depends on
+ * (N, n3) only, so a pixel-sharded run reproduces the 1-GPU sums bitwise. */
+int ppc_gram_plan(int64_t N, int64_t n3, int64_t* chunks, int64_t* chunk);
+/* Partial Grams T_c^T T_c of `nchunks` consecutive chunks of `chunk` rows of
+ * T (rows x n3, leading dimension ldT): parts is nchunks x n3 x n3. */
+int ppc_gram_partials(const double* T, int64_t ldT, int64_t rows, int64_t n3, int64_t chunk,
+                      int64_t nchunks, double* parts, int loc);
+/* parts[0] = fixed pairwise tree sum of nparts arrays of `elems` doubles. */
+int ppc_tree_reduce(double* parts, int64_t nparts, int64_t elems, int loc);
+/* Top-p eigenvectors Q (n x p, sign rule) and sigma = sqrt(lambda) (nullable)
+ * of the symmetric PSD Gram G (n x n): the tail of data_dependent_transform. */
+int ppc_sym_eig_top(const double* G, int64_t n, int64_t p, double* Q, double* sigma, int loc);
+/* {sum (A - recon)^2, sum A^2} over a lateral block of pixels: A_blk is the
+ * n1 x nj x n3 block of columns [j0, j0+nj) (leading dims n1 and ldA = n1*n2
+ * between frontal slices), U (n1,k,p), S (k,p), V (n2,k,p) full factors. */
+int ppc_recon_residual_block(const double* A_blk, int64_t n1, int64_t nj, int64_t n3,
+                             int64_t ldA, const double* U, const double* S, const double* V,
+                             int64_t n2, int64_t j0, const double* Q, int64_t p, int64_t k,
+                             double* sums, int loc);
+
 /* The `projprod compress --method tsvdq --transform data` pipeline
  * (tools/main.cpp:186-283: data_dependent_transform -> tsvdq ->
  * tsvdq_reconstruct -> relative_error) as one call: A is staged once, the

@@ -67,6 +67,11 @@ def lib() -> C.CDLL:
         "ppc_tsvdq_error": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, vp, i64, i64, pd, pd, pd, C.c_int]),
         "ppc_relative_error": (C.c_int, [vp, vp, i64, pd, C.c_int]),
         "ppc_tsvdq_relative_error": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, vp, i64, i64, pd, C.c_int]),
+        "ppc_gram_plan": (C.c_int, [i64, i64, C.POINTER(i64), C.POINTER(i64)]),
+        "ppc_gram_partials": (C.c_int, [vp, i64, i64, i64, i64, i64, vp, C.c_int]),
+        "ppc_tree_reduce": (C.c_int, [vp, i64, i64, C.c_int]),
+        "ppc_sym_eig_top": (C.c_int, [vp, i64, i64, vp, vp, C.c_int]),
+        "ppc_recon_residual_block": (C.c_int, [vp, i64, i64, i64, i64, vp, vp, vp, i64, i64, vp, i64, i64, pd, C.c_int]),
         "ppc_tsvdq_compress": (C.c_int, [vp, i64, i64, i64, i64, i64, vp, vp, vp, vp, vp, pd, C.c_int]),
     }
     for name, (res, args) in sig.items():

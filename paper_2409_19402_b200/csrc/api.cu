@@ -10,6 +10,7 @@
 #include "jacobi.cuh"
 #include "kernels.cuh"
 #include "engine.h"
+#include "slice_svd.cuh"
 
 using namespace ppc;
 
@@ -244,6 +245,79 @@ int ppc_tsvdq_relative_error(const double* A, int64_t n1, int64_t n2, int64_t n3
         const auto r = recon_residual(a.d, n1, n2, n3, u.d, sv.d, v.d, q.d, p, k, s);
         if (r[1] == 0.0) fail(PPC_DEGENERATE, "relative_error: reference tensor is zero");
         *re = std::sqrt(r[0]) / std::sqrt(r[1]);
+    });
+}
+
+int ppc_gram_plan(int64_t N, int64_t n3, int64_t* chunks, int64_t* chunk) {
+    return guarded([&] {
+        if (N < 1 || n3 < 1) fail(PPC_SHAPE, "gram_plan: extents must be positive");
+        const GramPlan g = gram_plan(N, n3);
+        *chunks = g.chunks;
+        *chunk = g.chunk;
+    });
+}
+
+int ppc_gram_partials(const double* T, int64_t ldT, int64_t rows, int64_t n3, int64_t chunk,
+                      int64_t nchunks, double* parts, int loc) {
+    return guarded([&] {
+        validate_loc(loc);
+        if (rows < 1 || n3 < 1 || ldT < rows || chunk < 1 || nchunks < 1)
+            fail(PPC_SHAPE, "gram_partials: bad extents");
+        if (chunk % 16) fail(PPC_ARGUMENT, "gram_partials: chunk must be a multiple of 16");
+        cudaStream_t s = stream();
+        In t(T, ldT * (n3 - 1) + rows, loc);
+        Out o(parts, nchunks * n3 * n3, loc);
+        gram_chunks(t.d, ldT, rows, n3, chunk, nchunks, o.d, s);
+        o.finish();
+        if (loc == PPC_HOST) PPC_CUDA_CHECK(cudaStreamSynchronize(s));
+    });
+}
+
+int ppc_tree_reduce(double* parts, int64_t nparts, int64_t elems, int loc) {
+    return guarded([&] {
+        validate_loc(loc);
+        if (nparts < 1 || elems < 1) fail(PPC_SHAPE, "tree_reduce: bad extents");
+        cudaStream_t s = stream();
+        In in(parts, nparts * elems, loc);
+        double* d = const_cast<double*>(in.d);
+        tree_reduce(d, nparts, elems, s);
+        if (loc == PPC_HOST) {
+            PPC_CUDA_CHECK(cudaMemcpyAsync(parts, d, sizeof(double) * elems, cudaMemcpyDeviceToHost, s));
+            PPC_CUDA_CHECK(cudaStreamSynchronize(s));
+        }
+    });
+}
+
+int ppc_sym_eig_top(const double* G, int64_t n, int64_t p, double* Q, double* sigma, int loc) {
+    return guarded([&] {
+        validate_loc(loc);
+        check_transform(n, p);
+        cudaStream_t s = stream();
+        In g(G, n * n, loc);
+        Out q(Q, n * p, loc), sg(sigma, sigma ? p : 0, loc);
+        eig_to_basis(g.d, n, p, q.d, sigma ? sg.d : nullptr, s);
+        q.finish();
+        if (sigma) sg.finish();
+        if (loc == PPC_HOST) PPC_CUDA_CHECK(cudaStreamSynchronize(s));
+    });
+}
+
+int ppc_recon_residual_block(const double* A_blk, int64_t n1, int64_t nj, int64_t n3, int64_t ldA,
+                             const double* U, const double* S, const double* V, int64_t n2,
+                             int64_t j0, const double* Q, int64_t p, int64_t k, double* sums,
+                             int loc) {
+    return guarded([&] {
+        validate_loc(loc);
+        check_tensor(n1, nj, n3);
+        check_transform(n3, p);
+        if (j0 < 0 || j0 + nj > n2 || ldA < n1 * nj) fail(PPC_BOUNDS, "recon_residual_block: block outside the tensor");
+        if (!sums) fail(PPC_ARGUMENT, "null output");
+        cudaStream_t s = stream();
+        In a(A_blk, ldA * (n3 - 1) + n1 * nj, loc), u(U, n1 * k * p, loc), sv(S, k * p, loc),
+            v(V, n2 * k * p, loc), q(Q, n3 * p, loc);
+        const auto r = recon_residual_block(a.d, n1, nj, n3, ldA, u.d, sv.d, v.d, n2, j0, q.d, p, k, s);
+        sums[0] = r[0];
+        sums[1] = r[1];
     });
 }
 

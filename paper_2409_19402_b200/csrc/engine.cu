@@ -137,6 +137,40 @@ std::array<double, 2> recon_residual(const double* A, int64_t n1, int64_t n2, in
     return residual_sums(d, A, N, 0, s);
 }
 
+std::array<double, 2> recon_residual_block(const double* A_blk, int64_t n1, int64_t nj, int64_t n3,
+                                           int64_t ldA, const double* U, const double* S,
+                                           const double* V, int64_t n2, int64_t j0,
+                                           const double* Q, int64_t p, int64_t k, cudaStream_t s) {
+    // Chat_i restricted to columns [j0, j0+nj): (U_i S_i) V_i[j0:j0+nj, :]^T
+    const int64_t Nb = n1 * nj;
+    StageTimer tm("recon_residual", s, 2.0 * p * Nb * k + 2.0 * Nb * p * n3, 8.0 * Nb * (p + n3));
+    DeviceBuffer us(sizeof(double) * n1 * k * p), ch(sizeof(double) * Nb * p);
+    launch_scale_columns(U, S, us.d(), n1, k, p, s);
+    {
+        GemmDesc d;
+        d.M = n1; d.N = nj; d.K = k; d.batch = p;
+        d.A = us.d(); d.lda = n1; d.strideA = n1 * k;
+        d.B = V + j0; d.ldb = n2; d.strideB = n2 * k; d.b_nmajor = true;
+        d.C = ch.d(); d.ldc = n1; d.strideC = Nb;
+        gemm(d, s);
+    }
+    // The block's tube matrix: row i + (j-j0)*n1 is contiguous inside each
+    // frontal slice (lateral columns j0.. are adjacent), column stride ldA.
+    GemmDesc d;
+    d.M = Nb; d.N = n3; d.K = p;
+    d.A = ch.d(); d.lda = Nb;
+    d.B = Q; d.ldb = n3; d.b_nmajor = true;
+    const int64_t ctas = gemm_residual_ctas(d);
+    DeviceBuffer part(sizeof(double) * 2 * (ctas + 1));
+    gemm_residual(d, A_blk, ldA, 0, part.d(), s);
+    double* fin = part.d() + 2 * ctas;
+    launch_reduce_pairs(part.d(), ctas, fin, s);
+    std::array<double, 2> out{};
+    PPC_CUDA_CHECK(cudaMemcpyAsync(out.data(), fin, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    PPC_CUDA_CHECK(cudaStreamSynchronize(s));
+    return out;
+}
+
 void tsvdq(const double* A, int64_t n1, int64_t n2, int64_t n3, const double* Q, int64_t p,
            int64_t k, double* U, double* S, double* V, cudaStream_t s) {
     const int64_t N = n1 * n2;

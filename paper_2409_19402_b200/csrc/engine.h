@@ -37,6 +37,16 @@ void slice_svd(const double* A, int64_t m, int64_t n, int64_t stride, int64_t ba
 void gram(const double* T, int64_t N, int64_t n3, double* G, cudaStream_t s);
 // Top-p eigenpairs of a symmetric PSD n x n matrix G: Q (n x p), lambda (p).
 void sym_eig_top(const double* G, int64_t n, int64_t p, double* Q, double* lambda, cudaStream_t s);
+// Partial Grams of nchunks consecutive row chunks (T rows x n3, leading dim ldT).
+void gram_chunks(const double* T, int64_t ldT, int64_t rows, int64_t n3, int64_t chunk,
+                 int64_t nchunks, double* parts, cudaStream_t s);
+// Eigensolve tail of data_q: Q (sign rule) and sigma from the Gram G.
+void eig_to_basis(const double* G, int64_t n3, int64_t p, double* Q, double* sigma, cudaStream_t s);
+// Residual sums over a lateral pixel block [j0, j0+nj) (A_blk leading dims n1, ldA).
+std::array<double, 2> recon_residual_block(const double* A_blk, int64_t n1, int64_t nj, int64_t n3,
+                                           int64_t ldA, const double* U, const double* S,
+                                           const double* V, int64_t n2, int64_t j0,
+                                           const double* Q, int64_t p, int64_t k, cudaStream_t s);
 // transforms.cpp:97-115 on the device. Returns completed_basis.
 bool data_q(const double* T, int64_t N, int64_t n3, int64_t p, double* Q, double* sigma,
             cudaStream_t s);

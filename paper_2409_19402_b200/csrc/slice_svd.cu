@@ -34,14 +34,14 @@ __global__ void tree_add_kernel(double* parts, int64_t nparts, int64_t elems, in
 // Tb = T re-laid as consecutive blocks of KB rows: block kb is the KB x n3
 // column-major matrix of rows [kb*KB, kb*KB + KB) (zero-padded at the end).
 __global__ void block_rows_kernel(const double* __restrict__ T, double* __restrict__ Tb, int64_t N,
-                                  int64_t n3, int kshift, int64_t total) {
+                                  int64_t ldT, int64_t n3, int kshift, int64_t total) {
     const int64_t KB = 1LL << kshift;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += stride) {
         const int64_t kb = e / (KB * n3), rem = e - kb * KB * n3;
         const int64_t a = rem >> kshift, ii = rem & (KB - 1);
         const int64_t i = (kb << kshift) + ii;
-        Tb[e] = i < N ? T[i + a * N] : 0.0;
+        Tb[e] = i < N ? T[i + a * ldT] : 0.0;
     }
 }
 
@@ -96,33 +96,40 @@ void tree_reduce(double* parts, int64_t nparts, int64_t elems, cudaStream_t s) {
     }
 }
 
-void gram(const double* T, int64_t N, int64_t n3, double* G, cudaStream_t s) {
-    StageTimer tm("gram_syrk", s, (double)N * n3 * n3, 8.0 * N * n3);
-    const GramPlan g = gram_plan(N, n3);
+// Partial Grams of `nchunks` consecutive chunks of `chunk` rows of T (rows x
+// n3, leading dimension ldT) into parts (nchunks x n3 x n3).
+void gram_chunks(const double* T, int64_t ldT, int64_t rows, int64_t n3, int64_t chunk,
+                 int64_t nchunks, double* parts, cudaStream_t s) {
     // Large tube matrices: each SYRK pipeline stage would touch one 2 MB page
-    // per column (columns are N*8 bytes apart), thrashing the TLB. Re-lay T
+    // per column (columns are ldT*8 bytes apart), thrashing the TLB. Re-lay T
     // into 2048-row blocks first (one extra HBM pass); same summation order.
-    const int kshift = (N >= (1LL << 20) && n3 >= 64) ? 11 : 0;
+    const int kshift = (ldT >= (1LL << 20) && n3 >= 64) ? 11 : 0;
     DeviceBuffer tb;
     const double* src = T;
-    int64_t ld = N;
+    int64_t ld = ldT;
     if (kshift) {
-        StageTimer tr("gram_relayout", s, 0.0, 16.0 * N * n3);
-        const int64_t KB = 1LL << kshift, nb = (N + KB - 1) / KB;
+        StageTimer tr("gram_relayout", s, 0.0, 16.0 * rows * n3);
+        const int64_t KB = 1LL << kshift, nb = (rows + KB - 1) / KB;
         tb = DeviceBuffer(sizeof(double) * nb * KB * n3);
         const int64_t total = nb * KB * n3;
-        block_rows_kernel<<<148 * 16, 256, 0, s>>>(T, tb.d(), N, n3, kshift, total);
+        block_rows_kernel<<<148 * 16, 256, 0, s>>>(T, tb.d(), rows, ldT, n3, kshift, total);
         count_launch();
         check_launch("block_rows");
         src = tb.d();
         ld = KB;
     }
+    gram_partials(src, ld, rows, n3, chunk, nchunks, parts, s, kshift);
+}
+
+void gram(const double* T, int64_t N, int64_t n3, double* G, cudaStream_t s) {
+    StageTimer tm("gram_syrk", s, (double)N * n3 * n3, 8.0 * N * n3);
+    const GramPlan g = gram_plan(N, n3);
     if (g.chunks == 1) {
-        gram_partials(src, ld, N, n3, g.chunk, 1, G, s, kshift);
+        gram_chunks(T, N, N, n3, g.chunk, 1, G, s);
         return;
     }
     DeviceBuffer parts(sizeof(double) * g.chunks * n3 * n3);
-    gram_partials(src, ld, N, n3, g.chunk, g.chunks, parts.d(), s, kshift);
+    gram_chunks(T, N, N, n3, g.chunk, g.chunks, parts.d(), s);
     tree_reduce(parts.d(), g.chunks, n3 * n3, s);
     PPC_CUDA_CHECK(cudaMemcpyAsync(G, parts.d(), sizeof(double) * n3 * n3, cudaMemcpyDeviceToDevice, s));
 }
@@ -137,17 +144,11 @@ void sym_eig_top(const double* G, int64_t n, int64_t p, double* Q, double* lambd
     subspace_eig_top(G, n, 1, p, Q, lambda, s, false);
 }
 
-bool data_q(const double* T, int64_t N, int64_t n3, int64_t p, double* Q, double* sigma,
-            cudaStream_t s) {
-    DeviceBuffer G(sizeof(double) * n3 * n3), lam(sizeof(double) * n3);
-    gram(T, N, n3, G.d(), s);
-    const int64_t avail = std::min(n3, N);
-    // When p > min(n3, N) the unfolding has only `avail` singular vectors;
-    // the eigenvectors of G for its zero eigenvalues complete the basis
-    // (transforms.cpp:104-111 pads with an orthonormal completion).
+void eig_to_basis(const double* G, int64_t n3, int64_t p, double* Q, double* sigma, cudaStream_t s) {
+    DeviceBuffer lam(sizeof(double) * n3);
     {
         StageTimer tm("eig_q", s);
-        sym_eig_top(G.d(), n3, p, Q, lam.d(), s);
+        sym_eig_top(G, n3, p, Q, lam.d(), s);
     }
     sign_rule(Q, n3, p, 1, nullptr, 0, s);  // fix_svd_signs on U3 (matrix_kernels.cpp:35)
     if (sigma) {
@@ -155,7 +156,17 @@ bool data_q(const double* T, int64_t N, int64_t n3, int64_t p, double* Q, double
         count_launch();
         check_launch("sqrt_clamp");
     }
-    return p > avail;
+}
+
+bool data_q(const double* T, int64_t N, int64_t n3, int64_t p, double* Q, double* sigma,
+            cudaStream_t s) {
+    DeviceBuffer G(sizeof(double) * n3 * n3);
+    gram(T, N, n3, G.d(), s);
+    // When p > min(n3, N) the unfolding has only min(n3, N) singular vectors;
+    // the eigenvectors of G for its zero eigenvalues complete the basis
+    // (transforms.cpp:104-111 pads with an orthonormal completion).
+    eig_to_basis(G.d(), n3, p, Q, sigma, s);
+    return p > std::min(n3, N);
 }
 
 void slice_svd(const double* A, int64_t m, int64_t n, int64_t stride, int64_t batch, int64_t k,

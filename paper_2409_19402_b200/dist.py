@@ -1,0 +1,208 @@
+"""Multi-GPU tSVDQ with a data-driven basis, one process per GPU.
+
+The cfg5 pipeline is sharded as follows:
+
+1. Pixels are sharded by lateral j-blocks. Rank r holds A[:, j0:j1, :] as its own
+   n1 x nj x n3 tensor. Block boundaries are aligned to the Gram plan's row
+   chunks, and the plan depends on (N, n3) only.
+2. Each rank computes the partial Grams of its chunks (DMMA SYRK). It reduces them
+   locally with the fixed pairwise tree; its chunk group is an aligned power of
+   two, so the local result is a subtree. The G subtree roots are all-gathered
+   and the same tree is finished on every rank. The Gram, and therefore Q, is
+   bitwise identical to the 1-GPU run (verify.cpp:452-455 determinism,
+   SURVEY finding 8).
+3. The top-p eigensolve is replicated: deterministic, same Q everywhere.
+4. The forward transform of the local pixels (A_blk x3 Q^T) runs locally.
+5. Â is resharded pixel -> slice by all_to_all_single: each rank gets p/G
+   complete slices.
+6. The slice SVDs run locally, then the factor stacks are all-gathered.
+7. The fused reconstruction residual runs over the local pixel block, then the
+   two scalars are all-reduced.
+
+Compute goes through a backend object. `DeviceBackend` calls the engine's C-ABI
+on CUDA tensors, and collectives use torch.distributed (NCCL on GPUs). The
+CPU tests inject a numpy backend over gloo to check the orchestration.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import torch
+import torch.distributed as dist
+
+from . import _lib
+
+
+def _check(rc):
+    if rc:
+        raise RuntimeError(_lib.lib().ppc_last_error().decode())
+
+
+def _fempty(shape, device):
+    return torch.empty(tuple(reversed(shape)), dtype=torch.float64,
+                       device=device).permute(*reversed(range(len(shape))))
+
+
+def _p(t):
+    return C.c_void_p(t.data_ptr())
+
+
+class DeviceBackend:
+    """The engine's C-ABI on Fortran-laid-out CUDA tensors (loc = PPC_DEVICE)."""
+
+    def __init__(self, device):
+        self.device = torch.device(device)
+        self.L = _lib.lib()
+        _check(self.L.ppc_set_device(self.device.index or 0))
+        _check(self.L.ppc_set_stream(C.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)))
+
+    def gram_plan(self, N, n3):
+        c, ch = C.c_int64(), C.c_int64()
+        _check(self.L.ppc_gram_plan(N, n3, C.byref(c), C.byref(ch)))
+        return c.value, ch.value
+
+    def gram_partials(self, A_blk, rows, n3, chunk, nchunks):
+        parts = torch.empty(nchunks * n3 * n3, dtype=torch.float64, device=self.device)
+        _check(self.L.ppc_gram_partials(_p(A_blk), rows, rows, n3, chunk, nchunks, _p(parts), 1))
+        return parts.view(nchunks, n3 * n3)
+
+    def tree_reduce(self, parts):
+        parts = parts.contiguous()
+        _check(self.L.ppc_tree_reduce(_p(parts), parts.shape[0], parts.shape[1], 1))
+        return parts[0].clone()
+
+    def sym_eig_top(self, G, n3, p):
+        Q = _fempty((n3, p), self.device)
+        sig = torch.empty(p, dtype=torch.float64, device=self.device)
+        _check(self.L.ppc_sym_eig_top(_p(G), n3, p, _p(Q), _p(sig), 1))
+        return Q, sig
+
+    def mode3_fwd(self, A_blk, n1, nj, n3, Q, p):
+        out = _fempty((n1, nj, p), self.device)
+        _check(self.L.ppc_mode3_product(_p(A_blk), n1, nj, n3, _p(Q), p, 1, _p(out), 1))
+        return out
+
+    def svd_slices(self, S_loc, n1, n2, ps, k):
+        U = _fempty((n1, k, ps), self.device)
+        s = _fempty((k, ps), self.device)
+        V = _fempty((n2, k, ps), self.device)
+        _check(self.L.ppc_svd_batched(_p(S_loc), n1, n2, ps, k, _p(U), _p(s), _p(V), 1))
+        return U, s, V
+
+    def recon_block(self, A_blk, n1, nj, n3, U, S, V, n2, j0, Q, p, k):
+        sums = (C.c_double * 2)()
+        _check(self.L.ppc_recon_residual_block(_p(A_blk), n1, nj, n3, n1 * nj, _p(U), _p(S), _p(V),
+                                               n2, j0, _p(Q), p, k, sums, 1))
+        return float(sums[0]), float(sums[1])
+
+
+@dataclass
+class ShardPlan:
+    world: int
+    rank: int
+    n1: int
+    n2: int
+    n3: int
+    p: int
+    chunks: int
+    chunk: int
+
+    @property
+    def cols_per_rank(self):
+        return self.n2 // self.world
+
+    @property
+    def j0(self):
+        return self.rank * self.cols_per_rank
+
+    @property
+    def nj(self):
+        return self.cols_per_rank
+
+    @property
+    def slices_per_rank(self):
+        return self.p // self.world
+
+    @property
+    def chunks_per_rank(self):
+        return self.chunks // self.world
+
+
+def make_plan(n1, n2, n3, p, world, rank, backend) -> ShardPlan:
+    chunks, chunk = backend.gram_plan(n1 * n2, n3)
+    if world & (world - 1):
+        raise ValueError("world size must be a power of two (pairwise Gram tree)")
+    if chunks % world or n2 % world or p % world:
+        raise ValueError(f"cannot shard: chunks={chunks}, n2={n2}, p={p} vs world={world}")
+    if (n2 // world) * n1 != (chunks // world) * chunk:
+        raise ValueError("lateral blocks do not align with the Gram chunks")
+    return ShardPlan(world, rank, n1, n2, n3, p, chunks, chunk)
+
+
+def _tree_finish(roots):
+    """Finish the pairwise tree over the G subtree roots (rank order), as the
+    engine's tree_reduce does over chunks: width 1, 2, 4, ..."""
+    roots = list(roots)
+    w = 1
+    while w < len(roots):
+        for a in range(0, len(roots), 2 * w):
+            if a + w < len(roots):
+                roots[a] = roots[a] + roots[a + w]
+        w *= 2
+    return roots[0]
+
+
+def sharded_compress(A_blk, plan: ShardPlan, k: int, backend, group=None):
+    """Runs the sharded pipeline on this rank's lateral block A_blk
+    (n1 x nj x n3, Fortran layout). Returns (Q, U, S, V, relative_error) with
+    the full factor stacks on every rank."""
+    n1, n2, n3, p, nj, G = plan.n1, plan.n2, plan.n3, plan.p, plan.nj, plan.world
+    rows = n1 * nj
+    # 1-2. partial Grams of the local chunks, local subtree, global finish
+    parts = backend.gram_partials(A_blk, rows, n3, plan.chunk, plan.chunks_per_rank)
+    root = backend.tree_reduce(parts)
+    roots = [torch.empty_like(root) for _ in range(G)]
+    if G > 1:
+        dist.all_gather(roots, root, group=group)
+    else:
+        roots = [root]
+    Gm = _tree_finish(roots)
+    # 3. replicated eigensolve
+    Q, _ = backend.sym_eig_top(Gm, n3, p)
+    # 4. local forward transform
+    Ah = backend.mode3_fwd(A_blk, n1, nj, n3, Q, p)  # (n1, nj, p) Fortran
+    # 5. reshard pixel -> slice: chunk for rank s = my block of its slices
+    ps = plan.slices_per_rank
+    send = Ah.permute(2, 1, 0).contiguous()  # (p, nj, n1) C-order == Fortran (n1, nj, p)
+    send = send.view(G, ps * nj * n1)
+    recv = torch.empty_like(send)
+    if G > 1:
+        dist.all_to_all_single(recv, send, group=group)
+    else:
+        recv.copy_(send)
+    # recv[r] = rank r's lateral block (columns j0_r..) of my ps slices
+    blocks = recv.view(G, ps, nj, n1)                 # [r][slice][j][i]
+    full = blocks.permute(1, 0, 2, 3).reshape(ps, n2, n1)  # [slice][j][i], j ascending by rank
+    S_loc = full.permute(2, 1, 0)                     # (n1, n2, ps) Fortran view
+    # 6. slice SVDs, all-gather the factor stacks
+    U, s, V = backend.svd_slices(S_loc, n1, n2, ps, k)
+    Uc = U.permute(2, 1, 0).contiguous()  # (ps, k, n1)
+    sc = s.permute(1, 0).contiguous()     # (ps, k)
+    Vc = V.permute(2, 1, 0).contiguous()  # (ps, k, n2)
+    if G > 1:
+        Ug = [torch.empty_like(Uc) for _ in range(G)]
+        sg = [torch.empty_like(sc) for _ in range(G)]
+        Vg = [torch.empty_like(Vc) for _ in range(G)]
+        dist.all_gather(Ug, Uc, group=group)
+        dist.all_gather(sg, sc, group=group)
+        dist.all_gather(Vg, Vc, group=group)
+        Uc, sc, Vc = torch.cat(Ug), torch.cat(sg), torch.cat(Vg)
+    Uf, Sf, Vf = Uc.permute(2, 1, 0), sc.permute(1, 0), Vc.permute(2, 1, 0)  # (n1,k,p) (k,p) (n2,k,p)
+    # 7. fused residual on the local pixel block, all-reduce the sums
+    sd, sa = backend.recon_block(A_blk, n1, nj, n3, Uf, Sf, Vf, n2, plan.j0, Q, p, k)
+    t = torch.tensor([sd, sa], dtype=torch.float64, device=Ah.device)
+    if G > 1:
+        dist.all_reduce(t, group=group)
+    re = float((t[0].sqrt() / t[1].sqrt()).item())
+    return Q, Uf, Sf, Vf, re

@@ -1,0 +1,159 @@
+"""World-size-2 `gloo` tests of the sharded tSVDQ driver (paper_2409_19402_b200/dist.py)
+on CPU, with a numpy stand-in for the engine's per-rank kernels (test-only).
+
+They check the orchestration:
+  * the lateral blocks align with the Gram chunks;
+  * the pairwise-tree finish over the rank roots reproduces the 1-process
+    Gram bitwise;
+  * the pixel -> slice reshard (all_to_all_single) assembles the right slices;
+  * the factor all-gather and the all-reduced residual give the same Q,
+    factors and relative error as the 1-process run.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2409_19402_b200 import dist as pdist
+
+
+def _f(t):
+    """numpy view of a Fortran-laid-out CPU tensor (no copy when possible)."""
+    return np.asfortranarray(t.numpy()) if t.is_contiguous() else t.contiguous().numpy()
+
+
+def _ft(a):
+    a = np.asfortranarray(a)
+    return torch.from_numpy(np.ascontiguousarray(a.transpose())).permute(*reversed(range(a.ndim)))
+
+
+def _sign_rule(U, V):
+    for j in range(U.shape[1]):
+        i = int(np.argmax(np.abs(U[:, j])))
+        if U[i, j] < 0:
+            U[:, j] *= -1
+            V[:, j] *= -1
+
+
+class NumpyBackend:
+    """Same contract as DeviceBackend, computed with numpy on the host."""
+
+    def gram_plan(self, N, n3):
+        # the engine's own plan (host-only C-ABI call, no GPU needed)
+        import ctypes as C
+        from paper_2409_19402_b200 import _lib
+        c, ch = C.c_int64(), C.c_int64()
+        assert _lib.lib().ppc_gram_plan(N, n3, C.byref(c), C.byref(ch)) == 0
+        return c.value, ch.value
+
+    def gram_partials(self, A_blk, rows, n3, chunk, nchunks):
+        T = A_blk.permute(2, 1, 0).contiguous().numpy().reshape(n3, rows).T
+        parts = [T[c * chunk:(c + 1) * chunk].T @ T[c * chunk:(c + 1) * chunk] for c in range(nchunks)]
+        return torch.from_numpy(np.stack([p.reshape(-1) for p in parts]))
+
+    def tree_reduce(self, parts):
+        return pdist._tree_finish([parts[i].clone() for i in range(parts.shape[0])])
+
+    def sym_eig_top(self, G, n3, p):
+        w, V = np.linalg.eigh(G.numpy().reshape(n3, n3))
+        order = np.argsort(-w, kind="stable")[:p]
+        Q = V[:, order].copy()
+        _sign_rule(Q, np.zeros_like(Q))
+        return _ft(Q), torch.from_numpy(np.sqrt(np.maximum(w[order], 0)))
+
+    def mode3_fwd(self, A_blk, n1, nj, n3, Q, p):
+        T = A_blk.permute(2, 1, 0).contiguous().numpy().reshape(n3, n1 * nj).T
+        Qn = Q.permute(1, 0).contiguous().numpy().T
+        return _ft((T @ Qn).reshape(n1, nj, p, order="F"))
+
+    def svd_slices(self, S_loc, n1, n2, ps, k):
+        S = S_loc.permute(2, 1, 0).contiguous().numpy().transpose(2, 1, 0)
+        U, s, V = np.zeros((n1, k, ps)), np.zeros((k, ps)), np.zeros((n2, k, ps))
+        for z in range(ps):
+            u, sv, vt = np.linalg.svd(S[:, :, z], full_matrices=False)
+            uu, vv = u[:, :k].copy(), vt[:k].T.copy()
+            _sign_rule(uu, vv)
+            U[:, :, z], s[:, z], V[:, :, z] = uu, sv[:k], vv
+        return _ft(U), _ft(s), _ft(V)
+
+    def recon_block(self, A_blk, n1, nj, n3, U, S, V, n2, j0, Q, p, k):
+        A = A_blk.permute(2, 1, 0).contiguous().numpy().transpose(2, 1, 0)
+        Un = U.permute(2, 1, 0).contiguous().numpy().transpose(2, 1, 0)
+        Sn = S.permute(1, 0).contiguous().numpy().T
+        Vn = V.permute(2, 1, 0).contiguous().numpy().transpose(2, 1, 0)
+        Qn = Q.permute(1, 0).contiguous().numpy().T
+        ch = np.stack([(Un[:, :, i] * Sn[:, i]) @ Vn[j0:j0 + nj, :, i].T for i in range(p)], axis=2)
+        rec = np.einsum("ijl,kl->ijk", ch, Qn)
+        return float(np.sum((A - rec) ** 2)), float(np.sum(A ** 2))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def _tensor(n1, n2, n3, seed=3):
+    rng = np.random.default_rng(seed)
+    r = 3
+    a = np.einsum("ir,jr,kr->ijk", rng.standard_normal((n1, r)), rng.standard_normal((n2, r)),
+                  rng.standard_normal((n3, r))) + 1e-2 * rng.standard_normal((n1, n2, n3))
+    return np.asfortranarray(a)
+
+
+def _run(rank, world, port, shape, p, k, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n1, n2, n3 = shape
+        a = _tensor(n1, n2, n3)
+        be = NumpyBackend()
+        plan = pdist.make_plan(n1, n2, n3, p, world, rank, be)
+        blk = _ft(a[:, plan.j0:plan.j0 + plan.nj, :])
+        Q, U, S, V, re = pdist.sharded_compress(blk, plan, k, be)
+        np.savez(os.path.join(out_dir, f"r{rank}.npz"), Q=Q.permute(1, 0).contiguous().numpy().T,
+                 S=S.permute(1, 0).contiguous().numpy().T, re=re,
+                 U=U.permute(2, 1, 0).contiguous().numpy().transpose(2, 1, 0),
+                 V=V.permute(2, 1, 0).contiguous().numpy().transpose(2, 1, 0))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_sharded_compress_world2_matches_world1(tmp_path):
+    shape, p, k = (16, 64, 24), 4, 3
+    res = {}
+    for world in (1, 2):
+        d = tmp_path / f"w{world}"
+        d.mkdir()
+        mp.spawn(_run, args=(world, _free_port(), shape, p, k, str(d)), nprocs=world, join=True)
+        res[world] = [np.load(d / f"r{r}.npz") for r in range(world)]
+    one = res[1][0]
+    for r in res[2]:
+        assert np.array_equal(r["Q"], one["Q"])          # bitwise: same Gram tree
+        np.testing.assert_allclose(r["S"], one["S"], rtol=1e-12)
+        np.testing.assert_allclose(r["U"], one["U"], atol=1e-10)
+        np.testing.assert_allclose(r["V"], one["V"], atol=1e-10)
+        assert abs(float(r["re"]) - float(one["re"])) <= 1e-13 * float(one["re"])
+    # and the 1-process result is the plain (unsharded) pipeline
+    a = _tensor(*shape)
+    T = a.reshape(-1, shape[2], order="F")
+    w, Vg = np.linalg.eigh(T.T @ T)
+    lam = np.sort(w)[::-1][:p]
+    Qn = one["Q"]
+    np.testing.assert_allclose(np.sum((T @ Qn) ** 2, axis=0), lam, rtol=1e-10)
+
+
+def test_plan_rejects_misaligned_shards():
+    be = NumpyBackend()
+    with pytest.raises(ValueError):
+        pdist.make_plan(16, 64, 24, 4, 3, 0, be)   # world not a power of two
+    with pytest.raises(ValueError):
+        pdist.make_plan(16, 64, 24, 3, 2, 0, be)   # p not divisible

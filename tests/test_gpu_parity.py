@@ -421,3 +421,20 @@ def test_cp_scaled_pipeline(engine, oracle):
     U, S, V = oracle.tsvdq(a, qo, 16)
     reo = oracle.relative_error(a, oracle.tsvdq_reconstruct(U, S, V, qo))
     assert abs(engine.tsvdq_relative_error(a, f) - reo) <= 1e-10 * reo
+
+
+# ------------------------------------------------------------ sharded driver
+def test_dist_driver_single_rank_matches_fused(engine):
+    # dist.py's per-rank path (DeviceBackend, world=1) against ppc_tsvdq_compress
+    import torch
+    from paper_2409_19402_b200 import dist as pdist
+    a = synth.cp_tensor(96, 128, 64, rank=12, noise=1e-3, seed=11)
+    da = engine.to_device(a)
+    f, re = engine.compress_tsvdq(da, 16, 6)
+    be = pdist.DeviceBackend("cuda:0")
+    plan = pdist.make_plan(96, 128, 64, 16, 1, 0, be)
+    Q, U, S, V, re2 = pdist.sharded_compress(da, plan, 6, be)
+    torch.cuda.synchronize()
+    assert np.array_equal(engine.to_host(Q), f.transform.q)  # same Gram tree, same eigensolve
+    np.testing.assert_allclose(engine.to_host(S), engine.to_host(f.s), rtol=1e-12)
+    assert abs(re2 - re) <= 1e-12 * re
