@@ -14,8 +14,9 @@ Workloads (BASELINE.json configs, synthetic inputs of the named shapes):
 One step = one pass of the hot path over one input already resident in HBM
 (`value`); `e2e` repeats it through the C-ABI with pinned HOST buffers, the
 H2D of the inputs and the D2H of the result inside the timed region.
-Under torchrun (N>1) every rank runs its own instance of the workload
-(independent tensors, no data-path collective): weak scaling.
+Under torchrun (N>1) cfg5 is pixel-sharded across the ranks (dist.py; strong
+scaling, one global tensor); the other workloads run one independent instance
+per rank (weak scaling, no data-path collective).
 """
 from __future__ import annotations
 
@@ -311,7 +312,71 @@ class Tsvdq:
                                                   f"tensor of the same distribution (p={p}, k={k}), 1 rep")
 
 
-def make_workload(name):
+class TsvdqSharded:
+    """cfg5 pixel-sharded over the torchrun ranks (paper_2409_19402_b200/dist.py):
+    every rank holds one lateral block; Gram partials -> pairwise tree across
+    ranks (bitwise the 1-GPU Gram) -> replicated eigensolve -> local forward
+    transform -> all_to_all reshard -> slice SVDs -> factor all-gather ->
+    local fused residual -> all-reduce. Strong scaling (total work fixed)."""
+
+    metric, unit = "tsvdq_input_GBps", "GB/s"
+
+    def __init__(self, world, rank, local, n1=2048, n2=2048, n3=1024, p=128, k=32, seed=0):
+        import torch
+        from paper_2409_19402_b200 import dist as pdist, synth
+        self.name = "cfg5"
+        self.torch = torch
+        self.dims = (n1, n2, n3, p, k)
+        self.world = world
+        self.be = pdist.DeviceBackend(f"cuda:{local}")
+        self.plan = pdist.make_plan(n1, n2, n3, p, world, rank, self.be)
+        self.pdist = pdist
+        self.A = synth.cp_block_device(n1, n2, n3, self.plan.j0, self.plan.nj, 50, 1e-3, seed,
+                                       device=f"cuda:{local}")
+        self.in_bytes = 8.0 * n1 * n2 * n3  # the whole tensor (all ranks)
+        self.re = None
+
+    def config(self):
+        n1, n2, n3, p, k = self.dims
+        return {"workload": "cfg5 rank-50 CP + N(0,1e-3^2) noise tSVDQ with data-driven Q, pixel-sharded",
+                "shape": [n1, n2, n3], "p": p, "k": k, "l2": "input > L2",
+                "step": "dist.sharded_compress (Gram tree + NCCL all_gather / all_to_all / all_reduce)"}
+
+    def step(self, L):
+        _, _, _, _, k = self.dims
+        self.be.L.ppc_set_stream(C.c_void_p(self.torch.cuda.current_stream().cuda_stream))
+        *_, self.re = self.pdist.sharded_compress(self.A, self.plan, k, self.be)
+
+    def value(self, sec):
+        return self.in_bytes / sec / 1e9 / self.world  # main() multiplies by world
+
+    def dominant(self, stages):
+        best = max(stages.items(), key=lambda kv: kv[1]["ms"])[0] if stages else "gram_syrk"
+        return best, "tensor"
+
+    def e2e_setup(self):
+        self.hA = flat_host(self.A)
+        n1, n2, n3, p, k = self.dims
+        self.h2d = 8 * n1 * n2 * n3
+        self.d2h = 8 * (n3 * p + (n1 + n2 + 1) * k * p)
+
+    def e2e_step(self, L):
+        torch = self.torch
+        n1, n2, n3, p, k = self.dims
+        blk = self.torch.empty_like(self.A.permute(2, 1, 0)).reshape(-1)
+        blk.copy_(self.hA, non_blocking=True)
+        A = blk.view(n3, self.plan.nj, n1).permute(2, 1, 0)
+        Q, U, S, V, _ = self.pdist.sharded_compress(A, self.plan, k, self.be)
+        for t in (Q, U, S, V):
+            t.cpu()
+
+    def cpu_sample(self, ppo, threads):
+        return Tsvdq.cpu_sample(self, ppo, threads)
+
+
+def make_workload(name, world=1, rank=0, local=0):
+    if name == "cfg5" and world > 1:
+        return TsvdqSharded(world, rank, local)
     if name == "cfg4":
         return StarQ()
     dims = {"cfg5": (2048, 2048, 1024, 128, 32), "cfg3": (512, 512, 224, 32, 16),
@@ -403,7 +468,7 @@ def main():
     L.ppc_set_stream(C.c_void_p(stream.cuda_stream))
 
     peaks = load_peaks()
-    wl = make_workload(args.workload)
+    wl = make_workload(args.workload, world, rank, local)
     torch.cuda.synchronize()
 
     for _ in range(args.warmup):
@@ -487,10 +552,12 @@ def main():
 
     if rank == 0:
         cfg = wl.config()
-        cfg["parallelism"] = f"replicas{world}" if world > 1 else "single"
+        sharded = isinstance(wl, TsvdqSharded)
+        cfg["parallelism"] = (f"pixel-sharded dp{world}" if sharded else
+                              (f"replicas{world}" if world > 1 else "single"))
         line = {"metric": wl.metric, "value": value, "unit": wl.unit, "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "higher_is_better": True, "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f64",
                 "data": "synthetic", "config": cfg, "roofline": roof, "cpu_baseline": cpu,
                 "e2e": e2e, "gpu_launches": launches, "clocks": clk, "stages": stage_summary}
         if getattr(wl, "re", None) is not None:

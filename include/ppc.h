@@ -59,8 +59,9 @@ int ppc_version(void);
  * mirroring PROJPROD_THREADS (parallel.cpp:13-27). */
 int ppc_device_count(void);
 int ppc_set_device(int device);
-/* Stream (cudaStream_t) used by this thread's subsequent calls; NULL = the
- * library's own non-blocking stream. */
+/* Stream (cudaStream_t) used by this thread's subsequent calls. NULL selects
+ * the legacy default stream (what torch reports as stream 0). Until the first
+ * call the library uses its own non-blocking stream. */
 int ppc_set_stream(void* stream);
 void* ppc_get_stream(void);
 int ppc_synchronize(void);

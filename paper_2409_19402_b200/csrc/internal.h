@@ -34,6 +34,7 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
 struct Context {
     int device = -1;
     cudaStream_t stream = nullptr;      // user stream (ppc_set_stream) or own
+    bool stream_set = false;            // set explicitly (NULL = legacy default stream)
     cudaStream_t own_stream = nullptr;  // created lazily per device
     int sms = 148;
     int64_t launches = 0;

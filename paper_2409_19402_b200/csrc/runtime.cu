@@ -71,7 +71,7 @@ Context& ctx() {
 
 cudaStream_t stream() {
     Context& c = ctx();
-    if (c.stream) return c.stream;
+    if (c.stream_set) return c.stream;  // may be the legacy default stream (0)
     if (!c.own_stream) PPC_CUDA_CHECK(cudaStreamCreateWithFlags(&c.own_stream, cudaStreamNonBlocking));
     return c.own_stream;
 }
@@ -171,8 +171,11 @@ int ppc_set_device(int device) {
     try {
         int n = ppc::visible_devices();
         if (device < 0 || device >= n) ppc::fail(PPC_ARGUMENT, "ppc_set_device: no such device");
-        ppc::t_ctx.stream = nullptr;
-        ppc::t_ctx.own_stream = nullptr;
+        if (ppc::t_ctx.device != device) {
+            ppc::t_ctx.stream = nullptr;
+            ppc::t_ctx.stream_set = false;
+            ppc::t_ctx.own_stream = nullptr;
+        }
         ppc::init_device(device);
         return 0;
     } catch (const ppc::Error& e) {
@@ -184,6 +187,7 @@ int ppc_set_device(int device) {
 int ppc_set_stream(void* s) {
     try {
         ppc::ctx().stream = static_cast<cudaStream_t>(s);
+        ppc::ctx().stream_set = true;
         return 0;
     } catch (const ppc::Error& e) {
         ppc::set_error(e.what());

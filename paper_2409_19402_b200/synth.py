@@ -125,3 +125,31 @@ def cp_tensor_device(n1=2048, n2=2048, n3=1024, rank=50, noise=1e-3, seed=0, dev
             slab.add_(torch.randn(slab.shape, dtype=torch.float64, device=device, generator=g),
                       alpha=noise)
     return flat.view(n3, n2, n1).permute(2, 1, 0)
+
+
+def cp_block_device(n1, n2, n3, j0, nj, rank=50, noise=1e-3, seed=0, device="cuda"):
+    """Lateral block A[:, j0:j0+nj, :] of the cfg5 CP tensor for one rank of a
+    pixel-sharded run: the CP factors are common (same seed on every rank);
+    the noise of the block is drawn from a (seed, j0) stream."""
+    import torch
+    g = torch.Generator(device=device)
+    g.manual_seed(int(seed) * 7919 + 5)
+    f1 = torch.randn(n1, rank, dtype=torch.float64, device=device, generator=g)
+    f2 = torch.randn(n2, rank, dtype=torch.float64, device=device, generator=g)
+    f3 = torch.randn(n3, rank, dtype=torch.float64, device=device, generator=g)
+    f2 = f2[j0:j0 + nj]
+    kr = (f1[:, None, :] * f2[None, :, :]).permute(1, 0, 2).reshape(n1 * nj, rank)
+    Nb = n1 * nj
+    flat = torch.empty(Nb * n3, dtype=torch.float64, device=device)
+    tubes = flat.view(n3, Nb)
+    gn = torch.Generator(device=device)
+    gn.manual_seed(int(seed) * 1000003 + 17 + int(j0))
+    step = max(1, (1 << 28) // Nb)
+    for k0 in range(0, n3, step):
+        k1 = min(n3, k0 + step)
+        slab = tubes[k0:k1]
+        torch.matmul(f3[k0:k1], kr.T, out=slab)
+        if noise:
+            slab.add_(torch.randn(slab.shape, dtype=torch.float64, device=device, generator=gn),
+                      alpha=noise)
+    return flat.view(n3, nj, n1).permute(2, 1, 0)
