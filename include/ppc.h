@@ -72,6 +72,10 @@ int64_t ppc_launch_count(int reset);
  * (off by default). ppc_timing_report writes a JSON object
  * {"stage": {"ms", "n", "flops", "bytes"}} (algorithmic flops/bytes). */
 int ppc_timing_enable(int on);
+/* GEMM kernel selection: 0 = automatic (warp-specialized TMA kernel where
+ * eligible), 1 = always the cp.async kernel. Both accumulate every output in
+ * the same order, so results are bitwise identical (used by the tests). */
+int ppc_set_gemm_path(int mode);
 int ppc_timing_report(char* buf, int64_t cap, int reset);
 
 /* ---- L3 kernels (tensor.hpp, matrix_kernels.hpp) ------------------------ */

@@ -277,7 +277,12 @@ struct GemmDesc {
     int kshift = 0;      // k-blocked K-major operands (see GemmParams)
     int64_t kbstride = 0;
     const int* zmap = nullptr;  // device array of `batch` batch indices (nullable)
+    bool allow_ws = true;       // may use the warp-specialized TMA kernel
 };
+
+// Warp-specialized persistent TMA kernel (gemm_ws.cu); false = not eligible.
+bool gemm_ws(const GemmDesc& d, int epi, const double* X, int64_t ldx, int64_t strideX, double* partials,
+             int64_t* ctas_out, cudaStream_t s);
 
 // D = alpha op(A) op(B) + beta Cin (EPI_STORE).
 void gemm(const GemmDesc& d, cudaStream_t s);

@@ -1,0 +1,279 @@
+// Warp-specialized, persistent FP64 DMMA GEMM with TMA staging (sm_100a).
+//
+// Same math and shared-memory layout as dmma_gemm.cuh (32-byte interleaved
+// quads -> conflict-free DMMA fragment reads), but:
+//   - one producer warp issues cp.async.bulk.tensor (TMA) loads into an
+//     S-stage ring guarded by mbarriers (full: tx-count; empty: one arrive
+//     per consumer warp); consumers never __syncthreads in the main loop;
+//   - CTAs are persistent (grid = #SMs) over a static tile schedule, so the
+//     producer streams the next tile's operands while consumers run the
+//     epilogue of the current one;
+//   - the interleaved layout is expressed as a 5-D tensor map:
+//       d0 = 4 (quad), d1 = other dim, d2 = contiguous-dim quads (within a
+//       block), d3 = contiguous-dim blocks (k-blocked Gram layout), d4 = batch.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "dmma_gemm.cuh"
+
+namespace ppc {
+
+struct WsParams {
+    int64_t M, N, K;
+    int64_t batch;
+    int64_t mtiles, ntiles, tiles_per_batch, total_tiles;  // tile schedule
+    int tri;     // symmetric: upper tiles only (mtiles == ntiles), mirrored store
+    int nfast;   // raster
+    int64_t kchunk;        // split-K: K range per split (tiles of different splits are distinct work items)
+    int64_t splits;
+    int64_t strideCsplit;
+    double* C; int64_t ldc, strideC;
+    const double* Cin; int64_t ldcin, strideCin;
+    double alpha, beta;
+    const double* X; int64_t ldx, strideX;  // RESID
+    double* partial;                        // RESID: 2 per CTA
+    int a_kblock, b_kblock;                 // log2 of the k-block (0 = none)
+};
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"((unsigned)__cvta_generic_to_shared(bar)),
+                 "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(bar)),
+                 "r"(bytes));
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"((unsigned)__cvta_generic_to_shared(bar)));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    const unsigned addr = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "LAB_WAIT:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra LAB_WAIT;\n"
+        "}\n" ::"r"(addr),
+        "r"(parity));
+}
+__device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                            int c2, int c3, int c4) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+        "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4),
+        "r"((unsigned)__cvta_generic_to_shared(bar))
+        : "memory");
+}
+
+// Tile coordinates of work item w (batch, split, m-tile, n-tile).
+__device__ __forceinline__ void ws_tile(const WsParams& P, int64_t w, int64_t& b, int64_t& sp, int64_t& mt,
+                                        int64_t& nt) {
+    const int64_t per_split = P.tiles_per_batch;
+    const int64_t per_batch = per_split * P.splits;
+    b = w / per_batch;
+    int64_t r = w - b * per_batch;
+    int64_t t = r % per_split;
+    sp = r / per_split;
+    if (P.tri) {
+        mt = 0;
+        while (t >= P.ntiles - mt) {
+            t -= P.ntiles - mt;
+            ++mt;
+        }
+        nt = mt + t;
+    } else if (P.nfast) {
+        nt = t % P.ntiles;
+        mt = t / P.ntiles;
+    } else {
+        mt = t % P.mtiles;
+        nt = t / P.mtiles;
+    }
+}
+
+template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, bool AK, bool BNM, int EPI>
+__global__ void __launch_bounds__((WARPS_M * WARPS_N + 1) * 32, 1)
+    dmma_gemm_ws_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                        const WsParams P) {
+    constexpr int NCW = WARPS_M * WARPS_N;  // consumer warps
+    constexpr int WM = BM / WARPS_M, WN = BN / WARPS_N;
+    constexpr int TM = WM / 8, TN = WN / 8;
+    constexpr unsigned STAGE_BYTES = (BM * BK + BK * BN) * 8;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    double* As = reinterpret_cast<double*>(smem_raw);
+    double* Bs = As + STAGES * BM * BK;
+    uint64_t* full = reinterpret_cast<uint64_t*>(Bs + STAGES * BK * BN);
+    uint64_t* empty = full + STAGES;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NCW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+    }
+    __syncthreads();
+
+    if (warp == NCW) {
+        // ------------------------------------------------ TMA producer warp
+        if (lane == 0) {
+            asm volatile("prefetch.tensormap [%0];\n" ::"l"(&mapA));
+            asm volatile("prefetch.tensormap [%0];\n" ::"l"(&mapB));
+            int stage = 0;
+            unsigned phase = 0;
+            for (int64_t w = blockIdx.x; w < P.total_tiles; w += gridDim.x) {
+                int64_t b, sp, mt, nt;
+                ws_tile(P, w, b, sp, mt, nt);
+                const int64_t kb = sp * P.kchunk, ke = min(P.K, kb + P.kchunk);
+                for (int64_t k0 = kb; k0 < ke; k0 += BK) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    mbar_expect_tx(&full[stage], STAGE_BYTES);
+                    double* as = As + stage * BM * BK;
+                    double* bs = Bs + stage * BK * BN;
+                    if constexpr (!AK)
+                        tma_load_5d(as, &mapA, &full[stage], 0, (int)k0, (int)(mt * BM / 4), 0, (int)b);
+                    else {
+                        const int ks = P.a_kblock;
+                        const int64_t kk = ks ? (k0 & ((1LL << ks) - 1)) : k0;
+                        const int64_t kq = ks ? (k0 >> ks) : 0;
+                        tma_load_5d(as, &mapA, &full[stage], 0, (int)(mt * BM), (int)(kk / 4), (int)kq, (int)b);
+                    }
+                    if constexpr (BNM)
+                        tma_load_5d(bs, &mapB, &full[stage], 0, (int)k0, (int)(nt * BN / 4), 0, (int)b);
+                    else {
+                        const int ks = P.b_kblock;
+                        const int64_t kk = ks ? (k0 & ((1LL << ks) - 1)) : k0;
+                        const int64_t kq = ks ? (k0 >> ks) : 0;
+                        tma_load_5d(bs, &mapB, &full[stage], 0, (int)(nt * BN), (int)(kk / 4), (int)kq, (int)b);
+                    }
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+        return;
+    }
+
+    // ------------------------------------------------------ consumer warps
+    const int g = lane >> 2, t = lane & 3;
+    const int wm = warp % WARPS_M, wn = warp / WARPS_M;
+    int stage = 0;
+    unsigned phase = 0;
+    double sd = 0.0, sx = 0.0;  // RESID running sums (fixed tile order per CTA)
+
+    for (int64_t w = blockIdx.x; w < P.total_tiles; w += gridDim.x) {
+        int64_t b, sp, mt, nt;
+        ws_tile(P, w, b, sp, mt, nt);
+        const int64_t kb = sp * P.kchunk, ke = min(P.K, kb + P.kchunk);
+        double acc[TM][TN][2];
+#pragma unroll
+        for (int i = 0; i < TM; ++i)
+#pragma unroll
+            for (int j = 0; j < TN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+        for (int64_t k0 = kb; k0 < ke; k0 += BK) {
+            mbar_wait(&full[stage], phase);
+            const double* as = As + stage * BM * BK;
+            const double* bs = Bs + stage * BK * BN;
+#pragma unroll
+            for (int kk = 0; kk < BK; kk += 4) {
+                double af[TM], bf[TN];
+#pragma unroll
+                for (int i = 0; i < TM; ++i) {
+                    const int m = wm * WM + i * 8 + g, k = kk + t;
+                    af[i] = AK ? as[((k >> 2) * BM + m) * 4 + (k & 3)] : as[((m >> 2) * BK + k) * 4 + (m & 3)];
+                }
+#pragma unroll
+                for (int j = 0; j < TN; ++j) {
+                    const int n = wn * WN + j * 8 + g, k = kk + t;
+                    bf[j] = BNM ? bs[((n >> 2) * BK + k) * 4 + (n & 3)] : bs[((k >> 2) * BN + n) * 4 + (k & 3)];
+                }
+#pragma unroll
+                for (int i = 0; i < TM; ++i)
+#pragma unroll
+                    for (int j = 0; j < TN; ++j) dmma884(acc[i][j], af[i], bf[j]);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[stage]);
+            if (++stage == STAGES) {
+                stage = 0;
+                phase ^= 1;
+            }
+        }
+
+        const int64_t m0 = mt * BM, n0 = nt * BN;
+        if constexpr (EPI == EPI_STORE) {
+            double* C = P.C + b * P.strideC + sp * P.strideCsplit;
+            const double* Cin = P.Cin ? P.Cin + b * P.strideCin : nullptr;
+            const bool diag = P.tri && (mt == nt);
+#pragma unroll
+            for (int i = 0; i < TM; ++i)
+#pragma unroll
+                for (int j = 0; j < TN; ++j)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int64_t m = m0 + wm * WM + i * 8 + g;
+                        const int64_t n = n0 + wn * WN + j * 8 + 2 * t + e;
+                        if (m < P.M && n < P.N) {
+                            if (diag && m > n) continue;
+                            double v = P.alpha * acc[i][j][e];
+                            if (Cin && P.beta != 0.0) v += P.beta * Cin[m + n * P.ldcin];
+                            C[m + n * P.ldc] = v;
+                            if (P.tri && m != n) C[n + m * P.ldc] = v;
+                        }
+                    }
+        } else {
+            const double* X = P.X + b * P.strideX;
+#pragma unroll
+            for (int i = 0; i < TM; ++i)
+#pragma unroll
+                for (int j = 0; j < TN; ++j)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int64_t m = m0 + wm * WM + i * 8 + g;
+                        const int64_t n = n0 + wn * WN + j * 8 + 2 * t + e;
+                        if (m < P.M && n < P.N) {
+                            const double x = X[m + n * P.ldx];
+                            const double d = x - P.alpha * acc[i][j][e];
+                            sd = fma(d, d, sd);
+                            sx = fma(x, x, sx);
+                        }
+                    }
+        }
+    }
+
+    if constexpr (EPI == EPI_RESID) {
+        // fixed-order CTA reduction over the consumer warps
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) {
+            sd += __shfl_xor_sync(0xffffffffu, sd, off);
+            sx += __shfl_xor_sync(0xffffffffu, sx, off);
+        }
+        __shared__ double red[2 * 32];
+        if (lane == 0) {
+            red[2 * warp] = sd;
+            red[2 * warp + 1] = sx;
+        }
+        asm volatile("bar.sync 1, %0;\n" ::"r"(NCW * 32));  // consumers only
+        if (threadIdx.x == 0) {
+            double a = 0.0, c = 0.0;
+            for (int i = 0; i < NCW; ++i) {
+                a += red[2 * i];
+                c += red[2 * i + 1];
+            }
+            P.partial[2 * blockIdx.x] = a;
+            P.partial[2 * blockIdx.x + 1] = c;
+        }
+    }
+}
+
+}  // namespace ppc

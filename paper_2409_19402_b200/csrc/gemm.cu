@@ -101,6 +101,7 @@ int64_t kchunk_of(const GemmDesc& d) {
 void gemm(const GemmDesc& d, cudaStream_t s) {
     validate(d);
     if (d.M == 0 || d.N == 0) return;
+    if (d.allow_ws && gemm_ws(d, EPI_STORE, nullptr, 0, 0, nullptr, nullptr, s)) return;
     const CfgId id = choose(d);
     const int64_t kchunk = kchunk_of(d);
     GemmParams P;
@@ -117,6 +118,7 @@ void gemm(const GemmDesc& d, cudaStream_t s) {
 
 int64_t gemm_residual_ctas(const GemmDesc& d) {
     int64_t ctas = 0;
+    if (d.allow_ws && gemm_ws(d, EPI_RESID, nullptr, 0, 0, nullptr, &ctas, nullptr)) return ctas;
     grid_for(choose(d), d, &ctas);
     return ctas;
 }
@@ -126,6 +128,7 @@ void gemm_residual(const GemmDesc& d, const double* X, int64_t ldx, int64_t stri
     validate(d);
     if (d.symmetric || d.splits != 1) fail(PPC_ARGUMENT, "gemm_residual: plain tiling only");
     if (d.M == 0 || d.N == 0) return;
+    if (d.allow_ws && gemm_ws(d, EPI_RESID, X, ldx, strideX, partials, nullptr, s)) return;
     const CfgId id = choose(d);
     const int64_t kchunk = kchunk_of(d);
     GemmParams P;

@@ -335,6 +335,7 @@ void slice_tail_energy(const double* A, int64_t m, int64_t n, int64_t stride, in
     d.M = m; d.N = n; d.K = k; d.batch = batch;
     d.A = us.d(); d.lda = m; d.strideA = m * k;
     d.B = V; d.ldb = n; d.strideB = n * k; d.b_nmajor = true;
+    d.allow_ws = false;  // per-batch CTA groups are needed for the per-slice sums
     const int64_t ctas = gemm_residual_ctas(d);
     DeviceBuffer part(sizeof(double) * 2 * ctas);
     gemm_residual(d, A, m, stride, part.d(), s);

@@ -438,3 +438,53 @@ def test_dist_driver_single_rank_matches_fused(engine):
     assert np.array_equal(engine.to_host(Q), f.transform.q)  # same Gram tree, same eigensolve
     np.testing.assert_allclose(engine.to_host(S), engine.to_host(f.s), rtol=1e-12)
     assert abs(re2 - re) <= 1e-12 * re
+
+
+# ------------------------------------------- warp-specialized TMA GEMM path
+def _both_paths(fn):
+    from paper_2409_19402_b200 import _lib
+    L = _lib.lib()
+    outs = []
+    for mode in (0, 1):
+        assert L.ppc_set_gemm_path(mode) == 0
+        try:
+            outs.append(fn())
+        finally:
+            L.ppc_set_gemm_path(0)
+    return outs
+
+
+@pytest.mark.parametrize("shape,q", [((256, 128, 256), 64), ((512, 96, 200), 128), ((300, 100, 64), 32),
+                                     ((1024, 64, 96), 20)])
+def test_ws_mode3_bitwise_and_vs_numpy(engine, shape, q):
+    rng = np.random.default_rng(1)
+    a = np.asfortranarray(rng.standard_normal(shape))
+    m = np.asfortranarray(rng.standard_normal((q, shape[2])))
+    ws, classic = _both_paths(lambda: engine.mode3_product(a, m))
+    assert np.array_equal(ws, classic)
+    want = np.einsum("ijk,lk->ijl", a, m)
+    assert rel(ws, want) <= 1e-13
+
+
+def test_ws_facewise_starq_bitwise(engine):
+    rng = np.random.default_rng(2)
+    a = np.asfortranarray(rng.standard_normal((256, 192, 24)))
+    b = np.asfortranarray(rng.standard_normal((192, 320, 24)))
+    t = engine.Transform("dct", 24, 8)
+    f1, f0 = _both_paths(lambda: engine.facewise_product(a, b))
+    assert np.array_equal(f1, f0)
+    assert rel(f1, np.einsum("imk,mjk->ijk", a, b)) <= 1e-13
+    s1, s0 = _both_paths(lambda: engine.star_q(a, b, t))
+    assert np.array_equal(s1, s0)
+
+
+def test_ws_gram_and_residual_bitwise(engine, oracle):
+    a = synth.cp_tensor(256, 200, 160, rank=20, noise=1e-3, seed=3)
+    q1, q0 = _both_paths(lambda: engine.data_dependent_transform(a, 24).q)
+    assert np.array_equal(q1, q0)
+    t = engine.Transform.custom(q1)
+    f = engine.tsvdq(a, t, 8)
+    r1, r0 = _both_paths(lambda: engine.tsvdq_relative_error(a, f))
+    assert abs(r1 - r0) <= 1e-15 * r0  # residual partial sums grouped differently
+    re = oracle.relative_error(a, oracle.tsvdq_reconstruct(*[engine.to_host(x) for x in (f.u, f.s, f.v)], q1))
+    assert abs(r1 - re) <= 1e-12 * re
