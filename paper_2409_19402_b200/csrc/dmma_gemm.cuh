@@ -277,6 +277,7 @@ struct GemmDesc {
     int kshift = 0;      // k-blocked K-major operands (see GemmParams)
     int64_t kbstride = 0;
     const int* zmap = nullptr;  // device array of `batch` batch indices (nullable)
+    int64_t zmap_extent = 0;    // with zmap: number of batches the indices refer to
     bool allow_ws = true;       // may use the warp-specialized TMA kernel
 };
 

@@ -37,6 +37,7 @@ struct WsParams {
     const double* X; int64_t ldx, strideX;  // RESID
     double* partial;                        // RESID: 2 per CTA
     int a_kblock, b_kblock;                 // log2 of the k-block (0 = none)
+    const int* zmap;                        // nullable batch index indirection
 };
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
@@ -79,6 +80,7 @@ __device__ __forceinline__ void ws_tile(const WsParams& P, int64_t w, int64_t& b
     const int64_t per_batch = per_split * P.splits;
     b = w / per_batch;
     int64_t r = w - b * per_batch;
+    if (P.zmap) b = P.zmap[b];
     int64_t t = r % per_split;
     sp = r / per_split;
     if (P.tri) {

@@ -112,7 +112,9 @@ bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 bool gemm_ws(const GemmDesc& d, int epi, const double* X, int64_t ldx, int64_t strideX, double* partials,
              int64_t* ctas_out, cudaStream_t s) {
     if (gemm_path() == 1) return false;  // forced classic cp.async kernel
-    if (d.M < 1 || d.N < 1 || d.K < 1 || d.zmap) return false;
+    if (d.M < 1 || d.N < 1 || d.K < 1) return false;
+    if (d.zmap && d.zmap_extent < 1) return false;
+    const int64_t map_batch = d.zmap ? d.zmap_extent : d.batch;
     if (d.a_kmajor && d.b_nmajor) return false;
     if (epi == EPI_RESID && (d.a_kmajor || !d.b_nmajor)) return false;
     // configuration
@@ -144,14 +146,14 @@ bool gemm_ws(const GemmDesc& d, int epi, const double* X, int64_t ldx, int64_t s
     CUtensorMap ma, mb;
     bool ok;
     if (!d.a_kmajor)
-        ok = make_map(&ma, d.A, false, d.M, d.K, d.lda, d.batch, d.strideA, bm, bk, 0, 0);
+        ok = make_map(&ma, d.A, false, d.M, d.K, d.lda, map_batch, d.strideA, bm, bk, 0, 0);
     else
-        ok = make_map(&ma, d.A, true, d.K, d.M, d.lda, d.batch, d.strideA, bk, bm, d.kshift, d.kbstride);
+        ok = make_map(&ma, d.A, true, d.K, d.M, d.lda, map_batch, d.strideA, bk, bm, d.kshift, d.kbstride);
     if (!ok) return false;
     if (d.b_nmajor)
-        ok = make_map(&mb, d.B, false, d.N, d.K, d.ldb, d.batch, d.strideB, bn, bk, 0, 0);
+        ok = make_map(&mb, d.B, false, d.N, d.K, d.ldb, map_batch, d.strideB, bn, bk, 0, 0);
     else
-        ok = make_map(&mb, d.B, true, d.K, d.N, d.ldb, d.batch, d.strideB, bk, bn, d.kshift, d.kbstride);
+        ok = make_map(&mb, d.B, true, d.K, d.N, d.ldb, map_batch, d.strideB, bk, bn, d.kshift, d.kbstride);
     if (!ok) return false;
 
     WsParams P{};
@@ -164,6 +166,7 @@ bool gemm_ws(const GemmDesc& d, int epi, const double* X, int64_t ldx, int64_t s
     P.Cin = d.Cin; P.ldcin = d.ldcin; P.strideCin = d.strideCin;
     P.alpha = d.alpha; P.beta = d.beta;
     P.X = X; P.ldx = ldx; P.strideX = strideX; P.partial = partials;
+    P.zmap = d.zmap;
     P.a_kblock = d.a_kmajor ? d.kshift : 0;
     P.b_kblock = !d.b_nmajor ? d.kshift : 0;
     const int sms = ctx().sms;

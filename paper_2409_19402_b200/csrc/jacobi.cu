@@ -11,7 +11,11 @@
 // order (deterministic). Working set (W = R x C, V = C x C) lives in shared
 // memory when it fits (<= ~200 KB), else in a global workspace (L2-resident
 // for the sizes that reach this path).
+#include <algorithm>
 #include <cfloat>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
 
 #include "internal.h"
 #include "jacobi.cuh"
@@ -32,7 +36,7 @@ __device__ __forceinline__ double warp_sum(double v) {
 __global__ void jacobi_svd_kernel(const double* __restrict__ A, int64_t m, int64_t n,
                                   int64_t strideA, int64_t k, double* __restrict__ U,
                                   double* __restrict__ S, double* __restrict__ V, double* gws,
-                                  int use_smem, double* tail2) {
+                                  int use_smem, double* tail2, int* info) {
     extern __shared__ __align__(16) double sm[];
     __shared__ int s_rot;
     const int64_t b = blockIdx.x;
@@ -64,6 +68,7 @@ __global__ void jacobi_svd_kernel(const double* __restrict__ A, int64_t m, int64
     const double tol = kEps * sqrt((double)R);
     const int64_t P = (Cc + 1) & ~int64_t(1);  // players, padded to even
     int sweep = 0;
+    int* info_out = info;
     for (; sweep < 60 && Cc > 1; ++sweep) {
         if (tid == 0) s_rot = 0;
         __syncthreads();
@@ -115,6 +120,7 @@ __global__ void jacobi_svd_kernel(const double* __restrict__ A, int64_t m, int64
         __syncthreads();
     }
 
+    if (tid == 0 && info_out) info_out[b] = sweep;
     // singular values = column norms
     for (int64_t c = warp; c < Cc; c += nw) {
         double acc = 0.0;
@@ -370,7 +376,7 @@ void jacobi_svd(const double* A, int64_t m, int64_t n, int64_t strideA, int64_t 
     const int64_t R = m > n ? m : n, C = m > n ? n : m;
     if (k < 1 || k > C) fail(PPC_ARGUMENT, "jacobi_svd: k out of range");
     const size_t smem = jacobi_smem_bytes(m, n);
-    const int threads = C >= 96 ? 512 : (C >= 32 ? 256 : 128);
+    const int threads = C >= 96 ? 1024 : (C >= 48 ? 512 : (C >= 24 ? 256 : 128));
     const bool use_smem = smem <= 200 * 1024;
     if (!use_smem && !U && !tail2 && m == n && (size_t)n * n * sizeof(double) <= 200 * 1024) {
         // eigen mode, W fits but W + V does not: logged rotations + replay
@@ -381,21 +387,28 @@ void jacobi_svd(const double* A, int64_t m, int64_t n, int64_t strideA, int64_t 
         const size_t wsm = (size_t)n * n * sizeof(double);
         PPC_CUDA_CHECK(cudaFuncSetAttribute(jacobi_logged_kernel,
                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm));
-        jacobi_logged_kernel<<<(unsigned)batch, 512, wsm, s>>>(A, n, strideA, lg.as<double2>(),
+        jacobi_logged_kernel<<<(unsigned)batch, 1024, wsm, s>>>(A, n, strideA, lg.as<double2>(),
                                                                 max_sweeps, ns.as<int>(), sg.d(),
                                                                 rk.as<int>());
         count_launch();
         check_launch("jacobi_logged");
-        constexpr int ROWS = 32;
+        constexpr int ROWS = 8;
         const size_t rsm = (size_t)ROWS * n * sizeof(double);
         PPC_CUDA_CHECK(cudaFuncSetAttribute(replay_rotations_kernel<ROWS>,
                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));
         dim3 grid((unsigned)((n + ROWS - 1) / ROWS), (unsigned)batch);
-        replay_rotations_kernel<ROWS><<<grid, 512, rsm, s>>>(lg.as<double2>(), ns.as<int>(), n,
+        replay_rotations_kernel<ROWS><<<grid, 256, rsm, s>>>(lg.as<double2>(), ns.as<int>(), n,
                                                              max_sweeps, sg.d(), rk.as<int>(), k,
                                                              V, S);
         count_launch();
         check_launch("replay_rotations");
+        if (std::getenv("PPC_JACOBI_DEBUG")) {
+            std::vector<int> h(batch);
+            PPC_CUDA_CHECK(cudaMemcpyAsync(h.data(), ns.d(), sizeof(int) * batch, cudaMemcpyDeviceToHost, s));
+            PPC_CUDA_CHECK(cudaStreamSynchronize(s));
+            fprintf(stderr, "[jacobi-logged] %lldx%lld batch %lld sweeps %d\n", (long long)n, (long long)n,
+                    (long long)batch, h[0]);
+        }
         return;
     }
     DeviceBuffer ws;
@@ -404,10 +417,22 @@ void jacobi_svd(const double* A, int64_t m, int64_t n, int64_t strideA, int64_t 
         PPC_CUDA_CHECK(cudaFuncSetAttribute(jacobi_svd_kernel,
                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     if (batch > 0x7fffffffLL) fail(PPC_ARGUMENT, "jacobi_svd: batch too large");
+    static const bool dbg = std::getenv("PPC_JACOBI_DEBUG") != nullptr;
+    DeviceBuffer dinfo(sizeof(int) * batch);
     jacobi_svd_kernel<<<(unsigned)batch, threads, use_smem ? smem : 0, s>>>(
-        A, m, n, strideA, k, U, S, V, ws.d(), use_smem ? 1 : 0, tail2);
+        A, m, n, strideA, k, U, S, V, ws.d(), use_smem ? 1 : 0, tail2, dinfo.as<int>());
     count_launch();
     check_launch("jacobi_svd");
+    if (dbg) {
+        std::vector<int> h(batch);
+        PPC_CUDA_CHECK(cudaMemcpyAsync(h.data(), dinfo.d(), sizeof(int) * batch, cudaMemcpyDeviceToHost, s));
+        PPC_CUDA_CHECK(cudaStreamSynchronize(s));
+        int mx = 0;
+        long sum = 0;
+        for (int v : h) { mx = std::max(mx, v); sum += v; }
+        fprintf(stderr, "[jacobi] %lldx%lld batch %lld k %lld smem %d sweeps max %d avg %.1f\n", (long long)m,
+                (long long)n, (long long)batch, (long long)k, use_smem ? 1 : 0, mx, (double)sum / batch);
+    }
 }
 
 }  // namespace ppc
