@@ -33,6 +33,87 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
+// Sum over the 16 lanes of a half-warp (fixed order, deterministic).
+__device__ __forceinline__ double half_sum(double v) {
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Round-robin pair pi of round r among P (even) players, returned as a < c.
+__device__ __forceinline__ void rr_pair(int64_t r, int64_t pi, int64_t P, int64_t& a, int64_t& c) {
+    if (pi == 0) {
+        a = r;
+        c = P - 1;
+    } else {
+        a = (r + pi) % (P - 1);
+        c = (r + P - 1 - pi) % (P - 1);
+    }
+    if (a > c) {
+        const int64_t t = a;
+        a = c;
+        c = t;
+    }
+}
+
+// One Jacobi round: every pair of the round handled by a 16-lane group.
+// Rotates the columns of W (R rows) and, if Va != nullptr, of Va (Cc rows);
+// logs (cs, sn) per pair when lg != nullptr. Returns nonzero in *rot if any
+// rotation was applied.
+__device__ __forceinline__ void jacobi_round(double* W, int64_t R, double* Va, int64_t Cc, int64_t P,
+                                             int64_t r, double tol, double2* lg, int* rot) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int grp = tid >> 4, l16 = tid & 15, ngrp = nt >> 4;
+    for (int64_t base = 0; base < P / 2; base += ngrp) {
+        const int64_t pi = base + grp;
+        // all 32 lanes of a warp stay converged for the shuffles: pairs past
+        // the end work on a dummy (no memory traffic)
+        const bool live = pi < P / 2;
+        int64_t a = 0, c = 0;
+        if (live) rr_pair(r, pi, P, a, c);
+        const bool act = live && c < Cc;
+        double al = 0.0, be = 0.0, ga = 0.0;
+        if (act) {
+            const double* wa = W + a * R;
+            const double* wc = W + c * R;
+            for (int64_t i = l16; i < R; i += 16) {
+                const double x = wa[i], y = wc[i];
+                al = fma(x, x, al);
+                be = fma(y, y, be);
+                ga = fma(x, y, ga);
+            }
+        }
+        al = half_sum(al);
+        be = half_sum(be);
+        ga = half_sum(ga);
+        double cs = 1.0, sn = 0.0;
+        if (act && ga != 0.0 && fabs(ga) > tol * sqrt(al * be)) {
+            const double zeta = (be - al) / (2.0 * ga);
+            const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+            cs = rsqrt(1.0 + tt * tt);
+            sn = cs * tt;
+            double* wa = W + a * R;
+            double* wc = W + c * R;
+            for (int64_t i = l16; i < R; i += 16) {
+                const double x = wa[i], y = wc[i];
+                wa[i] = cs * x - sn * y;
+                wc[i] = sn * x + cs * y;
+            }
+            if (Va) {
+                double* va = Va + a * Cc;
+                double* vc = Va + c * Cc;
+                for (int64_t i = l16; i < Cc; i += 16) {
+                    const double x = va[i], y = vc[i];
+                    va[i] = cs * x - sn * y;
+                    vc[i] = sn * x + cs * y;
+                }
+            }
+            if (l16 == 0) *rot = 1;
+        }
+        if (lg && live && l16 == 0) lg[pi] = make_double2(cs, sn);
+    }
+}
+
 __global__ void jacobi_svd_kernel(const double* __restrict__ A, int64_t m, int64_t n,
                                   int64_t strideA, int64_t k, double* __restrict__ U,
                                   double* __restrict__ S, double* __restrict__ V, double* gws,
@@ -73,47 +154,7 @@ __global__ void jacobi_svd_kernel(const double* __restrict__ A, int64_t m, int64
         if (tid == 0) s_rot = 0;
         __syncthreads();
         for (int64_t r = 0; r < P - 1; ++r) {
-            for (int64_t pi = warp; pi < P / 2; pi += nw) {
-                int64_t a, c;
-                if (pi == 0) {
-                    a = r;
-                    c = P - 1;
-                } else {
-                    a = (r + pi) % (P - 1);
-                    c = (r + P - 1 - pi) % (P - 1);
-                }
-                if (a > c) { int64_t t = a; a = c; c = t; }
-                if (c >= Cc) continue;  // dummy player
-                double* wa = W + a * R;
-                double* wc = W + c * R;
-                double al = 0.0, be = 0.0, ga = 0.0;
-                for (int64_t i = lane; i < R; i += 32) {
-                    const double x = wa[i], y = wc[i];
-                    al = fma(x, x, al);
-                    be = fma(y, y, be);
-                    ga = fma(x, y, ga);
-                }
-                al = warp_sum(al);
-                be = warp_sum(be);
-                ga = warp_sum(ga);
-                if (ga == 0.0 || !(fabs(ga) > tol * sqrt(al * be))) continue;
-                const double zeta = (be - al) / (2.0 * ga);
-                const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-                const double cs = rsqrt(1.0 + tt * tt), sn = cs * tt;
-                for (int64_t i = lane; i < R; i += 32) {
-                    const double x = wa[i], y = wc[i];
-                    wa[i] = cs * x - sn * y;
-                    wc[i] = sn * x + cs * y;
-                }
-                double* va = Va + a * Cc;
-                double* vc = Va + c * Cc;
-                for (int64_t i = lane; i < Cc; i += 32) {
-                    const double x = va[i], y = vc[i];
-                    va[i] = cs * x - sn * y;
-                    vc[i] = sn * x + cs * y;
-                }
-                if (lane == 0) s_rot = 1;
-            }
+            jacobi_round(W, R, Va, Cc, P, r, tol, nullptr, &s_rot);
             __syncthreads();
         }
         if (!s_rot) break;
@@ -260,36 +301,7 @@ __global__ void jacobi_logged_kernel(const double* __restrict__ A, int64_t b, in
         if (tid == 0) s_rot = 0;
         __syncthreads();
         for (int64_t r = 0; r < P - 1; ++r) {
-            for (int64_t pi = warp; pi < P / 2; pi += nw) {
-                int64_t a, c;
-                if (pi == 0) { a = r; c = P - 1; }
-                else { a = (r + pi) % (P - 1); c = (r + P - 1 - pi) % (P - 1); }
-                if (a > c) { int64_t t = a; a = c; c = t; }
-                double cs = 1.0, sn = 0.0;
-                if (c < b) {
-                    double* wa = W + a * b;
-                    double* wc = W + c * b;
-                    double al = 0.0, be = 0.0, ga = 0.0;
-                    for (int64_t i = lane; i < b; i += 32) {
-                        const double x = wa[i], y = wc[i];
-                        al = fma(x, x, al); be = fma(y, y, be); ga = fma(x, y, ga);
-                    }
-                    al = warp_sum(al); be = warp_sum(be); ga = warp_sum(ga);
-                    if (ga != 0.0 && fabs(ga) > tol * sqrt(al * be)) {
-                        const double zeta = (be - al) / (2.0 * ga);
-                        const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-                        cs = rsqrt(1.0 + tt * tt);
-                        sn = cs * tt;
-                        for (int64_t i = lane; i < b; i += 32) {
-                            const double x = wa[i], y = wc[i];
-                            wa[i] = cs * x - sn * y;
-                            wc[i] = sn * x + cs * y;
-                        }
-                        if (lane == 0) s_rot = 1;
-                    }
-                }
-                if (lane == 0) lg[sweep * per_sweep + r * (P / 2) + pi] = make_double2(cs, sn);
-            }
+            jacobi_round(W, b, nullptr, b, P, r, tol, lg + sweep * per_sweep + r * (P / 2), &s_rot);
             __syncthreads();
         }
         if (!s_rot) { ++sweep; break; }
