@@ -73,6 +73,10 @@ __device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* map, u
         : "memory");
 }
 
+__device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(p), "r"(bytes) : "memory");
+}
+
 // Tile coordinates of work item w (batch, split, m-tile, n-tile).
 __device__ __forceinline__ void ws_tile(const WsParams& P, int64_t w, int64_t& b, int64_t& sp, int64_t& mt,
                                         int64_t& nt) {
@@ -134,6 +138,17 @@ __global__ void __launch_bounds__((WARPS_M * WARPS_N + 1) * 32, 1)
                 int64_t b, sp, mt, nt;
                 ws_tile(P, w, b, sp, mt, nt);
                 const int64_t kb = sp * P.kchunk, ke = min(P.K, kb + P.kchunk);
+                if constexpr (EPI == EPI_RESID) {
+                    // warm L2 with this tile's reference block: the epilogue
+                    // reads it after the k-loop (hides HBM latency)
+                    const int64_t m0 = mt * BM, n0 = nt * BN;
+                    const int64_t rows = min((int64_t)BM, P.M - m0);
+                    const unsigned bytes = (unsigned)(rows * 8) & ~15u;
+                    if (bytes && ((P.ldx & 1) == 0)) {
+                        const double* X = P.X + b * P.strideX + m0;
+                        for (int64_t n = n0; n < min(P.N, n0 + BN); ++n) prefetch_l2(X + n * P.ldx, bytes);
+                    }
+                }
                 for (int64_t k0 = kb; k0 < ke; k0 += BK) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     mbar_expect_tx(&full[stage], STAGE_BYTES);

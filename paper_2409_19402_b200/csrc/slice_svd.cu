@@ -7,6 +7,7 @@
 //   data_q     — transforms.cpp:97-115 via Gram + symmetric eigensolve (K5).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "dmma_gemm.cuh"
@@ -103,7 +104,8 @@ void gram_chunks(const double* T, int64_t ldT, int64_t rows, int64_t n3, int64_t
     // Large tube matrices: each SYRK pipeline stage would touch one 2 MB page
     // per column (columns are ldT*8 bytes apart), thrashing the TLB. Re-lay T
     // into 2048-row blocks first (one extra HBM pass); same summation order.
-    const int kshift = (ldT >= (1LL << 20) && n3 >= 64) ? 11 : 0;
+    static const bool no_relayout = std::getenv("PPC_NO_RELAYOUT") != nullptr;
+    const int kshift = (!no_relayout && ldT >= (1LL << 20) && n3 >= 64) ? 11 : 0;
     DeviceBuffer tb;
     const double* src = T;
     int64_t ld = ldT;
