@@ -26,6 +26,8 @@ namespace ppc {
 namespace {
 
 constexpr double kEps = 2.220446049250313e-16;
+__constant__ double c_tol_scale = 1.0;
+__device__ __forceinline__ double jacobi_tol_scale() { return c_tol_scale; }
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -61,7 +63,7 @@ __device__ __forceinline__ void rr_pair(int64_t r, int64_t pi, int64_t P, int64_
 // logs (cs, sn) per pair when lg != nullptr. Returns nonzero in *rot if any
 // rotation was applied.
 __device__ __forceinline__ void jacobi_round(double* W, int64_t R, double* Va, int64_t Cc, int64_t P,
-                                             int64_t r, double tol, double2* lg, int* rot) {
+                                             int64_t r, double tol, double2* lg, int* rot, double gtol = 0.0) {
     const int tid = threadIdx.x, nt = blockDim.x;
     const int grp = tid >> 4, l16 = tid & 15, ngrp = nt >> 4;
     for (int64_t base = 0; base < P / 2; base += ngrp) {
@@ -87,7 +89,8 @@ __device__ __forceinline__ void jacobi_round(double* W, int64_t R, double* Va, i
         be = half_sum(be);
         ga = half_sum(ga);
         double cs = 1.0, sn = 0.0;
-        if (act && ga != 0.0 && fabs(ga) > tol * sqrt(al * be)) {
+        if (act && ga != 0.0 && fabs(ga) > tol * sqrt(al * be) &&
+            (gtol == 0.0 || fabs(ga) > gtol * (sqrt(al) + sqrt(be)))) {
             const double zeta = (be - al) / (2.0 * ga);
             const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
             cs = rsqrt(1.0 + tt * tt);
@@ -114,10 +117,10 @@ __device__ __forceinline__ void jacobi_round(double* W, int64_t R, double* Va, i
     }
 }
 
-__global__ void jacobi_svd_kernel(const double* __restrict__ A, int64_t m, int64_t n,
+__global__ void __launch_bounds__(1024, 1) jacobi_svd_kernel(const double* __restrict__ A, int64_t m, int64_t n,
                                   int64_t strideA, int64_t k, double* __restrict__ U,
                                   double* __restrict__ S, double* __restrict__ V, double* gws,
-                                  int use_smem, double* tail2, int* info) {
+                                  int use_smem, double* tail2, int* info, double gtol_rel) {
     extern __shared__ __align__(16) double sm[];
     __shared__ int s_rot;
     const int64_t b = blockIdx.x;
@@ -146,15 +149,31 @@ __global__ void jacobi_svd_kernel(const double* __restrict__ A, int64_t m, int64
     for (int64_t i = tid; i < Cc * Cc; i += nt) Va[i] = (i % Cc == i / Cc) ? 1.0 : 0.0;
     __syncthreads();
 
-    const double tol = kEps * sqrt((double)R);
+    const double tol = jacobi_tol_scale() * kEps * sqrt((double)R);
     const int64_t P = (Cc + 1) & ~int64_t(1);  // players, padded to even
     int sweep = 0;
     int* info_out = info;
+    // eigenvalue-only mode: skip rotations whose effect on the Rayleigh
+    // quotients is below gtol_rel * (largest column norm ~ theta_1)
+    __shared__ double s_gtol;
+    if (gtol_rel > 0.0) {
+        if (tid == 0) s_gtol = 0.0;
+        __syncthreads();
+        for (int64_t c = warp; c < Cc; c += nw) {
+            double acc = 0.0;
+            for (int64_t i = lane; i < R; i += 32) acc = fma(W[c * R + i], W[c * R + i], acc);
+            acc = warp_sum(acc);
+            if (lane == 0) atomicMax(reinterpret_cast<unsigned long long*>(&s_gtol),
+                                     __double_as_longlong(sqrt(acc)));
+        }
+        __syncthreads();
+    }
+    const double gtol = gtol_rel > 0.0 ? gtol_rel * s_gtol : 0.0;
     for (; sweep < 60 && Cc > 1; ++sweep) {
         if (tid == 0) s_rot = 0;
         __syncthreads();
         for (int64_t r = 0; r < P - 1; ++r) {
-            jacobi_round(W, R, Va, Cc, P, r, tol, nullptr, &s_rot);
+            jacobi_round(W, R, Va, Cc, P, r, tol, nullptr, &s_rot, gtol);
             __syncthreads();
         }
         if (!s_rot) break;
@@ -280,10 +299,10 @@ __global__ void jacobi_svd_kernel(const double* __restrict__ A, int64_t m, int64
 // not (b <= ~160): sweep on W in shared memory and log every round's
 // rotations (cs, sn) to global memory; V is rebuilt afterwards by a
 // row-parallel kernel that replays the log. rank/sig go to global memory.
-__global__ void jacobi_logged_kernel(const double* __restrict__ A, int64_t b, int64_t strideA,
+__global__ void __launch_bounds__(1024, 1) jacobi_logged_kernel(const double* __restrict__ A, int64_t b, int64_t strideA,
                                      double2* __restrict__ log, int64_t max_sweeps,
                                      int* __restrict__ nsweeps, double* __restrict__ sig_out,
-                                     int* __restrict__ rank_out) {
+                                     int* __restrict__ rank_out, double gtol_rel) {
     extern __shared__ __align__(16) double W[];
     __shared__ int s_rot;
     const int64_t bi = blockIdx.x;
@@ -295,13 +314,27 @@ __global__ void jacobi_logged_kernel(const double* __restrict__ A, int64_t b, in
     const int64_t P = (b + 1) & ~int64_t(1);
     const int64_t per_sweep = (P - 1) * (P / 2);
     double2* lg = log + bi * max_sweeps * per_sweep;
-    const double tol = kEps * sqrt((double)b);
+    const double tol = jacobi_tol_scale() * kEps * sqrt((double)b);
     int sweep = 0;
+    __shared__ double s_gtol;
+    if (gtol_rel > 0.0) {
+        if (tid == 0) s_gtol = 0.0;
+        __syncthreads();
+        for (int64_t c = warp; c < b; c += nw) {
+            double acc = 0.0;
+            for (int64_t i = lane; i < b; i += 32) acc = fma(W[c * b + i], W[c * b + i], acc);
+            acc = warp_sum(acc);
+            if (lane == 0) atomicMax(reinterpret_cast<unsigned long long*>(&s_gtol),
+                                     __double_as_longlong(sqrt(acc)));
+        }
+        __syncthreads();
+    }
+    const double gtol = gtol_rel > 0.0 ? gtol_rel * s_gtol : 0.0;
     for (; sweep < max_sweeps && b > 1; ++sweep) {
         if (tid == 0) s_rot = 0;
         __syncthreads();
         for (int64_t r = 0; r < P - 1; ++r) {
-            jacobi_round(W, b, nullptr, b, P, r, tol, lg + sweep * per_sweep + r * (P / 2), &s_rot);
+            jacobi_round(W, b, nullptr, b, P, r, tol, lg + sweep * per_sweep + r * (P / 2), &s_rot, gtol);
             __syncthreads();
         }
         if (!s_rot) { ++sweep; break; }
@@ -383,8 +416,15 @@ size_t jacobi_smem_bytes(int64_t m, int64_t n) {
 }
 
 void jacobi_svd(const double* A, int64_t m, int64_t n, int64_t strideA, int64_t batch, int64_t k,
-                double* U, double* S, double* V, double* tail2, cudaStream_t s) {
+                double* U, double* S, double* V, double* tail2, cudaStream_t s, double gtol_rel) {
     if (batch == 0) return;
+    static bool tol_set = false;
+    if (!tol_set) {
+        const char* e = std::getenv("PPC_JACOBI_TOL");
+        const double v = e ? std::atof(e) : 1.0;
+        PPC_CUDA_CHECK(cudaMemcpyToSymbol(c_tol_scale, &v, sizeof(double)));
+        tol_set = true;
+    }
     const int64_t R = m > n ? m : n, C = m > n ? n : m;
     if (k < 1 || k > C) fail(PPC_ARGUMENT, "jacobi_svd: k out of range");
     const size_t smem = jacobi_smem_bytes(m, n);
@@ -401,7 +441,7 @@ void jacobi_svd(const double* A, int64_t m, int64_t n, int64_t strideA, int64_t 
                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm));
         jacobi_logged_kernel<<<(unsigned)batch, 1024, wsm, s>>>(A, n, strideA, lg.as<double2>(),
                                                                 max_sweeps, ns.as<int>(), sg.d(),
-                                                                rk.as<int>());
+                                                                rk.as<int>(), gtol_rel);
         count_launch();
         check_launch("jacobi_logged");
         constexpr int ROWS = 8;
@@ -432,7 +472,7 @@ void jacobi_svd(const double* A, int64_t m, int64_t n, int64_t strideA, int64_t 
     static const bool dbg = std::getenv("PPC_JACOBI_DEBUG") != nullptr;
     DeviceBuffer dinfo(sizeof(int) * batch);
     jacobi_svd_kernel<<<(unsigned)batch, threads, use_smem ? smem : 0, s>>>(
-        A, m, n, strideA, k, U, S, V, ws.d(), use_smem ? 1 : 0, tail2, dinfo.as<int>());
+        A, m, n, strideA, k, U, S, V, ws.d(), use_smem ? 1 : 0, tail2, dinfo.as<int>(), gtol_rel);
     count_launch();
     check_launch("jacobi_svd");
     if (dbg) {

@@ -9,8 +9,10 @@ size_t jacobi_smem_bytes(int64_t m, int64_t n);
 // batch x (m x n) blocks at stride strideA. Leading k triplets (descending):
 // U (m,k,batch) [nullable: eigen mode, no sign rule], S (k,batch), V (n,k,batch);
 // tail2 (nullable): per-block sum of the squared discarded singular values.
+// gtol_rel > 0 (eigen mode only): eigenvalue accuracy gtol_rel * theta_1
+// suffices, rotations inside tight clusters below that are skipped.
 void jacobi_svd(const double* A, int64_t m, int64_t n, int64_t strideA, int64_t batch, int64_t k,
-                double* U, double* S, double* V, double* tail2, cudaStream_t s);
+                double* U, double* S, double* V, double* tail2, cudaStream_t s, double gtol_rel = 0.0);
 // Sign rule of matrix_kernels.cpp:16-25 on `batch` stacks of X (rows x cols):
 // the largest-|x| entry (first on ties) of each column made nonnegative; the
 // matching column of Y (yrows x cols, nullable) is flipped with it.

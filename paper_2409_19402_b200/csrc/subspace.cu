@@ -123,7 +123,7 @@ __global__ void residual_kernel(const double* GX, const double* X, const double*
 // One CTA per slice: R = chol(S + shift*I) (upper, S = R^T R), then R^{-1}
 // in place (LAPACK trti2 order, one row per thread), written out as a full
 // b x b column-major block with zeros below the diagonal. b <= 160 (smem).
-__global__ void chol_inv_kernel(const double* __restrict__ S, double* __restrict__ Rinv, int64_t b,
+__global__ void __launch_bounds__(1024, 1) chol_inv_kernel(const double* __restrict__ S, double* __restrict__ Rinv, int64_t b,
                                 int shift_pass, int* fail, double* __restrict__ Rout) {
     extern __shared__ __align__(16) double M[];
     __shared__ double piv;
@@ -306,7 +306,8 @@ void cholqr3(Work& w, double* Y, double* Xout, int64_t c0, cudaStream_t s) {
 
 // Rayleigh-Ritz on the orthonormal active columns [c0, b) of Xn: X, theta,
 // W = G X and residual norms for those columns (locked ones keep theirs).
-void rayleigh_ritz(Work& w, const double* G, int64_t sG, double* Xn, int64_t c0, cudaStream_t s) {
+void rayleigh_ritz(Work& w, const double* G, int64_t sG, double* Xn, int64_t c0, cudaStream_t s,
+                   double gtol_rel) {
     const int64_t r = w.r, b = w.b, batch = w.batch, bc = b - c0, per = r * b;
     StageTimer tm("ss.rayleigh_ritz", s);
     gg(G, r, sG, false, Xn + c0 * r, r, per, w.Z.d() + c0 * r, r, per, r, bc, r, batch, 1.0, 0.0, s);  // Z = G Xn
@@ -314,7 +315,7 @@ void rayleigh_ritz(Work& w, const double* G, int64_t sG, double* Xn, int64_t c0,
     {
         StageTimer tj("ss.rr_eig", s);
         // H (PSD) = Hv diag(theta) Hv^T by one-sided Jacobi (eigen mode)
-        jacobi_svd(w.S.d(), bc, bc, bc * bc, batch, bc, nullptr, w.P.d(), w.Hv.d(), nullptr, s);
+        jacobi_svd(w.S.d(), bc, bc, bc * bc, batch, bc, nullptr, w.P.d(), w.Hv.d(), nullptr, s, gtol_rel);
     }
     PPC_CUDA_CHECK(cudaMemcpy2DAsync(w.th.d() + c0, sizeof(double) * b, w.P.d(), sizeof(double) * bc,
                                      sizeof(double) * bc, batch, cudaMemcpyDeviceToDevice, s));
@@ -368,7 +369,8 @@ void subspace_eig_top(const double* G, int64_t r, int64_t batch, int64_t k, doub
     randn_kernel<<<grid1(per * batch), 256, 0, s>>>(w.Y.d(), per * batch, 0x5eed5eedULL + (uint64_t)r * 131 + b);
     count_launch();
     cholqr3(w, w.Y.d(), w.Yp.d(), 0, s);
-    rayleigh_ritz(w, G, r * r, w.Yp.d(), 0, s);
+    const double gtol_rel = vectors_for_reconstruction ? 0.0 : 1e-14;
+    rayleigh_ritz(w, G, r * r, w.Yp.d(), 0, s, gtol_rel);
 
     std::vector<double> th(b * batch), res(b * batch), coef(3 * batch), wm(b * batch),
         thp(b * batch, 0.0);
@@ -412,11 +414,12 @@ void subspace_eig_top(const double* G, int64_t r, int64_t batch, int64_t k, doub
                 while (L < k && rr[L] <= thr) ++L;  // locked prefix
             } else {
                 // basis Q: judged on eigenvalues / captured energy (SURVEY 8c
-                // rule 5) -> also lock Ritz values that moved < 1e-14 theta_1
-                // in the last iteration (linear convergence: remaining error
-                // well under the 1e-12 theta_1 parity bound)
+                // rule 5) -> also lock Ritz values that moved < 5e-13 theta_1
+                // in the last iteration (linear convergence, rate ~0.35 on the
+                // cfg5 noise plateau: remaining error ~0.5x the last move,
+                // under the 1e-12 theta_1 parity bound)
                 while (L < k && (rr[L] <= thr ||
-                                 (it >= 2 && std::fabs(t[L] - thp[sl * b + L]) <= 1e-13 * scale &&
+                                 (it >= 2 && std::fabs(t[L] - thp[sl * b + L]) <= 5e-13 * scale &&
                                   rr[L] <= 1e-6 * scale)))
                     ++L;
             }
@@ -520,7 +523,7 @@ void subspace_eig_top(const double* G, int64_t r, int64_t batch, int64_t k, doub
             PPC_CUDA_CHECK(cudaMemcpy2DAsync(Xn, sizeof(double) * per, w.X.d(), sizeof(double) * per,
                                              sizeof(double) * r * c0, batch, cudaMemcpyDeviceToDevice, s));
         cholqr3(w, Y, Xn, c0, s);
-        rayleigh_ritz(w, G, r * r, Xn, c0, s);
+        rayleigh_ritz(w, G, r * r, Xn, c0, s, gtol_rel);
     }
     // outputs: leading k Ritz pairs
     PPC_CUDA_CHECK(cudaMemcpy2DAsync(Xout, sizeof(double) * r * k, w.X.d(), sizeof(double) * per,
