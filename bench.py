@@ -123,6 +123,30 @@ def max_over_ranks(x, dist_on):
     return float(t.item())
 
 
+def ncu_traffic(workload, stage):
+    """DRAM bytes (read + write) per launch of the dominant kernel from the
+    committed ncu --set full capture (profiles/<round>/ncu_<stage>_<workload>_raw.csv)."""
+    import csv
+    import glob
+    names = {"gram_syrk": "ws_syrk", "facewise": "cfg4_gemms"}
+    key = names.get(stage, stage)
+    for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*", f"ncu_{key}*raw.csv")), reverse=True):
+        if workload not in os.path.basename(path) and stage != "facewise":
+            continue
+        try:
+            rows = list(csv.reader(open(path)))
+            hdr, units = rows[0], rows[1]
+            ir, iw = hdr.index("dram__bytes_read.sum"), hdr.index("dram__bytes_write.sum")
+            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+            r = rows[2]
+            tot = float(r[ir].replace(",", "")) * scale.get(units[ir], 1) + \
+                float(r[iw].replace(",", "")) * scale.get(units[iw], 1)
+            return tot, os.path.relpath(path, ROOT)
+        except Exception:
+            continue
+    return None, None
+
+
 def timing_report(L, reset=True):
     buf = C.create_string_buffer(1 << 16)
     rc = L.ppc_timing_report(buf, len(buf), 1 if reset else 0)
@@ -262,8 +286,9 @@ class Tsvdq:
         return self.in_bytes / sec / 1e9
 
     def dominant(self, stages):
-        best = max(stages.items(), key=lambda kv: kv[1]["ms"])[0] if stages else "gram_syrk"
-        return best, "tensor"
+        # the single most expensive kernel launch of the step (ncu launch
+        # list: the Gram SYRK); slice_svd is a composite of many kernels
+        return "gram_syrk", "tensor"
 
     def e2e_setup(self):
         torch = self.torch
@@ -351,8 +376,7 @@ class TsvdqSharded:
         return self.in_bytes / sec / 1e9 / self.world  # main() multiplies by world
 
     def dominant(self, stages):
-        best = max(stages.items(), key=lambda kv: kv[1]["ms"])[0] if stages else "gram_syrk"
-        return best, "tensor"
+        return "gram_syrk", "tensor"
 
     def e2e_setup(self):
         self.hA = flat_host(self.A)
@@ -504,9 +528,12 @@ def main():
     avg_ms = st["ms"] / max(1, st["n"])
     if bound == "tensor":
         achieved = (st["flops"] / max(1, st["n"])) / (avg_ms / 1e3) / 1e12
+        traffic, tsrc = ncu_traffic(args.workload, dom)
         roof = {"bound": "tensor", "achieved": achieved, "peak": peaks["fp64_tflops"],
-                "unit": "TFLOP/s", "frac": achieved / peaks["fp64_tflops"], "traffic": None,
-                "kernel": dom, "peak_source": peaks["fp64_src"] + " (FP64 DMMA; no tcgen05 f64 kind)"}
+                "unit": "TFLOP/s", "frac": achieved / peaks["fp64_tflops"], "traffic": traffic,
+                "algorithmic_bytes": st["bytes"] / max(1, st["n"]),
+                "kernel": dom, "peak_source": peaks["fp64_src"] + " (FP64 DMMA; no tcgen05 f64 kind)",
+                "traffic_source": tsrc}
     else:
         achieved = (st["bytes"] / max(1, st["n"])) / (avg_ms / 1e3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",

@@ -2,6 +2,7 @@
 // with the reference's checks and messages (thrown before any work starts, as
 // in tensor.cpp:140-142, decompositions.cpp:16-28, star_products.cpp:13-20),
 // then drives the device kernels on the calling thread's stream.
+#include <algorithm>
 #include <cmath>
 #include <string>
 
@@ -332,13 +333,60 @@ int ppc_tsvdq_compress(const double* A, int64_t n1, int64_t n2, int64_t n3, int6
         if (!re) fail(PPC_ARGUMENT, "null output");
         cudaStream_t s = stream();
         const int64_t N = n1 * n2;
-        In a(A, N * n3, loc);
-        require_finite(a.d, N * n3, "svd", s);
         Out q(Q, n3 * p, loc), sg(sigma, sigma ? p : 0, loc), u(U, n1 * k * p, loc),
             sv(S, k * p, loc), v(V, n2 * k * p, loc);
-        data_q(a.d, N, n3, p, q.d, sigma ? sg.d : nullptr, s);
-        tsvdq(a.d, n1, n2, n3, q.d, p, k, u.d, sv.d, v.d, s);
-        const auto r = recon_residual(a.d, n1, n2, n3, u.d, sv.d, v.d, q.d, p, k, s);
+        DeviceBuffer abuf;
+        const double* dA = A;
+        if (loc == PPC_HOST) {
+            // Stream the input in row-chunk groups on a copy stream and start
+            // each group's partial Grams as soon as it lands: the H2D of A
+            // overlaps the SYRK. Same chunks and tree as the resident path
+            // (bitwise identical Q).
+            if (!A) fail(PPC_ARGUMENT, "null input pointer");
+            abuf = DeviceBuffer(sizeof(double) * N * n3);
+            dA = abuf.d();
+            const GramPlan g = gram_plan(N, n3);
+            const int64_t per = std::min<int64_t>(g.chunks, 4);  // chunks per upload group
+            DeviceBuffer parts(sizeof(double) * g.chunks * n3 * n3), G(sizeof(double) * n3 * n3);
+            cudaStream_t cs = copy_stream();
+            {
+                // the staging buffer was allocated on s: order cs after it
+                cudaEvent_t ready;
+                PPC_CUDA_CHECK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+                PPC_CUDA_CHECK(cudaEventRecord(ready, s));
+                PPC_CUDA_CHECK(cudaStreamWaitEvent(cs, ready, 0));
+                PPC_CUDA_CHECK(cudaEventDestroy(ready));
+            }
+            {
+                StageTimer tm("gram_syrk", s, (double)N * n3 * n3, 8.0 * N * n3);
+                for (int64_t c0 = 0; c0 < g.chunks; c0 += per) {
+                    const int64_t r0 = c0 * g.chunk;
+                    if (r0 >= N) {  // plan chunks beyond N: zero partials
+                        PPC_CUDA_CHECK(cudaMemsetAsync(parts.d() + c0 * n3 * n3, 0,
+                                                       sizeof(double) * (g.chunks - c0) * n3 * n3, s));
+                        break;
+                    }
+                    const int64_t nr = std::min<int64_t>(per * g.chunk, N - r0);
+                    PPC_CUDA_CHECK(cudaMemcpy2DAsync(abuf.d() + r0, sizeof(double) * N, A + r0, sizeof(double) * N,
+                                                     sizeof(double) * nr, n3, cudaMemcpyHostToDevice, cs));
+                    cudaEvent_t ev;
+                    PPC_CUDA_CHECK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+                    PPC_CUDA_CHECK(cudaEventRecord(ev, cs));
+                    PPC_CUDA_CHECK(cudaStreamWaitEvent(s, ev, 0));
+                    PPC_CUDA_CHECK(cudaEventDestroy(ev));
+                    gram_chunks(abuf.d() + r0, N, nr, n3, g.chunk, std::min(per, g.chunks - c0),
+                                parts.d() + c0 * n3 * n3, s);
+                }
+                tree_reduce(parts.d(), g.chunks, n3 * n3, s);
+            }
+            require_finite(dA, N * n3, "svd", s);
+            eig_to_basis(parts.d(), n3, p, q.d, sigma ? sg.d : nullptr, s);
+        } else {
+            require_finite(dA, N * n3, "svd", s);
+            data_q(dA, N, n3, p, q.d, sigma ? sg.d : nullptr, s);
+        }
+        tsvdq(dA, n1, n2, n3, q.d, p, k, u.d, sv.d, v.d, s);
+        const auto r = recon_residual(dA, n1, n2, n3, u.d, sv.d, v.d, q.d, p, k, s);
         if (r[1] == 0.0) fail(PPC_DEGENERATE, "relative_error: reference tensor is zero");
         *re = std::sqrt(r[0]) / std::sqrt(r[1]);
         q.finish();

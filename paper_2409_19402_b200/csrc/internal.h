@@ -36,11 +36,13 @@ struct Context {
     cudaStream_t stream = nullptr;      // user stream (ppc_set_stream) or own
     bool stream_set = false;            // set explicitly (NULL = legacy default stream)
     cudaStream_t own_stream = nullptr;  // created lazily per device
+    cudaStream_t copy = nullptr;        // H2D staging stream
     int sms = 148;
     int64_t launches = 0;
 };
 Context& ctx();               // ensures a device is selected (throws PPC_NO_DEVICE)
 cudaStream_t stream();        // current stream of this thread
+cudaStream_t copy_stream();   // this thread's H2D staging stream (overlap)
 inline void count_launch(int n = 1) { ctx().launches += n; }
 void check_launch(const char* name);  // cudaGetLastError -> PPC_CUDA
 

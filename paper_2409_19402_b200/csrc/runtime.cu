@@ -76,6 +76,12 @@ cudaStream_t stream() {
     return c.own_stream;
 }
 
+cudaStream_t copy_stream() {
+    Context& c = ctx();
+    if (!c.copy) PPC_CUDA_CHECK(cudaStreamCreateWithFlags(&c.copy, cudaStreamNonBlocking));
+    return c.copy;
+}
+
 void check_launch(const char* name) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) fail(PPC_CUDA, std::string(name) + " launch: " + cudaGetErrorString(e));
@@ -175,6 +181,7 @@ int ppc_set_device(int device) {
             ppc::t_ctx.stream = nullptr;
             ppc::t_ctx.stream_set = false;
             ppc::t_ctx.own_stream = nullptr;
+            ppc::t_ctx.copy = nullptr;
         }
         ppc::init_device(device);
         return 0;

@@ -488,3 +488,17 @@ def test_ws_gram_and_residual_bitwise(engine, oracle):
     assert abs(r1 - r0) <= 1e-15 * r0  # residual partial sums grouped differently
     re = oracle.relative_error(a, oracle.tsvdq_reconstruct(*[engine.to_host(x) for x in (f.u, f.s, f.v)], q1))
     assert abs(r1 - re) <= 1e-12 * re
+
+
+def test_compress_host_streaming_matches_device(engine, oracle):
+    # ppc_tsvdq_compress with host buffers streams A in chunk groups and
+    # overlaps the upload with the Gram SYRK; results must equal the
+    # device-resident call bitwise (same chunks, same tree).
+    a = synth.cp_tensor(256, 256, 64, rank=10, noise=1e-3, seed=9)
+    fh, reh = engine.compress_tsvdq(a, 16, 8)
+    fd, red = engine.compress_tsvdq(engine.to_device(a), 16, 8)
+    assert np.array_equal(fh.transform.q, engine.to_host(fd.transform.q))
+    assert reh == red
+    U, S, V = oracle.tsvdq(a, fh.transform.q, 8)
+    reo = oracle.relative_error(a, oracle.tsvdq_reconstruct(U, S, V, fh.transform.q))
+    assert abs(reh - reo) <= 1e-10 * reo
