@@ -120,7 +120,7 @@ __device__ __forceinline__ void jacobi_round(double* W, int64_t R, double* Va, i
 __global__ void __launch_bounds__(1024, 1) jacobi_svd_kernel(const double* __restrict__ A, int64_t m, int64_t n,
                                   int64_t strideA, int64_t k, double* __restrict__ U,
                                   double* __restrict__ S, double* __restrict__ V, double* gws,
-                                  int use_smem, double* tail2, int* info, double gtol_rel) {
+                                  int use_smem, double* tail2, int* info, double gtol_rel, int max_sweeps) {
     extern __shared__ __align__(16) double sm[];
     __shared__ int s_rot;
     const int64_t b = blockIdx.x;
@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(1024, 1) jacobi_svd_kernel(const double* __res
         __syncthreads();
     }
     const double gtol = gtol_rel > 0.0 ? gtol_rel * s_gtol : 0.0;
-    for (; sweep < 60 && Cc > 1; ++sweep) {
+    for (; sweep < max_sweeps && Cc > 1; ++sweep) {
         if (tid == 0) s_rot = 0;
         __syncthreads();
         for (int64_t r = 0; r < P - 1; ++r) {
@@ -416,7 +416,8 @@ size_t jacobi_smem_bytes(int64_t m, int64_t n) {
 }
 
 void jacobi_svd(const double* A, int64_t m, int64_t n, int64_t strideA, int64_t batch, int64_t k,
-                double* U, double* S, double* V, double* tail2, cudaStream_t s, double gtol_rel) {
+                double* U, double* S, double* V, double* tail2, cudaStream_t s, double gtol_rel,
+                int sweep_cap) {
     if (batch == 0) return;
     static bool tol_set = false;
     if (!tol_set) {
@@ -433,7 +434,7 @@ void jacobi_svd(const double* A, int64_t m, int64_t n, int64_t strideA, int64_t 
     if (!use_smem && !U && !tail2 && m == n && (size_t)n * n * sizeof(double) <= 200 * 1024) {
         // eigen mode, W fits but W + V does not: logged rotations + replay
         const int64_t P = (n + 1) & ~int64_t(1);
-        const int64_t max_sweeps = 40;
+        const int64_t max_sweeps = sweep_cap > 0 ? std::min(sweep_cap, 40) : 40;
         DeviceBuffer lg(sizeof(double2) * batch * max_sweeps * (P - 1) * (P / 2)),
             ns(sizeof(int) * batch), sg(sizeof(double) * batch * n), rk(sizeof(int) * batch * n);
         const size_t wsm = (size_t)n * n * sizeof(double);
@@ -472,7 +473,8 @@ void jacobi_svd(const double* A, int64_t m, int64_t n, int64_t strideA, int64_t 
     static const bool dbg = std::getenv("PPC_JACOBI_DEBUG") != nullptr;
     DeviceBuffer dinfo(sizeof(int) * batch);
     jacobi_svd_kernel<<<(unsigned)batch, threads, use_smem ? smem : 0, s>>>(
-        A, m, n, strideA, k, U, S, V, ws.d(), use_smem ? 1 : 0, tail2, dinfo.as<int>(), gtol_rel);
+        A, m, n, strideA, k, U, S, V, ws.d(), use_smem ? 1 : 0, tail2, dinfo.as<int>(), gtol_rel,
+        sweep_cap > 0 ? sweep_cap : 60);
     count_launch();
     check_launch("jacobi_svd");
     if (dbg) {

@@ -307,7 +307,7 @@ void cholqr3(Work& w, double* Y, double* Xout, int64_t c0, cudaStream_t s) {
 // Rayleigh-Ritz on the orthonormal active columns [c0, b) of Xn: X, theta,
 // W = G X and residual norms for those columns (locked ones keep theirs).
 void rayleigh_ritz(Work& w, const double* G, int64_t sG, double* Xn, int64_t c0, cudaStream_t s,
-                   double gtol_rel) {
+                   double gtol_rel, int sweep_cap) {
     const int64_t r = w.r, b = w.b, batch = w.batch, bc = b - c0, per = r * b;
     StageTimer tm("ss.rayleigh_ritz", s);
     gg(G, r, sG, false, Xn + c0 * r, r, per, w.Z.d() + c0 * r, r, per, r, bc, r, batch, 1.0, 0.0, s);  // Z = G Xn
@@ -315,7 +315,8 @@ void rayleigh_ritz(Work& w, const double* G, int64_t sG, double* Xn, int64_t c0,
     {
         StageTimer tj("ss.rr_eig", s);
         // H (PSD) = Hv diag(theta) Hv^T by one-sided Jacobi (eigen mode)
-        jacobi_svd(w.S.d(), bc, bc, bc * bc, batch, bc, nullptr, w.P.d(), w.Hv.d(), nullptr, s, gtol_rel);
+        jacobi_svd(w.S.d(), bc, bc, bc * bc, batch, bc, nullptr, w.P.d(), w.Hv.d(), nullptr, s, gtol_rel,
+                   sweep_cap);
     }
     PPC_CUDA_CHECK(cudaMemcpy2DAsync(w.th.d() + c0, sizeof(double) * b, w.P.d(), sizeof(double) * bc,
                                      sizeof(double) * bc, batch, cudaMemcpyDeviceToDevice, s));
@@ -370,7 +371,8 @@ void subspace_eig_top(const double* G, int64_t r, int64_t batch, int64_t k, doub
     count_launch();
     cholqr3(w, w.Y.d(), w.Yp.d(), 0, s);
     const double gtol_rel = vectors_for_reconstruction ? 0.0 : 1e-14;
-    rayleigh_ritz(w, G, r * r, w.Yp.d(), 0, s, gtol_rel);
+    // early Rayleigh-Ritz steps only steer the filter: 4 Jacobi sweeps
+    rayleigh_ritz(w, G, r * r, w.Yp.d(), 0, s, gtol_rel, 4);
 
     std::vector<double> th(b * batch), res(b * batch), coef(3 * batch), wm(b * batch),
         thp(b * batch, 0.0);
@@ -523,7 +525,10 @@ void subspace_eig_top(const double* G, int64_t r, int64_t batch, int64_t k, doub
             PPC_CUDA_CHECK(cudaMemcpy2DAsync(Xn, sizeof(double) * per, w.X.d(), sizeof(double) * per,
                                              sizeof(double) * r * c0, batch, cudaMemcpyDeviceToDevice, s));
         cholqr3(w, Y, Xn, c0, s);
-        rayleigh_ritz(w, G, r * r, Xn, c0, s, gtol_rel);
+        // approximate Ritz pairs until something has converged (locking uses
+        // true residuals, so an inexact early Rayleigh-Ritz cannot lock early)
+        const bool early = it < 2 && c0 == 0;
+        rayleigh_ritz(w, G, r * r, Xn, c0, s, gtol_rel, early ? 4 : 0);
     }
     // outputs: leading k Ritz pairs
     PPC_CUDA_CHECK(cudaMemcpy2DAsync(Xout, sizeof(double) * r * k, w.X.d(), sizeof(double) * per,
