@@ -289,7 +289,7 @@ bool gemm_ws(const GemmDesc& d, int epi, const double* X, int64_t ldx, int64_t s
 void gemm(const GemmDesc& d, cudaStream_t s);
 // Fused residual: per-CTA partial sums of (X - alpha op(A)op(B))^2 and X^2.
 // Returns the number of CTAs (partials has room for 2*ctas doubles).
-int64_t gemm_residual_ctas(const GemmDesc& d);
+int64_t gemm_residual_ctas(const GemmDesc& d, const double* X, int64_t ldx, int64_t strideX);
 void gemm_residual(const GemmDesc& d, const double* X, int64_t ldx, int64_t strideX,
                    double* partials, cudaStream_t s);
 

@@ -106,7 +106,7 @@ __device__ __forceinline__ void ws_tile(const WsParams& P, int64_t w, int64_t& b
 template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, bool AK, bool BNM, int EPI>
 __global__ void __launch_bounds__((WARPS_M * WARPS_N + 1) * 32, 1)
     dmma_gemm_ws_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
-                        const WsParams P) {
+                        const __grid_constant__ CUtensorMap mapX, const WsParams P) {
     constexpr int NCW = WARPS_M * WARPS_N;  // consumer warps
     constexpr int WM = BM / WARPS_M, WN = BN / WARPS_N;
     constexpr int TM = WM / 8, TN = WN / 8;
@@ -114,14 +114,24 @@ __global__ void __launch_bounds__((WARPS_M * WARPS_N + 1) * 32, 1)
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double* As = reinterpret_cast<double*>(smem_raw);
     double* Bs = As + STAGES * BM * BK;
-    uint64_t* full = reinterpret_cast<uint64_t*>(Bs + STAGES * BK * BN);
+    // RESID: the tile's reference block X (BN columns of BM rows, [n][m])
+    // is staged by TMA right after the operand ring
+    constexpr bool XS = (EPI == EPI_RESID);
+    double* Xs = Bs + STAGES * BK * BN;
+    uint64_t* full = reinterpret_cast<uint64_t*>(Xs + (XS ? BM * BN : 0));
     uint64_t* empty = full + STAGES;
+    uint64_t* xfull = empty + STAGES;
+    uint64_t* xempty = xfull + 1;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], NCW);
+        }
+        if constexpr (XS) {
+            mbar_init(xfull, 1);
+            mbar_init(xempty, NCW);
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
     }
@@ -132,22 +142,26 @@ __global__ void __launch_bounds__((WARPS_M * WARPS_N + 1) * 32, 1)
         if (lane == 0) {
             asm volatile("prefetch.tensormap [%0];\n" ::"l"(&mapA));
             asm volatile("prefetch.tensormap [%0];\n" ::"l"(&mapB));
+            if constexpr (XS) asm volatile("prefetch.tensormap [%0];\n" ::"l"(&mapX));
             int stage = 0;
             unsigned phase = 0;
+            unsigned xphase = 0;
             for (int64_t w = blockIdx.x; w < P.total_tiles; w += gridDim.x) {
                 int64_t b, sp, mt, nt;
                 ws_tile(P, w, b, sp, mt, nt);
                 const int64_t kb = sp * P.kchunk, ke = min(P.K, kb + P.kchunk);
-                if constexpr (EPI == EPI_RESID) {
-                    // warm L2 with this tile's reference block: the epilogue
-                    // reads it after the k-loop (hides HBM latency)
-                    const int64_t m0 = mt * BM, n0 = nt * BN;
-                    const int64_t rows = min((int64_t)BM, P.M - m0);
-                    const unsigned bytes = (unsigned)(rows * 8) & ~15u;
-                    if (bytes && ((P.ldx & 1) == 0)) {
-                        const double* X = P.X + b * P.strideX + m0;
-                        for (int64_t n = n0; n < min(P.N, n0 + BN); ++n) prefetch_l2(X + n * P.ldx, bytes);
-                    }
+                if constexpr (XS) {
+                    // reference block of this tile -> Xs (after the previous
+                    // tile's epilogue released it); lands during the k-loop
+                    mbar_wait(xempty, xphase ^ 1);
+                    mbar_expect_tx(xfull, (unsigned)(BM * BN * 8));
+                    asm volatile(
+                        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes "
+                        "[%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"((unsigned)__cvta_generic_to_shared(Xs)),
+                        "l"(&mapX), "r"((int)(mt * BM)), "r"((int)(nt * BN)), "r"((int)b),
+                        "r"((unsigned)__cvta_generic_to_shared(xfull))
+                        : "memory");
+                    xphase ^= 1;
                 }
                 for (int64_t k0 = kb; k0 < ke; k0 += BK) {
                     mbar_wait(&empty[stage], phase ^ 1);
@@ -185,6 +199,7 @@ __global__ void __launch_bounds__((WARPS_M * WARPS_N + 1) * 32, 1)
     const int wm = warp % WARPS_M, wn = warp / WARPS_M;
     int stage = 0;
     unsigned phase = 0;
+    unsigned xph = 0;
     double sd = 0.0, sx = 0.0;  // RESID running sums (fixed tile order per CTA)
 
     for (int64_t w = blockIdx.x; w < P.total_tiles; w += gridDim.x) {
@@ -249,22 +264,25 @@ __global__ void __launch_bounds__((WARPS_M * WARPS_N + 1) * 32, 1)
                         }
                     }
         } else {
-            const double* X = P.X + b * P.strideX;
+            mbar_wait(xfull, xph);
+            xph ^= 1;
 #pragma unroll
             for (int i = 0; i < TM; ++i)
 #pragma unroll
                 for (int j = 0; j < TN; ++j)
 #pragma unroll
                     for (int e = 0; e < 2; ++e) {
-                        const int64_t m = m0 + wm * WM + i * 8 + g;
-                        const int64_t n = n0 + wn * WN + j * 8 + 2 * t + e;
-                        if (m < P.M && n < P.N) {
-                            const double x = X[m + n * P.ldx];
+                        const int ml = wm * WM + i * 8 + g;
+                        const int nl = wn * WN + j * 8 + 2 * t + e;
+                        if (m0 + ml < P.M && n0 + nl < P.N) {
+                            const double x = Xs[nl * BM + ml];
                             const double d = x - P.alpha * acc[i][j][e];
                             sd = fma(d, d, sd);
                             sx = fma(x, x, sx);
                         }
                     }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(xempty);
         }
     }
 

@@ -65,7 +65,7 @@ namespace {
 // Fused residual GEMM: {sum (X - alpha op(A)op(B))^2, sum X^2} as host doubles.
 std::array<double, 2> residual_sums(const GemmDesc& d, const double* X, int64_t ldx,
                                     int64_t strideX, cudaStream_t s) {
-    const int64_t ctas = gemm_residual_ctas(d);
+    const int64_t ctas = gemm_residual_ctas(d, X, ldx, strideX);
     DeviceBuffer part(sizeof(double) * 2 * (ctas + 1));
     gemm_residual(d, X, ldx, strideX, part.d(), s);
     double* fin = part.d() + 2 * ctas;
@@ -160,7 +160,7 @@ std::array<double, 2> recon_residual_block(const double* A_blk, int64_t n1, int6
     d.M = Nb; d.N = n3; d.K = p;
     d.A = ch.d(); d.lda = Nb;
     d.B = Q; d.ldb = n3; d.b_nmajor = true;
-    const int64_t ctas = gemm_residual_ctas(d);
+    const int64_t ctas = gemm_residual_ctas(d, A_blk, ldA, 0);
     DeviceBuffer part(sizeof(double) * 2 * (ctas + 1));
     gemm_residual(d, A_blk, ldA, 0, part.d(), s);
     double* fin = part.d() + 2 * ctas;

@@ -116,9 +116,9 @@ void gemm(const GemmDesc& d, cudaStream_t s) {
     launch(id, P, grid, d, vec2_ok(d, kchunk), EPI_STORE, s);
 }
 
-int64_t gemm_residual_ctas(const GemmDesc& d) {
+int64_t gemm_residual_ctas(const GemmDesc& d, const double* X, int64_t ldx, int64_t strideX) {
     int64_t ctas = 0;
-    if (d.allow_ws && gemm_ws(d, EPI_RESID, nullptr, 0, 0, nullptr, &ctas, nullptr)) return ctas;
+    if (d.allow_ws && gemm_ws(d, EPI_RESID, X, ldx, strideX, nullptr, &ctas, nullptr)) return ctas;
     grid_for(choose(d), d, &ctas);
     return ctas;
 }

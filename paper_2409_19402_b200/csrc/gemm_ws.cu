@@ -80,28 +80,46 @@ struct WsCfg {
     static constexpr size_t smem = (size_t)STAGES * (BM * 16 + 16 * BN) * 8 + 2 * STAGES * 8 + 128;
     static constexpr int threads = (WARPS_M * WARPS_N + 1) * 32;
     template <bool AK, bool BNM, int EPI>
-    static void launch(const CUtensorMap& a, const CUtensorMap& b, const WsParams& P, int grid, cudaStream_t s) {
+    static void launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& x, const WsParams& P,
+                       int grid, cudaStream_t s) {
         auto k = dmma_gemm_ws_kernel<BM, BN, 16, WARPS_M, WARPS_N, STAGES, AK, BNM, EPI>;
+        const size_t sm = smem + (EPI == EPI_RESID ? (size_t)BM * BN * 8 + 16 : 0);
         static bool set = false;
         if (!set) {
-            PPC_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            PPC_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
             set = true;
         }
-        k<<<grid, threads, smem, s>>>(a, b, P);
+        k<<<grid, threads, sm, s>>>(a, b, x, P);
     }
 };
 using WsL = WsCfg<128, 128, 2, 4, 5>;
+using WsR = WsCfg<128, 128, 2, 4, 3>;  // fused residual: 3 stages + the 128 KB X tile
 using WsM = WsCfg<128, 64, 4, 2, 6>;
 using WsT = WsCfg<128, 32, 4, 1, 8>;
 
 template <class Cfg>
-void dispatch(bool ak, bool bnm, int epi, const CUtensorMap& a, const CUtensorMap& b, const WsParams& P,
-              int grid, cudaStream_t s) {
-    if (!ak && !bnm && epi == EPI_STORE) return Cfg::template launch<false, false, EPI_STORE>(a, b, P, grid, s);
-    if (!ak && bnm && epi == EPI_STORE) return Cfg::template launch<false, true, EPI_STORE>(a, b, P, grid, s);
-    if (ak && !bnm && epi == EPI_STORE) return Cfg::template launch<true, false, EPI_STORE>(a, b, P, grid, s);
-    if (!ak && bnm && epi == EPI_RESID) return Cfg::template launch<false, true, EPI_RESID>(a, b, P, grid, s);
+void dispatch(bool ak, bool bnm, int epi, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& x,
+              const WsParams& P, int grid, cudaStream_t s) {
+    if (!ak && !bnm && epi == EPI_STORE) return Cfg::template launch<false, false, EPI_STORE>(a, b, x, P, grid, s);
+    if (!ak && bnm && epi == EPI_STORE) return Cfg::template launch<false, true, EPI_STORE>(a, b, x, P, grid, s);
+    if (ak && !bnm && epi == EPI_STORE) return Cfg::template launch<true, false, EPI_STORE>(a, b, x, P, grid, s);
     fail(PPC_ARGUMENT, "gemm_ws: unsupported variant");
+}
+
+// 3-D map of the residual reference X (M x N column-major, ld, batch stride):
+// box = one BM x BN tile, written to smem as [n][m].
+bool make_map_x(CUtensorMap* map, const double* X, int64_t M, int64_t N, int64_t ld, int64_t batch,
+                int64_t bstride, int bm, int bn) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[3] = {(cuuint64_t)M, (cuuint64_t)N, (cuuint64_t)batch};
+    cuuint64_t strides[2] = {(cuuint64_t)ld * 8, (cuuint64_t)(bstride ? bstride : ld * N) * 8};
+    cuuint32_t box[3] = {(cuuint32_t)bm, (cuuint32_t)bn, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    if (strides[0] % 16 || strides[1] % 16) return false;
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(X), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
@@ -143,7 +161,7 @@ bool gemm_ws(const GemmDesc& d, int epi, const double* X, int64_t ldx, int64_t s
     if (d.a_kmajor ? (d.K % 4 && !d.kshift) : (d.M % 4)) return false;
     if (d.b_nmajor ? (d.N % 4) : (d.K % 4 && !d.kshift)) return false;
     if (d.kshift && ((1LL << d.kshift) % bk)) return false;
-    CUtensorMap ma, mb;
+    CUtensorMap ma, mb, mx_;
     bool ok;
     if (!d.a_kmajor)
         ok = make_map(&ma, d.A, false, d.M, d.K, d.lda, map_batch, d.strideA, bm, bk, 0, 0);
@@ -171,12 +189,21 @@ bool gemm_ws(const GemmDesc& d, int epi, const double* X, int64_t ldx, int64_t s
     P.b_kblock = !d.b_nmajor ? d.kshift : 0;
     const int sms = ctx().sms;
     const int grid = (int)std::min<int64_t>(total, sms);
+    if (epi == EPI_RESID) {
+        // the fused residual stages X through shared memory: 128 x 128 tiles
+        if (cfg != 0 || d.zmap || !X || (ldx & 1) || (strideX & 1) || !al16(X)) return false;
+        if (!make_map_x(&mx_, X, d.M, d.N, ldx, d.batch, strideX, bm, bn)) return false;
+    }
     if (ctas_out) *ctas_out = grid;
     if (!partials && epi == EPI_RESID) return true;  // sizing query only
-    switch (cfg) {
-        case 0: dispatch<WsL>(d.a_kmajor, d.b_nmajor, epi, ma, mb, P, grid, s); break;
-        case 1: dispatch<WsM>(d.a_kmajor, d.b_nmajor, epi, ma, mb, P, grid, s); break;
-        default: dispatch<WsT>(d.a_kmajor, d.b_nmajor, epi, ma, mb, P, grid, s); break;
+    if (epi == EPI_RESID) {
+        WsR::launch<false, true, EPI_RESID>(ma, mb, mx_, P, grid, s);
+    } else {
+        switch (cfg) {
+            case 0: dispatch<WsL>(d.a_kmajor, d.b_nmajor, epi, ma, mb, ma, P, grid, s); break;
+            case 1: dispatch<WsM>(d.a_kmajor, d.b_nmajor, epi, ma, mb, ma, P, grid, s); break;
+            default: dispatch<WsT>(d.a_kmajor, d.b_nmajor, epi, ma, mb, ma, P, grid, s); break;
+        }
     }
     count_launch();
     check_launch("dmma_gemm_ws");

@@ -342,7 +342,7 @@ void slice_tail_energy(const double* A, int64_t m, int64_t n, int64_t stride, in
     d.A = us.d(); d.lda = m; d.strideA = m * k;
     d.B = V; d.ldb = n; d.strideB = n * k; d.b_nmajor = true;
     d.allow_ws = false;  // per-batch CTA groups are needed for the per-slice sums
-    const int64_t ctas = gemm_residual_ctas(d);
+    const int64_t ctas = gemm_residual_ctas(d, A, m, stride);
     DeviceBuffer part(sizeof(double) * 2 * ctas);
     gemm_residual(d, A, m, stride, part.d(), s);
     group_sum_kernel<<<(unsigned)batch, 256, 0, s>>>(part.d(), ctas / batch, tail2);
