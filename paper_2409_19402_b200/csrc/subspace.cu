@@ -57,13 +57,19 @@ __global__ void randn_kernel(double* X, int64_t n, uint64_t seed) {
     }
 }
 
-// Y_next = a*Z + b*Y + c*Yp with per-slice coefficients coef[3*slice + {0,1,2}].
+// Y_next = a*Z + b*Y + c*Yp with per-slice coefficients coef[3*slice + {0,1,2}];
+// columns below c0 (locked in every filtered slice) just carry Y.
 __global__ void cheb_kernel(double* __restrict__ Yn, const double* __restrict__ Z,
                             const double* __restrict__ Y, const double* __restrict__ Yp,
-                            const double* __restrict__ coef, int64_t per_slice, int64_t total) {
+                            const double* __restrict__ coef, int64_t per_slice, int64_t total,
+                            int64_t r, int64_t c0) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
         const int64_t s = i / per_slice;
+        if ((i - s * per_slice) / r < c0) {
+            Yn[i] = Y[i];
+            continue;
+        }
         const double a = coef[3 * s], b = coef[3 * s + 1], c = coef[3 * s + 2];
         double v = b * Y[i];
         if (a != 0.0) v += a * Z[i];  // frozen slices: Z is not computed for them
@@ -72,11 +78,11 @@ __global__ void cheb_kernel(double* __restrict__ Yn, const double* __restrict__ 
     }
 }
 
-// P(i, j, s) *= w(i, s)   (rows of the b x b block scaled: Theta_L mask)
-__global__ void scale_rows_kernel(double* P, const double* w, int64_t b, int64_t total) {
+// P(i, j, s) *= w(i, s)   (rows of the b x cols block scaled: Theta_L mask)
+__global__ void scale_rows_kernel(double* P, const double* w, int64_t b, int64_t cols, int64_t total) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
-        const int64_t row = i % b, s = i / (b * b);
+        const int64_t row = i % b, s = i / (b * cols);
         P[i] *= w[row + s * b];
     }
 }
@@ -260,9 +266,9 @@ struct Work {
 // General strided-batch GEMM on column panels: C = alpha op(A) B + beta C.
 void gg(const double* A, int64_t lda, int64_t sA, bool at, const double* B, int64_t ldb, int64_t sB,
         double* C, int64_t ldc, int64_t sC, int64_t M, int64_t N, int64_t K, int64_t batch,
-        double alpha, double beta, cudaStream_t s, const int* zmap = nullptr) {
+        double alpha, double beta, cudaStream_t s, const int* zmap = nullptr, int64_t zext = 0) {
     GemmDesc d;
-    d.M = M; d.N = N; d.K = K; d.batch = batch; d.zmap = zmap;
+    d.M = M; d.N = N; d.K = K; d.batch = batch; d.zmap = zmap; d.zmap_extent = zext;
     d.A = A; d.lda = lda; d.strideA = sA; d.a_kmajor = at;
     d.B = B; d.ldb = ldb; d.strideB = sB;
     d.C = C; d.ldc = ldc; d.strideC = sC;
@@ -329,6 +335,12 @@ void rayleigh_ritz(Work& w, const double* G, int64_t sG, double* Xn, int64_t c0,
 }
 
 }  // namespace
+
+// Chebyshev degree cap per outer iteration (runtime-tunable for experiments)
+static double max_degree() {
+    static const double v = std::getenv("PPC_CHEB_MAX") ? std::atof(std::getenv("PPC_CHEB_MAX")) : 10.0;
+    return v;
+}
 
 // tail2[z] = ||A_z - U_z diag(S_z) V_z^T||_F^2 (= the discarded energy sum_{j>=k} s_j^2
 // of slice z by Eckart-Young), via the fused residual GEMM.
@@ -443,11 +455,19 @@ void subspace_eig_top(const double* G, int64_t r, int64_t batch, int64_t k, doub
             // block's bottom (x = 1, T_d(1) = 1) kept <= 1e10;
             // (b) the spread inside the wanted active set (precision of the
             // smaller wanted components) kept <= 1e6.
-            double d = 10.0;
+            double d = max_degree();
             if (xt > 1.0) d = std::min(d, std::acosh(1e10) / std::acosh(xt));
             const double spread = std::acosh(xt) - std::acosh(xk);
             if (spread > 0) d = std::min(d, std::log(1e6) / spread);
             if (xk <= 1.0 + 1e-12) d = std::min(d, 2.0);  // no separation yet: gentle
+            // no more than this slice needs: the residuals of the unlocked
+            // wanted columns fall by ~exp(-acosh(x_k)) per degree
+            if (xk > 1.0 + 1e-12 && it >= 2) {
+                double rmax = 0.0;
+                for (int64_t j = L; j < k; ++j) rmax = std::max(rmax, rr[j]);
+                const double need = std::log(std::max(rmax / thr, 1.0)) / std::acosh(xk);
+                d = std::min(d, std::max(1.0, std::ceil(need) + 1.0));
+            }
             deg[sl] = std::max(1, (int)d);
             dmax = std::max(dmax, deg[sl]);
             if (dbg && (sl < 4 || it % 10 == 0))
@@ -487,19 +507,31 @@ void subspace_eig_top(const double* G, int64_t r, int64_t batch, int64_t k, doub
         double* Yn = w.Yn.d();
         {
             StageTimer tf("ss.filter", s);
+            // columns below the smallest locked prefix of the filtered slices
+            // are final: filter only [cf, b)
+            int64_t cf = b;
+            for (int64_t sl = 0; sl < batch; ++sl)
+                if (deg[sl] > 0) cf = std::min<int64_t>(cf, nlock[sl]);
+            if (cf >= b) cf = 0;
+            const int64_t bf = b - cf;
             for (int j = 0; j < dmax; ++j) {
                 // only the slices still filtering at this degree (compacted batch)
                 const int na = nact[j];
                 const int* zm = w.zmap.as<int>() + (int64_t)j * batch;
                 if (na > 0) {
-                    g_AB(G, Y, w.Z.d(), r, r, b, na, r * r, per, 1.0, nullptr, 0.0, s, zm, batch);  // Z = G Y
-                    g_AtB(w.X.d(), Y, w.P.d(), r, b, b, na, per, per, s, zm, batch);              // P = X^T Y
-                    scale_rows_kernel<<<grid1(b * b * batch), 256, 0, s>>>(w.P.d(), w.wmask.d(), b, b * b * batch);
+                    // Z = G Y, P = X^T Y, Z -= X diag(theta_L) P   (columns [cf, b))
+                    gg(G, r, r * r, false, Y + cf * r, r, per, w.Z.d() + cf * r, r, per, r, bf, r, na, 1.0, 0.0, s,
+                       zm, batch);
+                    gg(w.X.d(), r, per, true, Y + cf * r, r, per, w.P.d(), b, b * bf, b, bf, r, na, 1.0, 0.0, s,
+                       zm, batch);
+                    scale_rows_kernel<<<grid1(b * bf * batch), 256, 0, s>>>(w.P.d(), w.wmask.d(), b, bf,
+                                                                             b * bf * batch);
                     count_launch();
-                    g_AB(w.X.d(), w.P.d(), w.Z.d(), r, b, b, na, per, b * b, -1.0, w.Z.d(), 1.0, s, zm, batch);  // Z -= X P
+                    gg(w.X.d(), r, per, false, w.P.d(), b, b * bf, w.Z.d() + cf * r, r, per, r, bf, b, na, -1.0, 1.0,
+                       s, zm, batch);
                 }
                 cheb_kernel<<<grid1(per * batch), 256, 0, s>>>(Yn, w.Z.d(), Y, Yp, w.coef.d() + 3 * j * batch,
-                                                                per, per * batch);
+                                                                per, per * batch, r, cf);
                 count_launch();
                 check_launch("cheb");
                 double* t = Yp;  // rotate (Yp, Y, Yn) <- (Y, Yn, Yp)
