@@ -275,6 +275,16 @@ class Tsvdq:
 
     def step(self, L):
         n1, n2, n3, p, k = self.dims
+        if self.name == "cfg2":
+            # BASELINE configs[1]: tSVDQ at k in {1, 5, 10, 20} -> the sweep
+            ks = (C.c_int64 * 4)(1, 5, 10, 20)
+            ps = (C.c_int64 * 1)(p)
+            re = (C.c_double * 4)()
+            rc = L.ppc_tsvdq_sweep(ptr(self.A), n1, n2, n3, ps, 1, ks, 4, None, re, 1)
+            if rc:
+                raise RuntimeError(L.ppc_last_error().decode())
+            self.re = list(re)
+            return
         re = C.c_double()
         rc = L.ppc_tsvdq_compress(ptr(self.A), n1, n2, n3, p, k, ptr(self.Q), None, ptr(self.U),
                                   ptr(self.S), ptr(self.V), C.byref(re), 1)

@@ -183,6 +183,17 @@ int ppc_recon_residual_block(const double* A_blk, int64_t n1, int64_t nj, int64_
                              int64_t n2, int64_t j0, const double* Q, int64_t p, int64_t k,
                              double* sums, int loc);
 
+/* The `projprod sweep` loop (tools/main.cpp:299-341: relative error of the
+ * rank-k tSVDQ over a grid of (p, k)), amortized: one basis at
+ * max p (data-dependent bases of smaller p are its leading columns, exactly
+ * as data_dependent_transform(A, p) = U3(:,1:p); cf. verify.cpp:1149-1158),
+ * one slice SVD per transform-domain slice at max k (slice i does not depend
+ * on p), then one fused residual pass per (p, k). Q (n3 x max p) is used
+ * when non-null, else the data-driven basis is built. re (nk x np,
+ * column-major): re[ik + ip*nk]. Extents in ps / ks are host arrays. */
+int ppc_tsvdq_sweep(const double* A, int64_t n1, int64_t n2, int64_t n3, const int64_t* ps,
+                    int64_t np, const int64_t* ks, int64_t nk, const double* Q, double* re, int loc);
+
 /* The `projprod compress --method tsvdq --transform data` pipeline
  * (tools/main.cpp:186-283: data_dependent_transform -> tsvdq ->
  * tsvdq_reconstruct -> relative_error) as one call: A is staged once, the

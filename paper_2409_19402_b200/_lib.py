@@ -73,6 +73,7 @@ def lib() -> C.CDLL:
         "ppc_tree_reduce": (C.c_int, [vp, i64, i64, C.c_int]),
         "ppc_sym_eig_top": (C.c_int, [vp, i64, i64, vp, vp, C.c_int]),
         "ppc_recon_residual_block": (C.c_int, [vp, i64, i64, i64, i64, vp, vp, vp, i64, i64, vp, i64, i64, pd, C.c_int]),
+        "ppc_tsvdq_sweep": (C.c_int, [vp, i64, i64, i64, C.POINTER(i64), i64, C.POINTER(i64), i64, vp, vp, C.c_int]),
         "ppc_tsvdq_compress": (C.c_int, [vp, i64, i64, i64, i64, i64, vp, vp, vp, vp, vp, pd, C.c_int]),
     }
     for name, (res, args) in sig.items():

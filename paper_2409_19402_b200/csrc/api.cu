@@ -322,6 +322,43 @@ int ppc_recon_residual_block(const double* A_blk, int64_t n1, int64_t nj, int64_
     });
 }
 
+int ppc_tsvdq_sweep(const double* A, int64_t n1, int64_t n2, int64_t n3, const int64_t* ps, int64_t np,
+                    const int64_t* ks, int64_t nk, const double* Q, double* re, int loc) {
+    return guarded([&] {
+        validate_loc(loc);
+        check_tensor(n1, n2, n3);
+        if (np < 1 || nk < 1 || !ps || !ks || !re) fail(PPC_ARGUMENT, "sweep: empty p or k grid");
+        const int64_t kcap = std::min(n1, n2);
+        int64_t pmax = 0, kmax = 0;
+        for (int64_t i = 0; i < np; ++i) {  // tools/main.cpp:314-321 checks
+            if (ps[i] < 1 || ps[i] > n3)
+                fail(PPC_ARGUMENT, "p = " + std::to_string(ps[i]) + " exceeds n3 = " + std::to_string(n3));
+            pmax = std::max(pmax, ps[i]);
+        }
+        for (int64_t i = 0; i < nk; ++i) {
+            if (ks[i] < 1 || ks[i] > kcap)
+                fail(PPC_ARGUMENT, "k = " + std::to_string(ks[i]) + " exceeds min(n1,n2) = " + std::to_string(kcap));
+            kmax = std::max(kmax, ks[i]);
+        }
+        cudaStream_t s = stream();
+        const int64_t N = n1 * n2;
+        In a(A, N * n3, loc);
+        require_finite(a.d, N * n3, "svd", s);
+        DeviceBuffer qbuf;
+        const double* dQ;
+        if (Q) {
+            In qi(Q, n3 * pmax, loc);
+            qbuf = DeviceBuffer(sizeof(double) * n3 * pmax);
+            PPC_CUDA_CHECK(cudaMemcpyAsync(qbuf.d(), qi.d, sizeof(double) * n3 * pmax, cudaMemcpyDeviceToDevice, s));
+        } else {
+            qbuf = DeviceBuffer(sizeof(double) * n3 * pmax);
+            data_q(a.d, N, n3, pmax, qbuf.d(), nullptr, s);
+        }
+        dQ = qbuf.d();
+        sweep_errors(a.d, n1, n2, n3, dQ, pmax, kmax, ps, np, ks, nk, re, s);
+    });
+}
+
 int ppc_tsvdq_compress(const double* A, int64_t n1, int64_t n2, int64_t n3, int64_t p, int64_t k,
                        double* Q, double* sigma, double* U, double* S, double* V, double* re,
                        int loc) {

@@ -184,6 +184,46 @@ void tsvdq(const double* A, int64_t n1, int64_t n2, int64_t n3, const double* Q,
     }
 }
 
+void sweep_errors(const double* A, int64_t n1, int64_t n2, int64_t n3, const double* Q, int64_t pmax,
+                  int64_t kmax, const int64_t* ps, int64_t np, const int64_t* ks, int64_t nk, double* re,
+                  cudaStream_t s) {
+    const int64_t N = n1 * n2;
+    DeviceBuffer ah(sizeof(double) * N * pmax), U(sizeof(double) * n1 * kmax * pmax),
+        S(sizeof(double) * kmax * pmax), V(sizeof(double) * n2 * kmax * pmax);
+    mode3(A, N, n3, Q, pmax, true, ah.d(), 1.0, s);  // all slices at max p
+    require_finite(ah.d(), N * pmax, "svd", s);
+    {
+        StageTimer tm("slice_svd", s);
+        slice_svd(ah.d(), n1, n2, N, pmax, kmax, U.d(), S.d(), V.d(), nullptr, s);
+    }
+    ah = DeviceBuffer();
+    double anorm2[2];
+    sumsq(A, nullptr, N * n3, anorm2, s);
+    if (anorm2[1] == 0.0) fail(PPC_DEGENERATE, "relative_error: reference tensor is zero");
+    DeviceBuffer us(sizeof(double) * n1 * kmax * pmax), ch(sizeof(double) * N * pmax);
+    for (int64_t ip = 0; ip < np; ++ip) {
+        const int64_t p = ps[ip];
+        for (int64_t ik = 0; ik < nk; ++ik) {
+            const int64_t k = ks[ik];
+            StageTimer tm("recon_residual", s, 2.0 * p * N * k + 2.0 * N * p * n3, 8.0 * N * (p + n3));
+            // U(:, :k, i) diag(S(:k, i)) V(:, :k, i)^T for the first p slices
+            launch_scale_columns_strided(U.d(), S.d(), us.d(), n1, k, kmax, p, s);
+            GemmDesc d;
+            d.M = n1; d.N = n2; d.K = k; d.batch = p;
+            d.A = us.d(); d.lda = n1; d.strideA = n1 * k;
+            d.B = V.d(); d.ldb = n2; d.strideB = n2 * kmax; d.b_nmajor = true;
+            d.C = ch.d(); d.ldc = n1; d.strideC = N;
+            gemm(d, s);
+            GemmDesc r;
+            r.M = N; r.N = n3; r.K = p;
+            r.A = ch.d(); r.lda = N;
+            r.B = Q; r.ldb = n3; r.b_nmajor = true;
+            const auto sums = residual_sums(r, A, N, 0, s);
+            re[ik + ip * nk] = std::sqrt(sums[0]) / std::sqrt(sums[1]);
+        }
+    }
+}
+
 ErrorParts tsvdq_error(const double* A, int64_t n1, int64_t n2, int64_t n3, const double* U,
                        const double* S, const double* V, const double* Q, int64_t p, int64_t k,
                        cudaStream_t s) {

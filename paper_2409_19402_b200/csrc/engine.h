@@ -64,6 +64,10 @@ void reconstruct(const double* U, const double* S, const double* V, const double
 std::array<double, 2> recon_residual(const double* A, int64_t n1, int64_t n2, int64_t n3,
                                      const double* U, const double* S, const double* V,
                                      const double* Q, int64_t p, int64_t k, cudaStream_t s);
+// tools/main.cpp:299-341 sweep, amortized: re[ik + ip*nk] for every (p, k).
+void sweep_errors(const double* A, int64_t n1, int64_t n2, int64_t n3, const double* Q, int64_t pmax,
+                  int64_t kmax, const int64_t* ps, int64_t np, const int64_t* ks, int64_t nk, double* re,
+                  cudaStream_t s);
 struct ErrorParts {
     double total, eckart_young, projection;
 };

@@ -90,6 +90,16 @@ __global__ void scale_columns_kernel(const double* __restrict__ U, const double*
     }
 }
 
+__global__ void scale_columns_strided_kernel(const double* __restrict__ U, const double* __restrict__ S,
+                                             double* __restrict__ out, int64_t rows, int64_t k, int64_t kmax,
+                                             int64_t total) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
+        const int64_t r = i % rows, jb = i / rows, j = jb % k, b = jb / k;
+        out[i] = U[r + (j + b * kmax) * rows] * S[j + b * kmax];
+    }
+}
+
 __global__ void transpose_kernel(const double* __restrict__ in, double* __restrict__ out,
                                  int64_t rows, int64_t cols) {
     __shared__ double tile[32][33];
@@ -150,6 +160,15 @@ void launch_scale_columns(const double* U, const double* S, double* out, int64_t
     scale_columns_kernel<<<grid_for(total, 256), 256, 0, s>>>(U, S, out, rows, k, total);
     count_launch();
     check_launch("scale_columns");
+}
+
+void launch_scale_columns_strided(const double* U, const double* S, double* out, int64_t rows, int64_t k,
+                                  int64_t kmax, int64_t batch, cudaStream_t s) {
+    const int64_t total = rows * k * batch;
+    if (!total) return;
+    scale_columns_strided_kernel<<<grid_for(total, 256), 256, 0, s>>>(U, S, out, rows, k, kmax, total);
+    count_launch();
+    check_launch("scale_columns_strided");
 }
 
 void launch_transpose(const double* in, double* out, int64_t rows, int64_t cols, int64_t batch,

@@ -21,6 +21,10 @@ void launch_reduce_pairs(const double* partials, int64_t n, double* out, cudaStr
 // out(:, j, b) = U(:, j, b) * S(j, b) for a stack of `batch` rows x k blocks.
 void launch_scale_columns(const double* U, const double* S, double* out, int64_t rows,
                           int64_t k, int64_t batch, cudaStream_t s);
+// out(:, j, b) = U(:, j, b) * S(j, b) for j < k, where U / S carry kmax
+// columns per block (leading-k prefix of a wider factor stack).
+void launch_scale_columns_strided(const double* U, const double* S, double* out, int64_t rows, int64_t k,
+                                  int64_t kmax, int64_t batch, cudaStream_t s);
 // out(j, i, b) = in(i, j, b) for `batch` rows x cols blocks.
 void launch_transpose(const double* in, double* out, int64_t rows, int64_t cols, int64_t batch,
                       cudaStream_t s);

@@ -27,7 +27,7 @@ __all__ = [
     "FormatError", "EngineError", "Transform", "TsvdqFactors", "mode3_product",
     "facewise_product", "frobenius_norm", "svd", "truncated_svd", "data_dependent_transform",
     "projection_error", "star_q", "star_q_product", "tsvdq", "tsvdq_reconstruct", "tsvdq_error",
-    "relative_error", "tsvdq_relative_error", "compress_tsvdq", "to_device", "empty_device", "to_host",
+    "relative_error", "tsvdq_relative_error", "compress_tsvdq", "tsvdq_sweep", "to_device", "empty_device", "to_host",
     "launch_count",
 ]
 
@@ -436,6 +436,31 @@ def compress_tsvdq(a, p: int, k: int):
           C.byref(re), args.loc)
     t = Transform._from_q(to_host(q) if args.device else q, "data")
     return TsvdqFactors(U, S, V, t, k, n1, n2), re.value
+
+
+def tsvdq_sweep(a, ps, ks, transform=None):
+    """tools/main.cpp:299-341 `sweep` (relative error of the rank-k tSVDQ for
+    every (p, k)), amortized on the device: one basis (data-driven when
+    `transform` is None, else the transform's leading p columns), one slice
+    SVD per slice at max k, one fused residual per (p, k).
+    Returns an array re[ik, ip]."""
+    args = _Args(a)
+    a_, pa = args.inp(a, 3)
+    n1, n2, n3 = a_.shape
+    ps = [int(x) for x in ps]
+    ks = [int(x) for x in ks]
+    P = (C.c_int64 * len(ps))(*ps)
+    K = (C.c_int64 * len(ks))(*ks)
+    pq = None
+    if transform is not None:
+        q = transform.q if isinstance(transform, Transform) else transform
+        if args.device and not _is_dev(q):
+            q = to_device(q)
+        q_, pq = args.inp(q, 2)
+    re = np.empty((len(ks), len(ps)), order="F")
+    _call(args, _lib.lib().ppc_tsvdq_sweep, pa, n1, n2, n3, P, len(ps), K, len(ks), pq,
+          C.c_void_p(re.ctypes.data), args.loc)
+    return re
 
 
 def tsvdq_relative_error(a, f: TsvdqFactors) -> float:

@@ -502,3 +502,40 @@ def test_compress_host_streaming_matches_device(engine, oracle):
     U, S, V = oracle.tsvdq(a, fh.transform.q, 8)
     reo = oracle.relative_error(a, oracle.tsvdq_reconstruct(U, S, V, fh.transform.q))
     assert abs(reh - reo) <= 1e-10 * reo
+
+
+# ---------------------------------------------------------- sweep
+def test_sweep_vs_oracle(engine, oracle):
+    # cfg2 distribution (scaled frames), k in {1, 5, 10, 20} x p in {4, 12, 20}
+    a = synth.video(60, 80, 50, seed=12)
+    ps, ks = [4, 12, 20], [1, 5, 10, 20]
+    re = engine.tsvdq_sweep(a, ps, ks)
+    qmax, _, _ = oracle.data_dependent_q(a, 20)
+    for ip, p in enumerate(ps):
+        q = qmax[:, :p]  # data_dependent_transform(A, p) = U3(:, 1:p)
+        for ik, k in enumerate(ks):
+            U, S, V = oracle.tsvdq(a, q, k)
+            want = oracle.relative_error(a, oracle.tsvdq_reconstruct(U, S, V, q))
+            assert abs(re[ik, ip] - want) <= 1e-10 * want, (p, k)
+    # with a given basis; and the reference's grid checks
+    t = engine.Transform("dct", 50, 20)
+    re2 = engine.tsvdq_sweep(a, [20], [10], t)
+    f = engine.tsvdq(a, t, 10)
+    assert abs(re2[0, 0] - engine.tsvdq_relative_error(a, f)) <= 1e-12 * re2[0, 0]
+    with pytest.raises(engine.ArgumentError):
+        engine.tsvdq_sweep(a, [51], [1])
+    with pytest.raises(engine.ArgumentError):
+        engine.tsvdq_sweep(a, [4], [61])
+
+
+def test_sweep_large_slices(engine, oracle):
+    a = synth.video(240, 320, 30, seed=13)
+    ps, ks = [8, 16], [2, 12]
+    re = engine.tsvdq_sweep(a, ps, ks)
+    qmax, _, _ = oracle.data_dependent_q(a, 16)
+    for ip, p in enumerate(ps):
+        for ik, k in enumerate(ks):
+            q = qmax[:, :p]
+            U, S, V = oracle.tsvdq(a, q, k)
+            want = oracle.relative_error(a, oracle.tsvdq_reconstruct(U, S, V, q))
+            assert abs(re[ik, ip] - want) <= 1e-10 * want
