@@ -269,6 +269,12 @@ class Tsvdq:
         n1, n2, n3, p, k = self.dims
         desc = {"cfg5": "cfg5 rank-50 CP + N(0,1e-3^2) noise", "cfg3": "cfg3 hyperspectral",
                 "cfg2": "cfg2 video"}[self.name]
+        if self.name == "cfg2":
+            return {"workload": desc + " tSVDQ sweep with data-driven Q", "shape": [n1, n2, n3], "p": p,
+                    "k": [1, 5, 10, 20],
+                    "step": "ppc_tsvdq_sweep = data_dependent_transform + tsvdq + relative_error(A, recon) "
+                            "for every k (tools/main.cpp:299-341 cmd_sweep), slice SVDs shared at kmax",
+                    "l2": "input > L2" if self.in_bytes > 126e6 else "input < L2 (resident)"}
         return {"workload": desc + " tSVDQ with data-driven Q", "shape": [n1, n2, n3], "p": p,
                 "k": k, "step": "ppc_tsvdq_compress = data_dependent_transform + tsvdq + relative_error(A, recon) (tools/main.cpp:186-283)",
                 "l2": "input > L2" if self.in_bytes > 126e6 else "input < L2 (resident)"}
@@ -312,9 +318,19 @@ class Tsvdq:
         # H2D of A, D2H of Q + factors + the relative error
         self.h2d = 8 * n1 * n2 * n3
         self.d2h = 8 * (n3 * p + (n1 + n2 + 1) * k * p) + 8
+        if self.name == "cfg2":  # the sweep returns the RE grid only
+            self.d2h = 8 * 4
 
     def e2e_step(self, L):
         n1, n2, n3, p, k = self.dims
+        if self.name == "cfg2":
+            ks = (C.c_int64 * 4)(1, 5, 10, 20)
+            ps = (C.c_int64 * 1)(p)
+            re = (C.c_double * 4)()
+            rc = L.ppc_tsvdq_sweep(ptr(self.hA), n1, n2, n3, ps, 1, ks, 4, None, re, 0)
+            if rc:
+                raise RuntimeError(L.ppc_last_error().decode())
+            return
         re = C.c_double()
         rc = L.ppc_tsvdq_compress(ptr(self.hA), n1, n2, n3, p, k, ptr(self.hQ), None, ptr(self.hU),
                                   ptr(self.hS), ptr(self.hV), C.byref(re), 0)
@@ -340,6 +356,13 @@ class Tsvdq:
             a = synth.video(n1, n2, n3, seed=1)
         t0 = time.perf_counter()
         q, _, _ = ppo.data_dependent_q(a, p)
+        if self.name == "cfg2":  # cmd_sweep: one tsvdq + reconstruction per k
+            for kk in (1, 5, 10, 20):
+                U, S, V = ppo.tsvdq(a, q, kk)
+                re = ppo.relative_error(a, ppo.tsvdq_reconstruct(U, S, V, q))
+            sec = time.perf_counter() - t0
+            return (8.0 * s1 * s2 * n3) / sec / 1e9, (f"oracle data Q + tsvdq + RE for k in 1,5,10,20 on the "
+                                                      f"full {s1}x{s2}x{n3} video (p={p}), 1 rep")
         U, S, V = ppo.tsvdq(a, q, k)
         re = ppo.relative_error(a, ppo.tsvdq_reconstruct(U, S, V, q))
         sec = time.perf_counter() - t0

@@ -403,6 +403,86 @@ ApproxError tsvdq_error(const Tensor3& A, const TsvdqFactors& F) {  // decomposi
     return e;
 }
 
+Index TsvdqIIFactors::implicit_rank() const {  // decompositions.cpp:116-118
+    Index acc = 0;
+    for (Index r : multirank) acc += r;
+    return acc;
+}
+
+TsvdqIIFactors tsvdq2(const Tensor3& A, const Transform& T, double gamma) {  // decompositions.cpp:120-190
+    check_transform_match(A, T, "tsvdq2");
+    const Index p = T.p(), n1 = A.n1(), n2 = A.n2(), r = std::min(n1, n2);
+    std::vector<double> U(static_cast<std::size_t>(n1 * r * p)), S(static_cast<std::size_t>(r * p)),
+        V(static_cast<std::size_t>(n2 * r * p));
+    std::vector<int64_t> mr(static_cast<std::size_t>(p));
+    check(ppc_tsvdq2(A.data(), n1, n2, A.n3(), T.Q.data(), p, gamma, U.data(), S.data(), V.data(),
+                     mr.data(), PPC_HOST));
+    TsvdqIIFactors F;
+    F.gamma = gamma;
+    F.transform = T;
+    F.n1 = n1;
+    F.n2 = n2;
+    for (Index i = 0; i < p; ++i) {
+        const Index rho = mr[static_cast<std::size_t>(i)];
+        F.multirank.push_back(rho);
+        Matrix u(n1, rho), v(n2, rho);
+        Vector s(rho);
+        std::copy(U.data() + i * n1 * r, U.data() + i * n1 * r + n1 * rho, u.data());
+        std::copy(V.data() + i * n2 * r, V.data() + i * n2 * r + n2 * rho, v.data());
+        std::copy(S.data() + i * r, S.data() + i * r + rho, s.data());
+        F.Uhat.push_back(std::move(u));
+        F.shat.push_back(std::move(s));
+        F.Vhat.push_back(std::move(v));
+    }
+    return F;
+}
+
+namespace {
+// Ragged factors -> the padded stacks of ppc_tsvdq2_* (r = min(n1,n2) columns per slice).
+Stacks pack2(const TsvdqIIFactors& F, std::vector<int64_t>& mr) {
+    const Index p = F.transform.p(), r = std::min(F.n1, F.n2);
+    if (static_cast<Index>(F.Uhat.size()) != p || static_cast<Index>(F.Vhat.size()) != p ||
+        static_cast<Index>(F.shat.size()) != p || static_cast<Index>(F.multirank.size()) != p)
+        throw shape_error("tsvdq2 factors: stack length differs from the transform width");
+    Stacks s;
+    s.U.assign(static_cast<std::size_t>(F.n1 * r * p), 0.0);
+    s.S.assign(static_cast<std::size_t>(r * p), 0.0);
+    s.V.assign(static_cast<std::size_t>(F.n2 * r * p), 0.0);
+    mr.assign(F.multirank.begin(), F.multirank.end());
+    for (Index i = 0; i < p; ++i) {
+        const auto ui = static_cast<std::size_t>(i);
+        const Index rho = F.multirank[ui];
+        if (rho < 0 || rho > r || F.Uhat[ui].cols() != rho || F.Vhat[ui].cols() != rho ||
+            F.shat[ui].size() != rho)
+            throw shape_error("tsvdq2 factors: slice " + std::to_string(i) + " disagrees with its multirank");
+        std::copy(F.Uhat[ui].data(), F.Uhat[ui].data() + F.n1 * rho, s.U.data() + i * F.n1 * r);
+        std::copy(F.shat[ui].data(), F.shat[ui].data() + rho, s.S.data() + i * r);
+        std::copy(F.Vhat[ui].data(), F.Vhat[ui].data() + F.n2 * rho, s.V.data() + i * F.n2 * r);
+    }
+    return s;
+}
+}  // namespace
+
+Tensor3 tsvdq2_reconstruct(const TsvdqIIFactors& F) {  // decompositions.cpp:192-201
+    std::vector<int64_t> mr;
+    const Stacks s = pack2(F, mr);
+    Tensor3 out(F.n1, F.n2, F.transform.n3());
+    check(ppc_tsvdq2_reconstruct(s.U.data(), s.S.data(), s.V.data(), F.transform.Q.data(), F.n1, F.n2,
+                                 F.transform.n3(), F.transform.p(), mr.data(), out.data(), PPC_HOST));
+    return out;
+}
+
+ApproxError tsvdq2_error(const Tensor3& A, const TsvdqIIFactors& F) {  // decompositions.cpp:203-209
+    check_transform_match(A, F.transform, "tsvdq2_error");
+    std::vector<int64_t> mr;
+    const Stacks s = pack2(F, mr);
+    ApproxError e;
+    check(ppc_tsvdq2_error(A.data(), A.n1(), A.n2(), A.n3(), s.U.data(), s.S.data(), s.V.data(),
+                           F.transform.Q.data(), F.transform.p(), mr.data(), &e.total, &e.eckart_young,
+                           &e.projection, PPC_HOST));
+    return e;
+}
+
 Index star_q_rank(const Tensor3& A, const Transform& T, double tol_rel) {  // decompositions.cpp:105-114
     check_transform_match(A, T, "star_q_rank");
     const Index r = std::min(A.n1(), A.n2()), p = T.p();

@@ -161,6 +161,28 @@ int ppc_tsvdq_relative_error(const double* A, int64_t n1, int64_t n2, int64_t n3
                              const double* Q, int64_t p, int64_t k,
                              double* re, int loc);
 
+/* ---- tsvdq2: energy-truncated multirank ------------------ */
+/* decompositions.cpp:120-190 tsvdq2(A, T, gamma), gamma in (0,1]. Full
+ * transform-domain spectra on the device; the global descending sort (ties
+ * by slice, then position) and the prefix-energy cut over the p*r values on
+ * the host. The ragged per-slice factors of TsvdqIIFactors
+ * (decompositions.hpp:45-56) are returned padded to r = min(n1,n2) columns:
+ * U (n1,r,p), S (r,p), V (n2,r,p), zero beyond multirank[i]. multirank is a
+ * HOST array of p entries in every mode (it is bookkeeping, not data). */
+int ppc_tsvdq2(const double* A, int64_t n1, int64_t n2, int64_t n3,
+               const double* Q, int64_t p, double gamma,
+               double* U, double* S, double* V, int64_t* multirank, int loc);
+/* decompositions.cpp:192-201 on the padded factors above. */
+int ppc_tsvdq2_reconstruct(const double* U, const double* S, const double* V,
+                           const double* Q, int64_t n1, int64_t n2, int64_t n3,
+                           int64_t p, const int64_t* multirank, double* out, int loc);
+/* decompositions.cpp:203-209: eckart_young from fresh full spectra with the
+ * per-slice multirank; total fused as in ppc_tsvdq_error. */
+int ppc_tsvdq2_error(const double* A, int64_t n1, int64_t n2, int64_t n3,
+                     const double* U, const double* S, const double* V,
+                     const double* Q, int64_t p, const int64_t* multirank,
+                     double* total, double* eckart_young, double* projection, int loc);
+
 /* ---- shard-level building blocks (multi-GPU driver, dist.py) ------------ */
 /* Deterministic Gram plan for a tube matrix of N rows and n3 columns: the
  * number of row chunks (a power of two) and the chunk length. Depends on

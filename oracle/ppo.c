@@ -761,3 +761,84 @@ int ppo_relative_error(const double* A, const double* Ahat, int64_t count, doubl
     *re = sqrt(acc) / ref;
     return 0;
 }
+
+/* ------------------------------------------------------------- tsvdq2 */
+typedef struct { double value; int64_t slice, pos; } pool_entry;
+/* descending by value; ties by slice, then position (decompositions.cpp:148-150) */
+static int pool_cmp(const void* x, const void* y) {
+    const pool_entry* a = (const pool_entry*)x;
+    const pool_entry* b = (const pool_entry*)y;
+    if (a->value != b->value) return a->value > b->value ? -1 : 1;
+    if (a->slice != b->slice) return a->slice < b->slice ? -1 : 1;
+    if (a->pos != b->pos) return a->pos < b->pos ? -1 : 1;
+    return 0;
+}
+
+int ppo_tsvdq2(const double* A, int64_t n1, int64_t n2, int64_t n3,
+               const double* Q, int64_t p, double gamma,
+               double* U, double* S, double* V, int64_t* multirank) {
+    if (!(gamma > 0.0 && gamma <= 1.0))
+        return fail(PPO_ARGUMENT, "tsvdq2: gamma must lie in (0,1], got %g", gamma);
+    const int64_t N = n1 * n2, r = n1 < n2 ? n1 : n2;
+    double* Ah = (double*)malloc(sizeof(double) * N * p);
+    gemm('N', 'N', N, p, n3, 1.0, A, N, Q, n3, 0.0, Ah, N);
+    /* full SVDs of every slice (decompositions.cpp:126) */
+    svd_ctx c = {Ah, n1, n2, r, r, U, S, V, NULL, 0};
+    parallel_for(p, slice_svd_body, &c);
+    free(Ah);
+    if (c.err) return fail(c.err, "tsvdq2: slice svd failed");
+    /* pool of values above 1e-12 * global max (:137-145) */
+    double gmax = 0.0;
+    for (int64_t i = 0; i < p; ++i) if (S[i * r] > gmax) gmax = S[i * r];
+    const double cutoff = 1e-12 * gmax;
+    pool_entry* pool = (pool_entry*)malloc(sizeof(pool_entry) * (size_t)(p * r + 1));
+    int64_t np = 0;
+    for (int64_t i = 0; i < p; ++i)
+        for (int64_t j = 0; j < r; ++j)
+            if (S[j + i * r] > cutoff) pool[np++] = (pool_entry){S[j + i * r], i, j};
+    qsort(pool, (size_t)np, sizeof(pool_entry), pool_cmp);
+    /* prefix energy K (:154-167) */
+    double total = 0.0;
+    double* cum = (double*)malloc(sizeof(double) * (size_t)(np + 1));
+    for (int64_t i = 0; i < np; ++i) { total += pool[i].value * pool[i].value; cum[i] = total; }
+    int64_t K = 0;
+    if (total > 0.0) {
+        const double want = gamma * total;
+        while (K < np && cum[K] < want) ++K;
+        ++K;
+        if (K > np) K = np;
+    }
+    for (int64_t i = 0; i < p; ++i) multirank[i] = 0;
+    for (int64_t i = 0; i < K; ++i) multirank[pool[i].slice] += 1;
+    /* keep the leading multirank[i] triplets, zero the rest */
+    for (int64_t i = 0; i < p; ++i)
+        for (int64_t j = multirank[i]; j < r; ++j) {
+            S[j + i * r] = 0.0;
+            for (int64_t q = 0; q < n1; ++q) U[q + (j + i * r) * n1] = 0.0;
+            for (int64_t q = 0; q < n2; ++q) V[q + (j + i * r) * n2] = 0.0;
+        }
+    free(pool); free(cum);
+    return 0;
+}
+
+int ppo_tsvdq2_error(const double* A, int64_t n1, int64_t n2, int64_t n3,
+                     const double* U, const double* S, const double* V,
+                     const double* Q, int64_t p, const int64_t* multirank,
+                     double* total, double* eckart_young, double* projection) {
+    const int64_t N = n1 * n2, r = n1 < n2 ? n1 : n2;
+    double* s_all = (double*)malloc(sizeof(double) * r * p);
+    int rc = ppo_slice_spectra(A, n1, n2, n3, Q, p, s_all);
+    if (rc) { free(s_all); return rc; }
+    double tail = 0.0;
+    for (int64_t i = 0; i < p; ++i)
+        for (int64_t j = multirank[i]; j < r; ++j) tail += s_all[j + i * r] * s_all[j + i * r];
+    free(s_all);
+    double* rec = (double*)malloc(sizeof(double) * N * n3);
+    ppo_tsvdq_reconstruct(U, S, V, Q, n1, n2, n3, p, r, rec);
+    double acc = 0.0;
+    for (int64_t i = 0; i < N * n3; ++i) { double d = A[i] - rec[i]; acc += d * d; }
+    free(rec);
+    *total = sqrt(acc);
+    *eckart_young = sqrt(tail);
+    return ppo_projection_error(A, n1, n2, n3, Q, p, projection);
+}

@@ -84,6 +84,17 @@ int ppo_tsvdq_error(const double* A, int64_t n1, int64_t n2, int64_t n3,
  * s_all is (r, p). Used by tests for tail energies and tsvdq2. */
 int ppo_slice_spectra(const double* A, int64_t n1, int64_t n2, int64_t n3,
                       const double* Q, int64_t p, double* s_all);
+/* decompositions.cpp:120-209 tsvdq2: energy-truncated multirank. Factor
+ * stacks are padded to r = min(n1,n2) columns per slice (zero beyond
+ * multirank[i]); multirank has p entries. */
+int ppo_tsvdq2(const double* A, int64_t n1, int64_t n2, int64_t n3,
+               const double* Q, int64_t p, double gamma,
+               double* U, double* S, double* V, int64_t* multirank);
+/* decompositions.cpp:344-350: tail energies with the per-slice multirank. */
+int ppo_tsvdq2_error(const double* A, int64_t n1, int64_t n2, int64_t n3,
+                     const double* U, const double* S, const double* V,
+                     const double* Q, int64_t p, const int64_t* multirank,
+                     double* total, double* eckart_young, double* projection);
 /* metrics.cpp:21-28 */
 int ppo_relative_error(const double* A, const double* Ahat, int64_t count,
                        double* re);

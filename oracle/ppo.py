@@ -263,3 +263,31 @@ def relative_error(a, ahat):
     re = C.c_double()
     _chk(lib().ppo_relative_error(_p(a), _p(ahat), I(a.size), C.byref(re)))
     return re.value
+
+
+def tsvdq2(a, q, gamma):
+    """decompositions.cpp:120-209 -> (U (n1,r,p), S (r,p), V (n2,r,p), multirank (p,))
+    with r = min(n1, n2) and zero columns beyond each slice's rank."""
+    a, q = _f(a), _f(q)
+    n1, n2, n3 = a.shape
+    p = q.shape[1]
+    r = min(n1, n2)
+    U = np.empty((n1, r, p), order="F")
+    S = np.empty((r, p), order="F")
+    V = np.empty((n2, r, p), order="F")
+    mr = np.zeros(p, dtype=np.int64)
+    _chk(lib().ppo_tsvdq2(_p(a), I(n1), I(n2), I(n3), _p(q), I(p), C.c_double(gamma), _p(U), _p(S),
+                          _p(V), mr.ctypes.data_as(C.POINTER(C.c_int64))))
+    return U, S, V, mr
+
+
+def tsvdq2_error(a, U, S, V, q, multirank):
+    a, U, S, V, q = _f(a), _f(U), _f(S), _f(V), _f(q)
+    n1, n2, n3 = a.shape
+    p = q.shape[1]
+    mr = np.ascontiguousarray(multirank, dtype=np.int64)
+    t, e, pr = C.c_double(), C.c_double(), C.c_double()
+    _chk(lib().ppo_tsvdq2_error(_p(a), I(n1), I(n2), I(n3), _p(U), _p(S), _p(V), _p(q), I(p),
+                                mr.ctypes.data_as(C.POINTER(C.c_int64)), C.byref(t), C.byref(e),
+                                C.byref(pr)))
+    return t.value, e.value, pr.value

@@ -249,6 +249,78 @@ int ppc_tsvdq_relative_error(const double* A, int64_t n1, int64_t n2, int64_t n3
     });
 }
 
+namespace {
+
+void check_multirank(const int64_t* multirank, int64_t p, int64_t r, const char* who) {
+    if (!multirank) fail(PPC_ARGUMENT, std::string(who) + ": null multirank");
+    for (int64_t i = 0; i < p; ++i)
+        if (multirank[i] < 0 || multirank[i] > r)
+            fail(PPC_BOUNDS, std::string(who) + ": multirank[" + std::to_string(i) + "]=" +
+                                 std::to_string(multirank[i]) + " outside [0," + std::to_string(r) + "]");
+}
+
+}  // namespace
+
+int ppc_tsvdq2(const double* A, int64_t n1, int64_t n2, int64_t n3, const double* Q, int64_t p,
+               double gamma, double* U, double* S, double* V, int64_t* multirank, int loc) {
+    return guarded([&] {
+        validate_loc(loc);
+        check_tensor(n1, n2, n3);
+        check_transform(n3, p);  // decompositions.cpp:121
+        if (!(gamma > 0.0 && gamma <= 1.0))  // :122-124
+            fail(PPC_ARGUMENT, "tsvdq2: gamma must lie in (0,1], got " + std::to_string(gamma));
+        if (!multirank) fail(PPC_ARGUMENT, "tsvdq2: null multirank");
+        const int64_t r = std::min(n1, n2);
+        cudaStream_t s = stream();
+        In a(A, n1 * n2 * n3, loc), q(Q, n3 * p, loc);
+        Out u(U, n1 * r * p, loc), sv(S, r * p, loc), v(V, n2 * r * p, loc);
+        tsvdq2(a.d, n1, n2, n3, q.d, p, gamma, u.d, sv.d, v.d, multirank, s);
+        u.finish();
+        sv.finish();
+        v.finish();
+        if (loc == PPC_HOST) PPC_CUDA_CHECK(cudaStreamSynchronize(s));
+    });
+}
+
+int ppc_tsvdq2_reconstruct(const double* U, const double* S, const double* V, const double* Q,
+                           int64_t n1, int64_t n2, int64_t n3, int64_t p, const int64_t* multirank,
+                           double* out, int loc) {
+    return guarded([&] {
+        validate_loc(loc);
+        check_tensor(n1, n2, n3);
+        check_transform(n3, p);
+        const int64_t r = std::min(n1, n2);
+        check_multirank(multirank, p, r, "tsvdq2_reconstruct");
+        cudaStream_t s = stream();
+        In u(U, n1 * r * p, loc), sv(S, r * p, loc), v(V, n2 * r * p, loc), q(Q, n3 * p, loc);
+        Out o(out, n1 * n2 * n3, loc);
+        tsvdq2_reconstruct(u.d, sv.d, v.d, q.d, n1, n2, n3, p, multirank, o.d, s);
+        o.finish();
+        if (loc == PPC_HOST) PPC_CUDA_CHECK(cudaStreamSynchronize(s));
+    });
+}
+
+int ppc_tsvdq2_error(const double* A, int64_t n1, int64_t n2, int64_t n3, const double* U,
+                     const double* S, const double* V, const double* Q, int64_t p,
+                     const int64_t* multirank, double* total, double* eckart_young,
+                     double* projection, int loc) {
+    return guarded([&] {
+        validate_loc(loc);
+        check_tensor(n1, n2, n3);
+        check_transform(n3, p);  // decompositions.cpp:204
+        if (!total || !eckart_young || !projection) fail(PPC_ARGUMENT, "null output");
+        const int64_t r = std::min(n1, n2);
+        check_multirank(multirank, p, r, "tsvdq2_error");
+        cudaStream_t s = stream();
+        In a(A, n1 * n2 * n3, loc), u(U, n1 * r * p, loc), sv(S, r * p, loc), v(V, n2 * r * p, loc),
+            q(Q, n3 * p, loc);
+        const ErrorParts e = tsvdq2_error(a.d, n1, n2, n3, u.d, sv.d, v.d, q.d, p, multirank, s);
+        *total = e.total;
+        *eckart_young = e.eckart_young;
+        *projection = e.projection;
+    });
+}
+
 int ppc_gram_plan(int64_t N, int64_t n3, int64_t* chunks, int64_t* chunk) {
     return guarded([&] {
         if (N < 1 || n3 < 1) fail(PPC_SHAPE, "gram_plan: extents must be positive");

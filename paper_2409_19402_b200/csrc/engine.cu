@@ -104,32 +104,42 @@ void require_finite(const double* x, int64_t n, const char* who, cudaStream_t s)
 }
 
 void core_from_factors(const double* U, const double* S, const double* V, int64_t n1, int64_t n2,
-                       int64_t p, int64_t k, double* Chat, cudaStream_t s) {
+                       int64_t p, int64_t k, double* Chat, cudaStream_t s, int64_t kstride) {
+    if (kstride <= 0) kstride = k;
+    if (k == 0) {  // an all-zero multirank: the core is zero
+        PPC_CUDA_CHECK(cudaMemsetAsync(Chat, 0, sizeof(double) * n1 * n2 * p, s));
+        return;
+    }
     DeviceBuffer us(sizeof(double) * n1 * k * p);
-    launch_scale_columns(U, S, us.d(), n1, k, p, s);
+    if (kstride == k)
+        launch_scale_columns(U, S, us.d(), n1, k, p, s);
+    else
+        launch_scale_columns_strided(U, S, us.d(), n1, k, kstride, p, s);
     // Chat_i (n1 x n2) = US_i (n1 x k) * V_i^T: B(kk, n) = V_i[n + kk*n2]
     GemmDesc d;
     d.M = n1; d.N = n2; d.K = k; d.batch = p;
     d.A = us.d(); d.lda = n1; d.strideA = n1 * k;
-    d.B = V; d.ldb = n2; d.strideB = n2 * k; d.b_nmajor = true;
+    d.B = V; d.ldb = n2; d.strideB = n2 * kstride; d.b_nmajor = true;
     d.C = Chat; d.ldc = n1; d.strideC = n1 * n2;
     gemm(d, s);
 }
 
 void reconstruct(const double* U, const double* S, const double* V, const double* Q, int64_t n1,
-                 int64_t n2, int64_t n3, int64_t p, int64_t k, double* out, cudaStream_t s) {
+                 int64_t n2, int64_t n3, int64_t p, int64_t k, double* out, cudaStream_t s,
+                 int64_t kstride) {
     DeviceBuffer ch(sizeof(double) * n1 * n2 * p);
-    core_from_factors(U, S, V, n1, n2, p, k, ch.d(), s);
+    core_from_factors(U, S, V, n1, n2, p, k, ch.d(), s, kstride);
     mode3(ch.d(), n1 * n2, p, Q, n3, false, out, 1.0, s);
 }
 
 std::array<double, 2> recon_residual(const double* A, int64_t n1, int64_t n2, int64_t n3,
                                      const double* U, const double* S, const double* V,
-                                     const double* Q, int64_t p, int64_t k, cudaStream_t s) {
+                                     const double* Q, int64_t p, int64_t k, cudaStream_t s,
+                                     int64_t kstride) {
     const int64_t N = n1 * n2;
     StageTimer tm("recon_residual", s, 2.0 * p * N * k + 2.0 * N * p * n3, 8.0 * N * (p + n3));
     DeviceBuffer ch(sizeof(double) * N * p);
-    core_from_factors(U, S, V, n1, n2, p, k, ch.d(), s);
+    core_from_factors(U, S, V, n1, n2, p, k, ch.d(), s, kstride);
     GemmDesc d;
     d.M = N; d.N = n3; d.K = p;
     d.A = ch.d(); d.lda = N;
@@ -245,6 +255,111 @@ ErrorParts tsvdq_error(const double* A, int64_t n1, int64_t n2, int64_t n3, cons
     const auto pr = projection_residual(A, N, n3, Q, p, ah.d(), s);
     double ey = 0.0;
     for (int64_t i = 0; i < p; ++i) ey += th[i];  // decompositions.cpp:41-49 order (slice-major)
+    return ErrorParts{std::sqrt(tot[0]), std::sqrt(ey), std::sqrt(pr[0])};
+}
+
+void tsvdq2_select(const double* s_all, int64_t r, int64_t p, double gamma, int64_t* multirank) {
+    // :137-145 pool of values above 1e-12 * the global maximum
+    double gmax = 0.0;
+    for (int64_t i = 0; i < p; ++i)
+        if (r > 0) gmax = std::max(gmax, s_all[i * r]);
+    const double cutoff = 1e-12 * gmax;  // kDefaultRankTol (matrix_kernels.hpp)
+    struct Entry {
+        double value;
+        int64_t slice, pos;
+    };
+    std::vector<Entry> pool;
+    pool.reserve((size_t)(r * p));
+    for (int64_t i = 0; i < p; ++i)
+        for (int64_t j = 0; j < r; ++j)
+            if (s_all[j + i * r] > cutoff) pool.push_back({s_all[j + i * r], i, j});
+    // :148-150 descending by value, ties by slice then position
+    std::sort(pool.begin(), pool.end(), [](const Entry& a, const Entry& b) {
+        if (a.value != b.value) return a.value > b.value;
+        if (a.slice != b.slice) return a.slice < b.slice;
+        return a.pos < b.pos;
+    });
+    // :154-167 prefix energy in sorted order decides K
+    std::vector<double> cum(pool.size());
+    double acc = 0.0;
+    for (size_t i = 0; i < pool.size(); ++i) {
+        acc += pool[i].value * pool[i].value;
+        cum[i] = acc;
+    }
+    const double total = pool.empty() ? 0.0 : cum.back();
+    size_t K = 0;
+    if (total > 0.0) {
+        const double want = gamma * total;
+        while (K < pool.size() && cum[K] < want) ++K;
+        ++K;
+        K = std::min(K, pool.size());
+    }
+    for (int64_t i = 0; i < p; ++i) multirank[i] = 0;
+    for (size_t i = 0; i < K; ++i) multirank[pool[i].slice] += 1;
+}
+
+namespace {
+
+// All r = min(n1,n2) singular triplets of every transform-domain slice
+// (decompositions.cpp:31-37 slice_svds).
+void full_slice_svds(const double* A, int64_t n1, int64_t n2, int64_t n3, const double* Q, int64_t p,
+                     double* U, double* S, double* V, cudaStream_t s) {
+    const int64_t N = n1 * n2, r = std::min(n1, n2);
+    DeviceBuffer ah(sizeof(double) * N * p);
+    mode3(A, N, n3, Q, p, true, ah.d(), 1.0, s);
+    require_finite(ah.d(), N * p, "svd", s);
+    StageTimer tm("slice_svd", s, (double)p * r * r * std::max(n1, n2), 8.0 * p * N);
+    slice_svd(ah.d(), n1, n2, N, p, r, U, S, V, nullptr, s);
+}
+
+}  // namespace
+
+void tsvdq2(const double* A, int64_t n1, int64_t n2, int64_t n3, const double* Q, int64_t p,
+            double gamma, double* U, double* S, double* V, int64_t* multirank, cudaStream_t s) {
+    const int64_t r = std::min(n1, n2);
+    full_slice_svds(A, n1, n2, n3, Q, p, U, S, V, s);  // :125-126
+    std::vector<double> sh((size_t)(r * p));
+    PPC_CUDA_CHECK(cudaMemcpyAsync(sh.data(), S, sizeof(double) * r * p, cudaMemcpyDeviceToHost, s));
+    PPC_CUDA_CHECK(cudaStreamSynchronize(s));
+    tsvdq2_select(sh.data(), r, p, gamma, multirank);
+    // :178-188 keep the leading multirank[i] triplets of slice i
+    DeviceBuffer rk(sizeof(int64_t) * p);
+    PPC_CUDA_CHECK(cudaMemcpyAsync(rk.d(), multirank, sizeof(int64_t) * p, cudaMemcpyHostToDevice, s));
+    launch_truncate_columns(U, n1, r, p, rk.as<int64_t>(), s);
+    launch_truncate_columns(S, 1, r, p, rk.as<int64_t>(), s);
+    launch_truncate_columns(V, n2, r, p, rk.as<int64_t>(), s);
+    PPC_CUDA_CHECK(cudaStreamSynchronize(s));  // rk and the pageable multirank outlive the copy
+}
+
+void tsvdq2_reconstruct(const double* U, const double* S, const double* V, const double* Q,
+                        int64_t n1, int64_t n2, int64_t n3, int64_t p, const int64_t* multirank,
+                        double* out, cudaStream_t s) {
+    const int64_t r = std::min(n1, n2);
+    int64_t kmax = 0;
+    for (int64_t i = 0; i < p; ++i) kmax = std::max(kmax, multirank[i]);
+    reconstruct(U, S, V, Q, n1, n2, n3, p, kmax, out, s, r);
+}
+
+ErrorParts tsvdq2_error(const double* A, int64_t n1, int64_t n2, int64_t n3, const double* U,
+                        const double* S, const double* V, const double* Q, int64_t p,
+                        const int64_t* multirank, cudaStream_t s) {
+    const int64_t N = n1 * n2, r = std::min(n1, n2);
+    // :205-206 fresh full slice spectra for the tail energies
+    std::vector<double> sh((size_t)(r * p));
+    {
+        DeviceBuffer u(sizeof(double) * n1 * r * p), sv(sizeof(double) * r * p),
+            v(sizeof(double) * n2 * r * p);
+        full_slice_svds(A, n1, n2, n3, Q, p, u.d(), sv.d(), v.d(), s);
+        PPC_CUDA_CHECK(cudaMemcpyAsync(sh.data(), sv.d(), sizeof(double) * r * p, cudaMemcpyDeviceToHost, s));
+        PPC_CUDA_CHECK(cudaStreamSynchronize(s));
+    }
+    double ey = 0.0;  // decompositions.cpp:41-49 order: slice-major, position ascending
+    for (int64_t i = 0; i < p; ++i)
+        for (int64_t j = multirank[i]; j < r; ++j) ey += sh[j + i * r] * sh[j + i * r];
+    int64_t kmax = 0;
+    for (int64_t i = 0; i < p; ++i) kmax = std::max(kmax, multirank[i]);
+    const auto tot = recon_residual(A, n1, n2, n3, U, S, V, Q, p, kmax, s, r);
+    const auto pr = projection_residual(A, N, n3, Q, p, nullptr, s);
     return ErrorParts{std::sqrt(tot[0]), std::sqrt(ey), std::sqrt(pr[0])};
 }
 

@@ -55,15 +55,19 @@ bool data_q(const double* T, int64_t N, int64_t n3, int64_t p, double* Q, double
 void tsvdq(const double* A, int64_t n1, int64_t n2, int64_t n3, const double* Q, int64_t p,
            int64_t k, double* U, double* S, double* V, cudaStream_t s);
 // Chat (n1 x n2 x p) = U diag(S) V^T facewise             [decompositions.cpp:88-92]
+// over the leading k columns of factor stacks that carry kstride >= k
+// columns per slice (kstride 0 = k).
 void core_from_factors(const double* U, const double* S, const double* V, int64_t n1, int64_t n2,
-                       int64_t p, int64_t k, double* Chat, cudaStream_t s);
+                       int64_t p, int64_t k, double* Chat, cudaStream_t s, int64_t kstride = 0);
 // decompositions.cpp:85-94
 void reconstruct(const double* U, const double* S, const double* V, const double* Q, int64_t n1,
-                 int64_t n2, int64_t n3, int64_t p, int64_t k, double* out, cudaStream_t s);
+                 int64_t n2, int64_t n3, int64_t p, int64_t k, double* out, cudaStream_t s,
+                 int64_t kstride = 0);
 // {||A - recon(F)||^2, ||A||^2} without materializing recon(F).
 std::array<double, 2> recon_residual(const double* A, int64_t n1, int64_t n2, int64_t n3,
                                      const double* U, const double* S, const double* V,
-                                     const double* Q, int64_t p, int64_t k, cudaStream_t s);
+                                     const double* Q, int64_t p, int64_t k, cudaStream_t s,
+                                     int64_t kstride = 0);
 // tools/main.cpp:299-341 sweep, amortized: re[ik + ip*nk] for every (p, k).
 void sweep_errors(const double* A, int64_t n1, int64_t n2, int64_t n3, const double* Q, int64_t pmax,
                   int64_t kmax, const int64_t* ps, int64_t np, const int64_t* ks, int64_t nk, double* re,
@@ -75,5 +79,23 @@ struct ErrorParts {
 ErrorParts tsvdq_error(const double* A, int64_t n1, int64_t n2, int64_t n3, const double* U,
                        const double* S, const double* V, const double* Q, int64_t p, int64_t k,
                        cudaStream_t s);
+
+// decompositions.cpp:120-190 tsvdq2 (energy-truncated multirank). Full slice
+// spectra on the device; the global sort and prefix-energy cut over the
+// p*r values on the host. Factor stacks padded to r = min(n1,n2) columns
+// per slice, zero beyond multirank[i] (host array, p entries).
+void tsvdq2(const double* A, int64_t n1, int64_t n2, int64_t n3, const double* Q, int64_t p,
+            double gamma, double* U, double* S, double* V, int64_t* multirank, cudaStream_t s);
+// The selection alone (decompositions.cpp:131-176): multirank from the full
+// spectra s_all (r x p, host, descending per slice).
+void tsvdq2_select(const double* s_all, int64_t r, int64_t p, double gamma, int64_t* multirank);
+// decompositions.cpp:192-201 on padded factors (only max(multirank) columns used).
+void tsvdq2_reconstruct(const double* U, const double* S, const double* V, const double* Q,
+                        int64_t n1, int64_t n2, int64_t n3, int64_t p, const int64_t* multirank,
+                        double* out, cudaStream_t s);
+// decompositions.cpp:203-209
+ErrorParts tsvdq2_error(const double* A, int64_t n1, int64_t n2, int64_t n3, const double* U,
+                        const double* S, const double* V, const double* Q, int64_t p,
+                        const int64_t* multirank, cudaStream_t s);
 
 }  // namespace ppc

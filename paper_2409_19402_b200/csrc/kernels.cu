@@ -100,6 +100,15 @@ __global__ void scale_columns_strided_kernel(const double* __restrict__ U, const
     }
 }
 
+__global__ void truncate_columns_kernel(double* __restrict__ X, int64_t rows, int64_t r,
+                                        const int64_t* __restrict__ rank, int64_t total) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
+        const int64_t jb = i / rows, j = jb % r, b = jb / r;
+        if (j >= rank[b]) X[i] = 0.0;
+    }
+}
+
 __global__ void transpose_kernel(const double* __restrict__ in, double* __restrict__ out,
                                  int64_t rows, int64_t cols) {
     __shared__ double tile[32][33];
@@ -169,6 +178,15 @@ void launch_scale_columns_strided(const double* U, const double* S, double* out,
     scale_columns_strided_kernel<<<grid_for(total, 256), 256, 0, s>>>(U, S, out, rows, k, kmax, total);
     count_launch();
     check_launch("scale_columns_strided");
+}
+
+void launch_truncate_columns(double* X, int64_t rows, int64_t r, int64_t batch, const int64_t* rank,
+                             cudaStream_t s) {
+    const int64_t total = rows * r * batch;
+    if (!total) return;
+    truncate_columns_kernel<<<grid_for(total, 256), 256, 0, s>>>(X, rows, r, rank, total);
+    count_launch();
+    check_launch("truncate_columns");
 }
 
 void launch_transpose(const double* in, double* out, int64_t rows, int64_t cols, int64_t batch,

@@ -25,6 +25,10 @@ void launch_scale_columns(const double* U, const double* S, double* out, int64_t
 // columns per block (leading-k prefix of a wider factor stack).
 void launch_scale_columns_strided(const double* U, const double* S, double* out, int64_t rows, int64_t k,
                                   int64_t kmax, int64_t batch, cudaStream_t s);
+// X(:, j, b) = 0 for rank[b] <= j < r: the tail of each block of a padded
+// (rows, r, batch) factor stack (rank is a device array of batch entries).
+void launch_truncate_columns(double* X, int64_t rows, int64_t r, int64_t batch, const int64_t* rank,
+                             cudaStream_t s);
 // out(j, i, b) = in(i, j, b) for `batch` rows x cols blocks.
 void launch_transpose(const double* in, double* out, int64_t rows, int64_t cols, int64_t batch,
                       cudaStream_t s);

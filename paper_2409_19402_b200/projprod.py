@@ -27,7 +27,8 @@ __all__ = [
     "FormatError", "EngineError", "Transform", "TsvdqFactors", "mode3_product",
     "facewise_product", "frobenius_norm", "svd", "truncated_svd", "data_dependent_transform",
     "projection_error", "star_q", "star_q_product", "tsvdq", "tsvdq_reconstruct", "tsvdq_error",
-    "relative_error", "tsvdq_relative_error", "compress_tsvdq", "tsvdq_sweep", "to_device", "empty_device", "to_host",
+    "relative_error", "tsvdq_relative_error", "TsvdqIIFactors", "tsvdq2", "tsvdq2_reconstruct",
+    "tsvdq2_error", "compress_tsvdq", "tsvdq_sweep", "to_device", "empty_device", "to_host",
     "launch_count",
 ]
 
@@ -405,6 +406,99 @@ def tsvdq_error(a, f: TsvdqFactors):
     t, e, pr = C.c_double(), C.c_double(), C.c_double()
     _call(args, _lib.lib().ppc_tsvdq_error, pa, n1, n2, n3, pu, ps, pv, pq, p, k, C.byref(t),
           C.byref(e), C.byref(pr), args.loc)
+    return t.value, e.value, pr.value
+
+
+@dataclass
+class TsvdqIIFactors:
+    """decompositions.hpp:45-56 (bindings.cpp:132-142). The ragged per-slice
+    factors are held padded to r = min(n1, n2) columns: u (n1, r, p), s (r, p),
+    v (n2, r, p), zero beyond multirank[i]; uhat(i)/shat(i)/vhat(i) give the
+    reference's ragged views."""
+
+    u: object
+    s: object
+    v: object
+    multirank: np.ndarray
+    gamma: float
+    transform: Transform
+    n1: int = field(default=0)
+    n2: int = field(default=0)
+
+    @property
+    def implicit_rank(self) -> int:
+        """decompositions.cpp:116-118: kappa = sum of the multirank."""
+        return int(np.sum(self.multirank))
+
+    def uhat(self, i):
+        return self.u[:, : int(self.multirank[i]), i]
+
+    def shat(self, i):
+        return self.s[: int(self.multirank[i]), i]
+
+    def vhat(self, i):
+        return self.v[:, : int(self.multirank[i]), i]
+
+
+def _i64p(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_int64))
+
+
+def tsvdq2(a, t: Transform, gamma: float) -> TsvdqIIFactors:
+    """decompositions.cpp:120-190 (energy-truncated multirank tSVDQ)."""
+    args = _Args(a)
+    a_, pa = args.inp(a, 3)
+    q_, pq = _q_of(t, args)
+    n1, n2, n3 = a_.shape
+    if q_.shape[0] != n3:
+        raise ShapeError(f"tsvdq2: transform length {q_.shape[0]} != tensor n3 {n3}")
+    p = q_.shape[1]
+    r = min(n1, n2)
+    U, pu = args.out((n1, r, p))
+    S, ps = args.out((r, p))
+    V, pv = args.out((n2, r, p))
+    mr = np.zeros(p, dtype=np.int64)
+    _call(args, _lib.lib().ppc_tsvdq2, pa, n1, n2, n3, pq, p, C.c_double(gamma), pu, ps, pv,
+          _i64p(mr), args.loc)
+    return TsvdqIIFactors(U, S, V, mr, float(gamma), t, n1, n2)
+
+
+def _multirank(f: TsvdqIIFactors, p: int) -> np.ndarray:
+    mr = np.ascontiguousarray(f.multirank, dtype=np.int64)
+    if mr.shape != (p,):
+        raise ShapeError(f"tsvdq2: multirank has {mr.size} entries, transform p={p}")
+    return mr
+
+
+def tsvdq2_reconstruct(f: TsvdqIIFactors):
+    """decompositions.cpp:192-201."""
+    args = _Args(f.u, f.s, f.v)
+    u_, s_, v_, q_, pu, ps, pv, pq = _factor_args(f, args)
+    n1, _, p = u_.shape
+    n2 = v_.shape[0]
+    n3 = q_.shape[0]
+    mr = _multirank(f, p)
+    out, po = args.out((n1, n2, n3))
+    _call(args, _lib.lib().ppc_tsvdq2_reconstruct, pu, ps, pv, pq, n1, n2, n3, p, _i64p(mr), po,
+          args.loc)
+    return out
+
+
+def tsvdq2_error(a, f: TsvdqIIFactors):
+    """decompositions.cpp:203-209 -> (total, eckart_young, projection)."""
+    args = _Args(a, f.u, f.s, f.v)
+    a_, pa = args.inp(a, 3)
+    u_, s_, v_, q_, pu, ps, pv, pq = _factor_args(f, args)
+    n1, n2, n3 = a_.shape
+    if q_.shape[0] != n3:
+        raise ShapeError(f"tsvdq2_error: transform length {q_.shape[0]} != tensor n3 {n3}")
+    if u_.shape[0] != n1 or v_.shape[0] != n2:
+        raise ShapeError("tsvdq2_error: factors do not match the tensor")
+    p = q_.shape[1]
+    mr = _multirank(f, p)
+    t, e, pr = C.c_double(), C.c_double(), C.c_double()
+    _call(args, _lib.lib().ppc_tsvdq2_error, pa, n1, n2, n3, pu, ps, pv, pq, p, _i64p(mr),
+          C.byref(t), C.byref(e), C.byref(pr), args.loc)
     return t.value, e.value, pr.value
 
 

@@ -184,6 +184,64 @@ int main() {
         Matrix Q = orthonormalize(Matrix::Identity(4, 2) + 0.1 * Matrix::Identity(4, 2));
         CHECK((Q.transpose() * Q - Matrix::Identity(2, 2)).norm() <= 1e-12);
     }
+    // test_decompositions.cpp:126-146 — tsvdq2 keeps everything at gamma = 1
+    {
+        Tensor3 A = seeded(4, 5, 6, 44);
+        Transform T = dct_transform(6, 4);
+        TsvdqIIFactors F = tsvdq2(A, T, 1.0);
+        Tensor3 Ahat = mode3_product(A, T.Q.transpose());
+        for (Index i = 0; i < 4; ++i)
+            CHECK(F.multirank[(size_t)i] == numerical_rank(svd(Ahat.slice(i)).s, kDefaultRankTol));
+        ApproxError e = tsvdq2_error(A, F);
+        CHECK(std::fabs(e.total - projection_error(A, T)) <= 1e-10 * frobenius_norm(A));
+        CHECK(e.eckart_young <= 1e-10 * frobenius_norm(A));
+        check_throws<argument_error>([&] { tsvdq2(A, T, 0.0); }, "gamma 0");
+        check_throws<argument_error>([&] { tsvdq2(A, T, 1.5); }, "gamma 1.5");
+    }
+    // test_decompositions.cpp:148-160 — tie-break on the 2x2x2 fixture
+    {
+        TsvdqIIFactors F = tsvdq2(counterexample(), identity_transform(2, 2), 0.5);
+        CHECK(F.implicit_rank() == 2 && F.multirank[0] == 2 && F.multirank[1] == 0);
+        ApproxError e = tsvdq2_error(counterexample(), F);
+        CHECK(std::fabs(e.total * e.total - 2.0) <= 1e-12);
+    }
+    // test_decompositions.cpp:162-177 — exact-rank slices reproduce tsvdq
+    {
+        Transform T = dct_transform(5, 3);
+        Tensor3 Ahat(4, 4, 3);  // rank-2 transform-domain slices, lifted by Q
+        for (Index i = 0; i < 3; ++i) {
+            Tensor3 u = seeded(4, 2, 1, 60 + (unsigned)i), v = seeded(4, 2, 1, 70 + (unsigned)i);
+            Matrix m(4, 4);
+            for (Index a = 0; a < 4; ++a)
+                for (Index b = 0; b < 4; ++b)
+                    m(a, b) = u(a, 0, 0) * v(b, 0, 0) + u(a, 1, 0) * v(b, 1, 0);
+            Ahat.set_slice(i, m);
+        }
+        Tensor3 A = mode3_product(Ahat, T.Q);
+        TsvdqIIFactors F2 = tsvdq2(A, T, 1.0);
+        for (Index r : F2.multirank) CHECK(r == 2);
+        TsvdqFactors F1 = tsvdq(A, T, 2);
+        CHECK(frobenius_norm(tsvdq2_reconstruct(F2) - tsvdq_reconstruct(F1)) <= 1e-12 * frobenius_norm(A));
+        CHECK(std::fabs(tsvdq2_error(A, F2).total - tsvdq_error(A, F1).total) <= 1e-12 * frobenius_norm(A));
+    }
+    // test_decompositions.cpp:179-188 — full transform, gamma = 1: lossless
+    {
+        Tensor3 A = seeded(3, 4, 4, 46);
+        ApproxError e = tsvdq2_error(A, tsvdq2(A, dct_transform(4, 4), 1.0));
+        const double sc = frobenius_norm(A);
+        CHECK(e.total <= 1e-10 * sc && e.eckart_young <= 1e-10 * sc && e.projection <= 1e-10 * sc);
+    }
+    // test_decompositions.cpp:190-205 — error decomposition on random instances
+    for (int i = 0; i < 10; ++i) {
+        Tensor3 A = seeded(4, 3, 5, 470 + (unsigned)i);
+        Transform T = random_orthogonal_transform(5, 3, 100 + (uint64_t)i);
+        TsvdqIIFactors F = tsvdq2(A, T, 0.8);
+        ApproxError e = tsvdq2_error(A, F);
+        const double lhs = e.total * e.total,
+                     rhs = e.eckart_young * e.eckart_young + e.projection * e.projection;
+        CHECK(std::fabs(lhs - rhs) <= 1e-10 * lhs);
+        CHECK(std::fabs(e.total - frobenius_norm(A - tsvdq2_reconstruct(F))) <= 1e-10 * frobenius_norm(A));
+    }
     // errors: argument / shape / degenerate
     check_throws<argument_error>([&] { identity_transform(4, 9); }, "p > n3");
     check_throws<argument_error>([&] { haar_transform(3, 2); }, "haar n3");

@@ -539,3 +539,117 @@ def test_sweep_large_slices(engine, oracle):
             U, S, V = oracle.tsvdq(a, q, k)
             want = oracle.relative_error(a, oracle.tsvdq_reconstruct(U, S, V, q))
             assert abs(re[ik, ip] - want) <= 1e-10 * want
+
+
+# ------------------------------------------------------------------ tsvdq2
+def _tsvdq2_parity(engine, oracle, a, q, gamma):
+    f = engine.tsvdq2(a, engine.Transform.custom(q) if not isinstance(q, engine.Transform) else q, gamma)
+    qq = q.q if isinstance(q, engine.Transform) else q
+    U, S, V, mr = oracle.tsvdq2(a, qq, gamma)
+    assert list(f.multirank) == list(mr)
+    assert f.implicit_rank == int(mr.sum())
+    r = min(a.shape[0], a.shape[1])
+    assert f.u.shape == (a.shape[0], r, qq.shape[1]) and f.s.shape == (r, qq.shape[1])
+    smax = max(S.max(), 1e-300)
+    assert np.abs(f.s - S).max() <= 1e-10 * smax
+    nrm = np.linalg.norm(a)
+    rec = engine.tsvdq2_reconstruct(f)
+    assert np.linalg.norm(rec - oracle.tsvdq_reconstruct(U, S, V, qq, a.shape[2])) <= 1e-10 * nrm
+    got = engine.tsvdq2_error(a, f)
+    want = oracle.tsvdq2_error(a, U, S, V, qq, mr)
+    for g, w in zip(got, want):
+        assert abs(g - w) <= 1e-10 * nrm
+    for i in range(qq.shape[1]):  # kept columns orthonormal, dropped ones zero
+        k = int(f.multirank[i])
+        u = f.u[:, :k, i]
+        assert np.linalg.norm(u.T @ u - np.eye(k)) <= 1e-10 * max(k, 1)
+        assert not f.u[:, k:, i].any() and not f.s[k:, i].any() and not f.v[:, k:, i].any()
+    return f
+
+
+def test_tsvdq2_reference_cases(engine, oracle):
+    # tests/test_decompositions.cpp:126-146
+    a = oracle.random_tensor(4, 5, 6, 44)
+    t = engine.Transform("dct", 6, 4)
+    f = _tsvdq2_parity(engine, oracle, a, t, 1.0)
+    tot, ey, _ = engine.tsvdq2_error(a, f)
+    assert abs(tot - engine.projection_error(a, t)) <= 1e-10 * np.linalg.norm(a)
+    assert ey <= 1e-10 * np.linalg.norm(a)
+    for g in (0.0, 1.5):
+        with pytest.raises(engine.ArgumentError):
+            engine.tsvdq2(a, t, g)
+    # :148-160 tie-break
+    c = counterexample()
+    f = engine.tsvdq2(c, engine.Transform("identity", 2, 2), 0.5)
+    assert list(f.multirank) == [2, 0] and f.implicit_rank == 2
+    assert abs(engine.tsvdq2_error(c, f)[0] ** 2 - 2.0) <= 1e-12
+    # :179-188 full transform lossless
+    a = oracle.random_tensor(3, 4, 4, 46)
+    tot, ey, pr = engine.tsvdq2_error(a, engine.tsvdq2(a, engine.Transform("dct", 4, 4), 1.0))
+    assert max(tot, ey, pr) <= 1e-10 * np.linalg.norm(a)
+    # :190-205 error decomposition
+    for i in range(10):
+        a = oracle.random_tensor(4, 3, 5, 470 + i)
+        f = engine.tsvdq2(a, engine.Transform("random", 5, 3, seed=100 + i), 0.8)
+        tot, ey, pr = engine.tsvdq2_error(a, f)
+        assert abs(tot ** 2 - (ey ** 2 + pr ** 2)) <= 1e-10 * tot ** 2
+        assert abs(tot - np.linalg.norm(a - engine.tsvdq2_reconstruct(f))) <= 1e-10 * np.linalg.norm(a)
+
+
+def test_tsvdq2_exact_rank_matches_tsvdq(engine, oracle):
+    # tests/test_decompositions.cpp:162-177; verify.cpp:833-848
+    q = oracle.dct_q(5, 3)
+    hat = np.zeros((4, 4, 3), order="F")
+    for s in range(3):
+        hat[:, :, s] = oracle.random_matrix(4, 2, 300 + s) @ oracle.random_matrix(4, 2, 400 + s).T
+    a = oracle.mode3_product(hat, q)
+    t = engine.Transform.custom(q)
+    f2 = engine.tsvdq2(a, t, 1.0)
+    assert list(f2.multirank) == [2, 2, 2]
+    f1 = engine.tsvdq(a, t, 2)
+    nrm = np.linalg.norm(a)
+    assert np.linalg.norm(engine.tsvdq2_reconstruct(f2) - engine.tsvdq_reconstruct(f1)) <= 1e-12 * nrm
+    assert abs(engine.tsvdq2_error(a, f2)[0] - engine.tsvdq_error(a, f1)[0]) <= 1e-12 * nrm
+
+
+@pytest.mark.parametrize("shape,p,gamma", [((6, 5, 7), 4, 0.9), ((64, 48, 32), 8, 0.5),
+                                           ((37, 29, 20), 20, 0.99), ((30, 40, 12), 5, 0.3),
+                                           ((200, 180, 6), 3, 0.7)])
+def test_tsvdq2_vs_oracle(engine, oracle, shape, p, gamma):
+    a = oracle.random_tensor(*shape, 7 + p)
+    q = oracle.random_orthogonal_q(shape[2], p, 3)
+    _tsvdq2_parity(engine, oracle, a, q, gamma)
+
+
+def test_tsvdq2_video_and_dominance(engine, oracle):
+    # verify.cpp:796-822: gamma set to the energy tsvdq keeps at k -> tsvdq2 is
+    # no worse and keeps at most k*p triplets
+    a = synth.video(60, 80, 50, seed=3)
+    q, _, _ = oracle.data_dependent_q(a, 20)
+    t = engine.Transform.custom(q)
+    ahat2 = np.linalg.norm(oracle.mode3_product(a, q.T)) ** 2
+    for k in (1, 5, 10):
+        es = engine.tsvdq_error(a, engine.tsvdq(a, t, k))
+        gamma = min(1.0, max((ahat2 - es[1] ** 2) / ahat2, 1e-300)) * (1 - 1e-12)
+        f2 = _tsvdq2_parity(engine, oracle, a, q, gamma)
+        assert f2.implicit_rank <= k * 20
+        assert engine.tsvdq2_error(a, f2)[0] <= es[0] * (1 + 1e-12)
+
+
+def test_tsvdq2_device_arrays_and_zero(engine, oracle):
+    import torch
+    a = oracle.random_tensor(24, 20, 16, 5)
+    q = oracle.dct_q(16, 6)
+    t = engine.Transform.custom(q)
+    fh = engine.tsvdq2(a, t, 0.75)
+    fd = engine.tsvdq2(engine.to_device(a), t, 0.75)
+    assert isinstance(fd.u, torch.Tensor) and fd.u.is_cuda
+    assert list(fd.multirank) == list(fh.multirank)
+    assert np.array_equal(engine.to_host(fd.s), fh.s)
+    rd = engine.to_host(engine.tsvdq2_reconstruct(fd))
+    assert np.array_equal(rd, engine.tsvdq2_reconstruct(fh))
+    assert engine.tsvdq2_error(engine.to_device(a), fd) == engine.tsvdq2_error(a, fh)
+    z = np.zeros((5, 4, 6))
+    fz = engine.tsvdq2(z, engine.Transform("dct", 6, 3), 1.0)
+    assert list(fz.multirank) == [0, 0, 0]
+    assert not engine.tsvdq2_reconstruct(fz).any()

@@ -224,3 +224,85 @@ def test_random_orthogonal_deterministic():
     assert np.abs(t.T @ t - np.eye(5)).max() <= 1e-10
     assert np.array_equal(t, ppo.random_orthogonal_q(8, 5, 1))
     assert np.abs(t - ppo.random_orthogonal_q(8, 5, 2)).max() > 1e-6
+
+
+# ---------------------------------------------------------------- tsvdq2
+def test_tsvdq2_gamma_one_keeps_numerical_rank():
+    # tests/test_decompositions.cpp:126-146
+    a = ppo.random_tensor(4, 5, 6, 44)
+    q = ppo.dct_q(6, 4)
+    U, S, V, mr = ppo.tsvdq2(a, q, 1.0)
+    sp = ppo.slice_spectra(a, q)
+    for i in range(4):
+        assert mr[i] == int(np.sum(sp[:, i] > 1e-12 * sp[0, i]))
+    tot, ey, pr = ppo.tsvdq2_error(a, U, S, V, q, mr)
+    nrm = np.linalg.norm(a)
+    assert abs(tot - ppo.projection_error(a, q)) <= 1e-10 * nrm
+    assert ey <= 1e-10 * nrm
+    for g in (0.0, 1.5, -0.1):
+        with pytest.raises(ValueError):
+            ppo.tsvdq2(a, q, g)
+
+
+def test_tsvdq2_tie_break_counterexample():
+    # tests/test_decompositions.cpp:148-160; verify.cpp:205-211
+    a = counterexample()
+    q = np.eye(2)
+    U, S, V, mr = ppo.tsvdq2(a, q, 0.5)
+    assert list(mr) == [2, 0]
+    tot, _, _ = ppo.tsvdq2_error(a, U, S, V, q, mr)
+    assert abs(tot * tot - 2.0) <= 1e-12
+    # padded stacks: the dropped slice is all zeros
+    assert not S[:, 1].any() and not U[:, :, 1].any() and not V[:, :, 1].any()
+
+
+def test_tsvdq2_exact_rank_reproduces_tsvdq():
+    # tests/test_decompositions.cpp:162-177
+    q = ppo.dct_q(5, 3)
+    hat = np.zeros((4, 4, 3), order="F")
+    for s in range(3):
+        hat[:, :, s] = ppo.random_matrix(4, 2, 300 + s) @ ppo.random_matrix(4, 2, 400 + s).T
+    a = ppo.mode3_product(hat, q)
+    U2, S2, V2, mr = ppo.tsvdq2(a, q, 1.0)
+    assert list(mr) == [2, 2, 2]
+    U1, S1, V1 = ppo.tsvdq(a, q, 2)
+    nrm = np.linalg.norm(a)
+    r2 = ppo.tsvdq_reconstruct(U2, S2, V2, q, 5)
+    r1 = ppo.tsvdq_reconstruct(U1, S1, V1, q, 5)
+    assert np.linalg.norm(r2 - r1) <= 1e-12 * nrm
+    assert abs(ppo.tsvdq2_error(a, U2, S2, V2, q, mr)[0] - ppo.tsvdq_error(a, U1, S1, V1, q)[0]) \
+        <= 1e-12 * nrm
+
+
+def test_tsvdq2_full_transform_lossless():
+    # tests/test_decompositions.cpp:179-188
+    a = ppo.random_tensor(3, 4, 4, 46)
+    q = ppo.dct_q(4, 4)
+    U, S, V, mr = ppo.tsvdq2(a, q, 1.0)
+    tot, ey, pr = ppo.tsvdq2_error(a, U, S, V, q, mr)
+    nrm = np.linalg.norm(a)
+    assert tot <= 1e-10 * nrm and ey <= 1e-10 * nrm and pr <= 1e-10 * nrm
+
+
+def test_tsvdq2_error_decomposition_and_selection_rule():
+    # tests/test_decompositions.cpp:190-205, plus the selection restated in numpy
+    for i in range(10):
+        a = ppo.random_tensor(4, 3, 5, 470 + i)
+        q = ppo.random_orthogonal_q(5, 3, 100 + i)
+        U, S, V, mr = ppo.tsvdq2(a, q, 0.8)
+        tot, ey, pr = ppo.tsvdq2_error(a, U, S, V, q, mr)
+        assert abs(tot ** 2 - (ey ** 2 + pr ** 2)) <= 1e-10 * tot ** 2
+        direct = np.linalg.norm(a - ppo.tsvdq_reconstruct(U, S, V, q, 5))
+        assert abs(tot - direct) <= 1e-10 * np.linalg.norm(a)
+        # independent restatement of decompositions.cpp:131-176 on LAPACK spectra
+        ah = np.einsum("ijk,kp->ijp", a, q)
+        sp = np.stack([np.linalg.svd(ah[:, :, s], compute_uv=False) for s in range(3)], axis=1)
+        pool = [(-sp[j, s], s, j) for s in range(3) for j in range(sp.shape[0])
+                if sp[j, s] > 1e-12 * sp[0].max()]
+        pool.sort()
+        cum = np.cumsum([v * v for v, _, _ in pool])
+        K = min(int(np.searchsorted(cum, 0.8 * cum[-1], side="left")) + 1, len(pool))
+        want = np.zeros(3, dtype=int)
+        for _, s, _ in pool[:K]:
+            want[s] += 1
+        assert list(mr) == list(want)
