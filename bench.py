@@ -431,9 +431,79 @@ class TsvdqSharded:
         return Tsvdq.cpu_sample(self, ppo, threads)
 
 
+class StarQSharded:
+    """cfg4 row-sharded over the torchrun ranks (dist.sharded_star_q): rank r
+    holds A's row block and B's lateral block, transforms both, all-gathers B^
+    in slice groups overlapped with the facewise GEMMs, and inverse-transforms
+    its own C rows. Strong scaling (the cfg4 product is fixed)."""
+
+    name = "cfg4"
+    metric, unit = "starq_tflops", "TFLOP/s"
+
+    def __init__(self, world, rank, local, n1=1024, m=512, n2=1024, n3=256, p=64, seed=0):
+        import torch
+        import paper_2409_19402_b200 as pp
+        from paper_2409_19402_b200 import dist as pdist, synth
+        self.torch = torch
+        self.pdist = pdist
+        self.dims = (n1, m, n2, n3, p)
+        self.world = world
+        dev = f"cuda:{local}"
+        self.be = pdist.DeviceBackend(dev)
+        self.plan = pdist.make_star_plan(n1, m, n2, n3, p, world, rank)
+        pl = self.plan
+        A = synth.gaussian_device(n1, m, n3, seed, 1, device=dev)   # same bits as the 1-GPU run
+        B = synth.gaussian_device(m, n2, n3, seed, 2, device=dev)
+        self.A = A[pl.i0:pl.i0 + pl.rows].permute(2, 1, 0).contiguous().permute(2, 1, 0)
+        self.B = B[:, pl.j0:pl.j0 + pl.cols].permute(2, 1, 0).contiguous().permute(2, 1, 0)
+        del A, B
+        self.Q = pp.to_device(pp.Transform("dct", n3, p).q, device=dev)
+        self.flops = 2.0 * p * (n1 * m * n3 + m * n2 * n3 + n1 * m * n2 + n1 * n2 * n3)
+
+    def config(self):
+        n1, m, n2, n3, p = self.dims
+        return {"workload": "cfg4 star-Q product, output rows sharded", "A": [n1, m, n3], "B": [m, n2, n3],
+                "p": p, "transform": "dct", "l2": "inputs (2 GiB) > L2; no flush needed",
+                "step": "dist.sharded_star_q (local transforms, NCCL all_gather of B^ in 4 slice groups "
+                        "overlapped with the facewise GEMMs, local inverse)"}
+
+    def step(self, L):
+        self.be.L.ppc_set_stream(C.c_void_p(self.torch.cuda.current_stream().cuda_stream))
+        self.C = self.pdist.sharded_star_q(self.A, self.B, self.Q, self.plan, self.be)
+
+    def value(self, sec):
+        return self.flops / sec / 1e12 / self.world  # main() multiplies by world
+
+    def dominant(self, stages):
+        return "facewise", "tensor"
+
+    def e2e_setup(self):
+        self.hA = flat_host(self.A)
+        self.hB = flat_host(self.B)
+        n1, m, n2, n3, p = self.dims
+        self.h2d = 8 * (self.plan.rows * m * n3 + m * self.plan.cols * n3)
+        self.d2h = 8 * self.plan.rows * n2 * n3
+
+    def e2e_step(self, L):
+        torch = self.torch
+        A = torch.empty_like(self.A.permute(2, 1, 0)).reshape(-1)
+        B = torch.empty_like(self.B.permute(2, 1, 0)).reshape(-1)
+        A.copy_(self.hA, non_blocking=True)
+        B.copy_(self.hB, non_blocking=True)
+        Av = A.view(self.A.shape[::-1]).permute(2, 1, 0)
+        Bv = B.view(self.B.shape[::-1]).permute(2, 1, 0)
+        Cr = self.pdist.sharded_star_q(Av, Bv, self.Q, self.plan, self.be)
+        Cr.cpu()
+
+    def cpu_sample(self, ppo, threads):
+        return StarQ.cpu_sample(self, ppo, threads)
+
+
 def make_workload(name, world=1, rank=0, local=0):
     if name == "cfg5" and world > 1:
         return TsvdqSharded(world, rank, local)
+    if name == "cfg4" and world > 1:
+        return StarQSharded(world, rank, local)
     if name == "cfg4":
         return StarQ()
     dims = {"cfg5": (2048, 2048, 1024, 128, 32), "cfg3": (512, 512, 224, 32, 16),
@@ -612,8 +682,8 @@ def main():
 
     if rank == 0:
         cfg = wl.config()
-        sharded = isinstance(wl, TsvdqSharded)
-        cfg["parallelism"] = (f"pixel-sharded dp{world}" if sharded else
+        sharded = isinstance(wl, (TsvdqSharded, StarQSharded))
+        cfg["parallelism"] = (f"{'row' if isinstance(wl, StarQSharded) else 'pixel'}-sharded dp{world}" if sharded else
                               (f"replicas{world}" if world > 1 else "single"))
         line = {"metric": wl.metric, "value": value, "unit": wl.unit, "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,

@@ -188,6 +188,19 @@ int ppc_tsvdq2_error(const double* A, int64_t n1, int64_t n2, int64_t n3,
  * number of row chunks (a power of two) and the chunk length. Depends on
  * (N, n3) only, so a pixel-sharded run reproduces the 1-GPU sums bitwise. */
 int ppc_gram_plan(int64_t N, int64_t n3, int64_t* chunks, int64_t* chunk);
+/* Strided batched FP64 GEMM on DEVICE memory, the sharded star-Q driver's
+ * building block (facewise GEMM into a lateral block of the output slices;
+ * inverse transform with the scale folded into the epilogue, as
+ * star_products.cpp:56-58 applies it):
+ *   C_b = alpha * op(A_b) * op(B_b),  b < batch,
+ * op(A) = A (M x K, lda) or, trans_a, A^T with A stored K x M (lda);
+ * op(B) = B (K x N, ldb) or, trans_b, B^T with B stored N x K (ldb);
+ * X_b = X + b * strideX. Same DMMA kernels and accumulation order as the
+ * engine's own mode-3 / facewise stages. */
+int ppc_gemm_strided(int64_t M, int64_t N, int64_t K, int64_t batch, double alpha,
+                     const double* A, int64_t lda, int64_t strideA, int trans_a,
+                     const double* B, int64_t ldb, int64_t strideB, int trans_b,
+                     double* C, int64_t ldc, int64_t strideC);
 /* Partial Grams T_c^T T_c of `nchunks` consecutive chunks of `chunk` rows of
  * T (rows x n3, leading dimension ldT): parts is nchunks x n3 x n3. */
 int ppc_gram_partials(const double* T, int64_t ldT, int64_t rows, int64_t n3, int64_t chunk,

@@ -76,6 +76,8 @@ def lib() -> C.CDLL:
         "ppc_tsvdq2": (C.c_int, [vp, i64, i64, i64, vp, i64, C.c_double, vp, vp, vp, C.POINTER(i64), C.c_int]),
         "ppc_tsvdq2_reconstruct": (C.c_int, [vp, vp, vp, vp, i64, i64, i64, i64, C.POINTER(i64), vp, C.c_int]),
         "ppc_tsvdq2_error": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, vp, i64, C.POINTER(i64), pd, pd, pd, C.c_int]),
+        "ppc_gemm_strided": (C.c_int, [i64, i64, i64, i64, C.c_double, vp, i64, i64, C.c_int, vp, i64, i64,
+                                       C.c_int, vp, i64, i64]),
         "ppc_tsvdq_sweep": (C.c_int, [vp, i64, i64, i64, C.POINTER(i64), i64, C.POINTER(i64), i64, vp, vp, C.c_int]),
         "ppc_tsvdq_compress": (C.c_int, [vp, i64, i64, i64, i64, i64, vp, vp, vp, vp, vp, pd, C.c_int]),
     }

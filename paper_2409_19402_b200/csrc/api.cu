@@ -321,6 +321,31 @@ int ppc_tsvdq2_error(const double* A, int64_t n1, int64_t n2, int64_t n3, const 
     });
 }
 
+int ppc_gemm_strided(int64_t M, int64_t N, int64_t K, int64_t batch, double alpha, const double* A,
+                     int64_t lda, int64_t strideA, int trans_a, const double* B, int64_t ldb,
+                     int64_t strideB, int trans_b, double* C, int64_t ldc, int64_t strideC) {
+    return guarded([&] {
+        if (M < 0 || N < 0 || K < 0 || batch < 0) fail(PPC_SHAPE, "gemm_strided: negative extent");
+        if (!M || !N || !batch) return;
+        if (!A || !B || !C) fail(PPC_ARGUMENT, "gemm_strided: null operand");
+        if (lda < (trans_a ? K : M) || ldb < (trans_b ? N : K) || ldc < M)
+            fail(PPC_ARGUMENT, "gemm_strided: leading dimension too small");
+        GemmDesc d;
+        d.M = M; d.N = N; d.K = K; d.batch = batch;
+        d.A = A; d.lda = lda; d.strideA = strideA; d.a_kmajor = trans_a != 0;
+        d.B = B; d.ldb = ldb; d.strideB = strideB; d.b_nmajor = trans_b != 0;
+        d.C = C; d.ldc = ldc; d.strideC = strideC;
+        d.alpha = alpha;
+        if (K == 0) {  // empty sum: C = 0
+            for (int64_t b = 0; b < batch; ++b)
+                PPC_CUDA_CHECK(cudaMemset2DAsync(C + b * strideC, sizeof(double) * ldc, 0, sizeof(double) * M,
+                                                 (size_t)N, stream()));
+            return;
+        }
+        gemm(d, stream());
+    });
+}
+
 int ppc_gram_plan(int64_t N, int64_t n3, int64_t* chunks, int64_t* chunk) {
     return guarded([&] {
         if (N < 1 || n3 < 1) fail(PPC_SHAPE, "gram_plan: extents must be positive");

@@ -1,4 +1,7 @@
-"""Multi-GPU tSVDQ with a data-driven basis, one process per GPU.
+"""Multi-GPU tSVDQ with a data-driven basis and multi-GPU star-Q product
+(SURVEY §8e), one process per GPU.
+
+tSVDQ (sharded_compress):
 
 The cfg5 pipeline is sharded as follows:
 
@@ -18,6 +21,14 @@ The cfg5 pipeline is sharded as follows:
 6. The slice SVDs run locally, then the factor stacks are all-gathered.
 7. The fused reconstruction residual runs over the local pixel block, then the
    two scalars are all-reduced.
+
+star-Q (sharded_star_q, cfg4): output rows are partitioned. Rank r holds the
+row block A[i0:i1, :, :] and the lateral block B[:, j0:j1, :]. It transforms
+both locally, all-gathers B^ in slice groups, and runs the facewise GEMMs of a
+group into the matching lateral blocks of its C^ rows while the next group is
+still in flight. It then applies the inverse transform to its own rows. C has
+no reduction, and every element takes the same DMMA accumulation order as the
+1-GPU product, so the row blocks are bitwise the 1-GPU C.
 
 Compute goes through a backend object. `DeviceBackend` calls the engine's C-ABI
 on CUDA tensors, and collectives use torch.distributed (NCCL on GPUs). The
@@ -81,6 +92,23 @@ class DeviceBackend:
     def mode3_fwd(self, A_blk, n1, nj, n3, Q, p):
         out = _fempty((n1, nj, p), self.device)
         _check(self.L.ppc_mode3_product(_p(A_blk), n1, nj, n3, _p(Q), p, 1, _p(out), 1))
+        return out
+
+    def facewise_into(self, Ah, Bb, Cv):
+        """Cv(:, :, s) = Ah(:, :, s) Bb(:, :, s): Ah (a x m x ns) and Bb (m x b x ns)
+        Fortran, Cv a strided (a x b x ns) view into the C^ rows."""
+        a, m, ns = Ah.shape
+        b = Bb.shape[1]
+        _check(self.L.ppc_gemm_strided(a, b, m, ns, C.c_double(1.0), _p(Ah), Ah.stride(1), Ah.stride(2), 0,
+                                       _p(Bb), Bb.stride(1), Bb.stride(2), 0, _p(Cv), Cv.stride(1),
+                                       Cv.stride(2)))
+
+    def mode3_inv(self, Ch, d1, d2, p, Q, n3, scale):
+        """(Ch x3 Q) * scale, the scale in the GEMM epilogue (star_products.cpp:56-58)."""
+        out = _fempty((d1, d2, n3), self.device)
+        N = d1 * d2
+        _check(self.L.ppc_gemm_strided(N, n3, p, 1, C.c_double(scale), _p(Ch), N, 0, 0, _p(Q), n3, 0, 1,
+                                       _p(out), N, 0))
         return out
 
     def svd_slices(self, S_loc, n1, n2, ps, k):
@@ -206,3 +234,97 @@ def sharded_compress(A_blk, plan: ShardPlan, k: int, backend, group=None):
         dist.all_reduce(t, group=group)
     re = float((t[0].sqrt() / t[1].sqrt()).item())
     return Q, Uf, Sf, Vf, re
+
+
+# ------------------------------------------------------------------ star-Q
+@dataclass
+class StarPlan:
+    world: int
+    rank: int
+    n1: int
+    m: int
+    n2: int
+    n3: int
+    p: int
+
+    @property
+    def rows(self):
+        return self.n1 // self.world
+
+    @property
+    def i0(self):
+        return self.rank * self.rows
+
+    @property
+    def cols(self):
+        return self.n2 // self.world
+
+    @property
+    def j0(self):
+        return self.rank * self.cols
+
+
+def make_star_plan(n1, m, n2, n3, p, world, rank) -> StarPlan:
+    if n1 % world or n2 % world:
+        raise ValueError(f"cannot shard star-Q: n1={n1}, n2={n2} vs world={world}")
+    return StarPlan(world, rank, n1, m, n2, n3, p)
+
+
+def _slice_groups(p, groups):
+    groups = max(1, min(groups, p))
+    step = -(-p // groups)
+    return [(s, min(s + step, p)) for s in range(0, p, step)]
+
+
+def nccl_gather(group=None, world=1):
+    """all_gather of one contiguous tensor, asynchronous: returns a handle
+    whose wait() yields the G per-rank tensors."""
+
+    class _H:
+        def __init__(self, t):
+            self.out = [torch.empty_like(t) for _ in range(world)]
+            self.work = dist.all_gather(self.out, t, group=group, async_op=True) if world > 1 else None
+            if world == 1:
+                self.out[0] = t
+
+        def wait(self):
+            if self.work is not None:
+                self.work.wait()
+            return self.out
+
+    return _H
+
+
+def sharded_star_q(A_rows, B_cols, Q, plan: StarPlan, backend, scale=1.0, group=None, groups=4,
+                   gather=None):
+    """star_products.cpp:51-59 on the rank's row block. A_rows is
+    (n1/G x m x n3), B_cols is (m x n2/G x n3), both Fortran; Q is n3 x p.
+    Returns this rank's rows C[i0:i1, :, :] (n1/G x n2 x n3, Fortran)."""
+    Ah = backend.mode3_fwd(A_rows, plan.rows, plan.m, plan.n3, Q, plan.p)   # (rows, m, p)
+    Bh = backend.mode3_fwd(B_cols, plan.m, plan.cols, plan.n3, Q, plan.p)   # (m, cols, p)
+    return star_finish(Ah, Bh, Q, plan, backend, scale,
+                       gather or nccl_gather(group, plan.world), groups)
+
+
+def star_finish(Ah, Bh, Q, plan: StarPlan, backend, scale, gather, groups=4):
+    """All-gather B^ in slice groups (group g+1 in flight while group g's
+    facewise GEMMs run), facewise into the C^ rows, inverse transform."""
+    G, rows, cols, m, p = plan.world, plan.rows, plan.cols, plan.m, plan.p
+    Ch = _fempty((rows, plan.n2, p), Ah.device)
+    spans = _slice_groups(p, groups)
+
+    def start(span):
+        s0, s1 = span
+        send = Bh.permute(2, 1, 0)[s0:s1].contiguous()   # (ns, cols, m) C-order
+        return gather(send)
+
+    pending = start(spans[0])
+    for g, (s0, s1) in enumerate(spans):
+        parts = pending.wait()
+        if g + 1 < len(spans):
+            pending = start(spans[g + 1])
+        for r in range(G):
+            Bb = parts[r].permute(2, 1, 0)                  # (m, cols, ns) Fortran
+            Cv = Ch[:, r * cols:(r + 1) * cols, s0:s1]
+            backend.facewise_into(Ah[:, :, s0:s1], Bb, Cv)
+    return backend.mode3_inv(Ch, rows, plan.n2, p, Q, plan.n3, scale)

@@ -1,4 +1,4 @@
-"""World-size-2 `gloo` tests of the sharded tSVDQ driver (paper_2409_19402_b200/dist.py)
+"""World-size-2 `gloo` tests of the sharded tSVDQ and star-Q drivers (paper_2409_19402_b200/dist.py)
 on CPU, with a numpy stand-in for the engine's per-rank kernels (test-only).
 
 They check the orchestration:
@@ -80,6 +80,18 @@ class NumpyBackend:
             U[:, :, z], s[:, z], V[:, :, z] = uu, sv[:k], vv
         return _ft(U), _ft(s), _ft(V)
 
+    def facewise_into(self, Ah, Bb, Cv):
+        a = Ah.numpy()
+        b = Bb.numpy()
+        c = Cv.numpy()          # strided view sharing Cv's memory
+        for s in range(a.shape[2]):
+            c[:, :, s] = a[:, :, s] @ b[:, :, s]
+
+    def mode3_inv(self, Ch, d1, d2, p, Q, n3, scale):
+        ch = Ch.permute(2, 1, 0).contiguous().numpy().transpose(2, 1, 0)
+        Qn = Q.permute(1, 0).contiguous().numpy().T
+        return _ft(scale * np.einsum("ijl,kl->ijk", ch, Qn))
+
     def recon_block(self, A_blk, n1, nj, n3, U, S, V, n2, j0, Q, p, k):
         A = A_blk.permute(2, 1, 0).contiguous().numpy().transpose(2, 1, 0)
         Un = U.permute(2, 1, 0).contiguous().numpy().transpose(2, 1, 0)
@@ -157,3 +169,52 @@ def test_plan_rejects_misaligned_shards():
         pdist.make_plan(16, 64, 24, 4, 3, 0, be)   # world not a power of two
     with pytest.raises(ValueError):
         pdist.make_plan(16, 64, 24, 3, 2, 0, be)   # p not divisible
+
+
+def _star_inputs(n1, m, n2, n3, p):
+    rng = np.random.default_rng(11)
+    a = np.asfortranarray(rng.standard_normal((n1, m, n3)))
+    b = np.asfortranarray(rng.standard_normal((m, n2, n3)))
+    q, _ = np.linalg.qr(rng.standard_normal((n3, p)))
+    return a, b, np.asfortranarray(q)
+
+
+def _run_star(rank, world, port, dims, scale, groups, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n1, m, n2, n3, p = dims
+        a, b, q = _star_inputs(*dims)
+        plan = pdist.make_star_plan(n1, m, n2, n3, p, world, rank)
+        A_rows = _ft(a[plan.i0:plan.i0 + plan.rows])
+        B_cols = _ft(b[:, plan.j0:plan.j0 + plan.cols])
+        Cr = pdist.sharded_star_q(A_rows, B_cols, _ft(q), plan, NumpyBackend(), scale=scale, groups=groups)
+        np.save(os.path.join(out_dir, f"c{rank}.npy"), Cr.permute(2, 1, 0).contiguous().numpy().transpose(2, 1, 0))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+@pytest.mark.parametrize("groups", [1, 3])
+def test_sharded_star_q_world2_matches_product(tmp_path, groups):
+    dims, scale = (8, 6, 10, 7, 5), -1.5
+    n1, m, n2, n3, p = dims
+    a, b, q = _star_inputs(*dims)
+    ah = np.einsum("ijk,kl->ijl", a, q)
+    bh = np.einsum("ijk,kl->ijl", b, q)
+    ch = np.einsum("iml,mjl->ijl", ah, bh)
+    want = scale * np.einsum("ijl,kl->ijk", ch, q)  # star_products.cpp:51-59
+    for world in (1, 2):
+        d = tmp_path / f"w{world}"
+        d.mkdir()
+        mp.spawn(_run_star, args=(world, _free_port(), dims, scale, groups, str(d)), nprocs=world, join=True)
+        got = np.concatenate([np.load(d / f"c{r}.npy") for r in range(world)], axis=0)
+        np.testing.assert_allclose(got, want, rtol=0, atol=1e-12 * np.abs(want).max())
+
+
+def test_star_plan_rejects_uneven_rows():
+    with pytest.raises(ValueError):
+        pdist.make_star_plan(9, 4, 8, 5, 3, 2, 0)
+    assert pdist._slice_groups(5, 3) == [(0, 2), (2, 4), (4, 5)]
+    assert pdist._slice_groups(2, 8) == [(0, 1), (1, 2)]

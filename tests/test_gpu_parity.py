@@ -653,3 +653,53 @@ def test_tsvdq2_device_arrays_and_zero(engine, oracle):
     fz = engine.tsvdq2(z, engine.Transform("dct", 6, 3), 1.0)
     assert list(fz.multirank) == [0, 0, 0]
     assert not engine.tsvdq2_reconstruct(fz).any()
+
+
+# ------------------------------------------------------- sharded star-Q (cfg4 §8e)
+@pytest.mark.parametrize("world,groups", [(1, 4), (2, 3), (4, 1)])
+def test_sharded_star_q_rows_bitwise(engine, world, groups):
+    """Every rank's row block of the sharded product equals the 1-GPU
+    ppc_star_q_product rows bitwise. Ranks run one after another on one GPU:
+    phase 1 (local transforms) for all ranks, then each rank's finish with a
+    gather that hands back the precomputed B^ groups (no cross-rank waits)."""
+    import torch
+    from paper_2409_19402_b200 import dist as pdist
+    n1, m, n2, n3, p, scale = 96, 80, 128, 40, 12, 0.75
+    A = synth.gaussian_device(n1, m, n3, 5, 1)
+    B = synth.gaussian_device(m, n2, n3, 5, 2)
+    Q = engine.to_device(engine.Transform("dct", n3, p).q)
+    want = engine.to_host(engine.star_q_product(A, B, engine.Transform.custom(engine.to_host(Q), scale)))
+    be = pdist.DeviceBackend("cuda:0")
+    plans = [pdist.make_star_plan(n1, m, n2, n3, p, world, r) for r in range(world)]
+
+    def rows_of(x, pl):
+        return x[pl.i0:pl.i0 + pl.rows].permute(2, 1, 0).contiguous().permute(2, 1, 0)
+
+    def cols_of(x, pl):
+        return x[:, pl.j0:pl.j0 + pl.cols].permute(2, 1, 0).contiguous().permute(2, 1, 0)
+
+    Bh = [be.mode3_fwd(cols_of(B, pl), m, pl.cols, n3, Q, p) for pl in plans]
+
+    class Pre:
+        """Hands back the G ranks' B^ blocks of the next slice group."""
+
+        def __init__(self, spans):
+            self.spans = iter(spans)
+
+        def __call__(self, send):
+            s0, s1 = next(self.spans)
+            assert send.shape[0] == s1 - s0
+            parts = [Bh[q].permute(2, 1, 0)[s0:s1].contiguous() for q in range(world)]
+
+            class H:
+                def wait(self):
+                    return parts
+            return H()
+
+    for r, pl in enumerate(plans):
+        Ah = be.mode3_fwd(rows_of(A, pl), pl.rows, m, n3, Q, p)
+        gather = Pre(pdist._slice_groups(p, groups))
+        Cr = pdist.star_finish(Ah, Bh[r], Q, pl, be, scale, gather, groups)
+        torch.cuda.synchronize()
+        got = engine.to_host(Cr)
+        assert np.array_equal(got, want[pl.i0:pl.i0 + pl.rows]), f"rank {r}"
