@@ -21,6 +21,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 #include <vector>
 
 #include "dmma_gemm.cuh"
@@ -250,6 +251,7 @@ void g_AB(const double* A, const double* B, double* C, int64_t m, int64_t kk, in
 
 struct Work {
     int64_t r, b, batch;
+    bool basis = false;  // eigenbasis Q (data_q) rather than slice SVDs: stage names sq.*
     DeviceBuffer X, Y, Yp, Yn, Z, W, P, S, Rinv, Hv, th, res, coef, wmask, nlock, fail, zmap;
     Work(int64_t r_, int64_t b_, int64_t batch_)
         : r(r_), b(b_), batch(batch_),
@@ -284,7 +286,7 @@ void gg(const double* A, int64_t lda, int64_t sA, bool at, const double* B, int6
 // cond(Y) up to ~1e15, two plain passes restore orthogonality.
 void cholqr3(Work& w, double* Y, double* Xout, int64_t c0, cudaStream_t s) {
     const int64_t r = w.r, b = w.b, batch = w.batch, bc = b - c0, per = r * b;
-    StageTimer tm("ss.cholqr3", s);
+    StageTimer tm(w.basis ? "sq.cholqr3" : "ss.cholqr3", s);
     if (c0 > 0)
         for (int pass = 0; pass < 2; ++pass) {
             // P = X_L^T Y_A (c0 x bc); Y_A -= X_L P
@@ -315,11 +317,11 @@ void cholqr3(Work& w, double* Y, double* Xout, int64_t c0, cudaStream_t s) {
 void rayleigh_ritz(Work& w, const double* G, int64_t sG, double* Xn, int64_t c0, cudaStream_t s,
                    double gtol_rel, int sweep_cap) {
     const int64_t r = w.r, b = w.b, batch = w.batch, bc = b - c0, per = r * b;
-    StageTimer tm("ss.rayleigh_ritz", s);
+    StageTimer tm(w.basis ? "sq.rayleigh_ritz" : "ss.rayleigh_ritz", s);
     gg(G, r, sG, false, Xn + c0 * r, r, per, w.Z.d() + c0 * r, r, per, r, bc, r, batch, 1.0, 0.0, s);  // Z = G Xn
     gg(Xn + c0 * r, r, per, true, w.Z.d() + c0 * r, r, per, w.S.d(), bc, bc * bc, bc, bc, r, batch, 1.0, 0.0, s);
     {
-        StageTimer tj("ss.rr_eig", s);
+        StageTimer tj(w.basis ? "sq.rr_eig" : "ss.rr_eig", s);
         // H (PSD) = Hv diag(theta) Hv^T by one-sided Jacobi (eigen mode)
         jacobi_svd(w.S.d(), bc, bc, bc * bc, batch, bc, nullptr, w.P.d(), w.Hv.d(), nullptr, s, gtol_rel,
                    sweep_cap);
@@ -377,6 +379,7 @@ void subspace_eig_top(const double* G, int64_t r, int64_t batch, int64_t k, doub
     b = std::min<int64_t>(b, 160);
     if (k > b) fail(PPC_ARGUMENT, "subspace_eig_top: k too large for the block");
     Work w(r, b, batch);
+    w.basis = !vectors_for_reconstruction;
     const int64_t per = r * b;
     PPC_CUDA_CHECK(cudaMemsetAsync(w.fail.d(), 0, 2 * sizeof(int), s));
     randn_kernel<<<grid1(per * batch), 256, 0, s>>>(w.Y.d(), per * batch, 0x5eed5eedULL + (uint64_t)r * 131 + b);
@@ -424,7 +427,37 @@ void subspace_eig_top(const double* G, int64_t r, int64_t batch, int64_t k, doub
                 thr = 1e-13 * scale;
             }
             int L = 0;
-            if (vectors_for_reconstruction) {
+            std::vector<double> thrv(k, thr);
+            if (vectors_for_reconstruction && it >= 2) {
+                // Per-column thresholds from Rayleigh-Ritz perturbation theory
+                // on the b-column block (the k-boundary gap alone is far too
+                // pessimistic on noise plateaus, where it is ~1e-3 theta_1):
+                //  g_j   = gap from theta_j to the uncaptured spectrum, taken
+                //          as half of theta_j - theta_b (theta_b <= lambda_b);
+                //  (i)   Ritz value error <= ||R||^2 / g_j, and the polished
+                //        sigma_j = sqrt(theta_j): res_j sqrt(k) <= sqrt(2e-10 theta_j g_j);
+                //  (ii)  the kept subspace misses v_j by res_j / g_j, which moves
+                //        the rank-k truncation by ~ sqrt(2) sigma_j res_j / g_j
+                //        <= 1e-11 ||A||;
+                //  (iii) x_j mixes with the discarded Ritz vectors by a further
+                //        factor ||R|| / (theta_j - theta_k) (Saad, Thm 4.6).
+                const double tout = std::max(t[b - 1], 0.0);
+                double R2 = 0.0;
+                for (int64_t j = 0; j < b; ++j) R2 += rr[j] * rr[j];
+                const double Rn = std::sqrt(R2), sk = std::sqrt((double)k), sE = std::sqrt(energy);
+                for (int64_t j = 0; j < k; ++j) {
+                    const double tj = std::max(t[j], 0.0);
+                    const double g = 0.5 * (tj - tout);
+                    if (!(g > 0.0)) break;  // no separation from the block bottom: keep thr
+                    const double sj = std::sqrt(tj);
+                    const double ti = std::sqrt(2e-10 * tj * g) / sk;
+                    const double cross = std::max(tj - t[k], 0.0);
+                    const double tii = 1e-11 * sE * g / (1.4142135623730951 * sj + 1e-300) *
+                                       std::min(1.0, cross / (Rn + 1e-300));
+                    thrv[j] = std::max(thr, std::max(32.0 * 2.22e-16 * scale, std::min(ti, tii)));
+                }
+                while (L < k && rr[L] <= thrv[L]) ++L;
+            } else if (vectors_for_reconstruction) {
                 while (L < k && rr[L] <= thr) ++L;  // locked prefix
             } else {
                 // basis Q: judged on eigenvalues / captured energy (SURVEY 8c
@@ -463,9 +496,9 @@ void subspace_eig_top(const double* G, int64_t r, int64_t batch, int64_t k, doub
             // no more than this slice needs: the residuals of the unlocked
             // wanted columns fall by ~exp(-acosh(x_k)) per degree
             if (xk > 1.0 + 1e-12 && it >= 2) {
-                double rmax = 0.0;
-                for (int64_t j = L; j < k; ++j) rmax = std::max(rmax, rr[j]);
-                const double need = std::log(std::max(rmax / thr, 1.0)) / std::acosh(xk);
+                double rmax = 1.0;  // largest residual / threshold ratio among unlocked wanted columns
+                for (int64_t j = L; j < k; ++j) rmax = std::max(rmax, rr[j] / thrv[j]);
+                const double need = std::log(rmax) / std::acosh(xk);
                 d = std::min(d, std::max(1.0, std::ceil(need) + 1.0));
             }
             deg[sl] = std::max(1, (int)d);
@@ -474,7 +507,17 @@ void subspace_eig_top(const double* G, int64_t r, int64_t batch, int64_t k, doub
                 fprintf(stderr, "[subspace] it %d slice %lld L=%d deg=%d t0=%.6e tk=%.6e tb=%.6e res0=%.3e resk=%.3e thr=%.3e\n",
                         it, (long long)sl, L, deg[sl], t[0], t[k - 1], t[b - 1], rr[0], rr[k - 1], thr);
         }
-        if (dbg) fprintf(stderr, "[subspace] it %d dmax %d\n", it, dmax);
+        if (dbg) {
+            int nact_sl = 0;
+            std::string act;
+            for (int64_t sl = 0; sl < batch; ++sl)
+                if (deg[sl] > 0) {
+                    ++nact_sl;
+                    if (act.size() < 600)
+                        act += " " + std::to_string(sl) + ":" + std::to_string(nlock[sl]) + "/" + std::to_string(deg[sl]);
+                }
+            fprintf(stderr, "[subspace] it %d dmax %d active %d (slice:L/deg)%s\n", it, dmax, nact_sl, act.c_str());
+        }
         thp = th;
         if (all_done) break;
         PPC_CUDA_CHECK(cudaMemcpyAsync(w.wmask.d(), wm.data(), sizeof(double) * b * batch, cudaMemcpyHostToDevice, s));
@@ -506,7 +549,7 @@ void subspace_eig_top(const double* G, int64_t r, int64_t batch, int64_t k, doub
         double* Yp = w.Yp.d();
         double* Yn = w.Yn.d();
         {
-            StageTimer tf("ss.filter", s);
+            StageTimer tf(w.basis ? "sq.filter" : "ss.filter", s);
             // columns below the smallest locked prefix of the filtered slices
             // are final: filter only [cf, b)
             int64_t cf = b;
@@ -575,6 +618,7 @@ void subspace_svd(const double* A, int64_t m, int64_t n, int64_t stride, int64_t
     const int64_t r = tall ? n : m;  // Gram dimension
     DeviceBuffer G(sizeof(double) * r * r * batch);
     {
+        StageTimer tg("ss.gram", s, (double)batch * r * r * (tall ? m : n), 8.0 * batch * m * n);
         GemmDesc d;
         d.M = r; d.N = r; d.batch = batch; d.symmetric = true;
         d.C = G.d(); d.ldc = r; d.strideC = r * r;
@@ -589,6 +633,7 @@ void subspace_svd(const double* A, int64_t m, int64_t n, int64_t stride, int64_t
     DeviceBuffer Xk(sizeof(double) * r * k * batch), lam(sizeof(double) * k * batch);
     subspace_eig_top(G.d(), r, batch, k, Xk.d(), lam.d(), s, true);
     // polish: W = A Xk (tall: m x k) or A^T Xk (wide: n x k)
+    StageTimer tp("ss.polish", s);
     const int64_t o = tall ? m : n;
     DeviceBuffer Wb(sizeof(double) * o * k * batch), Qw(sizeof(double) * o * k * batch),
         T1(sizeof(double) * o * k * batch), Sk(sizeof(double) * k * k * batch),
