@@ -9,6 +9,7 @@
 
 #include "ppc.h"
 #include "projprod/decompositions.hpp"
+#include "projprod/io.hpp"
 #include "projprod/errors.hpp"
 #include "projprod/matrix_kernels.hpp"
 #include "projprod/metrics.hpp"
@@ -515,6 +516,32 @@ double tsvdq_relative_error(const Tensor3& A, const TsvdqFactors& F) {
                                    s.V.data(), F.transform.Q.data(), F.transform.p(), F.k, &re,
                                    PPC_HOST));
     return re;
+}
+
+// --------------------------------------------------------------------- PT3 I/O
+void write_pt3(const std::filesystem::path& path, const Tensor3& A) {  // io.cpp:52-70
+    check(ppc_pt3_write(path.string().c_str(), A.data(), A.n1(), A.n2(), A.n3(), PPC_HOST));
+}
+
+Tensor3 read_pt3(const std::filesystem::path& path) {  // io.cpp:72-112
+    int64_t n1 = 0, n2 = 0, n3 = 0;
+    check(ppc_pt3_info(path.string().c_str(), &n1, &n2, &n3));
+    Tensor3 A(n1, n2, n3);
+    check(ppc_pt3_read(path.string().c_str(), A.data(), A.size(), PPC_HOST));
+    return A;
+}
+
+void write_pt3_matrix(const std::filesystem::path& path, const Matrix& M) {  // io.cpp:114-118
+    Tensor3 A(M.rows(), M.cols(), 1);
+    A.set_slice(0, M);
+    write_pt3(path, A);
+}
+
+Matrix read_pt3_matrix(const std::filesystem::path& path) {  // io.cpp:120-126
+    Tensor3 A = read_pt3(path);
+    if (A.n3() != 1)
+        throw format_error(path.string() + ": expected a matrix (n3 = 1), got n3 = " + std::to_string(A.n3()));
+    return A.slice(0);
 }
 
 }  // namespace projprod

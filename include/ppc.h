@@ -183,6 +183,19 @@ int ppc_tsvdq2_error(const double* A, int64_t n1, int64_t n2, int64_t n3,
                      const double* Q, int64_t p, const int64_t* multirank,
                      double* total, double* eckart_young, double* projection, int loc);
 
+/* ---- PT3 container I/O (io.hpp:11-30, io.cpp:52-112) ------ */
+/* Header: "PT3\0", u32 version 1, u8 dtype 1 (float64), u8 flags 0, 2 pad,
+ * u64 n1, n2, n3 (little endian), then the mode-1-fastest payload, which is
+ * the engine's tensor layout. Malformed files (magic, version, dtype, flags,
+ * zero extent, overflowing extents, truncated or trailing bytes) fail with
+ * PPC_FORMAT, as read_pt3 throws format_error. Device reads and writes stream
+ * through two pinned staging buffers on the copy stream, overlapping disk and
+ * PCIe; host calls are plain file I/O and need no GPU. */
+int ppc_pt3_info(const char* path, int64_t* n1, int64_t* n2, int64_t* n3);
+/* count must equal n1*n2*n3 of the file (PPC_SHAPE otherwise). */
+int ppc_pt3_read(const char* path, double* dst, int64_t count, int loc);
+int ppc_pt3_write(const char* path, const double* src, int64_t n1, int64_t n2, int64_t n3, int loc);
+
 /* ---- shard-level building blocks (multi-GPU driver, dist.py) ------------ */
 /* Deterministic Gram plan for a tube matrix of N rows and n3 columns: the
  * number of row chunks (a power of two) and the chunk length. Depends on

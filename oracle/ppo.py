@@ -291,3 +291,39 @@ def tsvdq2_error(a, U, S, V, q, multirank):
                                 mr.ctypes.data_as(C.POINTER(C.c_int64)), C.byref(t), C.byref(e),
                                 C.byref(pr)))
     return t.value, e.value, pr.value
+
+
+# ---------------------------------------------------------------- PT3 (io.cpp:52-126)
+def pt3_bytes(a) -> bytes:
+    """io.cpp:52-70 write_pt3, restated: the exact file bytes for tensor a
+    (a matrix is the degenerate n3 = 1 tensor, io.cpp:114-118)."""
+    import struct
+    a = np.asfortranarray(np.asarray(a, dtype="<f8"))
+    shape = a.shape + (1,) * (3 - a.ndim)
+    head = b"PT3\0" + struct.pack("<I", 1) + bytes([1, 0, 0, 0]) + struct.pack("<QQQ", *shape)
+    return head + a.tobytes(order="F")
+
+
+def pt3_parse(buf: bytes):
+    """io.cpp:72-112 read_pt3, restated; raises ValueError where the reference
+    throws format_error."""
+    import struct
+    if len(buf) < 36:
+        raise ValueError("truncated header")
+    if buf[:4] != b"PT3\0":
+        raise ValueError("bad magic")
+    if struct.unpack_from("<I", buf, 4)[0] != 1:
+        raise ValueError("unsupported version")
+    if buf[8] != 1:
+        raise ValueError("unsupported dtype")
+    if buf[9] != 0:
+        raise ValueError("unsupported field flags")
+    n1, n2, n3 = struct.unpack_from("<QQQ", buf, 12)
+    if 0 in (n1, n2, n3):
+        raise ValueError("zero extent")
+    cap = 1 << 59
+    if n1 > cap // n2 or n1 * n2 > cap // n3:
+        raise ValueError("element count overflows the addressable payload")
+    if len(buf) != 36 + 8 * n1 * n2 * n3:
+        raise ValueError("payload size mismatch (truncated or trailing bytes)")
+    return np.frombuffer(buf, dtype="<f8", offset=36).reshape((n1, n2, n3), order="F")

@@ -78,6 +78,9 @@ def lib() -> C.CDLL:
         "ppc_tsvdq2_error": (C.c_int, [vp, i64, i64, i64, vp, vp, vp, vp, i64, C.POINTER(i64), pd, pd, pd, C.c_int]),
         "ppc_gemm_strided": (C.c_int, [i64, i64, i64, i64, C.c_double, vp, i64, i64, C.c_int, vp, i64, i64,
                                        C.c_int, vp, i64, i64]),
+        "ppc_pt3_info": (C.c_int, [C.c_char_p, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)]),
+        "ppc_pt3_read": (C.c_int, [C.c_char_p, vp, i64, C.c_int]),
+        "ppc_pt3_write": (C.c_int, [C.c_char_p, vp, i64, i64, i64, C.c_int]),
         "ppc_tsvdq_sweep": (C.c_int, [vp, i64, i64, i64, C.POINTER(i64), i64, C.POINTER(i64), i64, vp, vp, C.c_int]),
         "ppc_tsvdq_compress": (C.c_int, [vp, i64, i64, i64, i64, i64, vp, vp, vp, vp, vp, pd, C.c_int]),
     }

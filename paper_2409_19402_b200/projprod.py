@@ -28,7 +28,8 @@ __all__ = [
     "facewise_product", "frobenius_norm", "svd", "truncated_svd", "data_dependent_transform",
     "projection_error", "star_q", "star_q_product", "tsvdq", "tsvdq_reconstruct", "tsvdq_error",
     "relative_error", "tsvdq_relative_error", "TsvdqIIFactors", "tsvdq2", "tsvdq2_reconstruct",
-    "tsvdq2_error", "compress_tsvdq", "tsvdq_sweep", "to_device", "empty_device", "to_host",
+    "tsvdq2_error", "read_pt3", "write_pt3", "read_pt3_matrix", "write_pt3_matrix", "pt3_shape",
+    "write_tsvdq_factors", "compress_tsvdq", "tsvdq_sweep", "to_device", "empty_device", "to_host",
     "launch_count",
 ]
 
@@ -500,6 +501,75 @@ def tsvdq2_error(a, f: TsvdqIIFactors):
     _call(args, _lib.lib().ppc_tsvdq2_error, pa, n1, n2, n3, pu, ps, pv, pq, p, _i64p(mr),
           C.byref(t), C.byref(e), C.byref(pr), args.loc)
     return t.value, e.value, pr.value
+
+
+# --------------------------------------------------------------------- PT3 I/O
+def pt3_shape(path) -> tuple:
+    """io.cpp:72-101 header validation: (n1, n2, n3) of a PT3 file."""
+    a, b, c = C.c_int64(), C.c_int64(), C.c_int64()
+    _check(_lib.lib().ppc_pt3_info(str(path).encode(), C.byref(a), C.byref(b), C.byref(c)))
+    return a.value, b.value, c.value
+
+
+def read_pt3(path, device=None):
+    """io.cpp:72-112 read_pt3. device=None returns a Fortran numpy array;
+    device="cuda[:i]" streams the payload straight into a device tensor."""
+    n1, n2, n3 = pt3_shape(path)
+    if device is None:
+        out = np.empty((n1, n2, n3), order="F")
+        _check(_lib.lib().ppc_pt3_read(str(path).encode(), C.c_void_p(out.ctypes.data), n1 * n2 * n3,
+                                       _lib.PPC_HOST))
+        return out
+    out = empty_device((n1, n2, n3), device)
+    _sync_stream_from_torch()
+    _check(_lib.lib().ppc_pt3_read(str(path).encode(), C.c_void_p(out.data_ptr()), n1 * n2 * n3,
+                                   _lib.PPC_DEVICE))
+    return out
+
+
+def write_pt3(path, a):
+    """io.cpp:52-70 write_pt3 from a host array or a device tensor."""
+    if _is_dev(a):
+        a_ = a if _fortran_ok(a) else a.permute(*reversed(range(a.dim()))).contiguous().permute(
+            *reversed(range(a.dim())))
+        shape = tuple(a_.shape) + (1,) * (3 - a_.dim())
+        _sync_stream_from_torch()
+        _check(_lib.lib().ppc_pt3_write(str(path).encode(), C.c_void_p(a_.data_ptr()), *shape,
+                                        _lib.PPC_DEVICE))
+        return
+    arr = np.asfortranarray(np.asarray(a, dtype=np.float64))
+    if arr.ndim not in (2, 3):
+        raise ShapeError(f"write_pt3: expected a matrix or an order-3 tensor, got ndim={arr.ndim}")
+    shape = arr.shape + (1,) * (3 - arr.ndim)
+    _check(_lib.lib().ppc_pt3_write(str(path).encode(), C.c_void_p(arr.ctypes.data), *shape, _lib.PPC_HOST))
+
+
+def write_pt3_matrix(path, m):
+    """io.cpp:114-118: a matrix travels as an n3 = 1 tensor."""
+    write_pt3(path, m)
+
+
+def read_pt3_matrix(path, device=None):
+    """io.cpp:120-126: rejects n3 != 1 with FormatError."""
+    n1, n2, n3 = pt3_shape(path)
+    if n3 != 1:
+        raise FormatError(f"{path}: expected a matrix (n3 = 1), got n3 = {n3}")
+    t = read_pt3(path, device)
+    return t[:, :, 0]
+
+
+def write_tsvdq_factors(prefix, f: TsvdqFactors):
+    """tools/main.cpp:211-222 factor export: <prefix>.U.pt3 (n1,k,p),
+    .S.pt3 (k,1,p), .V.pt3 (n2,k,p) and .Q.pt3 (n3,p) as a matrix."""
+    write_pt3(f"{prefix}.U.pt3", f.u)
+    s = f.s
+    if _is_dev(s):
+        write_pt3(f"{prefix}.S.pt3", s.unsqueeze(1))
+    else:
+        write_pt3(f"{prefix}.S.pt3", np.asfortranarray(np.asarray(s))[:, None, :])
+    write_pt3(f"{prefix}.V.pt3", f.v)
+    q = f.transform.q if isinstance(f.transform, Transform) else f.transform
+    write_pt3_matrix(f"{prefix}.Q.pt3", q)
 
 
 def relative_error(ref, approx) -> float:

@@ -2,13 +2,19 @@
 // restated without doctest/Eigen) run against libprojprod.so -> libppc.so.
 // Exit code 0 = all passed. Needs a B200.
 #include <cmath>
+#include <cstring>
+#include <filesystem>
+#include <fstream>
 #include <cstdio>
 #include <functional>
 #include <string>
 #include <vector>
 
+#include <unistd.h>
+
 #include "projprod/decompositions.hpp"
 #include "projprod/errors.hpp"
+#include "projprod/io.hpp"
 #include "projprod/metrics.hpp"
 #include "projprod/star_products.hpp"
 
@@ -241,6 +247,56 @@ int main() {
                      rhs = e.eckart_young * e.eckart_young + e.projection * e.projection;
         CHECK(std::fabs(lhs - rhs) <= 1e-10 * lhs);
         CHECK(std::fabs(e.total - frobenius_norm(A - tsvdq2_reconstruct(F))) <= 1e-10 * frobenius_norm(A));
+    }
+    // test_io.cpp:50-112 — PT3 round trip, matrix container, malformed files
+    {
+        namespace fs = std::filesystem;
+        const fs::path f = fs::temp_directory_path() / ("ppc_io_" + std::to_string(::getpid()) + ".pt3");
+        Tensor3 A = seeded(4, 3, 5, 71);
+        write_pt3(f, A);
+        Tensor3 B = read_pt3(f);
+        CHECK(B.n1() == 4 && B.n2() == 3 && B.n3() == 5);
+        CHECK(std::memcmp(A.data(), B.data(), sizeof(double) * (size_t)A.size()) == 0);
+        Matrix M = seeded(3, 7, 1, 5).slice(0);
+        write_pt3_matrix(f, M);
+        Matrix R = read_pt3_matrix(f);
+        CHECK(R.rows() == 3 && R.cols() == 7 && (M - R).norm() == 0.0);
+        write_pt3(f, seeded(2, 2, 2, 72));
+        std::vector<char> good;
+        {
+            std::ifstream in(f, std::ios::binary);
+            good.assign(std::istreambuf_iterator<char>(in), {});
+        }
+        auto spew = [&](const std::vector<char>& b) {
+            std::ofstream out(f, std::ios::binary | std::ios::trunc);
+            out.write(b.data(), (std::streamsize)b.size());
+        };
+        for (auto [off, val] : std::vector<std::pair<size_t, char>>{{0, 'X'}, {4, 9}, {8, 7}}) {
+            std::vector<char> b = good;
+            b[off] = val;
+            spew(b);
+            check_throws<format_error>([&] { read_pt3(f); }, "tampered header");
+        }
+        {
+            std::vector<char> b = good;
+            b.pop_back();
+            spew(b);
+            check_throws<format_error>([&] { read_pt3(f); }, "truncated");
+            b = good;
+            b.push_back(0);
+            spew(b);
+            check_throws<format_error>([&] { read_pt3(f); }, "trailing");
+            b = good;
+            for (size_t i = 12; i < 20; ++i) b[i] = '\xff';
+            spew(b);
+            check_throws<format_error>([&] { read_pt3(f); }, "overflow");
+            b = good;
+            for (size_t i = 12; i < 20; ++i) b[i] = 0;
+            spew(b);
+            check_throws<format_error>([&] { read_pt3(f); }, "zero extent");
+        }
+        check_throws<format_error>([&] { read_pt3(f.string() + ".does-not-exist"); }, "missing");
+        fs::remove(f);
     }
     // errors: argument / shape / degenerate
     check_throws<argument_error>([&] { identity_transform(4, 9); }, "p > n3");

@@ -703,3 +703,37 @@ def test_sharded_star_q_rows_bitwise(engine, world, groups):
         torch.cuda.synchronize()
         got = engine.to_host(Cr)
         assert np.array_equal(got, want[pl.i0:pl.i0 + pl.rows]), f"rank {r}"
+
+
+# ------------------------------------------------------------ PT3 device streaming
+def test_pt3_device_streaming_round_trip(engine, tmp_path):
+    """A file larger than one 64 MiB staging chunk streams into and out of
+    device memory bit-exactly (two alternating pinned buffers)."""
+    import torch
+    a = synth.gaussian_device(512, 400, 50, 3, 1)          # 81.9 MB payload
+    f = tmp_path / "big.pt3"
+    engine.write_pt3(f, a)                                  # device -> file
+    h = engine.read_pt3(f)                                  # file -> host
+    assert np.array_equal(h, engine.to_host(a))
+    d = engine.read_pt3(f, device="cuda")                   # file -> device
+    assert d.is_cuda and torch.equal(d, a)
+
+
+def test_pt3_compress_chain(engine, oracle, tmp_path):
+    """tools/main.cpp:186-222 compress chain: read_pt3 -> data transform ->
+    tsvdq -> factor export, on the device; exported factors read back equal."""
+    a = synth.video(60, 80, 50, seed=3)
+    f = tmp_path / "video.pt3"
+    engine.write_pt3(f, a)
+    ad = engine.read_pt3(f, device="cuda")
+    t = engine.data_dependent_transform(ad, 20)
+    fac = engine.tsvdq(ad, t, 5)
+    pre = str(tmp_path / "fac")
+    engine.write_tsvdq_factors(pre, fac)
+    assert np.array_equal(engine.read_pt3(pre + ".U.pt3"), engine.to_host(fac.u))
+    assert np.array_equal(engine.read_pt3(pre + ".S.pt3")[:, 0, :], engine.to_host(fac.s))
+    assert np.array_equal(engine.read_pt3(pre + ".V.pt3"), engine.to_host(fac.v))
+    assert np.array_equal(engine.read_pt3_matrix(pre + ".Q.pt3"), engine.to_host(t.q))
+    # and the host path gives the same factors
+    fh = engine.tsvdq(a, engine.Transform.custom(engine.to_host(t.q)), 5)
+    assert np.abs(fh.s - engine.to_host(fac.s)).max() <= 1e-12 * fh.s.max()
