@@ -291,6 +291,18 @@ StarContext StarContext::with_complement(Transform T) {
     return ctx;
 }
 
+Tensor3 star_m_product(const Tensor3& A, const Tensor3& B, const Matrix& M) {  // star_products.cpp:38-49
+    if (M.rows() != M.cols()) throw shape_error("star_m_product: M must be square");
+    if (A.n2() != B.n1())
+        throw shape_error("star product: inner extents differ (" + std::to_string(A.n2()) + " vs " +
+                          std::to_string(B.n1()) + ")");
+    if (A.n3() != M.rows() || B.n3() != M.rows())
+        throw shape_error("star product: mode-3 extents must match the transform");
+    Tensor3 C(A.n1(), B.n2(), A.n3());
+    check(ppc_star_m_product(A.data(), A.n1(), A.n2(), A.n3(), B.data(), B.n2(), M.data(), C.data(), PPC_HOST));
+    return C;
+}
+
 Tensor3 star_q_product(const Tensor3& A, const Tensor3& B, const StarContext& ctx) {
     const Transform& T = ctx.transform;  // star_products.cpp:13-20
     if (A.n2() != B.n1())
@@ -482,6 +494,37 @@ ApproxError tsvdq2_error(const Tensor3& A, const TsvdqIIFactors& F) {  // decomp
                            F.transform.Q.data(), F.transform.p(), mr.data(), &e.total, &e.eckart_young,
                            &e.projection, PPC_HOST));
     return e;
+}
+
+HosvdFactors hosvd(const Tensor3& A, Index k1, Index k2, Index k3) {  // decompositions.cpp:211-236
+    if (k1 < 1 || k1 > A.n1() || k2 < 1 || k2 > A.n2() || k3 < 1 || k3 > A.n3())
+        throw argument_error("hosvd: multirank (" + std::to_string(k1) + "," + std::to_string(k2) + "," +
+                             std::to_string(k3) + ") outside the tensor extents");
+    HosvdFactors F{Tensor3(k1, k2, k3), Matrix(A.n1(), k1), Matrix(A.n2(), k2), Matrix(A.n3(), k3)};
+    check(ppc_hosvd(A.data(), A.n1(), A.n2(), A.n3(), k1, k2, k3, F.core.data(), F.U1.data(), F.U2.data(),
+                    F.U3.data(), PPC_HOST));
+    return F;
+}
+
+Tensor3 hosvd_reconstruct(const HosvdFactors& F) {  // decompositions.cpp:238-242
+    Tensor3 out(F.U1.rows(), F.U2.rows(), F.U3.rows());
+    check(ppc_hosvd_reconstruct(F.core.data(), F.core.n1(), F.core.n2(), F.core.n3(), F.U1.data(), F.U1.rows(),
+                                F.U2.data(), F.U2.rows(), F.U3.data(), F.U3.rows(), out.data(), PPC_HOST));
+    return out;
+}
+
+MatrixSvdBaseline matrix_svd_baseline(const Tensor3& A, Index k) {  // decompositions.cpp:244-255
+    const Index cap = std::min(A.n1() * A.n3(), A.n2());
+    if (k < 1 || k > cap)
+        throw argument_error("matrix_svd_baseline: k=" + std::to_string(k) + " outside [1," +
+                             std::to_string(cap) + "]");
+    MatrixSvdBaseline out;
+    out.factors.U = Matrix(A.n1() * A.n3(), k);
+    out.factors.s = Vector(k);
+    out.factors.V = Matrix(A.n2(), k);
+    check(ppc_matrix_svd_baseline(A.data(), A.n1(), A.n2(), A.n3(), k, out.factors.U.data(),
+                                  out.factors.s.data(), out.factors.V.data(), &out.error, PPC_HOST));
+    return out;
 }
 
 Index star_q_rank(const Tensor3& A, const Transform& T, double tol_rel) {  // decompositions.cpp:105-114

@@ -183,6 +183,27 @@ int ppc_tsvdq2_error(const double* A, int64_t n1, int64_t n2, int64_t n3,
                      const double* Q, int64_t p, const int64_t* multirank,
                      double* total, double* eckart_young, double* projection, int loc);
 
+/* ---- star-M product and the Tucker / flattened baselines -- */
+/* star_products.cpp:38-49: C = [(A x3 M) facewise (B x3 M)] x3 M^{-1} for an
+ * invertible n3 x n3 M (PPC_DEGENERATE when numerically singular:
+ * numerical rank at 1e-12 below n3). A n1 x m x n3, B m x n2 x n3. */
+int ppc_star_m_product(const double* A, int64_t n1, int64_t m, int64_t n3,
+                       const double* B, int64_t n2, const double* M, double* C, int loc);
+/* decompositions.cpp:211-236 hosvd(A, k1, k2, k3): mode factors from the
+ * unfolding Grams (top eigenvectors, sign rule), core = A x1 U1^T x2 U2^T
+ * x3 U3^T. 1 <= ki <= ni (PPC_ARGUMENT otherwise). */
+int ppc_hosvd(const double* A, int64_t n1, int64_t n2, int64_t n3, int64_t k1, int64_t k2,
+              int64_t k3, double* core, double* U1, double* U2, double* U3, int loc);
+/* decompositions.cpp:238-242 */
+int ppc_hosvd_reconstruct(const double* core, int64_t k1, int64_t k2, int64_t k3,
+                          const double* U1, int64_t n1, const double* U2, int64_t n2,
+                          const double* U3, int64_t n3, double* out, int loc);
+/* decompositions.cpp:244-255 matrix_svd_baseline(A, k): rank-k SVD of the
+ * (n1 n3) x n2 stack of frontal slices; U ((n1 n3) x k), s (k), V (n2 x k),
+ * *error = ||B - U diag(s) V^T||_F measured directly. */
+int ppc_matrix_svd_baseline(const double* A, int64_t n1, int64_t n2, int64_t n3, int64_t k,
+                            double* U, double* s, double* V, double* error, int loc);
+
 /* ---- PT3 container I/O (io.hpp:11-30, io.cpp:52-112) ------ */
 /* Header: "PT3\0", u32 version 1, u8 dtype 1 (float64), u8 flags 0, 2 pad,
  * u64 n1, n2, n3 (little endian), then the mode-1-fastest payload, which is

@@ -327,3 +327,101 @@ def pt3_parse(buf: bytes):
     if len(buf) != 36 + 8 * n1 * n2 * n3:
         raise ValueError("payload size mismatch (truncated or trailing bytes)")
     return np.frombuffer(buf, dtype="<f8", offset=36).reshape((n1, n2, n3), order="F")
+
+
+# ------------------------------------------- star-M and baselines
+# numpy/LAPACK restatements (the reference routes these through Eigen's
+# JacobiSVD; the SVD here is LAPACK's, with the same sign rule).
+def _sign_fix(U, V=None):
+    """matrix_kernels.cpp:16-25: largest-|.| entry of each U column (first on
+    ties) made nonnegative, V flipped with it."""
+    U = U.copy()
+    V = None if V is None else V.copy()
+    for j in range(U.shape[1]):
+        i = int(np.argmax(np.abs(U[:, j])))
+        if U[i, j] < 0:
+            U[:, j] *= -1
+            if V is not None:
+                V[:, j] *= -1
+    return U, V
+
+
+def star_m_product(a, b, m):
+    """star_products.cpp:38-49."""
+    a, b, m = (np.asarray(x, dtype=float) for x in (a, b, m))
+    if m.shape[0] != m.shape[1]:
+        raise ValueError("star_m_product: M must be square")
+    if a.shape[1] != b.shape[0] or a.shape[2] != m.shape[0] or b.shape[2] != m.shape[0]:
+        raise ValueError("star product: shape mismatch")
+    u, s, vt = np.linalg.svd(m)
+    if int(np.sum(s > 1e-12 * s[0])) < m.shape[0]:
+        raise ValueError("star_m_product: M is numerically singular")
+    minv = vt.T @ np.diag(1.0 / s) @ u.T
+    ah = np.einsum("ijk,lk->ijl", a, m)
+    bh = np.einsum("ijk,lk->ijl", b, m)
+    ch = np.einsum("iml,mjl->ijl", ah, bh)
+    return np.asfortranarray(np.einsum("ijk,lk->ijl", ch, minv))
+
+
+def star_m_by_tubes(a, b, m):
+    """tests/support/oracles.hpp:65-80: tube-by-tube summation with an LU solve."""
+    a, b, m = (np.asarray(x, dtype=float) for x in (a, b, m))
+    out = np.zeros((a.shape[0], b.shape[1], a.shape[2]))
+    for j in range(b.shape[1]):
+        for i in range(a.shape[0]):
+            acc = np.zeros(a.shape[2])
+            for l in range(a.shape[1]):
+                acc += np.linalg.solve(m, (m @ a[i, l, :]) * (m @ b[l, j, :]))
+            out[i, j, :] = acc
+    return out
+
+
+def mode_unfold(a, mode):
+    """tensor.cpp:87-107."""
+    a = np.asarray(a, dtype=float)
+    n1, n2, n3 = a.shape
+    if mode == 1:
+        return a.reshape(n1, n2 * n3, order="F")
+    if mode == 2:
+        return np.concatenate([a[:, :, k].T for k in range(n3)], axis=1)
+    return a.reshape(n1 * n2, n3, order="F").T
+
+
+def hosvd(a, k1, k2, k3):
+    """decompositions.cpp:211-236 -> (core, U1, U2, U3)."""
+    a = np.asarray(a, dtype=float)
+    if not (1 <= k1 <= a.shape[0] and 1 <= k2 <= a.shape[1] and 1 <= k3 <= a.shape[2]):
+        raise ValueError("hosvd: multirank outside the tensor extents")
+    fac = []
+    for mode, ki in ((1, k1), (2, k2), (3, k3)):
+        X = mode_unfold(a, mode)
+        # beyond the unfolding's rank: LAPACK's completion of U (full_matrices)
+        u, s, vt = np.linalg.svd(X, full_matrices=ki > min(X.shape))
+        U, _ = _sign_fix(u[:, :ki], None)
+        fac.append(np.asfortranarray(U))
+    U1, U2, U3 = fac
+    g = np.einsum("ijk,ia->ajk", a, U1)
+    g = np.einsum("ajk,jb->abk", g, U2)
+    core = np.einsum("abk,kc->abc", g, U3)
+    return np.asfortranarray(core), U1, U2, U3
+
+
+def hosvd_reconstruct(core, U1, U2, U3):
+    """decompositions.cpp:238-242."""
+    t = np.einsum("abc,ia->ibc", core, U1)
+    t = np.einsum("ibc,jb->ijc", t, U2)
+    return np.asfortranarray(np.einsum("ijc,kc->ijk", t, U3))
+
+
+def matrix_svd_baseline(a, k):
+    """decompositions.cpp:244-255 -> (U, s, V, error)."""
+    a = np.asarray(a, dtype=float)
+    n1, n2, n3 = a.shape
+    B = np.concatenate([a[:, :, s] for s in range(n3)], axis=0)
+    cap = min(B.shape)
+    if k < 1 or k > cap:
+        raise ValueError("matrix_svd_baseline: k out of range")
+    u, s, vt = np.linalg.svd(B, full_matrices=False)
+    U, V = _sign_fix(u[:, :k], vt[:k].T)
+    err = np.linalg.norm(B - U @ np.diag(s[:k]) @ V.T)
+    return U, s[:k].copy(), V, float(err)

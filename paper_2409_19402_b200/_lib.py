@@ -81,6 +81,10 @@ def lib() -> C.CDLL:
         "ppc_pt3_info": (C.c_int, [C.c_char_p, C.POINTER(i64), C.POINTER(i64), C.POINTER(i64)]),
         "ppc_pt3_read": (C.c_int, [C.c_char_p, vp, i64, C.c_int]),
         "ppc_pt3_write": (C.c_int, [C.c_char_p, vp, i64, i64, i64, C.c_int]),
+        "ppc_star_m_product": (C.c_int, [vp, i64, i64, i64, vp, i64, vp, vp, C.c_int]),
+        "ppc_hosvd": (C.c_int, [vp, i64, i64, i64, i64, i64, i64, vp, vp, vp, vp, C.c_int]),
+        "ppc_hosvd_reconstruct": (C.c_int, [vp, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, C.c_int]),
+        "ppc_matrix_svd_baseline": (C.c_int, [vp, i64, i64, i64, i64, vp, vp, vp, pd, C.c_int]),
         "ppc_tsvdq_sweep": (C.c_int, [vp, i64, i64, i64, C.POINTER(i64), i64, C.POINTER(i64), i64, vp, vp, C.c_int]),
         "ppc_tsvdq_compress": (C.c_int, [vp, i64, i64, i64, i64, i64, vp, vp, vp, vp, vp, pd, C.c_int]),
     }

@@ -346,6 +346,78 @@ int ppc_gemm_strided(int64_t M, int64_t N, int64_t K, int64_t batch, double alph
     });
 }
 
+int ppc_star_m_product(const double* A, int64_t n1, int64_t m, int64_t n3, const double* B, int64_t n2,
+                       const double* M, double* C, int loc) {
+    return guarded([&] {
+        validate_loc(loc);
+        check_tensor(n1, m, n3);
+        require_positive(n2, "n2");
+        cudaStream_t s = stream();
+        In a(A, n1 * m * n3, loc), b(B, m * n2 * n3, loc), mm(M, n3 * n3, loc);
+        Out c(C, n1 * n2 * n3, loc);
+        star_m(a.d, n1, m, n3, b.d, n2, mm.d, c.d, s);
+        c.finish();
+        if (loc == PPC_HOST) PPC_CUDA_CHECK(cudaStreamSynchronize(s));
+    });
+}
+
+int ppc_hosvd(const double* A, int64_t n1, int64_t n2, int64_t n3, int64_t k1, int64_t k2, int64_t k3,
+              double* core, double* U1, double* U2, double* U3, int loc) {
+    return guarded([&] {
+        validate_loc(loc);
+        check_tensor(n1, n2, n3);
+        if (k1 < 1 || k1 > n1 || k2 < 1 || k2 > n2 || k3 < 1 || k3 > n3)  // decompositions.cpp:230-233
+            fail(PPC_ARGUMENT, "hosvd: multirank (" + std::to_string(k1) + "," + std::to_string(k2) + "," +
+                                   std::to_string(k3) + ") outside the tensor extents");
+        cudaStream_t s = stream();
+        In a(A, n1 * n2 * n3, loc);
+        Out c(core, k1 * k2 * k3, loc), u1(U1, n1 * k1, loc), u2(U2, n2 * k2, loc), u3(U3, n3 * k3, loc);
+        hosvd(a.d, n1, n2, n3, k1, k2, k3, c.d, u1.d, u2.d, u3.d, s);
+        c.finish();
+        u1.finish();
+        u2.finish();
+        u3.finish();
+        if (loc == PPC_HOST) PPC_CUDA_CHECK(cudaStreamSynchronize(s));
+    });
+}
+
+int ppc_hosvd_reconstruct(const double* core, int64_t k1, int64_t k2, int64_t k3, const double* U1, int64_t n1,
+                          const double* U2, int64_t n2, const double* U3, int64_t n3, double* out, int loc) {
+    return guarded([&] {
+        validate_loc(loc);
+        check_tensor(n1, n2, n3);
+        check_tensor(k1, k2, k3);
+        if (k1 > n1 || k2 > n2 || k3 > n3) fail(PPC_SHAPE, "hosvd_reconstruct: core exceeds the factors");
+        cudaStream_t s = stream();
+        In c(core, k1 * k2 * k3, loc), u1(U1, n1 * k1, loc), u2(U2, n2 * k2, loc), u3(U3, n3 * k3, loc);
+        Out o(out, n1 * n2 * n3, loc);
+        hosvd_reconstruct(c.d, k1, k2, k3, u1.d, n1, u2.d, n2, u3.d, n3, o.d, s);
+        o.finish();
+        if (loc == PPC_HOST) PPC_CUDA_CHECK(cudaStreamSynchronize(s));
+    });
+}
+
+int ppc_matrix_svd_baseline(const double* A, int64_t n1, int64_t n2, int64_t n3, int64_t k, double* U,
+                            double* S, double* V, double* error, int loc) {
+    return guarded([&] {
+        validate_loc(loc);
+        check_tensor(n1, n2, n3);
+        const int64_t cap = std::min(n1 * n3, n2);
+        if (k < 1 || k > cap)  // decompositions.cpp:248-251
+            fail(PPC_ARGUMENT, "matrix_svd_baseline: k=" + std::to_string(k) + " outside [1," +
+                                   std::to_string(cap) + "]");
+        if (!error) fail(PPC_ARGUMENT, "null output");
+        cudaStream_t s = stream();
+        In a(A, n1 * n2 * n3, loc);
+        Out u(U, n1 * n3 * k, loc), sv(S, k, loc), v(V, n2 * k, loc);
+        *error = matrix_svd_baseline(a.d, n1, n2, n3, k, u.d, sv.d, v.d, s);
+        u.finish();
+        sv.finish();
+        v.finish();
+        if (loc == PPC_HOST) PPC_CUDA_CHECK(cudaStreamSynchronize(s));
+    });
+}
+
 int ppc_gram_plan(int64_t N, int64_t n3, int64_t* chunks, int64_t* chunk) {
     return guarded([&] {
         if (N < 1 || n3 < 1) fail(PPC_SHAPE, "gram_plan: extents must be positive");

@@ -36,12 +36,16 @@ void slice_svd(const double* A, int64_t m, int64_t n, int64_t stride, int64_t ba
 // Deterministic Gram G = T^T T (n3 x n3) over the N rows of T (SYRK).
 void gram(const double* T, int64_t N, int64_t n3, double* G, cudaStream_t s);
 // Top-p eigenpairs of a symmetric PSD n x n matrix G: Q (n x p), lambda (p).
-void sym_eig_top(const double* G, int64_t n, int64_t p, double* Q, double* lambda, cudaStream_t s);
+// accurate_vectors: lock on the subspace (rank-p truncation) criteria rather
+// than on eigenvalues alone.
+void sym_eig_top(const double* G, int64_t n, int64_t p, double* Q, double* lambda, cudaStream_t s,
+                 bool accurate_vectors = false);
 // Partial Grams of nchunks consecutive row chunks (T rows x n3, leading dim ldT).
 void gram_chunks(const double* T, int64_t ldT, int64_t rows, int64_t n3, int64_t chunk,
                  int64_t nchunks, double* parts, cudaStream_t s);
 // Eigensolve tail of data_q: Q (sign rule) and sigma from the Gram G.
-void eig_to_basis(const double* G, int64_t n3, int64_t p, double* Q, double* sigma, cudaStream_t s);
+void eig_to_basis(const double* G, int64_t n3, int64_t p, double* Q, double* sigma, cudaStream_t s,
+                  bool accurate_vectors = false);
 // Residual sums over a lateral pixel block [j0, j0+nj) (A_blk leading dims n1, ldA).
 std::array<double, 2> recon_residual_block(const double* A_blk, int64_t n1, int64_t nj, int64_t n3,
                                            int64_t ldA, const double* U, const double* S,
@@ -97,5 +101,20 @@ void tsvdq2_reconstruct(const double* U, const double* S, const double* V, const
 ErrorParts tsvdq2_error(const double* A, int64_t n1, int64_t n2, int64_t n3, const double* U,
                         const double* S, const double* V, const double* Q, int64_t p,
                         const int64_t* multirank, cudaStream_t s);
+
+// SURVEY 8f #4 (baselines.cu)
+// star_products.cpp:38-49: [(A x3 M) facewise (B x3 M)] x3 M^{-1}, M n3 x n3.
+void star_m(const double* A, int64_t n1, int64_t m, int64_t n3, const double* B, int64_t n2,
+            const double* M, double* C, cudaStream_t s);
+// decompositions.cpp:211-236: core (k1,k2,k3), U1 (n1,k1), U2 (n2,k2), U3 (n3,k3).
+void hosvd(const double* A, int64_t n1, int64_t n2, int64_t n3, int64_t k1, int64_t k2, int64_t k3,
+           double* core, double* U1, double* U2, double* U3, cudaStream_t s);
+// decompositions.cpp:238-242
+void hosvd_reconstruct(const double* core, int64_t k1, int64_t k2, int64_t k3, const double* U1, int64_t n1,
+                       const double* U2, int64_t n2, const double* U3, int64_t n3, double* out,
+                       cudaStream_t s);
+// decompositions.cpp:244-255: U ((n1 n3) x k), S (k), V (n2 x k); returns the error.
+double matrix_svd_baseline(const double* A, int64_t n1, int64_t n2, int64_t n3, int64_t k, double* U,
+                           double* S, double* V, cudaStream_t s);
 
 }  // namespace ppc

@@ -136,21 +136,23 @@ void gram(const double* T, int64_t N, int64_t n3, double* G, cudaStream_t s) {
     PPC_CUDA_CHECK(cudaMemcpyAsync(G, parts.d(), sizeof(double) * n3 * n3, cudaMemcpyDeviceToDevice, s));
 }
 
-void sym_eig_top(const double* G, int64_t n, int64_t p, double* Q, double* lambda, cudaStream_t s) {
+void sym_eig_top(const double* G, int64_t n, int64_t p, double* Q, double* lambda, cudaStream_t s,
+                 bool accurate_vectors) {
     // One-sided Jacobi on the PSD G: V = eigenvectors, column norms of G V =
     // eigenvalues, descending (stable order on ties).
     if (n <= kSubspaceMinN) {
         jacobi_svd(G, n, n, n * n, 1, p, nullptr, lambda, Q, nullptr, s);
         return;
     }
-    subspace_eig_top(G, n, 1, p, Q, lambda, s, false);
+    subspace_eig_top(G, n, 1, p, Q, lambda, s, accurate_vectors);
 }
 
-void eig_to_basis(const double* G, int64_t n3, int64_t p, double* Q, double* sigma, cudaStream_t s) {
+void eig_to_basis(const double* G, int64_t n3, int64_t p, double* Q, double* sigma, cudaStream_t s,
+                  bool accurate_vectors) {
     DeviceBuffer lam(sizeof(double) * n3);
     {
         StageTimer tm("eig_q", s);
-        sym_eig_top(G, n3, p, Q, lam.d(), s);
+        sym_eig_top(G, n3, p, Q, lam.d(), s, accurate_vectors);
     }
     sign_rule(Q, n3, p, 1, nullptr, 0, s);  // fix_svd_signs on U3 (matrix_kernels.cpp:35)
     if (sigma) {

@@ -29,7 +29,8 @@ __all__ = [
     "projection_error", "star_q", "star_q_product", "tsvdq", "tsvdq_reconstruct", "tsvdq_error",
     "relative_error", "tsvdq_relative_error", "TsvdqIIFactors", "tsvdq2", "tsvdq2_reconstruct",
     "tsvdq2_error", "read_pt3", "write_pt3", "read_pt3_matrix", "write_pt3_matrix", "pt3_shape",
-    "write_tsvdq_factors", "compress_tsvdq", "tsvdq_sweep", "to_device", "empty_device", "to_host",
+    "write_tsvdq_factors", "star_m", "star_m_product", "HosvdFactors", "hosvd", "hosvd_reconstruct",
+    "MatrixSvdBaseline", "matrix_svd_baseline", "matrix_svd_error", "compress_tsvdq", "tsvdq_sweep", "to_device", "empty_device", "to_host",
     "launch_count",
 ]
 
@@ -354,6 +355,101 @@ def star_q_product(a, b, t):
 
 
 star_q = star_q_product
+
+
+def star_m_product(a, b, m):
+    """star_products.cpp:38-49 (bindings.cpp:151-157 `star_m`)."""
+    args = _Args(a, b, m if _is_dev(m) else None)
+    a_, pa = args.inp(a, 3)
+    b_, pb = args.inp(b, 3)
+    if args.device and not _is_dev(m):
+        m = to_device(m)
+    m_, pm = args.inp(m, 2)
+    n1, k, n3 = a_.shape
+    if m_.shape[0] != m_.shape[1]:
+        raise ShapeError("star_m_product: M must be square")
+    if b_.shape[0] != k:
+        raise ShapeError(f"star product: inner extents differ ({k} vs {b_.shape[0]})")
+    if n3 != m_.shape[0] or b_.shape[2] != m_.shape[0]:
+        raise ShapeError("star product: mode-3 extents must match the transform")
+    out, po = args.out((n1, b_.shape[1], n3))
+    _call(args, _lib.lib().ppc_star_m_product, pa, n1, k, n3, pb, b_.shape[1], pm, po, args.loc)
+    return out
+
+
+star_m = star_m_product
+
+
+@dataclass
+class HosvdFactors:
+    """decompositions.hpp:62-67 (bindings.cpp:144-149)."""
+
+    core: object  # (k1, k2, k3)
+    u1: object    # (n1, k1)
+    u2: object    # (n2, k2)
+    u3: object    # (n3, k3)
+
+
+def hosvd(a, k1: int, k2: int, k3: int) -> HosvdFactors:
+    """decompositions.cpp:211-236."""
+    args = _Args(a)
+    a_, pa = args.inp(a, 3)
+    n1, n2, n3 = a_.shape
+    if not (1 <= k1 <= n1 and 1 <= k2 <= n2 and 1 <= k3 <= n3):
+        raise ArgumentError(f"hosvd: multirank ({k1},{k2},{k3}) outside the tensor extents")
+    core, pc = args.out((k1, k2, k3))
+    u1, p1 = args.out((n1, k1))
+    u2, p2 = args.out((n2, k2))
+    u3, p3 = args.out((n3, k3))
+    _call(args, _lib.lib().ppc_hosvd, pa, n1, n2, n3, k1, k2, k3, pc, p1, p2, p3, args.loc)
+    return HosvdFactors(core, u1, u2, u3)
+
+
+def hosvd_reconstruct(f: HosvdFactors):
+    """decompositions.cpp:238-242."""
+    args = _Args(f.core, f.u1, f.u2, f.u3)
+    c_, pc = args.inp(f.core, 3)
+    u1, p1 = args.inp(f.u1, 2)
+    u2, p2 = args.inp(f.u2, 2)
+    u3, p3 = args.inp(f.u3, 2)
+    k1, k2, k3 = c_.shape
+    n1, n2, n3 = u1.shape[0], u2.shape[0], u3.shape[0]
+    if (u1.shape[1], u2.shape[1], u3.shape[1]) != (k1, k2, k3):
+        raise ShapeError("hosvd_reconstruct: factors do not match the core")
+    out, po = args.out((n1, n2, n3))
+    _call(args, _lib.lib().ppc_hosvd_reconstruct, pc, k1, k2, k3, p1, n1, p2, n2, p3, n3, po, args.loc)
+    return out
+
+
+@dataclass
+class MatrixSvdBaseline:
+    """decompositions.hpp:70-74: rank-k SVD of the (n1 n3) x n2 slice stack."""
+
+    u: object  # (n1 n3, k)
+    s: object  # (k,)
+    v: object  # (n2, k)
+    error: float
+
+
+def matrix_svd_baseline(a, k: int) -> MatrixSvdBaseline:
+    """decompositions.cpp:244-255."""
+    args = _Args(a)
+    a_, pa = args.inp(a, 3)
+    n1, n2, n3 = a_.shape
+    cap = min(n1 * n3, n2)
+    if k < 1 or k > cap:
+        raise ArgumentError(f"matrix_svd_baseline: k={k} outside [1,{cap}]")
+    U, pu = args.out((n1 * n3, k))
+    S, ps = args.out((k,))
+    V, pv = args.out((n2, k))
+    err = C.c_double()
+    _call(args, _lib.lib().ppc_matrix_svd_baseline, pa, n1, n2, n3, k, pu, ps, pv, C.byref(err), args.loc)
+    return MatrixSvdBaseline(U, S, V, err.value)
+
+
+def matrix_svd_error(a, k: int) -> float:
+    """bindings.cpp:225-230."""
+    return matrix_svd_baseline(a, k).error
 
 
 def tsvdq(a, t: Transform, k: int) -> TsvdqFactors:

@@ -298,6 +298,42 @@ int main() {
         check_throws<format_error>([&] { read_pt3(f.string() + ".does-not-exist"); }, "missing");
         fs::remove(f);
     }
+    // test_star_products.cpp:34-68 — star_m
+    {
+        Tensor3 a = make_tube({2, 4, 6, 8}), b = make_tube({1, -1, 1, 0});
+        Tensor3 ab = star_m_product(a, b, haar_transform(4, 4).Q.transpose());
+        const double want[4] = {2, 4, 3, 8};
+        for (Index k = 0; k < 4; ++k) CHECK(std::fabs(ab(0, 0, k) - want[k]) <= 1e-12);
+        Tensor3 e = star_m_product(make_tube({1, 2, 3}), make_tube({4, -5, 0.5}), Matrix::Identity(3, 3));
+        CHECK(std::fabs(e(0, 0, 0) - 4) <= 1e-14 && std::fabs(e(0, 0, 1) + 10) <= 1e-14 &&
+              std::fabs(e(0, 0, 2) - 1.5) <= 1e-14);
+        Matrix singular(2, 2);
+        singular(0, 0) = 1.0;
+        check_throws<degenerate_input_error>([&] { star_m_product(make_tube({1, 2}), make_tube({1, 2}), singular); },
+                                             "singular M");
+        check_throws<shape_error>([&] { star_m_product(make_tube({1, 2}), make_tube({1, 2, 3}), Matrix::Identity(2, 2)); },
+                                  "star_m shapes");
+    }
+    // test_decompositions.cpp:203-255 — hosvd and the matrix SVD baseline
+    {
+        Tensor3 A = seeded(4, 3, 5, 48);
+        HosvdFactors F = hosvd(A, 4, 3, 5);
+        CHECK(frobenius_norm(A - hosvd_reconstruct(F)) <= 1e-10 * frobenius_norm(A));
+        CHECK((F.U1.transpose() * F.U1 - Matrix::Identity(4, 4)).norm() <= 1e-10 * 4);
+        HosvdFactors Fc = hosvd(counterexample(), 2, 2, 1);
+        const double err = frobenius_norm(counterexample() - hosvd_reconstruct(Fc));
+        CHECK(std::fabs(err * err - 2.0) <= 1e-12);
+        check_throws<argument_error>([&] { hosvd(A, 0, 1, 1); }, "hosvd k1");
+        check_throws<argument_error>([&] { hosvd(A, 1, 4, 1); }, "hosvd k2");
+        Tensor3 B = seeded(3, 4, 5, 49);
+        CHECK(matrix_svd_baseline(B, 4).error <= 1e-10 * frobenius_norm(B));
+        MatrixSvdBaseline mb = matrix_svd_baseline(counterexample(), 1);
+        CHECK(mb.factors.s.size() == 1 && std::fabs(mb.factors.s(0) - s2) <= 1e-12);
+        CHECK(std::fabs(mb.error * mb.error - 2.0) <= 1e-12);
+        CHECK(matrix_svd_baseline(Tensor3(2, 3, 2), 2).error == 0.0);
+        check_throws<argument_error>([&] { matrix_svd_baseline(B, 0); }, "msvd k0");
+        check_throws<argument_error>([&] { matrix_svd_baseline(B, 5); }, "msvd k5");
+    }
     // errors: argument / shape / degenerate
     check_throws<argument_error>([&] { identity_transform(4, 9); }, "p > n3");
     check_throws<argument_error>([&] { haar_transform(3, 2); }, "haar n3");

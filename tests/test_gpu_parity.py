@@ -737,3 +737,108 @@ def test_pt3_compress_chain(engine, oracle, tmp_path):
     # and the host path gives the same factors
     fh = engine.tsvdq(a, engine.Transform.custom(engine.to_host(t.q)), 5)
     assert np.abs(fh.s - engine.to_host(fac.s)).max() <= 1e-12 * fh.s.max()
+
+
+# ---------------------------------------------- star-M and baselines
+def test_star_m_kats(engine, oracle):
+    # tests/test_star_products.cpp:34-68
+    a, b = tube([2, 4, 6, 8]), tube([1, -1, 1, 0])
+    h4 = engine.Transform("haar", 4, 4).q
+    np.testing.assert_allclose(engine.star_m_product(a, b, h4.T).ravel(), [2, 4, 3, 8], atol=1e-12)
+    np.testing.assert_allclose(engine.star_m_product(tube([1, 2, 3]), tube([4, -5, 0.5]), np.eye(3)).ravel(),
+                               [4, -10, 1.5], atol=1e-14)
+    A = oracle.random_tensor(2, 3, 4, 31)
+    B = oracle.random_tensor(3, 2, 4, 32)
+    M = oracle.random_matrix(4, 4, 33)
+    fast = engine.star_m_product(A, B, M)
+    assert np.linalg.norm(fast - oracle.star_m_by_tubes(A, B, M)) <= 1e-12 * np.linalg.norm(fast)
+    sing = np.zeros((2, 2))
+    sing[0, 0] = 1.0
+    with pytest.raises(engine.DegenerateInputError):
+        engine.star_m_product(tube([1, 2]), tube([1, 2]), sing)
+    with pytest.raises(engine.ShapeError):
+        engine.star_m_product(tube([1, 2]), tube([1, 2, 3]), np.eye(2))
+    wide = np.zeros((1, 2, 2))
+    with pytest.raises(engine.ShapeError):
+        engine.star_m_product(wide, wide, np.eye(2))
+    # test_star_products.cpp:80-88: star_q with p = n3 is star_m with M = Q^T
+    A = oracle.random_tensor(3, 4, 6, 34)
+    B = oracle.random_tensor(4, 2, 6, 35)
+    t = engine.Transform("random", 6, 6, seed=36)
+    sq = engine.star_q_product(A, B, t)
+    sm = engine.star_m_product(A, B, t.q.T)
+    assert np.linalg.norm(sq - sm) <= 1e-12 * np.linalg.norm(sq)
+
+
+@pytest.mark.parametrize("n1,m,n2,n3", [(37, 29, 41, 24), (64, 96, 80, 200)])
+def test_star_m_vs_oracle(engine, oracle, n1, m, n2, n3):
+    A = oracle.random_tensor(n1, m, n3, 40)
+    B = oracle.random_tensor(m, n2, n3, 41)
+    M = oracle.random_matrix(n3, n3, 42) + 3.0 * np.eye(n3)   # well conditioned
+    got = engine.star_m_product(A, B, M)
+    want = oracle.star_m_product(A, B, M)
+    assert np.linalg.norm(got - want) <= 1e-11 * np.linalg.norm(want)
+
+
+def test_hosvd_kats(engine, oracle):
+    # tests/test_decompositions.cpp:203-232
+    A = oracle.random_tensor(4, 3, 5, 48)
+    f = engine.hosvd(A, 4, 3, 5)
+    assert np.linalg.norm(A - engine.hosvd_reconstruct(f)) <= 1e-10 * np.linalg.norm(A)
+    for U, n in ((f.u1, 4), (f.u2, 3), (f.u3, 5)):
+        assert np.linalg.norm(U.T @ U - np.eye(n)) <= 1e-10 * n
+    x, y, z = oracle.random_matrix(4, 1, 1), oracle.random_matrix(3, 1, 2), oracle.random_matrix(5, 1, 3)
+    R = np.einsum("i,j,k->ijk", x[:, 0], y[:, 0], z[:, 0])
+    assert np.linalg.norm(R - engine.hosvd_reconstruct(engine.hosvd(R, 1, 1, 1))) <= 1e-10 * np.linalg.norm(R)
+    C = counterexample()
+    err = np.linalg.norm(C - engine.hosvd_reconstruct(engine.hosvd(C, 2, 2, 1)))
+    assert abs(err * err - 2.0) <= 1e-12
+    for bad in ((0, 1, 1), (1, 4, 1)):
+        with pytest.raises(engine.ArgumentError):
+            engine.hosvd(A, *bad)
+
+
+@pytest.mark.parametrize("shape,ks", [((12, 9, 14), (5, 4, 6)), ((30, 24, 20), (30, 24, 20)),
+                                      ((200, 180, 170), (20, 16, 12)), ((6, 5, 40), (6, 5, 40))])
+def test_hosvd_vs_oracle(engine, oracle, shape, ks):
+    A = oracle.random_tensor(*shape, 50)
+    f = engine.hosvd(A, *ks)
+    core, U1, U2, U3 = oracle.hosvd(A, *ks)
+    nrm = np.linalg.norm(A)
+    rec = engine.hosvd_reconstruct(f)
+    assert np.linalg.norm(rec - oracle.hosvd_reconstruct(core, U1, U2, U3)) <= 1e-10 * nrm
+    assert abs(np.linalg.norm(f.core) - np.linalg.norm(core)) <= 1e-10 * nrm
+    # factors agree column by column where the unfolding's spectrum separates them
+    for mode, (Ug, Uo) in enumerate(((f.u1, U1), (f.u2, U2), (f.u3, U3)), start=1):
+        s = np.linalg.svd(oracle.mode_unfold(A, mode), compute_uv=False)
+        s = np.concatenate([s, np.zeros(Ug.shape[0])])
+        for j in range(Ug.shape[1]):
+            gap = min(s[j - 1] - s[j] if j else np.inf, s[j] - s[j + 1]) / s[0]
+            if gap >= 1e-6 and s[j] > 1e-8 * s[0]:
+                assert np.abs(Ug[:, j] - Uo[:, j]).max() <= 1e-8, (mode, j)
+
+
+def test_matrix_svd_baseline_vs_oracle(engine, oracle):
+    # tests/test_decompositions.cpp:234-255
+    A = oracle.random_tensor(3, 4, 5, 49)
+    assert engine.matrix_svd_baseline(A, 4).error <= 1e-10 * np.linalg.norm(A)
+    mb = engine.matrix_svd_baseline(counterexample(), 1)
+    assert mb.s.shape == (1,) and abs(mb.s[0] - SQ2) <= 1e-12 and abs(mb.error ** 2 - 2.0) <= 1e-12
+    assert engine.matrix_svd_baseline(np.zeros((2, 3, 2)), 2).error == 0.0
+    for k in (0, 5):
+        with pytest.raises(engine.ArgumentError):
+            engine.matrix_svd_baseline(A, k)
+    for shape, k in (((20, 30, 8), 6), ((60, 200, 30), 12)):
+        A = oracle.random_tensor(*shape, 51)
+        got = engine.matrix_svd_baseline(A, k)
+        U, s, V, err = oracle.matrix_svd_baseline(A, k)
+        nrm = np.linalg.norm(A)
+        assert np.abs(got.s - s).max() <= 1e-10 * s[0]
+        assert abs(got.error - err) <= 1e-10 * nrm
+        assert abs(engine.matrix_svd_error(A, k) - err) <= 1e-10 * nrm
+        sf = np.linalg.svd(np.concatenate([A[:, :, z] for z in range(shape[2])]), compute_uv=False)
+        for j in range(k):
+            gap = min(sf[j - 1] - sf[j] if j else np.inf, sf[j] - sf[j + 1]) / sf[0]
+            if gap >= 1e-6:
+                assert np.abs(got.u[:, j] - U[:, j]).max() <= 1e-8
+                assert np.abs(got.v[:, j] - V[:, j]).max() <= 1e-8

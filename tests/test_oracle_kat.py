@@ -306,3 +306,54 @@ def test_tsvdq2_error_decomposition_and_selection_rule():
         for _, s, _ in pool[:K]:
             want[s] += 1
         assert list(mr) == list(want)
+
+
+# --------------------------------------------------- star-M and baselines
+def test_star_m_kats():
+    # tests/test_star_products.cpp:34-55
+    a, b = tube([2, 4, 6, 8]), tube([1, -1, 1, 0])
+    np.testing.assert_allclose(ppo.star_m_product(a, b, ppo.haar_q(4, 4).T).ravel(), [2, 4, 3, 8],
+                               atol=1e-12)
+    np.testing.assert_allclose(ppo.star_m_product(tube([1, 2, 3]), tube([4, -5, 0.5]), np.eye(3)).ravel(),
+                               [4, -10, 1.5], atol=1e-14)
+    A = ppo.random_tensor(2, 3, 4, 31)
+    B = ppo.random_tensor(3, 2, 4, 32)
+    M = ppo.random_matrix(4, 4, 33)
+    fast = ppo.star_m_product(A, B, M)
+    slow = ppo.star_m_by_tubes(A, B, M)
+    assert np.linalg.norm(fast - slow) <= 1e-12 * np.linalg.norm(fast)
+    sing = np.zeros((2, 2))
+    sing[0, 0] = 1.0
+    with pytest.raises(ValueError):
+        ppo.star_m_product(tube([1, 2]), tube([1, 2]), sing)
+
+
+def test_hosvd_kats():
+    # tests/test_decompositions.cpp:203-232
+    A = ppo.random_tensor(4, 3, 5, 48)
+    core, U1, U2, U3 = ppo.hosvd(A, 4, 3, 5)
+    assert np.linalg.norm(A - ppo.hosvd_reconstruct(core, U1, U2, U3)) <= 1e-10 * np.linalg.norm(A)
+    for U, n in ((U1, 4), (U2, 3), (U3, 5)):
+        assert np.linalg.norm(U.T @ U - np.eye(n)) <= 1e-10 * n
+    x, y, z = ppo.random_matrix(4, 1, 1), ppo.random_matrix(3, 1, 2), ppo.random_matrix(5, 1, 3)
+    R = np.einsum("i,j,k->ijk", x[:, 0], y[:, 0], z[:, 0])
+    f = ppo.hosvd(R, 1, 1, 1)
+    assert np.linalg.norm(R - ppo.hosvd_reconstruct(*f)) <= 1e-10 * np.linalg.norm(R)
+    C = counterexample()
+    err = np.linalg.norm(C - ppo.hosvd_reconstruct(*ppo.hosvd(C, 2, 2, 1)))
+    assert abs(err * err - 2.0) <= 1e-12
+    for bad in ((0, 1, 1), (1, 4, 1)):
+        with pytest.raises(ValueError):
+            ppo.hosvd(A, *bad)
+
+
+def test_matrix_svd_baseline_kats():
+    # tests/test_decompositions.cpp:234-255
+    A = ppo.random_tensor(3, 4, 5, 49)
+    assert ppo.matrix_svd_baseline(A, 4)[3] <= 1e-10 * np.linalg.norm(A)
+    U, s, V, err = ppo.matrix_svd_baseline(counterexample(), 1)
+    assert s.shape == (1,) and abs(s[0] - SQ2) <= 1e-12 and abs(err * err - 2.0) <= 1e-12
+    assert ppo.matrix_svd_baseline(np.zeros((2, 3, 2)), 2)[3] == 0.0
+    for k in (0, 5):
+        with pytest.raises(ValueError):
+            ppo.matrix_svd_baseline(A, k)
