@@ -35,86 +35,127 @@ __device__ __forceinline__ double warp_sum(double v) {
     return v;
 }
 
-// Sum over the 16 lanes of a half-warp (fixed order, deterministic).
-__device__ __forceinline__ double half_sum(double v) {
-#pragma unroll
-    for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    return v;
-}
-
 // Round-robin pair pi of round r among P (even) players, returned as a < c.
-__device__ __forceinline__ void rr_pair(int64_t r, int64_t pi, int64_t P, int64_t& a, int64_t& c) {
+// 32-bit arithmetic: P <= 2^15 on every path (the working set lives in
+// shared memory or an L2-resident workspace).
+__device__ __forceinline__ void rr_pair(int r, int pi, int P, int& a, int& c) {
     if (pi == 0) {
         a = r;
         c = P - 1;
     } else {
-        a = (r + pi) % (P - 1);
-        c = (r + P - 1 - pi) % (P - 1);
+        const int m = P - 1;
+        a = r + pi;
+        if (a >= m) a -= m;
+        c = r + m - pi;
+        if (c >= m) c -= m;
     }
     if (a > c) {
-        const int64_t t = a;
+        const int t = a;
         a = c;
         c = t;
     }
 }
 
-// One Jacobi round: every pair of the round handled by a 16-lane group.
-// Rotates the columns of W (R rows) and, if Va != nullptr, of Va (Cc rows);
-// logs (cs, sn) per pair when lg != nullptr. Returns nonzero in *rot if any
-// rotation was applied.
-__device__ __forceinline__ void jacobi_round(double* W, int64_t R, double* Va, int64_t Cc, int64_t P,
-                                             int64_t r, double tol, double2* lg, int* rot, double gtol = 0.0) {
+// Sum over the G lanes of a lane group (fixed butterfly order, deterministic).
+template <int G>
+__device__ __forceinline__ double group_sum(double v) {
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// One Jacobi round: every pair of the round handled by a G-lane group. Rotates the columns of W
+// (R rows) and, if Va != nullptr, of Va (Cc rows); logs (cs, sn) per pair when
+// lg != nullptr. Returns nonzero in *rot if any rotation was applied. Lane l
+// of a group sums rows l, l+G, ... in ascending order, then a fixed butterfly.
+template <int G>
+__device__ __forceinline__ void jacobi_round_g(double* W, int R, double* Va, int Cc, int P, int r, double tol,
+                                               double2* lg, int* rot, double gtol) {
     const int tid = threadIdx.x, nt = blockDim.x;
-    const int grp = tid >> 4, l16 = tid & 15, ngrp = nt >> 4;
-    for (int64_t base = 0; base < P / 2; base += ngrp) {
-        const int64_t pi = base + grp;
+    const int grp = tid / G, lg_ = tid & (G - 1), ngrp = nt / G;
+    const double tol2 = tol * tol;
+    for (int base = 0; base < P / 2; base += ngrp) {
+        const int pi = base + grp;
         // all 32 lanes of a warp stay converged for the shuffles: pairs past
         // the end work on a dummy (no memory traffic)
         const bool live = pi < P / 2;
-        int64_t a = 0, c = 0;
+        int a = 0, c = 0;
         if (live) rr_pair(r, pi, P, a, c);
         const bool act = live && c < Cc;
         double al = 0.0, be = 0.0, ga = 0.0;
         if (act) {
-            const double* wa = W + a * R;
-            const double* wc = W + c * R;
-            for (int64_t i = l16; i < R; i += 16) {
+            const double* wa = W + (int64_t)a * R;
+            const double* wc = W + (int64_t)c * R;
+            int i = lg_;
+            for (; i + 3 * G < R; i += 4 * G) {
+                const double x0 = wa[i], y0 = wc[i], x1 = wa[i + G], y1 = wc[i + G];
+                const double x2 = wa[i + 2 * G], y2 = wc[i + 2 * G], x3 = wa[i + 3 * G], y3 = wc[i + 3 * G];
+                al = fma(x0, x0, al); be = fma(y0, y0, be); ga = fma(x0, y0, ga);
+                al = fma(x1, x1, al); be = fma(y1, y1, be); ga = fma(x1, y1, ga);
+                al = fma(x2, x2, al); be = fma(y2, y2, be); ga = fma(x2, y2, ga);
+                al = fma(x3, x3, al); be = fma(y3, y3, be); ga = fma(x3, y3, ga);
+            }
+            for (; i < R; i += G) {
                 const double x = wa[i], y = wc[i];
                 al = fma(x, x, al);
                 be = fma(y, y, be);
                 ga = fma(x, y, ga);
             }
         }
-        al = half_sum(al);
-        be = half_sum(be);
-        ga = half_sum(ga);
+        al = group_sum<G>(al);
+        be = group_sum<G>(be);
+        ga = group_sum<G>(ga);
         double cs = 1.0, sn = 0.0;
-        if (act && ga != 0.0 && fabs(ga) > tol * sqrt(al * be) &&
+        // |ga| > tol sqrt(al be), compared in squares (al, be >= 0)
+        if (act && ga != 0.0 && ga * ga > tol2 * (al * be) &&
             (gtol == 0.0 || fabs(ga) > gtol * (sqrt(al) + sqrt(be)))) {
             const double zeta = (be - al) / (2.0 * ga);
             const double tt = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
             cs = rsqrt(1.0 + tt * tt);
             sn = cs * tt;
-            double* wa = W + a * R;
-            double* wc = W + c * R;
-            for (int64_t i = l16; i < R; i += 16) {
+            double* wa = W + (int64_t)a * R;
+            double* wc = W + (int64_t)c * R;
+            int i = lg_;
+            for (; i + G < R; i += 2 * G) {
+                const double x0 = wa[i], y0 = wc[i], x1 = wa[i + G], y1 = wc[i + G];
+                wa[i] = cs * x0 - sn * y0;
+                wc[i] = sn * x0 + cs * y0;
+                wa[i + G] = cs * x1 - sn * y1;
+                wc[i + G] = sn * x1 + cs * y1;
+            }
+            for (; i < R; i += G) {
                 const double x = wa[i], y = wc[i];
                 wa[i] = cs * x - sn * y;
                 wc[i] = sn * x + cs * y;
             }
             if (Va) {
-                double* va = Va + a * Cc;
-                double* vc = Va + c * Cc;
-                for (int64_t i = l16; i < Cc; i += 16) {
-                    const double x = va[i], y = vc[i];
-                    va[i] = cs * x - sn * y;
-                    vc[i] = sn * x + cs * y;
+                double* va = Va + (int64_t)a * Cc;
+                double* vc = Va + (int64_t)c * Cc;
+                int j = lg_;
+                for (; j + G < Cc; j += 2 * G) {
+                    const double x0 = va[j], y0 = vc[j], x1 = va[j + G], y1 = vc[j + G];
+                    va[j] = cs * x0 - sn * y0;
+                    vc[j] = sn * x0 + cs * y0;
+                    va[j + G] = cs * x1 - sn * y1;
+                    vc[j + G] = sn * x1 + cs * y1;
+                }
+                for (; j < Cc; j += G) {
+                    const double x = va[j], y = vc[j];
+                    va[j] = cs * x - sn * y;
+                    vc[j] = sn * x + cs * y;
                 }
             }
-            if (l16 == 0) *rot = 1;
+            if (lg_ == 0) *rot = 1;
         }
-        if (lg && live && l16 == 0) lg[pi] = make_double2(cs, sn);
+        if (lg && live && lg_ == 0) lg[pi] = make_double2(cs, sn);
     }
+}
+
+__device__ __forceinline__ void jacobi_round(double* W, int64_t R, double* Va, int64_t Cc, int64_t P, int64_t r,
+                                             double tol, double2* lg, int* rot, double gtol = 0.0) {
+    // 16-lane groups: measured faster than 4/8-lane groups on the 64..160
+    // column eigenproblems (latency, not issue, bound with fewer warps)
+    jacobi_round_g<16>(W, (int)R, Va, (int)Cc, (int)P, (int)r, tol, lg, rot, gtol);
 }
 
 __global__ void __launch_bounds__(1024, 1) jacobi_svd_kernel(const double* __restrict__ A, int64_t m, int64_t n,

@@ -339,9 +339,10 @@ void rayleigh_ritz(Work& w, const double* G, int64_t sG, double* Xn, int64_t c0,
 }  // namespace
 
 // Chebyshev degree cap per outer iteration (runtime-tunable for experiments)
-static double max_degree() {
+static double max_degree(bool basis) {
     static const double v = std::getenv("PPC_CHEB_MAX") ? std::atof(std::getenv("PPC_CHEB_MAX")) : 10.0;
-    return v;
+    static const double vq = std::getenv("PPC_CHEB_MAX_Q") ? std::atof(std::getenv("PPC_CHEB_MAX_Q")) : 10.0;
+    return basis ? vq : v;
 }
 
 // tail2[z] = ||A_z - U_z diag(S_z) V_z^T||_F^2 (= the discarded energy sum_{j>=k} s_j^2
@@ -456,6 +457,10 @@ void subspace_eig_top(const double* G, int64_t r, int64_t batch, int64_t k, doub
                                        std::min(1.0, cross / (Rn + 1e-300));
                     thrv[j] = std::max(thr, std::max(32.0 * 2.22e-16 * scale, std::min(ti, tii)));
                 }
+                // A locked column's residual couples into the deflated operator
+                // and floors the residuals of the columns after it, so no column
+                // may lock looser than any later wanted column needs.
+                for (int64_t j = k - 2; j >= 0; --j) thrv[j] = std::min(thrv[j], thrv[j + 1]);
                 while (L < k && rr[L] <= thrv[L]) ++L;
             } else if (vectors_for_reconstruction) {
                 while (L < k && rr[L] <= thr) ++L;  // locked prefix
@@ -488,7 +493,7 @@ void subspace_eig_top(const double* G, int64_t r, int64_t batch, int64_t k, doub
             // block's bottom (x = 1, T_d(1) = 1) kept <= 1e10;
             // (b) the spread inside the wanted active set (precision of the
             // smaller wanted components) kept <= 1e6.
-            double d = max_degree();
+            double d = max_degree(w.basis);
             if (xt > 1.0) d = std::min(d, std::acosh(1e10) / std::acosh(xt));
             const double spread = std::acosh(xt) - std::acosh(xk);
             if (spread > 0) d = std::min(d, std::log(1e6) / spread);
