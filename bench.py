@@ -39,7 +39,14 @@ FP64_PEAK_FALLBACK = 36.914  # TFLOP/s, MEASURED_FP64.json (DMMA m8n8k4, this po
 
 def load_peaks():
     peaks = {"hbm_gbs": 6540.5, "fp64_tflops": FP64_PEAK_FALLBACK,
-             "hbm_src": "MEASURED_PEAKS.json", "fp64_src": "MEASURED_FP64.json"}
+             "hbm_src": "MEASURED_PEAKS.json", "fp64_src": "MEASURED_FP64.json",
+             "int8_tops": 4500.0, "int8_src": "nominal B200 dense INT8 (fallback)"}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_INT8.json")) as f:
+            peaks["int8_tops"] = float(json.load(f)["int8_tops"])
+        peaks["int8_src"] = "MEASURED_INT8.json (cuBLASLt int8 8192^3 on this pool, tools/int8_peak.py)"
+    except Exception:
+        pass
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             peaks["hbm_gbs"] = float(json.load(f)["hbm_gbs"])
@@ -128,7 +135,7 @@ def ncu_traffic(workload, stage):
     committed ncu --set full capture (profiles/<round>/ncu_<stage>_<workload>_raw.csv)."""
     import csv
     import glob
-    names = {"gram_syrk": "ws_syrk", "facewise": "cfg4_gemms"}
+    names = {"gram_syrk": "ws_syrk", "facewise": "cfg4_gemms", "ozaki_syrk": "ozaki_syrk"}
     key = names.get(stage, stage)
     for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*", f"ncu_{key}*raw.csv")), reverse=True):
         if workload not in os.path.basename(path) and stage != "facewise":
@@ -303,8 +310,9 @@ class Tsvdq:
 
     def dominant(self, stages):
         # the single most expensive kernel launch of the step (ncu launch
-        # list: the Gram SYRK); slice_svd is a composite of many kernels
-        return "gram_syrk", "tensor"
+        # list: the Gram SYRK, on the INT8 tensor cores when the Ozaki path
+        # runs); slice_svd is a composite of many kernels
+        return ("ozaki_syrk", "int8") if "ozaki_syrk" in stages else ("gram_syrk", "tensor")
 
     def e2e_setup(self):
         torch = self.torch
@@ -409,7 +417,7 @@ class TsvdqSharded:
         return self.in_bytes / sec / 1e9 / self.world  # main() multiplies by world
 
     def dominant(self, stages):
-        return "gram_syrk", "tensor"
+        return ("ozaki_syrk", "int8") if "ozaki_syrk" in stages else ("gram_syrk", "tensor")
 
     def e2e_setup(self):
         self.hA = flat_host(self.A)
@@ -629,7 +637,16 @@ def main():
     dom, bound = wl.dominant(stages)
     st = stages.get(dom, {"ms": float("nan"), "n": 1, "flops": 0.0, "bytes": 0.0})
     avg_ms = st["ms"] / max(1, st["n"])
-    if bound == "tensor":
+    if bound == "int8":
+        # INT8 tensor-core ops (2 per multiply-add) of the Ozaki digit products
+        achieved = (st["flops"] / max(1, st["n"])) / (avg_ms / 1e3) / 1e12
+        traffic, tsrc = ncu_traffic(args.workload, dom)
+        roof = {"bound": "tensor", "achieved": achieved, "peak": peaks["int8_tops"],
+                "unit": "TFLOP/s", "op_kind": "int8 ops (TOPS), tcgen05 kind::i8",
+                "frac": achieved / peaks["int8_tops"], "traffic": traffic,
+                "algorithmic_bytes": st["bytes"] / max(1, st["n"]), "kernel": dom,
+                "peak_source": peaks["int8_src"], "traffic_source": tsrc}
+    elif bound == "tensor":
         achieved = (st["flops"] / max(1, st["n"])) / (avg_ms / 1e3) / 1e12
         traffic, tsrc = ncu_traffic(args.workload, dom)
         roof = {"bound": "tensor", "achieved": achieved, "peak": peaks["fp64_tflops"],

@@ -76,6 +76,10 @@ int ppc_timing_enable(int on);
  * eligible), 1 = always the cp.async kernel. Both accumulate every output in
  * the same order, so results are bitwise identical (used by the tests). */
 int ppc_set_gemm_path(int mode);
+/* FP64 Gram path: 1 = automatic (the INT8 tensor-core Ozaki SYRK, 7 digits,
+ * where eligible; default), 0 = always the FP64 DMMA SYRK. PPC_OZAKI=0 in the
+ * environment sets 0. Results agree to ~1e-14 relative (not bitwise). */
+int ppc_set_ozaki(int mode);
 int ppc_timing_report(char* buf, int64_t cap, int reset);
 
 /* ---- L3 kernels (tensor.hpp, matrix_kernels.hpp) ------------------------ */

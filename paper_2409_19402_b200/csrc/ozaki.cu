@@ -1,0 +1,356 @@
+// FP64 Gram SYRK on the INT8 tensor cores (tcgen05 kind::i8): the Ozaki
+// scheme (Ozaki, Ogita, Oishi, Rump 2012; the INT8 form of Ootomo, Ozaki and
+// Yokota 2024).
+//
+// The data-driven basis needs G = T^T T over N = n1*n2 pixel rows. Per chunk
+// of KC rows and per column j of T, the column is scaled by a power of two
+// sigma_j with |T(:,j)| / sigma_j <= 1/2 and cut into S signed 7-bit digits,
+//     T(i,j) = sigma_j * ( sum_s d_s(i,j) 2^{-7s} + r(i,j) 2^{-7S} ),
+// |d_s| <= 64, |r| <= 1/2 (every step is exact in FP64). Then
+//     G(a,b) ~= sigma_a sigma_b sum_{L=2}^{S+1} 2^{-7L} Q_L(a,b),
+//     Q_L = sum_{s+t=L} D_s^T D_t,
+// where every Q_L is an exact int32 sum of int8 products (KC * 64^2 * S <
+// 2^31) computed by tcgen05.mma into its own TMEM accumulator. The FP64
+// epilogue adds the levels smallest first. With S = 7 the truncation is
+// ~2^{-49} |T_a| |T_b| per product and the per-row sum is exact, so the error
+// does not grow with the chunk length (FP64 SYRK: ~sqrt(K) eps).
+//
+// Kernels: ozaki_split_kernel (one CTA per (chunk, column): max, scale,
+// digits), ozaki_syrk_kernel (TMA SWIZZLE_64B operand tiles of all S digit
+// planes per stage, one elected thread issuing the S(S+1)/2 digit-pair MMAs,
+// four epilogue warps draining TMEM), sub_sum_kernel (fixed-order sum of a
+// plan chunk's sub-chunk partials).
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdlib>
+#include <mutex>
+
+#include "internal.h"
+#include "ozaki.h"
+#include "umma_i8.cuh"
+
+namespace ppc {
+
+namespace {
+
+using namespace umma;
+
+constexpr int kS = 7;          // digits per value
+constexpr int kBM = 128;       // UMMA M
+constexpr int kBN = 64;        // UMMA N (S levels x 64 columns of TMEM)
+constexpr int kBK = 64;        // bytes (= int8 elements) of K per stage, SWIZZLE_64B
+constexpr int kStages = 2;
+constexpr int64_t kKC = 65536;  // rows per sub-chunk: 65536 * 64^2 * 7 < 2^31
+
+// ------------------------------------------------------------------ split
+// One CTA per (sub-chunk c, column j). D layout: [(c*S + s)*n3 + j][KCp] int8.
+__global__ void __launch_bounds__(512) ozaki_split_kernel(const double* __restrict__ T, int64_t ldT, int64_t rows,
+                                                          int64_t n3, int64_t KC, int64_t KCp,
+                                                          int8_t* __restrict__ D, double* __restrict__ scale) {
+    const int64_t j = blockIdx.x, c = blockIdx.y;
+    const int64_t r0 = c * KC;
+    const int64_t len = std::min<int64_t>(KC, rows - r0);
+    const double* col = T + j * ldT + r0;
+    double mx = 0.0;
+    for (int64_t i = threadIdx.x; i < len; i += blockDim.x) mx = fmax(mx, fabs(col[i]));
+    __shared__ double red[16];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        mx = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if (threadIdx.x == 0) red[0] = mx;
+    }
+    __syncthreads();
+    mx = red[0];
+    // sigma = 2^e with mx / sigma <= 1/2 (mx = 0: all digits zero)
+    const int e = mx > 0.0 ? ilogb(mx) + 2 : 0;
+    if (threadIdx.x == 0) scale[c * n3 + j] = mx > 0.0 ? ldexp(1.0, e) : 0.0;
+    int8_t* out = D + ((c * kS) * n3 + j) * KCp;
+    const int64_t plane = n3 * KCp;
+    for (int64_t i = threadIdx.x; i < KCp; i += blockDim.x) {
+        double x = i < len ? ldexp(col[i], -e) : 0.0;
+#pragma unroll
+        for (int s = 0; s < kS; ++s) {
+            const double t = x * 128.0;
+            const double d = rint(t);
+            x = t - d;
+            out[s * plane + i] = (int8_t)d;
+        }
+    }
+}
+
+// ------------------------------------------------------------------- syrk
+struct SyrkParams {
+    int64_t n3, nsub;
+    int64_t ntiles_n;      // column tiles (kBN wide)
+    int64_t tiles;         // upper-triangle tiles per sub-chunk
+    int64_t KCp;           // padded sub-chunk length (multiple of kBK)
+    const double* scale;   // [nsub][n3]
+    double* out;           // [nsub][n3][n3] column-major partials
+};
+
+// tile t (upper-triangle order) -> (mb, nb): column tile nb holds
+// floor((nb*kBN + kBN - 1) / kBM) + 1 row tiles.
+__device__ __forceinline__ void tri_tile(int64_t t, int64_t& mb, int64_t& nb) {
+    nb = 0;
+    for (;;) {
+        const int64_t cnt = (nb * kBN + kBN - 1) / kBM + 1;
+        if (t < cnt) break;
+        t -= cnt;
+        ++nb;
+    }
+    mb = t;
+}
+
+__global__ void __launch_bounds__(192, 1)
+    ozaki_syrk_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                      const SyrkParams P) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    constexpr int A_TILE = kBM * kBK, B_TILE = kBN * kBK;
+    constexpr int STAGE = kS * (A_TILE + B_TILE);
+    uint64_t* full = reinterpret_cast<uint64_t*>(base + kStages * STAGE);
+    uint64_t* empty = full + kStages;
+    uint64_t* tfull = empty + kStages;
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(tfull + 1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t item = blockIdx.x;
+    const int64_t sub = item / P.tiles;
+    int64_t mb, nb;
+    tri_tile(item - sub * P.tiles, mb, nb);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            bar_init(&full[s], 1);
+            bar_init(&empty[s], 1);
+        }
+        bar_init(tfull, 1);
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc<512>(tslot);
+    fence_before_sync();
+    __syncthreads();
+    fence_after_sync();
+    const uint32_t tmem = *tslot;
+    const int nk = (int)(P.KCp / kBK);
+
+    if (warp == 0) {
+        if (elect_one()) {
+            for (int kb = 0; kb < nk; ++kb) {
+                const int st = kb % kStages;
+                bar_wait(&empty[st], ((kb / kStages) & 1) ^ 1);
+                bar_expect_tx(&full[st], STAGE);
+                uint8_t* sa = base + st * STAGE;
+                uint8_t* sb = sa + kS * A_TILE;
+#pragma unroll
+                for (int s = 0; s < kS; ++s) {
+                    const int plane = (int)(sub * kS + s);
+                    tma_load_3d(sa + s * A_TILE, &mapA, &full[st], kb * kBK, (int)(mb * kBM), plane);
+                    tma_load_3d(sb + s * B_TILE, &mapB, &full[st], kb * kBK, (int)(nb * kBN), plane);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        constexpr uint32_t idesc = idesc_i8<kBM, kBN>();
+        for (int kb = 0; kb < nk; ++kb) {
+            const int st = kb % kStages;
+            bar_wait(&full[st], (kb / kStages) & 1);
+            fence_after_sync();
+            if (elect_one()) {
+                const uint8_t* sa = base + st * STAGE;
+                const uint8_t* sb = sa + kS * A_TILE;
+#pragma unroll
+                for (int l = 0; l < kS; ++l) {  // level L = l + 2
+                    const int L = l + 2;
+                    const int s_lo = L - kS > 1 ? L - kS : 1, s_hi = L - 1 < kS ? L - 1 : kS;
+#pragma unroll
+                    for (int s = s_lo; s <= s_hi; ++s) {
+                        const int t = L - s;
+                        const uint64_t da = sdesc_k_sw64(sa + (s - 1) * A_TILE);
+                        const uint64_t db = sdesc_k_sw64(sb + (t - 1) * B_TILE);
+#pragma unroll
+                        for (int kk = 0; kk < kBK / 32; ++kk)
+                            mma_i8(tmem + (uint32_t)(l * kBN), da + (uint64_t)(kk * 2), db + (uint64_t)(kk * 2), idesc,
+                                   (kb > 0 || s > s_lo || kk > 0) ? 1u : 0u);
+                    }
+                }
+                mma_commit(&empty[st]);
+            }
+            __syncwarp();
+        }
+        if (elect_one()) mma_commit(tfull);
+        __syncwarp();
+    } else {
+        // epilogue: warp w drains TMEM lanes 32*(w%4) .. +32 (rows of the tile)
+        bar_wait(tfull, 0);
+        fence_after_sync();
+        const int q = warp & 3;
+        const int64_t m = mb * kBM + q * 32 + lane;
+        double acc[kBN];
+#pragma unroll
+        for (int j = 0; j < kBN; ++j) acc[j] = 0.0;
+#pragma unroll 1
+        for (int l = kS - 1; l >= 0; --l) {  // smallest weight first
+            const double w = ldexp(1.0, -7 * (l + 2));
+#pragma unroll
+            for (int h = 0; h < kBN; h += 32) {
+                int32_t v[32];
+                tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(l * kBN + h), v);
+                tmem_ld_wait();
+#pragma unroll
+                for (int j = 0; j < 32; ++j) acc[h + j] = fma((double)v[j], w, acc[h + j]);
+            }
+        }
+        if (m < P.n3) {
+            const double* sc = P.scale + sub * P.n3;
+            const double sm = sc[m];
+            double* C = P.out + sub * P.n3 * P.n3;
+#pragma unroll 4
+            for (int j = 0; j < kBN; ++j) {
+                const int64_t n = nb * kBN + j;
+                if (n >= P.n3) break;
+                const double v = acc[j] * sm * sc[n];
+                C[m + n * P.n3] = v;  // (m, n), coalesced over the warp's rows
+                C[n + m * P.n3] = v;  // mirror (n, m): the same exact integer sums
+            }
+        }
+    }
+    fence_before_sync();
+    __syncthreads();
+    if (warp == 1) tmem_free<512>(tmem);
+}
+
+// parts[c] = sum_{u < per} sub[c*per + u] in ascending u (fixed order)
+__global__ void sub_sum_kernel(const double* __restrict__ sub, int64_t per, int64_t elems, int64_t total,
+                               double* __restrict__ parts) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
+        const int64_t c = i / elems, e = i - c * elems;
+        const double* p = sub + c * per * elems + e;
+        double a = p[0];
+        for (int64_t u = 1; u < per; ++u) a += p[u * elems];
+        parts[i] = a;
+    }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    return fn;
+}
+
+// 3-D int8 map over the digit planes: (k, row, plane), box (kBK, rows, 1),
+// SWIZZLE_64B (rows beyond n3 read as zeros: they never reach another plane).
+bool make_digit_map(CUtensorMap* map, const int8_t* D, int64_t KCp, int64_t n3, int64_t planes, int box_rows) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[3] = {(cuuint64_t)KCp, (cuuint64_t)n3, (cuuint64_t)planes};
+    cuuint64_t strides[2] = {(cuuint64_t)KCp, (cuuint64_t)(KCp * n3)};
+    cuuint32_t box[3] = {(cuuint32_t)kBK, (cuuint32_t)box_rows, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(D), dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+std::atomic<int> g_ozaki{-1};
+bool ozaki_enabled() {
+    int v = g_ozaki.load();
+    if (v < 0) {
+        const char* e = std::getenv("PPC_OZAKI");
+        v = (e && e[0] == '0') ? 0 : 1;
+        g_ozaki.store(v);
+    }
+    return v == 1;
+}
+
+}  // namespace
+
+bool ozaki_gram_partials(const double* T, int64_t ldT, int64_t rows, int64_t n3, int64_t chunk, int64_t nchunks,
+                         double* parts, cudaStream_t s) {
+    if (!ozaki_enabled()) return false;
+    // the integer path pays off once each output tile sees a long K range
+    if (n3 < 128 || n3 > 65535 || chunk < 4096 || rows < 4096 * 4) return false;
+    if (rows > chunk * nchunks) return false;
+    // sub-chunks of KC = min(chunk, kKC) rows tile every plan chunk exactly
+    // (a plan chunk longer than kKC must be a multiple of it), so a plan
+    // chunk's partial never depends on how the rows are sharded
+    if (chunk > kKC && chunk % kKC != 0) return false;
+    const int64_t KC = std::min<int64_t>(chunk, kKC);
+    const int64_t KCp = (KC + kBK - 1) / kBK * kBK;
+    const int64_t nsub = nchunks * (chunk / KC + (chunk % KC ? 1 : 0));
+    if (nsub * kS > 65535) return false;
+    StageTimer tm("gram_ozaki", s, (double)rows * n3 * n3, 8.0 * rows * n3);
+    DeviceBuffer D(sizeof(int8_t) * nsub * kS * n3 * KCp), sc(sizeof(double) * nsub * n3);
+    {
+        StageTimer ts("ozaki_split", s, 0.0, 8.0 * rows * n3 + (double)kS * rows * n3);
+        // sub-chunk c covers rows [c*KC, c*KC+KC) of T (plan chunks are KC-aligned)
+        dim3 grid((unsigned)n3, (unsigned)nsub);
+        ozaki_split_kernel<<<grid, 512, 0, s>>>(T, ldT, rows, n3, KC, KCp, D.as<int8_t>(), sc.d());
+        count_launch();
+        check_launch("ozaki_split");
+    }
+    CUtensorMap ma, mb;
+    if (!make_digit_map(&ma, D.as<int8_t>(), KCp, n3, nsub * kS, kBM) ||
+        !make_digit_map(&mb, D.as<int8_t>(), KCp, n3, nsub * kS, kBN))
+        fail(PPC_CUDA, "ozaki: tensor map encoding failed");
+    SyrkParams P;
+    P.n3 = n3;
+    P.nsub = nsub;
+    P.ntiles_n = (n3 + kBN - 1) / kBN;
+    P.tiles = 0;
+    for (int64_t nb = 0; nb < P.ntiles_n; ++nb) P.tiles += std::min<int64_t>((nb * kBN + kBN - 1) / kBM + 1, (n3 + kBM - 1) / kBM);
+    P.KCp = KCp;
+    P.scale = sc.d();
+    const int64_t per_chunk = nsub / nchunks;
+    DeviceBuffer subp;
+    double* out = parts;
+    if (per_chunk > 1) {
+        subp = DeviceBuffer(sizeof(double) * nsub * n3 * n3);
+        out = subp.d();
+    }
+    P.out = out;
+    const size_t smem = 1024 + (size_t)kStages * kS * (kBM + kBN) * kBK + (2 * kStages + 1) * 8 + 16;
+    static bool attr = false;
+    if (!attr) {
+        PPC_CUDA_CHECK(cudaFuncSetAttribute(ozaki_syrk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    {
+        StageTimer tk("ozaki_syrk", s, 2.0 * kS * (kS + 1) / 2 * (double)rows * n3 * n3 / 2,
+                      (double)kS * rows * n3);
+        const int64_t items = nsub * P.tiles;
+        ozaki_syrk_kernel<<<(unsigned)items, 192, smem, s>>>(ma, mb, P);
+        count_launch();
+        check_launch("ozaki_syrk");
+    }
+    if (per_chunk > 1) {
+        const int64_t elems = n3 * n3, total = nchunks * elems;
+        sub_sum_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, 148 * 16), 256, 0, s>>>(out, per_chunk, elems,
+                                                                                               total, parts);
+        count_launch();
+        check_launch("sub_sum");
+    }
+    return true;
+}
+
+}  // namespace ppc
+
+extern "C" int ppc_set_ozaki(int mode) {
+    if (mode < 0 || mode > 1) return PPC_ARGUMENT;
+    ppc::g_ozaki.store(mode);
+    return 0;
+}

@@ -15,6 +15,7 @@
 #include "internal.h"
 #include "jacobi.cuh"
 #include "kernels.cuh"
+#include "ozaki.h"
 #include "slice_svd.cuh"
 
 namespace ppc {
@@ -101,6 +102,9 @@ void tree_reduce(double* parts, int64_t nparts, int64_t elems, cudaStream_t s) {
 // n3, leading dimension ldT) into parts (nchunks x n3 x n3).
 void gram_chunks(const double* T, int64_t ldT, int64_t rows, int64_t n3, int64_t chunk,
                  int64_t nchunks, double* parts, cudaStream_t s) {
+    // INT8 tensor-core (Ozaki) path for large Grams; it reads T column by
+    // column, so no re-layout either
+    if (ozaki_gram_partials(T, ldT, rows, n3, chunk, nchunks, parts, s)) return;
     // Large tube matrices: each SYRK pipeline stage would touch one 2 MB page
     // per column (columns are ldT*8 bytes apart), thrashing the TLB. Re-lay T
     // into 2048-row blocks first (one extra HBM pass); same summation order.

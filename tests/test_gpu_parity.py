@@ -842,3 +842,70 @@ def test_matrix_svd_baseline_vs_oracle(engine, oracle):
             if gap >= 1e-6:
                 assert np.abs(got.u[:, j] - U[:, j]).max() <= 1e-8
                 assert np.abs(got.v[:, j] - V[:, j]).max() <= 1e-8
+
+
+# ------------------------------------------------ Ozaki INT8 Gram (tcgen05 kind::i8)
+def _gram_parts(L, T, rows, n3):
+    import ctypes as C
+    import torch
+    c, ch = C.c_int64(), C.c_int64()
+    assert L.ppc_gram_plan(rows, n3, C.byref(c), C.byref(ch)) == 0
+    parts = torch.empty(c.value * n3 * n3, dtype=torch.float64, device="cuda")
+    assert L.ppc_gram_partials(C.c_void_p(T.data_ptr()), rows, rows, n3, ch.value, c.value,
+                               C.c_void_p(parts.data_ptr()), 1) == 0, L.ppc_last_error()
+    torch.cuda.synchronize()
+    return parts.view(c.value, n3, n3).clone(), ch.value
+
+
+@pytest.mark.parametrize("rows,n3,kind", [(1 << 18, 512, "gauss"), (1 << 22, 512, "cp")])
+def test_ozaki_gram_vs_dmma(engine, rows, n3, kind):
+    """The INT8 Ozaki Gram (7 digits) against the FP64 DMMA SYRK: agreement to
+    ~1e-14 of max|G|, exact symmetry, bitwise determinism, and the plan-chunk
+    partials tile the same way on every call (row 8e sharding invariant)."""
+    import torch
+    from paper_2409_19402_b200 import _lib
+    L = _lib.lib()
+    if kind == "gauss":
+        T = synth.gaussian_device(rows, 1, n3, 5, 1).reshape(rows, n3)
+    else:
+        T = synth.cp_tensor_device(1 << 11, rows >> 11, n3, rank=50, noise=1e-3, seed=2).reshape(rows, n3)
+    try:
+        assert L.ppc_set_ozaki(1) == 0
+        L.ppc_timing_enable(1)
+        oz, chunk = _gram_parts(L, T, rows, n3)
+        import ctypes as C
+        buf = C.create_string_buffer(1 << 16)
+        L.ppc_timing_report(buf, len(buf), 1)
+        L.ppc_timing_enable(0)
+        assert "ozaki_syrk" in buf.value.decode(), "Ozaki path not taken"
+        oz2, _ = _gram_parts(L, T, rows, n3)
+        assert torch.equal(oz, oz2)
+        assert L.ppc_set_ozaki(0) == 0
+        dm, _ = _gram_parts(L, T, rows, n3)
+    finally:
+        L.ppc_set_ozaki(1)
+    G_oz, G_dm = oz.sum(0), dm.sum(0)
+    rel = ((G_oz - G_dm).abs().max() / G_dm.abs().max()).item()
+    assert rel <= 1e-13, rel
+    for c in range(oz.shape[0]):
+        assert torch.equal(oz[c], oz[c].T)
+    w_dm = torch.linalg.eigvalsh(G_dm).flip(0)[:16]
+    w_oz = torch.linalg.eigvalsh(G_oz).flip(0)[:16]
+    assert ((w_dm - w_oz).abs().max() / w_dm[0]).item() <= 1e-13
+
+
+def test_ozaki_data_q_vs_numpy(engine):
+    """data_dependent_transform through the Ozaki Gram (cfg5 distribution,
+    512x512 pixels, n3 = 512) against LAPACK on the host: eigenvalue parity
+    (SURVEY 8c rule 5) and captured energy."""
+    import torch
+    a = synth.cp_tensor_device(512, 512, 512, rank=50, noise=1e-3, seed=4)
+    t = engine.data_dependent_transform(a, 64)
+    T = a.permute(2, 1, 0).reshape(512, -1).T.cpu().numpy()  # tube matrix (N x n3)
+    G = T.T @ T
+    w = np.linalg.eigvalsh(G)[::-1]
+    q = t.q
+    lam = np.einsum("ij,ij->j", q, G @ q)
+    assert np.abs(lam - w[:64]).max() <= 1e-12 * w[0]
+    assert abs(lam.sum() - w[:64].sum()) <= 1e-12 * w[:64].sum()
+    assert np.linalg.norm(q.T @ q - np.eye(64)) <= 1e-12
