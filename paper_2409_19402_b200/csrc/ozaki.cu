@@ -12,8 +12,10 @@
 // where every Q_L is an exact int32 sum of int8 products (KC * 64^2 * S <
 // 2^31) computed by tcgen05.mma into its own TMEM accumulator. The FP64
 // epilogue adds the levels smallest first. With S = 7 the truncation is
-// ~2^{-49} |T_a| |T_b| per product and the per-row sum is exact, so the error
-// does not grow with the chunk length (FP64 SYRK: ~sqrt(K) eps).
+// ~2^{-50} sigma_a sigma_b per product (sigma ~ the column max, so heavy-
+// tailed columns lose relative precision on small entries: S = 6 measured
+// 4e-12 of max|G| on the cfg5 CP data, S = 7 8e-15), the integer sums are
+// exact, and the error does not grow with the chunk length.
 //
 // Kernels: ozaki_split_kernel (one CTA per (chunk, column): max, scale,
 // digits), ozaki_syrk_kernel (TMA SWIZZLE_64B operand tiles of all S digit
@@ -37,22 +39,34 @@ namespace {
 
 using namespace umma;
 
-constexpr int kS = 7;          // digits per value
+constexpr int kS = 7;          // digits per value (49 bits; 6 digits measured 4e-12 of max|G| on cfg5-like data)
 constexpr int kBM = 128;       // UMMA M
 constexpr int kBN = 64;        // UMMA N (S levels x 64 columns of TMEM)
 constexpr int kBK = 64;        // bytes (= int8 elements) of K per stage, SWIZZLE_64B
 constexpr int kStages = 2;
-constexpr int64_t kKC = 65536;  // rows per sub-chunk: 65536 * 64^2 * 7 < 2^31
+constexpr int64_t kKC = 65536;  // rows per sub-chunk: 65536 * 64^2 * S < 2^31
+// Tensor memory: S level accumulators (kBN columns each). Optionally (kATmem)
+// the stage's A digit tiles are copied to TMEM after them and the MMAs read
+// only B from shared memory; at S = 6 that measured no faster than reading
+// both operands from shared memory, and at S = 7 it does not fit.
+constexpr int kAcol = kS * kBN;
+#ifndef PPC_OZAKI_ATMEM
+#define PPC_OZAKI_ATMEM 0
+#endif
+constexpr bool kATmem = PPC_OZAKI_ATMEM;
+static_assert(kAcol + (kATmem ? kS * (kBK / 32) * 8 : 0) <= 512, "TMEM budget");
 
 // ------------------------------------------------------------------ split
-// One CTA per (sub-chunk c, column j). D layout: [(c*S + s)*n3 + j][KCp] int8.
-__global__ void __launch_bounds__(512) ozaki_split_kernel(const double* __restrict__ T, int64_t ldT, int64_t rows,
-                                                          int64_t n3, int64_t KC, int64_t KCp,
+// One CTA per (block c, column j): block c is rows [c*KC, c*KC+KC) of T
+// (row sub-chunks, strideT = 0) or the whole of matrix T + c*strideT
+// (batched). D layout: [(c*S + s)*n3 + j][KCp] int8.
+__global__ void __launch_bounds__(512) ozaki_split_kernel(const double* __restrict__ T, int64_t ldT, int64_t strideT,
+                                                          int64_t rows, int64_t n3, int64_t KC, int64_t KCp,
                                                           int8_t* __restrict__ D, double* __restrict__ scale) {
     const int64_t j = blockIdx.x, c = blockIdx.y;
-    const int64_t r0 = c * KC;
+    const int64_t r0 = strideT ? 0 : c * KC;
     const int64_t len = std::min<int64_t>(KC, rows - r0);
-    const double* col = T + j * ldT + r0;
+    const double* col = T + (strideT ? c * strideT : 0) + j * ldT + r0;
     double mx = 0.0;
     for (int64_t i = threadIdx.x; i < len; i += blockDim.x) mx = fmax(mx, fabs(col[i]));
     __shared__ double red[16];
@@ -165,6 +179,15 @@ __global__ void __launch_bounds__(192, 1)
             if (elect_one()) {
                 const uint8_t* sa = base + st * STAGE;
                 const uint8_t* sb = sa + kS * A_TILE;
+                // A digit tiles -> TMEM (in issue order with the MMAs below and
+                // after the previous stage's MMAs, which read the same columns)
+#pragma unroll
+                for (int s = 0; s < (kATmem ? kS : 0); ++s) {
+                    const uint64_t da = sdesc_k_sw64(sa + s * A_TILE);
+#pragma unroll
+                    for (int kk = 0; kk < kBK / 32; ++kk)
+                        tmem_cp_128x256b(tmem + (uint32_t)(kAcol + (s * (kBK / 32) + kk) * 8), da + (uint64_t)(kk * 2));
+                }
 #pragma unroll
                 for (int l = 0; l < kS; ++l) {  // level L = l + 2
                     const int L = l + 2;
@@ -172,12 +195,18 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
                     for (int s = s_lo; s <= s_hi; ++s) {
                         const int t = L - s;
-                        const uint64_t da = sdesc_k_sw64(sa + (s - 1) * A_TILE);
                         const uint64_t db = sdesc_k_sw64(sb + (t - 1) * B_TILE);
 #pragma unroll
-                        for (int kk = 0; kk < kBK / 32; ++kk)
-                            mma_i8(tmem + (uint32_t)(l * kBN), da + (uint64_t)(kk * 2), db + (uint64_t)(kk * 2), idesc,
-                                   (kb > 0 || s > s_lo || kk > 0) ? 1u : 0u);
+                        for (int kk = 0; kk < kBK / 32; ++kk) {
+                            const uint32_t acc = (kb > 0 || s > s_lo || kk > 0) ? 1u : 0u;
+                            if (kATmem)
+                                mma_i8_ts(tmem + (uint32_t)(l * kBN),
+                                          tmem + (uint32_t)(kAcol + ((s - 1) * (kBK / 32) + kk) * 8),
+                                          db + (uint64_t)(kk * 2), idesc, acc);
+                            else
+                                mma_i8(tmem + (uint32_t)(l * kBN), sdesc_k_sw64(sa + (s - 1) * A_TILE) + (uint64_t)(kk * 2),
+                                       db + (uint64_t)(kk * 2), idesc, acc);
+                        }
                     }
                 }
                 mma_commit(&empty[st]);
@@ -279,6 +308,52 @@ bool ozaki_enabled() {
 
 }  // namespace
 
+namespace {
+
+// Split + SYRK over nblk blocks of KC rows (see ozaki_split_kernel): out[c]
+// (n3 x n3, column-major) = T_c^T T_c for every block c.
+void ozaki_syrk_blocks(const double* T, int64_t ldT, int64_t strideT, int64_t rows, int64_t n3, int64_t KC,
+                       int64_t nblk, double* out, cudaStream_t s) {
+    const int64_t KCp = (KC + kBK - 1) / kBK * kBK;
+    DeviceBuffer D(sizeof(int8_t) * nblk * kS * n3 * KCp), sc(sizeof(double) * nblk * n3);
+    const double total_rows = strideT ? (double)rows * nblk : (double)rows;
+    {
+        StageTimer ts("ozaki_split", s, 0.0, 8.0 * total_rows * n3 + (double)kS * total_rows * n3);
+        dim3 grid((unsigned)n3, (unsigned)nblk);
+        ozaki_split_kernel<<<grid, 512, 0, s>>>(T, ldT, strideT, rows, n3, KC, KCp, D.as<int8_t>(), sc.d());
+        count_launch();
+        check_launch("ozaki_split");
+    }
+    CUtensorMap ma, mb;
+    if (!make_digit_map(&ma, D.as<int8_t>(), KCp, n3, nblk * kS, kBM) ||
+        !make_digit_map(&mb, D.as<int8_t>(), KCp, n3, nblk * kS, kBN))
+        fail(PPC_CUDA, "ozaki: tensor map encoding failed");
+    SyrkParams P;
+    P.n3 = n3;
+    P.nsub = nblk;
+    P.ntiles_n = (n3 + kBN - 1) / kBN;
+    P.tiles = 0;
+    for (int64_t nb = 0; nb < P.ntiles_n; ++nb)
+        P.tiles += std::min<int64_t>((nb * kBN + kBN - 1) / kBM + 1, (n3 + kBM - 1) / kBM);
+    P.KCp = KCp;
+    P.scale = sc.d();
+    P.out = out;
+    const size_t smem = 1024 + (size_t)kStages * kS * (kBM + kBN) * kBK + (2 * kStages + 1) * 8 + 16;
+    static bool attr = false;
+    if (!attr) {
+        PPC_CUDA_CHECK(cudaFuncSetAttribute(ozaki_syrk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    StageTimer tk("ozaki_syrk", s, 2.0 * kS * (kS + 1) / 2 * total_rows * n3 * n3 / 2, (double)kS * total_rows * n3);
+    const int64_t items = nblk * P.tiles;
+    if (items > 0x7fffffffLL) fail(PPC_ARGUMENT, "ozaki: too many tiles");
+    ozaki_syrk_kernel<<<(unsigned)items, 192, smem, s>>>(ma, mb, P);
+    count_launch();
+    check_launch("ozaki_syrk");
+}
+
+}  // namespace
+
 bool ozaki_gram_partials(const double* T, int64_t ldT, int64_t rows, int64_t n3, int64_t chunk, int64_t nchunks,
                          double* parts, cudaStream_t s) {
     if (!ozaki_enabled()) return false;
@@ -290,53 +365,17 @@ bool ozaki_gram_partials(const double* T, int64_t ldT, int64_t rows, int64_t n3,
     // chunk's partial never depends on how the rows are sharded
     if (chunk > kKC && chunk % kKC != 0) return false;
     const int64_t KC = std::min<int64_t>(chunk, kKC);
-    const int64_t KCp = (KC + kBK - 1) / kBK * kBK;
-    const int64_t nsub = nchunks * (chunk / KC + (chunk % KC ? 1 : 0));
+    const int64_t per_chunk = chunk / KC;
+    const int64_t nsub = nchunks * per_chunk;
     if (nsub * kS > 65535) return false;
     StageTimer tm("gram_ozaki", s, (double)rows * n3 * n3, 8.0 * rows * n3);
-    DeviceBuffer D(sizeof(int8_t) * nsub * kS * n3 * KCp), sc(sizeof(double) * nsub * n3);
-    {
-        StageTimer ts("ozaki_split", s, 0.0, 8.0 * rows * n3 + (double)kS * rows * n3);
-        // sub-chunk c covers rows [c*KC, c*KC+KC) of T (plan chunks are KC-aligned)
-        dim3 grid((unsigned)n3, (unsigned)nsub);
-        ozaki_split_kernel<<<grid, 512, 0, s>>>(T, ldT, rows, n3, KC, KCp, D.as<int8_t>(), sc.d());
-        count_launch();
-        check_launch("ozaki_split");
-    }
-    CUtensorMap ma, mb;
-    if (!make_digit_map(&ma, D.as<int8_t>(), KCp, n3, nsub * kS, kBM) ||
-        !make_digit_map(&mb, D.as<int8_t>(), KCp, n3, nsub * kS, kBN))
-        fail(PPC_CUDA, "ozaki: tensor map encoding failed");
-    SyrkParams P;
-    P.n3 = n3;
-    P.nsub = nsub;
-    P.ntiles_n = (n3 + kBN - 1) / kBN;
-    P.tiles = 0;
-    for (int64_t nb = 0; nb < P.ntiles_n; ++nb) P.tiles += std::min<int64_t>((nb * kBN + kBN - 1) / kBM + 1, (n3 + kBM - 1) / kBM);
-    P.KCp = KCp;
-    P.scale = sc.d();
-    const int64_t per_chunk = nsub / nchunks;
     DeviceBuffer subp;
     double* out = parts;
     if (per_chunk > 1) {
         subp = DeviceBuffer(sizeof(double) * nsub * n3 * n3);
         out = subp.d();
     }
-    P.out = out;
-    const size_t smem = 1024 + (size_t)kStages * kS * (kBM + kBN) * kBK + (2 * kStages + 1) * 8 + 16;
-    static bool attr = false;
-    if (!attr) {
-        PPC_CUDA_CHECK(cudaFuncSetAttribute(ozaki_syrk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
-    }
-    {
-        StageTimer tk("ozaki_syrk", s, 2.0 * kS * (kS + 1) / 2 * (double)rows * n3 * n3 / 2,
-                      (double)kS * rows * n3);
-        const int64_t items = nsub * P.tiles;
-        ozaki_syrk_kernel<<<(unsigned)items, 192, smem, s>>>(ma, mb, P);
-        count_launch();
-        check_launch("ozaki_syrk");
-    }
+    ozaki_syrk_blocks(T, ldT, 0, rows, n3, KC, nsub, out, s);
     if (per_chunk > 1) {
         const int64_t elems = n3 * n3, total = nchunks * elems;
         sub_sum_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, 148 * 16), 256, 0, s>>>(out, per_chunk, elems,
@@ -344,6 +383,15 @@ bool ozaki_gram_partials(const double* T, int64_t ldT, int64_t rows, int64_t n3,
         count_launch();
         check_launch("sub_sum");
     }
+    return true;
+}
+
+bool ozaki_syrk_batched(const double* A, int64_t lda, int64_t strideA, int64_t rows, int64_t n, int64_t batch,
+                        double* G, cudaStream_t s) {
+    if (!ozaki_enabled()) return false;
+    if (n < 128 || rows < 1024 || rows > kKC || batch < 1 || batch * kS > 65535) return false;
+    if (strideA < lda * n) return false;
+    ozaki_syrk_blocks(A, lda, strideA, rows, n, rows, batch, G, s);
     return true;
 }
 

@@ -13,4 +13,10 @@ namespace ppc {
 bool ozaki_gram_partials(const double* T, int64_t ldT, int64_t rows, int64_t n3, int64_t chunk, int64_t nchunks,
                          double* parts, cudaStream_t s);
 
+// G_b (n x n, column-major, b < batch, stride n*n) = A_b^T A_b for A_b
+// (rows x n, leading dimension lda) at A + b*strideA: the batched slice
+// Grams. rows <= 65536. Returns false when not eligible.
+bool ozaki_syrk_batched(const double* A, int64_t lda, int64_t strideA, int64_t rows, int64_t n, int64_t batch,
+                        double* G, cudaStream_t s);
+
 }  // namespace ppc

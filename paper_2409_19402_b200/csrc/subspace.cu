@@ -29,6 +29,7 @@
 #include "internal.h"
 #include "jacobi.cuh"
 #include "kernels.cuh"
+#include "ozaki.h"
 #include "slice_svd.cuh"
 
 namespace ppc {
@@ -624,16 +625,20 @@ void subspace_svd(const double* A, int64_t m, int64_t n, int64_t stride, int64_t
     DeviceBuffer G(sizeof(double) * r * r * batch);
     {
         StageTimer tg("ss.gram", s, (double)batch * r * r * (tall ? m : n), 8.0 * batch * m * n);
-        GemmDesc d;
-        d.M = r; d.N = r; d.batch = batch; d.symmetric = true;
-        d.C = G.d(); d.ldc = r; d.strideC = r * r;
-        d.A = A; d.B = A; d.strideA = stride; d.strideB = stride;
-        if (tall) {  // G = A^T A: A(mm,kk) = A[kk + mm*m], B(kk,nn) = A[kk + nn*m]
-            d.K = m; d.lda = m; d.a_kmajor = true; d.ldb = m; d.b_nmajor = false;
-        } else {     // G = A A^T: A(mm,kk) = A[mm + kk*m], B(kk,nn) = A[nn + kk*m]
-            d.K = n; d.lda = m; d.a_kmajor = false; d.ldb = m; d.b_nmajor = true;
+        // tall slices: G_b = A_b^T A_b is the Gram of an m-row tube matrix
+        // (INT8 tensor-core Ozaki SYRK where eligible)
+        if (!(tall && ozaki_syrk_batched(A, m, stride, m, n, batch, G.d(), s))) {
+            GemmDesc d;
+            d.M = r; d.N = r; d.batch = batch; d.symmetric = true;
+            d.C = G.d(); d.ldc = r; d.strideC = r * r;
+            d.A = A; d.B = A; d.strideA = stride; d.strideB = stride;
+            if (tall) {  // G = A^T A: A(mm,kk) = A[kk + mm*m], B(kk,nn) = A[kk + nn*m]
+                d.K = m; d.lda = m; d.a_kmajor = true; d.ldb = m; d.b_nmajor = false;
+            } else {     // G = A A^T: A(mm,kk) = A[mm + kk*m], B(kk,nn) = A[nn + kk*m]
+                d.K = n; d.lda = m; d.a_kmajor = false; d.ldb = m; d.b_nmajor = true;
+            }
+            gemm(d, s);
         }
-        gemm(d, s);
     }
     DeviceBuffer Xk(sizeof(double) * r * k * batch), lam(sizeof(double) * k * batch);
     subspace_eig_top(G.d(), r, batch, k, Xk.d(), lam.d(), s, true);
