@@ -100,13 +100,18 @@ __global__ void __launch_bounds__(512) ozaki_split_kernel(const double* __restri
 }
 
 // ------------------------------------------------------------------- syrk
-struct SyrkParams {
-    int64_t n3, nsub;
-    int64_t ntiles_n;      // column tiles (kBN wide)
-    int64_t tiles;         // upper-triangle tiles per sub-chunk
-    int64_t KCp;           // padded sub-chunk length (multiple of kBK)
-    const double* scale;   // [nsub][n3]
-    double* out;           // [nsub][n3][n3] column-major partials
+// One launch covers `items` = nbatch * tiles work items: item -> batch bi,
+// tile t; bi -> operand/output block blk (zmap, else bi). SYM: the tiles are
+// the upper triangle of an M x M Gram, written together with their mirror.
+struct OzParams {
+    int64_t M, N;          // output extents per block
+    int64_t mtiles, tiles; // row tiles; tiles per block
+    int64_t KCp;           // padded K length (multiple of kBK)
+    const int* zmap;       // nullable batch -> block map
+    const double* sa;      // row scales [blk][M]
+    const double* sb;      // column scales [blk][N]
+    double* C;             // output block blk at C + blk*strideC, (m, n) at m + n*ldc
+    int64_t ldc, strideC;
 };
 
 // tile t (upper-triangle order) -> (mb, nb): column tile nb holds
@@ -122,9 +127,10 @@ __device__ __forceinline__ void tri_tile(int64_t t, int64_t& mb, int64_t& nb) {
     mb = t;
 }
 
+template <bool SYM>
 __global__ void __launch_bounds__(192, 1)
-    ozaki_syrk_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
-                      const SyrkParams P) {
+    ozaki_mma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                     const OzParams P) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     constexpr int A_TILE = kBM * kBK, B_TILE = kBN * kBK;
@@ -135,9 +141,16 @@ __global__ void __launch_bounds__(192, 1)
     uint32_t* tslot = reinterpret_cast<uint32_t*>(tfull + 1);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t item = blockIdx.x;
-    const int64_t sub = item / P.tiles;
+    const int64_t bi = item / P.tiles;
+    const int64_t sub = P.zmap ? P.zmap[bi] : bi;
     int64_t mb, nb;
-    tri_tile(item - sub * P.tiles, mb, nb);
+    if (SYM) {
+        tri_tile(item - bi * P.tiles, mb, nb);
+    } else {
+        const int64_t t = item - bi * P.tiles;
+        mb = t % P.mtiles;
+        nb = t / P.mtiles;
+    }
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
@@ -236,17 +249,17 @@ __global__ void __launch_bounds__(192, 1)
                 for (int j = 0; j < 32; ++j) acc[h + j] = fma((double)v[j], w, acc[h + j]);
             }
         }
-        if (m < P.n3) {
-            const double* sc = P.scale + sub * P.n3;
-            const double sm = sc[m];
-            double* C = P.out + sub * P.n3 * P.n3;
+        if (m < P.M) {
+            const double sm = P.sa[sub * P.M + m];
+            const double* sc = P.sb + sub * P.N;
+            double* C = P.C + sub * P.strideC;
 #pragma unroll 4
             for (int j = 0; j < kBN; ++j) {
                 const int64_t n = nb * kBN + j;
-                if (n >= P.n3) break;
+                if (n >= P.N) break;
                 const double v = acc[j] * sm * sc[n];
-                C[m + n * P.n3] = v;  // (m, n), coalesced over the warp's rows
-                C[n + m * P.n3] = v;  // mirror (n, m): the same exact integer sums
+                C[m + n * P.ldc] = v;                // (m, n), coalesced over the warp's rows
+                if (SYM) C[n + m * P.ldc] = v;       // mirror (n, m): the same exact integer sums
             }
         }
     }
@@ -308,51 +321,94 @@ bool ozaki_enabled() {
 
 }  // namespace
 
+void OzakiDigits::split(const double* X, int64_t ldx, int64_t stride, int64_t rows_, int64_t cols_, int64_t KC,
+                        int64_t nblk_, cudaStream_t s) {
+    rows = rows_;
+    cols = cols_;
+    nblk = nblk_;
+    KCp = (KC + kBK - 1) / kBK * kBK;
+    const size_t dbytes = sizeof(int8_t) * nblk * kS * cols * KCp, sbytes = sizeof(double) * nblk * cols;
+    if (D.bytes() < dbytes) D = DeviceBuffer(dbytes);
+    if (sc.bytes() < sbytes) sc = DeviceBuffer(sbytes);
+    const double total_rows = stride ? (double)rows * nblk : (double)rows;
+    StageTimer ts("ozaki_split", s, 0.0, 8.0 * total_rows * cols + (double)kS * total_rows * cols);
+    dim3 grid((unsigned)cols, (unsigned)nblk);
+    ozaki_split_kernel<<<grid, 512, 0, s>>>(X, ldx, stride, rows, cols, KC, KCp, D.as<int8_t>(), sc.d());
+    count_launch();
+    check_launch("ozaki_split");
+}
+
 namespace {
+
+template <bool SYM>
+void launch_mma(const CUtensorMap& ma, const CUtensorMap& mb, const OzParams& P, int64_t items, cudaStream_t s) {
+    const size_t smem = 1024 + (size_t)kStages * kS * (kBM + kBN) * kBK + (2 * kStages + 1) * 8 + 16;
+    static bool attr = false;
+    if (!attr) {
+        PPC_CUDA_CHECK(cudaFuncSetAttribute(ozaki_mma_kernel<SYM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    if (items > 0x7fffffffLL) fail(PPC_ARGUMENT, "ozaki: too many tiles");
+    if (items == 0) return;
+    ozaki_mma_kernel<SYM><<<(unsigned)items, 192, smem, s>>>(ma, mb, P);
+    count_launch();
+    check_launch("ozaki_mma");
+}
 
 // Split + SYRK over nblk blocks of KC rows (see ozaki_split_kernel): out[c]
 // (n3 x n3, column-major) = T_c^T T_c for every block c.
 void ozaki_syrk_blocks(const double* T, int64_t ldT, int64_t strideT, int64_t rows, int64_t n3, int64_t KC,
-                       int64_t nblk, double* out, cudaStream_t s) {
-    const int64_t KCp = (KC + kBK - 1) / kBK * kBK;
-    DeviceBuffer D(sizeof(int8_t) * nblk * kS * n3 * KCp), sc(sizeof(double) * nblk * n3);
-    const double total_rows = strideT ? (double)rows * nblk : (double)rows;
-    {
-        StageTimer ts("ozaki_split", s, 0.0, 8.0 * total_rows * n3 + (double)kS * total_rows * n3);
-        dim3 grid((unsigned)n3, (unsigned)nblk);
-        ozaki_split_kernel<<<grid, 512, 0, s>>>(T, ldT, strideT, rows, n3, KC, KCp, D.as<int8_t>(), sc.d());
-        count_launch();
-        check_launch("ozaki_split");
-    }
+                       int64_t nblk, double* out, cudaStream_t s, const char* stage) {
+    OzakiDigits d;
+    d.split(T, ldT, strideT, rows, n3, KC, nblk, s);
     CUtensorMap ma, mb;
-    if (!make_digit_map(&ma, D.as<int8_t>(), KCp, n3, nblk * kS, kBM) ||
-        !make_digit_map(&mb, D.as<int8_t>(), KCp, n3, nblk * kS, kBN))
+    if (!make_digit_map(&ma, d.D.as<int8_t>(), d.KCp, n3, nblk * kS, kBM) ||
+        !make_digit_map(&mb, d.D.as<int8_t>(), d.KCp, n3, nblk * kS, kBN))
         fail(PPC_CUDA, "ozaki: tensor map encoding failed");
-    SyrkParams P;
-    P.n3 = n3;
-    P.nsub = nblk;
-    P.ntiles_n = (n3 + kBN - 1) / kBN;
+    OzParams P;
+    P.M = P.N = n3;
+    P.mtiles = (n3 + kBM - 1) / kBM;
     P.tiles = 0;
-    for (int64_t nb = 0; nb < P.ntiles_n; ++nb)
-        P.tiles += std::min<int64_t>((nb * kBN + kBN - 1) / kBM + 1, (n3 + kBM - 1) / kBM);
-    P.KCp = KCp;
-    P.scale = sc.d();
-    P.out = out;
-    const size_t smem = 1024 + (size_t)kStages * kS * (kBM + kBN) * kBK + (2 * kStages + 1) * 8 + 16;
-    static bool attr = false;
-    if (!attr) {
-        PPC_CUDA_CHECK(cudaFuncSetAttribute(ozaki_syrk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
-    }
-    StageTimer tk("ozaki_syrk", s, 2.0 * kS * (kS + 1) / 2 * total_rows * n3 * n3 / 2, (double)kS * total_rows * n3);
-    const int64_t items = nblk * P.tiles;
-    if (items > 0x7fffffffLL) fail(PPC_ARGUMENT, "ozaki: too many tiles");
-    ozaki_syrk_kernel<<<(unsigned)items, 192, smem, s>>>(ma, mb, P);
-    count_launch();
-    check_launch("ozaki_syrk");
+    for (int64_t nb = 0; nb < (n3 + kBN - 1) / kBN; ++nb)
+        P.tiles += std::min<int64_t>((nb * kBN + kBN - 1) / kBM + 1, P.mtiles);
+    P.KCp = d.KCp;
+    P.zmap = nullptr;
+    P.sa = P.sb = d.sc.d();
+    P.C = out;
+    P.ldc = n3;
+    P.strideC = n3 * n3;
+    const double total_rows = strideT ? (double)rows * nblk : (double)rows;
+    StageTimer tk(stage, s, 2.0 * kS * (kS + 1) / 2 * total_rows * n3 * n3 / 2, (double)kS * total_rows * n3);
+    launch_mma<true>(ma, mb, P, nblk * P.tiles, s);
 }
 
 }  // namespace
+
+void ozaki_gemm(const OzakiDigits& A, const OzakiDigits& B, int64_t nbatch, const int* zmap, double* C, int64_t ldc,
+                int64_t strideC, cudaStream_t s) {
+    if (A.KCp != B.KCp || A.rows != B.rows) fail(PPC_ARGUMENT, "ozaki_gemm: K mismatch");
+    CUtensorMap ma, mb;
+    if (!make_digit_map(&ma, A.D.as<int8_t>(), A.KCp, A.cols, A.nblk * kS, kBM) ||
+        !make_digit_map(&mb, B.D.as<int8_t>(), B.KCp, B.cols, B.nblk * kS, kBN))
+        fail(PPC_CUDA, "ozaki: tensor map encoding failed");
+    OzParams P;
+    P.M = A.cols;
+    P.N = B.cols;
+    P.mtiles = (P.M + kBM - 1) / kBM;
+    P.tiles = P.mtiles * ((P.N + kBN - 1) / kBN);
+    P.KCp = A.KCp;
+    P.zmap = zmap;
+    P.sa = A.sc.d();
+    P.sb = B.sc.d();
+    P.C = C;
+    P.ldc = ldc;
+    P.strideC = strideC;
+    StageTimer tk("ozaki_gemm", s, 2.0 * kS * (kS + 1) / 2 * (double)nbatch * P.M * P.N * A.rows,
+                  (double)kS * nbatch * (P.M + P.N) * A.rows);
+    launch_mma<false>(ma, mb, P, nbatch * P.tiles, s);
+}
+
+bool ozaki_gemm_eligible(int64_t M, int64_t K) { return ozaki_enabled() && M >= kBM && K >= 256 && K <= kKC; }
 
 bool ozaki_gram_partials(const double* T, int64_t ldT, int64_t rows, int64_t n3, int64_t chunk, int64_t nchunks,
                          double* parts, cudaStream_t s) {
@@ -375,7 +431,7 @@ bool ozaki_gram_partials(const double* T, int64_t ldT, int64_t rows, int64_t n3,
         subp = DeviceBuffer(sizeof(double) * nsub * n3 * n3);
         out = subp.d();
     }
-    ozaki_syrk_blocks(T, ldT, 0, rows, n3, KC, nsub, out, s);
+    ozaki_syrk_blocks(T, ldT, 0, rows, n3, KC, nsub, out, s, "ozaki_syrk");
     if (per_chunk > 1) {
         const int64_t elems = n3 * n3, total = nchunks * elems;
         sub_sum_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, 148 * 16), 256, 0, s>>>(out, per_chunk, elems,
@@ -391,7 +447,7 @@ bool ozaki_syrk_batched(const double* A, int64_t lda, int64_t strideA, int64_t r
     if (!ozaki_enabled()) return false;
     if (n < 128 || rows < 1024 || rows > kKC || batch < 1 || batch * kS > 65535) return false;
     if (strideA < lda * n) return false;
-    ozaki_syrk_blocks(A, lda, strideA, rows, n, rows, batch, G, s);
+    ozaki_syrk_blocks(A, lda, strideA, rows, n, rows, batch, G, s, "ozaki_syrk_batched");
     return true;
 }
 

@@ -3,7 +3,28 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 
+#include "internal.h"
+
 namespace ppc {
+
+// Ozaki digits of nblk FP64 blocks: block c is X + c*stride (rows x cols,
+// leading dimension ldx; stride 0: the row sub-chunk [c*KC, c*KC+KC) of one
+// matrix). Every column is scaled by a power of two and cut into 7 signed
+// 7-bit digits along the rows (the K dimension of the products below).
+struct OzakiDigits {
+    DeviceBuffer D, sc;  // int8 planes [blk][digit][col][KCp]; scales [blk][col]
+    int64_t rows = 0, cols = 0, KCp = 0, nblk = 0;
+    void split(const double* X, int64_t ldx, int64_t stride, int64_t rows, int64_t cols, int64_t KC, int64_t nblk,
+               cudaStream_t s);
+};
+
+// C_b (A.cols x B.cols, (m, n) at m + n*ldc, b at blk*strideC) = A_blk^T B_blk
+// for the nbatch blocks blk = zmap[b] (or b): the FP64 product of the two
+// split operands on the INT8 tensor cores (exact int32 digit-level sums).
+void ozaki_gemm(const OzakiDigits& A, const OzakiDigits& B, int64_t nbatch, const int* zmap, double* C, int64_t ldc,
+                int64_t strideC, cudaStream_t s);
+// Whether the integer path applies to an output with M rows and K-length sums.
+bool ozaki_gemm_eligible(int64_t M, int64_t K);
 
 // Per-plan-chunk partial Grams parts[c] = T_c^T T_c (nchunks x n3 x n3) of a
 // tube matrix T (rows x n3, leading dimension ldT), as gram_partials, through

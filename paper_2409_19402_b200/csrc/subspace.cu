@@ -383,6 +383,13 @@ void subspace_eig_top(const double* G, int64_t r, int64_t batch, int64_t k, doub
     Work w(r, b, batch);
     w.basis = !vectors_for_reconstruction;
     const int64_t per = r * b;
+    // Chebyshev filter products G Y on the INT8 tensor cores (Ozaki, 7
+    // digits): G is split once, the block Y at every degree. Rayleigh-Ritz
+    // and the residuals keep the FP64 DMMA products, so locking and the
+    // final accuracy do not depend on the emulated filter.
+    const bool oz_filter = vectors_for_reconstruction && batch >= 8 && ozaki_gemm_eligible(r, r);
+    OzakiDigits Gd, Yd;
+    if (oz_filter) Gd.split(G, r, r * r, r, r, r, batch, s);
     PPC_CUDA_CHECK(cudaMemsetAsync(w.fail.d(), 0, 2 * sizeof(int), s));
     randn_kernel<<<grid1(per * batch), 256, 0, s>>>(w.Y.d(), per * batch, 0x5eed5eedULL + (uint64_t)r * 131 + b);
     count_launch();
@@ -569,8 +576,13 @@ void subspace_eig_top(const double* G, int64_t r, int64_t batch, int64_t k, doub
                 const int* zm = w.zmap.as<int>() + (int64_t)j * batch;
                 if (na > 0) {
                     // Z = G Y, P = X^T Y, Z -= X diag(theta_L) P   (columns [cf, b))
-                    gg(G, r, r * r, false, Y + cf * r, r, per, w.Z.d() + cf * r, r, per, r, bf, r, na, 1.0, 0.0, s,
-                       zm, batch);
+                    if (oz_filter) {
+                        Yd.split(Y + cf * r, r, per, r, bf, r, batch, s);
+                        ozaki_gemm(Gd, Yd, na, zm, w.Z.d() + cf * r, r, per, s);
+                    } else {
+                        gg(G, r, r * r, false, Y + cf * r, r, per, w.Z.d() + cf * r, r, per, r, bf, r, na, 1.0, 0.0,
+                           s, zm, batch);
+                    }
                     gg(w.X.d(), r, per, true, Y + cf * r, r, per, w.P.d(), b, b * bf, b, bf, r, na, 1.0, 0.0, s,
                        zm, batch);
                     scale_rows_kernel<<<grid1(b * bf * batch), 256, 0, s>>>(w.P.d(), w.wmask.d(), b, bf,
