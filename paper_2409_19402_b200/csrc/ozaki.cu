@@ -59,17 +59,28 @@ static_assert(kAcol + (kATmem ? kS * (kBK / 32) * 8 : 0) <= 512, "TMEM budget");
 // ------------------------------------------------------------------ split
 // One CTA per (block c, column j): block c is rows [c*KC, c*KC+KC) of T
 // (row sub-chunks, strideT = 0) or the whole of matrix T + c*strideT
-// (batched). D layout: [(c*S + s)*n3 + j][KCp] int8.
-__global__ void __launch_bounds__(512) ozaki_split_kernel(const double* __restrict__ T, int64_t ldT, int64_t strideT,
+// (batched). D layout: [(c*S + s)*n3 + j][KCp] int8. Blocks of up to
+// kStageRows rows are read from HBM once (staged in shared memory for the
+// digit pass); each thread emits four consecutive rows per digit as one
+// 32-bit store.
+constexpr int64_t kStageRows = 4096;  // 32 KB of shared memory (several CTAs per SM)
+
+template <bool STAGE>
+__global__ void __launch_bounds__(256) ozaki_split_kernel(const double* __restrict__ T, int64_t ldT, int64_t strideT,
                                                           int64_t rows, int64_t n3, int64_t KC, int64_t KCp,
                                                           int8_t* __restrict__ D, double* __restrict__ scale) {
+    extern __shared__ double stage[];
     const int64_t j = blockIdx.x, c = blockIdx.y;
     const int64_t r0 = strideT ? 0 : c * KC;
-    const int64_t len = std::min<int64_t>(KC, rows - r0);
+    const int64_t len = std::max<int64_t>(0, std::min<int64_t>(KC, rows - r0));
     const double* col = T + (strideT ? c * strideT : 0) + j * ldT + r0;
     double mx = 0.0;
-    for (int64_t i = threadIdx.x; i < len; i += blockDim.x) mx = fmax(mx, fabs(col[i]));
-    __shared__ double red[16];
+    for (int64_t i = threadIdx.x; i < len; i += blockDim.x) {
+        const double v = col[i];
+        if (STAGE) stage[i] = v;
+        mx = fmax(mx, fabs(v));
+    }
+    __shared__ double red[8];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
@@ -87,15 +98,24 @@ __global__ void __launch_bounds__(512) ozaki_split_kernel(const double* __restri
     if (threadIdx.x == 0) scale[c * n3 + j] = mx > 0.0 ? ldexp(1.0, e) : 0.0;
     int8_t* out = D + ((c * kS) * n3 + j) * KCp;
     const int64_t plane = n3 * KCp;
-    for (int64_t i = threadIdx.x; i < KCp; i += blockDim.x) {
-        double x = i < len ? ldexp(col[i], -e) : 0.0;
+    for (int64_t i4 = (int64_t)threadIdx.x * 4; i4 < KCp; i4 += (int64_t)blockDim.x * 4) {
+        uint32_t w[kS];
 #pragma unroll
-        for (int s = 0; s < kS; ++s) {
-            const double t = x * 128.0;
-            const double d = rint(t);
-            x = t - d;
-            out[s * plane + i] = (int8_t)d;
+        for (int s = 0; s < kS; ++s) w[s] = 0u;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int64_t i = i4 + q;
+            double x = i < len ? ldexp(STAGE ? stage[i] : col[i], -e) : 0.0;
+#pragma unroll
+            for (int s = 0; s < kS; ++s) {
+                const double t = x * 128.0;
+                const double d = rint(t);
+                x = t - d;
+                w[s] |= (uint32_t)(uint8_t)(int8_t)d << (8 * q);
+            }
         }
+#pragma unroll
+        for (int s = 0; s < kS; ++s) *reinterpret_cast<uint32_t*>(out + s * plane + i4) = w[s];
     }
 }
 
@@ -333,7 +353,18 @@ void OzakiDigits::split(const double* X, int64_t ldx, int64_t stride, int64_t ro
     const double total_rows = stride ? (double)rows * nblk : (double)rows;
     StageTimer ts("ozaki_split", s, 0.0, 8.0 * total_rows * cols + (double)kS * total_rows * cols);
     dim3 grid((unsigned)cols, (unsigned)nblk);
-    ozaki_split_kernel<<<grid, 512, 0, s>>>(X, ldx, stride, rows, cols, KC, KCp, D.as<int8_t>(), sc.d());
+    if (KC <= kStageRows) {
+        const size_t sm = sizeof(double) * KC;
+        static bool attr = false;
+        if (!attr) {
+            PPC_CUDA_CHECK(cudaFuncSetAttribute(ozaki_split_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                (int)(sizeof(double) * kStageRows)));
+            attr = true;
+        }
+        ozaki_split_kernel<true><<<grid, 256, sm, s>>>(X, ldx, stride, rows, cols, KC, KCp, D.as<int8_t>(), sc.d());
+    } else {
+        ozaki_split_kernel<false><<<grid, 256, 0, s>>>(X, ldx, stride, rows, cols, KC, KCp, D.as<int8_t>(), sc.d());
+    }
     count_launch();
     check_launch("ozaki_split");
 }
@@ -416,9 +447,12 @@ bool ozaki_gram_partials(const double* T, int64_t ldT, int64_t rows, int64_t n3,
     // the integer path pays off once each output tile sees a long K range
     if (n3 < 128 || n3 > 65535 || chunk < 4096 || rows < 4096 * 4) return false;
     if (rows > chunk * nchunks) return false;
-    // sub-chunks of KC = min(chunk, kKC) rows tile every plan chunk exactly
-    // (a plan chunk longer than kKC must be a multiple of it), so a plan
-    // chunk's partial never depends on how the rows are sharded
+    // sub-chunks of KC rows tile every plan chunk exactly (a longer plan
+    // chunk must be a multiple of KC), so a plan chunk's partial never
+    // depends on how the rows are sharded
+    // (KC = kKC: longer sub-chunks keep the split's second read of each
+    // column chunk L2-resident and the sub-chunk partials few; staging 16K-row
+    // chunks in shared memory measured slower at one CTA per SM)
     if (chunk > kKC && chunk % kKC != 0) return false;
     const int64_t KC = std::min<int64_t>(chunk, kKC);
     const int64_t per_chunk = chunk / KC;
