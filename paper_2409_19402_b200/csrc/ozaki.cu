@@ -68,9 +68,10 @@ constexpr int64_t kStageRows = 4096;  // 32 KB of shared memory (several CTAs pe
 template <bool STAGE>
 __global__ void __launch_bounds__(256) ozaki_split_kernel(const double* __restrict__ T, int64_t ldT, int64_t strideT,
                                                           int64_t rows, int64_t n3, int64_t KC, int64_t KCp,
-                                                          int8_t* __restrict__ D, double* __restrict__ scale) {
+                                                          int8_t* __restrict__ D, double* __restrict__ scale,
+                                                          const int* __restrict__ zmap) {
     extern __shared__ double stage[];
-    const int64_t j = blockIdx.x, c = blockIdx.y;
+    const int64_t j = blockIdx.x, c = zmap ? zmap[blockIdx.y] : blockIdx.y;
     const int64_t r0 = strideT ? 0 : c * KC;
     const int64_t len = std::max<int64_t>(0, std::min<int64_t>(KC, rows - r0));
     const double* col = T + (strideT ? c * strideT : 0) + j * ldT + r0;
@@ -342,7 +343,7 @@ bool ozaki_enabled() {
 }  // namespace
 
 void OzakiDigits::split(const double* X, int64_t ldx, int64_t stride, int64_t rows_, int64_t cols_, int64_t KC,
-                        int64_t nblk_, cudaStream_t s) {
+                        int64_t nblk_, cudaStream_t s, const int* zmap, int64_t nz) {
     rows = rows_;
     cols = cols_;
     nblk = nblk_;
@@ -350,9 +351,12 @@ void OzakiDigits::split(const double* X, int64_t ldx, int64_t stride, int64_t ro
     const size_t dbytes = sizeof(int8_t) * nblk * kS * cols * KCp, sbytes = sizeof(double) * nblk * cols;
     if (D.bytes() < dbytes) D = DeviceBuffer(dbytes);
     if (sc.bytes() < sbytes) sc = DeviceBuffer(sbytes);
-    const double total_rows = stride ? (double)rows * nblk : (double)rows;
+    if (zmap && !stride) fail(PPC_ARGUMENT, "ozaki split: a block map needs batched blocks");
+    const int64_t launched = zmap ? nz : nblk;
+    if (launched <= 0) return;
+    const double total_rows = stride ? (double)rows * launched : (double)rows;
     StageTimer ts("ozaki_split", s, 0.0, 8.0 * total_rows * cols + (double)kS * total_rows * cols);
-    dim3 grid((unsigned)cols, (unsigned)nblk);
+    dim3 grid((unsigned)cols, (unsigned)launched);
     if (KC <= kStageRows) {
         const size_t sm = sizeof(double) * KC;
         static bool attr = false;
@@ -361,9 +365,11 @@ void OzakiDigits::split(const double* X, int64_t ldx, int64_t stride, int64_t ro
                                                 (int)(sizeof(double) * kStageRows)));
             attr = true;
         }
-        ozaki_split_kernel<true><<<grid, 256, sm, s>>>(X, ldx, stride, rows, cols, KC, KCp, D.as<int8_t>(), sc.d());
+        ozaki_split_kernel<true><<<grid, 256, sm, s>>>(X, ldx, stride, rows, cols, KC, KCp, D.as<int8_t>(), sc.d(),
+                                                       zmap);
     } else {
-        ozaki_split_kernel<false><<<grid, 256, 0, s>>>(X, ldx, stride, rows, cols, KC, KCp, D.as<int8_t>(), sc.d());
+        ozaki_split_kernel<false><<<grid, 256, 0, s>>>(X, ldx, stride, rows, cols, KC, KCp, D.as<int8_t>(), sc.d(),
+                                                        zmap);
     }
     count_launch();
     check_launch("ozaki_split");

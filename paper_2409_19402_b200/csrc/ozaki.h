@@ -14,8 +14,9 @@ namespace ppc {
 struct OzakiDigits {
     DeviceBuffer D, sc;  // int8 planes [blk][digit][col][KCp]; scales [blk][col]
     int64_t rows = 0, cols = 0, KCp = 0, nblk = 0;
+    // zmap (device, nz entries; batched blocks only): split just those blocks
     void split(const double* X, int64_t ldx, int64_t stride, int64_t rows, int64_t cols, int64_t KC, int64_t nblk,
-               cudaStream_t s);
+               cudaStream_t s, const int* zmap = nullptr, int64_t nz = 0);
 };
 
 // C_b (A.cols x B.cols, (m, n) at m + n*ldc, b at blk*strideC) = A_blk^T B_blk

@@ -577,7 +577,7 @@ void subspace_eig_top(const double* G, int64_t r, int64_t batch, int64_t k, doub
                 if (na > 0) {
                     // Z = G Y, P = X^T Y, Z -= X diag(theta_L) P   (columns [cf, b))
                     if (oz_filter) {
-                        Yd.split(Y + cf * r, r, per, r, bf, r, batch, s);
+                        Yd.split(Y + cf * r, r, per, r, bf, r, batch, s, zm, na);
                         ozaki_gemm(Gd, Yd, na, zm, w.Z.d() + cf * r, r, per, s);
                     } else {
                         gg(G, r, r * r, false, Y + cf * r, r, per, w.Z.d() + cf * r, r, per, r, bf, r, na, 1.0, 0.0,
