@@ -127,11 +127,16 @@ int ppc_star_q_product(const double* A, int64_t n1, int64_t m, int64_t n3, const
         check_tensor(m, n2, n3);
         check_transform(n3, p);
         cudaStream_t s = stream();
+        if (loc == PPC_HOST) {  // PCIe both ways at once behind the compute
+            if (!A || !B || !Q || !C) fail(PPC_ARGUMENT, "null pointer");
+            star_q_host(A, n1, m, n3, B, n2, Q, p, scale, C, s);
+            PPC_CUDA_CHECK(cudaStreamSynchronize(s));
+            return;
+        }
         In a(A, n1 * m * n3, loc), b(B, m * n2 * n3, loc), q(Q, n3 * p, loc);
         Out c(C, n1 * n2 * n3, loc);
         star_q(a.d, n1, m, n3, b.d, n2, q.d, p, scale, c.d, s);
         c.finish();
-        if (loc == PPC_HOST) PPC_CUDA_CHECK(cudaStreamSynchronize(s));
     });
 }
 

@@ -52,6 +52,85 @@ void star_q(const double* A, int64_t n1, int64_t m, int64_t n3, const double* B,
     mode3(ch.d(), n1 * n2, p, Q, n3, false, C, scale, s);  // x3 Q, scale in the epilogue
 }
 
+namespace {
+
+struct Event {
+    cudaEvent_t e = nullptr;
+    Event() { PPC_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming)); }
+    ~Event() { cudaEventDestroy(e); }
+    void record(cudaStream_t s) { PPC_CUDA_CHECK(cudaEventRecord(e, s)); }
+    void wait_on(cudaStream_t s) { PPC_CUDA_CHECK(cudaStreamWaitEvent(s, e, 0)); }
+};
+
+}  // namespace
+
+void star_q_host(const double* hA, int64_t n1, int64_t m, int64_t n3, const double* hB, int64_t n2,
+                 const double* hQ, int64_t p, double scale, double* hC, cudaStream_t s) {
+    cudaStream_t up = copy_stream(), down = copy_out_stream();
+    const int64_t NB = m * n2;
+    DeviceBuffer q(sizeof(double) * n3 * p), b(sizeof(double) * NB * n3), bh(sizeof(double) * NB * p);
+    Event ready;
+    ready.record(s);  // buffers allocated on s
+    ready.wait_on(up);
+    PPC_CUDA_CHECK(cudaMemcpyAsync(q.d(), hQ, sizeof(double) * n3 * p, cudaMemcpyHostToDevice, up));
+    // 1. B in pixel chunks: H2D (up) -> forward transform of those rows (s)
+    {
+        StageTimer tm("mode3_fwd", s, 2.0 * NB * n3 * p, 8.0 * (NB * n3 + NB * p + n3 * p));
+        const int64_t nch = 4, rows = (NB + nch - 1) / nch;
+        for (int64_t r0 = 0; r0 < NB; r0 += rows) {
+            const int64_t nr = std::min(rows, NB - r0);
+            PPC_CUDA_CHECK(cudaMemcpy2DAsync(b.d() + r0, sizeof(double) * NB, hB + r0, sizeof(double) * NB,
+                                             sizeof(double) * nr, n3, cudaMemcpyHostToDevice, up));
+            Event landed;
+            landed.record(up);
+            landed.wait_on(s);
+            GemmDesc d;  // Bh rows [r0, r0+nr) = B rows x Q
+            d.M = nr; d.N = p; d.K = n3;
+            d.A = b.d() + r0; d.lda = NB;
+            d.B = q.d(); d.ldb = n3;
+            d.C = bh.d() + r0; d.ldc = NB;
+            gemm(d, s);
+        }
+    }
+    b.release();
+    // 2. A row blocks: H2D (up) -> transforms + facewise (s) -> D2H (down)
+    const int64_t BI = std::min<int64_t>(n1, 128);
+    DeviceBuffer ablk[2], ahblk[2], chblk[2], cblk[2];
+    Event a_free[2], c_free[2];
+    for (int u = 0; u < 2; ++u) {
+        ablk[u] = DeviceBuffer(sizeof(double) * BI * m * n3);
+        ahblk[u] = DeviceBuffer(sizeof(double) * BI * m * p);
+        chblk[u] = DeviceBuffer(sizeof(double) * BI * n2 * p);
+        cblk[u] = DeviceBuffer(sizeof(double) * BI * n2 * n3);
+        a_free[u].record(s);
+        c_free[u].record(s);
+    }
+    for (int64_t i0 = 0, ib = 0; i0 < n1; i0 += BI, ++ib) {
+        const int u = (int)(ib & 1);
+        const int64_t bi = std::min(BI, n1 - i0);
+        a_free[u].wait_on(up);  // block ib-2's transform has read ablk[u]
+        PPC_CUDA_CHECK(cudaMemcpy2DAsync(ablk[u].d(), sizeof(double) * bi, hA + i0, sizeof(double) * n1,
+                                         sizeof(double) * bi, m * n3, cudaMemcpyHostToDevice, up));
+        Event landed;
+        landed.record(up);
+        landed.wait_on(s);
+        mode3(ablk[u].d(), bi * m, n3, q.d(), p, true, ahblk[u].d(), 1.0, s);  // A_blk x3 Q^T
+        a_free[u].record(s);
+        facewise(ahblk[u].d(), bi, m, p, bh.d(), n2, chblk[u].d(), s);
+        c_free[u].wait_on(s);  // block ib-2's C rows are down
+        mode3(chblk[u].d(), bi * n2, p, q.d(), n3, false, cblk[u].d(), scale, s);  // x3 Q, scale
+        Event done;
+        done.record(s);
+        done.wait_on(down);
+        PPC_CUDA_CHECK(cudaMemcpy2DAsync(hC + i0, sizeof(double) * n1, cblk[u].d(), sizeof(double) * bi,
+                                         sizeof(double) * bi, n2 * n3, cudaMemcpyDeviceToHost, down));
+        c_free[u].record(down);
+    }
+    Event all_down;
+    all_down.record(down);
+    all_down.wait_on(s);  // the stream-ordered frees below come after the last D2H
+}
+
 void sumsq(const double* a, const double* b, int64_t count, double sums[2], cudaStream_t s) {
     DeviceBuffer part(sizeof(double) * 2 * (kReduceBlocks + 1));
     double* fin = part.d() + 2 * kReduceBlocks;

@@ -20,6 +20,12 @@ void facewise(const double* A, int64_t n1, int64_t m, int64_t p, const double* B
 // star_products.cpp:51-59
 void star_q(const double* A, int64_t n1, int64_t m, int64_t n3, const double* B, int64_t n2,
             const double* Q, int64_t p, double scale, double* C, cudaStream_t s);
+// star_q on HOST buffers, pipelined: B is uploaded in pixel chunks and
+// transformed as they land; then A row blocks stream up while the finished C
+// row blocks stream down (separate H2D / D2H streams), so PCIe runs both
+// directions at once. Bitwise equal to star_q on device copies.
+void star_q_host(const double* hA, int64_t n1, int64_t m, int64_t n3, const double* hB, int64_t n2,
+                 const double* hQ, int64_t p, double scale, double* hC, cudaStream_t s);
 // host sums[0] = sum (a-b)^2 (or a^2 when b == nullptr), sums[1] = sum a^2.
 void sumsq(const double* a, const double* b, int64_t count, double sums[2], cudaStream_t s);
 // {||T - T Q Q^T||^2, ||T||^2}; coeff (N x p) may be supplied if already known.

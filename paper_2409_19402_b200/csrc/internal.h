@@ -37,12 +37,14 @@ struct Context {
     bool stream_set = false;            // set explicitly (NULL = legacy default stream)
     cudaStream_t own_stream = nullptr;  // created lazily per device
     cudaStream_t copy = nullptr;        // H2D staging stream
+    cudaStream_t copy_out = nullptr;    // D2H stream (runs beside the H2D one)
     int sms = 148;
     int64_t launches = 0;
 };
 Context& ctx();               // ensures a device is selected (throws PPC_NO_DEVICE)
 cudaStream_t stream();        // current stream of this thread
 cudaStream_t copy_stream();   // this thread's H2D staging stream (overlap)
+cudaStream_t copy_out_stream();  // this thread's D2H stream
 inline void count_launch(int n = 1) { ctx().launches += n; }
 void check_launch(const char* name);  // cudaGetLastError -> PPC_CUDA
 

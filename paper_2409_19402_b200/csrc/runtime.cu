@@ -76,6 +76,12 @@ cudaStream_t stream() {
     return c.own_stream;
 }
 
+cudaStream_t copy_out_stream() {
+    Context& c = ctx();
+    if (!c.copy_out) PPC_CUDA_CHECK(cudaStreamCreateWithFlags(&c.copy_out, cudaStreamNonBlocking));
+    return c.copy_out;
+}
+
 cudaStream_t copy_stream() {
     Context& c = ctx();
     if (!c.copy) PPC_CUDA_CHECK(cudaStreamCreateWithFlags(&c.copy, cudaStreamNonBlocking));

@@ -909,3 +909,16 @@ def test_ozaki_data_q_vs_numpy(engine):
     assert np.abs(lam - w[:64]).max() <= 1e-12 * w[0]
     assert abs(lam.sum() - w[:64].sum()) <= 1e-12 * w[:64].sum()
     assert np.linalg.norm(q.T @ q - np.eye(64)) <= 1e-12
+
+
+@pytest.mark.parametrize("n1,m,n2,n3,p", [(300, 96, 140, 40, 12), (1024, 512, 1024, 256, 64)])
+def test_star_q_host_pipeline_bitwise(engine, n1, m, n2, n3, p):
+    """ppc_star_q_product on host buffers (B chunks transformed as they land,
+    A row blocks up / C row blocks down on separate copy streams) equals the
+    device-resident product bitwise."""
+    A = synth.gaussian_device(n1, m, n3, 8, 1)
+    B = synth.gaussian_device(m, n2, n3, 8, 2)
+    t = engine.Transform("dct", n3, p)
+    dev = engine.to_host(engine.star_q_product(A, B, t))
+    host = engine.star_q_product(engine.to_host(A), engine.to_host(B), t)
+    assert np.array_equal(host, dev)
