@@ -80,6 +80,11 @@ int ppc_set_gemm_path(int mode);
  * where eligible; default), 0 = always the FP64 DMMA SYRK. PPC_OZAKI=0 in the
  * environment sets 0. Results agree to ~1e-14 relative (not bitwise). */
 int ppc_set_ozaki(int mode);
+/* The batched Ozaki SYRK on DEVICE memory (test hook for the INT8 path):
+ * G_b = A_b^T A_b (n x n) for A_b = A + b*strideA (rows x n, lda),
+ * 1024 <= rows <= 4096, n >= 128. PPC_ARGUMENT when not eligible. */
+int ppc_ozaki_syrk_batched(const double* A, int64_t lda, int64_t strideA, int64_t rows, int64_t n, int64_t batch,
+                           double* G);
 int ppc_timing_report(char* buf, int64_t cap, int reset);
 
 /* ---- L3 kernels (tensor.hpp, matrix_kernels.hpp) ------------------------ */

@@ -1,27 +1,34 @@
-// FP64 Gram SYRK on the INT8 tensor cores (tcgen05 kind::i8): the Ozaki
+// FP64 products on the INT8 tensor cores (tcgen05 kind::i8): the Ozaki
 // scheme (Ozaki, Ogita, Oishi, Rump 2012; the INT8 form of Ootomo, Ozaki and
-// Yokota 2024).
+// Yokota 2024), for the Grams and the Chebyshev filter products of the
+// tSVDQ path.
 //
-// The data-driven basis needs G = T^T T over N = n1*n2 pixel rows. Per chunk
-// of KC rows and per column j of T, the column is scaled by a power of two
-// sigma_j with |T(:,j)| / sigma_j <= 1/2 and cut into S signed 7-bit digits,
-//     T(i,j) = sigma_j * ( sum_s d_s(i,j) 2^{-7s} + r(i,j) 2^{-7S} ),
-// |d_s| <= 64, |r| <= 1/2 (every step is exact in FP64). Then
-//     G(a,b) ~= sigma_a sigma_b sum_{L=2}^{S+1} 2^{-7L} Q_L(a,b),
-//     Q_L = sum_{s+t=L} D_s^T D_t,
-// where every Q_L is an exact int32 sum of int8 products (KC * 64^2 * S <
-// 2^31) computed by tcgen05.mma into its own TMEM accumulator. The FP64
-// epilogue adds the levels smallest first. With S = 7 the truncation is
-// ~2^{-50} sigma_a sigma_b per product (sigma ~ the column max, so heavy-
-// tailed columns lose relative precision on small entries: S = 6 measured
-// 4e-12 of max|G| on the cfg5 CP data, S = 7 8e-15), the integer sums are
-// exact, and the error does not grow with the chunk length.
+// Split. Per block of at most KC = 4096 rows and per column j, the column is
+// scaled by sigma_j = 2^e with max|x| / sigma_j < 1/2, rounded to nearest at
+// 2^{-47} sigma_j and cut exactly into S = 6 balanced signed 8-bit digits:
+//     x / sigma = 2^{-7} ( d_1 + 2^{-8} d_2 + ... + 2^{-40} d_6 ) + O(2^{-48}),
+//     d_1 in [-64, 64], d_s in [-128, 127]
+// (the unsigned base-256 digits of 128 x / sigma + c with c = 128 sum_s
+// 2^{-8(s-1)}, each shifted by -128; every step is exact in FP64). Balanced
+// digits keep the dropped low-order pair products sign-symmetric: with
+// unsigned digits they are all positive and their chunk sums grew ~K,
+// measured 8e-13 of max|G| instead of ~1e-14. The one exception is a Gram's
+// diagonal, whose dropped same-digit products (d_4 d_4 at level 8, ...) are
+// squares; it is taken from FP64 column sums of squares instead.
+// Products. For C = A^T B over one block,
+//     C(a,b) ~= sigma_a sigma_b sum_{L=2}^{S+1} 2^{-14-8(L-2)} Q_L(a,b),
+//     Q_L = sum_{s+t=L} D_s^T D_t       (21 digit pairs, 6 levels),
+// and every Q_L is an exact int32 sum (4096 * 6 * 128^2 < 2^31), accumulated
+// by tcgen05.mma in its own TMEM accumulator. Between blocks the epilogue warps drain the levels
+// (smallest weight first), apply the block's scales and add into FP64
+// register accumulators, so one work item covers any number of blocks in a
+// fixed order (deterministic, independent of sharding).
 //
-// Kernels: ozaki_split_kernel (one CTA per (chunk, column): max, scale,
-// digits), ozaki_syrk_kernel (TMA SWIZZLE_64B operand tiles of all S digit
-// planes per stage, one elected thread issuing the S(S+1)/2 digit-pair MMAs,
-// four epilogue warps draining TMEM), sub_sum_kernel (fixed-order sum of a
-// plan chunk's sub-chunk partials).
+// Kernels: ozaki_split_kernel (one CTA per (block, column), block staged in
+// shared memory: one HBM read), ozaki_mma_kernel (one TMA producer warp, one
+// MMA-issuing warp, eight epilogue warps; TMA SWIZZLE_64B tiles of all six
+// digit planes of A (128 rows) and B (80 rows) per 64-byte K stage, 42 MMAs
+// of 128x80x32 per stage).
 #include <cudaTypedefs.h>
 
 #include <algorithm>
@@ -39,66 +46,81 @@ namespace {
 
 using namespace umma;
 
-constexpr int kS = 7;          // digits per value (49 bits; 6 digits measured 4e-12 of max|G| on cfg5-like data)
-constexpr int kBM = 128;       // UMMA M
-constexpr int kBN = 64;        // UMMA N (S levels x 64 columns of TMEM)
-constexpr int kBK = 64;        // bytes (= int8 elements) of K per stage, SWIZZLE_64B
+constexpr int kS = 6;           // digits per value: signed lead + 5 unsigned 8-bit
+constexpr int kBM = 128;        // UMMA M
+constexpr int kBN = 80;         // UMMA N: 6 level accumulators x 80 = 480 TMEM columns
+constexpr int kBK = 64;         // bytes (= int8 elements) of K per stage, SWIZZLE_64B
 constexpr int kStages = 2;
-constexpr int64_t kKC = 65536;  // rows per sub-chunk: 65536 * 64^2 * S < 2^31
-// Tensor memory: S level accumulators (kBN columns each). Optionally (kATmem)
-// the stage's A digit tiles are copied to TMEM after them and the MMAs read
-// only B from shared memory; at S = 6 that measured no faster than reading
-// both operands from shared memory, and at S = 7 it does not fit.
-constexpr int kAcol = kS * kBN;
-#ifndef PPC_OZAKI_ATMEM
-#define PPC_OZAKI_ATMEM 0
-#endif
-constexpr bool kATmem = PPC_OZAKI_ATMEM;
-static_assert(kAcol + (kATmem ? kS * (kBK / 32) * 8 : 0) <= 512, "TMEM budget");
+constexpr int64_t kKC = 4096;   // rows per exact int32 accumulation
+constexpr int kEpiWarps = 8;    // two per TMEM lane quadrant, 40 columns each
+constexpr int kThreads = (2 + kEpiWarps) * 32;
+static_assert(kS * kBN <= 512, "TMEM budget");
+static_assert(kBN / 2 == 40, "epilogue column split (32 + 8)");
 
 // ------------------------------------------------------------------ split
-// One CTA per (block c, column j): block c is rows [c*KC, c*KC+KC) of T
-// (row sub-chunks, strideT = 0) or the whole of matrix T + c*strideT
-// (batched). D layout: [(c*S + s)*n3 + j][KCp] int8. Blocks of up to
-// kStageRows rows are read from HBM once (staged in shared memory for the
-// digit pass); each thread emits four consecutive rows per digit as one
-// 32-bit store.
-constexpr int64_t kStageRows = 4096;  // 32 KB of shared memory (several CTAs per SM)
-
-template <bool STAGE>
-__global__ void __launch_bounds__(256) ozaki_split_kernel(const double* __restrict__ T, int64_t ldT, int64_t strideT,
-                                                          int64_t rows, int64_t n3, int64_t KC, int64_t KCp,
-                                                          int8_t* __restrict__ D, double* __restrict__ scale,
+// One CTA per (block b, column j). Row-chunked mode (stride == 0): block b is
+// sub-block u = b % per of plan chunk cp = b / per, rows
+// [cp*chunk + u*KC, min(cp*chunk + (u+1)*KC, (cp+1)*chunk, rows)). Batched
+// mode: block b is the first min(KC, rows) rows of X + b*stride.
+// D layout: [(b*S + s)*cols + j][KCp] bytes; scale[b*cols + j].
+__global__ void __launch_bounds__(256) ozaki_split_kernel(const double* __restrict__ X, int64_t ldx, int64_t stride,
+                                                          int64_t rows, int64_t cols, int64_t KC, int64_t KCp,
+                                                          int64_t chunk, int64_t per, int8_t* __restrict__ D,
+                                                          double* __restrict__ scale, double* __restrict__ sumsq,
                                                           const int* __restrict__ zmap) {
-    extern __shared__ double stage[];
-    const int64_t j = blockIdx.x, c = zmap ? zmap[blockIdx.y] : blockIdx.y;
-    const int64_t r0 = strideT ? 0 : c * KC;
-    const int64_t len = std::max<int64_t>(0, std::min<int64_t>(KC, rows - r0));
-    const double* col = T + (strideT ? c * strideT : 0) + j * ldT + r0;
-    double mx = 0.0;
+    __shared__ double stage[kKC];
+    const int64_t j = blockIdx.x;
+    const int64_t b = zmap ? zmap[blockIdx.y] : blockIdx.y;
+    int64_t r0, len;
+    if (stride) {
+        r0 = 0;
+        len = std::min<int64_t>(KC, rows);
+    } else {
+        const int64_t cp = b / per, u = b - cp * per;
+        r0 = cp * chunk + u * KC;
+        const int64_t end = std::min<int64_t>(std::min<int64_t>(r0 + KC, (cp + 1) * chunk), rows);
+        len = std::max<int64_t>(0, end - r0);
+    }
+    const double* col = X + (stride ? b * stride : 0) + j * ldx + r0;
+    double mx = 0.0, ss = 0.0;
     for (int64_t i = threadIdx.x; i < len; i += blockDim.x) {
         const double v = col[i];
-        if (STAGE) stage[i] = v;
+        stage[i] = v;
         mx = fmax(mx, fabs(v));
+        ss = fma(v, v, ss);
     }
-    __shared__ double red[8];
+    // block max and (fixed-order) sum of squares: the Gram diagonal in FP64
+    __shared__ double red[8], red2[8];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    for (int o = 16; o > 0; o >>= 1) {
+        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        red[threadIdx.x >> 5] = mx;
+        red2[threadIdx.x >> 5] = ss;
+    }
     __syncthreads();
     if (threadIdx.x < 32) {
         mx = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+        ss = threadIdx.x < (blockDim.x >> 5) ? red2[threadIdx.x] : 0.0;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-        if (threadIdx.x == 0) red[0] = mx;
+        for (int o = 16; o > 0; o >>= 1) {
+            mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            ss += __shfl_xor_sync(0xffffffffu, ss, o);
+        }
+        if (threadIdx.x == 0) {
+            red[0] = mx;
+            sumsq[b * cols + j] = ss;
+        }
     }
     __syncthreads();
     mx = red[0];
-    // sigma = 2^e with mx / sigma <= 1/2 (mx = 0: all digits zero)
+    // sigma = 2^e > 2 max |x| (mx = 0: all digits zero)
     const int e = mx > 0.0 ? ilogb(mx) + 2 : 0;
-    if (threadIdx.x == 0) scale[c * n3 + j] = mx > 0.0 ? ldexp(1.0, e) : 0.0;
-    int8_t* out = D + ((c * kS) * n3 + j) * KCp;
-    const int64_t plane = n3 * KCp;
+    if (threadIdx.x == 0) scale[b * cols + j] = mx > 0.0 ? ldexp(1.0, e) : 0.0;
+    int8_t* out = D + ((b * kS) * cols + j) * KCp;
+    const int64_t plane = cols * KCp;
     for (int64_t i4 = (int64_t)threadIdx.x * 4; i4 < KCp; i4 += (int64_t)blockDim.x * 4) {
         uint32_t w[kS];
 #pragma unroll
@@ -106,13 +128,19 @@ __global__ void __launch_bounds__(256) ozaki_split_kernel(const double* __restri
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const int64_t i = i4 + q;
-            double x = i < len ? ldexp(STAGE ? stage[i] : col[i], -e) : 0.0;
+            // y = 128 x / sigma (in (-64, 64)) rounded to a multiple of 2^-40,
+            // plus the offset c of the balanced digits: at most 48 bits, exact
+            constexpr double c = 0x1p-1 + 0x1p-9 + 0x1p-17 + 0x1p-25 + 0x1p-33;
+            const double y = (i < len ? ldexp(rint(ldexp(stage[i], 47 - e)), -40) : 0.0) + c;
+            double d = floor(y);  // in [-64, 64]
+            double r = y - d;
+            w[0] |= (uint32_t)(uint8_t)(int8_t)d << (8 * q);
 #pragma unroll
-            for (int s = 0; s < kS; ++s) {
-                const double t = x * 128.0;
-                const double d = rint(t);
-                x = t - d;
-                w[s] |= (uint32_t)(uint8_t)(int8_t)d << (8 * q);
+            for (int s = 1; s < kS; ++s) {
+                const double t = r * 256.0;
+                d = floor(t);  // in [0, 255]
+                r = t - d;
+                w[s] |= (uint32_t)(uint8_t)(int8_t)(d - 128.0) << (8 * q);
             }
         }
 #pragma unroll
@@ -120,27 +148,31 @@ __global__ void __launch_bounds__(256) ozaki_split_kernel(const double* __restri
     }
 }
 
-// ------------------------------------------------------------------- syrk
-// One launch covers `items` = nbatch * tiles work items: item -> batch bi,
-// tile t; bi -> operand/output block blk (zmap, else bi). SYM: the tiles are
-// the upper triangle of an M x M Gram, written together with their mirror.
+// ---------------------------------------------------------------- products
+// One launch covers nbatch * tiles work items: item -> batch bi, tile t;
+// bi -> output block ob (zmap, else bi), whose digit blocks are
+// ob*per .. ob*per + per - 1 in both operands (summed in that order).
+// SYM: the tiles are the upper triangle of an M x M Gram (A = B), each
+// written together with its mirror.
 struct OzParams {
     int64_t M, N;          // output extents per block
-    int64_t mtiles, tiles; // row tiles; tiles per block
-    int64_t KCp;           // padded K length (multiple of kBK)
-    const int* zmap;       // nullable batch -> block map
-    const double* sa;      // row scales [blk][M]
-    const double* sb;      // column scales [blk][N]
-    double* C;             // output block blk at C + blk*strideC, (m, n) at m + n*ldc
+    int64_t mtiles, tiles; // row tiles; tiles per output block
+    int64_t KCp;           // padded rows per digit block (multiple of kBK)
+    int64_t per;           // digit blocks per output block
+    const int* zmap;       // nullable batch -> output block map
+    const double* sa;      // row scales [digit block][M]
+    const double* sb;      // column scales [digit block][N]
+    const double* sq;      // SYM: column sums of squares [digit block][M] (the diagonal)
+    double* C;             // output block ob at C + ob*strideC, (m, n) at m + n*ldc
     int64_t ldc, strideC;
 };
 
 // tile t (upper-triangle order) -> (mb, nb): column tile nb holds
-// floor((nb*kBN + kBN - 1) / kBM) + 1 row tiles.
-__device__ __forceinline__ void tri_tile(int64_t t, int64_t& mb, int64_t& nb) {
+// min(floor((nb*kBN + kBN - 1) / kBM) + 1, mtiles) row tiles.
+__device__ __forceinline__ void tri_tile(int64_t t, int64_t mtiles, int64_t& mb, int64_t& nb) {
     nb = 0;
     for (;;) {
-        const int64_t cnt = (nb * kBN + kBN - 1) / kBM + 1;
+        const int64_t cnt = std::min<int64_t>((nb * kBN + kBN - 1) / kBM + 1, mtiles);
         if (t < cnt) break;
         t -= cnt;
         ++nb;
@@ -148,8 +180,9 @@ __device__ __forceinline__ void tri_tile(int64_t t, int64_t& mb, int64_t& nb) {
     mb = t;
 }
 
+
 template <bool SYM>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(kThreads, 1)
     ozaki_mma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                      const OzParams P) {
     extern __shared__ uint8_t smem_raw[];
@@ -159,26 +192,27 @@ __global__ void __launch_bounds__(192, 1)
     uint64_t* full = reinterpret_cast<uint64_t*>(base + kStages * STAGE);
     uint64_t* empty = full + kStages;
     uint64_t* tfull = empty + kStages;
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(tfull + 1);
+    uint64_t* tempty = tfull + 1;
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 1);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t item = blockIdx.x;
     const int64_t bi = item / P.tiles;
-    const int64_t sub = P.zmap ? P.zmap[bi] : bi;
+    const int64_t ob = P.zmap ? P.zmap[bi] : bi;
     int64_t mb, nb;
     if (SYM) {
-        tri_tile(item - bi * P.tiles, mb, nb);
+        tri_tile(item - bi * P.tiles, P.mtiles, mb, nb);
     } else {
         const int64_t t = item - bi * P.tiles;
         mb = t % P.mtiles;
         nb = t / P.mtiles;
     }
-
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
             bar_init(&full[s], 1);
             bar_init(&empty[s], 1);
         }
         bar_init(tfull, 1);
+        bar_init(tempty, kEpiWarps);
         fence_barrier_init();
     }
     if (warp == 1) tmem_alloc<512>(tslot);
@@ -186,120 +220,126 @@ __global__ void __launch_bounds__(192, 1)
     __syncthreads();
     fence_after_sync();
     const uint32_t tmem = *tslot;
-    const int nk = (int)(P.KCp / kBK);
+    const int nkc = (int)(P.KCp / kBK);  // stages per digit block
+    const int64_t per = P.per;
 
     if (warp == 0) {
         if (elect_one()) {
-            for (int kb = 0; kb < nk; ++kb) {
-                const int st = kb % kStages;
-                bar_wait(&empty[st], ((kb / kStages) & 1) ^ 1);
+            const int64_t total = per * nkc;
+            for (int64_t g = 0; g < total; ++g) {
+                const int st = (int)(g % kStages);
+                bar_wait(&empty[st], (uint32_t)(((g / kStages) & 1) ^ 1));
                 bar_expect_tx(&full[st], STAGE);
+                const int64_t blk = ob * per + g / nkc;
+                const int kx = (int)(g % nkc) * kBK;
                 uint8_t* sa = base + st * STAGE;
                 uint8_t* sb = sa + kS * A_TILE;
 #pragma unroll
                 for (int s = 0; s < kS; ++s) {
-                    const int plane = (int)(sub * kS + s);
-                    tma_load_3d(sa + s * A_TILE, &mapA, &full[st], kb * kBK, (int)(mb * kBM), plane);
-                    tma_load_3d(sb + s * B_TILE, &mapB, &full[st], kb * kBK, (int)(nb * kBN), plane);
+                    const int plane = (int)(blk * kS + s);
+                    tma_load_3d(sa + s * A_TILE, &mapA, &full[st], kx, (int)(mb * kBM), plane);
+                    tma_load_3d(sb + s * B_TILE, &mapB, &full[st], kx, (int)(nb * kBN), plane);
                 }
             }
         }
     } else if (warp == 1) {
-        constexpr uint32_t idesc = idesc_i8<kBM, kBN>();
-        for (int kb = 0; kb < nk; ++kb) {
-            const int st = kb % kStages;
-            bar_wait(&full[st], (kb / kStages) & 1);
-            fence_after_sync();
-            if (elect_one()) {
-                const uint8_t* sa = base + st * STAGE;
-                const uint8_t* sb = sa + kS * A_TILE;
-                // A digit tiles -> TMEM (in issue order with the MMAs below and
-                // after the previous stage's MMAs, which read the same columns)
+        constexpr uint32_t kIdesc = idesc_i8<kBM, kBN>();  // signed digits, S32 accumulate
+        for (int64_t cc = 0; cc < per; ++cc) {
+            if (cc > 0) {  // the epilogue has drained the previous block's levels
+                bar_wait(tempty, (uint32_t)((cc - 1) & 1));
+                fence_after_sync();
+            }
+            for (int kb = 0; kb < nkc; ++kb) {
+                const int64_t g = cc * nkc + kb;
+                const int st = (int)(g % kStages);
+                bar_wait(&full[st], (uint32_t)((g / kStages) & 1));
+                fence_after_sync();
+                if (elect_one()) {
+                    const uint8_t* sa = base + st * STAGE;
+                    const uint8_t* sb = sa + kS * A_TILE;
 #pragma unroll
-                for (int s = 0; s < (kATmem ? kS : 0); ++s) {
-                    const uint64_t da = sdesc_k_sw64(sa + s * A_TILE);
+                    for (int l = 0; l < kS; ++l) {  // level L = l + 2
+                        const int L = l + 2;
+                        const int s_lo = L - kS > 1 ? L - kS : 1, s_hi = L - 1 < kS ? L - 1 : kS;
 #pragma unroll
-                    for (int kk = 0; kk < kBK / 32; ++kk)
-                        tmem_cp_128x256b(tmem + (uint32_t)(kAcol + (s * (kBK / 32) + kk) * 8), da + (uint64_t)(kk * 2));
-                }
+                        for (int s = s_lo; s <= s_hi; ++s) {
+                            const int t = L - s;
+                            const uint64_t da = sdesc_k_sw64(sa + (s - 1) * A_TILE);
+                            const uint64_t db = sdesc_k_sw64(sb + (t - 1) * B_TILE);
 #pragma unroll
-                for (int l = 0; l < kS; ++l) {  // level L = l + 2
-                    const int L = l + 2;
-                    const int s_lo = L - kS > 1 ? L - kS : 1, s_hi = L - 1 < kS ? L - 1 : kS;
-#pragma unroll
-                    for (int s = s_lo; s <= s_hi; ++s) {
-                        const int t = L - s;
-                        const uint64_t db = sdesc_k_sw64(sb + (t - 1) * B_TILE);
-#pragma unroll
-                        for (int kk = 0; kk < kBK / 32; ++kk) {
-                            const uint32_t acc = (kb > 0 || s > s_lo || kk > 0) ? 1u : 0u;
-                            if (kATmem)
-                                mma_i8_ts(tmem + (uint32_t)(l * kBN),
-                                          tmem + (uint32_t)(kAcol + ((s - 1) * (kBK / 32) + kk) * 8),
-                                          db + (uint64_t)(kk * 2), idesc, acc);
-                            else
-                                mma_i8(tmem + (uint32_t)(l * kBN), sdesc_k_sw64(sa + (s - 1) * A_TILE) + (uint64_t)(kk * 2),
-                                       db + (uint64_t)(kk * 2), idesc, acc);
+                            for (int kk = 0; kk < kBK / 32; ++kk)
+                                mma_i8(tmem + (uint32_t)(l * kBN), da + (uint64_t)(kk * 2), db + (uint64_t)(kk * 2),
+                                       kIdesc, (kb > 0 || s > s_lo || kk > 0) ? 1u : 0u);
                         }
                     }
+                    mma_commit(&empty[st]);
                 }
-                mma_commit(&empty[st]);
+                __syncwarp();
             }
+            if (elect_one()) mma_commit(tfull);
             __syncwarp();
         }
-        if (elect_one()) mma_commit(tfull);
-        __syncwarp();
     } else {
-        // epilogue: warp w drains TMEM lanes 32*(w%4) .. +32 (rows of the tile)
-        bar_wait(tfull, 0);
-        fence_after_sync();
-        const int q = warp & 3;
+        // epilogue: warp w drains TMEM lanes 32*(w%4) .. +32 (rows of the
+        // tile), columns [h*40, h*40 + 40) with h = (w - 2) / 4
+        const int q = warp & 3, h = (warp - 2) >> 2;
+        constexpr int NH = kBN / 2;
         const int64_t m = mb * kBM + q * 32 + lane;
-        double acc[kBN];
+        const int64_t n0 = nb * kBN + h * NH;
+        double acc[NH];
 #pragma unroll
-        for (int j = 0; j < kBN; ++j) acc[j] = 0.0;
+        for (int j = 0; j < NH; ++j) acc[j] = 0.0;
+        for (int64_t cc = 0; cc < per; ++cc) {
+            bar_wait(tfull, (uint32_t)(cc & 1));
+            fence_after_sync();
+            const int64_t blk = ob * per + cc;
+            double inner[NH];
+#pragma unroll
+            for (int j = 0; j < NH; ++j) inner[j] = 0.0;
 #pragma unroll 1
-        for (int l = kS - 1; l >= 0; --l) {  // smallest weight first
-            const double w = ldexp(1.0, -7 * (l + 2));
-#pragma unroll
-            for (int h = 0; h < kBN; h += 32) {
+            for (int l = kS - 1; l >= 0; --l) {  // smallest weight first
+                const double w = ldexp(1.0, -14 - 8 * l);
+                const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(l * kBN + h * NH);
                 int32_t v[32];
-                tmem_ld_32x32b_x32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(l * kBN + h), v);
+                tmem_ld_32x32b_x32(ta, v);
+                int32_t v8[8];
+                tmem_ld_32x32b_x8(ta + 32, v8);
                 tmem_ld_wait();
 #pragma unroll
-                for (int j = 0; j < 32; ++j) acc[h + j] = fma((double)v[j], w, acc[h + j]);
+                for (int j = 0; j < 32; ++j) inner[j] = fma((double)v[j], w, inner[j]);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) inner[32 + j] = fma((double)v8[j], w, inner[32 + j]);
+            }
+            fence_before_sync();
+            __syncwarp();
+            if (lane == 0) bar_arrive(tempty);  // the MMAs may overwrite the levels
+            const double sm = m < P.M ? P.sa[blk * P.M + m] : 0.0;
+            const double* sc = P.sb + blk * P.N;
+#pragma unroll
+            for (int j = 0; j < NH; ++j) {
+                const int64_t n = n0 + j;
+                // the diagonal of a Gram from the FP64 sums of squares: its
+                // dropped same-digit pair products are squares (biased > 0)
+                if (SYM && n == m)
+                    acc[j] += P.sq[blk * P.M + m];
+                else
+                    acc[j] = fma(inner[j] * sm, n < P.N ? sc[n] : 0.0, acc[j]);
             }
         }
         if (m < P.M) {
-            const double sm = P.sa[sub * P.M + m];
-            const double* sc = P.sb + sub * P.N;
-            double* C = P.C + sub * P.strideC;
+            double* C = P.C + ob * P.strideC;
 #pragma unroll 4
-            for (int j = 0; j < kBN; ++j) {
-                const int64_t n = nb * kBN + j;
+            for (int j = 0; j < NH; ++j) {
+                const int64_t n = n0 + j;
                 if (n >= P.N) break;
-                const double v = acc[j] * sm * sc[n];
-                C[m + n * P.ldc] = v;                // (m, n), coalesced over the warp's rows
-                if (SYM) C[n + m * P.ldc] = v;       // mirror (n, m): the same exact integer sums
+                C[m + n * P.ldc] = acc[j];           // (m, n), coalesced over the warp's rows
+                if (SYM) C[n + m * P.ldc] = acc[j];  // mirror (n, m): the same exact integer sums
             }
         }
     }
     fence_before_sync();
     __syncthreads();
     if (warp == 1) tmem_free<512>(tmem);
-}
-
-// parts[c] = sum_{u < per} sub[c*per + u] in ascending u (fixed order)
-__global__ void sub_sum_kernel(const double* __restrict__ sub, int64_t per, int64_t elems, int64_t total,
-                               double* __restrict__ parts) {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
-        const int64_t c = i / elems, e = i - c * elems;
-        const double* p = sub + c * per * elems + e;
-        double a = p[0];
-        for (int64_t u = 1; u < per; ++u) a += p[u * elems];
-        parts[i] = a;
-    }
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -315,13 +355,13 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-// 3-D int8 map over the digit planes: (k, row, plane), box (kBK, rows, 1),
-// SWIZZLE_64B (rows beyond n3 read as zeros: they never reach another plane).
-bool make_digit_map(CUtensorMap* map, const int8_t* D, int64_t KCp, int64_t n3, int64_t planes, int box_rows) {
+// 3-D uint8 map over the digit planes: (k, row, plane), box (kBK, rows, 1),
+// SWIZZLE_64B (rows beyond `cols` read as zeros: they never reach another plane).
+bool make_digit_map(CUtensorMap* map, const int8_t* D, int64_t KCp, int64_t cols, int64_t planes, int box_rows) {
     auto fn = encode_fn();
     if (!fn) return false;
-    cuuint64_t dims[3] = {(cuuint64_t)KCp, (cuuint64_t)n3, (cuuint64_t)planes};
-    cuuint64_t strides[2] = {(cuuint64_t)KCp, (cuuint64_t)(KCp * n3)};
+    cuuint64_t dims[3] = {(cuuint64_t)KCp, (cuuint64_t)cols, (cuuint64_t)planes};
+    cuuint64_t strides[2] = {(cuuint64_t)KCp, (cuuint64_t)(KCp * cols)};
     cuuint32_t box[3] = {(cuuint32_t)kBK, (cuuint32_t)box_rows, 1};
     cuuint32_t es[3] = {1, 1, 1};
     return fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<int8_t*>(D), dims, strides, box, es,
@@ -340,46 +380,9 @@ bool ozaki_enabled() {
     return v == 1;
 }
 
-}  // namespace
-
-void OzakiDigits::split(const double* X, int64_t ldx, int64_t stride, int64_t rows_, int64_t cols_, int64_t KC,
-                        int64_t nblk_, cudaStream_t s, const int* zmap, int64_t nz) {
-    rows = rows_;
-    cols = cols_;
-    nblk = nblk_;
-    KCp = (KC + kBK - 1) / kBK * kBK;
-    const size_t dbytes = sizeof(int8_t) * nblk * kS * cols * KCp, sbytes = sizeof(double) * nblk * cols;
-    if (D.bytes() < dbytes) D = DeviceBuffer(dbytes);
-    if (sc.bytes() < sbytes) sc = DeviceBuffer(sbytes);
-    if (zmap && !stride) fail(PPC_ARGUMENT, "ozaki split: a block map needs batched blocks");
-    const int64_t launched = zmap ? nz : nblk;
-    if (launched <= 0) return;
-    const double total_rows = stride ? (double)rows * launched : (double)rows;
-    StageTimer ts("ozaki_split", s, 0.0, 8.0 * total_rows * cols + (double)kS * total_rows * cols);
-    dim3 grid((unsigned)cols, (unsigned)launched);
-    if (KC <= kStageRows) {
-        const size_t sm = sizeof(double) * KC;
-        static bool attr = false;
-        if (!attr) {
-            PPC_CUDA_CHECK(cudaFuncSetAttribute(ozaki_split_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                (int)(sizeof(double) * kStageRows)));
-            attr = true;
-        }
-        ozaki_split_kernel<true><<<grid, 256, sm, s>>>(X, ldx, stride, rows, cols, KC, KCp, D.as<int8_t>(), sc.d(),
-                                                       zmap);
-    } else {
-        ozaki_split_kernel<false><<<grid, 256, 0, s>>>(X, ldx, stride, rows, cols, KC, KCp, D.as<int8_t>(), sc.d(),
-                                                        zmap);
-    }
-    count_launch();
-    check_launch("ozaki_split");
-}
-
-namespace {
-
 template <bool SYM>
 void launch_mma(const CUtensorMap& ma, const CUtensorMap& mb, const OzParams& P, int64_t items, cudaStream_t s) {
-    const size_t smem = 1024 + (size_t)kStages * kS * (kBM + kBN) * kBK + (2 * kStages + 1) * 8 + 16;
+    const size_t smem = 1024 + (size_t)kStages * kS * (kBM + kBN) * kBK + (2 * kStages + 2) * 8 + 16;
     static bool attr = false;
     if (!attr) {
         PPC_CUDA_CHECK(cudaFuncSetAttribute(ozaki_mma_kernel<SYM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -387,43 +390,73 @@ void launch_mma(const CUtensorMap& ma, const CUtensorMap& mb, const OzParams& P,
     }
     if (items > 0x7fffffffLL) fail(PPC_ARGUMENT, "ozaki: too many tiles");
     if (items == 0) return;
-    ozaki_mma_kernel<SYM><<<(unsigned)items, 192, smem, s>>>(ma, mb, P);
+    ozaki_mma_kernel<SYM><<<(unsigned)items, kThreads, smem, s>>>(ma, mb, P);
     count_launch();
     check_launch("ozaki_mma");
 }
 
-// Split + SYRK over nblk blocks of KC rows (see ozaki_split_kernel): out[c]
-// (n3 x n3, column-major) = T_c^T T_c for every block c.
-void ozaki_syrk_blocks(const double* T, int64_t ldT, int64_t strideT, int64_t rows, int64_t n3, int64_t KC,
-                       int64_t nblk, double* out, cudaStream_t s, const char* stage) {
-    OzakiDigits d;
-    d.split(T, ldT, strideT, rows, n3, KC, nblk, s);
+int64_t tri_tiles(int64_t n) {
+    const int64_t mtiles = (n + kBM - 1) / kBM;
+    int64_t tiles = 0;
+    for (int64_t nb = 0; nb < (n + kBN - 1) / kBN; ++nb)
+        tiles += std::min<int64_t>((nb * kBN + kBN - 1) / kBM + 1, mtiles);
+    return tiles;
+}
+
+// Grams of `nout` outputs, each summing `per` digit blocks of d: out[ob] =
+// sum over its blocks of X_blk^T X_blk (cols x cols, column-major).
+void ozaki_syrk(const OzakiDigits& d, int64_t nout, int64_t per, double* out, cudaStream_t s, const char* stage,
+                double rows_total) {
     CUtensorMap ma, mb;
-    if (!make_digit_map(&ma, d.D.as<int8_t>(), d.KCp, n3, nblk * kS, kBM) ||
-        !make_digit_map(&mb, d.D.as<int8_t>(), d.KCp, n3, nblk * kS, kBN))
+    if (!make_digit_map(&ma, d.D.as<int8_t>(), d.KCp, d.cols, d.nblk * kS, kBM) ||
+        !make_digit_map(&mb, d.D.as<int8_t>(), d.KCp, d.cols, d.nblk * kS, kBN))
         fail(PPC_CUDA, "ozaki: tensor map encoding failed");
     OzParams P;
-    P.M = P.N = n3;
-    P.mtiles = (n3 + kBM - 1) / kBM;
-    P.tiles = 0;
-    for (int64_t nb = 0; nb < (n3 + kBN - 1) / kBN; ++nb)
-        P.tiles += std::min<int64_t>((nb * kBN + kBN - 1) / kBM + 1, P.mtiles);
+    P.M = P.N = d.cols;
+    P.mtiles = (d.cols + kBM - 1) / kBM;
+    P.tiles = tri_tiles(d.cols);
     P.KCp = d.KCp;
+    P.per = per;
     P.zmap = nullptr;
     P.sa = P.sb = d.sc.d();
+    P.sq = d.sq.d();
     P.C = out;
-    P.ldc = n3;
-    P.strideC = n3 * n3;
-    const double total_rows = strideT ? (double)rows * nblk : (double)rows;
-    StageTimer tk(stage, s, 2.0 * kS * (kS + 1) / 2 * total_rows * n3 * n3 / 2, (double)kS * total_rows * n3);
-    launch_mma<true>(ma, mb, P, nblk * P.tiles, s);
+    P.ldc = d.cols;
+    P.strideC = d.cols * d.cols;
+    // int8 ops of the 21 digit-pair products over the upper triangle
+    StageTimer tk(stage, s, 2.0 * kS * (kS + 1) / 2 * rows_total * d.cols * d.cols / 2,
+                  (double)kS * rows_total * d.cols);
+    launch_mma<true>(ma, mb, P, nout * P.tiles, s);
 }
 
 }  // namespace
 
+void OzakiDigits::split(const double* X, int64_t ldx, int64_t stride, int64_t rows_, int64_t cols_, int64_t KC,
+                        int64_t nblk_, cudaStream_t s, const int* zmap, int64_t nz, int64_t chunk, int64_t per) {
+    if (KC < 1 || KC > kKC) fail(PPC_ARGUMENT, "ozaki split: block length out of range");
+    if (zmap && !stride) fail(PPC_ARGUMENT, "ozaki split: a block map needs batched blocks");
+    rows = rows_;
+    cols = cols_;
+    nblk = nblk_;
+    KCp = (KC + kBK - 1) / kBK * kBK;
+    const size_t dbytes = sizeof(int8_t) * nblk * kS * cols * KCp, sbytes = sizeof(double) * nblk * cols;
+    if (D.bytes() < dbytes) D = DeviceBuffer(dbytes);
+    if (sc.bytes() < sbytes) sc = DeviceBuffer(sbytes);
+    if (sq.bytes() < sbytes) sq = DeviceBuffer(sbytes);
+    const int64_t launched = zmap ? nz : nblk;
+    if (launched <= 0) return;
+    const double total_rows = stride ? (double)std::min(KC, rows) * launched : (double)rows;
+    StageTimer ts("ozaki_split", s, 0.0, 8.0 * total_rows * cols + (double)kS * total_rows * cols);
+    dim3 grid((unsigned)cols, (unsigned)launched);
+    ozaki_split_kernel<<<grid, 256, 0, s>>>(X, ldx, stride, rows, cols, KC, KCp, chunk ? chunk : KC, per ? per : 1,
+                                            D.as<int8_t>(), sc.d(), sq.d(), zmap);
+    count_launch();
+    check_launch("ozaki_split");
+}
+
 void ozaki_gemm(const OzakiDigits& A, const OzakiDigits& B, int64_t nbatch, const int* zmap, double* C, int64_t ldc,
                 int64_t strideC, cudaStream_t s) {
-    if (A.KCp != B.KCp || A.rows != B.rows) fail(PPC_ARGUMENT, "ozaki_gemm: K mismatch");
+    if (A.KCp != B.KCp) fail(PPC_ARGUMENT, "ozaki_gemm: K mismatch");
     CUtensorMap ma, mb;
     if (!make_digit_map(&ma, A.D.as<int8_t>(), A.KCp, A.cols, A.nblk * kS, kBM) ||
         !make_digit_map(&mb, B.D.as<int8_t>(), B.KCp, B.cols, B.nblk * kS, kBN))
@@ -434,14 +467,17 @@ void ozaki_gemm(const OzakiDigits& A, const OzakiDigits& B, int64_t nbatch, cons
     P.mtiles = (P.M + kBM - 1) / kBM;
     P.tiles = P.mtiles * ((P.N + kBN - 1) / kBN);
     P.KCp = A.KCp;
+    P.per = 1;
     P.zmap = zmap;
     P.sa = A.sc.d();
     P.sb = B.sc.d();
+    P.sq = nullptr;
     P.C = C;
     P.ldc = ldc;
     P.strideC = strideC;
-    StageTimer tk("ozaki_gemm", s, 2.0 * kS * (kS + 1) / 2 * (double)nbatch * P.M * P.N * A.rows,
-                  (double)kS * nbatch * (P.M + P.N) * A.rows);
+    const double K = (double)std::min(A.rows, kKC);
+    StageTimer tk("ozaki_gemm", s, 2.0 * kS * (kS + 1) / 2 * (double)nbatch * P.M * P.N * K,
+                  (double)kS * nbatch * (P.M + P.N) * K);
     launch_mma<false>(ma, mb, P, nbatch * P.tiles, s);
 }
 
@@ -451,43 +487,28 @@ bool ozaki_gram_partials(const double* T, int64_t ldT, int64_t rows, int64_t n3,
                          double* parts, cudaStream_t s) {
     if (!ozaki_enabled()) return false;
     // the integer path pays off once each output tile sees a long K range
-    if (n3 < 128 || n3 > 65535 || chunk < 4096 || rows < 4096 * 4) return false;
+    if (n3 < 128 || chunk < 4096 || rows < 4096 * 4) return false;
     if (rows > chunk * nchunks) return false;
-    // sub-chunks of KC rows tile every plan chunk exactly (a longer plan
-    // chunk must be a multiple of KC), so a plan chunk's partial never
-    // depends on how the rows are sharded
-    // (KC = kKC: longer sub-chunks keep the split's second read of each
-    // column chunk L2-resident and the sub-chunk partials few; staging 16K-row
-    // chunks in shared memory measured slower at one CTA per SM)
-    if (chunk > kKC && chunk % kKC != 0) return false;
-    const int64_t KC = std::min<int64_t>(chunk, kKC);
-    const int64_t per_chunk = chunk / KC;
-    const int64_t nsub = nchunks * per_chunk;
-    if (nsub * kS > 65535) return false;
+    // each plan chunk is split into ceil(chunk / 4096) blocks that never cross
+    // a plan-chunk boundary, and its partial sums them in order inside one
+    // work item: the partial does not depend on how the rows are sharded
+    const int64_t per = (chunk + kKC - 1) / kKC;
+    const int64_t nblk = nchunks * per;
     StageTimer tm("gram_ozaki", s, (double)rows * n3 * n3, 8.0 * rows * n3);
-    DeviceBuffer subp;
-    double* out = parts;
-    if (per_chunk > 1) {
-        subp = DeviceBuffer(sizeof(double) * nsub * n3 * n3);
-        out = subp.d();
-    }
-    ozaki_syrk_blocks(T, ldT, 0, rows, n3, KC, nsub, out, s, "ozaki_syrk");
-    if (per_chunk > 1) {
-        const int64_t elems = n3 * n3, total = nchunks * elems;
-        sub_sum_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, 148 * 16), 256, 0, s>>>(out, per_chunk, elems,
-                                                                                               total, parts);
-        count_launch();
-        check_launch("sub_sum");
-    }
+    OzakiDigits d;
+    d.split(T, ldT, 0, rows, n3, kKC, nblk, s, nullptr, 0, chunk, per);
+    ozaki_syrk(d, nchunks, per, parts, s, "ozaki_syrk", (double)rows);
     return true;
 }
 
 bool ozaki_syrk_batched(const double* A, int64_t lda, int64_t strideA, int64_t rows, int64_t n, int64_t batch,
                         double* G, cudaStream_t s) {
     if (!ozaki_enabled()) return false;
-    if (n < 128 || rows < 1024 || rows > kKC || batch < 1 || batch * kS > 65535) return false;
+    if (n < 128 || rows < 1024 || rows > kKC || batch < 1) return false;
     if (strideA < lda * n) return false;
-    ozaki_syrk_blocks(A, lda, strideA, rows, n, rows, batch, G, s, "ozaki_syrk_batched");
+    OzakiDigits d;
+    d.split(A, lda, strideA, rows, n, rows, batch, s);
+    ozaki_syrk(d, batch, 1, G, s, "ozaki_syrk_batched", (double)rows * batch);
     return true;
 }
 
@@ -497,4 +518,13 @@ extern "C" int ppc_set_ozaki(int mode) {
     if (mode < 0 || mode > 1) return PPC_ARGUMENT;
     ppc::g_ozaki.store(mode);
     return 0;
+}
+
+extern "C" int ppc_ozaki_syrk_batched(const double* A, int64_t lda, int64_t strideA, int64_t rows, int64_t n,
+                                      int64_t batch, double* G) {
+    return ppc::guarded([&] {
+        if (!A || !G) ppc::fail(PPC_ARGUMENT, "null pointer");
+        if (!ppc::ozaki_syrk_batched(A, lda, strideA, rows, n, batch, G, ppc::stream()))
+            ppc::fail(PPC_ARGUMENT, "ozaki_syrk_batched: shape not eligible (or the path is off)");
+    });
 }

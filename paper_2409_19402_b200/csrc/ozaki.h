@@ -7,16 +7,18 @@
 
 namespace ppc {
 
-// Ozaki digits of nblk FP64 blocks: block c is X + c*stride (rows x cols,
-// leading dimension ldx; stride 0: the row sub-chunk [c*KC, c*KC+KC) of one
-// matrix). Every column is scaled by a power of two and cut into 7 signed
-// 7-bit digits along the rows (the K dimension of the products below).
+// Ozaki digits of nblk FP64 blocks of at most KC <= 4096 rows: block c is
+// X + c*stride (batched; its first min(KC, rows) rows), or, with stride 0,
+// sub-block c % per of plan chunk c / per (chunk rows each) of one matrix
+// (leading dimension ldx). Every column of a block is scaled by a power of
+// two and cut into 6 8-bit digits along the rows (the K dimension of the
+// products below): a signed lead digit and five unsigned ones.
 struct OzakiDigits {
-    DeviceBuffer D, sc;  // int8 planes [blk][digit][col][KCp]; scales [blk][col]
+    DeviceBuffer D, sc, sq;  // int8 planes [blk][digit][col][KCp]; scales, sums of squares [blk][col]
     int64_t rows = 0, cols = 0, KCp = 0, nblk = 0;
     // zmap (device, nz entries; batched blocks only): split just those blocks
     void split(const double* X, int64_t ldx, int64_t stride, int64_t rows, int64_t cols, int64_t KC, int64_t nblk,
-               cudaStream_t s, const int* zmap = nullptr, int64_t nz = 0);
+               cudaStream_t s, const int* zmap = nullptr, int64_t nz = 0, int64_t chunk = 0, int64_t per = 0);
 };
 
 // C_b (A.cols x B.cols, (m, n) at m + n*ldc, b at blk*strideC) = A_blk^T B_blk
@@ -29,7 +31,7 @@ bool ozaki_gemm_eligible(int64_t M, int64_t K);
 
 // Per-plan-chunk partial Grams parts[c] = T_c^T T_c (nchunks x n3 x n3) of a
 // tube matrix T (rows x n3, leading dimension ldT), as gram_partials, through
-// 7-digit int8 splitting and tcgen05 kind::i8 MMAs. Returns false when the
+// 8-bit digit splitting and tcgen05 kind::i8 MMAs. Returns false when the
 // shape is not eligible (caller falls back to the DMMA SYRK). PPC_OZAKI=0
 // disables it.
 bool ozaki_gram_partials(const double* T, int64_t ldT, int64_t rows, int64_t n3, int64_t chunk, int64_t nchunks,
@@ -37,7 +39,7 @@ bool ozaki_gram_partials(const double* T, int64_t ldT, int64_t rows, int64_t n3,
 
 // G_b (n x n, column-major, b < batch, stride n*n) = A_b^T A_b for A_b
 // (rows x n, leading dimension lda) at A + b*strideA: the batched slice
-// Grams. rows <= 65536. Returns false when not eligible.
+// Grams. rows <= 4096. Returns false when not eligible.
 bool ozaki_syrk_batched(const double* A, int64_t lda, int64_t strideA, int64_t rows, int64_t n, int64_t batch,
                         double* G, cudaStream_t s);
 
