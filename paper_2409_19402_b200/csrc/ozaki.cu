@@ -121,6 +121,11 @@ __global__ void __launch_bounds__(256) ozaki_split_kernel(const double* __restri
     if (threadIdx.x == 0) scale[b * cols + j] = mx > 0.0 ? ldexp(1.0, e) : 0.0;
     int8_t* out = D + ((b * kS) * cols + j) * KCp;
     const int64_t plane = cols * KCp;
+    // Integer digit extraction: y = rint(2^40 * 128 x / sigma) (|y| < 2^46),
+    // U = y + c * 2^40 with c * 2^40 = 0x8080808080; the lead digit is
+    // U >> 40 (arithmetic: floor) and the balanced low digits are the bytes
+    // of U ^ 0x8080808080 (u - 128 as int8).
+    const double scl = mx > 0.0 ? ldexp(1.0, 47 - e) : 0.0;
     for (int64_t i4 = (int64_t)threadIdx.x * 4; i4 < KCp; i4 += (int64_t)blockDim.x * 4) {
         uint32_t w[kS];
 #pragma unroll
@@ -128,20 +133,12 @@ __global__ void __launch_bounds__(256) ozaki_split_kernel(const double* __restri
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const int64_t i = i4 + q;
-            // y = 128 x / sigma (in (-64, 64)) rounded to a multiple of 2^-40,
-            // plus the offset c of the balanced digits: at most 48 bits, exact
-            constexpr double c = 0x1p-1 + 0x1p-9 + 0x1p-17 + 0x1p-25 + 0x1p-33;
-            const double y = (i < len ? ldexp(rint(ldexp(stage[i], 47 - e)), -40) : 0.0) + c;
-            double d = floor(y);  // in [-64, 64]
-            double r = y - d;
-            w[0] |= (uint32_t)(uint8_t)(int8_t)d << (8 * q);
+            const long long y = i < len ? __double2ll_rn(stage[i] * scl) : 0LL;
+            const long long U = y + 0x8080808080LL;
+            const uint64_t low = (uint64_t)U ^ 0x8080808080ULL;
+            w[0] |= (uint32_t)(uint8_t)(int8_t)(U >> 40) << (8 * q);
 #pragma unroll
-            for (int s = 1; s < kS; ++s) {
-                const double t = r * 256.0;
-                d = floor(t);  // in [0, 255]
-                r = t - d;
-                w[s] |= (uint32_t)(uint8_t)(int8_t)(d - 128.0) << (8 * q);
-            }
+            for (int s = 1; s < kS; ++s) w[s] |= (uint32_t)((low >> (40 - 8 * s)) & 0xFFu) << (8 * q);
         }
 #pragma unroll
         for (int s = 0; s < kS; ++s) *reinterpret_cast<uint32_t*>(out + s * plane + i4) = w[s];
