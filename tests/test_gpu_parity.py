@@ -922,3 +922,49 @@ def test_star_q_host_pipeline_bitwise(engine, n1, m, n2, n3, p):
     dev = engine.to_host(engine.star_q_product(A, B, t))
     host = engine.star_q_product(engine.to_host(A), engine.to_host(B), t)
     assert np.array_equal(host, dev)
+
+
+def test_ozaki_compress_matches_dmma(engine):
+    """ppc_tsvdq_compress with the INT8 (Ozaki) Gram, slice Grams and filter
+    products against the all-FP64-DMMA run (cfg5 distribution): relative
+    error and singular values agree to ~1e-12, the basis on its
+    well-separated (signal) columns to ~1e-9."""
+    import ctypes as C
+    from paper_2409_19402_b200 import _lib
+    L = _lib.lib()
+    n1, n2, n3, p, k = 512, 512, 512, 64, 16
+    a = synth.cp_tensor_device(n1, n2, n3, rank=50, noise=1e-3, seed=6)
+    res = {}
+    try:
+        for mode in (1, 0):
+            assert L.ppc_set_ozaki(mode) == 0
+            L.ppc_timing_enable(1)
+            Q, U, S, V = (engine.empty_device(sh) for sh in ((n3, p), (n1, k, p), (k, p), (n2, k, p)))
+            re = C.c_double()
+            rc = L.ppc_tsvdq_compress(C.c_void_p(a.data_ptr()), n1, n2, n3, p, k, C.c_void_p(Q.data_ptr()), None,
+                                      C.c_void_p(U.data_ptr()), C.c_void_p(S.data_ptr()), C.c_void_p(V.data_ptr()),
+                                      C.byref(re), 1)
+            buf = C.create_string_buffer(1 << 16)
+            L.ppc_timing_report(buf, len(buf), 1)
+            L.ppc_timing_enable(0)
+            assert rc == 0, L.ppc_last_error()
+            res[mode] = (re.value, engine.to_host(S), engine.to_host(Q), buf.value.decode())
+    finally:
+        L.ppc_set_ozaki(1)
+    assert "ozaki_syrk" in res[1][3], res[1][3]
+    assert "ozaki_syrk" not in res[0][3]
+    assert abs(res[1][0] - res[0][0]) <= 1e-11 * res[0][0], (res[1][0], res[0][0])
+    # signal slices (the noise columns of Q are not determined to the last
+    # bits on a plateau, so their slices differ with the basis)
+    assert np.abs(res[1][1][:, :40] - res[0][1][:, :40]).max() <= 1e-11 * res[0][1].max()
+    assert np.abs(res[1][2][:, :40] - res[0][2][:, :40]).max() <= 1e-9
+    # with a shared basis every slice (noise ones too) agrees to 1e-10 per value
+    t = engine.Transform.custom(res[0][2])
+    s_on = engine.to_host(engine.tsvdq(a, t, k).s)
+    try:
+        assert L.ppc_set_ozaki(0) == 0
+        s_off = engine.to_host(engine.tsvdq(a, t, k).s)
+    finally:
+        L.ppc_set_ozaki(1)
+    assert np.abs(s_on - s_off).max() <= 1e-10 * np.abs(s_off).max()
+    assert (np.abs(s_on - s_off) <= 1e-10 * s_off).all()
