@@ -125,7 +125,9 @@ __global__ void __launch_bounds__(256) ozaki_split_kernel(const double* __restri
     // U = y + c * 2^40 with c * 2^40 = 0x8080808080; the lead digit is
     // U >> 40 (arithmetic: floor) and the balanced low digits are the bytes
     // of U ^ 0x8080808080 (u - 128 as int8).
-    const double scl = mx > 0.0 ? ldexp(1.0, 47 - e) : 0.0;
+    // 2^(47-e) as two finite factors: e may be near -1074 (subnormal columns)
+    const int e1 = (47 - e) / 2;
+    const double scl1 = mx > 0.0 ? ldexp(1.0, e1) : 0.0, scl2 = ldexp(1.0, 47 - e - e1);
     for (int64_t i4 = (int64_t)threadIdx.x * 4; i4 < KCp; i4 += (int64_t)blockDim.x * 4) {
         uint32_t w[kS];
 #pragma unroll
@@ -133,7 +135,7 @@ __global__ void __launch_bounds__(256) ozaki_split_kernel(const double* __restri
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const int64_t i = i4 + q;
-            const long long y = i < len ? __double2ll_rn(stage[i] * scl) : 0LL;
+            const long long y = i < len ? __double2ll_rn(stage[i] * scl1 * scl2) : 0LL;
             const long long U = y + 0x8080808080LL;
             const uint64_t low = (uint64_t)U ^ 0x8080808080ULL;
             w[0] |= (uint32_t)(uint8_t)(int8_t)(U >> 40) << (8 * q);

@@ -412,6 +412,7 @@ void subspace_eig_top(const double* G, int64_t r, int64_t batch, int64_t k, doub
         double energy = 0.0;
         for (int64_t i = 0; i < b * batch; ++i) energy += std::max(th[i], 0.0);
         std::vector<int> deg(batch, 0);
+        bool near_floor = false;
         std::vector<double> cc(batch), ee(batch);
         for (int64_t sl = 0; sl < batch; ++sl) {
             const double* t = &th[sl * b];
@@ -490,6 +491,11 @@ void subspace_eig_top(const double* G, int64_t r, int64_t batch, int64_t k, doub
                 continue;
             }
             all_done = false;
+            // within ~1e-11 theta_1 of the lock thresholds the INT8 filter's
+            // own rounding (~1e-14 |G| |Y|) would floor the residuals: filter
+            // in FP64 from here on
+            for (int64_t j = L; j < k; ++j)
+                if (rr[j] <= 1e-11 * scale) near_floor = true;
             // Chebyshev interval [0, ub]: damp everything below the smallest Ritz value
             const double ub = std::max(t[b - 1], 0.0);
             const double c = 0.5 * ub, e = std::max(0.5 * ub, 1e-300 * scale);
@@ -576,7 +582,7 @@ void subspace_eig_top(const double* G, int64_t r, int64_t batch, int64_t k, doub
                 const int* zm = w.zmap.as<int>() + (int64_t)j * batch;
                 if (na > 0) {
                     // Z = G Y, P = X^T Y, Z -= X diag(theta_L) P   (columns [cf, b))
-                    if (oz_filter) {
+                    if (oz_filter && !near_floor) {
                         Yd.split(Y + cf * r, r, per, r, bf, r, batch, s, zm, na);
                         ozaki_gemm(Gd, Yd, na, zm, w.Z.d() + cf * r, r, per, s);
                     } else {

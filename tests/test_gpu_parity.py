@@ -968,3 +968,34 @@ def test_ozaki_compress_matches_dmma(engine):
         L.ppc_set_ozaki(1)
     assert np.abs(s_on - s_off).max() <= 1e-10 * np.abs(s_off).max()
     assert (np.abs(s_on - s_off) <= 1e-10 * s_off).all()
+
+
+def test_ozaki_gram_edge_columns(engine):
+    """The INT8 Gram with per-column scales across 1e-300 .. 1e+150 magnitudes,
+    subnormal and all-zero columns, against the FP64 DMMA SYRK."""
+    import torch
+    from paper_2409_19402_b200 import _lib
+    L = _lib.lib()
+    rows, n3 = 1 << 18, 512
+    T = synth.gaussian_device(rows, 1, n3, 9, 1).reshape(rows, n3).clone()
+    scales = torch.logspace(-300, 150, n3, dtype=torch.float64, device="cuda")
+    T = T * scales
+    T[:, 7] = 0.0
+    T[:, 11] = 4.9e-324 * torch.sign(T[:, 11])  # subnormal
+    T = T.T.contiguous().T  # Fortran layout
+    try:
+        assert L.ppc_set_ozaki(1) == 0
+        oz, _ = _gram_parts(L, T, rows, n3)
+        assert L.ppc_set_ozaki(0) == 0
+        dm, _ = _gram_parts(L, T, rows, n3)
+    finally:
+        L.ppc_set_ozaki(1)
+    Go, Gd = oz.sum(0), dm.sum(0)
+    assert torch.isfinite(Go).all()
+    # compare relative to each entry's natural scale sqrt(G_aa G_bb)
+    d = torch.sqrt(torch.clamp(torch.diagonal(Gd), min=0))
+    denom = torch.outer(d, d) + 1e-300
+    rel = ((Go - Gd).abs() / denom)
+    mask = denom > 1e-290
+    assert rel[mask].max().item() <= 1e-13
+    assert (Go[7] == 0).all() and (Go[:, 7] == 0).all()
