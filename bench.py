@@ -207,7 +207,8 @@ class StarQ:
         return self.flops / sec / 1e12
 
     def dominant(self, stages):
-        return "facewise", "tensor"
+        # the facewise product: on the INT8 tensor cores (Ozaki) when eligible
+        return ("ozaki_gemm", "int8") if "ozaki_gemm" in stages else ("facewise", "tensor")
 
     def e2e_setup(self):
         torch = self.torch
@@ -483,7 +484,7 @@ class StarQSharded:
         return self.flops / sec / 1e12 / self.world  # main() multiplies by world
 
     def dominant(self, stages):
-        return "facewise", "tensor"
+        return ("ozaki_gemm", "int8") if "ozaki_gemm" in stages else ("facewise", "tensor")
 
     def e2e_setup(self):
         self.hA = flat_host(self.A)

@@ -9,6 +9,7 @@
 #include "internal.h"
 #include "jacobi.cuh"
 #include "kernels.cuh"
+#include "ozaki.h"
 #include "slice_svd.cuh"
 
 namespace ppc {
@@ -42,13 +43,36 @@ void facewise(const double* A, int64_t n1, int64_t m, int64_t p, const double* B
     gemm(d, s);
 }
 
+namespace {
+
+// The transform-domain facewise product on the INT8 tensor cores (Ozaki):
+// Ch_i = Ah_i Bh_i with Ah_i^T (slice-wise transpose, K = m contiguous) and
+// Bh_i split into digits along m; Bd may carry B's digits from a previous
+// call (host pipeline: one B for every A row block).
+bool facewise_ozaki(const double* Ah, int64_t n1, int64_t m, int64_t p, const double* Bh, int64_t n2, double* Ch,
+                    OzakiDigits& Bd, bool b_ready, cudaStream_t s) {
+    if (!ozaki_gemm_eligible(n1, m) || n2 < 64) return false;
+    StageTimer tm("facewise", s, 2.0 * n1 * m * n2 * p, 8.0 * p * (n1 * m + m * n2 + n1 * n2));
+    DeviceBuffer at(sizeof(double) * n1 * m * p);
+    launch_transpose(Ah, at.d(), n1, m, p, s);  // (m x n1) per slice
+    OzakiDigits Ad;
+    Ad.split(at.d(), m, m * n1, m, n1, m, p, s);
+    if (!b_ready) Bd.split(Bh, m, m * n2, m, n2, m, p, s);
+    ozaki_gemm(Ad, Bd, p, nullptr, Ch, n1, n1 * n2, s);
+    return true;
+}
+
+}  // namespace
+
 void star_q(const double* A, int64_t n1, int64_t m, int64_t n3, const double* B, int64_t n2,
             const double* Q, int64_t p, double scale, double* C, cudaStream_t s) {
     DeviceBuffer ah(sizeof(double) * n1 * m * p), bh(sizeof(double) * m * n2 * p),
         ch(sizeof(double) * n1 * n2 * p);
     mode3(A, n1 * m, n3, Q, p, true, ah.d(), 1.0, s);   // A x3 Q^T
     mode3(B, m * n2, n3, Q, p, true, bh.d(), 1.0, s);   // B x3 Q^T
-    facewise(ah.d(), n1, m, p, bh.d(), n2, ch.d(), s);   // facewise
+    OzakiDigits bd;
+    if (!facewise_ozaki(ah.d(), n1, m, p, bh.d(), n2, ch.d(), bd, false, s))
+        facewise(ah.d(), n1, m, p, bh.d(), n2, ch.d(), s);   // facewise
     mode3(ch.d(), n1 * n2, p, Q, n3, false, C, scale, s);  // x3 Q, scale in the epilogue
 }
 
@@ -95,6 +119,8 @@ void star_q_host(const double* hA, int64_t n1, int64_t m, int64_t n3, const doub
     b.release();
     // 2. A row blocks: H2D (up) -> transforms + facewise (s) -> D2H (down)
     const int64_t BI = std::min<int64_t>(n1, 128);
+    OzakiDigits bd;  // B's digits, split with the first block
+    bool b_ready = false;
     DeviceBuffer ablk[2], ahblk[2], chblk[2], cblk[2];
     Event a_free[2], c_free[2];
     for (int u = 0; u < 2; ++u) {
@@ -116,7 +142,10 @@ void star_q_host(const double* hA, int64_t n1, int64_t m, int64_t n3, const doub
         landed.wait_on(s);
         mode3(ablk[u].d(), bi * m, n3, q.d(), p, true, ahblk[u].d(), 1.0, s);  // A_blk x3 Q^T
         a_free[u].record(s);
-        facewise(ahblk[u].d(), bi, m, p, bh.d(), n2, chblk[u].d(), s);
+        if (facewise_ozaki(ahblk[u].d(), bi, m, p, bh.d(), n2, chblk[u].d(), bd, b_ready, s))
+            b_ready = true;
+        else
+            facewise(ahblk[u].d(), bi, m, p, bh.d(), n2, chblk[u].d(), s);
         c_free[u].wait_on(s);  // block ib-2's C rows are down
         mode3(chblk[u].d(), bi * n2, p, q.d(), n3, false, cblk[u].d(), scale, s);  // x3 Q, scale
         Event done;
