@@ -180,10 +180,28 @@ __device__ __forceinline__ void tri_tile(int64_t t, int64_t mtiles, int64_t& mb,
 }
 
 
+// Work item -> (output block ob, row tile mb, column tile nb).
+template <bool SYM>
+__device__ __forceinline__ void decode_item(const OzParams& P, int64_t item, int64_t& ob, int64_t& mb, int64_t& nb) {
+    const int64_t bi = item / P.tiles;
+    ob = P.zmap ? P.zmap[bi] : bi;
+    if (SYM) {
+        tri_tile(item - bi * P.tiles, P.mtiles, mb, nb);
+    } else {
+        const int64_t t = item - bi * P.tiles;
+        mb = t % P.mtiles;
+        nb = t / P.mtiles;
+    }
+}
+
+// Persistent: CTA c runs items c, c + gridDim.x, ... The producer's stage
+// counter and the MMA / epilogue block counter run on across items, so the
+// next item's operands stream in while the current one is drained; one TMEM
+// allocation serves every item.
 template <bool SYM>
 __global__ void __launch_bounds__(kThreads, 1)
     ozaki_mma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
-                     const OzParams P) {
+                     const OzParams P, int64_t items) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     constexpr int A_TILE = kBM * kBK, B_TILE = kBN * kBK;
@@ -194,17 +212,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* tempty = tfull + 1;
     uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 1);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t item = blockIdx.x;
-    const int64_t bi = item / P.tiles;
-    const int64_t ob = P.zmap ? P.zmap[bi] : bi;
-    int64_t mb, nb;
-    if (SYM) {
-        tri_tile(item - bi * P.tiles, P.mtiles, mb, nb);
-    } else {
-        const int64_t t = item - bi * P.tiles;
-        mb = t % P.mtiles;
-        nb = t / P.mtiles;
-    }
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
             bar_init(&full[s], 1);
@@ -224,115 +231,126 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (warp == 0) {
         if (elect_one()) {
-            const int64_t total = per * nkc;
-            for (int64_t g = 0; g < total; ++g) {
-                const int st = (int)(g % kStages);
-                bar_wait(&empty[st], (uint32_t)(((g / kStages) & 1) ^ 1));
-                bar_expect_tx(&full[st], STAGE);
-                const int64_t blk = ob * per + g / nkc;
-                const int kx = (int)(g % nkc) * kBK;
-                uint8_t* sa = base + st * STAGE;
-                uint8_t* sb = sa + kS * A_TILE;
+            int64_t g = 0;  // stage counter across items
+            for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
+                int64_t ob, mb, nb;
+                decode_item<SYM>(P, item, ob, mb, nb);
+                for (int64_t gl = 0; gl < per * nkc; ++gl, ++g) {
+                    const int st = (int)(g % kStages);
+                    bar_wait(&empty[st], (uint32_t)(((g / kStages) & 1) ^ 1));
+                    bar_expect_tx(&full[st], STAGE);
+                    const int64_t blk = ob * per + gl / nkc;
+                    const int kx = (int)(gl % nkc) * kBK;
+                    uint8_t* sa = base + st * STAGE;
+                    uint8_t* sb = sa + kS * A_TILE;
 #pragma unroll
-                for (int s = 0; s < kS; ++s) {
-                    const int plane = (int)(blk * kS + s);
-                    tma_load_3d(sa + s * A_TILE, &mapA, &full[st], kx, (int)(mb * kBM), plane);
-                    tma_load_3d(sb + s * B_TILE, &mapB, &full[st], kx, (int)(nb * kBN), plane);
+                    for (int s = 0; s < kS; ++s) {
+                        const int plane = (int)(blk * kS + s);
+                        tma_load_3d(sa + s * A_TILE, &mapA, &full[st], kx, (int)(mb * kBM), plane);
+                        tma_load_3d(sb + s * B_TILE, &mapB, &full[st], kx, (int)(nb * kBN), plane);
+                    }
                 }
             }
         }
     } else if (warp == 1) {
         constexpr uint32_t kIdesc = idesc_i8<kBM, kBN>();  // signed digits, S32 accumulate
-        for (int64_t cc = 0; cc < per; ++cc) {
-            if (cc > 0) {  // the epilogue has drained the previous block's levels
-                bar_wait(tempty, (uint32_t)((cc - 1) & 1));
-                fence_after_sync();
-            }
-            for (int kb = 0; kb < nkc; ++kb) {
-                const int64_t g = cc * nkc + kb;
-                const int st = (int)(g % kStages);
-                bar_wait(&full[st], (uint32_t)((g / kStages) & 1));
-                fence_after_sync();
-                if (elect_one()) {
-                    const uint8_t* sa = base + st * STAGE;
-                    const uint8_t* sb = sa + kS * A_TILE;
-#pragma unroll
-                    for (int l = 0; l < kS; ++l) {  // level L = l + 2
-                        const int L = l + 2;
-                        const int s_lo = L - kS > 1 ? L - kS : 1, s_hi = L - 1 < kS ? L - 1 : kS;
-#pragma unroll
-                        for (int s = s_lo; s <= s_hi; ++s) {
-                            const int t = L - s;
-                            const uint64_t da = sdesc_k_sw64(sa + (s - 1) * A_TILE);
-                            const uint64_t db = sdesc_k_sw64(sb + (t - 1) * B_TILE);
-#pragma unroll
-                            for (int kk = 0; kk < kBK / 32; ++kk)
-                                mma_i8(tmem + (uint32_t)(l * kBN), da + (uint64_t)(kk * 2), db + (uint64_t)(kk * 2),
-                                       kIdesc, (kb > 0 || s > s_lo || kk > 0) ? 1u : 0u);
-                        }
-                    }
-                    mma_commit(&empty[st]);
+        int64_t g = 0, cg = 0;  // stage and digit-block counters across items
+        for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
+            for (int64_t cc = 0; cc < per; ++cc, ++cg) {
+                if (cg > 0) {  // the epilogue has drained the previous block's levels
+                    bar_wait(tempty, (uint32_t)((cg - 1) & 1));
+                    fence_after_sync();
                 }
+                for (int kb = 0; kb < nkc; ++kb, ++g) {
+                    const int st = (int)(g % kStages);
+                    bar_wait(&full[st], (uint32_t)((g / kStages) & 1));
+                    fence_after_sync();
+                    if (elect_one()) {
+                        const uint8_t* sa = base + st * STAGE;
+                        const uint8_t* sb = sa + kS * A_TILE;
+#pragma unroll
+                        for (int l = 0; l < kS; ++l) {  // level L = l + 2
+                            const int L = l + 2;
+                            const int s_lo = L - kS > 1 ? L - kS : 1, s_hi = L - 1 < kS ? L - 1 : kS;
+#pragma unroll
+                            for (int s = s_lo; s <= s_hi; ++s) {
+                                const int t = L - s;
+                                const uint64_t da = sdesc_k_sw64(sa + (s - 1) * A_TILE);
+                                const uint64_t db = sdesc_k_sw64(sb + (t - 1) * B_TILE);
+#pragma unroll
+                                for (int kk = 0; kk < kBK / 32; ++kk)
+                                    mma_i8(tmem + (uint32_t)(l * kBN), da + (uint64_t)(kk * 2),
+                                           db + (uint64_t)(kk * 2), kIdesc, (kb > 0 || s > s_lo || kk > 0) ? 1u : 0u);
+                            }
+                        }
+                        mma_commit(&empty[st]);
+                    }
+                    __syncwarp();
+                }
+                if (elect_one()) mma_commit(tfull);
                 __syncwarp();
             }
-            if (elect_one()) mma_commit(tfull);
-            __syncwarp();
         }
     } else {
         // epilogue: warp w drains TMEM lanes 32*(w%4) .. +32 (rows of the
         // tile), columns [h*40, h*40 + 40) with h = (w - 2) / 4
         const int q = warp & 3, h = (warp - 2) >> 2;
         constexpr int NH = kBN / 2;
-        const int64_t m = mb * kBM + q * 32 + lane;
-        const int64_t n0 = nb * kBN + h * NH;
-        double acc[NH];
+        int64_t cg = 0;
+        for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
+            int64_t ob, mb, nb;
+            decode_item<SYM>(P, item, ob, mb, nb);
+            const int64_t m = mb * kBM + q * 32 + lane;
+            const int64_t n0 = nb * kBN + h * NH;
+            double acc[NH];
 #pragma unroll
-        for (int j = 0; j < NH; ++j) acc[j] = 0.0;
-        for (int64_t cc = 0; cc < per; ++cc) {
-            bar_wait(tfull, (uint32_t)(cc & 1));
-            fence_after_sync();
-            const int64_t blk = ob * per + cc;
-            double inner[NH];
+            for (int j = 0; j < NH; ++j) acc[j] = 0.0;
+            for (int64_t cc = 0; cc < per; ++cc, ++cg) {
+                bar_wait(tfull, (uint32_t)(cg & 1));
+                fence_after_sync();
+                const int64_t blk = ob * per + cc;
+                double inner[NH];
 #pragma unroll
-            for (int j = 0; j < NH; ++j) inner[j] = 0.0;
+                for (int j = 0; j < NH; ++j) inner[j] = 0.0;
 #pragma unroll 1
-            for (int l = kS - 1; l >= 0; --l) {  // smallest weight first
-                const double w = ldexp(1.0, -14 - 8 * l);
-                const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(l * kBN + h * NH);
-                int32_t v[32];
-                tmem_ld_32x32b_x32(ta, v);
-                int32_t v8[8];
-                tmem_ld_32x32b_x8(ta + 32, v8);
-                tmem_ld_wait();
+                for (int l = kS - 1; l >= 0; --l) {  // smallest weight first
+                    const double w = ldexp(1.0, -14 - 8 * l);
+                    const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(l * kBN + h * NH);
+                    int32_t v[32];
+                    tmem_ld_32x32b_x32(ta, v);
+                    int32_t v8[8];
+                    tmem_ld_32x32b_x8(ta + 32, v8);
+                    tmem_ld_wait();
 #pragma unroll
-                for (int j = 0; j < 32; ++j) inner[j] = fma((double)v[j], w, inner[j]);
+                    for (int j = 0; j < 32; ++j) inner[j] = fma((double)v[j], w, inner[j]);
 #pragma unroll
-                for (int j = 0; j < 8; ++j) inner[32 + j] = fma((double)v8[j], w, inner[32 + j]);
+                    for (int j = 0; j < 8; ++j) inner[32 + j] = fma((double)v8[j], w, inner[32 + j]);
+                }
+                fence_before_sync();
+                __syncwarp();
+                if (lane == 0) bar_arrive(tempty);  // the MMAs may overwrite the levels
+                const double sm = m < P.M ? P.sa[blk * P.M + m] : 0.0;
+                const double* sc = P.sb + blk * P.N;
+#pragma unroll
+                for (int j = 0; j < NH; ++j) {
+                    const int64_t n = n0 + j;
+                    // the diagonal of a Gram from the FP64 sums of squares: its
+                    // dropped same-digit pair products are squares (biased > 0)
+                    if (SYM && n == m)
+                        acc[j] += P.sq[blk * P.M + m];
+                    else
+                        acc[j] = fma(inner[j] * sm, n < P.N ? sc[n] : 0.0, acc[j]);
+                }
             }
-            fence_before_sync();
-            __syncwarp();
-            if (lane == 0) bar_arrive(tempty);  // the MMAs may overwrite the levels
-            const double sm = m < P.M ? P.sa[blk * P.M + m] : 0.0;
-            const double* sc = P.sb + blk * P.N;
-#pragma unroll
-            for (int j = 0; j < NH; ++j) {
-                const int64_t n = n0 + j;
-                // the diagonal of a Gram from the FP64 sums of squares: its
-                // dropped same-digit pair products are squares (biased > 0)
-                if (SYM && n == m)
-                    acc[j] += P.sq[blk * P.M + m];
-                else
-                    acc[j] = fma(inner[j] * sm, n < P.N ? sc[n] : 0.0, acc[j]);
-            }
-        }
-        if (m < P.M) {
-            double* C = P.C + ob * P.strideC;
+            if (m < P.M) {
+                double* C = P.C + ob * P.strideC;
 #pragma unroll 4
-            for (int j = 0; j < NH; ++j) {
-                const int64_t n = n0 + j;
-                if (n >= P.N) break;
-                C[m + n * P.ldc] = acc[j];           // (m, n), coalesced over the warp's rows
-                if (SYM) C[n + m * P.ldc] = acc[j];  // mirror (n, m): the same exact integer sums
+                for (int j = 0; j < NH; ++j) {
+                    const int64_t n = n0 + j;
+                    if (n >= P.N) break;
+                    C[m + n * P.ldc] = acc[j];           // (m, n), coalesced over the warp's rows
+                    if (SYM) C[n + m * P.ldc] = acc[j];  // mirror (n, m): the same exact integer sums
+                }
             }
         }
     }
@@ -387,9 +405,9 @@ void launch_mma(const CUtensorMap& ma, const CUtensorMap& mb, const OzParams& P,
         PPC_CUDA_CHECK(cudaFuncSetAttribute(ozaki_mma_kernel<SYM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = true;
     }
-    if (items > 0x7fffffffLL) fail(PPC_ARGUMENT, "ozaki: too many tiles");
     if (items == 0) return;
-    ozaki_mma_kernel<SYM><<<(unsigned)items, kThreads, smem, s>>>(ma, mb, P);
+    const int64_t grid = std::min<int64_t>(items, ctx().sms);  // one persistent CTA per SM
+    ozaki_mma_kernel<SYM><<<(unsigned)grid, kThreads, smem, s>>>(ma, mb, P, items);
     count_launch();
     check_launch("ozaki_mma");
 }
