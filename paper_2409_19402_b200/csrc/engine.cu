@@ -248,6 +248,10 @@ std::array<double, 2> recon_residual(const double* A, int64_t n1, int64_t n2, in
     StageTimer tm("recon_residual", s, 2.0 * p * N * k + 2.0 * N * p * n3, 8.0 * N * (p + n3));
     DeviceBuffer ch(sizeof(double) * N * p);
     core_from_factors(U, S, V, n1, n2, p, k, ch.d(), s, kstride);
+    {
+        std::array<double, 2> oz{};
+        if (ozaki_recon_residual(A, N, n3, ch.d(), Q, p, oz.data(), s)) return oz;
+    }
     GemmDesc d;
     d.M = N; d.N = n3; d.K = p;
     d.A = ch.d(); d.lda = N;

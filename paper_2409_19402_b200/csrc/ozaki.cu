@@ -37,6 +37,7 @@
 #include <mutex>
 
 #include "internal.h"
+#include "kernels.cuh"
 #include "ozaki.h"
 #include "umma_i8.cuh"
 
@@ -164,6 +165,12 @@ struct OzParams {
     const double* sq;      // SYM: column sums of squares [digit block][M] (the diagonal)
     double* C;             // output block ob at C + ob*strideC, (m, n) at m + n*ldc
     int64_t ldc, strideC;
+    // RESID: instead of C, per-CTA sums {(X - C)^2, X^2} into partial[2*cta]
+    // with X block ob at X + ob*strideX, (m, n) at m + n*ldx, rows
+    // ob*M + m < m_total
+    const double* X;
+    int64_t ldx, strideX, m_total;
+    double* partial;
 };
 
 // tile t (upper-triangle order) -> (mb, nb): column tile nb holds
@@ -197,8 +204,9 @@ __device__ __forceinline__ void decode_item(const OzParams& P, int64_t item, int
 // Persistent: CTA c runs items c, c + gridDim.x, ... The producer's stage
 // counter and the MMA / epilogue block counter run on across items, so the
 // next item's operands stream in while the current one is drained; one TMEM
-// allocation serves every item.
-template <bool SYM>
+// allocation serves every item. AMN: the A digits are MN-major ([plane][k][m],
+// m contiguous), loaded as two 64-byte x 64-row boxes per digit (LBO 4096 B).
+template <bool SYM, bool AMN, bool RESID>
 __global__ void __launch_bounds__(kThreads, 1)
     ozaki_mma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                      const OzParams P, int64_t items) {
@@ -246,14 +254,20 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int s = 0; s < kS; ++s) {
                         const int plane = (int)(blk * kS + s);
-                        tma_load_3d(sa + s * A_TILE, &mapA, &full[st], kx, (int)(mb * kBM), plane);
+                        if (AMN) {
+                            tma_load_3d(sa + s * A_TILE, &mapA, &full[st], (int)(mb * kBM), kx, plane);
+                            tma_load_3d(sa + s * A_TILE + 4096, &mapA, &full[st], (int)(mb * kBM + 64), kx, plane);
+                        } else {
+                            tma_load_3d(sa + s * A_TILE, &mapA, &full[st], kx, (int)(mb * kBM), plane);
+                        }
                         tma_load_3d(sb + s * B_TILE, &mapB, &full[st], kx, (int)(nb * kBN), plane);
                     }
                 }
             }
         }
     } else if (warp == 1) {
-        constexpr uint32_t kIdesc = idesc_i8<kBM, kBN>();  // signed digits, S32 accumulate
+        // signed digits, S32 accumulate; A MN-major for AMN
+        constexpr uint32_t kIdesc = idesc_i8<kBM, kBN>() | (AMN ? (1u << 15) : 0u);
         int64_t g = 0, cg = 0;  // stage and digit-block counters across items
         for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
             for (int64_t cc = 0; cc < per; ++cc, ++cg) {
@@ -275,12 +289,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                             for (int s = s_lo; s <= s_hi; ++s) {
                                 const int t = L - s;
-                                const uint64_t da = sdesc_k_sw64(sa + (s - 1) * A_TILE);
                                 const uint64_t db = sdesc_k_sw64(sb + (t - 1) * B_TILE);
 #pragma unroll
-                                for (int kk = 0; kk < kBK / 32; ++kk)
-                                    mma_i8(tmem + (uint32_t)(l * kBN), da + (uint64_t)(kk * 2),
-                                           db + (uint64_t)(kk * 2), kIdesc, (kb > 0 || s > s_lo || kk > 0) ? 1u : 0u);
+                                for (int kk = 0; kk < kBK / 32; ++kk) {
+                                    const uint64_t da = AMN ? sdesc_mn_sw64(sa + (s - 1) * A_TILE + kk * 2048, 4096)
+                                                            : sdesc_k_sw64(sa + (s - 1) * A_TILE) + (uint64_t)(kk * 2);
+                                    mma_i8(tmem + (uint32_t)(l * kBN), da, db + (uint64_t)(kk * 2), kIdesc,
+                                           (kb > 0 || s > s_lo || kk > 0) ? 1u : 0u);
+                                }
                             }
                         }
                         mma_commit(&empty[st]);
@@ -297,65 +313,129 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int q = warp & 3, h = (warp - 2) >> 2;
         constexpr int NH = kBN / 2;
         int64_t cg = 0;
+        double rsd = 0.0, rsx = 0.0;  // RESID: this thread's residual sums
         for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
             int64_t ob, mb, nb;
             decode_item<SYM>(P, item, ob, mb, nb);
             const int64_t m = mb * kBM + q * 32 + lane;
             const int64_t n0 = nb * kBN + h * NH;
-            double acc[NH];
+            const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(h * NH);
+            if constexpr (!SYM) {
+                // one digit block per item (per == 1): each 8-column chunk goes
+                // straight from TMEM to C (or into the residual sums)
+                const bool xrow = RESID && m < P.M && ob * P.M + m < P.m_total;
+                double xv[RESID ? NH : 1];
+                if constexpr (RESID) {  // X loads in flight while the MMAs run
+                    const double* X = P.X + ob * P.strideX + m;
 #pragma unroll
-            for (int j = 0; j < NH; ++j) acc[j] = 0.0;
-            for (int64_t cc = 0; cc < per; ++cc, ++cg) {
+                    for (int j = 0; j < NH; ++j) xv[j] = xrow && n0 + j < P.N ? __ldcs(X + (n0 + j) * P.ldx) : 0.0;
+                }
                 bar_wait(tfull, (uint32_t)(cg & 1));
                 fence_after_sync();
-                const int64_t blk = ob * per + cc;
-                double inner[NH];
+                const double sm = m < P.M ? (P.sa ? P.sa[ob * P.M + m] : 1.0) : 0.0;
+                const double* sc = P.sb + ob * P.N;
+                double* C = RESID ? nullptr : P.C + ob * P.strideC;
 #pragma unroll
-                for (int j = 0; j < NH; ++j) inner[j] = 0.0;
-#pragma unroll 1
-                for (int l = kS - 1; l >= 0; --l) {  // smallest weight first
-                    const double w = ldexp(1.0, -14 - 8 * l);
-                    const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(l * kBN + h * NH);
-                    int32_t v[32];
-                    tmem_ld_32x32b_x32(ta, v);
-                    int32_t v8[8];
-                    tmem_ld_32x32b_x8(ta + 32, v8);
+                for (int c = 0; c < NH / 8; ++c) {  // all six levels of 8 columns in flight
+                    int32_t v[kS][8];
+#pragma unroll
+                    for (int l = 0; l < kS; ++l) tmem_ld_32x32b_x8(ta + (uint32_t)(l * kBN + c * 8), v[l]);
                     tmem_ld_wait();
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) inner[j] = fma((double)v[j], w, inner[j]);
+                    for (int jj = 0; jj < 8; ++jj) {
+                        const int j = c * 8 + jj;
+                        const int64_t n = n0 + j;
+                        double inner = 0.0;
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) inner[32 + j] = fma((double)v8[j], w, inner[32 + j]);
+                        for (int l = kS - 1; l >= 0; --l)  // smallest weight first
+                            inner = fma((double)v[l][jj], ldexp(1.0, -14 - 8 * l), inner);
+                        const double val = (inner * sm) * (n < P.N ? sc[n] : 0.0);
+                        if constexpr (RESID) {  // columns past N: x = val = 0
+                            const double r = xv[j] - val;
+                            rsd = fma(r, r, rsd);
+                            rsx = fma(xv[j], xv[j], rsx);
+                        } else if (m < P.M && n < P.N) {
+                            C[m + n * P.ldc] = val;  // (m, n), coalesced over the warp's rows
+                        }
+                    }
                 }
                 fence_before_sync();
                 __syncwarp();
                 if (lane == 0) bar_arrive(tempty);  // the MMAs may overwrite the levels
-                const double sm = m < P.M ? P.sa[blk * P.M + m] : 0.0;
-                const double* sc = P.sb + blk * P.N;
+                ++cg;
+            } else {
+                double acc[NH];
 #pragma unroll
-                for (int j = 0; j < NH; ++j) {
-                    const int64_t n = n0 + j;
-                    // the diagonal of a Gram from the FP64 sums of squares: its
-                    // dropped same-digit pair products are squares (biased > 0)
-                    if (SYM && n == m)
-                        acc[j] += P.sq[blk * P.M + m];
-                    else
-                        acc[j] = fma(inner[j] * sm, n < P.N ? sc[n] : 0.0, acc[j]);
+                for (int j = 0; j < NH; ++j) acc[j] = 0.0;
+                for (int64_t cc = 0; cc < per; ++cc, ++cg) {
+                    bar_wait(tfull, (uint32_t)(cg & 1));
+                    fence_after_sync();
+                    const int64_t blk = ob * per + cc;
+                    const double sm = m < P.M ? P.sa[blk * P.M + m] : 0.0;
+                    const double* sc = P.sb + blk * P.N;
+#pragma unroll
+                    for (int c = 0; c < NH / 8; ++c) {
+                        int32_t v[kS][8];
+#pragma unroll
+                        for (int l = 0; l < kS; ++l) tmem_ld_32x32b_x8(ta + (uint32_t)(l * kBN + c * 8), v[l]);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int jj = 0; jj < 8; ++jj) {
+                            const int j = c * 8 + jj;
+                            const int64_t n = n0 + j;
+                            double inner = 0.0;
+#pragma unroll
+                            for (int l = kS - 1; l >= 0; --l)
+                                inner = fma((double)v[l][jj], ldexp(1.0, -14 - 8 * l), inner);
+                            // the diagonal of a Gram from the FP64 sums of squares: its
+                            // dropped same-digit pair products are squares (biased > 0)
+                            if (n == m)
+                                acc[j] += P.sq[blk * P.M + m];
+                            else
+                                acc[j] = fma(inner * sm, n < P.N ? sc[n] : 0.0, acc[j]);
+                        }
+                    }
+                    fence_before_sync();
+                    __syncwarp();
+                    if (lane == 0) bar_arrive(tempty);
+                }
+                if (m < P.M) {
+                    double* C = P.C + ob * P.strideC;
+#pragma unroll
+                    for (int j = 0; j < NH; ++j) {  // fully unrolled: acc stays in registers
+                        const int64_t n = n0 + j;
+                        if (n < P.N) {
+                            C[m + n * P.ldc] = acc[j];  // (m, n), coalesced over the warp's rows
+                            C[n + m * P.ldc] = acc[j];  // mirror (n, m): the same exact integer sums
+                        }
+                    }
                 }
             }
-            if (m < P.M) {
-                double* C = P.C + ob * P.strideC;
-#pragma unroll 4
-                for (int j = 0; j < NH; ++j) {
-                    const int64_t n = n0 + j;
-                    if (n >= P.N) break;
-                    C[m + n * P.ldc] = acc[j];           // (m, n), coalesced over the warp's rows
-                    if (SYM) C[n + m * P.ldc] = acc[j];  // mirror (n, m): the same exact integer sums
-                }
+        }
+        if (RESID) {  // fixed-order warp sums -> shared memory
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                rsd += __shfl_xor_sync(0xffffffffu, rsd, o);
+                rsx += __shfl_xor_sync(0xffffffffu, rsx, o);
+            }
+            if (lane == 0) {
+                reinterpret_cast<double*>(tslot + 2)[2 * (warp - 2)] = rsd;
+                reinterpret_cast<double*>(tslot + 2)[2 * (warp - 2) + 1] = rsx;
             }
         }
     }
     fence_before_sync();
     __syncthreads();
+    if (RESID && threadIdx.x == 0) {  // fixed-order CTA sum of the epilogue warps
+        const double* ws = reinterpret_cast<const double*>(tslot + 2);
+        double sd = 0.0, sx = 0.0;
+        for (int w = 0; w < kEpiWarps; ++w) {
+            sd += ws[2 * w];
+            sx += ws[2 * w + 1];
+        }
+        P.partial[2 * blockIdx.x] = sd;
+        P.partial[2 * blockIdx.x + 1] = sx;
+    }
     if (warp == 1) tmem_free<512>(tmem);
 }
 
@@ -397,17 +477,20 @@ bool ozaki_enabled() {
     return v == 1;
 }
 
-template <bool SYM>
+int64_t ozaki_grid(int64_t items) { return std::min<int64_t>(items, ctx().sms); }  // one persistent CTA per SM
+
+template <bool SYM, bool AMN = false, bool RESID = false>
 void launch_mma(const CUtensorMap& ma, const CUtensorMap& mb, const OzParams& P, int64_t items, cudaStream_t s) {
-    const size_t smem = 1024 + (size_t)kStages * kS * (kBM + kBN) * kBK + (2 * kStages + 2) * 8 + 16;
+    // stages + barriers + TMEM slot + the epilogue warps' residual sums
+    const size_t smem = 1024 + (size_t)kStages * kS * (kBM + kBN) * kBK + (2 * kStages + 2) * 8 + 16 + 16 * kEpiWarps;
     static bool attr = false;
     if (!attr) {
-        PPC_CUDA_CHECK(cudaFuncSetAttribute(ozaki_mma_kernel<SYM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        PPC_CUDA_CHECK(cudaFuncSetAttribute(ozaki_mma_kernel<SYM, AMN, RESID>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = true;
     }
     if (items == 0) return;
-    const int64_t grid = std::min<int64_t>(items, ctx().sms);  // one persistent CTA per SM
-    ozaki_mma_kernel<SYM><<<(unsigned)grid, kThreads, smem, s>>>(ma, mb, P, items);
+    ozaki_mma_kernel<SYM, AMN, RESID><<<(unsigned)ozaki_grid(items), kThreads, smem, s>>>(ma, mb, P, items);
     count_launch();
     check_launch("ozaki_mma");
 }
@@ -440,6 +523,9 @@ void ozaki_syrk(const OzakiDigits& d, int64_t nout, int64_t per, double* out, cu
     P.C = out;
     P.ldc = d.cols;
     P.strideC = d.cols * d.cols;
+    P.X = nullptr;
+    P.ldx = P.strideX = P.m_total = 0;
+    P.partial = nullptr;
     // int8 ops of the 21 digit-pair products over the upper triangle
     StageTimer tk(stage, s, 2.0 * kS * (kS + 1) / 2 * rows_total * d.cols * d.cols / 2,
                   (double)kS * rows_total * d.cols);
@@ -492,6 +578,9 @@ void ozaki_gemm(const OzakiDigits& A, const OzakiDigits& B, int64_t nbatch, cons
     P.C = C;
     P.ldc = ldc;
     P.strideC = strideC;
+    P.X = nullptr;
+    P.ldx = P.strideX = P.m_total = 0;
+    P.partial = nullptr;
     const double K = (double)std::min(A.rows, kKC);
     StageTimer tk("ozaki_gemm", s, 2.0 * kS * (kS + 1) / 2 * (double)nbatch * P.M * P.N * K,
                   (double)kS * nbatch * (P.M + P.N) * K);
@@ -499,6 +588,72 @@ void ozaki_gemm(const OzakiDigits& A, const OzakiDigits& B, int64_t nbatch, cons
 }
 
 bool ozaki_gemm_eligible(int64_t M, int64_t K) { return ozaki_enabled() && M >= kBM && K >= 256 && K <= kKC; }
+
+namespace {
+
+// Bt[c] (p x n3, column-major) = diag(sigma_c) Q^T: the per-(row block,
+// slice) scales of the core's digits folded into the transform.
+__global__ void fold_qt_kernel(const double* __restrict__ sc, const double* __restrict__ Q, int64_t n3, int64_t p,
+                               int64_t total, double* __restrict__ Bt) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
+        const int64_t c = i / (p * n3), r = i - c * p * n3, n = r % p, j = r / p;
+        Bt[i] = sc[c * p + n] * Q[j + n * n3];
+    }
+}
+
+}  // namespace
+
+bool ozaki_recon_residual(const double* X, int64_t N, int64_t n3, const double* Ch, const double* Q, int64_t p,
+                          double sums[2], cudaStream_t s) {
+    if (!ozaki_enabled() || n3 < kBN || p < 32 || p > kKC || N < kKC) return false;
+    const int64_t nblk = (N + kKC - 1) / kKC;
+    // A = the core's digits per (4096-row block, slice), read MN-major
+    OzakiDigits cd, bd;
+    cd.split(Ch, N, 0, N, p, kKC, nblk, s, nullptr, 0, kKC, 1);
+    DeviceBuffer bt(sizeof(double) * nblk * p * n3);
+    {
+        const int64_t total = nblk * p * n3;
+        fold_qt_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, 148 * 16), 256, 0, s>>>(cd.sc.d(), Q, n3, p,
+                                                                                               total, bt.d());
+        count_launch();
+        check_launch("fold_qt");
+    }
+    bd.split(bt.d(), p, p * n3, p, n3, p, nblk, s);
+    CUtensorMap ma, mb;
+    if (!make_digit_map(&ma, cd.D.as<int8_t>(), cd.KCp, p, nblk * kS, 64) ||
+        !make_digit_map(&mb, bd.D.as<int8_t>(), bd.KCp, n3, nblk * kS, kBN))
+        fail(PPC_CUDA, "ozaki: tensor map encoding failed");
+    OzParams P;
+    P.M = kKC;
+    P.N = n3;
+    P.mtiles = kKC / kBM;
+    P.tiles = P.mtiles * ((n3 + kBN - 1) / kBN);
+    P.KCp = bd.KCp;  // the K extent: p, padded
+    P.per = 1;
+    P.zmap = nullptr;
+    P.sa = nullptr;  // folded into Bt
+    P.sb = bd.sc.d();
+    P.sq = nullptr;
+    P.C = nullptr;
+    P.ldc = P.strideC = 0;
+    P.X = X;
+    P.ldx = N;
+    P.strideX = kKC;
+    P.m_total = N;
+    const int64_t items = nblk * P.tiles, grid = ozaki_grid(items);
+    DeviceBuffer part(sizeof(double) * 2 * (grid + 1));
+    P.partial = part.d();
+    {
+        StageTimer tk("ozaki_resid", s, 2.0 * kS * (kS + 1) / 2 * (double)N * n3 * p, 8.0 * N * n3);
+        launch_mma<false, true, true>(ma, mb, P, items, s);
+    }
+    double* fin = part.d() + 2 * grid;
+    launch_reduce_pairs(part.d(), grid, fin, s);
+    PPC_CUDA_CHECK(cudaMemcpyAsync(sums, fin, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    PPC_CUDA_CHECK(cudaStreamSynchronize(s));
+    return true;
+}
 
 bool ozaki_gram_partials(const double* T, int64_t ldT, int64_t rows, int64_t n3, int64_t chunk, int64_t nchunks,
                          double* parts, cudaStream_t s) {

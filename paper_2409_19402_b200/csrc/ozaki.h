@@ -29,6 +29,13 @@ void ozaki_gemm(const OzakiDigits& A, const OzakiDigits& B, int64_t nbatch, cons
 // Whether the integer path applies to an output with M rows and K-length sums.
 bool ozaki_gemm_eligible(int64_t M, int64_t K);
 
+// {||X - Ch Q^T||^2, ||X||^2} for X (N x n3, leading dimension N), the
+// reconstruction core Ch (N x p) and the basis Q (n3 x p): the core's digits
+// per (4096-row block, slice) read MN-major, the scales folded into Q^T, a
+// residual epilogue on the INT8 tensor cores. false when not eligible.
+bool ozaki_recon_residual(const double* X, int64_t N, int64_t n3, const double* Ch, const double* Q, int64_t p,
+                          double sums[2], cudaStream_t s);
+
 // Per-plan-chunk partial Grams parts[c] = T_c^T T_c (nchunks x n3 x n3) of a
 // tube matrix T (rows x n3, leading dimension ldT), as gram_partials, through
 // 8-bit digit splitting and tcgen05 kind::i8 MMAs. Returns false when the

@@ -123,6 +123,20 @@ __device__ __forceinline__ uint64_t sdesc_k_sw64(const void* smem_tile) {
     return d;
 }
 
+// MN-major operand (contiguous M/N) in 64-byte SWIZZLE_64B atoms: 64 M
+// bytes x 8 K rows per 512-byte atom; K groups SBO = 512 B apart, M atoms
+// LBO apart. A 32-row K slice is a +2048 B start-address step.
+__device__ __forceinline__ uint64_t sdesc_mn_sw64(const void* smem_tile, uint32_t lbo_bytes) {
+    const uint32_t a = smem_u32(smem_tile);
+    uint64_t d = 0;
+    d |= (uint64_t)((a >> 4) & 0x3FFF);
+    d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)(512 >> 4) << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)4 << 61;
+    return d;
+}
+
 // Instruction descriptor: kind::i8, signed A and B, S32 accumulate, both
 // K-major, M x N.
 template <int M, int N>
