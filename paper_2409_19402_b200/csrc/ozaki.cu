@@ -27,8 +27,8 @@
 // Kernels: ozaki_split_kernel (one CTA per (block, column), block staged in
 // shared memory: one HBM read), ozaki_mma_kernel (one TMA producer warp, one
 // MMA-issuing warp, eight epilogue warps; TMA SWIZZLE_64B tiles of all six
-// digit planes of A (128 rows) and B (80 rows) per 64-byte K stage, 42 MMAs
-// of 128x80x32 per stage).
+// digit planes of A (128 rows) and B (80 rows) per 64-byte K stage, 20 MMAs
+// of 128 x {80,160,240} x 32 per stage).
 #include <cudaTypedefs.h>
 
 #include <algorithm>
@@ -266,8 +266,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp == 1) {
-        // signed digits, S32 accumulate; A MN-major for AMN
-        constexpr uint32_t kIdesc = idesc_i8<kBM, kBN>() | (AMN ? (1u << 15) : 0u);
+        // signed digits, S32 accumulate; A MN-major for AMN. The B digit tiles
+        // sit back to back in shared memory (one 80-row K-major matrix per
+        // digit, same 512-byte atom stride), so digit i of A meets up to three
+        // consecutive B digits j0..j0+2 in one MMA of N = 80 (j1 - j0 + 1): its
+        // columns land exactly on the level accumulators i+j0 .. i+j1. 10 MMAs
+        // per 32-byte k-slice instead of 21, each A tile read from shared memory
+        // once per 240 columns instead of once per 80.
+        constexpr uint32_t kAmn = AMN ? (1u << 15) : 0u;
+        constexpr uint32_t kIdesc1 = idesc_i8<kBM, kBN>() | kAmn;
+        constexpr uint32_t kIdesc2 = idesc_i8<kBM, 2 * kBN>() | kAmn;
+        constexpr uint32_t kIdesc3 = idesc_i8<kBM, 3 * kBN>() | kAmn;
         int64_t g = 0, cg = 0;  // stage and digit-block counters across items
         for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
             for (int64_t cc = 0; cc < per; ++cc, ++cg) {
@@ -283,19 +292,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const uint8_t* sa = base + st * STAGE;
                         const uint8_t* sb = sa + kS * A_TILE;
 #pragma unroll
-                        for (int l = 0; l < kS; ++l) {  // level L = l + 2
-                            const int L = l + 2;
-                            const int s_lo = L - kS > 1 ? L - kS : 1, s_hi = L - 1 < kS ? L - 1 : kS;
+                        for (int kk = 0; kk < kBK / 32; ++kk) {
+                            // digit 1 of A spans every level: its MMAs start the block
+                            const uint32_t acc0 = (kb > 0 || kk > 0) ? 1u : 0u;
 #pragma unroll
-                            for (int s = s_lo; s <= s_hi; ++s) {
-                                const int t = L - s;
-                                const uint64_t db = sdesc_k_sw64(sb + (t - 1) * B_TILE);
+                            for (int i = 1; i <= kS; ++i) {
+                                const uint64_t da = AMN ? sdesc_mn_sw64(sa + (i - 1) * A_TILE + kk * 2048, 4096)
+                                                        : sdesc_k_sw64(sa + (i - 1) * A_TILE) + (uint64_t)(kk * 2);
+                                const int jmax = kS + 1 - i;  // levels i + j <= S + 1
 #pragma unroll
-                                for (int kk = 0; kk < kBK / 32; ++kk) {
-                                    const uint64_t da = AMN ? sdesc_mn_sw64(sa + (s - 1) * A_TILE + kk * 2048, 4096)
-                                                            : sdesc_k_sw64(sa + (s - 1) * A_TILE) + (uint64_t)(kk * 2);
-                                    mma_i8(tmem + (uint32_t)(l * kBN), da, db + (uint64_t)(kk * 2), kIdesc,
-                                           (kb > 0 || s > s_lo || kk > 0) ? 1u : 0u);
+                                for (int j0 = 1; j0 <= jmax; j0 += 3) {
+                                    const int nj = jmax - j0 + 1 < 3 ? jmax - j0 + 1 : 3;
+                                    const uint32_t idesc = nj == 3 ? kIdesc3 : (nj == 2 ? kIdesc2 : kIdesc1);
+                                    const uint64_t db = sdesc_k_sw64(sb + (j0 - 1) * B_TILE) + (uint64_t)(kk * 2);
+                                    mma_i8(tmem + (uint32_t)((i + j0 - 2) * kBN), da, db, idesc, i == 1 ? acc0 : 1u);
                                 }
                             }
                         }
