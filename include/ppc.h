@@ -65,6 +65,10 @@ int ppc_set_device(int device);
 int ppc_set_stream(void* stream);
 void* ppc_get_stream(void);
 int ppc_synchronize(void);
+/* Release this thread's cached large device workspaces (blocks >= 256 MB that
+ * the library keeps between calls of the same shapes) on the current device.
+ * Engine extension: the CPU reference has no device memory to trim. */
+int ppc_trim_workspace(void);
 /* Kernel launches issued by the library on this thread since the last reset
  * (for the bench's gpu_launches count). */
 int64_t ppc_launch_count(int reset);

@@ -46,6 +46,7 @@ def lib() -> C.CDLL:
         "ppc_set_stream": (C.c_int, [vp]),
         "ppc_get_stream": (vp, []),
         "ppc_synchronize": (C.c_int, []),
+        "ppc_trim_workspace": (C.c_int, []),
         "ppc_launch_count": (i64, [C.c_int]),
         "ppc_timing_enable": (C.c_int, [C.c_int]),
         "ppc_set_gemm_path": (C.c_int, [C.c_int]),

@@ -171,10 +171,9 @@ int ppc_data_dependent_q(const double* A, int64_t n1, int64_t n2, int64_t n3, in
         cudaStream_t s = stream();
         const int64_t N = n1 * n2;
         In a(A, N * n3, loc);
-        require_finite(a.d, N * n3, "svd", s);
         Out q(Q, n3 * p, loc);
         Out sg(sigma, sigma ? p : 0, loc);
-        const bool comp = data_q(a.d, N, n3, p, q.d, sigma ? sg.d : nullptr, s);
+        const bool comp = data_q(a.d, N, n3, p, q.d, sigma ? sg.d : nullptr, s, true);
         if (completed) *completed = comp ? 1 : 0;
         q.finish();
         if (sigma) sg.finish();
@@ -517,16 +516,16 @@ int ppc_tsvdq_sweep(const double* A, int64_t n1, int64_t n2, int64_t n3, const i
         cudaStream_t s = stream();
         const int64_t N = n1 * n2;
         In a(A, N * n3, loc);
-        require_finite(a.d, N * n3, "svd", s);
         DeviceBuffer qbuf;
         const double* dQ;
         if (Q) {
+            require_finite(a.d, N * n3, "svd", s);
             In qi(Q, n3 * pmax, loc);
             qbuf = DeviceBuffer(sizeof(double) * n3 * pmax);
             PPC_CUDA_CHECK(cudaMemcpyAsync(qbuf.d(), qi.d, sizeof(double) * n3 * pmax, cudaMemcpyDeviceToDevice, s));
         } else {
             qbuf = DeviceBuffer(sizeof(double) * n3 * pmax);
-            data_q(a.d, N, n3, pmax, qbuf.d(), nullptr, s);
+            data_q(a.d, N, n3, pmax, qbuf.d(), nullptr, s, true);
         }
         dQ = qbuf.d();
         sweep_errors(a.d, n1, n2, n3, dQ, pmax, kmax, ps, np, ks, nk, re, s);
@@ -568,6 +567,8 @@ int ppc_tsvdq_compress(const double* A, int64_t n1, int64_t n2, int64_t n3, int6
                 PPC_CUDA_CHECK(cudaStreamWaitEvent(cs, ready, 0));
                 PPC_CUDA_CHECK(cudaEventDestroy(ready));
             }
+            FiniteFlag nf(s);
+            bool checked = true;  // every slab's Gram pass also checked finiteness
             {
                 StageTimer tm("gram_syrk", s, (double)N * n3 * n3, 8.0 * N * n3);
                 for (int64_t c0 = 0; c0 < g.chunks; c0 += per) {
@@ -585,16 +586,18 @@ int ppc_tsvdq_compress(const double* A, int64_t n1, int64_t n2, int64_t n3, int6
                     PPC_CUDA_CHECK(cudaEventRecord(ev, cs));
                     PPC_CUDA_CHECK(cudaStreamWaitEvent(s, ev, 0));
                     PPC_CUDA_CHECK(cudaEventDestroy(ev));
-                    gram_chunks(abuf.d() + r0, N, nr, n3, g.chunk, std::min(per, g.chunks - c0),
-                                parts.d() + c0 * n3 * n3, s);
+                    checked &= gram_chunks(abuf.d() + r0, N, nr, n3, g.chunk, std::min(per, g.chunks - c0),
+                                           parts.d() + c0 * n3 * n3, s, nf.d());
                 }
                 tree_reduce(parts.d(), g.chunks, n3 * n3, s);
             }
-            require_finite(dA, N * n3, "svd", s);
+            if (checked)
+                nf.check(s, "svd");
+            else
+                require_finite(dA, N * n3, "svd", s);
             eig_to_basis(parts.d(), n3, p, q.d, sigma ? sg.d : nullptr, s);
         } else {
-            require_finite(dA, N * n3, "svd", s);
-            data_q(dA, N, n3, p, q.d, sigma ? sg.d : nullptr, s);
+            data_q(dA, N, n3, p, q.d, sigma ? sg.d : nullptr, s, true);
         }
         tsvdq(dA, n1, n2, n3, q.d, p, k, u.d, sv.d, v.d, s);
         const auto r = recon_residual(dA, n1, n2, n3, u.d, sv.d, v.d, q.d, p, k, s);

@@ -202,13 +202,9 @@ std::array<double, 2> projection_residual(const double* T, int64_t N, int64_t n3
 }
 
 void require_finite(const double* x, int64_t n, const char* who, cudaStream_t s) {
-    DeviceBuffer flag(sizeof(int) * 2);
-    PPC_CUDA_CHECK(cudaMemsetAsync(flag.as<int>(), 0, sizeof(int), s));
-    launch_nonfinite(x, n, flag.as<int>(), s);
-    int h = 0;
-    PPC_CUDA_CHECK(cudaMemcpyAsync(&h, flag.as<int>(), sizeof(int), cudaMemcpyDeviceToHost, s));
-    PPC_CUDA_CHECK(cudaStreamSynchronize(s));
-    if (h) fail(PPC_NUMERIC, std::string(who) + ": input has non-finite entries");
+    FiniteFlag nf(s);
+    launch_nonfinite(x, n, nf.d(), s);
+    nf.check(s, who);
 }
 
 void core_from_factors(const double* U, const double* S, const double* V, int64_t n1, int64_t n2,

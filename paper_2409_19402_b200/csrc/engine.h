@@ -8,6 +8,8 @@
 
 #include <cuda_runtime.h>
 
+#include "internal.h"
+
 namespace ppc {
 
 // out (N x q) = alpha * T (N x n3) * op(M):  trans_m=false: M is q x n3 (M^T);
@@ -40,15 +42,18 @@ void slice_svd(const double* A, int64_t m, int64_t n, int64_t stride, int64_t ba
                double* U, double* S, double* V, double* tail2, cudaStream_t s);
 
 // Deterministic Gram G = T^T T (n3 x n3) over the N rows of T (SYRK).
-void gram(const double* T, int64_t N, int64_t n3, double* G, cudaStream_t s);
+// nonfinite (nullable device int): when the Gram's own pass over T can also
+// detect NaN / Inf it sets *nonfinite on a hit and gram returns true; false
+// means T was not checked.
+bool gram(const double* T, int64_t N, int64_t n3, double* G, cudaStream_t s, int* nonfinite = nullptr);
 // Top-p eigenpairs of a symmetric PSD n x n matrix G: Q (n x p), lambda (p).
 // accurate_vectors: lock on the subspace (rank-p truncation) criteria rather
 // than on eigenvalues alone.
 void sym_eig_top(const double* G, int64_t n, int64_t p, double* Q, double* lambda, cudaStream_t s,
                  bool accurate_vectors = false);
 // Partial Grams of nchunks consecutive row chunks (T rows x n3, leading dim ldT).
-void gram_chunks(const double* T, int64_t ldT, int64_t rows, int64_t n3, int64_t chunk,
-                 int64_t nchunks, double* parts, cudaStream_t s);
+bool gram_chunks(const double* T, int64_t ldT, int64_t rows, int64_t n3, int64_t chunk,
+                 int64_t nchunks, double* parts, cudaStream_t s, int* nonfinite = nullptr);
 // Eigensolve tail of data_q: Q (sign rule) and sigma from the Gram G.
 void eig_to_basis(const double* G, int64_t n3, int64_t p, double* Q, double* sigma, cudaStream_t s,
                   bool accurate_vectors = false);
@@ -58,8 +63,17 @@ std::array<double, 2> recon_residual_block(const double* A_blk, int64_t n1, int6
                                            const double* V, int64_t n2, int64_t j0,
                                            const double* Q, int64_t p, int64_t k, cudaStream_t s);
 // transforms.cpp:97-115 on the device. Returns completed_basis.
+// check_finite: fail with PPC_NUMERIC on NaN / Inf in T (the svd guard,
+// matrix_kernels.cpp:32), folded into the Gram's pass over T where it can be.
 bool data_q(const double* T, int64_t N, int64_t n3, int64_t p, double* Q, double* sigma,
-            cudaStream_t s);
+            cudaStream_t s, bool check_finite = false);
+// Finiteness flag for gram / gram_chunks: reset, then test (fails loudly).
+struct FiniteFlag {
+    int* flag;
+    explicit FiniteFlag(cudaStream_t s);
+    int* d() { return flag; }
+    void check(cudaStream_t s, const char* who);
+};
 
 // decompositions.cpp:62-83
 void tsvdq(const double* A, int64_t n1, int64_t n2, int64_t n3, const double* Q, int64_t p,

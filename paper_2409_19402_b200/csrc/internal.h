@@ -38,6 +38,7 @@ struct Context {
     cudaStream_t own_stream = nullptr;  // created lazily per device
     cudaStream_t copy = nullptr;        // H2D staging stream
     cudaStream_t copy_out = nullptr;    // D2H stream (runs beside the H2D one)
+    int* flags[64] = {};                // per-device status words (cudaMalloc'd once)
     int sms = 148;
     int64_t launches = 0;
 };
@@ -45,11 +46,16 @@ Context& ctx();               // ensures a device is selected (throws PPC_NO_DEV
 cudaStream_t stream();        // current stream of this thread
 cudaStream_t copy_stream();   // this thread's H2D staging stream (overlap)
 cudaStream_t copy_out_stream();  // this thread's D2H stream
+// This thread's persistent 4-int device status scratch on the current device
+// (finiteness flags): allocated once outside the stream-ordered pool, so a
+// tiny flag never splits the pool's cached multi-GB blocks.
+int* status_words();
 inline void count_launch(int n = 1) { ctx().launches += n; }
 void check_launch(const char* name);  // cudaGetLastError -> PPC_CUDA
 
 // Stream-ordered device buffer (cudaMallocAsync on the current stream; the
 // default mempool keeps freed blocks, so steady-state calls do not hit the OS).
+// Blocks of >= 256 MB come from an exact-size per-thread cache (runtime.cu).
 class DeviceBuffer {
 public:
     DeviceBuffer() = default;
@@ -57,14 +63,20 @@ public:
     ~DeviceBuffer();
     DeviceBuffer(const DeviceBuffer&) = delete;
     DeviceBuffer& operator=(const DeviceBuffer&) = delete;
-    DeviceBuffer(DeviceBuffer&& o) noexcept : p_(o.p_), n_(o.n_) { o.p_ = nullptr; o.n_ = 0; }
+    DeviceBuffer(DeviceBuffer&& o) noexcept : p_(o.p_), n_(o.n_), dev_(o.dev_) {
+        o.p_ = nullptr;
+        o.n_ = 0;
+        o.dev_ = -1;
+    }
     DeviceBuffer& operator=(DeviceBuffer&& o) noexcept {
         if (this != &o) {
             release();
             p_ = o.p_;
             n_ = o.n_;
+            dev_ = o.dev_;
             o.p_ = nullptr;
             o.n_ = 0;
+            o.dev_ = -1;
         }
         return *this;
     }
@@ -75,7 +87,10 @@ public:
 private:
     void* p_ = nullptr;
     size_t n_ = 0;
+    int dev_ = -1;  // >= 0: a large block owned by the per-device cache
 };
+// Frees this thread's cached large blocks on the current device.
+void trim_workspace();
 
 // Input/output staging for loc = PPC_HOST: device copies on the current
 // stream; for PPC_DEVICE the pointers are passed through untouched.

@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(256) ozaki_split_kernel(const double* __restri
                                                           int64_t rows, int64_t cols, int64_t KC, int64_t KCp,
                                                           int64_t chunk, int64_t per, int8_t* __restrict__ D,
                                                           double* __restrict__ scale, double* __restrict__ sumsq,
-                                                          const int* __restrict__ zmap) {
+                                                          const int* __restrict__ zmap, int* __restrict__ nonfinite) {
     __shared__ double stage[kKC];
     const int64_t j = blockIdx.x;
     const int64_t b = zmap ? zmap[blockIdx.y] : blockIdx.y;
@@ -113,6 +113,9 @@ __global__ void __launch_bounds__(256) ozaki_split_kernel(const double* __restri
         if (threadIdx.x == 0) {
             red[0] = mx;
             sumsq[b * cols + j] = ss;
+            // the caller's finiteness check rides on this pass over the input:
+            // an Inf makes the max Inf, a NaN makes the sum of squares NaN
+            if (nonfinite && (!(mx <= 1.7976931348623157e308) || isnan(ss))) *nonfinite = 1;
         }
     }
     __syncthreads();
@@ -545,7 +548,8 @@ void ozaki_syrk(const OzakiDigits& d, int64_t nout, int64_t per, double* out, cu
 }  // namespace
 
 void OzakiDigits::split(const double* X, int64_t ldx, int64_t stride, int64_t rows_, int64_t cols_, int64_t KC,
-                        int64_t nblk_, cudaStream_t s, const int* zmap, int64_t nz, int64_t chunk, int64_t per) {
+                        int64_t nblk_, cudaStream_t s, const int* zmap, int64_t nz, int64_t chunk, int64_t per,
+                        int* nonfinite) {
     if (KC < 1 || KC > kKC) fail(PPC_ARGUMENT, "ozaki split: block length out of range");
     if (zmap && !stride) fail(PPC_ARGUMENT, "ozaki split: a block map needs batched blocks");
     rows = rows_;
@@ -562,7 +566,7 @@ void OzakiDigits::split(const double* X, int64_t ldx, int64_t stride, int64_t ro
     StageTimer ts("ozaki_split", s, 0.0, 8.0 * total_rows * cols + (double)kS * total_rows * cols);
     dim3 grid((unsigned)cols, (unsigned)launched);
     ozaki_split_kernel<<<grid, 256, 0, s>>>(X, ldx, stride, rows, cols, KC, KCp, chunk ? chunk : KC, per ? per : 1,
-                                            D.as<int8_t>(), sc.d(), sq.d(), zmap);
+                                            D.as<int8_t>(), sc.d(), sq.d(), zmap, nonfinite);
     count_launch();
     check_launch("ozaki_split");
 }
@@ -666,7 +670,7 @@ bool ozaki_recon_residual(const double* X, int64_t N, int64_t n3, const double* 
 }
 
 bool ozaki_gram_partials(const double* T, int64_t ldT, int64_t rows, int64_t n3, int64_t chunk, int64_t nchunks,
-                         double* parts, cudaStream_t s) {
+                         double* parts, cudaStream_t s, int* nonfinite) {
     if (!ozaki_enabled()) return false;
     // the integer path pays off once each output tile sees a long K range
     if (n3 < 128 || chunk < 4096 || rows < 4096 * 4) return false;
@@ -678,7 +682,7 @@ bool ozaki_gram_partials(const double* T, int64_t ldT, int64_t rows, int64_t n3,
     const int64_t nblk = nchunks * per;
     StageTimer tm("gram_ozaki", s, (double)rows * n3 * n3, 8.0 * rows * n3);
     OzakiDigits d;
-    d.split(T, ldT, 0, rows, n3, kKC, nblk, s, nullptr, 0, chunk, per);
+    d.split(T, ldT, 0, rows, n3, kKC, nblk, s, nullptr, 0, chunk, per, nonfinite);
     ozaki_syrk(d, nchunks, per, parts, s, "ozaki_syrk", (double)rows);
     return true;
 }

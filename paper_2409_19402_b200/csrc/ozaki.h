@@ -18,7 +18,8 @@ struct OzakiDigits {
     int64_t rows = 0, cols = 0, KCp = 0, nblk = 0;
     // zmap (device, nz entries; batched blocks only): split just those blocks
     void split(const double* X, int64_t ldx, int64_t stride, int64_t rows, int64_t cols, int64_t KC, int64_t nblk,
-               cudaStream_t s, const int* zmap = nullptr, int64_t nz = 0, int64_t chunk = 0, int64_t per = 0);
+               cudaStream_t s, const int* zmap = nullptr, int64_t nz = 0, int64_t chunk = 0, int64_t per = 0,
+               int* nonfinite = nullptr);
 };
 
 // C_b (A.cols x B.cols, (m, n) at m + n*ldc, b at blk*strideC) = A_blk^T B_blk
@@ -40,9 +41,10 @@ bool ozaki_recon_residual(const double* X, int64_t N, int64_t n3, const double* 
 // tube matrix T (rows x n3, leading dimension ldT), as gram_partials, through
 // 8-bit digit splitting and tcgen05 kind::i8 MMAs. Returns false when the
 // shape is not eligible (caller falls back to the DMMA SYRK). PPC_OZAKI=0
-// disables it.
+// disables it. nonfinite (nullable device int): set to 1 if any value of T
+// is NaN or Inf (the split reads every value once).
 bool ozaki_gram_partials(const double* T, int64_t ldT, int64_t rows, int64_t n3, int64_t chunk, int64_t nchunks,
-                         double* parts, cudaStream_t s);
+                         double* parts, cudaStream_t s, int* nonfinite = nullptr);
 
 // G_b (n x n, column-major, b < batch, stride n*n) = A_b^T A_b for A_b
 // (rows x n, leading dimension lda) at A + b*strideA: the batched slice

@@ -76,6 +76,13 @@ cudaStream_t stream() {
     return c.own_stream;
 }
 
+int* status_words() {
+    Context& c = ctx();
+    const int dev = c.device < 64 ? c.device : 63;
+    if (!c.flags[dev]) PPC_CUDA_CHECK(cudaMalloc(&c.flags[dev], 4 * sizeof(int)));
+    return c.flags[dev];
+}
+
 cudaStream_t copy_out_stream() {
     Context& c = ctx();
     if (!c.copy_out) PPC_CUDA_CHECK(cudaStreamCreateWithFlags(&c.copy_out, cudaStreamNonBlocking));
@@ -93,14 +100,101 @@ void check_launch(const char* name) {
     if (e != cudaSuccess) fail(PPC_CUDA, std::string(name) + " launch: " + cudaGetErrorString(e));
 }
 
+// Large buffers (>= 256 MB: tensor-sized transforms, digit planes, slice
+// Grams) recur with identical sizes from call to call. They are kept in a
+// per-thread, per-device exact-size cache instead of going back to the
+// stream-ordered pool: freed multi-GB blocks that the pool later carves small
+// allocations from made the next call map fresh memory, measured as 10..400 ms
+// stalls inside the Gram. A cached block carries the event of its release, so
+// reuse on another stream still waits for the last user.
+namespace {
+constexpr size_t kBigBytes = size_t(256) << 20;
+struct BigBlock {
+    size_t bytes;
+    void* p;
+    cudaEvent_t done;
+};
+struct BigCache {
+    std::vector<BigBlock> free;
+    size_t held = 0;
+};
+thread_local BigCache t_big[64];
+
+size_t big_cap(int dev) {  // keep at most half of the device memory cached
+    static size_t cap[64] = {};
+    if (!cap[dev]) {
+        size_t fr = 0, tot = 0;
+        cap[dev] = cudaMemGetInfo(&fr, &tot) == cudaSuccess ? tot / 2 : (size_t(64) << 30);
+    }
+    return cap[dev];
+}
+
+void big_drop(BigCache& c, size_t i) {
+    cudaEventSynchronize(c.free[i].done);
+    cudaEventDestroy(c.free[i].done);
+    cudaFree(c.free[i].p);
+    c.held -= c.free[i].bytes;
+    c.free.erase(c.free.begin() + (long)i);
+}
+}  // namespace
+
+void trim_workspace() {
+    Context& c = ctx();
+    BigCache& bc = t_big[c.device < 64 ? c.device : 63];
+    while (!bc.free.empty()) big_drop(bc, bc.free.size() - 1);
+}
+
 DeviceBuffer::DeviceBuffer(size_t bytes) : n_(bytes) {
-    if (bytes) PPC_CUDA_CHECK(cudaMallocAsync(&p_, bytes, stream()));
+    if (!bytes) return;
+    cudaStream_t s = stream();
+    if (bytes >= kBigBytes) {
+        const int dev = ctx().device < 64 ? ctx().device : 63;
+        dev_ = dev;
+        BigCache& c = t_big[dev];
+        for (size_t i = 0; i < c.free.size(); ++i)
+            if (c.free[i].bytes == bytes) {
+                p_ = c.free[i].p;
+                PPC_CUDA_CHECK(cudaStreamWaitEvent(s, c.free[i].done, 0));
+                PPC_CUDA_CHECK(cudaEventDestroy(c.free[i].done));
+                c.held -= bytes;
+                c.free.erase(c.free.begin() + (long)i);
+                return;
+            }
+        // not cached: a plain allocation (outside the pool) of this size
+        cudaError_t e = cudaMalloc(&p_, bytes);
+        while (e == cudaErrorMemoryAllocation && !c.free.empty()) {  // make room from the cache
+            cudaGetLastError();
+            big_drop(c, 0);
+            e = cudaMalloc(&p_, bytes);
+        }
+        PPC_CUDA_CHECK(e);
+        return;
+    }
+    PPC_CUDA_CHECK(cudaMallocAsync(&p_, bytes, s));
 }
 DeviceBuffer::~DeviceBuffer() { release(); }
 void DeviceBuffer::release() {
-    if (p_) cudaFreeAsync(p_, stream());
+    if (p_) {
+        if (dev_ >= 0) {
+            BigCache& c = t_big[dev_];
+            cudaEvent_t ev = nullptr;
+            if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) == cudaSuccess &&
+                cudaEventRecord(ev, stream()) == cudaSuccess) {
+                c.free.push_back({n_, p_, ev});
+                c.held += n_;
+                while (c.held > big_cap(dev_) && c.free.size() > 1) big_drop(c, 0);  // oldest first
+            } else {
+                if (ev) cudaEventDestroy(ev);
+                cudaDeviceSynchronize();
+                cudaFree(p_);
+            }
+        } else {
+            cudaFreeAsync(p_, stream());
+        }
+    }
     p_ = nullptr;
     n_ = 0;
+    dev_ = -1;
 }
 
 void validate_loc(int loc) {
@@ -219,6 +313,16 @@ void* ppc_get_stream(void) {
 int ppc_synchronize(void) {
     try {
         PPC_CUDA_CHECK(cudaStreamSynchronize(ppc::stream()));
+        return 0;
+    } catch (const ppc::Error& e) {
+        ppc::set_error(e.what());
+        return e.code;
+    }
+}
+
+int ppc_trim_workspace(void) {
+    try {
+        ppc::trim_workspace();
         return 0;
     } catch (const ppc::Error& e) {
         ppc::set_error(e.what());

@@ -100,11 +100,11 @@ void tree_reduce(double* parts, int64_t nparts, int64_t elems, cudaStream_t s) {
 
 // Partial Grams of `nchunks` consecutive chunks of `chunk` rows of T (rows x
 // n3, leading dimension ldT) into parts (nchunks x n3 x n3).
-void gram_chunks(const double* T, int64_t ldT, int64_t rows, int64_t n3, int64_t chunk,
-                 int64_t nchunks, double* parts, cudaStream_t s) {
+bool gram_chunks(const double* T, int64_t ldT, int64_t rows, int64_t n3, int64_t chunk,
+                 int64_t nchunks, double* parts, cudaStream_t s, int* nonfinite) {
     // INT8 tensor-core (Ozaki) path for large Grams; it reads T column by
     // column, so no re-layout either
-    if (ozaki_gram_partials(T, ldT, rows, n3, chunk, nchunks, parts, s)) return;
+    if (ozaki_gram_partials(T, ldT, rows, n3, chunk, nchunks, parts, s, nonfinite)) return nonfinite != nullptr;
     // Large tube matrices: each SYRK pipeline stage would touch one 2 MB page
     // per column (columns are ldT*8 bytes apart), thrashing the TLB. Re-lay T
     // into 2048-row blocks first (one extra HBM pass); same summation order.
@@ -125,19 +125,29 @@ void gram_chunks(const double* T, int64_t ldT, int64_t rows, int64_t n3, int64_t
         ld = KB;
     }
     gram_partials(src, ld, rows, n3, chunk, nchunks, parts, s, kshift);
+    return false;
 }
 
-void gram(const double* T, int64_t N, int64_t n3, double* G, cudaStream_t s) {
+bool gram(const double* T, int64_t N, int64_t n3, double* G, cudaStream_t s, int* nonfinite) {
     StageTimer tm("gram_syrk", s, (double)N * n3 * n3, 8.0 * N * n3);
     const GramPlan g = gram_plan(N, n3);
-    if (g.chunks == 1) {
-        gram_chunks(T, N, N, n3, g.chunk, 1, G, s);
-        return;
-    }
+    if (g.chunks == 1) return gram_chunks(T, N, N, n3, g.chunk, 1, G, s, nonfinite);
     DeviceBuffer parts(sizeof(double) * g.chunks * n3 * n3);
-    gram_chunks(T, N, N, n3, g.chunk, g.chunks, parts.d(), s);
+    const bool checked = gram_chunks(T, N, N, n3, g.chunk, g.chunks, parts.d(), s, nonfinite);
     tree_reduce(parts.d(), g.chunks, n3 * n3, s);
     PPC_CUDA_CHECK(cudaMemcpyAsync(G, parts.d(), sizeof(double) * n3 * n3, cudaMemcpyDeviceToDevice, s));
+    return checked;
+}
+
+FiniteFlag::FiniteFlag(cudaStream_t s) : flag(status_words()) {
+    PPC_CUDA_CHECK(cudaMemsetAsync(flag, 0, sizeof(int), s));
+}
+
+void FiniteFlag::check(cudaStream_t s, const char* who) {
+    int h = 0;
+    PPC_CUDA_CHECK(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+    PPC_CUDA_CHECK(cudaStreamSynchronize(s));
+    if (h) fail(PPC_NUMERIC, std::string(who) + ": input has non-finite entries");
 }
 
 void sym_eig_top(const double* G, int64_t n, int64_t p, double* Q, double* lambda, cudaStream_t s,
@@ -167,9 +177,17 @@ void eig_to_basis(const double* G, int64_t n3, int64_t p, double* Q, double* sig
 }
 
 bool data_q(const double* T, int64_t N, int64_t n3, int64_t p, double* Q, double* sigma,
-            cudaStream_t s) {
+            cudaStream_t s, bool check_finite) {
     DeviceBuffer G(sizeof(double) * n3 * n3);
-    gram(T, N, n3, G.d(), s);
+    if (check_finite) {
+        FiniteFlag nf(s);
+        if (gram(T, N, n3, G.d(), s, nf.d()))
+            nf.check(s, "svd");
+        else
+            require_finite(T, N * n3, "svd", s);
+    } else {
+        gram(T, N, n3, G.d(), s);
+    }
     // When p > min(n3, N) the unfolding has only min(n3, N) singular vectors;
     // the eigenvectors of G for its zero eigenvalues complete the basis
     // (transforms.cpp:104-111 pads with an orthonormal completion).

@@ -999,3 +999,25 @@ def test_ozaki_gram_edge_columns(engine):
     mask = denom > 1e-290
     assert rel[mask].max().item() <= 1e-13
     assert (Go[7] == 0).all() and (Go[:, 7] == 0).all()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("shape,val", [((256, 256, 256), float("nan")), ((256, 256, 256), float("inf")),
+                                       ((24, 20, 16), float("nan")), ((24, 20, 16), float("-inf"))])
+def test_nonfinite_input_rejected(engine, shape, val):
+    """The svd guard (matrix_kernels.cpp:32): NaN / Inf anywhere in the input
+    fails data_dependent_transform and compress_tsvdq with NumericError —
+    through the finiteness flag of the Ozaki Gram's split pass (256^3: the
+    INT8 Gram path) and through the plain scan (small shape: DMMA Gram)."""
+    n1, n2, n3 = shape
+    a = synth.cp_tensor_device(n1, n2, n3, rank=5, noise=1e-3, seed=1)
+    a[n1 // 3, n2 - 1, n3 // 2] = val  # one bad value deep inside a late chunk
+    with pytest.raises(engine.NumericError):
+        engine.data_dependent_transform(a, 8)
+    with pytest.raises(engine.NumericError):
+        engine.compress_tsvdq(a, 8, 4)
+    with pytest.raises(engine.NumericError):  # host input: the slab-streamed Gram
+        engine.compress_tsvdq(engine.to_host(a), 8, 4)
+    a[n1 // 3, n2 - 1, n3 // 2] = 0.0
+    t = engine.data_dependent_transform(a, 8)  # clean input passes again
+    assert np.isfinite(t.q).all()
