@@ -128,70 +128,112 @@ __global__ void residual_kernel(const double* GX, const double* X, const double*
     if (lane == 0) res[s * b + j] = sqrt(acc);
 }
 
-// One CTA per slice: R = chol(S + shift*I) (upper, S = R^T R), then R^{-1}
-// in place (LAPACK trti2 order, one row per thread), written out as a full
-// b x b column-major block with zeros below the diagonal. b <= 160 (smem).
-__global__ void __launch_bounds__(1024, 1) chol_inv_kernel(const double* __restrict__ S, double* __restrict__ Rinv, int64_t b,
+// One CTA per slice: R = chol(S + shift*I) (upper, S = R^T R), then R^{-1},
+// written out as a full b x b column-major block with zeros below the
+// diagonal (Rout: R itself, optional). b <= 160 (shared memory).
+//
+// The factor is built as L = R^T (lower, column-major in shared memory), so
+// a row of R is a contiguous column of L. Right-looking, one barrier per
+// step: step k updates the trailing lower triangle from the still unscaled
+// column k and d = M(k,k) (M(i,j) -= M(i,k) M(j,k) / d) while column k-1 is
+// scaled by 1/sqrt(d_{k-1}) (no longer read). R^{-1} is then solved column by
+// column (R x = e_j), one warp per column: x lives in registers (lane l holds
+// x(l + 32 t)), each back-substitution step is a lane-parallel dot with a
+// fixed butterfly reduction.
+constexpr int kCholSlots = 5;  // x slots per lane: b <= 160
+__global__ void __launch_bounds__(1024, 1) chol_inv_kernel(const double* __restrict__ S, double* __restrict__ Rinv, int64_t b64,
                                 int shift_pass, int* fail, double* __restrict__ Rout) {
     extern __shared__ __align__(16) double M[];
-    __shared__ double piv;
+    __shared__ double dinv[160];  // 1 / R(i,i)
     __shared__ int bad;
-    const int64_t s = blockIdx.x;
-    const double* Sin = S + s * b * b;
+    const int b = (int)b64;
+    const int64_t sl = blockIdx.x;
+    const double* Sin = S + sl * b64 * b64;
     const int tid = threadIdx.x, nt = blockDim.x;
-    for (int64_t i = tid; i < b * b; i += nt) M[i] = Sin[i];
+    const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
+    for (int i = tid; i < b * b; i += nt) M[i] = Sin[i];
     if (tid == 0) bad = 0;
     __syncthreads();
     if (shift_pass) {  // shifted CholQR (Fukaya et al.): tiny diagonal shift ~ u * trace
-        if (tid == 0) {
-            double t = 0.0;
-            for (int64_t i = 0; i < b; ++i) t += M[i + i * b];
-            piv = t;
-        }
+        double t = 0.0;
+        for (int i = 0; i < b; ++i) t += M[i + i * b];  // every thread, same order
         __syncthreads();
-        const double sh = 1e-15 * piv;
-        __syncthreads();
-        for (int64_t i = tid; i < b; i += nt) M[i + i * b] += sh;
+        const double sh = 1e-15 * t;
+        for (int i = tid; i < b; i += nt) M[i + i * b] += sh;
         __syncthreads();
     }
-    for (int64_t k = 0; k < b; ++k) {
-        if (tid == 0) {
-            const double d = M[k + k * b];
-            if (!(d > 0.0)) bad = 1;
-            piv = d > 0.0 ? sqrt(d) : 1.0;
-            M[k + k * b] = piv;
-        }
-        __syncthreads();
-        for (int64_t j = k + 1 + tid; j < b; j += nt) M[k + j * b] /= piv;
-        __syncthreads();
-        const int64_t rem = b - k - 1;
-        for (int64_t t = tid; t < rem * rem; t += nt) {
-            const int64_t i = k + 1 + t % rem, j = k + 1 + t / rem;
-            if (i <= j) M[i + j * b] -= M[k + i * b] * M[k + j * b];
-        }
-        __syncthreads();
+    if (b > 32 * kCholSlots) {  // the host sizes b <= 160 (shared memory)
+        if (tid == 0 && fail) atomicExch(fail, 1);
+        return;
     }
+    double dprev = 1.0;
+    for (int k = 0; k < b; ++k) {
+        const double d = M[k + k * b];
+        const bool ok = d > 0.0;
+        const double dk = ok ? d : 1.0;
+        const double rinv = 1.0 / dk;
+        // trailing lower triangle i >= j > k: warps over columns, lanes over rows
+        for (int j = k + 1 + warp; j < b; j += nw) {
+            const double mj = M[j + k * b] * rinv;
+            for (int i = j + lane; i < b; i += 32) M[i + j * b] = fma(-M[i + k * b], mj, M[i + j * b]);
+        }
+        // column k-1 is final: scale it (rows > k-1) by 1/sqrt(d_{k-1})
+        if (k > 0) {
+            const double sc = 1.0 / sqrt(dprev);
+            for (int i = k + tid; i < b; i += nt) M[i + (k - 1) * b] *= sc;
+        }
+        if (tid == 0) {
+            if (!ok) bad = 1;
+            dinv[k] = 1.0 / sqrt(dk);
+        }
+        dprev = dk;
+        __syncthreads();
+        if (tid == 0) M[k + k * b] = sqrt(dk);  // read by nobody after this step
+    }
+    __syncthreads();  // the last diagonal
+    // now M holds L = R^T below the diagonal; R(i, l) = M[l + i*b] for l >= i
     if (Rout) {
-        for (int64_t t = tid; t < b * b; t += nt) {
-            const int64_t i = t % b, j = t / b;
-            Rout[s * b * b + t] = (i <= j) ? M[t] : 0.0;
+        double* ro = Rout + sl * b64 * b64;
+        for (int t = tid; t < b * b; t += nt) {
+            const int i = t % b, jj = t / b;
+            ro[t] = (i <= jj) ? M[jj + i * b] : 0.0;
         }
-        __syncthreads();
     }
-    for (int64_t j = 0; j < b; ++j) {
-        if (tid == 0) M[j + j * b] = 1.0 / M[j + j * b];
-        __syncthreads();
-        double y = 0.0;
-        if (tid < j)
-            for (int64_t l = tid; l < j; ++l) y = fma(M[tid + l * b], M[l + j * b], y);
-        __syncthreads();
-        if (tid < j) M[tid + j * b] = -y * M[j + j * b];
-        __syncthreads();
-    }
-    double* out = Rinv + s * b * b;
-    for (int64_t t = tid; t < b * b; t += nt) {
-        const int64_t i = t % b, j = t / b;
-        out[t] = (i <= j) ? M[t] : 0.0;
+    double* out = Rinv + sl * b64 * b64;
+    // R x = e_j, x(i) = -(sum_{l=i+1..j} R(i,l) x(l)) / R(i,i); columns dealt to
+    // the warps in a zig-zag so every warp gets a similar number of steps
+    for (int c = warp; c < b; c += nw) {
+        const int round = c / nw, pos = c % nw;
+        const int cnt = b - round * nw < nw ? b - round * nw : nw;  // columns in this round
+        const int j = (round & 1) ? (round * nw + (cnt - 1 - pos)) : c;
+        double x[kCholSlots];
+#pragma unroll
+        for (int t = 0; t < kCholSlots; ++t) x[t] = 0.0;
+        const double xj = dinv[j];
+#pragma unroll
+        for (int t = 0; t < kCholSlots; ++t)
+            if (lane + 32 * t == j) x[t] = xj;
+        for (int i = j - 1; i >= 0; --i) {
+            const double* Li = M + i * b;  // row i of R: Li[l], l >= i
+            double part = 0.0;
+#pragma unroll
+            for (int t = 0; t < kCholSlots; ++t) {
+                const int l = lane + 32 * t;
+                if (l > i && l <= j) part = fma(Li[l], x[t], part);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+            const double xi = -part * dinv[i];
+#pragma unroll
+            for (int t = 0; t < kCholSlots; ++t)
+                if (lane + 32 * t == i) x[t] = xi;
+        }
+        // column j of R^{-1}: rows 0..j from the lanes' slots, zeros below
+#pragma unroll
+        for (int t = 0; t < kCholSlots; ++t) {
+            const int i = lane + 32 * t;
+            if (i < b) out[i + (int64_t)j * b] = i <= j ? x[t] : 0.0;
+        }
     }
     if (tid == 0 && bad && fail) atomicExch(fail, 1);
 }
