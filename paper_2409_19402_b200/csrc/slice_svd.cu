@@ -158,6 +158,12 @@ void sym_eig_top(const double* G, int64_t n, int64_t p, double* Q, double* lambd
         jacobi_svd(G, n, n, n * n, 1, p, nullptr, lambda, Q, nullptr, s);
         return;
     }
+    // one matrix: direct Householder tridiagonalization + bisection +
+    // inverse iteration (tridiag_eig.cu) instead of the subspace iteration
+    if (tridiag_eig_eligible(n, p)) {
+        tridiag_eig_top(G, n, p, Q, lambda, s);
+        return;
+    }
     subspace_eig_top(G, n, 1, p, Q, lambda, s, accurate_vectors);
 }
 

@@ -355,6 +355,34 @@ void cholqr3(Work& w, double* Y, double* Xout, int64_t c0, cudaStream_t s) {
     }
 }
 
+}  // namespace
+
+// Shifted CholQR3 of one r x k panel in place (the direct eigensolver's
+// inverse-iteration vectors): column order is kept, so Z R^{-1} is a
+// Gram-Schmidt of Z in eigenvalue order.
+void cholqr_inplace(double* Z, int64_t r, int64_t k, cudaStream_t s) {
+    if (k > 160) fail(PPC_ARGUMENT, "cholqr_inplace: too many columns");
+    DeviceBuffer S(sizeof(double) * k * k), Ri(sizeof(double) * k * k), T(sizeof(double) * r * k);
+    const size_t smem = (size_t)k * k * sizeof(double);
+    if (smem > 48 * 1024)
+        PPC_CUDA_CHECK(cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)smem));
+    double* src = Z;
+    double* dst = T.d();
+    for (int pass = 0; pass < 3; ++pass) {
+        gg(src, r, r * k, true, src, r, r * k, S.d(), k, k * k, k, k, r, 1, 1.0, 0.0, s);  // S = Z^T Z
+        chol_inv_kernel<<<1, k > 64 ? 1024 : 256, smem, s>>>(S.d(), Ri.d(), k, pass == 0 ? 1 : 0, nullptr,
+                                                             nullptr);
+        count_launch();
+        check_launch("chol_inv");
+        gg(src, r, r * k, false, Ri.d(), k, k * k, dst, r, r * k, r, k, k, 1, 1.0, 0.0, s);
+        std::swap(src, dst);
+    }
+    if (src != Z) PPC_CUDA_CHECK(cudaMemcpyAsync(Z, src, sizeof(double) * r * k, cudaMemcpyDeviceToDevice, s));
+}
+
+namespace {
+
 // Rayleigh-Ritz on the orthonormal active columns [c0, b) of Xn: X, theta,
 // W = G X and residual norms for those columns (locked ones keep theirs).
 void rayleigh_ritz(Work& w, const double* G, int64_t sG, double* Xn, int64_t c0, cudaStream_t s,

@@ -1,0 +1,729 @@
+// K5b — direct top-p eigensolver for ONE symmetric PSD n x n matrix (the
+// data-driven Q's Gram: transforms.cpp:97-115 takes U3 = left singular
+// vectors of the mode-3 unfolding, i.e. the top eigenvectors of G = T^T T).
+//
+// The Chebyshev subspace iteration (subspace.cu) is right for the 128-slice
+// batches of the facewise SVD, but for a single 1024 x 1024 Gram it spends
+// its time in one-CTA b x b Rayleigh-Ritz eigensolves on a noise plateau
+// (~40 ms at cfg5). The direct route here is latency-bound instead:
+//   1. Householder tridiagonalization T = H^T G H (LAPACK dsytd2, lower) in
+//      ONE persistent cooperative kernel: the matrix lives column-cyclic in
+//      the CTAs' shared memory; the owner of column j+1 publishes it before
+//      the step-j update, so every CTA rebuilds the next reflector itself and
+//      a step needs a single grid barrier (for the p = tau*G*v exchange);
+//   2. the top-p eigenvalues of T by Sturm-count bisection, 32-way
+//      multisection per warp (one warp per eigenvalue);
+//   3. their eigenvectors by inverse iteration on T - lambda I (tridiagonal
+//      LU with partial pivoting, deterministic random starts, 3 solves);
+//   4. shifted CholQR3 of Z in eigenvalue order (DMMA GEMMs, subspace.cu);
+//   5. back-transformation Q = H_0 ... H_{n-3} Z, one warp per column of Z
+//      held in registers, reflectors read from L2.
+// Every reduction has a fixed order, so Q is bitwise repeatable.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "engine.h"
+#include "internal.h"
+#include "slice_svd.cuh"
+
+namespace ppc {
+
+namespace {
+
+constexpr int kTrdThreads = 256;
+constexpr double kEps = 2.220446049250313e-16;
+constexpr double kSafeMin = 2.2250738585072014e-308;
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Grid barrier over co-resident CTAs (cooperative launch) on a monotonic
+// arrival counter: barrier number b completes when the counter reaches
+// b * nblk, so nobody resets anything on the critical path.
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblk, unsigned& target) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        target += nblk;
+        // release: this CTA's writes (ordered before by bar.sync) are visible
+        // to whoever acquires the counter; no return value to wait for
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+        while (ld_acquire(bar) < target) {
+        }
+    }
+    __syncthreads();
+}
+
+// Fixed-order block sum (every CTA running the same code on the same data
+// gets the same bits): thread-strided partials, then a fixed tree.
+__device__ __forceinline__ double block_sum(double v, double* red) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    double t = lane < nw ? red[lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    return t;  // every thread
+}
+
+struct TrdParams {
+    const double* G;  // n x n, column-major, symmetric
+    int n, nblk, cpc;
+    double* V;       // n x n: column j = v_j (zeros in rows <= j, 1 in row j+1)
+    double* tau;     // n
+    double* d;       // n
+    double* e;       // n - 1
+    double* pg;      // 2 x n  exchanged p = tau * A v, by step parity (a fast CTA
+                     //        writes step j+1 while a slow one still reads step j)
+    double* colpub;  // 2 x n  published next pivot column, by step parity
+    unsigned* bar;   // arrival counter
+};
+
+constexpr int kMaxCpc = 12;  // owned columns per CTA (n <= 1536 on 148 SMs)
+
+// Reflector of step jj from column jj (xs, rows jj+1..n-1), LAPACK dlarfg:
+// computed redundantly by every CTA (same bits everywhere). Writes vn and
+// returns tau; the CTA's slice of V(:, jj) and (CTA 0) d, e, tau go out.
+__device__ __forceinline__ double make_reflector(const TrdParams& P, int jj, const double* xs, double* vn,
+                                                 double* red) {
+    const int n = P.n, tid = threadIdx.x, nt = blockDim.x;
+    double s2 = 0.0;
+    for (int i = jj + 2 + tid; i < n; i += nt) s2 = fma(xs[i], xs[i], s2);
+    s2 = block_sum(s2, red);
+    const double alpha = xs[jj + 1];
+    double beta, tau, scal;
+    if (s2 == 0.0) {
+        beta = alpha;
+        tau = 0.0;
+        scal = 0.0;
+    } else {
+        beta = -copysign(sqrt(fma(alpha, alpha, s2)), alpha);
+        tau = (beta - alpha) / beta;
+        scal = 1.0 / (alpha - beta);
+    }
+    for (int i = tid; i < n; i += nt) vn[i] = i <= jj ? 0.0 : (i == jj + 1 ? 1.0 : xs[i] * scal);
+    if (blockIdx.x == 0 && tid == 0) {
+        P.d[jj] = xs[jj];
+        P.e[jj] = beta;
+        P.tau[jj] = tau;
+    }
+    // V(:, jj): CTA b stores rows [b*ch, (b+1)*ch)
+    const int ch = (n + P.nblk - 1) / P.nblk;
+    const int r0 = blockIdx.x * ch;
+    for (int i = r0 + tid; i < min(n, r0 + ch); i += nt)
+        P.V[(size_t)jj * n + i] = i <= jj ? 0.0 : (i == jj + 1 ? 1.0 : xs[i] * scal);
+    return tau;
+}
+
+// One pass over the owned columns c > j: the step-j rank-2 update
+// A(j+1:, c) -= v w_c + w v_c, fused with the step-(j+1) products
+// p_c = tau' A(j+2:, c)^T v' of the updated columns (vn == nullptr: update
+// only). One warp per owned column, two rows per lane per iteration from an
+// even start (v, w and v' are zero in rows <= j, so the extra row is left
+// unchanged); the owner of column j+2 publishes it as it goes.
+__device__ __forceinline__ void update_pass(const TrdParams& P, double* A, int j, const double* vs,
+                                            const double* ws, const double* vn, double taun) {
+    const int n = P.n, nblk = P.nblk, cpc = P.cpc, blk = blockIdx.x;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    const int i0 = (j + 1) & ~1;
+    double* cp = P.colpub + (size_t)((j + 1) & 1) * n;
+    for (int t = warp; t < cpc; t += nw) {
+        const int c = blk + t * nblk;
+        if (c <= j || c >= n) continue;  // warp-uniform
+        const double vc = vs[c], wc = ws[c];
+        double* a = A + (size_t)t * n;
+        const bool pub = (c == j + 2);
+        double acc = 0.0;
+        for (int i = i0 + 2 * lane; i < n; i += 64) {
+            const double2 av = *reinterpret_cast<const double2*>(a + i);
+            const double2 v2 = *reinterpret_cast<const double2*>(vs + i);
+            const double2 w2 = *reinterpret_cast<const double2*>(ws + i);
+            double2 nv;
+            nv.x = fma(-w2.x, vc, fma(-v2.x, wc, av.x));
+            nv.y = fma(-w2.y, vc, fma(-v2.y, wc, av.y));
+            *reinterpret_cast<double2*>(a + i) = nv;
+            if (vn) {
+                const double2 n2 = *reinterpret_cast<const double2*>(vn + i);
+                acc = fma(nv.x, n2.x, acc);
+                acc = fma(nv.y, n2.y, acc);
+            }
+            if (pub) *reinterpret_cast<double2*>(cp + i) = nv;
+        }
+        if (vn) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            if (lane == 0 && c > j + 1) P.pg[(size_t)((j + 1) & 1) * n + c] = taun * acc;
+        }
+    }
+}
+
+// Column c is owned by CTA c % nblk, slot c / nblk.
+__global__ void __launch_bounds__(kTrdThreads, 1) sytrd_kernel(TrdParams P) {
+    extern __shared__ __align__(16) double sm[];
+    const int n = P.n, nblk = P.nblk, cpc = P.cpc, blk = blockIdx.x;
+    double* A = sm;                    // cpc x n (slot t = column blk + t*nblk)
+    double* vs = A + (size_t)cpc * n;  // reflector of step j
+    double* vn = vs + n;               // reflector of step j+1
+    double* ws = vn + n;               // w = p - K v
+    double* xs = ws + n;               // pivot column
+    __shared__ double red[32];
+    const int tid = threadIdx.x, nt = blockDim.x;
+    unsigned target = 0;
+
+    for (int t = 0; t < cpc; ++t) {
+        const int c = blk + t * nblk;
+        if (c < n)
+            for (int i = tid; i < n; i += nt) A[(size_t)t * n + i] = P.G[(size_t)c * n + i];
+    }
+    for (int i = tid; i < n; i += nt) {
+        xs[i] = P.G[i];
+        ws[i] = 0.0;
+    }
+    __syncthreads();
+    // prologue: reflector 0, its products, column 1 published (an update
+    // with v = w = 0 leaves A unchanged)
+    double tau = make_reflector(P, 0, xs, vn, red);
+    for (int i = tid; i < n; i += nt) vs[i] = 0.0;
+    __syncthreads();
+    update_pass(P, A, -1, vs, ws, vn, tau);
+
+    for (int j = 0; j <= n - 3; ++j) {
+        {
+            double* t = vs;  // the step-j reflector is the one just built
+            vs = vn;
+            vn = t;
+        }
+        grid_barrier(P.bar, (unsigned)nblk, target);
+        // ---- p and the published column j+1 (both written before the barrier)
+        const double* pg = P.pg + (size_t)(j & 1) * n;
+        const double* cp = P.colpub + (size_t)(j & 1) * n;
+        double pv = 0.0;
+        for (int i = j + 1 + tid; i < n; i += nt) {
+            const double p = __ldcg(pg + i);
+            ws[i] = p;
+            xs[i] = __ldcg(cp + i);
+            pv = fma(p, vs[i], pv);
+        }
+        const double K = 0.5 * tau * block_sum(pv, red);
+        for (int i = j + 1 + tid; i < n; i += nt) ws[i] = fma(-K, vs[i], ws[i]);
+        if (tid == 0) ws[j] = 0.0;  // rows <= j of w stay zero (read by the paired-row pass)
+        __syncthreads();
+        // ---- pivot column j+1 after the step-j update
+        {
+            const double vc = vs[j + 1], wc = ws[j + 1];
+            for (int i = j + 1 + tid; i < n; i += nt) xs[i] = fma(-ws[i], vc, fma(-vs[i], wc, xs[i]));
+        }
+        __syncthreads();
+        if (j + 1 <= n - 3) {
+            const double taun = make_reflector(P, j + 1, xs, vn, red);
+            __syncthreads();
+            update_pass(P, A, j, vs, ws, vn, taun);
+            tau = taun;
+        } else {
+            update_pass(P, A, j, vs, ws, nullptr, 0.0);
+        }
+        __syncthreads();
+    }
+    // trailing 2 x 2 block: columns n-2 and n-1 are final in their owners
+    for (int t = 0; t < cpc; ++t) {
+        const int c = blk + t * nblk;
+        if (tid == 0 && c == n - 2) {
+            P.d[n - 2] = A[(size_t)t * n + n - 2];
+            P.e[n - 2] = A[(size_t)t * n + n - 1];
+            P.tau[n - 2] = 0.0;
+        }
+        if (tid == 0 && c == n - 1) {
+            P.d[n - 1] = A[(size_t)t * n + n - 1];
+            P.tau[n - 1] = 0.0;
+        }
+    }
+}
+
+// Number of eigenvalues of T below x (Sturm sequence, LAPACK dlaneg-style
+// pivot guard).
+__device__ __forceinline__ int sturm_count(const double* d, const double* e2, int n, double x,
+                                           double pivmin) {
+    double q = d[0] - x;
+    if (fabs(q) <= pivmin) q = -pivmin;
+    int c = q < 0.0;
+    for (int i = 1; i < n; ++i) {
+        q = d[i] - x - e2[i - 1] / q;
+        if (fabs(q) <= pivmin) q = -pivmin;
+        c += q < 0.0;
+    }
+    return c;
+}
+
+// One CTA per wanted eigenvalue m (0 = largest): kBisThreads-way
+// multisection, every thread one Sturm count per round (~7 bits a round).
+constexpr int kBisThreads = 256;
+__global__ void __launch_bounds__(kBisThreads) bisect_top_kernel(const double* __restrict__ dg,
+                                                                 const double* __restrict__ eg, int n,
+                                                                 double* __restrict__ lam,
+                                                                 double* __restrict__ bounds) {
+    extern __shared__ __align__(16) double sh[];
+    double* d = sh;
+    double* e2 = sh + n;
+    __shared__ double s_gl[kBisThreads / 32], s_gu[kBisThreads / 32], s_em[kBisThreads / 32];
+    __shared__ int s_first[kBisThreads / 32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = kBisThreads / 32;
+    // Gershgorin interval and the pivot floor (fixed order: same in every CTA)
+    double gl = 1e308, gu = -1e308, em = 0.0;
+    for (int i = tid; i < n; i += kBisThreads) {
+        const double di = dg[i];
+        const double el = i > 0 ? fabs(eg[i - 1]) : 0.0, er = i < n - 1 ? fabs(eg[i]) : 0.0;
+        d[i] = di;
+        e2[i] = er * er;
+        gl = fmin(gl, di - el - er);
+        gu = fmax(gu, di + el + er);
+        em = fmax(em, er * er);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        gl = fmin(gl, __shfl_xor_sync(0xffffffffu, gl, o));
+        gu = fmax(gu, __shfl_xor_sync(0xffffffffu, gu, o));
+        em = fmax(em, __shfl_xor_sync(0xffffffffu, em, o));
+    }
+    if (lane == 0) {
+        s_gl[warp] = gl;
+        s_gu[warp] = gu;
+        s_em[warp] = em;
+    }
+    __syncthreads();
+    gl = s_gl[0];
+    gu = s_gu[0];
+    em = s_em[0];
+    for (int w = 1; w < nw; ++w) {
+        gl = fmin(gl, s_gl[w]);
+        gu = fmax(gu, s_gu[w]);
+        em = fmax(em, s_em[w]);
+    }
+    const double tnorm = fmax(fabs(gl), fabs(gu));
+    const double pivmin = kSafeMin * fmax(1.0, em);
+    gl -= 2.0 * kEps * tnorm * n + 2.0 * pivmin;
+    gu += 2.0 * kEps * tnorm * n + 2.0 * pivmin;
+    const double atol = kEps * tnorm;
+    const int m = blockIdx.x;
+    const int want = n - m;  // invariant: count(hi) >= want > count(lo)
+    double lo = gl, hi = gu;
+    for (int it = 0; it < 40; ++it) {
+        if (hi - lo <= fmax(2.0 * kEps * fmax(fabs(lo), fabs(hi)), atol)) break;
+        const double x = lo + (hi - lo) * (double)(tid + 1) / (double)(kBisThreads + 1);
+        const int c = sturm_count(d, e2, n, x, pivmin);
+        const unsigned ge = __ballot_sync(0xffffffffu, c >= want);
+        if (lane == 0) s_first[warp] = ge ? warp * 32 + __ffs(ge) - 1 : kBisThreads;
+        __syncthreads();
+        int first = kBisThreads;
+        for (int w = 0; w < nw; ++w) first = min(first, s_first[w]);
+        const double h = (double)(hi - lo);
+        const double l0 = lo;
+        if (first < kBisThreads) hi = l0 + h * (double)(first + 1) / (double)(kBisThreads + 1);
+        if (first > 0) lo = l0 + h * (double)first / (double)(kBisThreads + 1);
+        __syncthreads();
+    }
+    if (tid == 0) {
+        lam[m] = 0.5 * (lo + hi);
+        if (bounds && m == 0) {
+            bounds[0] = tnorm;
+            bounds[1] = pivmin;
+        }
+    }
+}
+
+__device__ __forceinline__ double hash_unit(uint64_t z) {
+    z += 0x9e3779b97f4a7c15ULL;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    z ^= z >> 31;
+    return (double)(z >> 11) * 0x1.0p-52 - 1.0;  // [-1, 1)
+}
+
+// Inverse iteration, one CTA (one warp) per eigenvalue: LU with partial
+// pivoting of T - lambda I (dlagtf layout: U diagonal u0, superdiagonals
+// u1, u2, unit-L multipliers lm, pivot flags) by lane 0 in shared memory,
+// three solves from a deterministic random start with max-norm scaling in
+// between; the warp loads T, draws the start and normalizes. Pivots below
+// eps*||T|| are raised to it (dlagts job = -1).
+__global__ void inverse_iteration_kernel(const double* __restrict__ dg, const double* __restrict__ eg,
+                                         int n, const double* __restrict__ lam,
+                                         const double* __restrict__ bounds, double* __restrict__ Z) {
+    extern __shared__ __align__(16) double sh[];
+    double* d = sh;
+    double* e = d + n;
+    double* u0 = e + n;
+    double* u1 = u0 + n;
+    double* u2 = u1 + n;
+    double* lm = u2 + n;
+    double* x = lm + n;
+    unsigned char* pv = reinterpret_cast<unsigned char*>(x + n);
+    __shared__ double s_sc;
+    const int m = blockIdx.x, lane = threadIdx.x;
+    const double l = lam[m];
+    const double pert = kEps * fmax(bounds[0], kSafeMin);
+    for (int i = lane; i < n; i += 32) {
+        d[i] = dg[i] - l;
+        e[i] = i < n - 1 ? eg[i] : 0.0;
+        x[i] = hash_unit(((uint64_t)m << 32) ^ (uint64_t)i ^ 0x7a11d1a6ULL);
+    }
+    __syncwarp();
+    if (lane == 0) {
+        double a0 = d[0], a1 = e[0];
+        for (int i = 0; i < n - 1; ++i) {
+            const double sub = e[i], dn = d[i + 1], en = e[i + 1];
+            if (fabs(a0) >= fabs(sub)) {
+                double piv = a0;
+                if (fabs(piv) < pert) piv = piv >= 0.0 ? pert : -pert;
+                const double mult = sub / piv;
+                u0[i] = piv;
+                u1[i] = a1;
+                u2[i] = 0.0;
+                lm[i] = mult;
+                pv[i] = 0;
+                a0 = fma(-mult, a1, dn);
+                a1 = en;
+            } else {
+                const double mult = a0 / sub;
+                u0[i] = sub;
+                u1[i] = dn;
+                u2[i] = en;
+                lm[i] = mult;
+                pv[i] = 1;
+                a0 = fma(-mult, dn, a1);
+                a1 = -mult * en;
+            }
+        }
+        if (fabs(a0) < pert) a0 = a0 >= 0.0 ? pert : -pert;
+        u0[n - 1] = a0;
+        u1[n - 1] = 0.0;
+        u2[n - 1] = 0.0;
+        for (int i = 0; i < n; ++i) u0[i] = 1.0 / u0[i];  // reciprocals for the solves
+    }
+    for (int it = 0; it < 3; ++it) {
+        if (lane == 0) {
+            double bi = x[0];
+            for (int i = 0; i < n - 1; ++i) {
+                double bn = x[i + 1];
+                if (pv[i]) {
+                    const double t = bi;
+                    bi = bn;
+                    bn = t;
+                }
+                x[i] = bi;
+                bi = fma(-lm[i], bi, bn);
+            }
+            x[n - 1] = bi;
+            double xn1 = 0.0, xn2 = 0.0, mx = 0.0;
+            for (int i = n - 1; i >= 0; --i) {
+                const double v = fma(-u2[i], xn2, fma(-u1[i], xn1, x[i])) * u0[i];
+                x[i] = v;
+                xn2 = xn1;
+                xn1 = v;
+                mx = fmax(mx, fabs(v));
+            }
+            s_sc = mx > 0.0 ? 1.0 / mx : 1.0;
+        }
+        __syncwarp();
+        const double sc = s_sc;
+        for (int i = lane; i < n; i += 32) x[i] *= sc;
+        __syncwarp();
+    }
+    double nrm = 0.0;
+    for (int i = lane; i < n; i += 32) nrm = fma(x[i], x[i], nrm);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
+    const double inv = nrm > 0.0 ? 1.0 / sqrt(nrm) : 0.0;
+    for (int i = lane; i < n; i += 32) Z[(size_t)m * n + i] = x[i] * inv;
+}
+
+// Q = H_0 H_1 ... H_{n-3} Z. The reflectors go in chunks of kBtChunk,
+// last-first; a chunk H_jl ... H_jh (jh applied first) is one compact-WY
+// block I - V T V^T (LAPACK dlarft, forward: V = [v_jl .. v_jh], T upper
+// triangular), whose T factors are built beforehand by wy_t_kernel. Then
+// one warp per column of Z, held in registers (lane l owns row pairs
+// 2l + 64 s): d = V^T z in one pass (kBtChunk independent sums), y = T d,
+// z -= V y in a second pass. The CTA streams V chunks and T through shared
+// memory with cp.async, double-buffered.
+constexpr int kBtChunk = 8;
+constexpr int kBtWarps = 2;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(bar)));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// 1-D bulk copy global -> shared (TMA engine), completion on the mbarrier
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+// T of chunk c (rows/cols r = 0..cnt-1 <-> reflector jl + r): T(r,r) = tau,
+// T(0:r, r) = -tau_r T(0:r, 0:r) V(:, 0:r)^T v_r. One CTA per chunk.
+__global__ void wy_t_kernel(const double* __restrict__ V, const double* __restrict__ tau, int n,
+                            double* __restrict__ Tout) {
+    __shared__ double S[kBtChunk][kBtChunk];
+    __shared__ double T[kBtChunk][kBtChunk];
+    const int c = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    const int jtop = n - 3;
+    const int j1 = jtop - c * kBtChunk;
+    const int cnt = min(kBtChunk, j1 + 1);
+    const int jl = j1 - cnt + 1;
+    for (int q = warp; q < cnt * cnt; q += nw) {
+        const int a = q / cnt, b = q % cnt;
+        if (a >= b) continue;
+        const double* va = V + (size_t)(jl + a) * n;
+        const double* vb = V + (size_t)(jl + b) * n;
+        double acc = 0.0;
+        for (int i = lane; i < n; i += 32) acc = fma(va[i], vb[i], acc);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) S[a][b] = acc;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int r = 0; r < kBtChunk; ++r)
+            for (int q = 0; q < kBtChunk; ++q) T[q][r] = 0.0;
+        for (int r = 0; r < cnt; ++r) {
+            const double tr = tau[jl + r];
+            T[r][r] = tr;
+            for (int q = 0; q < r; ++q) {
+                double acc = 0.0;
+                for (int u = q; u < r; ++u) acc = fma(T[q][u], S[u][r], acc);
+                T[q][r] = -tr * acc;
+            }
+        }
+        double* out = Tout + (size_t)c * kBtChunk * kBtChunk;
+        for (int r = 0; r < kBtChunk; ++r)
+            for (int q = 0; q < kBtChunk; ++q) out[q * kBtChunk + r] = T[q][r];  // row-major T(q, r)
+    }
+}
+
+template <int NS, bool FULL>  // NS doubles per lane (NS/2 row pairs)
+__global__ void __launch_bounds__(32 * kBtWarps) back_transform_kernel(const double* __restrict__ V,
+                                                                       const double* __restrict__ Tg, int n,
+                                                                       int k, double* __restrict__ Z) {
+    extern __shared__ __align__(16) double sv[];  // 2 x (kBtChunk x n + kBtChunk^2)
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
+    const int col = blockIdx.x * kBtWarps + warp;
+    const bool live = col < k;
+    const size_t bufsz = (size_t)kBtChunk * n + kBtChunk * kBtChunk;
+    double z[NS];
+    double* zc = Z + (size_t)(live ? col : 0) * n;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+        const int i = 2 * lane + 64 * (s >> 1) + (s & 1);
+        z[s] = (live && (FULL || i < n)) ? zc[i] : 0.0;
+    }
+    const int jtop = n - 3;
+    const int nchunks = (jtop + kBtChunk) / kBtChunk;
+    __shared__ __align__(8) uint64_t full[2];
+    // one thread streams a chunk: its cnt reflectors (rows from the first
+    // 16-byte-aligned one past the zeros) and T, by the bulk-copy engine
+    auto load_chunk = [&](int c, int buf) {
+        const int j1 = jtop - c * kBtChunk;
+        const int cnt = min(kBtChunk, j1 + 1);
+        const int jl = j1 - cnt + 1;
+        double* dst = sv + (size_t)buf * bufsz;
+        const int r0 = (jl + 1) & ~1;  // rows < r0 are zero in every reflector of the chunk
+        const uint32_t rb = (uint32_t)(n - r0) * 8u;
+        mbar_expect_tx(&full[buf], cnt * rb + kBtChunk * kBtChunk * 8u);
+        for (int r = 0; r < cnt; ++r) bulk_g2s(dst + (size_t)r * n + r0, V + (size_t)(jl + r) * n + r0, rb, &full[buf]);
+        bulk_g2s(dst + (size_t)kBtChunk * n, Tg + (size_t)c * kBtChunk * kBtChunk, kBtChunk * kBtChunk * 8u,
+                 &full[buf]);
+    };
+    // rows below the chunk's first nonzero row are never copied: zero them once
+    for (size_t q = tid; q < 2 * bufsz; q += 32 * kBtWarps) sv[q] = 0.0;
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic writes before bulk copies
+    if (tid == 0) {
+        mbar_init(&full[0]);
+        mbar_init(&full[1]);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    if (tid == 0) {
+        load_chunk(0, 0);
+        if (nchunks > 1) load_chunk(1, 1);
+    }
+    for (int c = 0; c < nchunks; ++c) {
+        mbar_wait(&full[c & 1], (uint32_t)((c >> 1) & 1));
+        const int j1 = jtop - c * kBtChunk;
+        const int cnt = min(kBtChunk, j1 + 1);
+        const double* vb = sv + (size_t)(c & 1) * bufsz;
+        const double* T = vb + (size_t)kBtChunk * n;
+        double d[kBtChunk];
+#pragma unroll
+        for (int r = 0; r < kBtChunk; ++r) {
+            d[r] = 0.0;
+            if (r < cnt) {
+                const double* v = vb + (size_t)r * n;
+#pragma unroll
+                for (int s = 0; s < NS; s += 2) {
+                    const int i = 2 * lane + 64 * (s >> 1);
+                    if (FULL || i < n) {
+                        const double2 v2 = *reinterpret_cast<const double2*>(v + i);
+                        d[r] = fma(v2.x, z[s], d[r]);
+                        d[r] = fma(v2.y, z[s + 1], d[r]);
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+            for (int r = 0; r < kBtChunk; ++r) d[r] += __shfl_xor_sync(0xffffffffu, d[r], o);
+        double y[kBtChunk];
+#pragma unroll
+        for (int q = 0; q < kBtChunk; ++q) {
+            double acc = 0.0;
+#pragma unroll
+            for (int r = q; r < kBtChunk; ++r) acc = fma(T[q * kBtChunk + r], d[r], acc);
+            y[q] = acc;  // T rows/cols past cnt are zero
+        }
+#pragma unroll
+        for (int r = 0; r < kBtChunk; ++r) {
+            if (r < cnt) {
+                const double* v = vb + (size_t)r * n;
+#pragma unroll
+                for (int s = 0; s < NS; s += 2) {
+                    const int i = 2 * lane + 64 * (s >> 1);
+                    if (FULL || i < n) {
+                        const double2 v2 = *reinterpret_cast<const double2*>(v + i);
+                        z[s] = fma(-y[r], v2.x, z[s]);
+                        z[s + 1] = fma(-y[r], v2.y, z[s + 1]);
+                    }
+                }
+            }
+        }
+        __syncthreads();  // buffer c & 1 is refilled by the next-but-one chunk
+        if (tid == 0 && c + 2 < nchunks) load_chunk(c + 2, c & 1);
+    }
+    if (live) {
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+            const int i = 2 * lane + 64 * (s >> 1) + (s & 1);
+            if (FULL || i < n) zc[i] = z[s];
+        }
+    }
+}
+
+template <int NS>
+void launch_back_transform(const double* V, const double* tau, int n, int k, double* Z, double* Tws,
+                           cudaStream_t s) {
+    const int nchunks = (n - 3 + kBtChunk) / kBtChunk;
+    wy_t_kernel<<<(unsigned)nchunks, 128, 0, s>>>(V, tau, n, Tws);
+    count_launch();
+    check_launch("wy_t");
+    const size_t smem = 2 * ((size_t)kBtChunk * n + kBtChunk * kBtChunk) * sizeof(double);
+    const unsigned grid = (unsigned)((k + kBtWarps - 1) / kBtWarps);
+    if (n == 32 * NS) {
+        PPC_CUDA_CHECK(cudaFuncSetAttribute(back_transform_kernel<NS, true>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        back_transform_kernel<NS, true><<<grid, 32 * kBtWarps, smem, s>>>(V, Tws, n, k, Z);
+    } else {
+        PPC_CUDA_CHECK(cudaFuncSetAttribute(back_transform_kernel<NS, false>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        back_transform_kernel<NS, false><<<grid, 32 * kBtWarps, smem, s>>>(V, Tws, n, k, Z);
+    }
+}
+
+size_t trd_smem(int n, int cpc) { return ((size_t)cpc * n + 4 * (size_t)n) * sizeof(double); }
+
+}  // namespace
+
+bool tridiag_eig_eligible(int64_t n, int64_t p) {
+    if (n < 3 || n > 1536 || (n & 1) || p < 1 || p > 160 || p > n) return false;
+    static const bool off = std::getenv("PPC_TRIDIAG_EIG") && std::atoi(std::getenv("PPC_TRIDIAG_EIG")) == 0;
+    if (off) return false;
+    const int sms = ctx().sms;
+    const int nblk = (int)std::min<int64_t>(sms, n);
+    const int cpc = (int)((n + nblk - 1) / nblk);
+    return cpc <= kMaxCpc && trd_smem((int)n, cpc) <= 200 * 1024;
+}
+
+void tridiag_eig_top(const double* G, int64_t n64, int64_t k64, double* Q, double* lambda, cudaStream_t s) {
+    const int n = (int)n64, k = (int)k64;
+    if (!tridiag_eig_eligible(n64, k64)) fail(PPC_ARGUMENT, "tridiag_eig_top: size out of range");
+    const int nblk = std::min(ctx().sms, n);
+    const int cpc = (n + nblk - 1) / nblk;
+    const size_t smem = trd_smem(n, cpc);
+    DeviceBuffer Vb(sizeof(double) * (size_t)n * n), tb(sizeof(double) * n), db(sizeof(double) * n),
+        eb(sizeof(double) * n), pgb(sizeof(double) * 2 * n),
+        cpb(sizeof(double) * 2 * n), barb(sizeof(unsigned) * 4), bnd(sizeof(double) * 2);
+    PPC_CUDA_CHECK(cudaMemsetAsync(barb.d(), 0, sizeof(unsigned) * 4, s));
+    {
+        StageTimer tm("eig.tridiag", s);
+        TrdParams P;
+        P.G = G;
+        P.n = n;
+        P.nblk = nblk;
+        P.cpc = cpc;
+        P.V = Vb.d();
+        P.tau = tb.d();
+        P.d = db.d();
+        P.e = eb.d();
+        P.pg = pgb.d();
+        P.colpub = cpb.d();
+        P.bar = barb.as<unsigned>();
+        PPC_CUDA_CHECK(cudaFuncSetAttribute(sytrd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        void* args[] = {&P};
+        PPC_CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)sytrd_kernel, dim3(nblk), dim3(kTrdThreads), args,
+                                                   smem, s));
+        count_launch();
+        check_launch("sytrd");
+    }
+    {
+        StageTimer tm("eig.bisect", s);
+        bisect_top_kernel<<<(unsigned)k, kBisThreads, 2 * n * sizeof(double), s>>>(db.d(), eb.d(), n, lambda,
+                                                                              bnd.d());
+        count_launch();
+        check_launch("bisect_top");
+    }
+    {
+        StageTimer tm("eig.invit", s);
+        const size_t ism = 7 * (size_t)n * sizeof(double) + n + 16;
+        PPC_CUDA_CHECK(cudaFuncSetAttribute(inverse_iteration_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)ism));
+        inverse_iteration_kernel<<<(unsigned)k, 32, ism, s>>>(db.d(), eb.d(), n, lambda, bnd.d(), Q);
+        count_launch();
+        check_launch("inverse_iteration");
+    }
+    {
+        StageTimer tm("eig.orth", s);
+        cholqr_inplace(Q, n, k, s);
+    }
+    {
+        StageTimer tm("eig.backtransform", s);
+        DeviceBuffer Tws(sizeof(double) * ((n - 3 + kBtChunk) / kBtChunk) * kBtChunk * kBtChunk);
+        if (n <= 256) launch_back_transform<8>(Vb.d(), tb.d(), n, k, Q, Tws.d(), s);
+        else if (n <= 512) launch_back_transform<16>(Vb.d(), tb.d(), n, k, Q, Tws.d(), s);
+        else if (n <= 1024) launch_back_transform<32>(Vb.d(), tb.d(), n, k, Q, Tws.d(), s);
+        else launch_back_transform<48>(Vb.d(), tb.d(), n, k, Q, Tws.d(), s);
+        count_launch();
+        check_launch("back_transform");
+    }
+}
+
+}  // namespace ppc
