@@ -161,10 +161,12 @@ __device__ __forceinline__ void jacobi_round(double* W, int64_t R, double* Va, i
 __global__ void __launch_bounds__(1024, 1) jacobi_svd_kernel(const double* __restrict__ A, int64_t m, int64_t n,
                                   int64_t strideA, int64_t k, double* __restrict__ U,
                                   double* __restrict__ S, double* __restrict__ V, double* gws,
-                                  int use_smem, double* tail2, int* info, double gtol_rel, int max_sweeps) {
+                                  int use_smem, double* tail2, int* info, double gtol_rel, int max_sweeps,
+                                  const int* __restrict__ zmap) {
     extern __shared__ __align__(16) double sm[];
     __shared__ int s_rot;
-    const int64_t b = blockIdx.x;
+    const int64_t bz = blockIdx.x;                          // launch slot (workspace)
+    const int64_t b = zmap ? (int64_t)zmap[bz] : bz;       // matrix of the batch
     const bool tall = m >= n;
     const int64_t R = tall ? m : n, Cc = tall ? n : m;
     double* W;
@@ -173,7 +175,7 @@ __global__ void __launch_bounds__(1024, 1) jacobi_svd_kernel(const double* __res
         W = sm;
         Va = sm + R * Cc;
     } else {
-        W = gws + b * (R * Cc + Cc * Cc + 2 * Cc);
+        W = gws + bz * (R * Cc + Cc * Cc + 2 * Cc);
         Va = W + R * Cc;
     }
     double* sig = use_smem ? (Va + Cc * Cc) : (Va + Cc * Cc);
@@ -221,7 +223,7 @@ __global__ void __launch_bounds__(1024, 1) jacobi_svd_kernel(const double* __res
         __syncthreads();
     }
 
-    if (tid == 0 && info_out) info_out[b] = sweep;
+    if (tid == 0 && info_out) info_out[bz] = sweep;
     // singular values = column norms
     for (int64_t c = warp; c < Cc; c += nw) {
         double acc = 0.0;
@@ -343,11 +345,12 @@ __global__ void __launch_bounds__(1024, 1) jacobi_svd_kernel(const double* __res
 __global__ void __launch_bounds__(1024, 1) jacobi_logged_kernel(const double* __restrict__ A, int64_t b, int64_t strideA,
                                      double2* __restrict__ log, int64_t max_sweeps,
                                      int* __restrict__ nsweeps, double* __restrict__ sig_out,
-                                     int* __restrict__ rank_out, double gtol_rel) {
+                                     int* __restrict__ rank_out, double gtol_rel,
+                                     const int* __restrict__ zmap) {
     extern __shared__ __align__(16) double W[];
     __shared__ int s_rot;
-    const int64_t bi = blockIdx.x;
-    const double* Ab = A + bi * strideA;
+    const int64_t bi = blockIdx.x;  // launch slot: log / sweeps / sig / rank
+    const double* Ab = A + (zmap ? (int64_t)zmap[bi] : bi) * strideA;
     const int tid = threadIdx.x, nt = blockDim.x;
     const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
     for (int64_t i = tid; i < b * b; i += nt) W[i] = Ab[i];
@@ -405,7 +408,7 @@ template <int ROWS>
 __global__ void replay_rotations_kernel(const double2* __restrict__ log, const int* __restrict__ nsweeps,
                                         int64_t b, int64_t max_sweeps, const double* __restrict__ sig,
                                         const int* __restrict__ rank, int64_t k, double* __restrict__ V,
-                                        double* __restrict__ lambda) {
+                                        double* __restrict__ lambda, const int* __restrict__ zmap) {
     extern __shared__ __align__(16) double Vr[];  // ROWS x b, row-major
     const int64_t bi = blockIdx.y;
     const int64_t row0 = (int64_t)blockIdx.x * ROWS;
@@ -439,14 +442,15 @@ __global__ void replay_rotations_kernel(const double2* __restrict__ log, const i
             __syncthreads();
         }
     const int* rk = rank + bi * b;
+    const int64_t bo = zmap ? (int64_t)zmap[bi] : bi;  // output matrix of the batch
     for (int64_t t = tid; t < ROWS * b; t += nt) {
         const int64_t i = t / b, c = t % b;
         const int64_t o = rk[c];
-        if (o < k && row0 + i < b) V[(bi * k + o) * b + row0 + i] = Vr[t];
+        if (o < k && row0 + i < b) V[(bo * k + o) * b + row0 + i] = Vr[t];
     }
     if (blockIdx.x == 0)
         for (int64_t c = tid; c < b; c += nt)
-            if (rk[c] < k) lambda[bi * k + rk[c]] = sig[bi * b + c];
+            if (rk[c] < k) lambda[bo * k + rk[c]] = sig[bi * b + c];
 }
 
 }  // namespace
@@ -458,7 +462,7 @@ size_t jacobi_smem_bytes(int64_t m, int64_t n) {
 
 void jacobi_svd(const double* A, int64_t m, int64_t n, int64_t strideA, int64_t batch, int64_t k,
                 double* U, double* S, double* V, double* tail2, cudaStream_t s, double gtol_rel,
-                int sweep_cap) {
+                int sweep_cap, const int* zmap) {
     if (batch == 0) return;
     static bool tol_set = false;
     if (!tol_set) {
@@ -483,7 +487,7 @@ void jacobi_svd(const double* A, int64_t m, int64_t n, int64_t strideA, int64_t 
                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)wsm));
         jacobi_logged_kernel<<<(unsigned)batch, 1024, wsm, s>>>(A, n, strideA, lg.as<double2>(),
                                                                 max_sweeps, ns.as<int>(), sg.d(),
-                                                                rk.as<int>(), gtol_rel);
+                                                                rk.as<int>(), gtol_rel, zmap);
         count_launch();
         check_launch("jacobi_logged");
         constexpr int ROWS = 8;
@@ -493,7 +497,7 @@ void jacobi_svd(const double* A, int64_t m, int64_t n, int64_t strideA, int64_t 
         dim3 grid((unsigned)((n + ROWS - 1) / ROWS), (unsigned)batch);
         replay_rotations_kernel<ROWS><<<grid, 256, rsm, s>>>(lg.as<double2>(), ns.as<int>(), n,
                                                              max_sweeps, sg.d(), rk.as<int>(), k,
-                                                             V, S);
+                                                             V, S, zmap);
         count_launch();
         check_launch("replay_rotations");
         if (std::getenv("PPC_JACOBI_DEBUG")) {
@@ -515,7 +519,7 @@ void jacobi_svd(const double* A, int64_t m, int64_t n, int64_t strideA, int64_t 
     DeviceBuffer dinfo(sizeof(int) * batch);
     jacobi_svd_kernel<<<(unsigned)batch, threads, use_smem ? smem : 0, s>>>(
         A, m, n, strideA, k, U, S, V, ws.d(), use_smem ? 1 : 0, tail2, dinfo.as<int>(), gtol_rel,
-        sweep_cap > 0 ? sweep_cap : 60);
+        sweep_cap > 0 ? sweep_cap : 60, zmap);
     count_launch();
     check_launch("jacobi_svd");
     if (dbg) {

@@ -13,9 +13,11 @@ size_t jacobi_smem_bytes(int64_t m, int64_t n);
 // suffices, rotations inside tight clusters below that are skipped.
 // sweep_cap > 0 bounds the sweeps (approximate eigenpairs for early
 // Rayleigh-Ritz steps of the subspace iteration).
+// zmap (device, nullable): launch slot z works on block zmap[z] of the batch
+// (batch = number of slots); outputs land at the mapped block.
 void jacobi_svd(const double* A, int64_t m, int64_t n, int64_t strideA, int64_t batch, int64_t k,
                 double* U, double* S, double* V, double* tail2, cudaStream_t s, double gtol_rel = 0.0,
-                int sweep_cap = 0);
+                int sweep_cap = 0, const int* zmap = nullptr);
 // Sign rule of matrix_kernels.cpp:16-25 on `batch` stacks of X (rows x cols):
 // the largest-|x| entry (first on ties) of each column made nonnegative; the
 // matching column of Y (yrows x cols, nullable) is flipped with it.

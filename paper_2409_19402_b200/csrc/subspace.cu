@@ -61,14 +61,18 @@ __global__ void randn_kernel(double* X, int64_t n, uint64_t seed) {
 
 // Y_next = a*Z + b*Y + c*Yp with per-slice coefficients coef[3*slice + {0,1,2}];
 // columns below c0 (locked in every filtered slice) just carry Y.
+// zmap (nullable): element block z of the launch is slice zmap[z] (only the
+// slices still filtering at this degree; the others keep their own Y).
 __global__ void cheb_kernel(double* __restrict__ Yn, const double* __restrict__ Z,
                             const double* __restrict__ Y, const double* __restrict__ Yp,
                             const double* __restrict__ coef, int64_t per_slice, int64_t total,
-                            int64_t r, int64_t c0) {
+                            int64_t r, int64_t c0, const int* __restrict__ zmap) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
-        const int64_t s = i / per_slice;
-        if ((i - s * per_slice) / r < c0) {
+    for (int64_t ii = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; ii < total; ii += stride) {
+        const int64_t z = ii / per_slice, off = ii - z * per_slice;
+        const int64_t s = zmap ? (int64_t)zmap[z] : z;
+        const int64_t i = s * per_slice + off;
+        if (off / r < c0) {
             Yn[i] = Y[i];
             continue;
         }
@@ -91,8 +95,8 @@ __global__ void scale_rows_kernel(double* P, const double* w, int64_t b, int64_t
 
 // Y(:, j, s) = X(:, j, s) for j < nlock[s]; then normalize every column of Y.
 __global__ void restore_normalize_kernel(double* Y, const double* X, const int* nlock, int64_t r,
-                                         int64_t b) {
-    const int64_t s = blockIdx.y;
+                                         int64_t b, const int* __restrict__ zmap) {
+    const int64_t s = zmap ? (int64_t)zmap[blockIdx.y] : (int64_t)blockIdx.y;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t j = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
     if (j >= b) return;
@@ -111,8 +115,8 @@ __global__ void restore_normalize_kernel(double* Y, const double* X, const int* 
 
 // res(j, s) = || GX(:, j, s) - theta(j, s) X(:, j, s) ||
 __global__ void residual_kernel(const double* GX, const double* X, const double* theta,
-                                double* res, int64_t r, int64_t b) {
-    const int64_t s = blockIdx.y;
+                                double* res, int64_t r, int64_t b, const int* __restrict__ zmap) {
+    const int64_t s = zmap ? (int64_t)zmap[blockIdx.y] : (int64_t)blockIdx.y;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t j = (int64_t)blockIdx.x * (blockDim.x >> 5) + warp;
     if (j >= b) return;
@@ -142,12 +146,13 @@ __global__ void residual_kernel(const double* GX, const double* X, const double*
 // fixed butterfly reduction.
 constexpr int kCholSlots = 5;  // x slots per lane: b <= 160
 __global__ void __launch_bounds__(1024, 1) chol_inv_kernel(const double* __restrict__ S, double* __restrict__ Rinv, int64_t b64,
-                                int shift_pass, int* fail, double* __restrict__ Rout) {
+                                int shift_pass, int* fail, double* __restrict__ Rout,
+                                const int* __restrict__ zmap = nullptr) {
     extern __shared__ __align__(16) double M[];
     __shared__ double dinv[160];  // 1 / R(i,i)
     __shared__ int bad;
     const int b = (int)b64;
-    const int64_t sl = blockIdx.x;
+    const int64_t sl = zmap ? (int64_t)zmap[blockIdx.x] : (int64_t)blockIdx.x;
     const double* Sin = S + sl * b64 * b64;
     const int tid = threadIdx.x, nt = blockDim.x;
     const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
@@ -254,6 +259,24 @@ __global__ void group_sum_kernel(const double* part, int64_t per_group, double* 
     }
 }
 
+// th(c0 + j, s) = P(j, s), j < bc, for the slices of the launch (zmap).
+__global__ void copy_theta_kernel(double* __restrict__ th, const double* __restrict__ P, int64_t b,
+                                  int64_t bc, int64_t c0, const int* __restrict__ zmap) {
+    const int64_t s = zmap ? (int64_t)zmap[blockIdx.x] : (int64_t)blockIdx.x;
+    for (int64_t j = threadIdx.x; j < bc; j += blockDim.x) th[s * b + c0 + j] = P[s * bc + j];
+}
+
+// Slices that stopped filtering before the last degree left their block in
+// another buffer of the (Yp, Y, Yn) rotation: dst(:, s) = src[from[z]](:, s).
+__global__ void gather_filtered_kernel(double* __restrict__ dst, const double* __restrict__ b0,
+                                       const double* __restrict__ b1, const double* __restrict__ b2,
+                                       const int* __restrict__ list, int64_t per) {
+    const int s = list[2 * blockIdx.y], from = list[2 * blockIdx.y + 1];
+    const double* src = from == 0 ? b0 : (from == 1 ? b1 : b2);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < per; i += (int64_t)gridDim.x * blockDim.x)
+        dst[s * per + i] = src[s * per + i];
+}
+
 unsigned grid1(int64_t n) {
     int64_t g = (n + 255) / 256;
     return (unsigned)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 16));
@@ -295,7 +318,7 @@ void g_AB(const double* A, const double* B, double* C, int64_t m, int64_t kk, in
 struct Work {
     int64_t r, b, batch;
     bool basis = false;  // eigenbasis Q (data_q) rather than slice SVDs: stage names sq.*
-    DeviceBuffer X, Y, Yp, Yn, Z, W, P, S, Rinv, Hv, th, res, coef, wmask, nlock, fail, zmap;
+    DeviceBuffer X, Y, Yp, Yn, Z, W, P, S, Rinv, Hv, th, res, coef, wmask, nlock, fail, zmap, glist;
     Work(int64_t r_, int64_t b_, int64_t batch_)
         : r(r_), b(b_), batch(batch_),
           X(sizeof(double) * r_ * b_ * batch_), Y(sizeof(double) * r_ * b_ * batch_),
@@ -327,14 +350,18 @@ void gg(const double* A, int64_t lda, int64_t sA, bool at, const double* B, int6
 // then shifted CholQR3 (Fukaya, Kannan, Nakatsukasa, Yamamoto, Yanagisawa
 // 2020): the shifted first pass keeps the Cholesky factorization alive for
 // cond(Y) up to ~1e15, two plain passes restore orthogonality.
-void cholqr3(Work& w, double* Y, double* Xout, int64_t c0, cudaStream_t s) {
-    const int64_t r = w.r, b = w.b, batch = w.batch, bc = b - c0, per = r * b;
+void cholqr3(Work& w, double* Y, double* Xout, int64_t c0, cudaStream_t s, const int* zm = nullptr,
+             int64_t na = -1) {
+    const int64_t r = w.r, b = w.b, bc = b - c0, per = r * b;
+    const int64_t batch = na < 0 ? w.batch : na;  // launched slices (zm: which ones)
+    const int64_t zx = w.batch;
     StageTimer tm(w.basis ? "sq.cholqr3" : "ss.cholqr3", s);
     if (c0 > 0)
         for (int pass = 0; pass < 2; ++pass) {
             // P = X_L^T Y_A (c0 x bc); Y_A -= X_L P
-            gg(w.X.d(), r, per, true, Y + c0 * r, r, per, w.P.d(), c0, c0 * bc, c0, bc, r, batch, 1.0, 0.0, s);
-            gg(w.X.d(), r, per, false, w.P.d(), c0, c0 * bc, Y + c0 * r, r, per, r, bc, c0, batch, -1.0, 1.0, s);
+            gg(w.X.d(), r, per, true, Y + c0 * r, r, per, w.P.d(), c0, c0 * bc, c0, bc, r, batch, 1.0, 0.0, s, zm, zx);
+            gg(w.X.d(), r, per, false, w.P.d(), c0, c0 * bc, Y + c0 * r, r, per, r, bc, c0, batch, -1.0, 1.0, s, zm,
+               zx);
         }
     const size_t smem = (size_t)bc * bc * sizeof(double);
     if (smem > 200 * 1024) fail(PPC_ARGUMENT, "subspace: block too wide for the CholQR kernel");
@@ -344,13 +371,13 @@ void cholqr3(Work& w, double* Y, double* Xout, int64_t c0, cudaStream_t s) {
     double* src = Y + c0 * r;
     double* bufs[3] = {w.Yn.d() + c0 * r, w.Z.d() + c0 * r, Xout + c0 * r};
     for (int pass = 0; pass < 3; ++pass) {
-        gg(src, r, per, true, src, r, per, w.S.d(), bc, bc * bc, bc, bc, r, batch, 1.0, 0.0, s);  // S = Y^T Y
+        gg(src, r, per, true, src, r, per, w.S.d(), bc, bc * bc, bc, bc, r, batch, 1.0, 0.0, s, zm, zx);  // S = Y^T Y
         chol_inv_kernel<<<(unsigned)batch, bc > 64 ? 1024 : 256, smem, s>>>(w.S.d(), w.Rinv.d(), bc,
                                                                              pass == 0 ? 1 : 0,
-                                                                             w.fail.as<int>(), nullptr);
+                                                                             w.fail.as<int>(), nullptr, zm);
         count_launch();
         check_launch("chol_inv");
-        gg(src, r, per, false, w.Rinv.d(), bc, bc * bc, bufs[pass], r, per, r, bc, bc, batch, 1.0, 0.0, s);
+        gg(src, r, per, false, w.Rinv.d(), bc, bc * bc, bufs[pass], r, per, r, bc, bc, batch, 1.0, 0.0, s, zm, zx);
         src = bufs[pass];
     }
 }
@@ -386,23 +413,30 @@ namespace {
 // Rayleigh-Ritz on the orthonormal active columns [c0, b) of Xn: X, theta,
 // W = G X and residual norms for those columns (locked ones keep theirs).
 void rayleigh_ritz(Work& w, const double* G, int64_t sG, double* Xn, int64_t c0, cudaStream_t s,
-                   double gtol_rel, int sweep_cap) {
-    const int64_t r = w.r, b = w.b, batch = w.batch, bc = b - c0, per = r * b;
+                   double gtol_rel, int sweep_cap, const int* zm = nullptr, int64_t na = -1) {
+    const int64_t r = w.r, b = w.b, bc = b - c0, per = r * b;
+    const int64_t batch = na < 0 ? w.batch : na;  // launched slices (zm: which ones)
+    const int64_t zx = w.batch;
     StageTimer tm(w.basis ? "sq.rayleigh_ritz" : "ss.rayleigh_ritz", s);
-    gg(G, r, sG, false, Xn + c0 * r, r, per, w.Z.d() + c0 * r, r, per, r, bc, r, batch, 1.0, 0.0, s);  // Z = G Xn
-    gg(Xn + c0 * r, r, per, true, w.Z.d() + c0 * r, r, per, w.S.d(), bc, bc * bc, bc, bc, r, batch, 1.0, 0.0, s);
+    gg(G, r, sG, false, Xn + c0 * r, r, per, w.Z.d() + c0 * r, r, per, r, bc, r, batch, 1.0, 0.0, s, zm,
+       zx);  // Z = G Xn
+    gg(Xn + c0 * r, r, per, true, w.Z.d() + c0 * r, r, per, w.S.d(), bc, bc * bc, bc, bc, r, batch, 1.0, 0.0, s,
+       zm, zx);
     {
         StageTimer tj(w.basis ? "sq.rr_eig" : "ss.rr_eig", s);
         // H (PSD) = Hv diag(theta) Hv^T by one-sided Jacobi (eigen mode)
         jacobi_svd(w.S.d(), bc, bc, bc * bc, batch, bc, nullptr, w.P.d(), w.Hv.d(), nullptr, s, gtol_rel,
-                   sweep_cap);
+                   sweep_cap, zm);
     }
-    PPC_CUDA_CHECK(cudaMemcpy2DAsync(w.th.d() + c0, sizeof(double) * b, w.P.d(), sizeof(double) * bc,
-                                     sizeof(double) * bc, batch, cudaMemcpyDeviceToDevice, s));
-    gg(Xn + c0 * r, r, per, false, w.Hv.d(), bc, bc * bc, w.X.d() + c0 * r, r, per, r, bc, bc, batch, 1.0, 0.0, s);
-    gg(w.Z.d() + c0 * r, r, per, false, w.Hv.d(), bc, bc * bc, w.W.d() + c0 * r, r, per, r, bc, bc, batch, 1.0, 0.0, s);
+    copy_theta_kernel<<<(unsigned)batch, 64, 0, s>>>(w.th.d(), w.P.d(), b, bc, c0, zm);
+    count_launch();
+    check_launch("copy_theta");
+    gg(Xn + c0 * r, r, per, false, w.Hv.d(), bc, bc * bc, w.X.d() + c0 * r, r, per, r, bc, bc, batch, 1.0, 0.0, s,
+       zm, zx);
+    gg(w.Z.d() + c0 * r, r, per, false, w.Hv.d(), bc, bc * bc, w.W.d() + c0 * r, r, per, r, bc, bc, batch, 1.0,
+       0.0, s, zm, zx);
     dim3 grid((unsigned)((b + 7) / 8), (unsigned)batch);
-    residual_kernel<<<grid, 256, 0, s>>>(w.W.d(), w.X.d(), w.th.d(), w.res.d(), r, b);
+    residual_kernel<<<grid, 256, 0, s>>>(w.W.d(), w.X.d(), w.th.d(), w.res.d(), r, b, zm);
     count_launch();
     check_launch("residual");
 }
@@ -667,19 +701,46 @@ void subspace_eig_top(const double* G, int64_t r, int64_t batch, int64_t k, doub
                     gg(w.X.d(), r, per, false, w.P.d(), b, b * bf, w.Z.d() + cf * r, r, per, r, bf, b, na, -1.0, 1.0,
                        s, zm, batch);
                 }
-                cheb_kernel<<<grid1(per * batch), 256, 0, s>>>(Yn, w.Z.d(), Y, Yp, w.coef.d() + 3 * j * batch,
-                                                                per, per * batch, r, cf);
-                count_launch();
-                check_launch("cheb");
+                // only the slices still filtering at this degree; a slice that
+                // stops keeps its block in its own buffer of the rotation
+                if (na > 0) {
+                    cheb_kernel<<<grid1(per * na), 256, 0, s>>>(Yn, w.Z.d(), Y, Yp, w.coef.d() + 3 * j * batch,
+                                                                per, per * na, r, cf, zm);
+                    count_launch();
+                    check_launch("cheb");
+                }
                 double* t = Yp;  // rotate (Yp, Y, Yn) <- (Y, Yn, Yp)
                 Yp = Y;
                 Y = Yn;
                 Yn = t;
             }
         }
+        // slices that stopped early: their filtered block into the final buffer
+        // (after d degrees a slice's block sits in rotation slot d % 3)
+        {
+            std::vector<int> gl;
+            for (int64_t sl = 0; sl < batch; ++sl)
+                if (deg[sl] > 0 && deg[sl] % 3 != dmax % 3) {
+                    gl.push_back((int)sl);
+                    gl.push_back(deg[sl] % 3);
+                }
+            if (!gl.empty()) {
+                if ((int64_t)gl.size() * 4 > (int64_t)w.glist.bytes()) w.glist = DeviceBuffer(gl.size() * sizeof(int));
+                PPC_CUDA_CHECK(cudaMemcpyAsync(w.glist.d(), gl.data(), sizeof(int) * gl.size(), cudaMemcpyHostToDevice, s));
+                double* cyc[3] = {w.Y.d(), w.Yn.d(), w.Yp.d()};
+                gather_filtered_kernel<<<dim3(64, (unsigned)(gl.size() / 2)), 256, 0, s>>>(
+                    cyc[dmax % 3], cyc[0], cyc[1], cyc[2], w.glist.as<int>(), per);
+                count_launch();
+                check_launch("gather_filtered");
+            }
+        }
+        // the slices still iterating (degree-0 list of the filter): the rest
+        // are final and skip the orthonormalization and Rayleigh-Ritz
+        const int nact0 = nact[0];
+        const int* zact = w.zmap.as<int>();
         // locked columns back, normalize, CholQR2, Rayleigh-Ritz
-        dim3 grid((unsigned)((b + 7) / 8), (unsigned)batch);
-        restore_normalize_kernel<<<grid, 256, 0, s>>>(Y, w.X.d(), w.nlock.as<int>(), r, b);
+        dim3 grid((unsigned)((b + 7) / 8), (unsigned)nact0);
+        restore_normalize_kernel<<<grid, 256, 0, s>>>(Y, w.X.d(), w.nlock.as<int>(), r, b, zact);
         count_launch();
         check_launch("restore_normalize");
         // CholQR3 writes through w.Yn; make sure Y is not aliased with it
@@ -689,15 +750,17 @@ void subspace_eig_top(const double* G, int64_t r, int64_t batch, int64_t k, doub
         }
         double* Xn = (Y == w.Y.d()) ? w.Yp.d() : w.Y.d();
         // Rayleigh-Ritz only on the columns past the common locked prefix
-        const int64_t c0 = std::min<int64_t>(*std::min_element(nlock.begin(), nlock.end()), b - 1);
+        int64_t c0 = b - 1;
+        for (int64_t sl = 0; sl < batch; ++sl)
+            if (deg[sl] > 0) c0 = std::min<int64_t>(c0, nlock[sl]);
         if (c0 > 0)  // locked columns of the basis are final: copy them through
             PPC_CUDA_CHECK(cudaMemcpy2DAsync(Xn, sizeof(double) * per, w.X.d(), sizeof(double) * per,
                                              sizeof(double) * r * c0, batch, cudaMemcpyDeviceToDevice, s));
-        cholqr3(w, Y, Xn, c0, s);
+        cholqr3(w, Y, Xn, c0, s, zact, nact0);
         // approximate Ritz pairs until something has converged (locking uses
         // true residuals, so an inexact early Rayleigh-Ritz cannot lock early)
         const bool early = it < 2 && c0 == 0;
-        rayleigh_ritz(w, G, r * r, Xn, c0, s, gtol_rel, early ? 4 : 0);
+        rayleigh_ritz(w, G, r * r, Xn, c0, s, gtol_rel, early ? 4 : 0, zact, nact0);
     }
     // outputs: leading k Ritz pairs
     PPC_CUDA_CHECK(cudaMemcpy2DAsync(Xout, sizeof(double) * r * k, w.X.d(), sizeof(double) * per,
