@@ -209,14 +209,20 @@ __device__ __forceinline__ void decode_item(const OzParams& P, int64_t item, int
 // next item's operands stream in while the current one is drained; one TMEM
 // allocation serves every item. AMN: the A digits are MN-major ([plane][k][m],
 // m contiguous), loaded as two 64-byte x 64-row boxes per digit (LBO 4096 B).
-template <bool SYM, bool AMN, bool RESID>
+// BN: output tile width (UMMA N per digit; 80, or 64 for 64-column panels);
+// NL: digit levels computed (levels 2..NL+1, digits 1..NL of each operand:
+// kS = full FP64 accuracy; fewer give ~2^(-8 NL + 1) relative precision for
+// products that only steer an iteration).
+template <bool SYM, bool AMN, bool RESID, int BN = kBN, int NL = kS>
 __global__ void __launch_bounds__(kThreads, 1)
     ozaki_mma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                      const OzParams P, int64_t items) {
+    static_assert(NL * BN <= 512 && BN % 16 == 0 && (BN / 2) % 8 == 0 && NL >= 1 && NL <= kS, "tile shape");
     extern __shared__ uint8_t smem_raw[];
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    constexpr int A_TILE = kBM * kBK, B_TILE = kBN * kBK;
-    constexpr int STAGE = kS * (A_TILE + B_TILE);
+    constexpr int A_TILE = kBM * kBK, B_TILE = BN * kBK;
+    constexpr int STAGE = kS * (A_TILE + B_TILE);  // layout for all kS digits; NL of them are loaded
+    constexpr int STAGE_TX = NL * (A_TILE + B_TILE);
     uint64_t* full = reinterpret_cast<uint64_t*>(base + kStages * STAGE);
     uint64_t* empty = full + kStages;
     uint64_t* tfull = empty + kStages;
@@ -249,13 +255,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int64_t gl = 0; gl < per * nkc; ++gl, ++g) {
                     const int st = (int)(g % kStages);
                     bar_wait(&empty[st], (uint32_t)(((g / kStages) & 1) ^ 1));
-                    bar_expect_tx(&full[st], STAGE);
+                    bar_expect_tx(&full[st], STAGE_TX);
                     const int64_t blk = ob * per + gl / nkc;
                     const int kx = (int)(gl % nkc) * kBK;
                     uint8_t* sa = base + st * STAGE;
                     uint8_t* sb = sa + kS * A_TILE;
 #pragma unroll
-                    for (int s = 0; s < kS; ++s) {
+                    for (int s = 0; s < NL; ++s) {
                         const int plane = (int)(blk * kS + s);
                         if (AMN) {
                             tma_load_3d(sa + s * A_TILE, &mapA, &full[st], (int)(mb * kBM), kx, plane);
@@ -263,7 +269,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         } else {
                             tma_load_3d(sa + s * A_TILE, &mapA, &full[st], kx, (int)(mb * kBM), plane);
                         }
-                        tma_load_3d(sb + s * B_TILE, &mapB, &full[st], kx, (int)(nb * kBN), plane);
+                        tma_load_3d(sb + s * B_TILE, &mapB, &full[st], kx, (int)(nb * BN), plane);
                     }
                 }
             }
@@ -277,9 +283,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         // per 32-byte k-slice instead of 21, each A tile read from shared memory
         // once per 240 columns instead of once per 80.
         constexpr uint32_t kAmn = AMN ? (1u << 15) : 0u;
-        constexpr uint32_t kIdesc1 = idesc_i8<kBM, kBN>() | kAmn;
-        constexpr uint32_t kIdesc2 = idesc_i8<kBM, 2 * kBN>() | kAmn;
-        constexpr uint32_t kIdesc3 = idesc_i8<kBM, 3 * kBN>() | kAmn;
+        constexpr uint32_t kIdesc1 = idesc_i8<kBM, BN>() | kAmn;
+        constexpr uint32_t kIdesc2 = idesc_i8<kBM, 2 * BN>() | kAmn;
+        constexpr uint32_t kIdesc3 = idesc_i8<kBM, 3 * BN>() | kAmn;
         int64_t g = 0, cg = 0;  // stage and digit-block counters across items
         for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
             for (int64_t cc = 0; cc < per; ++cc, ++cg) {
@@ -299,16 +305,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                             // digit 1 of A spans every level: its MMAs start the block
                             const uint32_t acc0 = (kb > 0 || kk > 0) ? 1u : 0u;
 #pragma unroll
-                            for (int i = 1; i <= kS; ++i) {
+                            for (int i = 1; i <= NL; ++i) {
                                 const uint64_t da = AMN ? sdesc_mn_sw64(sa + (i - 1) * A_TILE + kk * 2048, 4096)
                                                         : sdesc_k_sw64(sa + (i - 1) * A_TILE) + (uint64_t)(kk * 2);
-                                const int jmax = kS + 1 - i;  // levels i + j <= S + 1
+                                const int jmax = NL + 1 - i;  // levels i + j <= NL + 1
 #pragma unroll
                                 for (int j0 = 1; j0 <= jmax; j0 += 3) {
                                     const int nj = jmax - j0 + 1 < 3 ? jmax - j0 + 1 : 3;
                                     const uint32_t idesc = nj == 3 ? kIdesc3 : (nj == 2 ? kIdesc2 : kIdesc1);
                                     const uint64_t db = sdesc_k_sw64(sb + (j0 - 1) * B_TILE) + (uint64_t)(kk * 2);
-                                    mma_i8(tmem + (uint32_t)((i + j0 - 2) * kBN), da, db, idesc, i == 1 ? acc0 : 1u);
+                                    mma_i8(tmem + (uint32_t)((i + j0 - 2) * BN), da, db, idesc, i == 1 ? acc0 : 1u);
                                 }
                             }
                         }
@@ -324,14 +330,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         // epilogue: warp w drains TMEM lanes 32*(w%4) .. +32 (rows of the
         // tile), columns [h*40, h*40 + 40) with h = (w - 2) / 4
         const int q = warp & 3, h = (warp - 2) >> 2;
-        constexpr int NH = kBN / 2;
+        constexpr int NH = BN / 2;
         int64_t cg = 0;
         double rsd = 0.0, rsx = 0.0;  // RESID: this thread's residual sums
         for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
             int64_t ob, mb, nb;
             decode_item<SYM>(P, item, ob, mb, nb);
             const int64_t m = mb * kBM + q * 32 + lane;
-            const int64_t n0 = nb * kBN + h * NH;
+            const int64_t n0 = nb * BN + h * NH;
             const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(h * NH);
             if constexpr (!SYM) {
                 // one digit block per item (per == 1): each 8-column chunk goes
@@ -350,9 +356,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 double* C = RESID ? nullptr : P.C + ob * P.strideC;
 #pragma unroll
                 for (int c = 0; c < NH / 8; ++c) {  // all six levels of 8 columns in flight
-                    int32_t v[kS][8];
+                    int32_t v[NL][8];
 #pragma unroll
-                    for (int l = 0; l < kS; ++l) tmem_ld_32x32b_x8(ta + (uint32_t)(l * kBN + c * 8), v[l]);
+                    for (int l = 0; l < NL; ++l) tmem_ld_32x32b_x8(ta + (uint32_t)(l * BN + c * 8), v[l]);
                     tmem_ld_wait();
 #pragma unroll
                     for (int jj = 0; jj < 8; ++jj) {
@@ -360,7 +366,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const int64_t n = n0 + j;
                         double inner = 0.0;
 #pragma unroll
-                        for (int l = kS - 1; l >= 0; --l)  // smallest weight first
+                        for (int l = NL - 1; l >= 0; --l)  // smallest weight first
                             inner = fma((double)v[l][jj], ldexp(1.0, -14 - 8 * l), inner);
                         const double val = (inner * sm) * (n < P.N ? sc[n] : 0.0);
                         if constexpr (RESID) {  // columns past N: x = val = 0
@@ -388,9 +394,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const double* sc = P.sb + blk * P.N;
 #pragma unroll
                     for (int c = 0; c < NH / 8; ++c) {
-                        int32_t v[kS][8];
+                        int32_t v[NL][8];
 #pragma unroll
-                        for (int l = 0; l < kS; ++l) tmem_ld_32x32b_x8(ta + (uint32_t)(l * kBN + c * 8), v[l]);
+                        for (int l = 0; l < NL; ++l) tmem_ld_32x32b_x8(ta + (uint32_t)(l * BN + c * 8), v[l]);
                         tmem_ld_wait();
 #pragma unroll
                         for (int jj = 0; jj < 8; ++jj) {
@@ -398,7 +404,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             const int64_t n = n0 + j;
                             double inner = 0.0;
 #pragma unroll
-                            for (int l = kS - 1; l >= 0; --l)
+                            for (int l = NL - 1; l >= 0; --l)
                                 inner = fma((double)v[l][jj], ldexp(1.0, -14 - 8 * l), inner);
                             // the diagonal of a Gram from the FP64 sums of squares: its
                             // dropped same-digit pair products are squares (biased > 0)
@@ -492,18 +498,18 @@ bool ozaki_enabled() {
 
 int64_t ozaki_grid(int64_t items) { return std::min<int64_t>(items, ctx().sms); }  // one persistent CTA per SM
 
-template <bool SYM, bool AMN = false, bool RESID = false>
+template <bool SYM, bool AMN = false, bool RESID = false, int BN = kBN, int NL = kS>
 void launch_mma(const CUtensorMap& ma, const CUtensorMap& mb, const OzParams& P, int64_t items, cudaStream_t s) {
     // stages + barriers + TMEM slot + the epilogue warps' residual sums
-    const size_t smem = 1024 + (size_t)kStages * kS * (kBM + kBN) * kBK + (2 * kStages + 2) * 8 + 16 + 16 * kEpiWarps;
+    const size_t smem = 1024 + (size_t)kStages * kS * (kBM + BN) * kBK + (2 * kStages + 2) * 8 + 16 + 16 * kEpiWarps;
     static bool attr = false;
     if (!attr) {
-        PPC_CUDA_CHECK(cudaFuncSetAttribute(ozaki_mma_kernel<SYM, AMN, RESID>,
+        PPC_CUDA_CHECK(cudaFuncSetAttribute(ozaki_mma_kernel<SYM, AMN, RESID, BN, NL>,
                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = true;
     }
     if (items == 0) return;
-    ozaki_mma_kernel<SYM, AMN, RESID><<<(unsigned)ozaki_grid(items), kThreads, smem, s>>>(ma, mb, P, items);
+    ozaki_mma_kernel<SYM, AMN, RESID, BN, NL><<<(unsigned)ozaki_grid(items), kThreads, smem, s>>>(ma, mb, P, items);
     count_launch();
     check_launch("ozaki_mma");
 }
@@ -572,17 +578,22 @@ void OzakiDigits::split(const double* X, int64_t ldx, int64_t stride, int64_t ro
 }
 
 void ozaki_gemm(const OzakiDigits& A, const OzakiDigits& B, int64_t nbatch, const int* zmap, double* C, int64_t ldc,
-                int64_t strideC, cudaStream_t s) {
+                int64_t strideC, cudaStream_t s, int levels) {
     if (A.KCp != B.KCp) fail(PPC_ARGUMENT, "ozaki_gemm: K mismatch");
+    if (levels != kS && levels != 4) fail(PPC_ARGUMENT, "ozaki_gemm: levels must be 6 or 4");
+    // 64-wide output tiles for panels of <= 64 columns (the 80-wide tile
+    // would spend a fifth of the MMAs on zero rows)
+    const int bn = (B.cols <= 64) ? 64 : kBN;
+    if (levels != kS && bn != 64) fail(PPC_ARGUMENT, "ozaki_gemm: reduced levels need <= 64 columns");
     CUtensorMap ma, mb;
     if (!make_digit_map(&ma, A.D.as<int8_t>(), A.KCp, A.cols, A.nblk * kS, kBM) ||
-        !make_digit_map(&mb, B.D.as<int8_t>(), B.KCp, B.cols, B.nblk * kS, kBN))
+        !make_digit_map(&mb, B.D.as<int8_t>(), B.KCp, B.cols, B.nblk * kS, bn))
         fail(PPC_CUDA, "ozaki: tensor map encoding failed");
     OzParams P;
     P.M = A.cols;
     P.N = B.cols;
     P.mtiles = (P.M + kBM - 1) / kBM;
-    P.tiles = P.mtiles * ((P.N + kBN - 1) / kBN);
+    P.tiles = P.mtiles * ((P.N + bn - 1) / bn);
     P.KCp = A.KCp;
     P.per = 1;
     P.zmap = zmap;
@@ -596,9 +607,12 @@ void ozaki_gemm(const OzakiDigits& A, const OzakiDigits& B, int64_t nbatch, cons
     P.ldx = P.strideX = P.m_total = 0;
     P.partial = nullptr;
     const double K = (double)std::min(A.rows, kKC);
-    StageTimer tk("ozaki_gemm", s, 2.0 * kS * (kS + 1) / 2 * (double)nbatch * P.M * P.N * K,
-                  (double)kS * nbatch * (P.M + P.N) * K);
-    launch_mma<false>(ma, mb, P, nbatch * P.tiles, s);
+    StageTimer tk(levels == kS ? "ozaki_gemm" : "ozaki_gemm_l4", s,
+                  2.0 * levels * (levels + 1) / 2 * (double)nbatch * P.M * P.N * K,
+                  (double)levels * nbatch * (P.M + P.N) * K);
+    if (bn == kBN) launch_mma<false>(ma, mb, P, nbatch * P.tiles, s);
+    else if (levels == kS) launch_mma<false, false, false, 64, kS>(ma, mb, P, nbatch * P.tiles, s);
+    else launch_mma<false, false, false, 64, 4>(ma, mb, P, nbatch * P.tiles, s);
 }
 
 bool ozaki_gemm_eligible(int64_t M, int64_t K) { return ozaki_enabled() && M >= kBM && K >= 256 && K <= kKC; }

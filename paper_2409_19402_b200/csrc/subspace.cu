@@ -84,11 +84,12 @@ __global__ void cheb_kernel(double* __restrict__ Yn, const double* __restrict__ 
     }
 }
 
-// P(i, j, s) *= w(i, s)   (rows of the b x cols block scaled: Theta_L mask)
-__global__ void scale_rows_kernel(double* P, const double* w, int64_t b, int64_t cols, int64_t total) {
+// P(i, j, s) *= w(i, s)   (rows of the lp x cols block scaled: Theta_L mask;
+// w has stride b per slice)
+__global__ void scale_rows_kernel(double* P, const double* w, int64_t lp, int64_t b, int64_t cols, int64_t total) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
-        const int64_t row = i % b, s = i / (b * cols);
+        const int64_t row = i % lp, s = i / (lp * cols);
         P[i] *= w[row + s * b];
     }
 }
@@ -443,6 +444,13 @@ void rayleigh_ritz(Work& w, const double* G, int64_t sG, double* Xn, int64_t c0,
 
 }  // namespace
 
+// Reduced-precision filter products while every unlocked residual of a slice
+// exceeds this fraction of its theta_1 (PPC_FILTER_LOWP; 0 disables).
+static double filter_lowp() {
+    static const double v = std::getenv("PPC_FILTER_LOWP") ? std::atof(std::getenv("PPC_FILTER_LOWP")) : 1e-6;
+    return v;
+}
+
 // Chebyshev degree cap per outer iteration (runtime-tunable for experiments)
 static double max_degree(bool basis) {
     static const double v = std::getenv("PPC_CHEB_MAX") ? std::atof(std::getenv("PPC_CHEB_MAX")) : 10.0;
@@ -517,6 +525,11 @@ void subspace_eig_top(const double* G, int64_t r, int64_t batch, int64_t k, doub
         for (int64_t i = 0; i < b * batch; ++i) energy += std::max(th[i], 0.0);
         std::vector<int> deg(batch, 0);
         bool near_floor = false;
+        // slices whose unlocked residuals are still far above the reduced
+        // filter's precision floor (~1e-9 |G|): their products take 4 digit
+        // levels (half the MMAs); locking always uses FP64 Rayleigh-Ritz
+        // residuals, so this only steers the iteration
+        std::vector<char> lowp(batch, 0);
         std::vector<double> cc(batch), ee(batch);
         for (int64_t sl = 0; sl < batch; ++sl) {
             const double* t = &th[sl * b];
@@ -600,6 +613,11 @@ void subspace_eig_top(const double* G, int64_t r, int64_t batch, int64_t k, doub
             // in FP64 from here on
             for (int64_t j = L; j < k; ++j)
                 if (rr[j] <= 1e-11 * scale) near_floor = true;
+            if (vectors_for_reconstruction && filter_lowp() > 0.0) {
+                double rmin = 1e300;
+                for (int64_t j = L; j < k; ++j) rmin = std::min(rmin, rr[j]);
+                lowp[sl] = rmin > filter_lowp() * scale;
+            }
             // Chebyshev interval [0, ub]: damp everything below the smallest Ritz value
             const double ub = std::max(t[b - 1], 0.0);
             const double c = 0.5 * ub, e = std::max(0.5 * ub, 1e-300 * scale);
@@ -659,10 +677,15 @@ void subspace_eig_top(const double* G, int64_t r, int64_t batch, int64_t k, doub
                 }
             }
         if ((int64_t)coef.size() * 8 > (int64_t)w.coef.bytes()) w.coef = DeviceBuffer(coef.size() * sizeof(double));
-        std::vector<int> zm((size_t)dmax * batch), nact(dmax, 0);
+        // per degree: every filtering slice | the reduced-precision ones | the rest
+        std::vector<int> zm((size_t)3 * dmax * batch), nact(dmax, 0), nlo(dmax, 0), nhi(dmax, 0);
         for (int j = 0; j < dmax; ++j)
             for (int64_t sl = 0; sl < batch; ++sl)
-                if (j < deg[sl]) zm[(size_t)j * batch + nact[j]++] = (int)sl;
+                if (j < deg[sl]) {
+                    zm[(size_t)j * batch + nact[j]++] = (int)sl;
+                    if (lowp[sl]) zm[(size_t)(dmax + j) * batch + nlo[j]++] = (int)sl;
+                    else zm[(size_t)(2 * dmax + j) * batch + nhi[j]++] = (int)sl;
+                }
         if ((int64_t)zm.size() * 4 > (int64_t)w.zmap.bytes()) w.zmap = DeviceBuffer(zm.size() * sizeof(int));
         PPC_CUDA_CHECK(cudaMemcpyAsync(w.zmap.d(), zm.data(), sizeof(int) * zm.size(), cudaMemcpyHostToDevice, s));
         PPC_CUDA_CHECK(cudaMemcpyAsync(w.coef.d(), coef.data(), sizeof(double) * coef.size(), cudaMemcpyHostToDevice, s));
@@ -680,6 +703,9 @@ void subspace_eig_top(const double* G, int64_t r, int64_t batch, int64_t k, doub
                 if (deg[sl] > 0) cf = std::min<int64_t>(cf, nlock[sl]);
             if (cf >= b) cf = 0;
             const int64_t bf = b - cf;
+            int64_t lmax = 0;
+            for (int64_t sl = 0; sl < batch; ++sl)
+                if (deg[sl] > 0) lmax = std::max<int64_t>(lmax, nlock[sl]);
             for (int j = 0; j < dmax; ++j) {
                 // only the slices still filtering at this degree (compacted batch)
                 const int na = nact[j];
@@ -688,18 +714,29 @@ void subspace_eig_top(const double* G, int64_t r, int64_t batch, int64_t k, doub
                     // Z = G Y, P = X^T Y, Z -= X diag(theta_L) P   (columns [cf, b))
                     if (oz_filter && !near_floor) {
                         Yd.split(Y + cf * r, r, per, r, bf, r, batch, s, zm, na);
-                        ozaki_gemm(Gd, Yd, na, zm, w.Z.d() + cf * r, r, per, s);
+                        const int* zlo = w.zmap.as<int>() + (int64_t)(dmax + j) * batch;
+                        const int* zhi = w.zmap.as<int>() + (int64_t)(2 * dmax + j) * batch;
+                        if (bf <= 64 && nlo[j] > 0) {
+                            ozaki_gemm(Gd, Yd, nlo[j], zlo, w.Z.d() + cf * r, r, per, s, 4);
+                            if (nhi[j] > 0) ozaki_gemm(Gd, Yd, nhi[j], zhi, w.Z.d() + cf * r, r, per, s);
+                        } else {
+                            ozaki_gemm(Gd, Yd, na, zm, w.Z.d() + cf * r, r, per, s);
+                        }
                     } else {
                         gg(G, r, r * r, false, Y + cf * r, r, per, w.Z.d() + cf * r, r, per, r, bf, r, na, 1.0, 0.0,
                            s, zm, batch);
                     }
-                    gg(w.X.d(), r, per, true, Y + cf * r, r, per, w.P.d(), b, b * bf, b, bf, r, na, 1.0, 0.0, s,
-                       zm, batch);
-                    scale_rows_kernel<<<grid1(b * bf * batch), 256, 0, s>>>(w.P.d(), w.wmask.d(), b, bf,
-                                                                             b * bf * batch);
-                    count_launch();
-                    gg(w.X.d(), r, per, false, w.P.d(), b, b * bf, w.Z.d() + cf * r, r, per, r, bf, b, na, -1.0, 1.0,
-                       s, zm, batch);
+                    // deflation over the locked columns only (lmax: most locked among
+                    // the filtered slices; none locked -> nothing to deflate)
+                    if (lmax > 0) {
+                        gg(w.X.d(), r, per, true, Y + cf * r, r, per, w.P.d(), lmax, lmax * bf, lmax, bf, r, na, 1.0,
+                           0.0, s, zm, batch);
+                        scale_rows_kernel<<<grid1(lmax * bf * batch), 256, 0, s>>>(w.P.d(), w.wmask.d(), lmax, b, bf,
+                                                                                    lmax * bf * batch);
+                        count_launch();
+                        gg(w.X.d(), r, per, false, w.P.d(), lmax, lmax * bf, w.Z.d() + cf * r, r, per, r, bf, lmax, na,
+                           -1.0, 1.0, s, zm, batch);
+                    }
                 }
                 // only the slices still filtering at this degree; a slice that
                 // stops keeps its block in its own buffer of the rotation
