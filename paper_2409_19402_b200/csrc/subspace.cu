@@ -413,14 +413,27 @@ namespace {
 
 // Rayleigh-Ritz on the orthonormal active columns [c0, b) of Xn: X, theta,
 // W = G X and residual norms for those columns (locked ones keep theirs).
+// Gd (nullable): G's Ozaki digits; then Z = G Xn runs on the INT8 tensor
+// cores at full digit depth (~1e-14 |G|, far below every residual the
+// caller still acts on; it passes nullptr near the lock thresholds).
 void rayleigh_ritz(Work& w, const double* G, int64_t sG, double* Xn, int64_t c0, cudaStream_t s,
-                   double gtol_rel, int sweep_cap, const int* zm = nullptr, int64_t na = -1) {
+                   double gtol_rel, int sweep_cap, const int* zm = nullptr, int64_t na = -1,
+                   const OzakiDigits* Gd = nullptr, OzakiDigits* Xd = nullptr) {
     const int64_t r = w.r, b = w.b, bc = b - c0, per = r * b;
     const int64_t batch = na < 0 ? w.batch : na;  // launched slices (zm: which ones)
     const int64_t zx = w.batch;
     StageTimer tm(w.basis ? "sq.rayleigh_ritz" : "ss.rayleigh_ritz", s);
-    gg(G, r, sG, false, Xn + c0 * r, r, per, w.Z.d() + c0 * r, r, per, r, bc, r, batch, 1.0, 0.0, s, zm,
-       zx);  // Z = G Xn
+    if (Gd && Xd && bc <= 64) {
+        Xd->split(Xn + c0 * r, r, per, r, bc, r, zx, s, zm, zm ? batch : 0);
+        if (zm) {
+            ozaki_gemm(*Gd, *Xd, batch, zm, w.Z.d() + c0 * r, r, per, s);
+        } else {
+            ozaki_gemm(*Gd, *Xd, batch, nullptr, w.Z.d() + c0 * r, r, per, s);
+        }
+    } else {
+        gg(G, r, sG, false, Xn + c0 * r, r, per, w.Z.d() + c0 * r, r, per, r, bc, r, batch, 1.0, 0.0, s, zm,
+           zx);  // Z = G Xn
+    }
     gg(Xn + c0 * r, r, per, true, w.Z.d() + c0 * r, r, per, w.S.d(), bc, bc * bc, bc, bc, r, batch, 1.0, 0.0, s,
        zm, zx);
     {
@@ -508,7 +521,7 @@ void subspace_eig_top(const double* G, int64_t r, int64_t batch, int64_t k, doub
     cholqr3(w, w.Y.d(), w.Yp.d(), 0, s);
     const double gtol_rel = vectors_for_reconstruction ? 0.0 : 1e-14;
     // early Rayleigh-Ritz steps only steer the filter: 4 Jacobi sweeps
-    rayleigh_ritz(w, G, r * r, w.Yp.d(), 0, s, gtol_rel, 4);
+    rayleigh_ritz(w, G, r * r, w.Yp.d(), 0, s, gtol_rel, 4, nullptr, -1, oz_filter ? &Gd : nullptr, &Yd);
 
     std::vector<double> th(b * batch), res(b * batch), coef(3 * batch), wm(b * batch),
         thp(b * batch, 0.0);
@@ -797,7 +810,8 @@ void subspace_eig_top(const double* G, int64_t r, int64_t batch, int64_t k, doub
         // approximate Ritz pairs until something has converged (locking uses
         // true residuals, so an inexact early Rayleigh-Ritz cannot lock early)
         const bool early = it < 2 && c0 == 0;
-        rayleigh_ritz(w, G, r * r, Xn, c0, s, gtol_rel, early ? 4 : 0, zact, nact0);
+        rayleigh_ritz(w, G, r * r, Xn, c0, s, gtol_rel, early ? 4 : 0, zact, nact0,
+                      (oz_filter && !near_floor) ? &Gd : nullptr, &Yd);
     }
     // outputs: leading k Ritz pairs
     PPC_CUDA_CHECK(cudaMemcpy2DAsync(Xout, sizeof(double) * r * k, w.X.d(), sizeof(double) * per,
