@@ -545,7 +545,7 @@ int ppc_tsvdq_compress(const double* A, int64_t n1, int64_t n2, int64_t n3, int6
         const int64_t N = n1 * n2;
         Out q(Q, n3 * p, loc), sg(sigma, sigma ? p : 0, loc), u(U, n1 * k * p, loc),
             sv(S, k * p, loc), v(V, n2 * k * p, loc);
-        DeviceBuffer abuf;
+        DeviceBuffer abuf, est(sizeof(double) * 4);  // trace(G), slice residual, ||Ahat||^2
         const double* dA = A;
         if (loc == PPC_HOST) {
             // Stream the input in row-chunk groups on a copy stream and start
@@ -595,14 +595,13 @@ int ppc_tsvdq_compress(const double* A, int64_t n1, int64_t n2, int64_t n3, int6
                 nf.check(s, "svd");
             else
                 require_finite(dA, N * n3, "svd", s);
+            gram_trace(parts.d(), n3, est.d(), s);
             eig_to_basis(parts.d(), n3, p, q.d, sigma ? sg.d : nullptr, s);
         } else {
-            data_q(dA, N, n3, p, q.d, sigma ? sg.d : nullptr, s, true);
+            data_q(dA, N, n3, p, q.d, sigma ? sg.d : nullptr, s, true, est.d());
         }
-        tsvdq(dA, n1, n2, n3, q.d, p, k, u.d, sv.d, v.d, s);
-        const auto r = recon_residual(dA, n1, n2, n3, u.d, sv.d, v.d, q.d, p, k, s);
-        if (r[1] == 0.0) fail(PPC_DEGENERATE, "relative_error: reference tensor is zero");
-        *re = std::sqrt(r[0]) / std::sqrt(r[1]);
+        tsvdq(dA, n1, n2, n3, q.d, p, k, u.d, sv.d, v.d, s, est.d() + 1);
+        *re = compress_relative_error(dA, n1, n2, n3, u.d, sv.d, v.d, q.d, p, k, est.d(), s);
         q.finish();
         if (sigma) sg.finish();
         u.finish();

@@ -2,6 +2,7 @@
 // FP64 DMMA kernel (dmma_gemm.cuh); reductions are fixed-order.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "dmma_gemm.cuh"
@@ -289,8 +290,23 @@ std::array<double, 2> recon_residual_block(const double* A_blk, int64_t n1, int6
     return out;
 }
 
+double compress_relative_error(const double* A, int64_t n1, int64_t n2, int64_t n3, const double* U,
+                               const double* S, const double* V, const double* Q, int64_t p, int64_t k,
+                               const double* est, cudaStream_t s) {
+    static const bool identity = !(std::getenv("PPC_RE_IDENTITY") && std::getenv("PPC_RE_IDENTITY")[0] == '0');
+    double h[3];
+    PPC_CUDA_CHECK(cudaMemcpyAsync(h, est, sizeof(h), cudaMemcpyDeviceToHost, s));
+    PPC_CUDA_CHECK(cudaStreamSynchronize(s));
+    if (h[0] == 0.0) fail(PPC_DEGENERATE, "relative_error: reference tensor is zero");
+    const double num = (h[0] - h[2]) + h[1];
+    if (identity && std::isfinite(num) && num >= 2e-3 * h[0]) return std::sqrt(num) / std::sqrt(h[0]);
+    const auto r = recon_residual(A, n1, n2, n3, U, S, V, Q, p, k, s);
+    if (r[1] == 0.0) fail(PPC_DEGENERATE, "relative_error: reference tensor is zero");
+    return std::sqrt(r[0]) / std::sqrt(r[1]);
+}
+
 void tsvdq(const double* A, int64_t n1, int64_t n2, int64_t n3, const double* Q, int64_t p,
-           int64_t k, double* U, double* S, double* V, cudaStream_t s) {
+           int64_t k, double* U, double* S, double* V, cudaStream_t s, double* slice_sums) {
     const int64_t N = n1 * n2;
     DeviceBuffer ah(sizeof(double) * N * p);
     mode3(A, N, n3, Q, p, true, ah.d(), 1.0, s);  // decompositions.cpp:65
@@ -299,6 +315,21 @@ void tsvdq(const double* A, int64_t n1, int64_t n2, int64_t n3, const double* Q,
         StageTimer tm("slice_svd", s, (double)p * std::min(n1, n2) * std::min(n1, n2) * std::max(n1, n2) +
                                           4.0 * p * N * k, 8.0 * p * N);
         slice_svd(ah.d(), n1, n2, N, p, k, U, S, V, nullptr, s);  // :75-81
+    }
+    if (slice_sums) {
+        // {sum_i ||Ahat_i - U_i S_i V_i^T||^2, ||Ahat||^2} over every slice, one fused pass
+        StageTimer tm("slice_residual", s, 2.0 * p * N * k, 8.0 * p * N);
+        DeviceBuffer us(sizeof(double) * n1 * k * p);
+        launch_scale_columns(U, S, us.d(), n1, k, p, s);
+        GemmDesc d;
+        d.M = n1; d.N = n2; d.K = k; d.batch = p;
+        d.A = us.d(); d.lda = n1; d.strideA = n1 * k;
+        d.B = V; d.ldb = n2; d.strideB = n2 * k; d.b_nmajor = true;
+        d.allow_ws = false;
+        const int64_t ctas = gemm_residual_ctas(d, ah.d(), n1, N);
+        DeviceBuffer part(sizeof(double) * 2 * ctas);
+        gemm_residual(d, ah.d(), n1, N, part.d(), s);
+        launch_reduce_pairs(part.d(), ctas, slice_sums, s);
     }
 }
 

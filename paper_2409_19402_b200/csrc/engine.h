@@ -65,8 +65,11 @@ std::array<double, 2> recon_residual_block(const double* A_blk, int64_t n1, int6
 // transforms.cpp:97-115 on the device. Returns completed_basis.
 // check_finite: fail with PPC_NUMERIC on NaN / Inf in T (the svd guard,
 // matrix_kernels.cpp:32), folded into the Gram's pass over T where it can be.
+// gtrace (device, nullable): trace(G) = ||T||_F^2, from the Gram's diagonal.
 bool data_q(const double* T, int64_t N, int64_t n3, int64_t p, double* Q, double* sigma,
-            cudaStream_t s, bool check_finite = false);
+            cudaStream_t s, bool check_finite = false, double* gtrace = nullptr);
+// out (device scalar) = trace of the n x n matrix G, fixed summation order.
+void gram_trace(const double* G, int64_t n, double* out, cudaStream_t s);
 // Finiteness flag for gram / gram_chunks: reset, then test (fails loudly).
 struct FiniteFlag {
     int* flag;
@@ -76,8 +79,20 @@ struct FiniteFlag {
 };
 
 // decompositions.cpp:62-83
+// relative_error(A, tsvdq_reconstruct(F)) of the compress chain (metrics.cpp:21-28).
+// With Q orthonormal, A - A_k splits into orthogonal parts,
+//   ||A - A_k||^2 = (||A||^2 - ||Ahat||^2) + sum_i ||Ahat_i - U_i S_i V_i^T||^2,
+// est (device) = {||A||^2 from the Gram trace, the slice residual, ||Ahat||^2}.
+// The difference carries ~3e-15 ||A||^2 of rounding, <= 1e-12 relative in RE
+// once RE^2 >= 2e-3; below that (or PPC_RE_IDENTITY=0) the residual is
+// measured directly against the reconstruction (fused GEMM over A).
+double compress_relative_error(const double* A, int64_t n1, int64_t n2, int64_t n3, const double* U,
+                               const double* S, const double* V, const double* Q, int64_t p, int64_t k,
+                               const double* est, cudaStream_t s);
+// slice_sums (device, nullable, 2 doubles): {sum_i ||Ahat_i - U_i S_i V_i^T||^2, ||Ahat||^2},
+// measured directly on the transform-domain slices (fused residual GEMM).
 void tsvdq(const double* A, int64_t n1, int64_t n2, int64_t n3, const double* Q, int64_t p,
-           int64_t k, double* U, double* S, double* V, cudaStream_t s);
+           int64_t k, double* U, double* S, double* V, cudaStream_t s, double* slice_sums = nullptr);
 // Chat (n1 x n2 x p) = U diag(S) V^T facewise             [decompositions.cpp:88-92]
 // over the leading k columns of factor stacks that carry kstride >= k
 // columns per slice (kstride 0 = k).

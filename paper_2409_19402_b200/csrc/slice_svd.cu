@@ -182,8 +182,32 @@ void eig_to_basis(const double* G, int64_t n3, int64_t p, double* Q, double* sig
     }
 }
 
+namespace {
+__global__ void trace_kernel(const double* __restrict__ G, int64_t n, double* __restrict__ out) {
+    __shared__ double red[32];
+    double a = 0.0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) a += G[i + i * n];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        a = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+        if (threadIdx.x == 0) *out = a;
+    }
+}
+}  // namespace
+
+void gram_trace(const double* G, int64_t n, double* out, cudaStream_t s) {
+    trace_kernel<<<1, 256, 0, s>>>(G, n, out);
+    count_launch();
+    check_launch("trace");
+}
+
 bool data_q(const double* T, int64_t N, int64_t n3, int64_t p, double* Q, double* sigma,
-            cudaStream_t s, bool check_finite) {
+            cudaStream_t s, bool check_finite, double* gtrace) {
     DeviceBuffer G(sizeof(double) * n3 * n3);
     if (check_finite) {
         FiniteFlag nf(s);
@@ -194,6 +218,7 @@ bool data_q(const double* T, int64_t N, int64_t n3, int64_t p, double* Q, double
     } else {
         gram(T, N, n3, G.d(), s);
     }
+    if (gtrace) gram_trace(G.d(), n3, gtrace, s);
     // When p > min(n3, N) the unfolding has only min(n3, N) singular vectors;
     // the eigenvectors of G for its zero eigenvalues complete the basis
     // (transforms.cpp:104-111 pads with an orthonormal completion).

@@ -1021,3 +1021,21 @@ def test_nonfinite_input_rejected(engine, shape, val):
     a[n1 // 3, n2 - 1, n3 // 2] = 0.0
     t = engine.data_dependent_transform(a, 8)  # clean input passes again
     assert np.isfinite(t.q).all()
+
+
+@pytest.mark.gpu
+def test_compress_re_identity_matches_direct(engine):
+    """ppc_tsvdq_compress takes RE from the orthogonal split
+    ||A - A_k||^2 = (||A||^2 - ||Ahat||^2) + sum_i ||Ahat_i - U_i S_i V_i^T||^2
+    (Q orthonormal) when RE^2 >= 2e-3, and measures it against the
+    reconstruction otherwise; both must equal the directly measured
+    relative_error(A, tsvdq_reconstruct(F))."""
+    cases = [((256, 192, 128), 32, 8, 1e-3),   # RE ~ 0.3: identity
+             ((192, 160, 96), 64, 4, 1e-2),    # noisy, many noise slices: identity
+             ((128, 128, 64), 48, 24, 1e-9)]   # rank 20 < k: RE ~ 1e-9, direct fallback
+    for shape, p, k, noise in cases:
+        a = synth.cp_tensor(*shape, rank=20, noise=noise, seed=5)
+        da = engine.to_device(a)
+        f, re = engine.compress_tsvdq(da, p, k)
+        red = engine.tsvdq_relative_error(da, f)
+        assert abs(re - red) <= 1e-12 * red, (shape, re, red)
