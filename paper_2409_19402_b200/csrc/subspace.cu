@@ -496,7 +496,8 @@ void slice_tail_energy(const double* A, int64_t m, int64_t n, int64_t stride, in
 void subspace_eig_top(const double* G, int64_t r, int64_t batch, int64_t k, double* Xout,
                       double* lambda, cudaStream_t s, bool vectors_for_reconstruction) {
     static const bool dbg = std::getenv("PPC_SUBSPACE_DEBUG") != nullptr;
-    int64_t b = k + std::max<int64_t>(k, 16);
+    static const int64_t guard_env = std::getenv("PPC_SUBSPACE_GUARD") ? std::atoll(std::getenv("PPC_SUBSPACE_GUARD")) : 0;
+    int64_t b = k + (guard_env > 0 ? guard_env : std::max<int64_t>(k, 16));
     b = (b + 7) / 8 * 8;
     if (b >= r || r <= 8) {
         // the block would cover the space: full Jacobi eigendecomposition
