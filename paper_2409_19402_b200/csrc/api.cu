@@ -11,6 +11,7 @@
 #include "jacobi.cuh"
 #include "kernels.cuh"
 #include "engine.h"
+#include "ozaki.h"
 #include "slice_svd.cuh"
 
 using namespace ppc;
@@ -546,6 +547,7 @@ int ppc_tsvdq_compress(const double* A, int64_t n1, int64_t n2, int64_t n3, int6
         Out q(Q, n3 * p, loc), sg(sigma, sigma ? p : 0, loc), u(U, n1 * k * p, loc),
             sv(S, k * p, loc), v(V, n2 * k * p, loc);
         DeviceBuffer abuf, est(sizeof(double) * 4);  // trace(G), slice residual, ||Ahat||^2
+        OzakiDigits tdig;  // A's Gram digits, reused by the forward transform (device path)
         const double* dA = A;
         if (loc == PPC_HOST) {
             // Stream the input in row-chunk groups on a copy stream and start
@@ -598,9 +600,10 @@ int ppc_tsvdq_compress(const double* A, int64_t n1, int64_t n2, int64_t n3, int6
             gram_trace(parts.d(), n3, est.d(), s);
             eig_to_basis(parts.d(), n3, p, q.d, sigma ? sg.d : nullptr, s);
         } else {
-            data_q(dA, N, n3, p, q.d, sigma ? sg.d : nullptr, s, true, est.d());
+            data_q(dA, N, n3, p, q.d, sigma ? sg.d : nullptr, s, true, est.d(), &tdig);
         }
-        tsvdq(dA, n1, n2, n3, q.d, p, k, u.d, sv.d, v.d, s, est.d() + 1);
+        tsvdq(dA, n1, n2, n3, q.d, p, k, u.d, sv.d, v.d, s, est.d() + 1, &tdig);
+        tdig = OzakiDigits();  // the 7-digit split of A (30 GB at cfg5) is not needed past the transform
         *re = compress_relative_error(dA, n1, n2, n3, u.d, sv.d, v.d, q.d, p, k, est.d(), s);
         q.finish();
         if (sigma) sg.finish();

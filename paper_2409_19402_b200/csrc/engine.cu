@@ -306,10 +306,12 @@ double compress_relative_error(const double* A, int64_t n1, int64_t n2, int64_t 
 }
 
 void tsvdq(const double* A, int64_t n1, int64_t n2, int64_t n3, const double* Q, int64_t p,
-           int64_t k, double* U, double* S, double* V, cudaStream_t s, double* slice_sums) {
+           int64_t k, double* U, double* S, double* V, cudaStream_t s, double* slice_sums,
+           const OzakiDigits* tdig) {
     const int64_t N = n1 * n2;
     DeviceBuffer ah(sizeof(double) * N * p);
-    mode3(A, N, n3, Q, p, true, ah.d(), 1.0, s);  // decompositions.cpp:65
+    if (!(tdig && ozaki_mode3_forward(*tdig, N, Q, p, ah.d(), s)))
+        mode3(A, N, n3, Q, p, true, ah.d(), 1.0, s);  // decompositions.cpp:65
     require_finite(ah.d(), N * p, "svd", s);       // matrix_kernels.cpp:32
     {
         StageTimer tm("slice_svd", s, (double)p * std::min(n1, n2) * std::min(n1, n2) * std::max(n1, n2) +

@@ -45,7 +45,11 @@ void slice_svd(const double* A, int64_t m, int64_t n, int64_t stride, int64_t ba
 // nonfinite (nullable device int): when the Gram's own pass over T can also
 // detect NaN / Inf it sets *nonfinite on a hit and gram returns true; false
 // means T was not checked.
-bool gram(const double* T, int64_t N, int64_t n3, double* G, cudaStream_t s, int* nonfinite = nullptr);
+struct OzakiDigits;
+// keep (nullable): T's 7-digit split is left there when the INT8 Gram path
+// ran on whole 4096-row blocks (reused by the forward transform).
+bool gram(const double* T, int64_t N, int64_t n3, double* G, cudaStream_t s, int* nonfinite = nullptr,
+          OzakiDigits* keep = nullptr);
 // Top-p eigenpairs of a symmetric PSD n x n matrix G: Q (n x p), lambda (p).
 // accurate_vectors: lock on the subspace (rank-p truncation) criteria rather
 // than on eigenvalues alone.
@@ -53,7 +57,8 @@ void sym_eig_top(const double* G, int64_t n, int64_t p, double* Q, double* lambd
                  bool accurate_vectors = false);
 // Partial Grams of nchunks consecutive row chunks (T rows x n3, leading dim ldT).
 bool gram_chunks(const double* T, int64_t ldT, int64_t rows, int64_t n3, int64_t chunk,
-                 int64_t nchunks, double* parts, cudaStream_t s, int* nonfinite = nullptr);
+                 int64_t nchunks, double* parts, cudaStream_t s, int* nonfinite = nullptr,
+                 OzakiDigits* keep = nullptr);
 // Eigensolve tail of data_q: Q (sign rule) and sigma from the Gram G.
 void eig_to_basis(const double* G, int64_t n3, int64_t p, double* Q, double* sigma, cudaStream_t s,
                   bool accurate_vectors = false);
@@ -67,7 +72,7 @@ std::array<double, 2> recon_residual_block(const double* A_blk, int64_t n1, int6
 // matrix_kernels.cpp:32), folded into the Gram's pass over T where it can be.
 // gtrace (device, nullable): trace(G) = ||T||_F^2, from the Gram's diagonal.
 bool data_q(const double* T, int64_t N, int64_t n3, int64_t p, double* Q, double* sigma,
-            cudaStream_t s, bool check_finite = false, double* gtrace = nullptr);
+            cudaStream_t s, bool check_finite = false, double* gtrace = nullptr, OzakiDigits* keep = nullptr);
 // out (device scalar) = trace of the n x n matrix G, fixed summation order.
 void gram_trace(const double* G, int64_t n, double* out, cudaStream_t s);
 // Finiteness flag for gram / gram_chunks: reset, then test (fails loudly).
@@ -91,8 +96,11 @@ double compress_relative_error(const double* A, int64_t n1, int64_t n2, int64_t 
                                const double* est, cudaStream_t s);
 // slice_sums (device, nullable, 2 doubles): {sum_i ||Ahat_i - U_i S_i V_i^T||^2, ||Ahat||^2},
 // measured directly on the transform-domain slices (fused residual GEMM).
+// tdig (nullable): A's retained 7-digit Gram split; the forward transform
+// then runs on the INT8 tensor cores (ozaki_mode3_forward).
 void tsvdq(const double* A, int64_t n1, int64_t n2, int64_t n3, const double* Q, int64_t p,
-           int64_t k, double* U, double* S, double* V, cudaStream_t s, double* slice_sums = nullptr);
+           int64_t k, double* U, double* S, double* V, cudaStream_t s, double* slice_sums = nullptr,
+           const OzakiDigits* tdig = nullptr);
 // Chat (n1 x n2 x p) = U diag(S) V^T facewise             [decompositions.cpp:88-92]
 // over the leading k columns of factor stacks that carry kstride >= k
 // columns per slice (kstride 0 = k).

@@ -47,7 +47,8 @@ namespace {
 
 using namespace umma;
 
-constexpr int kS = 6;           // digits per value: signed lead + 5 unsigned 8-bit
+constexpr int kS = 6;           // digits per value: signed lead + 5 balanced 8-bit
+constexpr int kSmax = 7;        // digit planes of a 7-digit split (the Gram digits the transform reuses)
 constexpr int kBM = 128;        // UMMA M
 constexpr int kBN = 80;         // UMMA N: 6 level accumulators x 80 = 480 TMEM columns
 constexpr int kBK = 64;         // bytes (= int8 elements) of K per stage, SWIZZLE_64B
@@ -64,6 +65,7 @@ static_assert(kBN / 2 == 40, "epilogue column split (32 + 8)");
 // [cp*chunk + u*KC, min(cp*chunk + (u+1)*KC, (cp+1)*chunk, rows)). Batched
 // mode: block b is the first min(KC, rows) rows of X + b*stride.
 // D layout: [(b*S + s)*cols + j][KCp] bytes; scale[b*cols + j].
+template <int ND>
 __global__ void __launch_bounds__(256) ozaki_split_kernel(const double* __restrict__ X, int64_t ldx, int64_t stride,
                                                           int64_t rows, int64_t cols, int64_t KC, int64_t KCp,
                                                           int64_t chunk, int64_t per, int8_t* __restrict__ D,
@@ -123,31 +125,33 @@ __global__ void __launch_bounds__(256) ozaki_split_kernel(const double* __restri
     // sigma = 2^e > 2 max |x| (mx = 0: all digits zero)
     const int e = mx > 0.0 ? ilogb(mx) + 2 : 0;
     if (threadIdx.x == 0) scale[b * cols + j] = mx > 0.0 ? ldexp(1.0, e) : 0.0;
-    int8_t* out = D + ((b * kS) * cols + j) * KCp;
+    int8_t* out = D + ((b * ND) * cols + j) * KCp;
     const int64_t plane = cols * KCp;
-    // Integer digit extraction: y = rint(2^40 * 128 x / sigma) (|y| < 2^46),
-    // U = y + c * 2^40 with c * 2^40 = 0x8080808080; the lead digit is
-    // U >> 40 (arithmetic: floor) and the balanced low digits are the bytes
-    // of U ^ 0x8080808080 (u - 128 as int8).
-    // 2^(47-e) as two finite factors: e may be near -1074 (subnormal columns)
-    const int e1 = (47 - e) / 2;
-    const double scl1 = mx > 0.0 ? ldexp(1.0, e1) : 0.0, scl2 = ldexp(1.0, 47 - e - e1);
+    // Integer digit extraction with SH = 8 (ND - 1): y = rint(2^SH * 128 x / sigma)
+    // (|y| < 2^(SH+6)), U = y + c 2^SH with c 2^SH = 0x80...80 (ND - 1 bytes);
+    // the lead digit is U >> SH (arithmetic: floor) and the balanced low
+    // digits are the bytes of U ^ 0x80...80 (u - 128 as int8).
+    constexpr int SH = 8 * (ND - 1);
+    constexpr unsigned long long C80 = 0x8080808080808080ULL >> (64 - SH);
+    // 2^(SH+7-e) as two finite factors: e may be near -1074 (subnormal columns)
+    const int e1 = (SH + 7 - e) / 2;
+    const double scl1 = mx > 0.0 ? ldexp(1.0, e1) : 0.0, scl2 = ldexp(1.0, SH + 7 - e - e1);
     for (int64_t i4 = (int64_t)threadIdx.x * 4; i4 < KCp; i4 += (int64_t)blockDim.x * 4) {
-        uint32_t w[kS];
+        uint32_t w[ND];
 #pragma unroll
-        for (int s = 0; s < kS; ++s) w[s] = 0u;
+        for (int s = 0; s < ND; ++s) w[s] = 0u;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const int64_t i = i4 + q;
             const long long y = i < len ? __double2ll_rn(stage[i] * scl1 * scl2) : 0LL;
-            const long long U = y + 0x8080808080LL;
-            const uint64_t low = (uint64_t)U ^ 0x8080808080ULL;
-            w[0] |= (uint32_t)(uint8_t)(int8_t)(U >> 40) << (8 * q);
+            const long long U = y + (long long)C80;
+            const uint64_t low = (uint64_t)U ^ C80;
+            w[0] |= (uint32_t)(uint8_t)(int8_t)(U >> SH) << (8 * q);
 #pragma unroll
-            for (int s = 1; s < kS; ++s) w[s] |= (uint32_t)((low >> (40 - 8 * s)) & 0xFFu) << (8 * q);
+            for (int s = 1; s < ND; ++s) w[s] |= (uint32_t)((low >> (SH - 8 * s)) & 0xFFu) << (8 * q);
         }
 #pragma unroll
-        for (int s = 0; s < kS; ++s) *reinterpret_cast<uint32_t*>(out + s * plane + i4) = w[s];
+        for (int s = 0; s < ND; ++s) *reinterpret_cast<uint32_t*>(out + s * plane + i4) = w[s];
     }
 }
 
@@ -162,6 +166,7 @@ struct OzParams {
     int64_t mtiles, tiles; // row tiles; tiles per output block
     int64_t KCp;           // padded rows per digit block (multiple of kBK)
     int64_t per;           // digit blocks per output block
+    int64_t nd;            // digit planes per block of both operands (6, or 7 for 7-digit splits)
     const int* zmap;       // nullable batch -> output block map
     const double* sa;      // row scales [digit block][M]
     const double* sb;      // column scales [digit block][N]
@@ -217,12 +222,12 @@ template <bool SYM, bool AMN, bool RESID, int BN = kBN, int NL = kS>
 __global__ void __launch_bounds__(kThreads, 1)
     ozaki_mma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                      const OzParams P, int64_t items) {
-    static_assert(NL * BN <= 512 && BN % 16 == 0 && (BN / 2) % 8 == 0 && NL >= 1 && NL <= kS, "tile shape");
+    static_assert(NL * BN <= 512 && BN % 16 == 0 && (BN / 2) % 8 == 0 && NL >= 1 && NL <= kSmax, "tile shape");
     extern __shared__ uint8_t smem_raw[];
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     constexpr int A_TILE = kBM * kBK, B_TILE = BN * kBK;
-    constexpr int STAGE = kS * (A_TILE + B_TILE);  // layout for all kS digits; NL of them are loaded
-    constexpr int STAGE_TX = NL * (A_TILE + B_TILE);
+    constexpr int STAGE = NL * (A_TILE + B_TILE);  // the NL digit tiles of A, then of B
+    constexpr int STAGE_TX = STAGE;
     uint64_t* full = reinterpret_cast<uint64_t*>(base + kStages * STAGE);
     uint64_t* empty = full + kStages;
     uint64_t* tfull = empty + kStages;
@@ -259,10 +264,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const int64_t blk = ob * per + gl / nkc;
                     const int kx = (int)(gl % nkc) * kBK;
                     uint8_t* sa = base + st * STAGE;
-                    uint8_t* sb = sa + kS * A_TILE;
+                    uint8_t* sb = sa + NL * A_TILE;
 #pragma unroll
                     for (int s = 0; s < NL; ++s) {
-                        const int plane = (int)(blk * kS + s);
+                        const int plane = (int)(blk * P.nd + s);
                         if (AMN) {
                             tma_load_3d(sa + s * A_TILE, &mapA, &full[st], (int)(mb * kBM), kx, plane);
                             tma_load_3d(sa + s * A_TILE + 4096, &mapA, &full[st], (int)(mb * kBM + 64), kx, plane);
@@ -299,7 +304,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     fence_after_sync();
                     if (elect_one()) {
                         const uint8_t* sa = base + st * STAGE;
-                        const uint8_t* sb = sa + kS * A_TILE;
+                        const uint8_t* sb = sa + NL * A_TILE;
 #pragma unroll
                         for (int kk = 0; kk < kBK / 32; ++kk) {
                             // digit 1 of A spans every level: its MMAs start the block
@@ -373,7 +378,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             const double r = xv[j] - val;
                             rsd = fma(r, r, rsd);
                             rsx = fma(xv[j], xv[j], rsx);
-                        } else if (m < P.M && n < P.N) {
+                        } else if (m < P.M && n < P.N && (P.m_total == 0 || ob * P.M + m < P.m_total)) {
                             C[m + n * P.ldc] = val;  // (m, n), coalesced over the warp's rows
                         }
                     }
@@ -501,7 +506,7 @@ int64_t ozaki_grid(int64_t items) { return std::min<int64_t>(items, ctx().sms); 
 template <bool SYM, bool AMN = false, bool RESID = false, int BN = kBN, int NL = kS>
 void launch_mma(const CUtensorMap& ma, const CUtensorMap& mb, const OzParams& P, int64_t items, cudaStream_t s) {
     // stages + barriers + TMEM slot + the epilogue warps' residual sums
-    const size_t smem = 1024 + (size_t)kStages * kS * (kBM + BN) * kBK + (2 * kStages + 2) * 8 + 16 + 16 * kEpiWarps;
+    const size_t smem = 1024 + (size_t)kStages * NL * (kBM + BN) * kBK + (2 * kStages + 2) * 8 + 16 + 16 * kEpiWarps;
     static bool attr = false;
     if (!attr) {
         PPC_CUDA_CHECK(cudaFuncSetAttribute(ozaki_mma_kernel<SYM, AMN, RESID, BN, NL>,
@@ -527,8 +532,8 @@ int64_t tri_tiles(int64_t n) {
 void ozaki_syrk(const OzakiDigits& d, int64_t nout, int64_t per, double* out, cudaStream_t s, const char* stage,
                 double rows_total) {
     CUtensorMap ma, mb;
-    if (!make_digit_map(&ma, d.D.as<int8_t>(), d.KCp, d.cols, d.nblk * kS, kBM) ||
-        !make_digit_map(&mb, d.D.as<int8_t>(), d.KCp, d.cols, d.nblk * kS, kBN))
+    if (!make_digit_map(&ma, d.D.as<int8_t>(), d.KCp, d.cols, d.nblk * d.nd, kBM) ||
+        !make_digit_map(&mb, d.D.as<int8_t>(), d.KCp, d.cols, d.nblk * d.nd, kBN))
         fail(PPC_CUDA, "ozaki: tensor map encoding failed");
     OzParams P;
     P.M = P.N = d.cols;
@@ -536,6 +541,7 @@ void ozaki_syrk(const OzakiDigits& d, int64_t nout, int64_t per, double* out, cu
     P.tiles = tri_tiles(d.cols);
     P.KCp = d.KCp;
     P.per = per;
+    P.nd = d.nd;
     P.zmap = nullptr;
     P.sa = P.sb = d.sc.d();
     P.sq = d.sq.d();
@@ -555,24 +561,30 @@ void ozaki_syrk(const OzakiDigits& d, int64_t nout, int64_t per, double* out, cu
 
 void OzakiDigits::split(const double* X, int64_t ldx, int64_t stride, int64_t rows_, int64_t cols_, int64_t KC,
                         int64_t nblk_, cudaStream_t s, const int* zmap, int64_t nz, int64_t chunk, int64_t per,
-                        int* nonfinite) {
+                        int* nonfinite, int ndig) {
+    if (ndig != kS && ndig != kSmax) fail(PPC_ARGUMENT, "ozaki split: 6 or 7 digits");
+    nd = ndig;
     if (KC < 1 || KC > kKC) fail(PPC_ARGUMENT, "ozaki split: block length out of range");
     if (zmap && !stride) fail(PPC_ARGUMENT, "ozaki split: a block map needs batched blocks");
     rows = rows_;
     cols = cols_;
     nblk = nblk_;
     KCp = (KC + kBK - 1) / kBK * kBK;
-    const size_t dbytes = sizeof(int8_t) * nblk * kS * cols * KCp, sbytes = sizeof(double) * nblk * cols;
+    const size_t dbytes = sizeof(int8_t) * nblk * nd * cols * KCp, sbytes = sizeof(double) * nblk * cols;
     if (D.bytes() < dbytes) D = DeviceBuffer(dbytes);
     if (sc.bytes() < sbytes) sc = DeviceBuffer(sbytes);
     if (sq.bytes() < sbytes) sq = DeviceBuffer(sbytes);
     const int64_t launched = zmap ? nz : nblk;
     if (launched <= 0) return;
     const double total_rows = stride ? (double)std::min(KC, rows) * launched : (double)rows;
-    StageTimer ts("ozaki_split", s, 0.0, 8.0 * total_rows * cols + (double)kS * total_rows * cols);
+    StageTimer ts("ozaki_split", s, 0.0, 8.0 * total_rows * cols + (double)nd * total_rows * cols);
     dim3 grid((unsigned)cols, (unsigned)launched);
-    ozaki_split_kernel<<<grid, 256, 0, s>>>(X, ldx, stride, rows, cols, KC, KCp, chunk ? chunk : KC, per ? per : 1,
-                                            D.as<int8_t>(), sc.d(), sq.d(), zmap, nonfinite);
+    if (nd == kSmax)
+        ozaki_split_kernel<kSmax><<<grid, 256, 0, s>>>(X, ldx, stride, rows, cols, KC, KCp, chunk ? chunk : KC,
+                                                       per ? per : 1, D.as<int8_t>(), sc.d(), sq.d(), zmap, nonfinite);
+    else
+        ozaki_split_kernel<kS><<<grid, 256, 0, s>>>(X, ldx, stride, rows, cols, KC, KCp, chunk ? chunk : KC,
+                                                    per ? per : 1, D.as<int8_t>(), sc.d(), sq.d(), zmap, nonfinite);
     count_launch();
     check_launch("ozaki_split");
 }
@@ -586,8 +598,9 @@ void ozaki_gemm(const OzakiDigits& A, const OzakiDigits& B, int64_t nbatch, cons
     const int bn = (B.cols <= 64) ? 64 : kBN;
     if (levels != kS && bn != 64) fail(PPC_ARGUMENT, "ozaki_gemm: reduced levels need <= 64 columns");
     CUtensorMap ma, mb;
-    if (!make_digit_map(&ma, A.D.as<int8_t>(), A.KCp, A.cols, A.nblk * kS, kBM) ||
-        !make_digit_map(&mb, B.D.as<int8_t>(), B.KCp, B.cols, B.nblk * kS, bn))
+    if (A.nd != B.nd) fail(PPC_ARGUMENT, "ozaki_gemm: digit counts differ");
+    if (!make_digit_map(&ma, A.D.as<int8_t>(), A.KCp, A.cols, A.nblk * A.nd, kBM) ||
+        !make_digit_map(&mb, B.D.as<int8_t>(), B.KCp, B.cols, B.nblk * B.nd, bn))
         fail(PPC_CUDA, "ozaki: tensor map encoding failed");
     OzParams P;
     P.M = A.cols;
@@ -596,6 +609,7 @@ void ozaki_gemm(const OzakiDigits& A, const OzakiDigits& B, int64_t nbatch, cons
     P.tiles = P.mtiles * ((P.N + bn - 1) / bn);
     P.KCp = A.KCp;
     P.per = 1;
+    P.nd = A.nd;
     P.zmap = zmap;
     P.sa = A.sc.d();
     P.sb = B.sc.d();
@@ -649,8 +663,8 @@ bool ozaki_recon_residual(const double* X, int64_t N, int64_t n3, const double* 
     }
     bd.split(bt.d(), p, p * n3, p, n3, p, nblk, s);
     CUtensorMap ma, mb;
-    if (!make_digit_map(&ma, cd.D.as<int8_t>(), cd.KCp, p, nblk * kS, 64) ||
-        !make_digit_map(&mb, bd.D.as<int8_t>(), bd.KCp, n3, nblk * kS, kBN))
+    if (!make_digit_map(&ma, cd.D.as<int8_t>(), cd.KCp, p, nblk * cd.nd, 64) ||
+        !make_digit_map(&mb, bd.D.as<int8_t>(), bd.KCp, n3, nblk * bd.nd, kBN))
         fail(PPC_CUDA, "ozaki: tensor map encoding failed");
     OzParams P;
     P.M = kKC;
@@ -659,6 +673,7 @@ bool ozaki_recon_residual(const double* X, int64_t N, int64_t n3, const double* 
     P.tiles = P.mtiles * ((n3 + kBN - 1) / kBN);
     P.KCp = bd.KCp;  // the K extent: p, padded
     P.per = 1;
+    P.nd = cd.nd;
     P.zmap = nullptr;
     P.sa = nullptr;  // folded into Bt
     P.sb = bd.sc.d();
@@ -684,7 +699,7 @@ bool ozaki_recon_residual(const double* X, int64_t N, int64_t n3, const double* 
 }
 
 bool ozaki_gram_partials(const double* T, int64_t ldT, int64_t rows, int64_t n3, int64_t chunk, int64_t nchunks,
-                         double* parts, cudaStream_t s, int* nonfinite) {
+                         double* parts, cudaStream_t s, int* nonfinite, OzakiDigits* keep) {
     if (!ozaki_enabled()) return false;
     // the integer path pays off once each output tile sees a long K range
     if (n3 < 128 || chunk < 4096 || rows < 4096 * 4) return false;
@@ -695,9 +710,73 @@ bool ozaki_gram_partials(const double* T, int64_t ldT, int64_t rows, int64_t n3,
     const int64_t per = (chunk + kKC - 1) / kKC;
     const int64_t nblk = nchunks * per;
     StageTimer tm("gram_ozaki", s, (double)rows * n3 * n3, 8.0 * rows * n3);
-    OzakiDigits d;
-    d.split(T, ldT, 0, rows, n3, kKC, nblk, s, nullptr, 0, chunk, per, nonfinite);
+    const bool retain = keep && chunk % kKC == 0;
+    OzakiDigits local;
+    OzakiDigits& d = retain ? *keep : local;
+    d.split(T, ldT, 0, rows, n3, kKC, nblk, s, nullptr, 0, chunk, per, nonfinite, retain ? kSmax : kS);
+    d.uniform = retain;
     ozaki_syrk(d, nchunks, per, parts, s, "ozaki_syrk", (double)rows);
+    return true;
+}
+
+namespace {
+
+// Bq[b] (n3 x p, column-major) = diag(sigma_{b,.}) Q: the per-(row block,
+// column) scales of T's digits folded into the transform.
+__global__ void fold_q_kernel(const double* __restrict__ sc, const double* __restrict__ Q, int64_t n3, int64_t p,
+                              int64_t total, double* __restrict__ Bq) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
+        const int64_t b = i / (n3 * p), r = i - b * n3 * p, c = r % n3;
+        Bq[i] = sc[b * n3 + c] * Q[r];
+    }
+}
+
+}  // namespace
+
+bool ozaki_mode3_forward(const OzakiDigits& td, int64_t N, const double* Q, int64_t p, double* out, cudaStream_t s) {
+    static const bool off = std::getenv("PPC_OZAKI_FWD") && std::getenv("PPC_OZAKI_FWD")[0] == '0';
+    if (off || !ozaki_enabled() || !td.uniform || td.nd != kSmax || td.KCp != kKC) return false;
+    const int64_t n3 = td.cols, nblk = td.nblk;
+    if (p < 64 || p % 64 || n3 < 256 || n3 > kKC || nblk * kKC < N) return false;
+    StageTimer tm("mode3_fwd", s, 2.0 * N * n3 * p, 8.0 * (N * n3 + N * p + n3 * p));
+    DeviceBuffer bq(sizeof(double) * nblk * n3 * p);
+    {
+        const int64_t total = nblk * n3 * p;
+        fold_q_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, 148 * 16), 256, 0, s>>>(td.sc.d(), Q, n3, p,
+                                                                                              total, bq.d());
+        count_launch();
+        check_launch("fold_q");
+    }
+    OzakiDigits bd;
+    bd.split(bq.d(), n3, n3 * p, n3, p, n3, nblk, s, nullptr, 0, 0, 0, nullptr, kSmax);
+    CUtensorMap ma, mb;
+    if (!make_digit_map(&ma, td.D.as<int8_t>(), td.KCp, n3, nblk * td.nd, 64) ||
+        !make_digit_map(&mb, bd.D.as<int8_t>(), bd.KCp, p, nblk * bd.nd, 64))
+        fail(PPC_CUDA, "ozaki: tensor map encoding failed");
+    OzParams P;
+    P.M = kKC;
+    P.N = p;
+    P.mtiles = kKC / kBM;
+    P.tiles = P.mtiles * (p / 64);
+    P.KCp = bd.KCp;  // the K extent: n3
+    P.per = 1;
+    P.nd = kSmax;
+    P.zmap = nullptr;
+    P.sa = nullptr;  // folded into Bq
+    P.sb = bd.sc.d();
+    P.sq = nullptr;
+    P.C = out;
+    P.ldc = N;
+    P.strideC = kKC;  // block b starts at row 4096 b
+    P.X = nullptr;
+    P.ldx = P.strideX = 0;
+    P.m_total = N;    // rows past N in the last block are not stored
+    P.partial = nullptr;
+    {
+        StageTimer tk("ozaki_fwd", s, 2.0 * kSmax * (kSmax + 1) / 2 * (double)N * n3 * p, (double)kSmax * N * n3);
+        launch_mma<false, true, false, 64, kSmax>(ma, mb, P, nblk * P.tiles, s);
+    }
     return true;
 }
 

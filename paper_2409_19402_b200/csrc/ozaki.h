@@ -16,10 +16,12 @@ namespace ppc {
 struct OzakiDigits {
     DeviceBuffer D, sc, sq;  // int8 planes [blk][digit][col][KCp]; scales, sums of squares [blk][col]
     int64_t rows = 0, cols = 0, KCp = 0, nblk = 0;
+    int nd = 6;              // digit planes per block (6; 7 adds 8 bits for products with cancellation)
+    bool uniform = false;    // block b holds rows [4096 b, 4096 b + 4096) of one matrix (row-chunked split)
     // zmap (device, nz entries; batched blocks only): split just those blocks
     void split(const double* X, int64_t ldx, int64_t stride, int64_t rows, int64_t cols, int64_t KC, int64_t nblk,
                cudaStream_t s, const int* zmap = nullptr, int64_t nz = 0, int64_t chunk = 0, int64_t per = 0,
-               int* nonfinite = nullptr);
+               int* nonfinite = nullptr, int ndig = 6);
 };
 
 // C_b (A.cols x B.cols, (m, n) at m + n*ldc, b at blk*strideC) = A_blk^T B_blk
@@ -46,8 +48,19 @@ bool ozaki_recon_residual(const double* X, int64_t N, int64_t n3, const double* 
 // shape is not eligible (caller falls back to the DMMA SYRK). PPC_OZAKI=0
 // disables it. nonfinite (nullable device int): set to 1 if any value of T
 // is NaN or Inf (the split reads every value once).
+// keep (nullable): when the plan chunks are whole 4096-row blocks, T is split
+// into 7 digits (the SYRK still uses 6 levels) and the digits are left in
+// *keep for ozaki_mode3_forward.
 bool ozaki_gram_partials(const double* T, int64_t ldT, int64_t rows, int64_t n3, int64_t chunk, int64_t nchunks,
-                         double* parts, cudaStream_t s, int* nonfinite = nullptr);
+                         double* parts, cudaStream_t s, int* nonfinite = nullptr, OzakiDigits* keep = nullptr);
+
+// out (N x p, leading dimension N) = T Q, the forward mode-3 transform, from
+// T's retained 7-digit Gram digits td (read MN-major: pixels contiguous per
+// column) and Q (n3 x p) with the per-(block, column) scales folded in: 28
+// digit pairs, ~2^-55 of the per-block column scale, as accurate as FP64
+// DMMA on the noise slices (where Ahat is ~1e-4 of |T||Q|). false when td
+// does not qualify.
+bool ozaki_mode3_forward(const OzakiDigits& td, int64_t N, const double* Q, int64_t p, double* out, cudaStream_t s);
 
 // G_b (n x n, column-major, b < batch, stride n*n) = A_b^T A_b for A_b
 // (rows x n, leading dimension lda) at A + b*strideA: the batched slice

@@ -101,10 +101,10 @@ void tree_reduce(double* parts, int64_t nparts, int64_t elems, cudaStream_t s) {
 // Partial Grams of `nchunks` consecutive chunks of `chunk` rows of T (rows x
 // n3, leading dimension ldT) into parts (nchunks x n3 x n3).
 bool gram_chunks(const double* T, int64_t ldT, int64_t rows, int64_t n3, int64_t chunk,
-                 int64_t nchunks, double* parts, cudaStream_t s, int* nonfinite) {
+                 int64_t nchunks, double* parts, cudaStream_t s, int* nonfinite, OzakiDigits* keep) {
     // INT8 tensor-core (Ozaki) path for large Grams; it reads T column by
     // column, so no re-layout either
-    if (ozaki_gram_partials(T, ldT, rows, n3, chunk, nchunks, parts, s, nonfinite)) return nonfinite != nullptr;
+    if (ozaki_gram_partials(T, ldT, rows, n3, chunk, nchunks, parts, s, nonfinite, keep)) return nonfinite != nullptr;
     // Large tube matrices: each SYRK pipeline stage would touch one 2 MB page
     // per column (columns are ldT*8 bytes apart), thrashing the TLB. Re-lay T
     // into 2048-row blocks first (one extra HBM pass); same summation order.
@@ -128,12 +128,12 @@ bool gram_chunks(const double* T, int64_t ldT, int64_t rows, int64_t n3, int64_t
     return false;
 }
 
-bool gram(const double* T, int64_t N, int64_t n3, double* G, cudaStream_t s, int* nonfinite) {
+bool gram(const double* T, int64_t N, int64_t n3, double* G, cudaStream_t s, int* nonfinite, OzakiDigits* keep) {
     StageTimer tm("gram_syrk", s, (double)N * n3 * n3, 8.0 * N * n3);
     const GramPlan g = gram_plan(N, n3);
-    if (g.chunks == 1) return gram_chunks(T, N, N, n3, g.chunk, 1, G, s, nonfinite);
+    if (g.chunks == 1) return gram_chunks(T, N, N, n3, g.chunk, 1, G, s, nonfinite, keep);
     DeviceBuffer parts(sizeof(double) * g.chunks * n3 * n3);
-    const bool checked = gram_chunks(T, N, N, n3, g.chunk, g.chunks, parts.d(), s, nonfinite);
+    const bool checked = gram_chunks(T, N, N, n3, g.chunk, g.chunks, parts.d(), s, nonfinite, keep);
     tree_reduce(parts.d(), g.chunks, n3 * n3, s);
     PPC_CUDA_CHECK(cudaMemcpyAsync(G, parts.d(), sizeof(double) * n3 * n3, cudaMemcpyDeviceToDevice, s));
     return checked;
@@ -207,16 +207,16 @@ void gram_trace(const double* G, int64_t n, double* out, cudaStream_t s) {
 }
 
 bool data_q(const double* T, int64_t N, int64_t n3, int64_t p, double* Q, double* sigma,
-            cudaStream_t s, bool check_finite, double* gtrace) {
+            cudaStream_t s, bool check_finite, double* gtrace, OzakiDigits* keep) {
     DeviceBuffer G(sizeof(double) * n3 * n3);
     if (check_finite) {
         FiniteFlag nf(s);
-        if (gram(T, N, n3, G.d(), s, nf.d()))
+        if (gram(T, N, n3, G.d(), s, nf.d(), keep))
             nf.check(s, "svd");
         else
             require_finite(T, N * n3, "svd", s);
     } else {
-        gram(T, N, n3, G.d(), s);
+        gram(T, N, n3, G.d(), s, nullptr, keep);
     }
     if (gtrace) gram_trace(G.d(), n3, gtrace, s);
     // When p > min(n3, N) the unfolding has only min(n3, N) singular vectors;

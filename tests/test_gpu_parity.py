@@ -1039,3 +1039,38 @@ def test_compress_re_identity_matches_direct(engine):
         f, re = engine.compress_tsvdq(da, p, k)
         red = engine.tsvdq_relative_error(da, f)
         assert abs(re - red) <= 1e-12 * red, (shape, re, red)
+
+
+@pytest.mark.gpu
+def test_ozaki_forward_transform_noise_slices(engine):
+    """ppc_tsvdq_compress reuses the data-driven Q Gram's 7-digit split of A
+    for Ahat = A x3 Q^T on the INT8 tensor cores (28 digit pairs). With the
+    same basis, every slice's singular values -- the noise slices, whose
+    Ahat is ~1e-4 of |A||Q|, included -- must agree with the FP64 DMMA
+    transform to 1e-10 per value."""
+    import ctypes as C
+    from paper_2409_19402_b200 import _lib
+    L = _lib.lib()
+    n1, n2, n3, p, k = 512, 512, 512, 64, 16
+    a = synth.cp_tensor_device(n1, n2, n3, rank=50, noise=1e-3, seed=8)
+    Q, U, S, V = (engine.empty_device(sh) for sh in ((n3, p), (n1, k, p), (k, p), (n2, k, p)))
+    re = C.c_double()
+    L.ppc_timing_enable(1)
+    rc = L.ppc_tsvdq_compress(C.c_void_p(a.data_ptr()), n1, n2, n3, p, k, C.c_void_p(Q.data_ptr()), None,
+                              C.c_void_p(U.data_ptr()), C.c_void_p(S.data_ptr()), C.c_void_p(V.data_ptr()),
+                              C.byref(re), 1)
+    buf = C.create_string_buffer(1 << 16)
+    L.ppc_timing_report(buf, len(buf), 1)
+    L.ppc_timing_enable(0)
+    assert rc == 0, L.ppc_last_error()
+    assert "ozaki_fwd" in buf.value.decode(), buf.value.decode()
+    s_fwd = engine.to_host(S)
+    t = engine.Transform.custom(engine.to_host(Q))
+    s_dmma = engine.to_host(engine.tsvdq(a, t, k).s)  # same Q, FP64 DMMA transform
+    assert (np.abs(s_fwd - s_dmma) <= 1e-10 * s_dmma).all(), np.max(np.abs(s_fwd - s_dmma) / s_dmma)
+    try:
+        assert L.ppc_set_ozaki(0) == 0
+        s_off = engine.to_host(engine.tsvdq(a, t, k).s)  # everything FP64 DMMA
+    finally:
+        L.ppc_set_ozaki(1)
+    assert (np.abs(s_fwd - s_off) <= 1e-10 * s_off).all(), np.max(np.abs(s_fwd - s_off) / s_off)
