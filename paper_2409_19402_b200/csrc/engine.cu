@@ -327,7 +327,7 @@ void tsvdq(const double* A, int64_t n1, int64_t n2, int64_t n3, const double* Q,
         d.M = n1; d.N = n2; d.K = k; d.batch = p;
         d.A = us.d(); d.lda = n1; d.strideA = n1 * k;
         d.B = V; d.ldb = n2; d.strideB = n2 * k; d.b_nmajor = true;
-        d.allow_ws = false;
+        // one total (no per-slice sums): the warp-specialized TMA kernel may run it
         const int64_t ctas = gemm_residual_ctas(d, ah.d(), n1, N);
         DeviceBuffer part(sizeof(double) * 2 * ctas);
         gemm_residual(d, ah.d(), n1, N, part.d(), s);

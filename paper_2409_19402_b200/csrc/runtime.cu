@@ -161,6 +161,10 @@ DeviceBuffer::DeviceBuffer(size_t bytes) : n_(bytes) {
                 return;
             }
         // not cached: a plain allocation (outside the pool) of this size
+        static const bool trace = std::getenv("PPC_TRACE_ALLOC") != nullptr;
+        if (trace)
+            fprintf(stderr, "[alloc] miss %.3f GB (cache holds %zu blocks, %.1f GB)\n", bytes / 1e9, c.free.size(),
+                    c.held / 1e9);
         cudaError_t e = cudaMalloc(&p_, bytes);
         while (e == cudaErrorMemoryAllocation && !c.free.empty()) {  // make room from the cache
             cudaGetLastError();
@@ -182,7 +186,11 @@ void DeviceBuffer::release() {
                 cudaEventRecord(ev, stream()) == cudaSuccess) {
                 c.free.push_back({n_, p_, ev});
                 c.held += n_;
-                while (c.held > big_cap(dev_) && c.free.size() > 1) big_drop(c, 0);  // oldest first
+                while (c.held > big_cap(dev_) && c.free.size() > 1) {  // oldest first
+                    if (std::getenv("PPC_TRACE_ALLOC"))
+                        fprintf(stderr, "[alloc] drop %.3f GB over the cap\n", c.free[0].bytes / 1e9);
+                    big_drop(c, 0);
+                }
             } else {
                 if (ev) cudaEventDestroy(ev);
                 cudaDeviceSynchronize();
