@@ -85,6 +85,18 @@ class ClockSampler:
         except Exception:
             self.proc = None
 
+    def mark(self):
+        """Start of the timed region: only samples written after this count.
+        (nvidia-smi is started before the warm-up steps: its start-up, which
+        holds the driver for a while, must not land inside the timed steps.)"""
+        self.skip = 0
+        if self.path:
+            try:
+                with open(self.path) as f:
+                    self.skip = sum(1 for _ in f)
+            except OSError:
+                pass
+
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
@@ -95,7 +107,9 @@ class ClockSampler:
         except Exception:
             self.proc.kill()
         rows = []
-        for line in open(self.path):
+        for i, line in enumerate(open(self.path)):
+            if i < getattr(self, "skip", 0):
+                continue
             parts = [p.strip() for p in line.split(",")]
             if len(parts) >= 9:
                 rows.append(parts)
@@ -607,12 +621,13 @@ def main():
     wl = make_workload(args.workload, world, rank, local)
     torch.cuda.synchronize()
 
+    clocks = ClockSampler(local)
+    clocks.start()
     for _ in range(args.warmup):
         wl.step(L)
     sync_all(dist_on)
 
-    clocks = ClockSampler(local)
-    clocks.start()
+    clocks.mark()
     L.ppc_launch_count(1)
     timing_report(L, reset=True)
     L.ppc_timing_enable(1)
