@@ -257,6 +257,16 @@ int ppc_tree_reduce(double* parts, int64_t nparts, int64_t elems, int loc);
 /* Top-p eigenvectors Q (n x p, sign rule) and sigma = sqrt(lambda) (nullable)
  * of the symmetric PSD Gram G (n x n): the tail of data_dependent_transform. */
 int ppc_sym_eig_top(const double* G, int64_t n, int64_t p, double* Q, double* sigma, int loc);
+/* sums[0..1] (host) = {sum_i ||A_i - U_i diag(S_i) V_i^T||^2, sum_i ||A_i||^2} over
+ * `batch` transform-domain slices A_i (n1 x n2, stride n1*n2) and their rank-k
+ * factors U (n1,k,batch), S (k,batch), V (n2,k,batch): the slice-space half of
+ * the orthogonal split of ||A - A_k||^2 (relative_error of the compress chain,
+ * metrics.cpp:21-28; the sharded driver sums it over the slice shards). */
+int ppc_slice_residual_sums(const double* A, int64_t n1, int64_t n2, int64_t batch, int64_t k,
+                            const double* U, const double* S, const double* V, double* sums, int loc);
+/* *trace (host) = trace of the n x n matrix G (fixed summation order): ||T||_F^2
+ * from the data-driven Q's Gram G = T^T T. */
+int ppc_gram_trace(const double* G, int64_t n, double* trace, int loc);
 /* {sum (A - recon)^2, sum A^2} over a lateral block of pixels: A_blk is the
  * n1 x nj x n3 block of columns [j0, j0+nj) (leading dims n1 and ldA = n1*n2
  * between frontal slices), U (n1,k,p), S (k,p), V (n2,k,p) full factors. */

@@ -75,6 +75,8 @@ def lib() -> C.CDLL:
         "ppc_gram_partials": (C.c_int, [vp, i64, i64, i64, i64, i64, vp, C.c_int]),
         "ppc_tree_reduce": (C.c_int, [vp, i64, i64, C.c_int]),
         "ppc_sym_eig_top": (C.c_int, [vp, i64, i64, vp, vp, C.c_int]),
+        "ppc_slice_residual_sums": (C.c_int, [vp, i64, i64, i64, i64, vp, vp, vp, pd, C.c_int]),
+        "ppc_gram_trace": (C.c_int, [vp, i64, pd, C.c_int]),
         "ppc_recon_residual_block": (C.c_int, [vp, i64, i64, i64, i64, vp, vp, vp, i64, i64, vp, i64, i64, pd, C.c_int]),
         "ppc_tsvdq2": (C.c_int, [vp, i64, i64, i64, vp, i64, C.c_double, vp, vp, vp, C.POINTER(i64), C.c_int]),
         "ppc_tsvdq2_reconstruct": (C.c_int, [vp, vp, vp, vp, i64, i64, i64, i64, C.POINTER(i64), vp, C.c_int]),

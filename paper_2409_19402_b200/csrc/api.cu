@@ -477,6 +477,36 @@ int ppc_sym_eig_top(const double* G, int64_t n, int64_t p, double* Q, double* si
     });
 }
 
+int ppc_slice_residual_sums(const double* A, int64_t n1, int64_t n2, int64_t batch, int64_t k,
+                            const double* U, const double* S, const double* V, double* sums, int loc) {
+    return guarded([&] {
+        validate_loc(loc);
+        check_tensor(n1, n2, batch);
+        check_spatial_rank(n1, n2, k, "slice_residual_sums");
+        if (!sums) fail(PPC_ARGUMENT, "null output");
+        cudaStream_t s = stream();
+        In a(A, n1 * n2 * batch, loc), u(U, n1 * k * batch, loc), sv(S, k * batch, loc), v(V, n2 * k * batch, loc);
+        DeviceBuffer out(sizeof(double) * 2);
+        slice_residual_sums(a.d, n1, n2, batch, k, u.d, sv.d, v.d, out.d(), s);
+        PPC_CUDA_CHECK(cudaMemcpyAsync(sums, out.d(), 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+        PPC_CUDA_CHECK(cudaStreamSynchronize(s));
+    });
+}
+
+int ppc_gram_trace(const double* G, int64_t n, double* trace, int loc) {
+    return guarded([&] {
+        validate_loc(loc);
+        require_positive(n, "n");
+        if (!trace) fail(PPC_ARGUMENT, "null output");
+        cudaStream_t s = stream();
+        In g(G, n * n, loc);
+        DeviceBuffer out(sizeof(double));
+        gram_trace(g.d, n, out.d(), s);
+        PPC_CUDA_CHECK(cudaMemcpyAsync(trace, out.d(), sizeof(double), cudaMemcpyDeviceToHost, s));
+        PPC_CUDA_CHECK(cudaStreamSynchronize(s));
+    });
+}
+
 int ppc_recon_residual_block(const double* A_blk, int64_t n1, int64_t nj, int64_t n3, int64_t ldA,
                              const double* U, const double* S, const double* V, int64_t n2,
                              int64_t j0, const double* Q, int64_t p, int64_t k, double* sums,

@@ -318,21 +318,24 @@ void tsvdq(const double* A, int64_t n1, int64_t n2, int64_t n3, const double* Q,
                                           4.0 * p * N * k, 8.0 * p * N);
         slice_svd(ah.d(), n1, n2, N, p, k, U, S, V, nullptr, s);  // :75-81
     }
-    if (slice_sums) {
-        // {sum_i ||Ahat_i - U_i S_i V_i^T||^2, ||Ahat||^2} over every slice, one fused pass
-        StageTimer tm("slice_residual", s, 2.0 * p * N * k, 8.0 * p * N);
-        DeviceBuffer us(sizeof(double) * n1 * k * p);
-        launch_scale_columns(U, S, us.d(), n1, k, p, s);
-        GemmDesc d;
-        d.M = n1; d.N = n2; d.K = k; d.batch = p;
-        d.A = us.d(); d.lda = n1; d.strideA = n1 * k;
-        d.B = V; d.ldb = n2; d.strideB = n2 * k; d.b_nmajor = true;
-        // one total (no per-slice sums): the warp-specialized TMA kernel may run it
-        const int64_t ctas = gemm_residual_ctas(d, ah.d(), n1, N);
-        DeviceBuffer part(sizeof(double) * 2 * ctas);
-        gemm_residual(d, ah.d(), n1, N, part.d(), s);
-        launch_reduce_pairs(part.d(), ctas, slice_sums, s);
-    }
+    if (slice_sums) slice_residual_sums(ah.d(), n1, n2, p, k, U, S, V, slice_sums, s);
+}
+
+void slice_residual_sums(const double* Ah, int64_t n1, int64_t n2, int64_t p, int64_t k, const double* U,
+                         const double* S, const double* V, double* out, cudaStream_t s) {
+    const int64_t N = n1 * n2;
+    StageTimer tm("slice_residual", s, 2.0 * p * N * k, 8.0 * p * N);
+    DeviceBuffer us(sizeof(double) * n1 * k * p);
+    launch_scale_columns(U, S, us.d(), n1, k, p, s);
+    GemmDesc d;
+    d.M = n1; d.N = n2; d.K = k; d.batch = p;
+    d.A = us.d(); d.lda = n1; d.strideA = n1 * k;
+    d.B = V; d.ldb = n2; d.strideB = n2 * k; d.b_nmajor = true;
+    // one total (no per-slice sums): the warp-specialized TMA kernel may run it
+    const int64_t ctas = gemm_residual_ctas(d, Ah, n1, N);
+    DeviceBuffer part(sizeof(double) * 2 * ctas);
+    gemm_residual(d, Ah, n1, N, part.d(), s);
+    launch_reduce_pairs(part.d(), ctas, out, s);
 }
 
 void sweep_errors(const double* A, int64_t n1, int64_t n2, int64_t n3, const double* Q, int64_t pmax,

@@ -94,6 +94,10 @@ struct FiniteFlag {
 double compress_relative_error(const double* A, int64_t n1, int64_t n2, int64_t n3, const double* U,
                                const double* S, const double* V, const double* Q, int64_t p, int64_t k,
                                const double* est, cudaStream_t s);
+// out (device, 2 doubles) = {sum_i ||Ahat_i - U_i S_i V_i^T||^2, ||Ahat||^2} over p slices
+// Ahat_i (n1 x n2, stride n1*n2): one fused residual GEMM.
+void slice_residual_sums(const double* Ah, int64_t n1, int64_t n2, int64_t p, int64_t k, const double* U,
+                         const double* S, const double* V, double* out, cudaStream_t s);
 // slice_sums (device, nullable, 2 doubles): {sum_i ||Ahat_i - U_i S_i V_i^T||^2, ||Ahat||^2},
 // measured directly on the transform-domain slices (fused residual GEMM).
 // tdig (nullable): A's retained 7-digit Gram split; the forward transform

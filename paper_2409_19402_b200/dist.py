@@ -19,8 +19,10 @@ The cfg5 pipeline is sharded as follows:
 5. Â is resharded pixel -> slice by all_to_all_single: each rank gets p/G
    complete slices.
 6. The slice SVDs run locally, then the factor stacks are all-gathered.
-7. The fused reconstruction residual runs over the local pixel block, then the
-   two scalars are all-reduced.
+7. RE from the orthogonal split (Gram trace - ||Ahat||^2 + slice residuals,
+   the slice sums all-reduced); below RE^2 = 2e-3 the fused reconstruction
+   residual runs over the local pixel block and its two scalars are
+   all-reduced instead.
 
 star-Q (sharded_star_q, cfg4): output rows are partitioned. Rank r holds the
 row block A[i0:i1, :, :] and the lateral block B[:, j0:j1, :]. It transforms
@@ -117,6 +119,16 @@ class DeviceBackend:
         V = _fempty((n2, k, ps), self.device)
         _check(self.L.ppc_svd_batched(_p(S_loc), n1, n2, ps, k, _p(U), _p(s), _p(V), 1))
         return U, s, V
+
+    def gram_trace(self, G, n):
+        t = C.c_double()
+        _check(self.L.ppc_gram_trace(_p(G), n, C.byref(t), 1))
+        return t.value
+
+    def slice_sums(self, S_loc, n1, n2, ps, k, U, s, V):
+        sums = (C.c_double * 2)()
+        _check(self.L.ppc_slice_residual_sums(_p(S_loc), n1, n2, ps, k, _p(U), _p(s), _p(V), sums, 1))
+        return float(sums[0]), float(sums[1])
 
     def recon_block(self, A_blk, n1, nj, n3, U, S, V, n2, j0, Q, p, k):
         sums = (C.c_double * 2)()
@@ -215,6 +227,8 @@ def sharded_compress(A_blk, plan: ShardPlan, k: int, backend, group=None):
     S_loc = full.permute(2, 1, 0)                     # (n1, n2, ps) Fortran view
     # 6. slice SVDs, all-gather the factor stacks
     U, s, V = backend.svd_slices(S_loc, n1, n2, ps, k)
+    # slice-space half of the error split, on the local slices (before the gather)
+    st, sa2 = backend.slice_sums(S_loc, n1, n2, ps, k, U, s, V)
     Uc = U.permute(2, 1, 0).contiguous()  # (ps, k, n1)
     sc = s.permute(1, 0).contiguous()     # (ps, k)
     Vc = V.permute(2, 1, 0).contiguous()  # (ps, k, n2)
@@ -227,12 +241,25 @@ def sharded_compress(A_blk, plan: ShardPlan, k: int, backend, group=None):
         dist.all_gather(Vg, Vc, group=group)
         Uc, sc, Vc = torch.cat(Ug), torch.cat(sg), torch.cat(Vg)
     Uf, Sf, Vf = Uc.permute(2, 1, 0), sc.permute(1, 0), Vc.permute(2, 1, 0)  # (n1,k,p) (k,p) (n2,k,p)
-    # 7. fused residual on the local pixel block, all-reduce the sums
-    sd, sa = backend.recon_block(A_blk, n1, nj, n3, Uf, Sf, Vf, n2, plan.j0, Q, p, k)
-    t = torch.tensor([sd, sa], dtype=torch.float64, device=Ah.device)
+    # 7. relative error. Q is orthonormal, so ||A - A_k||^2 =
+    # (||A||^2 - ||Ahat||^2) + sum_i ||Ahat_i - U_i S_i V_i^T||^2 with ||A||^2 the
+    # Gram trace (replicated) and the slice sums all-reduced over the slice
+    # shards; when RE^2 < 2e-3 the difference could cancel, so the fused
+    # residual runs over the local pixel block instead (engine.cu
+    # compress_relative_error; every rank takes the same branch).
+    a2 = backend.gram_trace(Gm, n3)
+    t = torch.tensor([st, sa2], dtype=torch.float64, device=Ah.device)
     if G > 1:
         dist.all_reduce(t, group=group)
-    re = float((t[0].sqrt() / t[1].sqrt()).item())
+    num = (a2 - float(t[1].item())) + float(t[0].item())
+    if a2 > 0.0 and num >= 2e-3 * a2:
+        re = (num ** 0.5) / (a2 ** 0.5)
+    else:
+        sd, sa = backend.recon_block(A_blk, n1, nj, n3, Uf, Sf, Vf, n2, plan.j0, Q, p, k)
+        t = torch.tensor([sd, sa], dtype=torch.float64, device=Ah.device)
+        if G > 1:
+            dist.all_reduce(t, group=group)
+        re = float((t[0].sqrt() / t[1].sqrt()).item())
     return Q, Uf, Sf, Vf, re
 
 

@@ -92,6 +92,17 @@ class NumpyBackend:
         Qn = Q.permute(1, 0).contiguous().numpy().T
         return _ft(scale * np.einsum("ijl,kl->ijk", ch, Qn))
 
+    def gram_trace(self, G, n):
+        return float(np.trace(G.numpy().reshape(n, n)))
+
+    def slice_sums(self, S_loc, n1, n2, ps, k, U, s, V):
+        S = S_loc.permute(2, 1, 0).contiguous().numpy().transpose(2, 1, 0)
+        Un = U.permute(2, 1, 0).contiguous().numpy().transpose(2, 1, 0)
+        sn = s.permute(1, 0).contiguous().numpy().T
+        Vn = V.permute(2, 1, 0).contiguous().numpy().transpose(2, 1, 0)
+        rd = sum(float(np.sum((S[:, :, z] - (Un[:, :, z] * sn[:, z]) @ Vn[:, :, z].T) ** 2)) for z in range(ps))
+        return rd, float(np.sum(S ** 2))
+
     def recon_block(self, A_blk, n1, nj, n3, U, S, V, n2, j0, Q, p, k):
         A = A_blk.permute(2, 1, 0).contiguous().numpy().transpose(2, 1, 0)
         Un = U.permute(2, 1, 0).contiguous().numpy().transpose(2, 1, 0)
@@ -111,21 +122,21 @@ def _free_port():
     return port
 
 
-def _tensor(n1, n2, n3, seed=3):
+def _tensor(n1, n2, n3, seed=3, noise=1e-2):
     rng = np.random.default_rng(seed)
     r = 3
     a = np.einsum("ir,jr,kr->ijk", rng.standard_normal((n1, r)), rng.standard_normal((n2, r)),
-                  rng.standard_normal((n3, r))) + 1e-2 * rng.standard_normal((n1, n2, n3))
+                  rng.standard_normal((n3, r))) + noise * rng.standard_normal((n1, n2, n3))
     return np.asfortranarray(a)
 
 
-def _run(rank, world, port, shape, p, k, out_dir):
+def _run(rank, world, port, shape, p, k, out_dir, noise=1e-2):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         n1, n2, n3 = shape
-        a = _tensor(n1, n2, n3)
+        a = _tensor(n1, n2, n3, noise=noise)
         be = NumpyBackend()
         plan = pdist.make_plan(n1, n2, n3, p, world, rank, be)
         blk = _ft(a[:, plan.j0:plan.j0 + plan.nj, :])
@@ -139,13 +150,14 @@ def _run(rank, world, port, shape, p, k, out_dir):
 
 
 @pytest.mark.timeout(300)
-def test_sharded_compress_world2_matches_world1(tmp_path):
+@pytest.mark.parametrize("noise", [1e-2, 1.0])  # RE^2 below / above 2e-3: direct residual / orthogonal split
+def test_sharded_compress_world2_matches_world1(tmp_path, noise):
     shape, p, k = (16, 64, 24), 4, 3
     res = {}
     for world in (1, 2):
         d = tmp_path / f"w{world}"
         d.mkdir()
-        mp.spawn(_run, args=(world, _free_port(), shape, p, k, str(d)), nprocs=world, join=True)
+        mp.spawn(_run, args=(world, _free_port(), shape, p, k, str(d), noise), nprocs=world, join=True)
         res[world] = [np.load(d / f"r{r}.npz") for r in range(world)]
     one = res[1][0]
     for r in res[2]:
@@ -154,8 +166,15 @@ def test_sharded_compress_world2_matches_world1(tmp_path):
         np.testing.assert_allclose(r["U"], one["U"], atol=1e-10)
         np.testing.assert_allclose(r["V"], one["V"], atol=1e-10)
         assert abs(float(r["re"]) - float(one["re"])) <= 1e-13 * float(one["re"])
+    # the relative error is the directly measured ||A - tsvdq_reconstruct(F)|| / ||A||
+    a = _tensor(*shape, noise=noise)
+    Qn = one["Q"]
+    ch = np.stack([(one["U"][:, :, i] * one["S"][:, i]) @ one["V"][:, :, i].T for i in range(p)], axis=2)
+    rec = np.einsum("ijl,kl->ijk", ch, Qn)
+    re_direct = np.linalg.norm(a - rec) / np.linalg.norm(a)
+    assert (re_direct ** 2 >= 2e-3) == (noise >= 1.0)
+    assert abs(float(one["re"]) - re_direct) <= 1e-12 * re_direct
     # and the 1-process result is the plain (unsharded) pipeline
-    a = _tensor(*shape)
     T = a.reshape(-1, shape[2], order="F")
     w, Vg = np.linalg.eigh(T.T @ T)
     lam = np.sort(w)[::-1][:p]
