@@ -577,7 +577,7 @@ int ppc_tsvdq_compress(const double* A, int64_t n1, int64_t n2, int64_t n3, int6
         Out q(Q, n3 * p, loc), sg(sigma, sigma ? p : 0, loc), u(U, n1 * k * p, loc),
             sv(S, k * p, loc), v(V, n2 * k * p, loc);
         DeviceBuffer abuf, est(sizeof(double) * 4);  // trace(G), slice residual, ||Ahat||^2
-        OzakiDigits tdig;  // A's Gram digits, reused by the forward transform (device path)
+        OzakiDigits tdig;  // A's 7-digit Gram split, reused by the forward transform
         const double* dA = A;
         if (loc == PPC_HOST) {
             // Stream the input in row-chunk groups on a copy stream and start
@@ -600,7 +600,10 @@ int ppc_tsvdq_compress(const double* A, int64_t n1, int64_t n2, int64_t n3, int6
                 PPC_CUDA_CHECK(cudaEventDestroy(ready));
             }
             FiniteFlag nf(s);
-            bool checked = true;  // every slab's Gram pass also checked finiteness
+            bool checked = true;  // every slab's Gram pass also checked finiteness (INT8 path)
+            // the groups' digits land in one allocation, block c0 * blk_per_chunk on
+            const int64_t blk_per_chunk = (g.chunk + 4095) / 4096;
+            const bool keep = g.chunk % 4096 == 0;
             {
                 StageTimer tm("gram_syrk", s, (double)N * n3 * n3, 8.0 * N * n3);
                 for (int64_t c0 = 0; c0 < g.chunks; c0 += per) {
@@ -619,10 +622,12 @@ int ppc_tsvdq_compress(const double* A, int64_t n1, int64_t n2, int64_t n3, int6
                     PPC_CUDA_CHECK(cudaStreamWaitEvent(s, ev, 0));
                     PPC_CUDA_CHECK(cudaEventDestroy(ev));
                     checked &= gram_chunks(abuf.d() + r0, N, nr, n3, g.chunk, std::min(per, g.chunks - c0),
-                                           parts.d() + c0 * n3 * n3, s, nf.d());
+                                           parts.d() + c0 * n3 * n3, s, nf.d(), keep ? &tdig : nullptr,
+                                           c0 * blk_per_chunk, g.chunks * blk_per_chunk);
                 }
                 tree_reduce(parts.d(), g.chunks, n3 * n3, s);
             }
+            tdig.uniform = keep && checked && tdig.nd == 7;  // every group on the INT8 path
             if (checked)
                 nf.check(s, "svd");
             else

@@ -58,7 +58,7 @@ void sym_eig_top(const double* G, int64_t n, int64_t p, double* Q, double* lambd
 // Partial Grams of nchunks consecutive row chunks (T rows x n3, leading dim ldT).
 bool gram_chunks(const double* T, int64_t ldT, int64_t rows, int64_t n3, int64_t chunk,
                  int64_t nchunks, double* parts, cudaStream_t s, int* nonfinite = nullptr,
-                 OzakiDigits* keep = nullptr);
+                 OzakiDigits* keep = nullptr, int64_t block_base = 0, int64_t total_blocks = 0);
 // Eigensolve tail of data_q: Q (sign rule) and sigma from the Gram G.
 void eig_to_basis(const double* G, int64_t n3, int64_t p, double* Q, double* sigma, cudaStream_t s,
                   bool accurate_vectors = false);

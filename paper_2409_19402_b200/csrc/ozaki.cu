@@ -530,10 +530,12 @@ int64_t tri_tiles(int64_t n) {
 // Grams of `nout` outputs, each summing `per` digit blocks of d: out[ob] =
 // sum over its blocks of X_blk^T X_blk (cols x cols, column-major).
 void ozaki_syrk(const OzakiDigits& d, int64_t nout, int64_t per, double* out, cudaStream_t s, const char* stage,
-                double rows_total) {
+                double rows_total, int64_t block_base = 0) {
+    // the nout * per blocks from block_base on
+    const int8_t* D0 = d.D.as<int8_t>() + (size_t)block_base * d.nd * d.cols * d.KCp;
     CUtensorMap ma, mb;
-    if (!make_digit_map(&ma, d.D.as<int8_t>(), d.KCp, d.cols, d.nblk * d.nd, kBM) ||
-        !make_digit_map(&mb, d.D.as<int8_t>(), d.KCp, d.cols, d.nblk * d.nd, kBN))
+    if (!make_digit_map(&ma, D0, d.KCp, d.cols, nout * per * d.nd, kBM) ||
+        !make_digit_map(&mb, D0, d.KCp, d.cols, nout * per * d.nd, kBN))
         fail(PPC_CUDA, "ozaki: tensor map encoding failed");
     OzParams P;
     P.M = P.N = d.cols;
@@ -543,8 +545,8 @@ void ozaki_syrk(const OzakiDigits& d, int64_t nout, int64_t per, double* out, cu
     P.per = per;
     P.nd = d.nd;
     P.zmap = nullptr;
-    P.sa = P.sb = d.sc.d();
-    P.sq = d.sq.d();
+    P.sa = P.sb = d.sc.d() + block_base * d.cols;
+    P.sq = d.sq.d() + block_base * d.cols;
     P.C = out;
     P.ldc = d.cols;
     P.strideC = d.cols * d.cols;
@@ -561,30 +563,36 @@ void ozaki_syrk(const OzakiDigits& d, int64_t nout, int64_t per, double* out, cu
 
 void OzakiDigits::split(const double* X, int64_t ldx, int64_t stride, int64_t rows_, int64_t cols_, int64_t KC,
                         int64_t nblk_, cudaStream_t s, const int* zmap, int64_t nz, int64_t chunk, int64_t per,
-                        int* nonfinite, int ndig) {
+                        int* nonfinite, int ndig, int64_t block_base, int64_t alloc_blocks) {
     if (ndig != kS && ndig != kSmax) fail(PPC_ARGUMENT, "ozaki split: 6 or 7 digits");
+    if (block_base < 0 || (block_base > 0 && block_base + nblk_ > alloc_blocks))
+        fail(PPC_ARGUMENT, "ozaki split: block range outside the allocation");
     nd = ndig;
     if (KC < 1 || KC > kKC) fail(PPC_ARGUMENT, "ozaki split: block length out of range");
     if (zmap && !stride) fail(PPC_ARGUMENT, "ozaki split: a block map needs batched blocks");
     rows = rows_;
     cols = cols_;
-    nblk = nblk_;
+    const int64_t ncall = nblk_;
+    nblk = std::max(nblk_, alloc_blocks);
     KCp = (KC + kBK - 1) / kBK * kBK;
     const size_t dbytes = sizeof(int8_t) * nblk * nd * cols * KCp, sbytes = sizeof(double) * nblk * cols;
     if (D.bytes() < dbytes) D = DeviceBuffer(dbytes);
     if (sc.bytes() < sbytes) sc = DeviceBuffer(sbytes);
     if (sq.bytes() < sbytes) sq = DeviceBuffer(sbytes);
-    const int64_t launched = zmap ? nz : nblk;
+    const int64_t launched = zmap ? nz : ncall;
     if (launched <= 0) return;
     const double total_rows = stride ? (double)std::min(KC, rows) * launched : (double)rows;
     StageTimer ts("ozaki_split", s, 0.0, 8.0 * total_rows * cols + (double)nd * total_rows * cols);
     dim3 grid((unsigned)cols, (unsigned)launched);
+    int8_t* D0 = D.as<int8_t>() + (size_t)block_base * nd * cols * KCp;
+    double* sc0 = sc.d() + block_base * cols;
+    double* sq0 = sq.d() + block_base * cols;
     if (nd == kSmax)
         ozaki_split_kernel<kSmax><<<grid, 256, 0, s>>>(X, ldx, stride, rows, cols, KC, KCp, chunk ? chunk : KC,
-                                                       per ? per : 1, D.as<int8_t>(), sc.d(), sq.d(), zmap, nonfinite);
+                                                       per ? per : 1, D0, sc0, sq0, zmap, nonfinite);
     else
         ozaki_split_kernel<kS><<<grid, 256, 0, s>>>(X, ldx, stride, rows, cols, KC, KCp, chunk ? chunk : KC,
-                                                    per ? per : 1, D.as<int8_t>(), sc.d(), sq.d(), zmap, nonfinite);
+                                                    per ? per : 1, D0, sc0, sq0, zmap, nonfinite);
     count_launch();
     check_launch("ozaki_split");
 }
@@ -699,7 +707,8 @@ bool ozaki_recon_residual(const double* X, int64_t N, int64_t n3, const double* 
 }
 
 bool ozaki_gram_partials(const double* T, int64_t ldT, int64_t rows, int64_t n3, int64_t chunk, int64_t nchunks,
-                         double* parts, cudaStream_t s, int* nonfinite, OzakiDigits* keep) {
+                         double* parts, cudaStream_t s, int* nonfinite, OzakiDigits* keep, int64_t block_base,
+                         int64_t total_blocks) {
     if (!ozaki_enabled()) return false;
     // the integer path pays off once each output tile sees a long K range
     if (n3 < 128 || chunk < 4096 || rows < 4096 * 4) return false;
@@ -713,9 +722,11 @@ bool ozaki_gram_partials(const double* T, int64_t ldT, int64_t rows, int64_t n3,
     const bool retain = keep && chunk % kKC == 0;
     OzakiDigits local;
     OzakiDigits& d = retain ? *keep : local;
-    d.split(T, ldT, 0, rows, n3, kKC, nblk, s, nullptr, 0, chunk, per, nonfinite, retain ? kSmax : kS);
-    d.uniform = retain;
-    ozaki_syrk(d, nchunks, per, parts, s, "ozaki_syrk", (double)rows);
+    const int64_t base = retain ? block_base : 0;
+    d.split(T, ldT, 0, rows, n3, kKC, nblk, s, nullptr, 0, chunk, per, nonfinite, retain ? kSmax : kS, base,
+            retain ? total_blocks : 0);
+    if (retain && base == 0 && total_blocks == 0) d.uniform = true;  // streamed groups: the caller decides
+    ozaki_syrk(d, nchunks, per, parts, s, "ozaki_syrk", (double)rows, base);
     return true;
 }
 
@@ -737,7 +748,7 @@ __global__ void fold_q_kernel(const double* __restrict__ sc, const double* __res
 bool ozaki_mode3_forward(const OzakiDigits& td, int64_t N, const double* Q, int64_t p, double* out, cudaStream_t s) {
     static const bool off = std::getenv("PPC_OZAKI_FWD") && std::getenv("PPC_OZAKI_FWD")[0] == '0';
     if (off || !ozaki_enabled() || !td.uniform || td.nd != kSmax || td.KCp != kKC) return false;
-    const int64_t n3 = td.cols, nblk = td.nblk;
+    const int64_t n3 = td.cols, nblk = std::min(td.nblk, (N + kKC - 1) / kKC);  // blocks holding rows < N
     if (p < 64 || p % 64 || n3 < 256 || n3 > kKC || nblk * kKC < N) return false;
     StageTimer tm("mode3_fwd", s, 2.0 * N * n3 * p, 8.0 * (N * n3 + N * p + n3 * p));
     DeviceBuffer bq(sizeof(double) * nblk * n3 * p);

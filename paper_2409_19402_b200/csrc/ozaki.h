@@ -21,7 +21,9 @@ struct OzakiDigits {
     // zmap (device, nz entries; batched blocks only): split just those blocks
     void split(const double* X, int64_t ldx, int64_t stride, int64_t rows, int64_t cols, int64_t KC, int64_t nblk,
                cudaStream_t s, const int* zmap = nullptr, int64_t nz = 0, int64_t chunk = 0, int64_t per = 0,
-               int* nonfinite = nullptr, int ndig = 6);
+               int* nonfinite = nullptr, int ndig = 6, int64_t block_base = 0, int64_t alloc_blocks = 0);
+    // block_base / alloc_blocks: this call's nblk_ blocks land at block_base of an
+    // allocation of max(nblk_, alloc_blocks) blocks (streamed row groups).
 };
 
 // C_b (A.cols x B.cols, (m, n) at m + n*ldc, b at blk*strideC) = A_blk^T B_blk
@@ -51,8 +53,12 @@ bool ozaki_recon_residual(const double* X, int64_t N, int64_t n3, const double* 
 // keep (nullable): when the plan chunks are whole 4096-row blocks, T is split
 // into 7 digits (the SYRK still uses 6 levels) and the digits are left in
 // *keep for ozaki_mode3_forward.
+// block_base / total_blocks: T is one row group of a larger matrix whose digits
+// go to blocks [block_base, ...) of a total_blocks allocation in *keep (the
+// caller sets keep->uniform once every group has landed).
 bool ozaki_gram_partials(const double* T, int64_t ldT, int64_t rows, int64_t n3, int64_t chunk, int64_t nchunks,
-                         double* parts, cudaStream_t s, int* nonfinite = nullptr, OzakiDigits* keep = nullptr);
+                         double* parts, cudaStream_t s, int* nonfinite = nullptr, OzakiDigits* keep = nullptr,
+                         int64_t block_base = 0, int64_t total_blocks = 0);
 
 // out (N x p, leading dimension N) = T Q, the forward mode-3 transform, from
 // T's retained 7-digit Gram digits td (read MN-major: pixels contiguous per

@@ -101,10 +101,12 @@ void tree_reduce(double* parts, int64_t nparts, int64_t elems, cudaStream_t s) {
 // Partial Grams of `nchunks` consecutive chunks of `chunk` rows of T (rows x
 // n3, leading dimension ldT) into parts (nchunks x n3 x n3).
 bool gram_chunks(const double* T, int64_t ldT, int64_t rows, int64_t n3, int64_t chunk,
-                 int64_t nchunks, double* parts, cudaStream_t s, int* nonfinite, OzakiDigits* keep) {
+                 int64_t nchunks, double* parts, cudaStream_t s, int* nonfinite, OzakiDigits* keep,
+                 int64_t block_base, int64_t total_blocks) {
     // INT8 tensor-core (Ozaki) path for large Grams; it reads T column by
     // column, so no re-layout either
-    if (ozaki_gram_partials(T, ldT, rows, n3, chunk, nchunks, parts, s, nonfinite, keep)) return nonfinite != nullptr;
+    if (ozaki_gram_partials(T, ldT, rows, n3, chunk, nchunks, parts, s, nonfinite, keep, block_base, total_blocks))
+        return nonfinite != nullptr;
     // Large tube matrices: each SYRK pipeline stage would touch one 2 MB page
     // per column (columns are ldT*8 bytes apart), thrashing the TLB. Re-lay T
     // into 2048-row blocks first (one extra HBM pass); same summation order.
