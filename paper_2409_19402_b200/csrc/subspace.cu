@@ -373,7 +373,7 @@ void cholqr3(Work& w, double* Y, double* Xout, int64_t c0, cudaStream_t s, const
     double* bufs[3] = {w.Yn.d() + c0 * r, w.Z.d() + c0 * r, Xout + c0 * r};
     for (int pass = 0; pass < 3; ++pass) {
         gg(src, r, per, true, src, r, per, w.S.d(), bc, bc * bc, bc, bc, r, batch, 1.0, 0.0, s, zm, zx);  // S = Y^T Y
-        chol_inv_kernel<<<(unsigned)batch, bc > 64 ? 1024 : 256, smem, s>>>(w.S.d(), w.Rinv.d(), bc,
+        chol_inv_kernel<<<(unsigned)batch, bc > 16 ? 1024 : 256, smem, s>>>(w.S.d(), w.Rinv.d(), bc,
                                                                              pass == 0 ? 1 : 0,
                                                                              w.fail.as<int>(), nullptr, zm);
         count_launch();
@@ -399,7 +399,7 @@ void cholqr_inplace(double* Z, int64_t r, int64_t k, cudaStream_t s) {
     double* dst = T.d();
     for (int pass = 0; pass < 3; ++pass) {
         gg(src, r, r * k, true, src, r, r * k, S.d(), k, k * k, k, k, r, 1, 1.0, 0.0, s);  // S = Z^T Z
-        chol_inv_kernel<<<1, k > 64 ? 1024 : 256, smem, s>>>(S.d(), Ri.d(), k, pass == 0 ? 1 : 0, nullptr,
+        chol_inv_kernel<<<1, k > 16 ? 1024 : 256, smem, s>>>(S.d(), Ri.d(), k, pass == 0 ? 1 : 0, nullptr,
                                                              nullptr);
         count_launch();
         check_launch("chol_inv");
@@ -868,12 +868,12 @@ void subspace_svd(const double* A, int64_t m, int64_t n, int64_t stride, int64_t
     if (ksm > 48 * 1024)
         PPC_CUDA_CHECK(cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ksm));
     g_AtB(Wb.d(), Wb.d(), Sk.d(), o, k, k, batch, o * k, o * k, s);
-    chol_inv_kernel<<<(unsigned)batch, 256, ksm, s>>>(Sk.d(), Ri.d(), k, 0, flag.as<int>(), R1.d());
+    chol_inv_kernel<<<(unsigned)batch, k > 16 ? 1024 : 256, ksm, s>>>(Sk.d(), Ri.d(), k, 0, flag.as<int>(), R1.d());
     count_launch();
     check_launch("chol_inv");
     g_AB(Wb.d(), Ri.d(), T1.d(), o, k, k, batch, o * k, k * k, 1.0, nullptr, 0.0, s);
     g_AtB(T1.d(), T1.d(), Sk.d(), o, k, k, batch, o * k, o * k, s);
-    chol_inv_kernel<<<(unsigned)batch, 256, ksm, s>>>(Sk.d(), Ri.d(), k, 0, flag.as<int>(), R2.d());
+    chol_inv_kernel<<<(unsigned)batch, k > 16 ? 1024 : 256, ksm, s>>>(Sk.d(), Ri.d(), k, 0, flag.as<int>(), R2.d());
     count_launch();
     check_launch("chol_inv");
     g_AB(T1.d(), Ri.d(), Qw.d(), o, k, k, batch, o * k, k * k, 1.0, nullptr, 0.0, s);
