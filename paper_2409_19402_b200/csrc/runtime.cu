@@ -2,6 +2,7 @@
 // workspace, host<->device staging. Replaces the reference's L2 runtime
 // (parallel.cpp:13-57: slice loops over std::threads) with CUDA grids on one
 // device per host thread.
+#include <chrono>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -100,7 +101,7 @@ void check_launch(const char* name) {
     if (e != cudaSuccess) fail(PPC_CUDA, std::string(name) + " launch: " + cudaGetErrorString(e));
 }
 
-// Large buffers (>= 256 MB: tensor-sized transforms, digit planes, slice
+// Large buffers (>= 32 MB: tensor-sized transforms, digit planes, slice
 // Grams) recur with identical sizes from call to call. They are kept in a
 // per-thread, per-device exact-size cache instead of going back to the
 // stream-ordered pool: freed multi-GB blocks that the pool later carves small
@@ -108,7 +109,7 @@ void check_launch(const char* name) {
 // stalls inside the Gram. A cached block carries the event of its release, so
 // reuse on another stream still waits for the last user.
 namespace {
-constexpr size_t kBigBytes = size_t(256) << 20;
+constexpr size_t kBigBytes = size_t(32) << 20;
 struct BigBlock {
     size_t bytes;
     void* p;
@@ -172,6 +173,14 @@ DeviceBuffer::DeviceBuffer(size_t bytes) : n_(bytes) {
             e = cudaMalloc(&p_, bytes);
         }
         PPC_CUDA_CHECK(e);
+        return;
+    }
+    static const bool trace = std::getenv("PPC_TRACE_ALLOC") != nullptr;
+    if (trace) {
+        const auto t0 = std::chrono::steady_clock::now();
+        PPC_CUDA_CHECK(cudaMallocAsync(&p_, bytes, s));
+        const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        if (ms > 2.0) fprintf(stderr, "[alloc] pool %.1f MB took %.1f ms\n", bytes / 1e6, ms);
         return;
     }
     PPC_CUDA_CHECK(cudaMallocAsync(&p_, bytes, s));

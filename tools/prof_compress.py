@@ -18,6 +18,8 @@ ap.add_argument("--p", type=int, default=128)
 ap.add_argument("--k", type=int, default=32)
 ap.add_argument("--warm", type=int, default=1)
 ap.add_argument("--reps", type=int, default=1)
+ap.add_argument("--per-call", action="store_true", help="stage timers of every call (slow calls only)")
+ap.add_argument("--empty-cache", action="store_true", help="return torch's cached blocks after building A")
 args = ap.parse_args()
 
 import torch  # noqa: E402
@@ -28,6 +30,8 @@ L = _lib.lib()
 n1, n2, n3 = args.shape
 p, k = args.p, args.k
 A = synth.cp_tensor_device(n1, n2, n3, rank=50, noise=1e-3, seed=0)
+if args.empty_cache:
+    torch.cuda.empty_cache()
 Q = pp.empty_device((n3, p))
 U = pp.empty_device((n1, k, p))
 S = pp.empty_device((k, p))
@@ -48,6 +52,9 @@ def call():
 for _ in range(args.warm):
     call()
 torch.cuda.synchronize()
+fr, tot = torch.cuda.mem_get_info()
+print(f"device memory: free {fr / 1e9:.1f} GB of {tot / 1e9:.1f}; torch reserved {torch.cuda.memory_reserved() / 1e9:.1f} GB",
+      flush=True)
 buf = C.create_string_buffer(1 << 16)
 L.ppc_timing_report(buf, len(buf), 1)
 L.ppc_timing_enable(1)
@@ -55,7 +62,14 @@ for _ in range(args.reps):
     t0 = time.perf_counter()
     re = call()
     torch.cuda.synchronize()
-    print(f"compress {1e3 * (time.perf_counter() - t0):.1f} ms  RE {re:.12e}", flush=True)
+    ms = 1e3 * (time.perf_counter() - t0)
+    print(f"compress {ms:.1f} ms  RE {re:.12e}", flush=True)
+    if args.per_call:
+        L.ppc_timing_report(buf, len(buf), 1)
+        if ms > 200:
+            import json
+            d = json.loads(buf.value.decode())
+            print("SLOW", {k: round(v["ms"], 2) for k, v in d.items()}, flush=True)
 L.ppc_timing_enable(0)
 L.ppc_timing_report(buf, len(buf), 1)
 print(buf.value.decode())
