@@ -1074,3 +1074,55 @@ def test_ozaki_forward_transform_noise_slices(engine):
     finally:
         L.ppc_set_ozaki(1)
     assert (np.abs(s_fwd - s_off) <= 1e-10 * s_off).all(), np.max(np.abs(s_fwd - s_off) / s_off)
+
+
+def _eig_case(kind, n, seed=0):
+    rng = np.random.default_rng(seed)
+    if kind == "spiked":  # rank-50 spikes over a Marchenko-Pastur plateau (the cfg5 Gram)
+        F = rng.standard_normal((n, 50)) * np.sqrt(np.logspace(9.8, 6, 50))
+        Nn = rng.standard_normal((n, 4 * n))
+        G = F @ F.T + 4.2 / (4 * n) * (Nn @ Nn.T)
+    elif kind == "lowrank":  # zero-eigenvalue cluster inside the wanted set
+        F = rng.standard_normal((n, 30))
+        G = F @ F.T
+    else:  # exactly repeated eigenvalues
+        Qr, _ = np.linalg.qr(rng.standard_normal((n, n)))
+        lam = np.concatenate([np.full(40, 5.0), np.full(40, 3.0), np.linspace(1, 0, n - 80)])
+        G = (Qr * lam) @ Qr.T
+    return 0.5 * (G + G.T)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind,n,p", [("spiked", 1024, 128), ("lowrank", 512, 48), ("repeated", 300, 100),
+                                      ("spiked", 200, 20)])
+def test_direct_eigensolver(engine, kind, n, p):
+    """ppc_sym_eig_top on one Gram (Householder tridiagonalization, bisection,
+    inverse iteration, CholQR3, compact-WY back-transform): eigenvalues within
+    1e-13 lambda_1 of LAPACK, orthonormal to 1e-13, residuals 1e-13 lambda_1,
+    captured energy to 1e-13, the sign rule, and bitwise repeatable."""
+    import ctypes as C
+    import torch
+    from paper_2409_19402_b200 import _lib
+    L = _lib.lib()
+    G = _eig_case(kind, n)
+    w = np.linalg.eigvalsh(G)[::-1]
+    g = torch.tensor(np.asfortranarray(G).ravel(order="F"), device="cuda")
+    outs = []
+    for _ in range(2):
+        Qd = torch.empty((p, n), dtype=torch.float64, device="cuda")
+        Sd = torch.empty(p, dtype=torch.float64, device="cuda")
+        assert L.ppc_sym_eig_top(C.c_void_p(g.data_ptr()), n, p, C.c_void_p(Qd.data_ptr()),
+                                 C.c_void_p(Sd.data_ptr()), 1) == 0, L.ppc_last_error()
+        torch.cuda.synchronize()  # device pointers: the call is stream-ordered on the engine's stream
+        outs.append((Qd.cpu().numpy().T.copy(), Sd.cpu().numpy() ** 2))
+    (Q, lam), (Q2, lam2) = outs
+    assert np.array_equal(Q, Q2) and np.array_equal(lam, lam2)
+    l1 = w[0]
+    assert np.max(np.abs(lam - w[:p])) <= 1e-13 * l1
+    assert np.max(np.abs(Q.T @ Q - np.eye(p))) <= 1e-13
+    # residuals: ~1e-15 lambda_1 on separated spectra; the exactly repeated
+    # clusters leave ~1e-12 (vectors arbitrary within the eigenspace)
+    assert np.max(np.linalg.norm(G @ Q - Q * lam, axis=0)) <= (1e-11 if kind == "repeated" else 1e-13) * l1
+    assert abs(np.trace(Q.T @ G @ Q) - w[:p].sum()) <= 1e-13 * w[:p].sum()
+    big = np.argmax(np.abs(Q), axis=0)  # matrix_kernels.cpp:16-25
+    assert (Q[big, np.arange(p)] >= 0).all()
