@@ -600,7 +600,7 @@ void OzakiDigits::split(const double* X, int64_t ldx, int64_t stride, int64_t ro
 void ozaki_gemm(const OzakiDigits& A, const OzakiDigits& B, int64_t nbatch, const int* zmap, double* C, int64_t ldc,
                 int64_t strideC, cudaStream_t s, int levels) {
     if (A.KCp != B.KCp) fail(PPC_ARGUMENT, "ozaki_gemm: K mismatch");
-    if (levels != kS && levels != 4) fail(PPC_ARGUMENT, "ozaki_gemm: levels must be 6 or 4");
+    if (levels != kS && levels != 4 && levels != 3) fail(PPC_ARGUMENT, "ozaki_gemm: levels must be 6, 4 or 3");
     // 64-wide output tiles for panels of <= 64 columns (the 80-wide tile
     // would spend a fifth of the MMAs on zero rows)
     const int bn = (B.cols <= 64) ? 64 : kBN;
@@ -629,12 +629,13 @@ void ozaki_gemm(const OzakiDigits& A, const OzakiDigits& B, int64_t nbatch, cons
     P.ldx = P.strideX = P.m_total = 0;
     P.partial = nullptr;
     const double K = (double)std::min(A.rows, kKC);
-    StageTimer tk(levels == kS ? "ozaki_gemm" : "ozaki_gemm_l4", s,
+    StageTimer tk(levels == kS ? "ozaki_gemm" : (levels == 4 ? "ozaki_gemm_l4" : "ozaki_gemm_l3"), s,
                   2.0 * levels * (levels + 1) / 2 * (double)nbatch * P.M * P.N * K,
                   (double)levels * nbatch * (P.M + P.N) * K);
     if (bn == kBN) launch_mma<false>(ma, mb, P, nbatch * P.tiles, s);
     else if (levels == kS) launch_mma<false, false, false, 64, kS>(ma, mb, P, nbatch * P.tiles, s);
-    else launch_mma<false, false, false, 64, 4>(ma, mb, P, nbatch * P.tiles, s);
+    else if (levels == 4) launch_mma<false, false, false, 64, 4>(ma, mb, P, nbatch * P.tiles, s);
+    else launch_mma<false, false, false, 64, 3>(ma, mb, P, nbatch * P.tiles, s);
 }
 
 bool ozaki_gemm_eligible(int64_t M, int64_t K) { return ozaki_enabled() && M >= kBM && K >= 256 && K <= kKC; }

@@ -29,9 +29,9 @@ struct OzakiDigits {
 // C_b (A.cols x B.cols, (m, n) at m + n*ldc, b at blk*strideC) = A_blk^T B_blk
 // for the nbatch blocks blk = zmap[b] (or b): the FP64 product of the two
 // split operands on the INT8 tensor cores (exact int32 digit-level sums).
-// levels = 4 (B.cols <= 64 only) keeps digit pairs of levels <= 5: ~1e-9
-// relative precision at half the MMAs, for products that only steer an
-// iteration (the Chebyshev filter far from convergence).
+// levels = 4 / 3 (B.cols <= 64 only) keep digit pairs of levels <= 5 / 4:
+// ~1e-9 / ~1e-7 relative precision at 1/2 / 3/10 of the MMAs, for products
+// that only steer an iteration (the Chebyshev filter far from convergence).
 void ozaki_gemm(const OzakiDigits& A, const OzakiDigits& B, int64_t nbatch, const int* zmap, double* C, int64_t ldc,
                 int64_t strideC, cudaStream_t s, int levels = 6);
 // Whether the integer path applies to an output with M rows and K-length sums.

@@ -458,7 +458,8 @@ void rayleigh_ritz(Work& w, const double* G, int64_t sG, double* Xn, int64_t c0,
 }  // namespace
 
 // Reduced-precision filter products while every unlocked residual of a slice
-// exceeds this fraction of its theta_1 (PPC_FILTER_LOWP; 0 disables).
+// exceeds this fraction of its theta_1 (PPC_FILTER_LOWP; 0 disables): 4 digit
+// levels above it, 3 levels above 1000x it.
 static double filter_lowp() {
     static const double v = std::getenv("PPC_FILTER_LOWP") ? std::atof(std::getenv("PPC_FILTER_LOWP")) : 1e-6;
     return v;
@@ -543,7 +544,7 @@ void subspace_eig_top(const double* G, int64_t r, int64_t batch, int64_t k, doub
         // filter's precision floor (~1e-9 |G|): their products take 4 digit
         // levels (half the MMAs); locking always uses FP64 Rayleigh-Ritz
         // residuals, so this only steers the iteration
-        std::vector<char> lowp(batch, 0);
+        std::vector<char> lowp(batch, 0);  // 0: 6 levels, 1: 4 levels, 2: 3 levels
         std::vector<double> cc(batch), ee(batch);
         for (int64_t sl = 0; sl < batch; ++sl) {
             const double* t = &th[sl * b];
@@ -630,7 +631,7 @@ void subspace_eig_top(const double* G, int64_t r, int64_t batch, int64_t k, doub
             if (vectors_for_reconstruction && filter_lowp() > 0.0) {
                 double rmin = 1e300;
                 for (int64_t j = L; j < k; ++j) rmin = std::min(rmin, rr[j]);
-                lowp[sl] = rmin > filter_lowp() * scale;
+                lowp[sl] = rmin > filter_lowp() * scale ? (rmin > 1e3 * filter_lowp() * scale ? 2 : 1) : 0;
             }
             // Chebyshev interval [0, ub]: damp everything below the smallest Ritz value
             const double ub = std::max(t[b - 1], 0.0);
@@ -692,12 +693,13 @@ void subspace_eig_top(const double* G, int64_t r, int64_t batch, int64_t k, doub
             }
         if ((int64_t)coef.size() * 8 > (int64_t)w.coef.bytes()) w.coef = DeviceBuffer(coef.size() * sizeof(double));
         // per degree: every filtering slice | the reduced-precision ones | the rest
-        std::vector<int> zm((size_t)3 * dmax * batch), nact(dmax, 0), nlo(dmax, 0), nhi(dmax, 0);
+        std::vector<int> zm((size_t)4 * dmax * batch), nact(dmax, 0), nlo(dmax, 0), nhi(dmax, 0), nl3(dmax, 0);
         for (int j = 0; j < dmax; ++j)
             for (int64_t sl = 0; sl < batch; ++sl)
                 if (j < deg[sl]) {
                     zm[(size_t)j * batch + nact[j]++] = (int)sl;
-                    if (lowp[sl]) zm[(size_t)(dmax + j) * batch + nlo[j]++] = (int)sl;
+                    if (lowp[sl] == 1) zm[(size_t)(dmax + j) * batch + nlo[j]++] = (int)sl;
+                    else if (lowp[sl] == 2) zm[(size_t)(3 * dmax + j) * batch + nl3[j]++] = (int)sl;
                     else zm[(size_t)(2 * dmax + j) * batch + nhi[j]++] = (int)sl;
                 }
         if ((int64_t)zm.size() * 4 > (int64_t)w.zmap.bytes()) w.zmap = DeviceBuffer(zm.size() * sizeof(int));
@@ -730,8 +732,10 @@ void subspace_eig_top(const double* G, int64_t r, int64_t batch, int64_t k, doub
                         Yd.split(Y + cf * r, r, per, r, bf, r, batch, s, zm, na);
                         const int* zlo = w.zmap.as<int>() + (int64_t)(dmax + j) * batch;
                         const int* zhi = w.zmap.as<int>() + (int64_t)(2 * dmax + j) * batch;
-                        if (bf <= 64 && nlo[j] > 0) {
-                            ozaki_gemm(Gd, Yd, nlo[j], zlo, w.Z.d() + cf * r, r, per, s, 4);
+                        const int* zl3 = w.zmap.as<int>() + (int64_t)(3 * dmax + j) * batch;
+                        if (bf <= 64 && nlo[j] + nl3[j] > 0) {
+                            if (nl3[j] > 0) ozaki_gemm(Gd, Yd, nl3[j], zl3, w.Z.d() + cf * r, r, per, s, 3);
+                            if (nlo[j] > 0) ozaki_gemm(Gd, Yd, nlo[j], zlo, w.Z.d() + cf * r, r, per, s, 4);
                             if (nhi[j] > 0) ozaki_gemm(Gd, Yd, nhi[j], zhi, w.Z.d() + cf * r, r, per, s);
                         } else {
                             ozaki_gemm(Gd, Yd, na, zm, w.Z.d() + cf * r, r, per, s);
