@@ -70,7 +70,8 @@ __global__ void __launch_bounds__(256) ozaki_split_kernel(const double* __restri
                                                           int64_t rows, int64_t cols, int64_t KC, int64_t KCp,
                                                           int64_t chunk, int64_t per, int8_t* __restrict__ D,
                                                           double* __restrict__ scale, double* __restrict__ sumsq,
-                                                          const int* __restrict__ zmap, int* __restrict__ nonfinite) {
+                                                          const int* __restrict__ zmap, int* __restrict__ nonfinite,
+                                                          const double* __restrict__ fixed_max) {
     __shared__ double stage[kKC];
     const int64_t j = blockIdx.x;
     const int64_t b = zmap ? zmap[blockIdx.y] : blockIdx.y;
@@ -121,7 +122,7 @@ __global__ void __launch_bounds__(256) ozaki_split_kernel(const double* __restri
         }
     }
     __syncthreads();
-    mx = red[0];
+    mx = fixed_max ? fixed_max[b] : red[0];  // a block-wide bound: one scale for every column
     // sigma = 2^e > 2 max |x| (mx = 0: all digits zero)
     const int e = mx > 0.0 ? ilogb(mx) + 2 : 0;
     if (threadIdx.x == 0) scale[b * cols + j] = mx > 0.0 ? ldexp(1.0, e) : 0.0;
@@ -218,10 +219,15 @@ __device__ __forceinline__ void decode_item(const OzParams& P, int64_t item, int
 // NL: digit levels computed (levels 2..NL+1, digits 1..NL of each operand:
 // kS = full FP64 accuracy; fewer give ~2^(-8 NL + 1) relative precision for
 // products that only steer an iteration).
-template <bool SYM, bool AMN, bool RESID, int BN = kBN, int NL = kS>
+// SYMA: A is symmetric with one scale per block (square digit blocks): its
+// tiles are read from the upper triangle only, K-major where the 64-byte K
+// stage lies at or left of the tile's rows and MN-major (mapA2, the same
+// planes as 64 x 64 boxes) where it lies to the right: half the DRAM reads of
+// A for products that stream it (the Chebyshev filter's G Y).
+template <bool SYM, bool AMN, bool RESID, int BN = kBN, int NL = kS, bool SYMA = false>
 __global__ void __launch_bounds__(kThreads, 1)
     ozaki_mma_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
-                     const OzParams P, int64_t items) {
+                     const __grid_constant__ CUtensorMap mapA2, const OzParams P, int64_t items) {
     static_assert(NL * BN <= 512 && BN % 16 == 0 && (BN / 2) % 8 == 0 && NL >= 1 && NL <= kSmax, "tile shape");
     extern __shared__ uint8_t smem_raw[];
     uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -265,10 +271,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const int kx = (int)(gl % nkc) * kBK;
                     uint8_t* sa = base + st * STAGE;
                     uint8_t* sb = sa + NL * A_TILE;
+                    const bool mn = SYMA && kx >= mb * kBM + kBM;  // stage right of the tile: read transposed
 #pragma unroll
                     for (int s = 0; s < NL; ++s) {
                         const int plane = (int)(blk * P.nd + s);
-                        if (AMN) {
+                        if (SYMA && mn) {
+                            tma_load_3d(sa + s * A_TILE, &mapA2, &full[st], (int)(mb * kBM), kx, plane);
+                            tma_load_3d(sa + s * A_TILE + 4096, &mapA2, &full[st], (int)(mb * kBM + 64), kx, plane);
+                        } else if (AMN) {
                             tma_load_3d(sa + s * A_TILE, &mapA, &full[st], (int)(mb * kBM), kx, plane);
                             tma_load_3d(sa + s * A_TILE + 4096, &mapA, &full[st], (int)(mb * kBM + 64), kx, plane);
                         } else {
@@ -293,6 +303,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         constexpr uint32_t kIdesc3 = idesc_i8<kBM, 3 * BN>() | kAmn;
         int64_t g = 0, cg = 0;  // stage and digit-block counters across items
         for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
+            int64_t mb_item = 0;
+            if (SYMA) {
+                int64_t ob_, nb_;
+                decode_item<SYM>(P, item, ob_, mb_item, nb_);
+            }
             for (int64_t cc = 0; cc < per; ++cc, ++cg) {
                 if (cg > 0) {  // the epilogue has drained the previous block's levels
                     bar_wait(tempty, (uint32_t)((cg - 1) & 1));
@@ -305,19 +320,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (elect_one()) {
                         const uint8_t* sa = base + st * STAGE;
                         const uint8_t* sb = sa + NL * A_TILE;
+                        const bool mn = SYMA && (int64_t)kb * kBK >= mb_item * kBM + kBM;
+                        const uint32_t amn = (AMN || mn) ? (1u << 15) : 0u;
 #pragma unroll
                         for (int kk = 0; kk < kBK / 32; ++kk) {
                             // digit 1 of A spans every level: its MMAs start the block
                             const uint32_t acc0 = (kb > 0 || kk > 0) ? 1u : 0u;
 #pragma unroll
                             for (int i = 1; i <= NL; ++i) {
-                                const uint64_t da = AMN ? sdesc_mn_sw64(sa + (i - 1) * A_TILE + kk * 2048, 4096)
-                                                        : sdesc_k_sw64(sa + (i - 1) * A_TILE) + (uint64_t)(kk * 2);
+                                const uint64_t da = (AMN || mn) ? sdesc_mn_sw64(sa + (i - 1) * A_TILE + kk * 2048, 4096)
+                                                                : sdesc_k_sw64(sa + (i - 1) * A_TILE) + (uint64_t)(kk * 2);
                                 const int jmax = NL + 1 - i;  // levels i + j <= NL + 1
 #pragma unroll
                                 for (int j0 = 1; j0 <= jmax; j0 += 3) {
                                     const int nj = jmax - j0 + 1 < 3 ? jmax - j0 + 1 : 3;
-                                    const uint32_t idesc = nj == 3 ? kIdesc3 : (nj == 2 ? kIdesc2 : kIdesc1);
+                                    const uint32_t idesc = (nj == 3 ? kIdesc3 : (nj == 2 ? kIdesc2 : kIdesc1)) | amn;
                                     const uint64_t db = sdesc_k_sw64(sb + (j0 - 1) * B_TILE) + (uint64_t)(kk * 2);
                                     mma_i8(tmem + (uint32_t)((i + j0 - 2) * BN), da, db, idesc, i == 1 ? acc0 : 1u);
                                 }
@@ -503,18 +520,20 @@ bool ozaki_enabled() {
 
 int64_t ozaki_grid(int64_t items) { return std::min<int64_t>(items, ctx().sms); }  // one persistent CTA per SM
 
-template <bool SYM, bool AMN = false, bool RESID = false, int BN = kBN, int NL = kS>
-void launch_mma(const CUtensorMap& ma, const CUtensorMap& mb, const OzParams& P, int64_t items, cudaStream_t s) {
+template <bool SYM, bool AMN = false, bool RESID = false, int BN = kBN, int NL = kS, bool SYMA = false>
+void launch_mma(const CUtensorMap& ma, const CUtensorMap& mb, const OzParams& P, int64_t items, cudaStream_t s,
+                const CUtensorMap* ma2 = nullptr) {
     // stages + barriers + TMEM slot + the epilogue warps' residual sums
     const size_t smem = 1024 + (size_t)kStages * NL * (kBM + BN) * kBK + (2 * kStages + 2) * 8 + 16 + 16 * kEpiWarps;
     static bool attr = false;
     if (!attr) {
-        PPC_CUDA_CHECK(cudaFuncSetAttribute(ozaki_mma_kernel<SYM, AMN, RESID, BN, NL>,
+        PPC_CUDA_CHECK(cudaFuncSetAttribute(ozaki_mma_kernel<SYM, AMN, RESID, BN, NL, SYMA>,
                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = true;
     }
     if (items == 0) return;
-    ozaki_mma_kernel<SYM, AMN, RESID, BN, NL><<<(unsigned)ozaki_grid(items), kThreads, smem, s>>>(ma, mb, P, items);
+    ozaki_mma_kernel<SYM, AMN, RESID, BN, NL, SYMA><<<(unsigned)ozaki_grid(items), kThreads, smem, s>>>(
+        ma, mb, ma2 ? *ma2 : ma, P, items);
     count_launch();
     check_launch("ozaki_mma");
 }
@@ -563,7 +582,8 @@ void ozaki_syrk(const OzakiDigits& d, int64_t nout, int64_t per, double* out, cu
 
 void OzakiDigits::split(const double* X, int64_t ldx, int64_t stride, int64_t rows_, int64_t cols_, int64_t KC,
                         int64_t nblk_, cudaStream_t s, const int* zmap, int64_t nz, int64_t chunk, int64_t per,
-                        int* nonfinite, int ndig, int64_t block_base, int64_t alloc_blocks) {
+                        int* nonfinite, int ndig, int64_t block_base, int64_t alloc_blocks,
+                        const double* fixed_max) {
     if (ndig != kS && ndig != kSmax) fail(PPC_ARGUMENT, "ozaki split: 6 or 7 digits");
     if (block_base < 0 || (block_base > 0 && block_base + nblk_ > alloc_blocks))
         fail(PPC_ARGUMENT, "ozaki split: block range outside the allocation");
@@ -589,16 +609,16 @@ void OzakiDigits::split(const double* X, int64_t ldx, int64_t stride, int64_t ro
     double* sq0 = sq.d() + block_base * cols;
     if (nd == kSmax)
         ozaki_split_kernel<kSmax><<<grid, 256, 0, s>>>(X, ldx, stride, rows, cols, KC, KCp, chunk ? chunk : KC,
-                                                       per ? per : 1, D0, sc0, sq0, zmap, nonfinite);
+                                                       per ? per : 1, D0, sc0, sq0, zmap, nonfinite, fixed_max);
     else
         ozaki_split_kernel<kS><<<grid, 256, 0, s>>>(X, ldx, stride, rows, cols, KC, KCp, chunk ? chunk : KC,
-                                                    per ? per : 1, D0, sc0, sq0, zmap, nonfinite);
+                                                    per ? per : 1, D0, sc0, sq0, zmap, nonfinite, fixed_max);
     count_launch();
     check_launch("ozaki_split");
 }
 
 void ozaki_gemm(const OzakiDigits& A, const OzakiDigits& B, int64_t nbatch, const int* zmap, double* C, int64_t ldc,
-                int64_t strideC, cudaStream_t s, int levels) {
+                int64_t strideC, cudaStream_t s, int levels, bool sym_a) {
     if (A.KCp != B.KCp) fail(PPC_ARGUMENT, "ozaki_gemm: K mismatch");
     if (levels != kS && levels != 4 && levels != 3) fail(PPC_ARGUMENT, "ozaki_gemm: levels must be 6, 4 or 3");
     // 64-wide output tiles for panels of <= 64 columns (the 80-wide tile
@@ -632,6 +652,15 @@ void ozaki_gemm(const OzakiDigits& A, const OzakiDigits& B, int64_t nbatch, cons
     StageTimer tk(levels == kS ? "ozaki_gemm" : (levels == 4 ? "ozaki_gemm_l4" : "ozaki_gemm_l3"), s,
                   2.0 * levels * (levels + 1) / 2 * (double)nbatch * P.M * P.N * K,
                   (double)levels * nbatch * (P.M + P.N) * K);
+    if (sym_a && bn == 64 && A.cols == A.rows && A.KCp == A.cols && A.nd == kS) {
+        CUtensorMap ma2;  // the same planes as 64 x 64 MN-major boxes
+        if (!make_digit_map(&ma2, A.D.as<int8_t>(), A.KCp, A.cols, A.nblk * A.nd, 64))
+            fail(PPC_CUDA, "ozaki: tensor map encoding failed");
+        if (levels == kS) launch_mma<false, false, false, 64, kS, true>(ma, mb, P, nbatch * P.tiles, s, &ma2);
+        else if (levels == 4) launch_mma<false, false, false, 64, 4, true>(ma, mb, P, nbatch * P.tiles, s, &ma2);
+        else launch_mma<false, false, false, 64, 3, true>(ma, mb, P, nbatch * P.tiles, s, &ma2);
+        return;
+    }
     if (bn == kBN) launch_mma<false>(ma, mb, P, nbatch * P.tiles, s);
     else if (levels == kS) launch_mma<false, false, false, 64, kS>(ma, mb, P, nbatch * P.tiles, s);
     else if (levels == 4) launch_mma<false, false, false, 64, 4>(ma, mb, P, nbatch * P.tiles, s);

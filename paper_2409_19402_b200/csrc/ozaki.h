@@ -21,7 +21,10 @@ struct OzakiDigits {
     // zmap (device, nz entries; batched blocks only): split just those blocks
     void split(const double* X, int64_t ldx, int64_t stride, int64_t rows, int64_t cols, int64_t KC, int64_t nblk,
                cudaStream_t s, const int* zmap = nullptr, int64_t nz = 0, int64_t chunk = 0, int64_t per = 0,
-               int* nonfinite = nullptr, int ndig = 6, int64_t block_base = 0, int64_t alloc_blocks = 0);
+               int* nonfinite = nullptr, int ndig = 6, int64_t block_base = 0, int64_t alloc_blocks = 0,
+               const double* fixed_max = nullptr);
+    // fixed_max (device, per block): a bound on max|x| over the whole block,
+    // giving every column the same scale (symmetric operands, sym_a below).
     // block_base / alloc_blocks: this call's nblk_ blocks land at block_base of an
     // allocation of max(nblk_, alloc_blocks) blocks (streamed row groups).
 };
@@ -32,8 +35,10 @@ struct OzakiDigits {
 // levels = 4 / 3 (B.cols <= 64 only) keep digit pairs of levels <= 5 / 4:
 // ~1e-9 / ~1e-7 relative precision at 1/2 / 3/10 of the MMAs, for products
 // that only steer an iteration (the Chebyshev filter far from convergence).
+// sym_a: A's blocks are symmetric and split with one scale per block
+// (fixed_max): A is streamed from its upper triangles only (half the reads).
 void ozaki_gemm(const OzakiDigits& A, const OzakiDigits& B, int64_t nbatch, const int* zmap, double* C, int64_t ldc,
-                int64_t strideC, cudaStream_t s, int levels = 6);
+                int64_t strideC, cudaStream_t s, int levels = 6, bool sym_a = false);
 // Whether the integer path applies to an output with M rows and K-length sums.
 bool ozaki_gemm_eligible(int64_t M, int64_t K);
 

@@ -260,6 +260,23 @@ __global__ void group_sum_kernel(const double* part, int64_t per_group, double* 
     }
 }
 
+// out[s] = max_i G_s(i, i): for a PSD G every |G(i, j)| <= sqrt(G_ii G_jj) is
+// bounded by it, so it scales all columns of the slice alike (symmetric split).
+__global__ void diag_max_kernel(const double* __restrict__ G, int64_t r, double* __restrict__ out) {
+    const double* g = G + (int64_t)blockIdx.x * r * r;
+    double m = 0.0;
+    for (int64_t i = threadIdx.x; i < r; i += blockDim.x) m = fmax(m, fabs(g[i + i * r]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    __shared__ double red[32];
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = fmax(m, red[w]);
+        out[blockIdx.x] = fmax(m, red[0]);
+    }
+}
+
 // th(c0 + j, s) = P(j, s), j < bc, for the slices of the launch (zmap).
 __global__ void copy_theta_kernel(double* __restrict__ th, const double* __restrict__ P, int64_t b,
                                   int64_t bc, int64_t c0, const int* __restrict__ zmap) {
@@ -426,9 +443,9 @@ void rayleigh_ritz(Work& w, const double* G, int64_t sG, double* Xn, int64_t c0,
     if (Gd && Xd && bc <= 64) {
         Xd->split(Xn + c0 * r, r, per, r, bc, r, zx, s, zm, zm ? batch : 0);
         if (zm) {
-            ozaki_gemm(*Gd, *Xd, batch, zm, w.Z.d() + c0 * r, r, per, s);
+            ozaki_gemm(*Gd, *Xd, batch, zm, w.Z.d() + c0 * r, r, per, s, 6, true);
         } else {
-            ozaki_gemm(*Gd, *Xd, batch, nullptr, w.Z.d() + c0 * r, r, per, s);
+            ozaki_gemm(*Gd, *Xd, batch, nullptr, w.Z.d() + c0 * r, r, per, s, 6, true);
         }
     } else {
         gg(G, r, sG, false, Xn + c0 * r, r, per, w.Z.d() + c0 * r, r, per, r, bc, r, batch, 1.0, 0.0, s, zm,
@@ -516,7 +533,16 @@ void subspace_eig_top(const double* G, int64_t r, int64_t batch, int64_t k, doub
     // final accuracy do not depend on the emulated filter.
     const bool oz_filter = vectors_for_reconstruction && batch >= 8 && ozaki_gemm_eligible(r, r);
     OzakiDigits Gd, Yd;
-    if (oz_filter) Gd.split(G, r, r * r, r, r, r, batch, s);
+    DeviceBuffer gmax;
+    if (oz_filter) {
+        // one scale per slice Gram (bounded by its largest diagonal entry): the
+        // filter and Rayleigh-Ritz products then read G from its upper triangle
+        gmax = DeviceBuffer(sizeof(double) * batch);
+        diag_max_kernel<<<(unsigned)batch, 256, 0, s>>>(G, r, gmax.d());
+        count_launch();
+        check_launch("diag_max");
+        Gd.split(G, r, r * r, r, r, r, batch, s, nullptr, 0, 0, 0, nullptr, 6, 0, 0, gmax.d());
+    }
     PPC_CUDA_CHECK(cudaMemsetAsync(w.fail.d(), 0, 2 * sizeof(int), s));
     randn_kernel<<<grid1(per * batch), 256, 0, s>>>(w.Y.d(), per * batch, 0x5eed5eedULL + (uint64_t)r * 131 + b);
     count_launch();
@@ -734,11 +760,11 @@ void subspace_eig_top(const double* G, int64_t r, int64_t batch, int64_t k, doub
                         const int* zhi = w.zmap.as<int>() + (int64_t)(2 * dmax + j) * batch;
                         const int* zl3 = w.zmap.as<int>() + (int64_t)(3 * dmax + j) * batch;
                         if (bf <= 64 && nlo[j] + nl3[j] > 0) {
-                            if (nl3[j] > 0) ozaki_gemm(Gd, Yd, nl3[j], zl3, w.Z.d() + cf * r, r, per, s, 3);
-                            if (nlo[j] > 0) ozaki_gemm(Gd, Yd, nlo[j], zlo, w.Z.d() + cf * r, r, per, s, 4);
-                            if (nhi[j] > 0) ozaki_gemm(Gd, Yd, nhi[j], zhi, w.Z.d() + cf * r, r, per, s);
+                            if (nl3[j] > 0) ozaki_gemm(Gd, Yd, nl3[j], zl3, w.Z.d() + cf * r, r, per, s, 3, true);
+                            if (nlo[j] > 0) ozaki_gemm(Gd, Yd, nlo[j], zlo, w.Z.d() + cf * r, r, per, s, 4, true);
+                            if (nhi[j] > 0) ozaki_gemm(Gd, Yd, nhi[j], zhi, w.Z.d() + cf * r, r, per, s, 6, true);
                         } else {
-                            ozaki_gemm(Gd, Yd, na, zm, w.Z.d() + cf * r, r, per, s);
+                            ozaki_gemm(Gd, Yd, na, zm, w.Z.d() + cf * r, r, per, s, 6, true);
                         }
                     } else {
                         gg(G, r, r * r, false, Y + cf * r, r, per, w.Z.d() + cf * r, r, per, r, bf, r, na, 1.0, 0.0,
