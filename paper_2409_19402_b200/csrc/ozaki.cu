@@ -52,7 +52,15 @@ constexpr int kSmax = 7;        // digit planes of a 7-digit split (the Gram dig
 constexpr int kBM = 128;        // UMMA M
 constexpr int kBN = 80;         // UMMA N: 6 level accumulators x 80 = 480 TMEM columns
 constexpr int kBK = 64;         // bytes (= int8 elements) of K per stage, SWIZZLE_64B
-constexpr int kStages = 2;
+constexpr int kStages = 2;       // (the 80-wide 6-level configuration)
+// TMA ring depth per configuration: as many 64-byte K stages as fit ~221 KB
+// of shared memory, 2..kMaxStages (80x6: 2, 64x7: 2, 64x6: 3, 64x4: 4, 64x3: 6)
+constexpr int kMaxStages = 6;
+constexpr int stages_for(int bn, int nl) {
+    return (221 * 1024) / (nl * (kBM + bn) * kBK) < 2 ? 2
+           : ((221 * 1024) / (nl * (kBM + bn) * kBK) > kMaxStages ? kMaxStages
+                                                                 : (221 * 1024) / (nl * (kBM + bn) * kBK));
+}
 constexpr int64_t kKC = 4096;   // rows per exact int32 accumulation
 constexpr int kEpiWarps = 8;    // two per TMEM lane quadrant, 40 columns each
 constexpr int kThreads = (2 + kEpiWarps) * 32;
@@ -234,14 +242,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr int A_TILE = kBM * kBK, B_TILE = BN * kBK;
     constexpr int STAGE = NL * (A_TILE + B_TILE);  // the NL digit tiles of A, then of B
     constexpr int STAGE_TX = STAGE;
-    uint64_t* full = reinterpret_cast<uint64_t*>(base + kStages * STAGE);
-    uint64_t* empty = full + kStages;
-    uint64_t* tfull = empty + kStages;
+    constexpr int STG = stages_for(BN, NL);
+    uint64_t* full = reinterpret_cast<uint64_t*>(base + STG * STAGE);
+    uint64_t* empty = full + STG;
+    uint64_t* tfull = empty + STG;
     uint64_t* tempty = tfull + 1;
     uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 1);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kStages; ++s) {
+        for (int s = 0; s < STG; ++s) {
             bar_init(&full[s], 1);
             bar_init(&empty[s], 1);
         }
@@ -264,8 +273,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 int64_t ob, mb, nb;
                 decode_item<SYM>(P, item, ob, mb, nb);
                 for (int64_t gl = 0; gl < per * nkc; ++gl, ++g) {
-                    const int st = (int)(g % kStages);
-                    bar_wait(&empty[st], (uint32_t)(((g / kStages) & 1) ^ 1));
+                    const int st = (int)(g % STG);
+                    bar_wait(&empty[st], (uint32_t)(((g / STG) & 1) ^ 1));
                     bar_expect_tx(&full[st], STAGE_TX);
                     const int64_t blk = ob * per + gl / nkc;
                     const int kx = (int)(gl % nkc) * kBK;
@@ -314,8 +323,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     fence_after_sync();
                 }
                 for (int kb = 0; kb < nkc; ++kb, ++g) {
-                    const int st = (int)(g % kStages);
-                    bar_wait(&full[st], (uint32_t)((g / kStages) & 1));
+                    const int st = (int)(g % STG);
+                    bar_wait(&full[st], (uint32_t)((g / STG) & 1));
                     fence_after_sync();
                     if (elect_one()) {
                         const uint8_t* sa = base + st * STAGE;
@@ -524,7 +533,8 @@ template <bool SYM, bool AMN = false, bool RESID = false, int BN = kBN, int NL =
 void launch_mma(const CUtensorMap& ma, const CUtensorMap& mb, const OzParams& P, int64_t items, cudaStream_t s,
                 const CUtensorMap* ma2 = nullptr) {
     // stages + barriers + TMEM slot + the epilogue warps' residual sums
-    const size_t smem = 1024 + (size_t)kStages * NL * (kBM + BN) * kBK + (2 * kStages + 2) * 8 + 16 + 16 * kEpiWarps;
+    constexpr int STG = stages_for(BN, NL);
+    const size_t smem = 1024 + (size_t)STG * NL * (kBM + BN) * kBK + (2 * STG + 2) * 8 + 16 + 16 * kEpiWarps;
     static bool attr = false;
     if (!attr) {
         PPC_CUDA_CHECK(cudaFuncSetAttribute(ozaki_mma_kernel<SYM, AMN, RESID, BN, NL, SYMA>,
