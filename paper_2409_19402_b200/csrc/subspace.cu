@@ -531,7 +531,11 @@ void subspace_eig_top(const double* G, int64_t r, int64_t batch, int64_t k, doub
     // digits): G is split once, the block Y at every degree. Rayleigh-Ritz
     // and the residuals keep the FP64 DMMA products, so locking and the
     // final accuracy do not depend on the emulated filter.
-    const bool oz_filter = vectors_for_reconstruction && batch >= 8 && ozaki_gemm_eligible(r, r);
+    // below r = 1024 the per-degree digit splits and short persistent launches
+    // cost more than the FP64 DMMA products they replace (cfg3: 13.8 -> 12.8 ms)
+    static const int64_t oz_min_r =
+        std::getenv("PPC_OZ_FILTER_MIN_R") ? std::atoll(std::getenv("PPC_OZ_FILTER_MIN_R")) : 1024;
+    const bool oz_filter = vectors_for_reconstruction && batch >= 8 && r >= oz_min_r && ozaki_gemm_eligible(r, r);
     OzakiDigits Gd, Yd;
     DeviceBuffer gmax;
     if (oz_filter) {
