@@ -18,6 +18,18 @@ def tube(v):
     return np.asarray(v, dtype=float).reshape(1, 1, -1)
 
 
+@pytest.fixture(autouse=True)
+def _engine_on_torch_stream(engine):
+    """Raw C-ABI calls with device pointers are ordered on the engine's current
+    stream (loc = PPC_DEVICE is stream-ordered): run it on torch's stream so the
+    tensors torch just built are ready, as the Python mirror does per call."""
+    import ctypes as C
+    import torch
+    from paper_2409_19402_b200 import _lib
+    assert _lib.lib().ppc_set_stream(C.c_void_p(torch.cuda.current_stream().cuda_stream)) == 0
+    yield
+
+
 def counterexample():
     a = np.zeros((2, 2, 2))
     a[:, :, 0] = np.eye(2)
@@ -1126,3 +1138,29 @@ def test_direct_eigensolver(engine, kind, n, p):
     assert abs(np.trace(Q.T @ G @ Q) - w[:p].sum()) <= 1e-13 * w[:p].sum()
     big = np.argmax(np.abs(Q), axis=0)  # matrix_kernels.cpp:16-25
     assert (Q[big, np.arange(p)] >= 0).all()
+
+
+@pytest.mark.gpu
+def test_ozaki_filter_large_slices(engine):
+    """Slices of r >= 1024 run the Chebyshev filter and Rayleigh-Ritz G X on
+    the INT8 tensor cores (3/4/6 digit levels, upper-triangle streaming of the
+    slice Grams): with a shared basis every singular value, noise slices
+    included, matches the all-FP64 path to 1e-10 per value."""
+    import ctypes as C
+    from paper_2409_19402_b200 import _lib
+    L = _lib.lib()
+    n1, n2, n3, p, k = 1024, 1024, 256, 16, 8
+    a = synth.cp_tensor_device(n1, n2, n3, rank=12, noise=1e-3, seed=12)
+    t = engine.data_dependent_transform(a, p)
+    L.ppc_timing_enable(1)
+    s_on = engine.to_host(engine.tsvdq(a, t, k).s)
+    buf = C.create_string_buffer(1 << 16)
+    L.ppc_timing_report(buf, len(buf), 1)
+    L.ppc_timing_enable(0)
+    assert "ozaki_gemm" in buf.value.decode(), buf.value.decode()
+    try:
+        assert L.ppc_set_ozaki(0) == 0
+        s_off = engine.to_host(engine.tsvdq(a, t, k).s)
+    finally:
+        L.ppc_set_ozaki(1)
+    assert (np.abs(s_on - s_off) <= 1e-10 * s_off).all(), np.max(np.abs(s_on - s_off) / s_off)
