@@ -252,6 +252,18 @@ int ppc_gemm_strided(int64_t M, int64_t N, int64_t K, int64_t batch, double alph
  * T (rows x n3, leading dimension ldT): parts is nchunks x n3 x n3. */
 int ppc_gram_partials(const double* T, int64_t ldT, int64_t rows, int64_t n3, int64_t chunk,
                       int64_t nchunks, double* parts, int loc);
+/* As ppc_gram_partials on device memory, and when the INT8 path splits T into
+ * whole 4096-row blocks it keeps T's 7-digit split in the engine: *handle > 0
+ * names it (0: nothing kept). ppc_mode3_forward_digits then forms T Q from the
+ * kept digits on the INT8 tensor cores (the sharded forward transform), and
+ * ppc_digits_release frees them. Handles belong to the calling thread. */
+int ppc_gram_partials_keep(const double* T, int64_t ldT, int64_t rows, int64_t n3, int64_t chunk,
+                           int64_t nchunks, double* parts, int64_t* handle);
+/* out (rows x p, leading dimension rows, device) = T Q (Q: n3 x p, device) from
+ * the digits kept under handle; PPC_ARGUMENT when the handle is unknown or the
+ * shape does not qualify (the caller then uses ppc_mode3_product). */
+int ppc_mode3_forward_digits(int64_t handle, const double* Q, int64_t p, double* out);
+int ppc_digits_release(int64_t handle);
 /* parts[0] = fixed pairwise tree sum of nparts arrays of `elems` doubles. */
 int ppc_tree_reduce(double* parts, int64_t nparts, int64_t elems, int loc);
 /* Top-p eigenvectors Q (n x p, sign rule) and sigma = sqrt(lambda) (nullable)

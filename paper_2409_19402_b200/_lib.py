@@ -75,6 +75,9 @@ def lib() -> C.CDLL:
         "ppc_gram_partials": (C.c_int, [vp, i64, i64, i64, i64, i64, vp, C.c_int]),
         "ppc_tree_reduce": (C.c_int, [vp, i64, i64, C.c_int]),
         "ppc_sym_eig_top": (C.c_int, [vp, i64, i64, vp, vp, C.c_int]),
+        "ppc_gram_partials_keep": (C.c_int, [vp, i64, i64, i64, i64, i64, vp, C.POINTER(C.c_int64)]),
+        "ppc_mode3_forward_digits": (C.c_int, [i64, vp, i64, vp]),
+        "ppc_digits_release": (C.c_int, [i64]),
         "ppc_slice_residual_sums": (C.c_int, [vp, i64, i64, i64, i64, vp, vp, vp, pd, C.c_int]),
         "ppc_gram_trace": (C.c_int, [vp, i64, pd, C.c_int]),
         "ppc_recon_residual_block": (C.c_int, [vp, i64, i64, i64, i64, vp, vp, vp, i64, i64, vp, i64, i64, pd, C.c_int]),

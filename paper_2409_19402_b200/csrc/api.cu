@@ -5,6 +5,8 @@
 #include <algorithm>
 #include <cmath>
 #include <string>
+#include <memory>
+#include <map>
 
 #include "dmma_gemm.cuh"
 #include "internal.h"
@@ -446,6 +448,46 @@ int ppc_gram_partials(const double* T, int64_t ldT, int64_t rows, int64_t n3, in
         o.finish();
         if (loc == PPC_HOST) PPC_CUDA_CHECK(cudaStreamSynchronize(s));
     });
+}
+
+namespace {
+// Gram digits kept for the sharded forward transform, per thread.
+thread_local std::map<int64_t, std::unique_ptr<OzakiDigits>> t_digits;
+thread_local int64_t t_digits_next = 1;
+}  // namespace
+
+int ppc_gram_partials_keep(const double* T, int64_t ldT, int64_t rows, int64_t n3, int64_t chunk,
+                           int64_t nchunks, double* parts, int64_t* handle) {
+    return guarded([&] {
+        if (!handle || !T || !parts) fail(PPC_ARGUMENT, "null pointer");
+        *handle = 0;
+        if (rows < 1 || n3 < 1 || ldT < rows || chunk < 1 || nchunks < 1)
+            fail(PPC_SHAPE, "gram_partials: bad extents");
+        if (chunk % 16) fail(PPC_ARGUMENT, "gram_partials: chunk must be a multiple of 16");
+        cudaStream_t s = stream();
+        auto d = std::make_unique<OzakiDigits>();
+        gram_chunks(T, ldT, rows, n3, chunk, nchunks, parts, s, nullptr, d.get());
+        if (d->uniform && d->nd == 7) {
+            *handle = t_digits_next++;
+            t_digits[*handle] = std::move(d);
+        }
+    });
+}
+
+int ppc_mode3_forward_digits(int64_t handle, const double* Q, int64_t p, double* out) {
+    return guarded([&] {
+        auto it = t_digits.find(handle);
+        if (it == t_digits.end()) fail(PPC_ARGUMENT, "mode3_forward_digits: unknown handle");
+        if (!Q || !out) fail(PPC_ARGUMENT, "null pointer");
+        const OzakiDigits& d = *it->second;
+        const int64_t rows = d.rows;
+        if (!ozaki_mode3_forward(d, rows, Q, p, out, stream()))
+            fail(PPC_ARGUMENT, "mode3_forward_digits: shape not eligible");
+    });
+}
+
+int ppc_digits_release(int64_t handle) {
+    return guarded([&] { t_digits.erase(handle); });
 }
 
 int ppc_tree_reduce(double* parts, int64_t nparts, int64_t elems, int loc) {

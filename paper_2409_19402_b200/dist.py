@@ -76,9 +76,27 @@ class DeviceBackend:
         return c.value, ch.value
 
     def gram_partials(self, A_blk, rows, n3, chunk, nchunks):
+        """Partial Grams of the local chunks; the engine keeps the block's
+        7-digit split (when the INT8 path ran on whole 4096-row blocks) for
+        mode3_fwd_kept."""
         parts = torch.empty(nchunks * n3 * n3, dtype=torch.float64, device=self.device)
-        _check(self.L.ppc_gram_partials(_p(A_blk), rows, rows, n3, chunk, nchunks, _p(parts), 1))
+        h = C.c_int64(0)
+        _check(self.L.ppc_gram_partials_keep(_p(A_blk), rows, rows, n3, chunk, nchunks, _p(parts), C.byref(h)))
+        self._kept = h.value
         return parts.view(nchunks, n3 * n3)
+
+    def mode3_fwd_kept(self, A_blk, n1, nj, n3, Q, p):
+        """A_blk x3 Q^T from the digits kept by gram_partials (INT8 tensor
+        cores, as the 1-GPU compress); the FP64 DMMA product otherwise."""
+        h, self._kept = getattr(self, "_kept", 0), 0
+        if h:
+            try:
+                out = _fempty((n1, nj, p), self.device)
+                if self.L.ppc_mode3_forward_digits(h, _p(Q), p, _p(out)) == 0:
+                    return out
+            finally:
+                _check(self.L.ppc_digits_release(h))
+        return self.mode3_fwd(A_blk, n1, nj, n3, Q, p)
 
     def tree_reduce(self, parts):
         parts = parts.contiguous()
@@ -210,8 +228,8 @@ def sharded_compress(A_blk, plan: ShardPlan, k: int, backend, group=None):
     Gm = _tree_finish(roots)
     # 3. replicated eigensolve
     Q, _ = backend.sym_eig_top(Gm, n3, p)
-    # 4. local forward transform
-    Ah = backend.mode3_fwd(A_blk, n1, nj, n3, Q, p)  # (n1, nj, p) Fortran
+    # 4. local forward transform (from the Gram's kept digits when it can)
+    Ah = backend.mode3_fwd_kept(A_blk, n1, nj, n3, Q, p)  # (n1, nj, p) Fortran
     # 5. reshard pixel -> slice: chunk for rank s = my block of its slices
     ps = plan.slices_per_rank
     send = Ah.permute(2, 1, 0).contiguous()  # (p, nj, n1) C-order == Fortran (n1, nj, p)

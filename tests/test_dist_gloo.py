@@ -70,6 +70,9 @@ class NumpyBackend:
         Qn = Q.permute(1, 0).contiguous().numpy().T
         return _ft((T @ Qn).reshape(n1, nj, p, order="F"))
 
+    def mode3_fwd_kept(self, A_blk, n1, nj, n3, Q, p):
+        return self.mode3_fwd(A_blk, n1, nj, n3, Q, p)
+
     def svd_slices(self, S_loc, n1, n2, ps, k):
         S = S_loc.permute(2, 1, 0).contiguous().numpy().transpose(2, 1, 0)
         U, s, V = np.zeros((n1, k, ps)), np.zeros((k, ps)), np.zeros((n2, k, ps))

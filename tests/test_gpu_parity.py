@@ -1164,3 +1164,32 @@ def test_ozaki_filter_large_slices(engine):
     finally:
         L.ppc_set_ozaki(1)
     assert (np.abs(s_on - s_off) <= 1e-10 * s_off).all(), np.max(np.abs(s_on - s_off) / s_off)
+
+
+@pytest.mark.gpu
+def test_dist_single_rank_kept_digits_matches_fused(engine):
+    """dist.py's per-rank path at a size where the Gram runs on the INT8 path
+    over whole 4096-row blocks: the engine keeps the 7-digit split
+    (ppc_gram_partials_keep) and the shard's forward transform reuses it
+    (ppc_mode3_forward_digits), as the fused ppc_tsvdq_compress does."""
+    import torch
+    from paper_2409_19402_b200 import dist as pdist
+    n1, n2, n3, p, k = 512, 512, 512, 64, 8
+    a = synth.cp_tensor_device(n1, n2, n3, rank=30, noise=1e-3, seed=13)
+    f, re = engine.compress_tsvdq(a, p, k)
+    import ctypes as C
+    from paper_2409_19402_b200 import _lib
+    L = _lib.lib()
+    be = pdist.DeviceBackend("cuda:0")
+    plan = pdist.make_plan(n1, n2, n3, p, 1, 0, be)
+    L.ppc_timing_enable(1)
+    Q, U, S, V, re2 = pdist.sharded_compress(a, plan, k, be)
+    torch.cuda.synchronize()
+    buf = C.create_string_buffer(1 << 16)
+    L.ppc_timing_report(buf, len(buf), 1)
+    L.ppc_timing_enable(0)
+    assert "ozaki_fwd" in buf.value.decode(), buf.value.decode()  # the kept digits were used
+    assert be._kept == 0  # and released
+    assert np.array_equal(engine.to_host(Q), f.transform.q)  # same digits, same Gram tree
+    np.testing.assert_allclose(engine.to_host(S), engine.to_host(f.s), rtol=1e-12)
+    assert abs(re2 - re) <= 1e-12 * re
