@@ -94,12 +94,20 @@ __global__ void __launch_bounds__(256) ozaki_split_kernel(const double* __restri
         len = std::max<int64_t>(0, end - r0);
     }
     const double* col = X + (stride ? b * stride : 0) + j * ldx + r0;
+    // all 16 loads of a thread in flight before any use (the kernel is
+    // DRAM-latency bound); same per-thread summation order as a strided loop
     double mx = 0.0, ss = 0.0;
-    for (int64_t i = threadIdx.x; i < len; i += blockDim.x) {
-        const double v = col[i];
-        stage[i] = v;
-        mx = fmax(mx, fabs(v));
-        ss = fma(v, v, ss);
+    double v[kKC / 256];
+#pragma unroll
+    for (int q = 0; q < kKC / 256; ++q) {
+        const int64_t i = threadIdx.x + 256 * q;
+        v[q] = i < len ? __ldcs(col + i) : 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < kKC / 256; ++q) {
+        stage[threadIdx.x + 256 * q] = v[q];
+        mx = fmax(mx, fabs(v[q]));
+        ss = fma(v[q], v[q], ss);
     }
     // block max and (fixed-order) sum of squares: the Gram diagonal in FP64
     __shared__ double red[8], red2[8];
