@@ -648,14 +648,18 @@ int ppc_tsvdq_compress(const double* A, int64_t n1, int64_t n2, int64_t n3, int6
             const bool keep = g.chunk % 4096 == 0;
             {
                 StageTimer tm("gram_syrk", s, (double)N * n3 * n3, 8.0 * N * n3);
-                for (int64_t c0 = 0; c0 < g.chunks; c0 += per) {
+                // groups of `per` chunks; the last chunk travels alone, so the
+                // Gram work left after the final byte lands is one chunk's
+                for (int64_t c0 = 0, take = 0; c0 < g.chunks; c0 += take) {
+                    take = std::min<int64_t>(per, g.chunks - c0);
+                    if (take > 1 && c0 + take == g.chunks) --take;
                     const int64_t r0 = c0 * g.chunk;
                     if (r0 >= N) {  // plan chunks beyond N: zero partials
                         PPC_CUDA_CHECK(cudaMemsetAsync(parts.d() + c0 * n3 * n3, 0,
                                                        sizeof(double) * (g.chunks - c0) * n3 * n3, s));
                         break;
                     }
-                    const int64_t nr = std::min<int64_t>(per * g.chunk, N - r0);
+                    const int64_t nr = std::min<int64_t>(take * g.chunk, N - r0);
                     PPC_CUDA_CHECK(cudaMemcpy2DAsync(abuf.d() + r0, sizeof(double) * N, A + r0, sizeof(double) * N,
                                                      sizeof(double) * nr, n3, cudaMemcpyHostToDevice, cs));
                     cudaEvent_t ev;
@@ -663,7 +667,7 @@ int ppc_tsvdq_compress(const double* A, int64_t n1, int64_t n2, int64_t n3, int6
                     PPC_CUDA_CHECK(cudaEventRecord(ev, cs));
                     PPC_CUDA_CHECK(cudaStreamWaitEvent(s, ev, 0));
                     PPC_CUDA_CHECK(cudaEventDestroy(ev));
-                    checked &= gram_chunks(abuf.d() + r0, N, nr, n3, g.chunk, std::min(per, g.chunks - c0),
+                    checked &= gram_chunks(abuf.d() + r0, N, nr, n3, g.chunk, take,
                                            parts.d() + c0 * n3 * n3, s, nf.d(), keep ? &tdig : nullptr,
                                            c0 * blk_per_chunk, g.chunks * blk_per_chunk);
                 }
