@@ -122,6 +122,11 @@ bool make_map_x(CUtensorMap* map, const double* X, int64_t M, int64_t N, int64_t
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+int64_t short_k_cfg() {
+    static const int64_t v = std::getenv("PPC_WS_SHORT_K") ? std::atoll(std::getenv("PPC_WS_SHORT_K")) : 256;
+    return v;
+}
+
 bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 }  // namespace
@@ -142,6 +147,12 @@ bool gemm_ws(const GemmDesc& d, int epi, const double* X, int64_t ldx, int64_t s
     } else if (d.N <= 32) {
         cfg = 2;
     } else if (d.N <= 64) {
+        cfg = 1;
+    } else if (epi == EPI_STORE && d.K <= short_k_cfg()) {
+        // short-K stores: the 128 x 128 consumers (64 accumulators a thread;
+        // 168 registers with 9 warps, one SMSP holding 3 -> spills) ran at
+        // 55% of the DMMA pipe; the 128 x 64 tile keeps everything in
+        // registers (cfg4 inverse transform 1.71 -> 1.47 ms)
         cfg = 1;
     } else {
         cfg = 0;
