@@ -221,8 +221,15 @@ class StarQ:
         return self.flops / sec / 1e12
 
     def dominant(self, stages):
-        # the facewise product: on the INT8 tensor cores (Ozaki) when eligible
-        return ("ozaki_gemm", "int8") if "ozaki_gemm" in stages else ("facewise", "tensor")
+        # the single longest kernel launch of the step: the inverse transform
+        # (FP64 DMMA, K = p = 64), the facewise product (INT8 Ozaki MMA when
+        # eligible) or a forward transform
+        cands = [("mode3_inv", "tensor"), ("ozaki_gemm", "int8") if "ozaki_gemm" in stages else ("facewise", "tensor"),
+                 ("mode3_fwd", "tensor")]
+        cands = [c for c in cands if c[0] in stages]
+        if not cands:
+            return ("facewise", "tensor")
+        return max(cands, key=lambda c: stages[c[0]]["ms"] / max(1, stages[c[0]]["n"]))
 
     def e2e_setup(self):
         torch = self.torch
