@@ -482,11 +482,16 @@ static double filter_lowp() {
     return v;
 }
 
-// Chebyshev degree cap per outer iteration (runtime-tunable for experiments)
-static double max_degree(bool basis) {
-    static const double v = std::getenv("PPC_CHEB_MAX") ? std::atof(std::getenv("PPC_CHEB_MAX")) : 10.0;
+// Chebyshev degree cap per outer iteration (runtime-tunable for experiments).
+// 20 with the INT8 reduced-level filter, where a degree costs less than the
+// CholQR3 + Rayleigh-Ritz of an extra outer iteration (cfg5 slice SVD 56 ->
+// 50 ms); 10 with the FP64 filter of small slices (cfg3: 20 is 12% slower).
+static double max_degree(bool basis, bool int8_filter) {
+    static const char* e = std::getenv("PPC_CHEB_MAX");
+    static const double v = e ? std::atof(e) : 0.0;
     static const double vq = std::getenv("PPC_CHEB_MAX_Q") ? std::atof(std::getenv("PPC_CHEB_MAX_Q")) : 10.0;
-    return basis ? vq : v;
+    if (basis) return vq;
+    return v > 0.0 ? v : (int8_filter ? 20.0 : 10.0);
 }
 
 // tail2[z] = ||A_z - U_z diag(S_z) V_z^T||_F^2 (= the discarded energy sum_{j>=k} s_j^2
@@ -674,7 +679,7 @@ void subspace_eig_top(const double* G, int64_t r, int64_t batch, int64_t k, doub
             // block's bottom (x = 1, T_d(1) = 1) kept <= 1e10;
             // (b) the spread inside the wanted active set (precision of the
             // smaller wanted components) kept <= 1e6.
-            double d = max_degree(w.basis);
+            double d = max_degree(w.basis, oz_filter);
             if (xt > 1.0) d = std::min(d, std::acosh(1e10) / std::acosh(xt));
             const double spread = std::acosh(xt) - std::acosh(xk);
             if (spread > 0) d = std::min(d, std::log(1e6) / spread);
