@@ -563,6 +563,11 @@ void subspace_eig_top(const double* G, int64_t r, int64_t batch, int64_t k, doub
     std::vector<double> th(b * batch), res(b * batch), coef(3 * batch), wm(b * batch),
         thp(b * batch, 0.0);
     std::vector<int> nlock(batch, 0);
+    // reduced-level filter guard: a slice whose smallest unlocked residual
+    // stopped halving between iterations while filtered at reduced precision
+    // is held at the next precision level from then on (cap[sl])
+    std::vector<double> prev_rmin(batch, 1e300);
+    std::vector<char> cap(batch, 2);
     const int max_iter = 100;
     for (int it = 0; it < max_iter; ++it) {
         PPC_CUDA_CHECK(cudaMemcpyAsync(th.data(), w.th.d(), sizeof(double) * b * batch, cudaMemcpyDeviceToHost, s));
@@ -666,7 +671,10 @@ void subspace_eig_top(const double* G, int64_t r, int64_t batch, int64_t k, doub
             if (vectors_for_reconstruction && filter_lowp() > 0.0) {
                 double rmin = 1e300;
                 for (int64_t j = L; j < k; ++j) rmin = std::min(rmin, rr[j]);
-                lowp[sl] = rmin > filter_lowp() * scale ? (rmin > 1e3 * filter_lowp() * scale ? 2 : 1) : 0;
+                char lv = rmin > filter_lowp() * scale ? (rmin > 1e3 * filter_lowp() * scale ? 2 : 1) : 0;
+                if (lv > 0 && lv == cap[sl] && it >= 2 && rmin > 0.5 * prev_rmin[sl]) cap[sl] = (char)(lv - 1);
+                lowp[sl] = std::min(lv, cap[sl]);
+                prev_rmin[sl] = rmin;
             }
             // Chebyshev interval [0, ub]: damp everything below the smallest Ritz value
             const double ub = std::max(t[b - 1], 0.0);
