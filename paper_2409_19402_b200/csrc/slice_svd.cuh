@@ -25,10 +25,17 @@ void subspace_eig_top(const double* G, int64_t n, int64_t batch, int64_t p, doub
                       double* lambda, cudaStream_t s, bool vectors_for_reconstruction);
 // Direct top-p eigensolver for one symmetric n x n matrix (tridiag_eig.cu):
 // Householder tridiagonalization, bisection, inverse iteration, back-transform.
-bool tridiag_eig_eligible(int64_t n, int64_t p);
+bool tridiag_eig_eligible(int64_t n, int64_t p, int64_t batch = 1);
+// eligible and expected faster than subspace iteration (one cluster per
+// matrix, or the whole batch in one wave)
+bool tridiag_eig_preferred(int64_t n, int64_t p, int64_t batch);
 void tridiag_eig_top(const double* G, int64_t n, int64_t p, double* Q, double* lambda, cudaStream_t s);
-// Z (r x k, column-major) <- orthonormal columns, shifted CholQR3 in column order (k <= 160).
-void cholqr_inplace(double* Z, int64_t r, int64_t k, cudaStream_t s);
+// `batch` matrices G + b * strideG: Q (n, p, batch), lambda (p, batch), descending.
+void tridiag_eig_top_batched(const double* G, int64_t n, int64_t strideG, int64_t batch, int64_t p, double* Q,
+                             double* lambda, cudaStream_t s);
+// Z (r x k per block, column-major, `batch` blocks of r*k) <- orthonormal columns,
+// shifted CholQR3 in column order (k <= 160).
+void cholqr_inplace(double* Z, int64_t r, int64_t k, cudaStream_t s, int64_t batch = 1);
 void slice_tail_energy(const double* A, int64_t m, int64_t n, int64_t stride, int64_t batch,
                        int64_t k, const double* U, const double* S, const double* V, double* tail2,
                        cudaStream_t s);

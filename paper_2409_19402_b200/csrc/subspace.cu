@@ -405,9 +405,10 @@ void cholqr3(Work& w, double* Y, double* Xout, int64_t c0, cudaStream_t s, const
 // Shifted CholQR3 of one r x k panel in place (the direct eigensolver's
 // inverse-iteration vectors): column order is kept, so Z R^{-1} is a
 // Gram-Schmidt of Z in eigenvalue order.
-void cholqr_inplace(double* Z, int64_t r, int64_t k, cudaStream_t s) {
+void cholqr_inplace(double* Z, int64_t r, int64_t k, cudaStream_t s, int64_t batch) {
     if (k > 160) fail(PPC_ARGUMENT, "cholqr_inplace: too many columns");
-    DeviceBuffer S(sizeof(double) * k * k), Ri(sizeof(double) * k * k), T(sizeof(double) * r * k);
+    DeviceBuffer S(sizeof(double) * k * k * batch), Ri(sizeof(double) * k * k * batch),
+        T(sizeof(double) * r * k * batch);
     const size_t smem = (size_t)k * k * sizeof(double);
     if (smem > 48 * 1024)
         PPC_CUDA_CHECK(cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -415,15 +416,16 @@ void cholqr_inplace(double* Z, int64_t r, int64_t k, cudaStream_t s) {
     double* src = Z;
     double* dst = T.d();
     for (int pass = 0; pass < 3; ++pass) {
-        gg(src, r, r * k, true, src, r, r * k, S.d(), k, k * k, k, k, r, 1, 1.0, 0.0, s);  // S = Z^T Z
-        chol_inv_kernel<<<1, k > 16 ? 1024 : 256, smem, s>>>(S.d(), Ri.d(), k, pass == 0 ? 1 : 0, nullptr,
-                                                             nullptr);
+        gg(src, r, r * k, true, src, r, r * k, S.d(), k, k * k, k, k, r, batch, 1.0, 0.0, s);  // S = Z^T Z
+        chol_inv_kernel<<<(unsigned)batch, k > 16 ? 1024 : 256, smem, s>>>(S.d(), Ri.d(), k, pass == 0 ? 1 : 0,
+                                                                          nullptr, nullptr);
         count_launch();
         check_launch("chol_inv");
-        gg(src, r, r * k, false, Ri.d(), k, k * k, dst, r, r * k, r, k, k, 1, 1.0, 0.0, s);
+        gg(src, r, r * k, false, Ri.d(), k, k * k, dst, r, r * k, r, k, k, batch, 1.0, 0.0, s);
         std::swap(src, dst);
     }
-    if (src != Z) PPC_CUDA_CHECK(cudaMemcpyAsync(Z, src, sizeof(double) * r * k, cudaMemcpyDeviceToDevice, s));
+    if (src != Z)
+        PPC_CUDA_CHECK(cudaMemcpyAsync(Z, src, sizeof(double) * r * k * batch, cudaMemcpyDeviceToDevice, s));
 }
 
 namespace {
@@ -891,7 +893,13 @@ void subspace_svd(const double* A, int64_t m, int64_t n, int64_t stride, int64_t
         }
     }
     DeviceBuffer Xk(sizeof(double) * r * k * batch), lam(sizeof(double) * k * batch);
-    subspace_eig_top(G.d(), r, batch, k, Xk.d(), lam.d(), s, true);
+    // slice Grams up to 1024: the batched direct solver (one cooperative
+    // launch tridiagonalizes every Gram); larger ones: subspace iteration
+    static const bool direct = !(std::getenv("PPC_SLICE_TRIDIAG") && std::atoi(std::getenv("PPC_SLICE_TRIDIAG")) == 0);
+    if (direct && tridiag_eig_preferred(r, k, batch))
+        tridiag_eig_top_batched(G.d(), r, r * r, batch, k, Xk.d(), lam.d(), s);
+    else
+        subspace_eig_top(G.d(), r, batch, k, Xk.d(), lam.d(), s, true);
     // polish: W = A Xk (tall: m x k) or A^T Xk (wide: n x k)
     StageTimer tp("ss.polish", s);
     const int64_t o = tall ? m : n;

@@ -84,10 +84,14 @@ struct TrdParams {
     double* pg;      // 2 x n  exchanged p = tau * A v, by step parity (a fast CTA
                      //        writes step j+1 while a slow one still reads step j)
     double* colpub;  // 2 x n  published next pivot column, by step parity
-    unsigned* bar;   // arrival counter
+    unsigned* bar;   // arrival counter (one per matrix, 128 bytes apart)
+    // batch: matrix b is G + b * strideG; its nblk CTAs are blocks
+    // [b * nblk, (b+1) * nblk) and every output above is per matrix
+    int64_t strideG;
+    int blk;         // the CTA's rank within its matrix (set in the kernel)
 };
 
-constexpr int kMaxCpc = 12;  // owned columns per CTA (n <= 1536 on 148 SMs)
+constexpr size_t kTrdSmemMax = 200 * 1024;
 
 // Reflector of step jj from column jj (xs, rows jj+1..n-1), LAPACK dlarfg:
 // computed redundantly by every CTA (same bits everywhere). Writes vn and
@@ -110,14 +114,14 @@ __device__ __forceinline__ double make_reflector(const TrdParams& P, int jj, con
         scal = 1.0 / (alpha - beta);
     }
     for (int i = tid; i < n; i += nt) vn[i] = i <= jj ? 0.0 : (i == jj + 1 ? 1.0 : xs[i] * scal);
-    if (blockIdx.x == 0 && tid == 0) {
+    if (P.blk == 0 && tid == 0) {
         P.d[jj] = xs[jj];
         P.e[jj] = beta;
         P.tau[jj] = tau;
     }
     // V(:, jj): CTA b stores rows [b*ch, (b+1)*ch)
     const int ch = (n + P.nblk - 1) / P.nblk;
-    const int r0 = blockIdx.x * ch;
+    const int r0 = P.blk * ch;
     for (int i = r0 + tid; i < min(n, r0 + ch); i += nt)
         P.V[(size_t)jj * n + i] = i <= jj ? 0.0 : (i == jj + 1 ? 1.0 : xs[i] * scal);
     return tau;
@@ -129,12 +133,14 @@ __device__ __forceinline__ double make_reflector(const TrdParams& P, int jj, con
 // only). One warp per owned column, two rows per lane per iteration from an
 // even start (v, w and v' are zero in rows <= j, so the extra row is left
 // unchanged); the owner of column j+2 publishes it as it goes.
+// The products go to pgo[c] (pgo[slot] with by_slot) and the published
+// column to cp.
 __device__ __forceinline__ void update_pass(const TrdParams& P, double* A, int j, const double* vs,
-                                            const double* ws, const double* vn, double taun) {
-    const int n = P.n, nblk = P.nblk, cpc = P.cpc, blk = blockIdx.x;
+                                            const double* ws, const double* vn, double taun, double* pgo,
+                                            double* cp, bool by_slot) {
+    const int n = P.n, nblk = P.nblk, cpc = P.cpc, blk = P.blk;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     const int i0 = (j + 1) & ~1;
-    double* cp = P.colpub + (size_t)((j + 1) & 1) * n;
     for (int t = warp; t < cpc; t += nw) {
         const int c = blk + t * nblk;
         if (c <= j || c >= n) continue;  // warp-uniform
@@ -160,15 +166,30 @@ __device__ __forceinline__ void update_pass(const TrdParams& P, double* A, int j
         if (vn) {
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-            if (lane == 0 && c > j + 1) P.pg[(size_t)((j + 1) & 1) * n + c] = taun * acc;
+            if (lane == 0 && c > j + 1) pgo[by_slot ? t : c] = taun * acc;
         }
     }
 }
 
 // Column c is owned by CTA c % nblk, slot c / nblk.
-__global__ void __launch_bounds__(kTrdThreads, 1) sytrd_kernel(TrdParams P) {
+__global__ void __launch_bounds__(kTrdThreads, 1) sytrd_kernel(TrdParams P0) {
     extern __shared__ __align__(16) double sm[];
-    const int n = P.n, nblk = P.nblk, cpc = P.cpc, blk = blockIdx.x;
+    // this CTA's matrix and rank, and the matrix's slices of every array
+    TrdParams P = P0;
+    const int mat = blockIdx.x / P0.nblk;
+    P.blk = blockIdx.x % P0.nblk;
+    {
+        const size_t n0 = (size_t)P0.n;
+        P.G += (size_t)mat * P0.strideG;
+        P.V += (size_t)mat * n0 * n0;
+        P.tau += (size_t)mat * n0;
+        P.d += (size_t)mat * n0;
+        P.e += (size_t)mat * n0;
+        P.pg += (size_t)mat * 2 * n0;
+        P.colpub += (size_t)mat * 2 * n0;
+        P.bar += (size_t)mat * 32;
+    }
+    const int n = P.n, nblk = P.nblk, cpc = P.cpc, blk = P.blk;
     double* A = sm;                    // cpc x n (slot t = column blk + t*nblk)
     double* vs = A + (size_t)cpc * n;  // reflector of step j
     double* vn = vs + n;               // reflector of step j+1
@@ -193,7 +214,7 @@ __global__ void __launch_bounds__(kTrdThreads, 1) sytrd_kernel(TrdParams P) {
     double tau = make_reflector(P, 0, xs, vn, red);
     for (int i = tid; i < n; i += nt) vs[i] = 0.0;
     __syncthreads();
-    update_pass(P, A, -1, vs, ws, vn, tau);
+    update_pass(P, A, -1, vs, ws, vn, tau, P.pg, P.colpub, false);
 
     for (int j = 0; j <= n - 3; ++j) {
         {
@@ -225,10 +246,11 @@ __global__ void __launch_bounds__(kTrdThreads, 1) sytrd_kernel(TrdParams P) {
         if (j + 1 <= n - 3) {
             const double taun = make_reflector(P, j + 1, xs, vn, red);
             __syncthreads();
-            update_pass(P, A, j, vs, ws, vn, taun);
+            update_pass(P, A, j, vs, ws, vn, taun, P.pg + (size_t)((j + 1) & 1) * n,
+                        P.colpub + (size_t)((j + 1) & 1) * n, false);
             tau = taun;
         } else {
-            update_pass(P, A, j, vs, ws, nullptr, 0.0);
+            update_pass(P, A, j, vs, ws, nullptr, 0.0, nullptr, P.colpub + (size_t)((j + 1) & 1) * n, false);
         }
         __syncthreads();
     }
@@ -266,10 +288,17 @@ __device__ __forceinline__ int sturm_count(const double* d, const double* e2, in
 // multisection, every thread one Sturm count per round (~7 bits a round).
 constexpr int kBisThreads = 256;
 __global__ void __launch_bounds__(kBisThreads) bisect_top_kernel(const double* __restrict__ dg,
-                                                                 const double* __restrict__ eg, int n,
+                                                                 const double* __restrict__ eg, int n, int k,
                                                                  double* __restrict__ lam,
                                                                  double* __restrict__ bounds) {
     extern __shared__ __align__(16) double sh[];
+    {  // matrix blockIdx.x / k of the batch
+        const int mat = blockIdx.x / k;
+        dg += (size_t)mat * n;
+        eg += (size_t)mat * n;
+        lam += (size_t)mat * k;
+        bounds += (size_t)mat * 2;
+    }
     double* d = sh;
     double* e2 = sh + n;
     __shared__ double s_gl[kBisThreads / 32], s_gu[kBisThreads / 32], s_em[kBisThreads / 32];
@@ -311,7 +340,7 @@ __global__ void __launch_bounds__(kBisThreads) bisect_top_kernel(const double* _
     gl -= 2.0 * kEps * tnorm * n + 2.0 * pivmin;
     gu += 2.0 * kEps * tnorm * n + 2.0 * pivmin;
     const double atol = kEps * tnorm;
-    const int m = blockIdx.x;
+    const int m = blockIdx.x % k;  // eigenvalue of matrix blockIdx.x / k
     const int want = n - m;  // invariant: count(hi) >= want > count(lo)
     double lo = gl, hi = gu;
     for (int it = 0; it < 40; ++it) {
@@ -353,8 +382,16 @@ __device__ __forceinline__ double hash_unit(uint64_t z) {
 // between; the warp loads T, draws the start and normalizes. Pivots below
 // eps*||T|| are raised to it (dlagts job = -1).
 __global__ void inverse_iteration_kernel(const double* __restrict__ dg, const double* __restrict__ eg,
-                                         int n, const double* __restrict__ lam,
+                                         int n, int k, const double* __restrict__ lam,
                                          const double* __restrict__ bounds, double* __restrict__ Z) {
+    {  // matrix blockIdx.x / k of the batch
+        const int mat = blockIdx.x / k;
+        dg += (size_t)mat * n;
+        eg += (size_t)mat * n;
+        lam += (size_t)mat * k;
+        bounds += (size_t)mat * 2;
+        Z += (size_t)mat * n * k;
+    }
     extern __shared__ __align__(16) double sh[];
     double* d = sh;
     double* e = d + n;
@@ -365,7 +402,7 @@ __global__ void inverse_iteration_kernel(const double* __restrict__ dg, const do
     double* x = lm + n;
     unsigned char* pv = reinterpret_cast<unsigned char*>(x + n);
     __shared__ double s_sc;
-    const int m = blockIdx.x, lane = threadIdx.x;
+    const int m = blockIdx.x % k, lane = threadIdx.x;
     const double l = lam[m];
     const double pert = kEps * fmax(bounds[0], kSafeMin);
     for (int i = lane; i < n; i += 32) {
@@ -482,11 +519,17 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 
 // T of chunk c (rows/cols r = 0..cnt-1 <-> reflector jl + r): T(r,r) = tau,
 // T(0:r, r) = -tau_r T(0:r, 0:r) V(:, 0:r)^T v_r. One CTA per chunk.
-__global__ void wy_t_kernel(const double* __restrict__ V, const double* __restrict__ tau, int n,
+__global__ void wy_t_kernel(const double* __restrict__ V, const double* __restrict__ tau, int n, int nchunks,
                             double* __restrict__ Tout) {
     __shared__ double S[kBtChunk][kBtChunk];
     __shared__ double T[kBtChunk][kBtChunk];
-    const int c = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    {  // matrix blockIdx.x / nchunks of the batch
+        const size_t mat = blockIdx.x / nchunks;
+        V += mat * n * n;
+        tau += mat * n;
+        Tout += mat * nchunks * kBtChunk * kBtChunk;
+    }
+    const int c = blockIdx.x % nchunks, warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     const int jtop = n - 3;
     const int j1 = jtop - c * kBtChunk;
     const int cnt = min(kBtChunk, j1 + 1);
@@ -527,7 +570,15 @@ __global__ void __launch_bounds__(32 * kBtWarps) back_transform_kernel(const dou
                                                                        int k, double* __restrict__ Z) {
     extern __shared__ __align__(16) double sv[];  // 2 x (kBtChunk x n + kBtChunk^2)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
-    const int col = blockIdx.x * kBtWarps + warp;
+    const int per_mat = (k + kBtWarps - 1) / kBtWarps;  // CTAs per matrix of the batch
+    {
+        const size_t mat = blockIdx.x / per_mat;
+        const size_t nch = (size_t)(n - 3 + kBtChunk) / kBtChunk;
+        V += mat * n * n;
+        Tg += mat * nch * kBtChunk * kBtChunk;
+        Z += mat * n * k;
+    }
+    const int col = (blockIdx.x % per_mat) * kBtWarps + warp;
     const bool live = col < k;
     const size_t bufsz = (size_t)kBtChunk * n + kBtChunk * kBtChunk;
     double z[NS];
@@ -630,14 +681,14 @@ __global__ void __launch_bounds__(32 * kBtWarps) back_transform_kernel(const dou
 }
 
 template <int NS>
-void launch_back_transform(const double* V, const double* tau, int n, int k, double* Z, double* Tws,
+void launch_back_transform(const double* V, const double* tau, int n, int k, int batch, double* Z, double* Tws,
                            cudaStream_t s) {
     const int nchunks = (n - 3 + kBtChunk) / kBtChunk;
-    wy_t_kernel<<<(unsigned)nchunks, 128, 0, s>>>(V, tau, n, Tws);
+    wy_t_kernel<<<(unsigned)(nchunks * batch), 128, 0, s>>>(V, tau, n, nchunks, Tws);
     count_launch();
     check_launch("wy_t");
     const size_t smem = 2 * ((size_t)kBtChunk * n + kBtChunk * kBtChunk) * sizeof(double);
-    const unsigned grid = (unsigned)((k + kBtWarps - 1) / kBtWarps);
+    const unsigned grid = (unsigned)(((k + kBtWarps - 1) / kBtWarps) * batch);
     if (n == 32 * NS) {
         PPC_CUDA_CHECK(cudaFuncSetAttribute(back_transform_kernel<NS, true>,
                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -651,53 +702,93 @@ void launch_back_transform(const double* V, const double* tau, int n, int k, dou
 
 size_t trd_smem(int n, int cpc) { return ((size_t)cpc * n + 4 * (size_t)n) * sizeof(double); }
 
+// CTAs per matrix and owned columns per CTA: a wave of `per_wave` matrices
+// runs in one cooperative launch, one CTA per SM, every owned column in
+// shared memory (the update pass streams each column once per step: from
+// L2 it would be ~1000x the matrix per reduction).
+struct TrdPlan {
+    int nblk = 0, cpc = 0, per_wave = 0;
+};
+TrdPlan trd_plan(int64_t n, int64_t batch) {
+    TrdPlan t;
+    const int sms = ctx().sms;
+    int nmin = 1;  // fewest CTAs per matrix that fit
+    while (nmin <= sms && nmin <= n && trd_smem((int)n, (int)((n + nmin - 1) / nmin)) > kTrdSmemMax) ++nmin;
+    if (nmin > sms || nmin > n || batch < 1) return t;
+    t.per_wave = (int)std::min<int64_t>(batch, sms / nmin);
+    // waves of equal size, then the SMs spread over the wave's matrices
+    const int64_t waves = (batch + t.per_wave - 1) / t.per_wave;
+    t.per_wave = (int)((batch + waves - 1) / waves);
+    t.nblk = (int)std::min<int64_t>(sms / t.per_wave, n);
+    t.cpc = (int)((n + t.nblk - 1) / t.nblk);
+    return t;
+}
+
 }  // namespace
 
-bool tridiag_eig_eligible(int64_t n, int64_t p) {
-    if (n < 3 || n > 1536 || (n & 1) || p < 1 || p > 160 || p > n) return false;
+bool tridiag_eig_preferred(int64_t n, int64_t p, int64_t batch) {
+    if (!tridiag_eig_eligible(n, p, batch)) return false;
+    // ~3-5 us a reduction step whatever the size (a latency chain): worth it
+    // while the waves' steps stay within cfg3's 3 x 512
+    const TrdPlan t = trd_plan(n, batch);
+    const int64_t waves = (batch + t.per_wave - 1) / t.per_wave;
+    return waves * n <= 1600;
+}
+
+bool tridiag_eig_eligible(int64_t n, int64_t p, int64_t batch) {
+    if (n < 3 || n > 1536 || (n & 1) || p < 1 || p > 160 || p > n || batch < 1) return false;
     static const bool off = std::getenv("PPC_TRIDIAG_EIG") && std::atoi(std::getenv("PPC_TRIDIAG_EIG")) == 0;
     if (off) return false;
-    const int sms = ctx().sms;
-    const int nblk = (int)std::min<int64_t>(sms, n);
-    const int cpc = (int)((n + nblk - 1) / nblk);
-    return cpc <= kMaxCpc && trd_smem((int)n, cpc) <= 200 * 1024;
+    return trd_plan(n, batch).nblk >= 1;
 }
 
 void tridiag_eig_top(const double* G, int64_t n64, int64_t k64, double* Q, double* lambda, cudaStream_t s) {
-    const int n = (int)n64, k = (int)k64;
-    if (!tridiag_eig_eligible(n64, k64)) fail(PPC_ARGUMENT, "tridiag_eig_top: size out of range");
-    const int nblk = std::min(ctx().sms, n);
-    const int cpc = (n + nblk - 1) / nblk;
+    tridiag_eig_top_batched(G, n64, n64 * n64, 1, k64, Q, lambda, s);
+}
+
+void tridiag_eig_top_batched(const double* G, int64_t n64, int64_t strideG, int64_t batch64, int64_t k64, double* Q,
+                             double* lambda, cudaStream_t s) {
+    const int n = (int)n64, k = (int)k64, batch = (int)batch64;
+    if (!tridiag_eig_eligible(n64, k64, batch64)) fail(PPC_ARGUMENT, "tridiag_eig_top: size out of range");
+    const TrdPlan t = trd_plan(n64, batch64);
+    const int nblk = t.nblk, cpc = t.cpc;
     const size_t smem = trd_smem(n, cpc);
-    DeviceBuffer Vb(sizeof(double) * (size_t)n * n), tb(sizeof(double) * n), db(sizeof(double) * n),
-        eb(sizeof(double) * n), pgb(sizeof(double) * 2 * n),
-        cpb(sizeof(double) * 2 * n), barb(sizeof(unsigned) * 4), bnd(sizeof(double) * 2);
-    PPC_CUDA_CHECK(cudaMemsetAsync(barb.d(), 0, sizeof(unsigned) * 4, s));
+    const size_t B = (size_t)batch;
+    DeviceBuffer Vb(sizeof(double) * (size_t)n * n * B), tb(sizeof(double) * n * B), db(sizeof(double) * n * B),
+        eb(sizeof(double) * n * B), pgb(sizeof(double) * 2 * n * B), cpb(sizeof(double) * 2 * n * B),
+        barb(sizeof(unsigned) * 32 * B), bnd(sizeof(double) * 2 * B);
+    PPC_CUDA_CHECK(cudaMemsetAsync(barb.d(), 0, sizeof(unsigned) * 32 * B, s));
     {
         StageTimer tm("eig.tridiag", s);
-        TrdParams P;
-        P.G = G;
-        P.n = n;
-        P.nblk = nblk;
-        P.cpc = cpc;
-        P.V = Vb.d();
-        P.tau = tb.d();
-        P.d = db.d();
-        P.e = eb.d();
-        P.pg = pgb.d();
-        P.colpub = cpb.d();
-        P.bar = barb.as<unsigned>();
         PPC_CUDA_CHECK(cudaFuncSetAttribute(sytrd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        void* args[] = {&P};
-        PPC_CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)sytrd_kernel, dim3(nblk), dim3(kTrdThreads), args,
-                                                   smem, s));
-        count_launch();
-        check_launch("sytrd");
+        for (int b0 = 0; b0 < batch; b0 += t.per_wave) {
+            const size_t o = (size_t)b0;
+            TrdParams P;
+            P.G = G + o * strideG;
+            P.n = n;
+            P.nblk = nblk;
+            P.cpc = cpc;
+            P.V = Vb.d() + o * n * n;
+            P.tau = tb.d() + o * n;
+            P.d = db.d() + o * n;
+            P.e = eb.d() + o * n;
+            P.pg = pgb.d() + o * 2 * n;
+            P.colpub = cpb.d() + o * 2 * n;
+            P.bar = barb.as<unsigned>() + o * 32;
+            P.strideG = strideG;
+            P.blk = 0;
+            void* args[] = {&P};
+            const int nm = std::min(t.per_wave, batch - b0);
+            PPC_CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)sytrd_kernel, dim3(nblk * nm),
+                                                       dim3(kTrdThreads), args, smem, s));
+            count_launch();
+            check_launch("sytrd");
+        }
     }
     {
         StageTimer tm("eig.bisect", s);
-        bisect_top_kernel<<<(unsigned)k, kBisThreads, 2 * n * sizeof(double), s>>>(db.d(), eb.d(), n, lambda,
-                                                                              bnd.d());
+        bisect_top_kernel<<<(unsigned)(k * batch), kBisThreads, 2 * n * sizeof(double), s>>>(db.d(), eb.d(), n, k,
+                                                                                        lambda, bnd.d());
         count_launch();
         check_launch("bisect_top");
     }
@@ -706,21 +797,21 @@ void tridiag_eig_top(const double* G, int64_t n64, int64_t k64, double* Q, doubl
         const size_t ism = 7 * (size_t)n * sizeof(double) + n + 16;
         PPC_CUDA_CHECK(cudaFuncSetAttribute(inverse_iteration_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             (int)ism));
-        inverse_iteration_kernel<<<(unsigned)k, 32, ism, s>>>(db.d(), eb.d(), n, lambda, bnd.d(), Q);
+        inverse_iteration_kernel<<<(unsigned)(k * batch), 32, ism, s>>>(db.d(), eb.d(), n, k, lambda, bnd.d(), Q);
         count_launch();
         check_launch("inverse_iteration");
     }
     {
         StageTimer tm("eig.orth", s);
-        cholqr_inplace(Q, n, k, s);
+        cholqr_inplace(Q, n, k, s, batch);
     }
     {
         StageTimer tm("eig.backtransform", s);
-        DeviceBuffer Tws(sizeof(double) * ((n - 3 + kBtChunk) / kBtChunk) * kBtChunk * kBtChunk);
-        if (n <= 256) launch_back_transform<8>(Vb.d(), tb.d(), n, k, Q, Tws.d(), s);
-        else if (n <= 512) launch_back_transform<16>(Vb.d(), tb.d(), n, k, Q, Tws.d(), s);
-        else if (n <= 1024) launch_back_transform<32>(Vb.d(), tb.d(), n, k, Q, Tws.d(), s);
-        else launch_back_transform<48>(Vb.d(), tb.d(), n, k, Q, Tws.d(), s);
+        DeviceBuffer Tws(sizeof(double) * ((n - 3 + kBtChunk) / kBtChunk) * kBtChunk * kBtChunk * B);
+        if (n <= 256) launch_back_transform<8>(Vb.d(), tb.d(), n, k, batch, Q, Tws.d(), s);
+        else if (n <= 512) launch_back_transform<16>(Vb.d(), tb.d(), n, k, batch, Q, Tws.d(), s);
+        else if (n <= 1024) launch_back_transform<32>(Vb.d(), tb.d(), n, k, batch, Q, Tws.d(), s);
+        else launch_back_transform<48>(Vb.d(), tb.d(), n, k, batch, Q, Tws.d(), s);
         count_launch();
         check_launch("back_transform");
     }

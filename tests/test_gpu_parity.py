@@ -388,6 +388,32 @@ def test_large_slice_svd_vs_lapack(engine, m, n, k, kind):
             assert U[i, j, z] >= 0
 
 
+@pytest.mark.parametrize("m,n,batch", [(512, 520, 16), (301, 333, 5)])
+def test_large_slice_svd_direct_batched(engine, m, n, batch):
+    """Slice Grams of even order <= ~1536 whose batch fits a few waves of the
+    cooperative Householder reduction go to the batched direct eigensolver
+    (tridiag_eig.cu; 16 x 512 runs in two waves); odd orders to subspace
+    iteration. Both give LAPACK's singular values."""
+    import ctypes as C
+    from paper_2409_19402_b200 import _lib
+    L = _lib.lib()
+    rng = np.random.default_rng(m + batch)
+    a = np.asfortranarray(rng.standard_normal((m, n, batch)) + 0.5)
+    k = 8
+    buf = C.create_string_buffer(1 << 16)
+    L.ppc_timing_report(buf, len(buf), 1)  # drop earlier records
+    L.ppc_timing_enable(1)
+    U, s, V = engine.truncated_svd(a, k)
+    L.ppc_timing_report(buf, len(buf), 1)
+    L.ppc_timing_enable(0)
+    assert ("eig.tridiag" in buf.value.decode()) == (min(m, n) % 2 == 0), buf.value.decode()
+    for z in range(batch):
+        sn, ak = _numpy_rank_k(a[:, :, z], k)
+        np.testing.assert_allclose(s[:, z], sn[:k], rtol=1e-10)
+        rec = (U[:, :, z] * s[:, z]) @ V[:, :, z].T
+        assert np.linalg.norm(rec - ak) <= 1e-10 * np.linalg.norm(a[:, :, z])
+
+
 @pytest.mark.parametrize("k", [1, 10, 20])
 def test_tsvdq_video_large_slices_vs_oracle(engine, oracle, k):
     # full cfg2 frame size 240x320 (Gram + subspace path), 40 frames
