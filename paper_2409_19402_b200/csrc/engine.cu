@@ -350,18 +350,43 @@ void sweep_errors(const double* A, int64_t n1, int64_t n2, int64_t n3, const dou
         StageTimer tm("slice_svd", s);
         slice_svd(ah.d(), n1, n2, N, pmax, kmax, U.d(), S.d(), V.d(), nullptr, s);
     }
-    ah = DeviceBuffer();
+    static const bool identity = !(std::getenv("PPC_RE_IDENTITY") && std::getenv("PPC_RE_IDENTITY")[0] == '0');
     double anorm2[2];
     sumsq(A, nullptr, N * n3, anorm2, s);
     if (anorm2[1] == 0.0) fail(PPC_DEGENERATE, "relative_error: reference tensor is zero");
-    DeviceBuffer us(sizeof(double) * n1 * kmax * pmax), ch(sizeof(double) * N * pmax);
+    DeviceBuffer us(sizeof(double) * n1 * kmax * pmax), ch;
     for (int64_t ip = 0; ip < np; ++ip) {
         const int64_t p = ps[ip];
         for (int64_t ik = 0; ik < nk; ++ik) {
             const int64_t k = ks[ik];
-            StageTimer tm("recon_residual", s, 2.0 * p * N * k + 2.0 * N * p * n3, 8.0 * N * (p + n3));
             // U(:, :k, i) diag(S(:k, i)) V(:, :k, i)^T for the first p slices
             launch_scale_columns_strided(U.d(), S.d(), us.d(), n1, k, kmax, p, s);
+            if (identity) {
+                // orthogonal split (as in compress_relative_error): ||A - Ahat_k x3 Q||^2 =
+                // (||A||^2 - ||Ahat_p||^2) + sum_i ||Ahat_i - U_i S_i V_i^T||^2, both
+                // sums from one fused residual pass over the p slices of Ahat
+                StageTimer tm("slice_residual", s, 2.0 * p * N * k, 8.0 * p * N);
+                GemmDesc d;
+                d.M = n1; d.N = n2; d.K = k; d.batch = p;
+                d.A = us.d(); d.lda = n1; d.strideA = n1 * k;
+                d.B = V.d(); d.ldb = n2; d.strideB = n2 * kmax; d.b_nmajor = true;
+                const int64_t ctas = gemm_residual_ctas(d, ah.d(), n1, N);
+                DeviceBuffer part(sizeof(double) * 2 * (ctas + 1));
+                gemm_residual(d, ah.d(), n1, N, part.d(), s);
+                double* fin = part.d() + 2 * ctas;
+                launch_reduce_pairs(part.d(), ctas, fin, s);
+                double h[2];
+                PPC_CUDA_CHECK(cudaMemcpyAsync(h, fin, sizeof(h), cudaMemcpyDeviceToHost, s));
+                PPC_CUDA_CHECK(cudaStreamSynchronize(s));
+                const double num = (anorm2[1] - h[1]) + h[0];
+                if (std::isfinite(num) && num >= 2e-3 * anorm2[1]) {
+                    re[ik + ip * nk] = std::sqrt(num) / std::sqrt(anorm2[1]);
+                    continue;
+                }
+            }
+            // small errors: measured directly against A (no cancellation)
+            StageTimer tm("recon_residual", s, 2.0 * p * N * k + 2.0 * N * p * n3, 8.0 * N * (p + n3));
+            if (!ch.d()) ch = DeviceBuffer(sizeof(double) * N * pmax);
             GemmDesc d;
             d.M = n1; d.N = n2; d.K = k; d.batch = p;
             d.A = us.d(); d.lda = n1; d.strideA = n1 * k;

@@ -566,6 +566,28 @@ def test_sweep_vs_oracle(engine, oracle):
         engine.tsvdq_sweep(a, [4], [61])
 
 
+def test_sweep_small_errors_direct_residual(engine, oracle):
+    """RE^2 below 2e-3 of ||A||^2: the sweep measures the residual directly
+    against A instead of through the orthogonal split (no cancellation)."""
+    rng = np.random.default_rng(21)
+    a = np.einsum("ir,jr,kr->ijk", rng.standard_normal((30, 3)), rng.standard_normal((20, 3)),
+                  rng.standard_normal((16, 3)))
+    a = np.asfortranarray(a + 1e-5 * rng.standard_normal(a.shape))
+    # a fixed basis (a data-driven one's noise directions are not determined
+    # to 1e-10): p = 16 keeps all of mode 3 (RE ~ 1e-5, direct residual),
+    # p = 8 drops half of it (RE ~ 0.5, orthogonal split)
+    ps, ks = [8, 16], [3, 5]
+    re = engine.tsvdq_sweep(a, ps, ks, engine.Transform("dct", 16, 16))
+    qmax = oracle.dct_q(16, 16)
+    for ip, p in enumerate(ps):
+        for ik, k in enumerate(ks):
+            q = qmax[:, :p]
+            U, S, V = oracle.tsvdq(a, q, k)
+            want = oracle.relative_error(a, oracle.tsvdq_reconstruct(U, S, V, q))
+            assert (want < 1e-3) == (p == 16)
+            assert abs(re[ik, ip] - want) <= 1e-10 * want, (p, k, re[ik, ip], want)
+
+
 def test_sweep_large_slices(engine, oracle):
     a = synth.video(240, 320, 30, seed=13)
     ps, ks = [8, 16], [2, 12]
