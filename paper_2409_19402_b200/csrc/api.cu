@@ -47,6 +47,71 @@ void check_spatial_rank(int64_t n1, int64_t n2, int64_t k, const char* who) {
 
 }  // namespace
 
+namespace {
+// Host input: stream A in row-chunk groups on the copy stream into abuf and
+// start each group's partial Grams as soon as it lands (the H2D overlaps
+// the SYRK); then Q (n3 x p) from the Gram. Same chunks and tree as the
+// resident path, so Q is bitwise identical. `tdig` keeps the groups' digit
+// split for the forward transform, `trace` receives trace(G).
+void host_streamed_q(const double* A, int64_t N, int64_t n3, int64_t p, DeviceBuffer& abuf, double* Qout,
+                     double* sigma, double* trace, OzakiDigits* tdig, cudaStream_t s) {
+    if (!A) fail(PPC_ARGUMENT, "null input pointer");
+    abuf = DeviceBuffer(sizeof(double) * N * n3);
+    const GramPlan g = gram_plan(N, n3);
+    const int64_t per = std::min<int64_t>(g.chunks, 4);  // chunks per upload group
+    DeviceBuffer parts(sizeof(double) * g.chunks * n3 * n3);
+    cudaStream_t cs = copy_stream();
+    {
+        // the staging buffer was allocated on s: order cs after it
+        cudaEvent_t ready;
+        PPC_CUDA_CHECK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+        PPC_CUDA_CHECK(cudaEventRecord(ready, s));
+        PPC_CUDA_CHECK(cudaStreamWaitEvent(cs, ready, 0));
+        PPC_CUDA_CHECK(cudaEventDestroy(ready));
+    }
+    FiniteFlag nf(s);
+    bool checked = true;  // every slab's Gram pass also checked finiteness (INT8 path)
+    // the groups' digits land in one allocation, block c0 * blk_per_chunk on
+    const int64_t blk_per_chunk = (g.chunk + 4095) / 4096;
+    const bool keep = tdig && g.chunk % 4096 == 0;
+    {
+        StageTimer tm("gram_syrk", s, (double)N * n3 * n3, 8.0 * N * n3);
+        // groups of `per` chunks; the last chunk travels alone, so the
+        // Gram work left after the final byte lands is one chunk's
+        for (int64_t c0 = 0, take = 0; c0 < g.chunks; c0 += take) {
+            take = std::min<int64_t>(per, g.chunks - c0);
+            if (take > 1 && c0 + take == g.chunks) --take;
+            const int64_t r0 = c0 * g.chunk;
+            if (r0 >= N) {  // plan chunks beyond N: zero partials
+                PPC_CUDA_CHECK(cudaMemsetAsync(parts.d() + c0 * n3 * n3, 0,
+                                               sizeof(double) * (g.chunks - c0) * n3 * n3, s));
+                break;
+            }
+            const int64_t nr = std::min<int64_t>(take * g.chunk, N - r0);
+            PPC_CUDA_CHECK(cudaMemcpy2DAsync(abuf.d() + r0, sizeof(double) * N, A + r0, sizeof(double) * N,
+                                             sizeof(double) * nr, n3, cudaMemcpyHostToDevice, cs));
+            cudaEvent_t ev;
+            PPC_CUDA_CHECK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+            PPC_CUDA_CHECK(cudaEventRecord(ev, cs));
+            PPC_CUDA_CHECK(cudaStreamWaitEvent(s, ev, 0));
+            PPC_CUDA_CHECK(cudaEventDestroy(ev));
+            checked &= gram_chunks(abuf.d() + r0, N, nr, n3, g.chunk, take,
+                                   parts.d() + c0 * n3 * n3, s, nf.d(), keep ? tdig : nullptr,
+                                   c0 * blk_per_chunk, g.chunks * blk_per_chunk);
+        }
+        tree_reduce(parts.d(), g.chunks, n3 * n3, s);
+    }
+    if (tdig) tdig->uniform = keep && checked && tdig->nd == 7;  // every group on the INT8 path
+    if (checked)
+        nf.check(s, "svd");
+    else
+        require_finite(abuf.d(), N * n3, "svd", s);
+    if (trace) gram_trace(parts.d(), n3, trace, s);
+    eig_to_basis(parts.d(), n3, p, Qout, sigma, s);
+}
+
+}  // namespace
+
 extern "C" {
 
 int ppc_mode3_product(const double* A, int64_t n1, int64_t n2, int64_t n3, const double* M,
@@ -588,9 +653,16 @@ int ppc_tsvdq_sweep(const double* A, int64_t n1, int64_t n2, int64_t n3, const i
         }
         cudaStream_t s = stream();
         const int64_t N = n1 * n2;
-        In a(A, N * n3, loc);
-        DeviceBuffer qbuf;
+        DeviceBuffer qbuf, abuf;
         const double* dQ;
+        if (!Q && loc == PPC_HOST) {  // data-driven Q: the Gram overlaps the upload
+            qbuf = DeviceBuffer(sizeof(double) * n3 * pmax);
+            host_streamed_q(A, N, n3, pmax, abuf, qbuf.d(), nullptr, nullptr, nullptr, s);
+            sweep_errors(abuf.d(), n1, n2, n3, qbuf.d(), pmax, kmax, ps, np, ks, nk, re, s);
+            PPC_CUDA_CHECK(cudaStreamSynchronize(s));
+            return;
+        }
+        In a(A, N * n3, loc);
         if (Q) {
             require_finite(a.d, N * n3, "svd", s);
             In qi(Q, n3 * pmax, loc);
@@ -622,64 +694,8 @@ int ppc_tsvdq_compress(const double* A, int64_t n1, int64_t n2, int64_t n3, int6
         OzakiDigits tdig;  // A's 7-digit Gram split, reused by the forward transform
         const double* dA = A;
         if (loc == PPC_HOST) {
-            // Stream the input in row-chunk groups on a copy stream and start
-            // each group's partial Grams as soon as it lands: the H2D of A
-            // overlaps the SYRK. Same chunks and tree as the resident path
-            // (bitwise identical Q).
-            if (!A) fail(PPC_ARGUMENT, "null input pointer");
-            abuf = DeviceBuffer(sizeof(double) * N * n3);
+            host_streamed_q(A, N, n3, p, abuf, q.d, sigma ? sg.d : nullptr, est.d(), &tdig, s);
             dA = abuf.d();
-            const GramPlan g = gram_plan(N, n3);
-            const int64_t per = std::min<int64_t>(g.chunks, 4);  // chunks per upload group
-            DeviceBuffer parts(sizeof(double) * g.chunks * n3 * n3), G(sizeof(double) * n3 * n3);
-            cudaStream_t cs = copy_stream();
-            {
-                // the staging buffer was allocated on s: order cs after it
-                cudaEvent_t ready;
-                PPC_CUDA_CHECK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
-                PPC_CUDA_CHECK(cudaEventRecord(ready, s));
-                PPC_CUDA_CHECK(cudaStreamWaitEvent(cs, ready, 0));
-                PPC_CUDA_CHECK(cudaEventDestroy(ready));
-            }
-            FiniteFlag nf(s);
-            bool checked = true;  // every slab's Gram pass also checked finiteness (INT8 path)
-            // the groups' digits land in one allocation, block c0 * blk_per_chunk on
-            const int64_t blk_per_chunk = (g.chunk + 4095) / 4096;
-            const bool keep = g.chunk % 4096 == 0;
-            {
-                StageTimer tm("gram_syrk", s, (double)N * n3 * n3, 8.0 * N * n3);
-                // groups of `per` chunks; the last chunk travels alone, so the
-                // Gram work left after the final byte lands is one chunk's
-                for (int64_t c0 = 0, take = 0; c0 < g.chunks; c0 += take) {
-                    take = std::min<int64_t>(per, g.chunks - c0);
-                    if (take > 1 && c0 + take == g.chunks) --take;
-                    const int64_t r0 = c0 * g.chunk;
-                    if (r0 >= N) {  // plan chunks beyond N: zero partials
-                        PPC_CUDA_CHECK(cudaMemsetAsync(parts.d() + c0 * n3 * n3, 0,
-                                                       sizeof(double) * (g.chunks - c0) * n3 * n3, s));
-                        break;
-                    }
-                    const int64_t nr = std::min<int64_t>(take * g.chunk, N - r0);
-                    PPC_CUDA_CHECK(cudaMemcpy2DAsync(abuf.d() + r0, sizeof(double) * N, A + r0, sizeof(double) * N,
-                                                     sizeof(double) * nr, n3, cudaMemcpyHostToDevice, cs));
-                    cudaEvent_t ev;
-                    PPC_CUDA_CHECK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-                    PPC_CUDA_CHECK(cudaEventRecord(ev, cs));
-                    PPC_CUDA_CHECK(cudaStreamWaitEvent(s, ev, 0));
-                    PPC_CUDA_CHECK(cudaEventDestroy(ev));
-                    checked &= gram_chunks(abuf.d() + r0, N, nr, n3, g.chunk, take,
-                                           parts.d() + c0 * n3 * n3, s, nf.d(), keep ? &tdig : nullptr,
-                                           c0 * blk_per_chunk, g.chunks * blk_per_chunk);
-                }
-                tree_reduce(parts.d(), g.chunks, n3 * n3, s);
-            }
-            tdig.uniform = keep && checked && tdig.nd == 7;  // every group on the INT8 path
-            if (checked)
-                nf.check(s, "svd");
-            else
-                require_finite(dA, N * n3, "svd", s);
-            gram_trace(parts.d(), n3, est.d(), s);
-            eig_to_basis(parts.d(), n3, p, q.d, sigma ? sg.d : nullptr, s);
         } else {
             data_q(dA, N, n3, p, q.d, sigma ? sg.d : nullptr, s, true, est.d(), &tdig);
         }
