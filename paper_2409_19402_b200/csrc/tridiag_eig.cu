@@ -33,7 +33,7 @@ namespace ppc {
 
 namespace {
 
-constexpr int kTrdThreads = 256;
+constexpr int kTrdThreads = 512;
 constexpr double kEps = 2.220446049250313e-16;
 constexpr double kSafeMin = 2.2250738585072014e-308;
 
