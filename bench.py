@@ -682,6 +682,13 @@ def main():
         roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / peaks["hbm_gbs"], "traffic": None, "kernel": dom,
                 "peak_source": peaks["hbm_src"]}
+    # the step's largest share may be latency-bound work with no throughput
+    # roofline (the Householder reductions of the eigensolvers: one grid
+    # barrier per column); say so beside the throughput kernel
+    tri = stages.get("eig.tridiag")
+    if tri and tri["ms"] > st["ms"]:
+        roof["largest_stage"] = {"stage": "eig.tridiag (sytrd_kernel)", "share": tri["ms"] / max(1e-9, ms),
+                                 "bound": "latency: one grid barrier + L2 exchange per column, ~3.5-5 us a step"}
     stage_summary = {}
     for name, s in stages.items():
         a_ms = s["ms"] / max(1, s["n"])
