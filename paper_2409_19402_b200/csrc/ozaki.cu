@@ -685,6 +685,8 @@ void ozaki_gemm(const OzakiDigits& A, const OzakiDigits& B, int64_t nbatch, cons
     else launch_mma<false, false, false, 64, 3>(ma, mb, P, nbatch * P.tiles, s);
 }
 
+bool ozaki_path_on() { return ozaki_enabled(); }
+
 bool ozaki_gemm_eligible(int64_t M, int64_t K) { return ozaki_enabled() && M >= kBM && K >= 256 && K <= kKC; }
 
 namespace {

@@ -41,6 +41,8 @@ void ozaki_gemm(const OzakiDigits& A, const OzakiDigits& B, int64_t nbatch, cons
                 int64_t strideC, cudaStream_t s, int levels = 6, bool sym_a = false);
 // Whether the integer path applies to an output with M rows and K-length sums.
 bool ozaki_gemm_eligible(int64_t M, int64_t K);
+// the INT8 path is on (PPC_OZAKI / ppc_set_ozaki)
+bool ozaki_path_on();
 
 // {||X - Ch Q^T||^2, ||X||^2} for X (N x n3, leading dimension N), the
 // reconstruction core Ch (N x p) and the basis Q (n3 x p): the core's digits

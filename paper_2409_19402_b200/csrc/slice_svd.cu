@@ -64,6 +64,10 @@ GramPlan gram_plan(int64_t N, int64_t n3) {
     int64_t maxc = std::max<int64_t>(1, N / 512);
     int64_t c = 1;
     while (c * 2 <= want && c * 2 <= maxc) c *= 2;
+    // the INT8 Ozaki SYRK wants chunks of >= 4096 rows (one digit block
+    // each); it is far faster than a wide split-K DMMA SYRK on short Grams
+    if (ozaki_path_on() && n3 >= 128 && N >= 4 * 4096)
+        while (c > 1 && (N + c - 1) / c < 4096) c /= 2;
     g.chunks = c;
     g.chunk = ((N + c - 1) / c + 15) / 16 * 16;
     return g;
