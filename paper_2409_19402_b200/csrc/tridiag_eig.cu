@@ -284,10 +284,12 @@ __device__ __forceinline__ int sturm_count(const double* d, const double* e2, in
     return c;
 }
 
-// One CTA per wanted eigenvalue m (0 = largest): kBisThreads-way
+// One CTA per wanted eigenvalue m (0 = largest): NT-way
 // multisection, every thread one Sturm count per round (~7 bits a round).
-constexpr int kBisThreads = 256;
-__global__ void __launch_bounds__(kBisThreads) bisect_top_kernel(const double* __restrict__ dg,
+// NT = 256 for a few eigenvalues (latency: 8 bits a round); 64 when a batch
+// brings hundreds (work: the SMs are full either way).
+template <int NT>
+__global__ void __launch_bounds__(NT) bisect_top_kernel(const double* __restrict__ dg,
                                                                  const double* __restrict__ eg, int n, int k,
                                                                  double* __restrict__ lam,
                                                                  double* __restrict__ bounds) {
@@ -301,12 +303,12 @@ __global__ void __launch_bounds__(kBisThreads) bisect_top_kernel(const double* _
     }
     double* d = sh;
     double* e2 = sh + n;
-    __shared__ double s_gl[kBisThreads / 32], s_gu[kBisThreads / 32], s_em[kBisThreads / 32];
-    __shared__ int s_first[kBisThreads / 32];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = kBisThreads / 32;
+    __shared__ double s_gl[NT / 32], s_gu[NT / 32], s_em[NT / 32];
+    __shared__ int s_first[NT / 32];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = NT / 32;
     // Gershgorin interval and the pivot floor (fixed order: same in every CTA)
     double gl = 1e308, gu = -1e308, em = 0.0;
-    for (int i = tid; i < n; i += kBisThreads) {
+    for (int i = tid; i < n; i += NT) {
         const double di = dg[i];
         const double el = i > 0 ? fabs(eg[i - 1]) : 0.0, er = i < n - 1 ? fabs(eg[i]) : 0.0;
         d[i] = di;
@@ -345,17 +347,17 @@ __global__ void __launch_bounds__(kBisThreads) bisect_top_kernel(const double* _
     double lo = gl, hi = gu;
     for (int it = 0; it < 40; ++it) {
         if (hi - lo <= fmax(2.0 * kEps * fmax(fabs(lo), fabs(hi)), atol)) break;
-        const double x = lo + (hi - lo) * (double)(tid + 1) / (double)(kBisThreads + 1);
+        const double x = lo + (hi - lo) * (double)(tid + 1) / (double)(NT + 1);
         const int c = sturm_count(d, e2, n, x, pivmin);
         const unsigned ge = __ballot_sync(0xffffffffu, c >= want);
-        if (lane == 0) s_first[warp] = ge ? warp * 32 + __ffs(ge) - 1 : kBisThreads;
+        if (lane == 0) s_first[warp] = ge ? warp * 32 + __ffs(ge) - 1 : NT;
         __syncthreads();
-        int first = kBisThreads;
+        int first = NT;
         for (int w = 0; w < nw; ++w) first = min(first, s_first[w]);
         const double h = (double)(hi - lo);
         const double l0 = lo;
-        if (first < kBisThreads) hi = l0 + h * (double)(first + 1) / (double)(kBisThreads + 1);
-        if (first > 0) lo = l0 + h * (double)first / (double)(kBisThreads + 1);
+        if (first < NT) hi = l0 + h * (double)(first + 1) / (double)(NT + 1);
+        if (first > 0) lo = l0 + h * (double)first / (double)(NT + 1);
         __syncthreads();
     }
     if (tid == 0) {
@@ -787,8 +789,12 @@ void tridiag_eig_top_batched(const double* G, int64_t n64, int64_t strideG, int6
     }
     {
         StageTimer tm("eig.bisect", s);
-        bisect_top_kernel<<<(unsigned)(k * batch), kBisThreads, 2 * n * sizeof(double), s>>>(db.d(), eb.d(), n, k,
-                                                                                        lambda, bnd.d());
+        const unsigned grid = (unsigned)(k * batch);
+        const size_t bsm = 2 * n * sizeof(double);
+        if (grid >= 2u * (unsigned)ctx().sms)
+            bisect_top_kernel<64><<<grid, 64, bsm, s>>>(db.d(), eb.d(), n, k, lambda, bnd.d());
+        else
+            bisect_top_kernel<256><<<grid, 256, bsm, s>>>(db.d(), eb.d(), n, k, lambda, bnd.d());
         count_launch();
         check_launch("bisect_top");
     }
