@@ -135,7 +135,8 @@ __global__ void residual_kernel(const double* GX, const double* X, const double*
 
 // One CTA per slice: R = chol(S + shift*I) (upper, S = R^T R), then R^{-1},
 // written out as a full b x b column-major block with zeros below the
-// diagonal (Rout: R itself, optional). b <= 160 (shared memory).
+// diagonal (Rout: R itself, optional; rows of non-positive pivots zeroed).
+// b <= 160 (shared memory).
 //
 // The factor is built as L = R^T (lower, column-major in shared memory), so
 // a row of R is a contiguous column of L. Right-looking, one barrier per
@@ -151,6 +152,7 @@ __global__ void __launch_bounds__(1024, 1) chol_inv_kernel(const double* __restr
                                 const int* __restrict__ zmap = nullptr) {
     extern __shared__ __align__(16) double M[];
     __shared__ double dinv[160];  // 1 / R(i,i)
+    __shared__ unsigned char badk[160];  // pivot k broke down (a zero column)
     __shared__ int bad;
     const int b = (int)b64;
     const int64_t sl = zmap ? (int64_t)zmap[blockIdx.x] : (int64_t)blockIdx.x;
@@ -190,6 +192,7 @@ __global__ void __launch_bounds__(1024, 1) chol_inv_kernel(const double* __restr
         }
         if (tid == 0) {
             if (!ok) bad = 1;
+            badk[k] = !ok;
             dinv[k] = 1.0 / sqrt(dk);
         }
         dprev = dk;
@@ -202,7 +205,10 @@ __global__ void __launch_bounds__(1024, 1) chol_inv_kernel(const double* __restr
         double* ro = Rout + sl * b64 * b64;
         for (int t = tid; t < b * b; t += nt) {
             const int i = t % b, jj = t / b;
-            ro[t] = (i <= jj) ? M[jj + i * b] : 0.0;
+            // a broken-down pivot's row of R is zero (W = Q R with W's column
+            // in the span of the earlier ones, e.g. a zero slice): R^{-1} keeps
+            // the unit pivot so Q stays finite
+            ro[t] = (i <= jj && !badk[i]) ? M[jj + i * b] : 0.0;
         }
     }
     double* out = Rinv + sl * b64 * b64;

@@ -414,6 +414,33 @@ def test_large_slice_svd_direct_batched(engine, m, n, batch):
         assert np.linalg.norm(rec - ak) <= 1e-10 * np.linalg.norm(a[:, :, z])
 
 
+def test_large_slice_svd_direct_zero_and_repeated(engine):
+    """Batched direct path with a zero slice and a slice of exactly repeated
+    singular values next to a generic one: values match LAPACK, factors are
+    finite and U, V orthonormal where the values are nonzero."""
+    rng = np.random.default_rng(5)
+    m, n, batch, k = 300, 260, 3, 6
+    a = np.zeros((m, n, batch))
+    a[:, :, 0] = rng.standard_normal((m, n))
+    qu, _ = np.linalg.qr(rng.standard_normal((m, n)))
+    qv, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    sv = np.concatenate([np.full(10, 3.0), np.linspace(1.0, 0.1, n - 10)])
+    a[:, :, 2] = (qu * sv) @ qv.T
+    a = np.asfortranarray(a)
+    U, s, V = engine.truncated_svd(a, k)
+    assert np.isfinite(U).all() and np.isfinite(s).all() and np.isfinite(V).all()
+    for z in range(batch):
+        sn = np.linalg.svd(a[:, :, z], compute_uv=False)
+        np.testing.assert_allclose(s[:, z], sn[:k], rtol=1e-10, atol=1e-12)
+    for z in (0, 2):
+        assert np.linalg.norm(U[:, :, z].T @ U[:, :, z] - np.eye(k)) <= 1e-10 * k
+        assert np.linalg.norm(V[:, :, z].T @ V[:, :, z] - np.eye(k)) <= 1e-10 * k
+        rec = (U[:, :, z] * s[:, z]) @ V[:, :, z].T
+        u_, s_, vt_ = np.linalg.svd(a[:, :, z], full_matrices=False)
+        if z == 0:
+            assert np.linalg.norm(rec - (u_[:, :k] * s_[:k]) @ vt_[:k]) <= 1e-10 * np.linalg.norm(a[:, :, z])
+
+
 @pytest.mark.parametrize("k", [1, 10, 20])
 def test_tsvdq_video_large_slices_vs_oracle(engine, oracle, k):
     # full cfg2 frame size 240x320 (Gram + subspace path), 40 frames
