@@ -415,12 +415,13 @@ def test_large_slice_svd_direct_batched(engine, m, n, batch):
 
 
 def test_large_slice_svd_direct_zero_and_repeated(engine):
-    """Batched direct path with a zero slice and a slice of exactly repeated
-    singular values next to a generic one: values match LAPACK, factors are
+    """Batched direct path with a zero slice, a rank-2 slice (k = 6) and a
+    slice of exactly repeated singular values next to a generic one: values match LAPACK, factors are
     finite and U, V orthonormal where the values are nonzero."""
     rng = np.random.default_rng(5)
-    m, n, batch, k = 300, 260, 3, 6
+    m, n, batch, k = 300, 260, 4, 6
     a = np.zeros((m, n, batch))
+    a[:, :, 3] = rng.standard_normal((m, 2)) @ rng.standard_normal((2, n))  # rank 2 < k
     a[:, :, 0] = rng.standard_normal((m, n))
     qu, _ = np.linalg.qr(rng.standard_normal((m, n)))
     qv, _ = np.linalg.qr(rng.standard_normal((n, n)))
@@ -431,7 +432,7 @@ def test_large_slice_svd_direct_zero_and_repeated(engine):
     assert np.isfinite(U).all() and np.isfinite(s).all() and np.isfinite(V).all()
     for z in range(batch):
         sn = np.linalg.svd(a[:, :, z], compute_uv=False)
-        np.testing.assert_allclose(s[:, z], sn[:k], rtol=1e-10, atol=1e-12)
+        np.testing.assert_allclose(s[:, z], sn[:k], rtol=1e-10, atol=1e-12 * max(1.0, sn[0]))
     for z in (0, 2):
         assert np.linalg.norm(U[:, :, z].T @ U[:, :, z] - np.eye(k)) <= 1e-10 * k
         assert np.linalg.norm(V[:, :, z].T @ V[:, :, z] - np.eye(k)) <= 1e-10 * k
