@@ -38,20 +38,30 @@ FP64_PEAK_FALLBACK = 36.914  # TFLOP/s, MEASURED_FP64.json (DMMA m8n8k4, this po
 
 
 def load_peaks():
+    """Roofline denominators. HBM and bf16 come from the driver-written
+    MEASURED_PEAKS.json; FP64 (DMMA) from MEASURED_FP64.json (tools/fp64_peaks.cu
+    on this pool: there is no FP64 tcgen05 kind, so the driver's bf16 GEMM says
+    nothing about it); dense INT8 is taken as 2x the driver's measured bf16
+    burst (the B200's dense INT8 rate is twice its bf16 rate: 4.5 vs 2.25
+    POPS nominal), with cuBLASLt's measured INT8 GEMM noted beside it."""
     peaks = {"hbm_gbs": 6540.5, "fp64_tflops": FP64_PEAK_FALLBACK,
              "hbm_src": "MEASURED_PEAKS.json", "fp64_src": "MEASURED_FP64.json",
-             "int8_tops": 4500.0, "int8_src": "nominal B200 dense INT8 (fallback)"}
-    try:
-        with open(os.path.join(ROOT, "MEASURED_INT8.json")) as f:
-            peaks["int8_tops"] = float(json.load(f)["int8_tops"])
-        peaks["int8_src"] = "MEASURED_INT8.json (cuBLASLt int8 8192^3 on this pool, tools/int8_peak.py)"
-    except Exception:
-        pass
+             "int8_tops": 4500.0, "int8_src": "nominal B200 dense INT8 (fallback)", "int8_cublaslt_tops": None}
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            peaks["hbm_gbs"] = float(json.load(f)["hbm_gbs"])
+            mp = json.load(f)
+        peaks["hbm_gbs"] = float(mp["hbm_gbs"])
+        if mp.get("bf16_tflops"):
+            peaks["int8_tops"] = 2.0 * float(mp["bf16_tflops"])
+            peaks["int8_src"] = ("2 x bf16_tflops (burst) of the driver-written MEASURED_PEAKS.json "
+                                 "(dense INT8 = 2x dense bf16 on B200)")
     except Exception:
         peaks["hbm_gbs"], peaks["hbm_src"] = 6650.0, "fallback (B200_PROFILING.md)"
+    try:
+        with open(os.path.join(ROOT, "MEASURED_INT8.json")) as f:
+            peaks["int8_cublaslt_tops"] = float(json.load(f)["int8_tops"])
+    except Exception:
+        pass
     try:
         with open(os.path.join(ROOT, "MEASURED_FP64.json")) as f:
             d = json.load(f)
@@ -249,23 +259,24 @@ class StarQ:
             raise RuntimeError(L.ppc_last_error().decode())
 
     def cpu_sample(self, ppo, threads):
-        """Bounded sample: the same product with n1 and n2 cut to 128 (p, m, n3 kept)."""
-        import numpy as np
-        n1, m, n2, n3, p = 128, 512, 128, 256, 64
-        rng = np.random.default_rng(0)
-        a = np.asfortranarray(rng.standard_normal((n1, m, n3)))
-        b = np.asfortranarray(rng.standard_normal((m, n2, n3)))
+        """The full cfg4 product (no cut, no extrapolation) on the oracle
+        (star_products.cpp:51-59 restated), GEMMs on OpenBLAS with `threads`."""
+        from paper_2409_19402_b200 import synth
+        n1, m, n2, n3, p = self.dims
+        a = synth.gaussian(n1, m, n3, seed=0, stream=1)
+        b = synth.gaussian(m, n2, n3, seed=0, stream=2)
         q = ppo.dct_q(n3, p)
         flops = 2.0 * p * (n1 * m * n3 + m * n2 * n3 + n1 * m * n2 + n1 * n2 * n3)
         t0 = time.perf_counter()
-        reps = 0
-        while True:
-            ppo.star_q_product(a, b, q)
-            reps += 1
-            if time.perf_counter() - t0 > 10.0 or reps >= 50:
-                break
-        sec = (time.perf_counter() - t0) / reps
-        return flops / sec / 1e12, f"star_q_product A {n1}x{m}x{n3}, B {m}x{n2}x{n3}, p={p} (n1,n2 cut 8x), {reps} reps"
+        ppo.star_q_product(a, b, q)
+        sec = time.perf_counter() - t0
+        return flops / sec / 1e12, {
+            "sample": f"the full cfg4 product A {n1}x{m}x{n3} * B {m}x{n2}x{n3}, p={p} (no cut), 1 rep",
+            "how": f"oracle/ppo.c star_q_product, GEMMs on OpenBLAS {threads} thread(s)", "extrapolated": False,
+            "seconds": sec}
+
+
+_CPU_SAMPLES = {}
 
 
 class Tsvdq:
@@ -368,17 +379,32 @@ class Tsvdq:
             raise RuntimeError(L.ppc_last_error().decode())
 
     def cpu_sample(self, ppo, threads):
-        """Bounded sample of the same pipeline on the oracle (reference algorithm
-        restated, OpenBLAS GEMMs): n1 cut so the sample takes ~10-30 s."""
+        """cfg5: the full config (n3=1024, p=128, k=32, 2048^2 slices) on the
+        LAPACK restatement (oracle/baseline.py), timed on an N/64 lateral pixel
+        sample (QR, transforms, reconstruction + residual) and one whole
+        2048^2 slice SVD, extrapolated linearly in N and p (BASELINE.md
+        section 4). cfg2: the full video on the C oracle. cfg3: the oracle on
+        a 128x128 cut of the cube (n3, p, k kept)."""
         import numpy as np
         from paper_2409_19402_b200 import synth
         n1, n2, n3, p, k = self.dims
         if self.name == "cfg5":
-            # n3 = 1024 makes the oracle's Jacobi SVD of the n3 x n3 factor
-            # O(n3^3 sweeps) ~ minutes; the sample cuts every extent by 8
-            s1, s2, n3, p, k = 256, 256, 128, 16, 4
-            a = synth.cp_tensor(s1, s2, n3, rank=50, noise=1e-3, seed=1)
-        elif self.name == "cfg3":
+            from oracle import baseline
+            nj = n2 // 64
+            if "cfg5" not in _CPU_SAMPLES:  # generated once per process (not timed)
+                _CPU_SAMPLES["cfg5"] = (synth.cp_block(n1, n2, n3, 0, nj, rank=50, noise=1e-3, seed=1),
+                                        synth.cp_slice(n1, n2, rank=50, noise=1e-3, seed=1, i=0))
+            blk, sl = _CPU_SAMPLES["cfg5"]
+            sec, det = baseline.compress_timed(lambda w: blk, n1, n2, n3, p, k, nj, lambda i: sl)
+            return (8.0 * n1 * n2 * n3) / sec / 1e9, {
+                "sample": (f"full config {n1}x{n2}x{n3}, p={p}, k={k}: QR/transforms/reconstruction on a "
+                           f"{n1}x{nj}x{n3} lateral pixel sample (N/64), 1 whole {n1}x{n2} slice SVD; "
+                           "extrapolated linearly in N and p"),
+                "how": ("reference chain restated on LAPACK/BLAS (oracle/baseline.py: dgeqrf + dgesdd for Q, "
+                        "dgemm transforms, dgesdd per slice; numpy OpenBLAS, all host threads); dgesdd is far "
+                        "faster than the reference's Jacobi SVD, so this CPU figure is optimistic"),
+                "extrapolated": True, "seconds": sec, "parts": det}
+        if self.name == "cfg3":
             s1, s2 = 128, 128
             a = synth.hyperspectral(s1, s2, n3, seed=1)
         else:
@@ -389,15 +415,17 @@ class Tsvdq:
         if self.name == "cfg2":  # cmd_sweep: one tsvdq + reconstruction per k
             for kk in (1, 5, 10, 20):
                 U, S, V = ppo.tsvdq(a, q, kk)
-                re = ppo.relative_error(a, ppo.tsvdq_reconstruct(U, S, V, q))
+                ppo.relative_error(a, ppo.tsvdq_reconstruct(U, S, V, q))
             sec = time.perf_counter() - t0
-            return (8.0 * s1 * s2 * n3) / sec / 1e9, (f"oracle data Q + tsvdq + RE for k in 1,5,10,20 on the "
-                                                      f"full {s1}x{s2}x{n3} video (p={p}), 1 rep")
+            return (8.0 * s1 * s2 * n3) / sec / 1e9, {
+                "sample": f"oracle data Q + tsvdq + RE for k in 1,5,10,20 on the full {s1}x{s2}x{n3} video (p={p})",
+                "how": "oracle/ppo.c (Jacobi SVDs), GEMMs on OpenBLAS", "extrapolated": False, "seconds": sec}
         U, S, V = ppo.tsvdq(a, q, k)
-        re = ppo.relative_error(a, ppo.tsvdq_reconstruct(U, S, V, q))
+        ppo.relative_error(a, ppo.tsvdq_reconstruct(U, S, V, q))
         sec = time.perf_counter() - t0
-        return (8.0 * s1 * s2 * n3) / sec / 1e9, (f"oracle data Q + tsvdq + RE on a {s1}x{s2}x{n3} "
-                                                  f"tensor of the same distribution (p={p}, k={k}), 1 rep")
+        return (8.0 * s1 * s2 * n3) / sec / 1e9, {
+            "sample": f"oracle data Q + tsvdq + RE on a {s1}x{s2}x{n3} cut (p={p}, k={k})",
+            "how": "oracle/ppo.c (Jacobi SVDs), GEMMs on OpenBLAS", "extrapolated": False, "seconds": sec}
 
 
 class TsvdqSharded:
@@ -542,49 +570,188 @@ def make_workload(name, world=1, rank=0, local=0):
 
 
 # --------------------------------------------------------------- reference arm
+def _cpu_threads():
+    return os.cpu_count() or 1
+
+
 def run_reference(args, rank, world):
-    """--impl reference: the reference algorithm (oracle port; the C++/Eigen
-    reference cannot be built here — no Eigen) timed on the host cores."""
+    """--impl reference: the reference's algorithm on the host cores (the C++
+    reference cannot be built here: Eigen is absent), one bounded sample of
+    the workload per step, all host threads: cfg5 on the LAPACK restatement
+    (oracle/baseline.py, extrapolated from a pixel sample and whole slices),
+    cfg4 the whole product on the C oracle with OpenBLAS GEMMs."""
     if rank != 0:
         return
     from oracle import ppo
-    ppo.use_openblas()
-    threads = os.cpu_count() or 1
-    ppo.set_threads(threads)
-    wl_cls = {"cfg4": StarQ}.get(args.workload)
-    vals = []
+    threads = _cpu_threads()
+    ppo.use_openblas(threads=threads)
+    ppo.set_threads(1 if args.workload == "cfg4" else threads)  # as cpu_leg
 
     class _Shim:  # cpu_sample needs only dims/name
         pass
 
+    shim = _Shim()
     if args.workload == "cfg4":
-        sample_fn = StarQ.cpu_sample
-        shim = _Shim()
-        metric, unit = StarQ.metric, StarQ.unit
+        shim.dims, shim.name = (1024, 512, 1024, 256, 64), "cfg4"
+        sample_fn, metric, unit = StarQ.cpu_sample, StarQ.metric, StarQ.unit
     else:
-        dims = {"cfg5": (2048, 2048, 1024, 128, 32), "cfg3": (512, 512, 224, 32, 16),
-                "cfg2": (240, 320, 200, 20, 10)}[args.workload]
-        shim = _Shim()
-        shim.name, shim.dims = args.workload, dims
-        sample_fn = Tsvdq.cpu_sample
-        metric, unit = Tsvdq.metric, Tsvdq.unit
-    desc = ""
-    for _ in range(args.warmup if args.workload == "cfg4" else 0):
+        shim.name, shim.dims = args.workload, TSVDQ_DIMS[args.workload]
+        sample_fn, metric, unit = Tsvdq.cpu_sample, Tsvdq.metric, Tsvdq.unit
+    for _ in range(min(args.warmup, 1) if args.workload in ("cfg4", "cfg5") else 0):
         sample_fn(shim, ppo, threads)
+    vals, info = [], {}
     for _ in range(args.steps):
-        v, desc = sample_fn(shim, ppo, threads)
+        v, info = sample_fn(shim, ppo, threads)
         vals.append(v)
     vals.sort()
     v = vals[len(vals) // 2]
+    cpu = {"value": v, "unit": unit, "cores": threads, "kind": "port", "sample": info["sample"],
+           "how": info["how"], "extrapolated": info["extrapolated"]}
     line = {"impl": "reference", "metric": metric, "value": v, "unit": unit, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
             "dtype": "f64", "data": "synthetic",
-            "config": {"workload": args.workload, "sample": desc},
-            "cpu_baseline": {"value": v, "unit": unit, "cores": threads, "kind": "port",
-                             "sample": desc + "; reference algorithm restated in C (oracle/ppo.c), "
-                                              "GEMMs on OpenBLAS 1 thread, slice loops on all cores"},
+            "config": {"workload": args.workload, "sample": info["sample"]},
+            "cpu_baseline": cpu,
             "e2e": {"value": v, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+TSVDQ_DIMS = {"cfg5": (2048, 2048, 1024, 128, 32), "cfg3": (512, 512, 224, 32, 16),
+              "cfg2": (240, 320, 200, 20, 10)}
+
+
+# --------------------------------------------------------------------- legs
+def roofline(wl, stages, peaks, workload, ms, bound_override=None):
+    """Dominant kernel: algorithmic flops (or bytes) per launch / its average
+    CUDA-event duration on the launching stream."""
+    dom, bound = wl.dominant(stages)
+    if bound_override:
+        dom, bound = bound_override
+    st = stages.get(dom, {"ms": float("nan"), "n": 1, "flops": 0.0, "bytes": 0.0})
+    avg_ms = st["ms"] / max(1, st["n"])
+    traffic, tsrc = ncu_traffic(workload, dom)
+    if bound == "int8":
+        achieved = (st["flops"] / max(1, st["n"])) / (avg_ms / 1e3) / 1e12
+        roof = {"bound": "tensor", "achieved": achieved, "peak": peaks["int8_tops"],
+                "unit": "TFLOP/s", "op_kind": "int8 ops (TOPS) of the Ozaki digit products, tcgen05 kind::i8",
+                "frac": achieved / peaks["int8_tops"], "traffic": traffic,
+                "algorithmic_bytes": st["bytes"] / max(1, st["n"]), "kernel": dom,
+                "peak_source": peaks["int8_src"], "traffic_source": tsrc,
+                "frac_vs_cublaslt_int8": (achieved / peaks["int8_cublaslt_tops"]) if peaks["int8_cublaslt_tops"]
+                else None,
+                "fp64_equivalent_tflops": None}
+    elif bound == "tensor":
+        achieved = (st["flops"] / max(1, st["n"])) / (avg_ms / 1e3) / 1e12
+        roof = {"bound": "tensor", "achieved": achieved, "peak": peaks["fp64_tflops"],
+                "unit": "TFLOP/s", "frac": achieved / peaks["fp64_tflops"], "traffic": traffic,
+                "algorithmic_bytes": st["bytes"] / max(1, st["n"]),
+                "kernel": dom, "peak_source": peaks["fp64_src"] + " (FP64 DMMA; no tcgen05 f64 kind)",
+                "traffic_source": tsrc}
+    else:
+        achieved = (st["bytes"] / max(1, st["n"])) / (avg_ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / peaks["hbm_gbs"], "traffic": traffic, "kernel": dom,
+                "peak_source": peaks["hbm_src"], "traffic_source": tsrc}
+    roof["ms_per_launch"] = avg_ms
+    roof["share_of_step"] = st["ms"] / ms if ms > 0 else None
+    return roof
+
+
+def stage_summary(stages, ms):
+    out = {}
+    for name, s in stages.items():
+        a_ms = s["ms"] / max(1, s["n"])
+        out[name] = {"ms_per_launch": round(a_ms, 4), "launches": s["n"],
+                     "share": round(s["ms"] / ms, 4) if ms > 0 else None}
+        if s["flops"]:
+            out[name]["tflops"] = round(s["flops"] / s["n"] / (a_ms / 1e3) / 1e12, 3)
+        if s["bytes"]:
+            out[name]["gbs"] = round(s["bytes"] / s["n"] / (a_ms / 1e3) / 1e9, 1)
+    return out
+
+
+def timed_leg(wl, L, stream, steps, warmup, dist_on):
+    """W untimed steps, then K steps between CUDA events on the engine's
+    stream with a barrier + synchronize on both sides; max over ranks."""
+    import torch
+    for _ in range(warmup):
+        wl.step(L)
+    sync_all(dist_on)
+    L.ppc_launch_count(1)
+    timing_report(L, reset=True)
+    L.ppc_timing_enable(1)
+    sync_all(dist_on)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        wl.step(L)
+    e1.record(stream)
+    sync_all(dist_on)
+    L.ppc_timing_enable(0)
+    ms = max_over_ranks(e0.elapsed_time(e1), dist_on)
+    launches = int(L.ppc_launch_count(1))
+    stages = timing_report(L, reset=True)
+    return ms / steps, stages, launches
+
+
+def e2e_leg(wl, L, steps, world, dist_on):
+    import torch
+    wl.e2e_setup()
+    wl.e2e_step(L)  # warm
+    sync_all(dist_on)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        wl.e2e_step(L)
+    torch.cuda.synchronize()
+    sec = max_over_ranks((time.perf_counter() - t0) / steps, dist_on)
+    return {"value": wl.value(sec) * world, "unit": wl.unit, "h2d_bytes_per_step": wl.h2d,
+            "d2h_bytes_per_step": wl.d2h, "ms_per_step": sec * 1e3}
+
+
+def cpu_leg(wl):
+    try:
+        from oracle import ppo
+        threads = _cpu_threads()
+        ppo.use_openblas(threads=threads)
+        # star-Q: every host thread inside each BLAS GEMM (faster here than a
+        # threaded slice loop over single-threaded GEMMs); tSVDQ: the slice
+        # loop on every thread (the oracle's Jacobi SVDs do not use BLAS)
+        ppo.set_threads(1 if wl.metric == StarQ.metric else threads)
+        v, info = wl.cpu_sample(ppo, threads)
+        return {"value": v, "unit": wl.unit, "cores": threads, "kind": "port", "sample": info["sample"],
+                "how": info["how"], "extrapolated": info["extrapolated"], "cpu_seconds_per_step": info["seconds"],
+                **({"parts": info["parts"]} if "parts" in info else {})}
+    except Exception as ex:  # pragma: no cover
+        return {"value": None, "unit": wl.unit, "cores": 0, "kind": "port", "sample": f"failed: {ex}"}
+
+
+def golden_re():
+    try:
+        with open(os.path.join(ROOT, "tests", "golden", "cfg5_dmma.json")) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+ARITHMETIC = ("FP64 emulated on the INT8 tensor cores (Ozaki digit splitting, exact int32 digit products, "
+              "FP64 accumulation): 6-digit / 21-pair Gram SYRKs, 7-digit / 28-pair forward transform, "
+              "3-6-level slice-SVD filter products; every other product (small GEMMs, polish, Rayleigh-Ritz, "
+              "eigensolvers) on FP64 DMMA / FP64 FMA. value_fp64_dmma: the same step with every product on "
+              "FP64 DMMA (ppc_set_ozaki(0))")
+
+
+def spawn_ranks(args):
+    """--gpus N > 1 outside torchrun: run this script under
+    torch.distributed.run with N ranks on this node (one per GPU)."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
 # --------------------------------------------------------------------- main
@@ -598,8 +765,12 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-fp64", action="store_true", help="skip the all-FP64-DMMA leg (cfg5)")
+    ap.add_argument("--no-secondary", action="store_true", help="skip the cfg4 star-Q leg of the cfg5 run")
     args = ap.parse_args()
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -633,112 +804,91 @@ def main():
     for _ in range(args.warmup):
         wl.step(L)
     sync_all(dist_on)
-
     clocks.mark()
-    L.ppc_launch_count(1)
-    timing_report(L, reset=True)
-    L.ppc_timing_enable(1)
-    sync_all(dist_on)
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(args.steps):
-        wl.step(L)
-    e1.record(stream)
-    sync_all(dist_on)
-    L.ppc_timing_enable(0)
-    ms = e0.elapsed_time(e1)
-    launches = int(L.ppc_launch_count(1))
-    stages = timing_report(L, reset=True)
+    ms_step, stages, launches = timed_leg(wl, L, stream, args.steps, 0, dist_on)
     clk = clocks.stop()
-    ms = max_over_ranks(ms, dist_on)
-    ms_step = ms / args.steps
-    value_rank = wl.value(ms_step / 1e3)
-    value = value_rank * world  # every rank processes its own instance (weak)
-
-    # dominant kernel roofline (algorithmic flops or bytes per launch / avg launch time)
-    dom, bound = wl.dominant(stages)
-    st = stages.get(dom, {"ms": float("nan"), "n": 1, "flops": 0.0, "bytes": 0.0})
-    avg_ms = st["ms"] / max(1, st["n"])
-    if bound == "int8":
-        # INT8 tensor-core ops (2 per multiply-add) of the Ozaki digit products
-        achieved = (st["flops"] / max(1, st["n"])) / (avg_ms / 1e3) / 1e12
-        traffic, tsrc = ncu_traffic(args.workload, dom)
-        roof = {"bound": "tensor", "achieved": achieved, "peak": peaks["int8_tops"],
-                "unit": "TFLOP/s", "op_kind": "int8 ops (TOPS), tcgen05 kind::i8",
-                "frac": achieved / peaks["int8_tops"], "traffic": traffic,
-                "algorithmic_bytes": st["bytes"] / max(1, st["n"]), "kernel": dom,
-                "peak_source": peaks["int8_src"], "traffic_source": tsrc}
-    elif bound == "tensor":
-        achieved = (st["flops"] / max(1, st["n"])) / (avg_ms / 1e3) / 1e12
-        traffic, tsrc = ncu_traffic(args.workload, dom)
-        roof = {"bound": "tensor", "achieved": achieved, "peak": peaks["fp64_tflops"],
-                "unit": "TFLOP/s", "frac": achieved / peaks["fp64_tflops"], "traffic": traffic,
-                "algorithmic_bytes": st["bytes"] / max(1, st["n"]),
-                "kernel": dom, "peak_source": peaks["fp64_src"] + " (FP64 DMMA; no tcgen05 f64 kind)",
-                "traffic_source": tsrc}
-    else:
-        achieved = (st["bytes"] / max(1, st["n"])) / (avg_ms / 1e3) / 1e9
-        roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "frac": achieved / peaks["hbm_gbs"], "traffic": None, "kernel": dom,
-                "peak_source": peaks["hbm_src"]}
+    value = wl.value(ms_step / 1e3) * world  # whole job (sharded: value() divides by world)
+    roof = roofline(wl, stages, peaks, args.workload, ms_step * args.steps)
     # the step's largest share may be latency-bound work with no throughput
-    # roofline (the Householder reductions of the eigensolvers: one grid
-    # barrier per column); say so beside the throughput kernel
+    # roofline (the Householder reductions of the eigensolvers)
     tri = stages.get("eig.tridiag")
-    if tri and tri["ms"] > st["ms"]:
-        roof["largest_stage"] = {"stage": "eig.tridiag (sytrd_kernel)", "share": tri["ms"] / max(1e-9, ms),
-                                 "bound": "latency: one grid barrier + L2 exchange per column, ~3.5-5 us a step"}
-    stage_summary = {}
-    for name, s in stages.items():
-        a_ms = s["ms"] / max(1, s["n"])
-        stage_summary[name] = {"ms_per_launch": round(a_ms, 4), "launches": s["n"],
-                               "share": round(s["ms"] / ms, 4) if ms > 0 else None}
-        if s["flops"]:
-            stage_summary[name]["tflops"] = round(s["flops"] / s["n"] / (a_ms / 1e3) / 1e12, 3)
-        if s["bytes"]:
-            stage_summary[name]["gbs"] = round(s["bytes"] / s["n"] / (a_ms / 1e3) / 1e9, 1)
+    if tri and tri["ms"] > stages.get(roof["kernel"], {"ms": 0.0})["ms"]:
+        roof["largest_stage"] = {"stage": "eig.tridiag (sytrd_kernel)", "share": tri["ms"] / (ms_step * args.steps),
+                                 "bound": "latency: grid barriers + L2 exchanges per column block"}
+    re_main = getattr(wl, "re", None)
 
-    # end-to-end through the C-ABI with pinned host buffers
-    e2e = None
-    if not args.no_e2e:
-        wl.e2e_setup()
-        wl.e2e_step(L)  # warm
-        sync_all(dist_on)
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            wl.e2e_step(L)
-        torch.cuda.synchronize()
-        sec = max_over_ranks((time.perf_counter() - t0) / args.steps, dist_on)
-        e2e = {"value": wl.value(sec) * world, "unit": wl.unit, "h2d_bytes_per_step": wl.h2d,
-               "d2h_bytes_per_step": wl.d2h, "ms_per_step": sec * 1e3}
+    e2e = None if args.no_e2e else e2e_leg(wl, L, args.steps, world, dist_on)
+
+    # the same step with every product on FP64 DMMA (no INT8 emulation)
+    fp64 = None
+    if args.workload == "cfg5" and not args.no_fp64:
+        L.ppc_trim_workspace()
+        assert L.ppc_set_ozaki(0) == 0
+        try:
+            k64 = max(2, min(3, args.steps))
+            ms64, st64, _ = timed_leg(wl, L, stream, k64, 1, dist_on)
+            roof64 = roofline(wl, st64, peaks, args.workload, ms64 * k64, bound_override=("gram_syrk", "tensor"))
+            fp64 = {"value": wl.value(ms64 / 1e3) * world, "unit": wl.unit, "ms_per_step": ms64, "steps": k64,
+                    "warmup": 1, "roofline": roof64, "relative_error": getattr(wl, "re", None),
+                    "stages": stage_summary(st64, ms64 * k64)}
+        finally:
+            L.ppc_set_ozaki(1)
+            L.ppc_trim_workspace()
+
+    # the other half of the BASELINE metric: star-Q product TFLOP/s (cfg4)
+    secondary = None
+    if args.workload == "cfg5" and not args.no_secondary:
+        wl4 = make_workload("cfg4", world, rank, local)
+        ms4, st4, l4 = timed_leg(wl4, L, stream, args.steps, args.warmup, dist_on)
+        secondary = {"metric": wl4.metric, "value": wl4.value(ms4 / 1e3) * world, "unit": wl4.unit,
+                     "ms_per_step": ms4, "steps": args.steps, "warmup": args.warmup,
+                     "config": wl4.config(), "gpu_launches": l4,
+                     "roofline": roofline(wl4, st4, peaks, "cfg4", ms4 * args.steps),
+                     "e2e": None if args.no_e2e else e2e_leg(wl4, L, args.steps, world, dist_on),
+                     "stages": stage_summary(st4, ms4 * args.steps)}
+        if rank == 0 and world == 1 and not args.no_cpu_baseline:
+            secondary["cpu_baseline"] = cpu_leg(wl4)
+        del wl4
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        try:
-            from oracle import ppo
-            ppo.use_openblas()
-            threads = os.cpu_count() or 1
-            ppo.set_threads(threads)
-            v, desc = wl.cpu_sample(ppo, threads)
-            cpu = {"value": v, "unit": wl.unit, "cores": threads, "kind": "port",
-                   "sample": desc + "; reference algorithm restated in C (oracle/ppo.c; Eigen "
-                                    "reference unbuildable here), OpenBLAS 1-thread GEMMs, slice loops on all cores"}
-        except Exception as ex:  # pragma: no cover
-            cpu = {"value": None, "unit": wl.unit, "cores": 0, "kind": "port", "sample": f"failed: {ex}"}
+        cpu = cpu_leg(wl)
 
     if rank == 0:
         cfg = wl.config()
         sharded = isinstance(wl, (TsvdqSharded, StarQSharded))
         cfg["parallelism"] = (f"{'row' if isinstance(wl, StarQSharded) else 'pixel'}-sharded dp{world}" if sharded else
                               (f"replicas{world}" if world > 1 else "single"))
+        if dist_on:
+            cfg["comm"] = {"backend": "nccl", "nccl": ".".join(map(str, torch.cuda.nccl.version()))}
         line = {"metric": wl.metric, "value": value, "unit": wl.unit, "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-                "higher_is_better": True, "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f64",
+                "higher_is_better": True, "scaling": "strong" if sharded else "weak", "vs_baseline": None,
+                "dtype": "f64", "arithmetic": ARITHMETIC if args.workload != "cfg4" else
+                ARITHMETIC.replace("6-digit / 21-pair Gram SYRKs, 7-digit / 28-pair forward transform, "
+                                   "3-6-level slice-SVD filter products", "6-digit facewise product (rows "
+                                   "passing the dynamic-range gate); transforms on FP64 DMMA"),
                 "data": "synthetic", "config": cfg, "roofline": roof, "cpu_baseline": cpu,
-                "e2e": e2e, "gpu_launches": launches, "clocks": clk, "stages": stage_summary}
-        if getattr(wl, "re", None) is not None:
-            line["result_check"] = {"relative_error": wl.re}
+                "e2e": e2e, "gpu_launches": launches, "clocks": clk,
+                "stages": stage_summary(stages, ms_step * args.steps)}
+        if fp64 is not None:
+            line["value_fp64_dmma"] = fp64
+        if secondary is not None:
+            line["secondary"] = secondary
+        if re_main is not None:
+            rc = {"relative_error": re_main}
+            if fp64 is not None and fp64["relative_error"] is not None:
+                r64 = fp64["relative_error"]
+                rc.update({"relative_error_fp64_dmma": r64, "rel_diff_vs_fp64_dmma": abs(re_main - r64) / r64})
+            gold = golden_re() if args.workload == "cfg5" and not sharded else None
+            if gold:
+                rl = gold["relative_error_lapack"]
+                rc.update({"relative_error_lapack_golden": rl, "rel_diff_vs_lapack_golden": abs(re_main - rl) / rl,
+                           "golden": "tests/golden/cfg5_dmma.json (tools/golden_cfg5.py)"})
+            diffs = [v for kk, v in rc.items() if kk.startswith("rel_diff")]
+            if diffs:
+                rc["ok_1e-10"] = all(d <= 1e-10 for d in diffs)
+            line["result_check"] = rc
         print(json.dumps(line), flush=True)
 
     if dist_on:

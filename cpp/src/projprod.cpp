@@ -9,6 +9,7 @@
 
 #include "ppc.h"
 #include "projprod/decompositions.hpp"
+#include "projprod/engine.hpp"
 #include "projprod/io.hpp"
 #include "projprod/errors.hpp"
 #include "projprod/matrix_kernels.hpp"
@@ -586,5 +587,11 @@ Matrix read_pt3_matrix(const std::filesystem::path& path) {  // io.cpp:120-126
         throw format_error(path.string() + ": expected a matrix (n3 = 1), got n3 = " + std::to_string(A.n3()));
     return A.slice(0);
 }
+
+// ------------------------------------------------------------ engine controls
+namespace engine {
+void set_fp64_only(bool on) { check(ppc_set_ozaki(on ? 0 : 1)); }
+bool fp64_only() { return ppc_get_ozaki() == 0; }
+}  // namespace engine
 
 }  // namespace projprod

@@ -80,10 +80,17 @@ int ppc_timing_enable(int on);
  * eligible), 1 = always the cp.async kernel. Both accumulate every output in
  * the same order, so results are bitwise identical (used by the tests). */
 int ppc_set_gemm_path(int mode);
-/* FP64 Gram path: 1 = automatic (the INT8 tensor-core Ozaki SYRK, 7 digits,
- * where eligible; default), 0 = always the FP64 DMMA SYRK. PPC_OZAKI=0 in the
- * environment sets 0. Results agree to ~1e-14 relative (not bitwise). */
+/* Arithmetic of the large products: 1 = automatic (default): the FP64 Gram
+ * SYRKs, the compress chain's forward transform, the slice-SVD filter /
+ * Rayleigh-Ritz products, the reconstruction residual and the star-Q facewise
+ * product run on the INT8 tensor cores as FP64 emulation (Ozaki digit
+ * splitting, 6-7 digits, where eligible; the facewise product only for
+ * operands that pass the dynamic-range gate), the rest on FP64 DMMA;
+ * 0 = every product on FP64 DMMA (the FP64-only switch). PPC_OZAKI=0 in the
+ * environment sets 0. Results agree to ~1e-14 relative (not bitwise).
+ * ppc_get_ozaki returns the current mode. */
 int ppc_set_ozaki(int mode);
+int ppc_get_ozaki(void);
 /* The batched Ozaki SYRK on DEVICE memory (test hook for the INT8 path):
  * G_b = A_b^T A_b (n x n) for A_b = A + b*strideA (rows x n, lda),
  * 1024 <= rows <= 4096, n >= 128. PPC_ARGUMENT when not eligible. */
@@ -248,6 +255,21 @@ int ppc_gemm_strided(int64_t M, int64_t N, int64_t K, int64_t batch, double alph
                      const double* A, int64_t lda, int64_t strideA, int trans_a,
                      const double* B, int64_t ldb, int64_t strideB, int trans_b,
                      double* C, int64_t ldc, int64_t strideC);
+/* ---- multi-GPU building blocks (paper_2409_19402_b200/dist.py) ----------- */
+/* Facewise product of one slice group into a strided output, DEVICE memory,
+ * stream-ordered: C(:,:,i) (at C + i*strideC, leading dimension ldc) =
+ * A(:,:,i) B(:,:,i), A n1 x m x batch and B m x n2 x batch contiguous. Runs
+ * on the INT8 tensor cores when star_q's facewise would (256 <= m <= 4096,
+ * rows in whole 128-row blocks, operands passing the dynamic-range gate),
+ * else on FP64 DMMA: the row-sharded star-Q's replacement of
+ * tensor.cpp:149-156 for the rank's C rows. */
+int ppc_facewise_strided(const double* A, int64_t n1, int64_t m, int64_t batch, const double* B, int64_t n2,
+                         double* C, int64_t ldc, int64_t strideC);
+/* The pixel -> slice reshard's unpack, DEVICE memory, stream-ordered:
+ * recv holds G blocks [r][slice][j][i] (rank r's nj lateral columns of my ps
+ * slices, as all_to_all_single delivers them); out receives the ps whole
+ * n1 x (G nj) slices [slice][r nj + j][i] that the slice SVDs read. */
+int ppc_reshard_slices(const double* recv, int64_t G, int64_t ps, int64_t nj, int64_t n1, double* out);
 /* Partial Grams T_c^T T_c of `nchunks` consecutive chunks of `chunk` rows of
  * T (rows x n3, leading dimension ldT): parts is nchunks x n3 x n3. */
 int ppc_gram_partials(const double* T, int64_t ldT, int64_t rows, int64_t n3, int64_t chunk,
@@ -256,9 +278,12 @@ int ppc_gram_partials(const double* T, int64_t ldT, int64_t rows, int64_t n3, in
  * whole 4096-row blocks it keeps T's 7-digit split in the engine: *handle > 0
  * names it (0: nothing kept). ppc_mode3_forward_digits then forms T Q from the
  * kept digits on the INT8 tensor cores (the sharded forward transform), and
- * ppc_digits_release frees them. Handles belong to the calling thread. */
+ * ppc_digits_release frees them. Handles belong to the calling thread.
+ * *nonfinite (host) = 1 when T holds a NaN or Inf (the shard's half of
+ * matrix_kernels.cpp:32; the multi-GPU driver combines it over the ranks and
+ * raises PPC_NUMERIC on every one of them), else 0. */
 int ppc_gram_partials_keep(const double* T, int64_t ldT, int64_t rows, int64_t n3, int64_t chunk,
-                           int64_t nchunks, double* parts, int64_t* handle);
+                           int64_t nchunks, double* parts, int64_t* handle, int* nonfinite);
 /* out (rows x p, leading dimension rows, device) = T Q (Q: n3 x p, device) from
  * the digits kept under handle; PPC_ARGUMENT when the handle is unknown or the
  * shape does not qualify (the caller then uses ppc_mode3_product). */

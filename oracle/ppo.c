@@ -93,6 +93,7 @@ typedef void (*dgemm_t)(const char*, const char*, const int*, const int*, const 
                         const double*, const double*, const int*, const double*,
                         const int*, const double*, double*, const int*);
 static dgemm_t g_dgemm = NULL;
+static void (*g_blas_threads)(int) = NULL;
 
 int ppo_use_blas(const char* path, const char* sym, const char* set_threads_sym) {
     void* h = dlopen(path, RTLD_NOW | RTLD_LOCAL);
@@ -100,9 +101,18 @@ int ppo_use_blas(const char* path, const char* sym, const char* set_threads_sym)
     g_dgemm = (dgemm_t)dlsym(h, sym);
     if (!g_dgemm) return fail(PPO_ARGUMENT, "symbol %s not found", sym);
     if (set_threads_sym && *set_threads_sym) {
-        void (*st)(int) = (void (*)(int))dlsym(h, set_threads_sym);
-        if (st) st(1); /* Eigen without OpenMP: single-threaded GEMM (CMakeLists.txt:30) */
+        g_blas_threads = (void (*)(int))dlsym(h, set_threads_sym);
+        if (g_blas_threads) g_blas_threads(1); /* Eigen without OpenMP: single-threaded GEMM (CMakeLists.txt:30) */
     }
+    return 0;
+}
+
+/* Threads of the BLAS GEMMs (1 by default, as the reference). The parity
+ * tests raise it to check BASELINE-sized products in seconds; the CPU
+ * baseline keeps the reference's single thread per GEMM. */
+int ppo_set_blas_threads(int n) {
+    if (!g_dgemm || !g_blas_threads) return fail(PPO_ARGUMENT, "no BLAS loaded");
+    g_blas_threads(n < 1 ? 1 : n);
     return 0;
 }
 

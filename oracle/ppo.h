@@ -36,6 +36,7 @@ int ppo_threads(void);
  * Used only to make the CPU baseline's GEMM comparable to Eigen's. */
 int ppo_use_blas(const char* lib_path, const char* dgemm_symbol,
                  const char* set_threads_symbol);
+int ppo_set_blas_threads(int n);
 
 /* tensor.cpp:139-147  out.tubes = A.tubes * M^T, M is q x n3. */
 int ppo_mode3_product(const double* A, int64_t n1, int64_t n2, int64_t n3,

@@ -75,9 +75,11 @@ def threads() -> int:
     return lib().ppo_threads()
 
 
-def use_openblas() -> bool:
-    """Route oracle GEMMs through SciPy's bundled OpenBLAS (single-threaded),
-    standing in for Eigen's single-threaded GEMM in the CPU baseline."""
+def use_openblas(threads: int = 1) -> bool:
+    """Route oracle GEMMs through SciPy's bundled OpenBLAS, standing in for
+    Eigen's single-threaded GEMM in the CPU baseline (threads=1, the
+    reference's setting); the parity tests use more threads to check
+    BASELINE-sized products in seconds."""
     import glob
     import scipy
     libs = glob.glob(os.path.join(os.path.dirname(scipy.__file__), os.pardir,
@@ -86,6 +88,8 @@ def use_openblas() -> bool:
         rc = lib().ppo_use_blas(path.encode(), b"scipy_dgemm_",
                                 b"scipy_openblas_set_num_threads")
         if rc == 0:
+            if threads != 1:
+                _chk(lib().ppo_set_blas_threads(int(threads)))
             return True
     return False
 

@@ -51,6 +51,9 @@ def lib() -> C.CDLL:
         "ppc_timing_enable": (C.c_int, [C.c_int]),
         "ppc_set_gemm_path": (C.c_int, [C.c_int]),
         "ppc_set_ozaki": (C.c_int, [C.c_int]),
+        "ppc_get_ozaki": (C.c_int, []),
+        "ppc_facewise_strided": (C.c_int, [vp, i64, i64, i64, vp, i64, vp, i64, i64]),
+        "ppc_reshard_slices": (C.c_int, [vp, i64, i64, i64, i64, vp]),
         "ppc_ozaki_syrk_batched": (C.c_int, [vp, i64, i64, i64, i64, i64, vp]),
         "ppc_timing_report": (C.c_int, [C.c_char_p, i64, C.c_int]),
         "ppc_mode3_product": (C.c_int, [vp, i64, i64, i64, vp, i64, C.c_int, vp, C.c_int]),
@@ -75,7 +78,8 @@ def lib() -> C.CDLL:
         "ppc_gram_partials": (C.c_int, [vp, i64, i64, i64, i64, i64, vp, C.c_int]),
         "ppc_tree_reduce": (C.c_int, [vp, i64, i64, C.c_int]),
         "ppc_sym_eig_top": (C.c_int, [vp, i64, i64, vp, vp, C.c_int]),
-        "ppc_gram_partials_keep": (C.c_int, [vp, i64, i64, i64, i64, i64, vp, C.POINTER(C.c_int64)]),
+        "ppc_gram_partials_keep": (C.c_int, [vp, i64, i64, i64, i64, i64, vp, C.POINTER(C.c_int64),
+                                            C.POINTER(C.c_int)]),
         "ppc_mode3_forward_digits": (C.c_int, [i64, vp, i64, vp]),
         "ppc_digits_release": (C.c_int, [i64]),
         "ppc_slice_residual_sums": (C.c_int, [vp, i64, i64, i64, i64, vp, vp, vp, pd, C.c_int]),

@@ -418,6 +418,30 @@ int ppc_gemm_strided(int64_t M, int64_t N, int64_t K, int64_t batch, double alph
     });
 }
 
+int ppc_facewise_strided(const double* A, int64_t n1, int64_t m, int64_t batch, const double* B, int64_t n2,
+                         double* C, int64_t ldc, int64_t strideC) {
+    return guarded([&] {
+        check_tensor(n1, m, batch);
+        require_positive(n2, "n2");
+        if (!A || !B || !C) fail(PPC_ARGUMENT, "facewise_strided: null operand");
+        if (ldc < n1 || strideC < ldc * n2) fail(PPC_ARGUMENT, "facewise_strided: output strides too small");
+        facewise_auto(A, n1, m, batch, B, n2, C, ldc, strideC, stream());
+    });
+}
+
+int ppc_reshard_slices(const double* recv, int64_t G, int64_t ps, int64_t nj, int64_t n1, double* out) {
+    return guarded([&] {
+        if (G < 1 || ps < 1 || nj < 1 || n1 < 1) fail(PPC_SHAPE, "reshard_slices: extents must be positive");
+        if (!recv || !out) fail(PPC_ARGUMENT, "reshard_slices: null pointer");
+        // recv [r][slice][j][i] (block r: rank r's lateral columns of my
+        // slices) -> out [slice][r*nj + j][i] (whole n1 x (G nj) slices)
+        const size_t blk = sizeof(double) * (size_t)(nj * n1);
+        for (int64_t r = 0; r < G; ++r)
+            PPC_CUDA_CHECK(cudaMemcpy2DAsync(out + r * nj * n1, blk * (size_t)G, recv + r * ps * nj * n1, blk, blk,
+                                             (size_t)ps, cudaMemcpyDeviceToDevice, stream()));
+    });
+}
+
 int ppc_star_m_product(const double* A, int64_t n1, int64_t m, int64_t n3, const double* B, int64_t n2,
                        const double* M, double* C, int loc) {
     return guarded([&] {
@@ -522,16 +546,27 @@ thread_local int64_t t_digits_next = 1;
 }  // namespace
 
 int ppc_gram_partials_keep(const double* T, int64_t ldT, int64_t rows, int64_t n3, int64_t chunk,
-                           int64_t nchunks, double* parts, int64_t* handle) {
+                           int64_t nchunks, double* parts, int64_t* handle, int* nonfinite) {
     return guarded([&] {
-        if (!handle || !T || !parts) fail(PPC_ARGUMENT, "null pointer");
+        if (!handle || !T || !parts || !nonfinite) fail(PPC_ARGUMENT, "null pointer");
         *handle = 0;
+        *nonfinite = 0;
         if (rows < 1 || n3 < 1 || ldT < rows || chunk < 1 || nchunks < 1)
             fail(PPC_SHAPE, "gram_partials: bad extents");
         if (chunk % 16) fail(PPC_ARGUMENT, "gram_partials: chunk must be a multiple of 16");
         cudaStream_t s = stream();
         auto d = std::make_unique<OzakiDigits>();
-        gram_chunks(T, ldT, rows, n3, chunk, nchunks, parts, s, nullptr, d.get());
+        // the shard's finiteness (matrix_kernels.cpp:32), reported instead of
+        // raised: the caller combines it over the ranks so all of them fail
+        FiniteFlag nf(s);
+        if (!gram_chunks(T, ldT, rows, n3, chunk, nchunks, parts, s, nf.d(), d.get())) {
+            if (ldT == rows)  // the DMMA SYRK did not look: scan the block
+                launch_nonfinite(T, rows * n3, nf.d(), s);
+            else
+                for (int64_t c = 0; c < n3; ++c) launch_nonfinite(T + c * ldT, rows, nf.d(), s);
+        }
+        PPC_CUDA_CHECK(cudaMemcpyAsync(nonfinite, nf.d(), sizeof(int), cudaMemcpyDeviceToHost, s));
+        PPC_CUDA_CHECK(cudaStreamSynchronize(s));
         if (d->uniform && d->nd == 7) {
             *handle = t_digits_next++;
             t_digits[*handle] = std::move(d);

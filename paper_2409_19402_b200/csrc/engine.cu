@@ -49,19 +49,73 @@ namespace {
 // The transform-domain facewise product on the INT8 tensor cores (Ozaki):
 // Ch_i = Ah_i Bh_i with Ah_i^T (slice-wise transpose, K = m contiguous) and
 // Bh_i split into digits along m; Bd may carry B's digits from a previous
-// call (host pipeline: one B for every A row block).
+// call (host pipeline: one B for every A row block). Rows run in blocks of
+// kFaceRows: a block whose rows (or B's columns) fail the dynamic-range gate
+// (ozaki_peak_ratios) is computed on FP64 DMMA instead, so the host pipeline
+// (one call per row block) and the device call decide every row the same way
+// and stay bitwise equal. Returns false when nothing ran on the INT8 path
+// (the caller then runs the DMMA facewise on all rows).
+constexpr int64_t kFaceRows = 128;
+
+void facewise_rows(const double* Ah, int64_t n1, int64_t i0, int64_t bi, int64_t m, int64_t p, const double* Bh,
+                   int64_t n2, double* Ch, int64_t ldc, int64_t strideC, cudaStream_t s) {
+    GemmDesc d;  // rows [i0, i0 + bi) of every slice
+    d.M = bi; d.N = n2; d.K = m; d.batch = p;
+    d.A = Ah + i0; d.lda = n1; d.strideA = n1 * m;
+    d.B = Bh; d.ldb = m; d.strideB = m * n2;
+    d.C = Ch + i0; d.ldc = ldc; d.strideC = strideC;
+    gemm(d, s);
+}
+
+// Ch (slice i at Ch + i*strideC, leading dimension ldc; n1 x n2 per slice).
 bool facewise_ozaki(const double* Ah, int64_t n1, int64_t m, int64_t p, const double* Bh, int64_t n2, double* Ch,
-                    OzakiDigits& Bd, bool b_ready, cudaStream_t s) {
+                    OzakiDigits& Bd, bool& b_ready, double& b_peak, cudaStream_t s, int64_t ldc = 0,
+                    int64_t strideC = 0) {
+    if (ldc <= 0) ldc = n1;
+    if (strideC <= 0) strideC = n1 * n2;
     if (!ozaki_gemm_eligible(n1, m) || n2 < 64) return false;
     StageTimer tm("facewise", s, 2.0 * n1 * m * n2 * p, 8.0 * p * (n1 * m + m * n2 + n1 * n2));
+    if (!b_ready) {
+        Bd.split(Bh, m, m * n2, m, n2, m, p, s);
+        b_peak = ozaki_peak_ratios(Bd, m, n2, s)[0];
+        b_ready = true;
+    }
+    if (b_peak > kOzakiPeakGate) return false;
     DeviceBuffer at(sizeof(double) * n1 * m * p);
     launch_transpose(Ah, at.d(), n1, m, p, s);  // (m x n1) per slice
     OzakiDigits Ad;
     Ad.split(at.d(), m, m * n1, m, n1, m, p, s);
-    if (!b_ready) Bd.split(Bh, m, m * n2, m, n2, m, p, s);
-    ozaki_gemm(Ad, Bd, p, nullptr, Ch, n1, n1 * n2, s);
+    const std::vector<double> a_peak = ozaki_peak_ratios(Ad, m, kFaceRows, s);
+    // a short last block runs on DMMA too, as it does as its own host-pipeline call
+    auto int8_rows = [&](size_t g) {
+        return a_peak[g] <= kOzakiPeakGate && n1 - (int64_t)g * kFaceRows >= kFaceRows;
+    };
+    bool any = false;
+    for (size_t g = 0; g < a_peak.size(); ++g) any |= int8_rows(g);
+    if (!any) return false;
+    ozaki_gemm(Ad, Bd, p, nullptr, Ch, ldc, strideC, s);
+    for (size_t g = 0; g < a_peak.size(); ++g)
+        if (!int8_rows(g)) {
+            const int64_t i0 = (int64_t)g * kFaceRows;
+            facewise_rows(Ah, n1, i0, std::min(kFaceRows, n1 - i0), m, p, Bh, n2, Ch, ldc, strideC, s);
+        }
     return true;
 }
+
+}  // namespace
+
+void facewise_auto(const double* Ah, int64_t n1, int64_t m, int64_t p, const double* Bh, int64_t n2, double* Ch,
+                   int64_t ldc, int64_t strideC, cudaStream_t s) {
+    OzakiDigits bd;
+    bool b_ready = false;
+    double b_peak = 0.0;
+    if (!facewise_ozaki(Ah, n1, m, p, Bh, n2, Ch, bd, b_ready, b_peak, s, ldc, strideC)) {
+        StageTimer tm("facewise", s, 2.0 * n1 * m * n2 * p, 8.0 * p * (n1 * m + m * n2 + n1 * n2));
+        facewise_rows(Ah, n1, 0, n1, m, p, Bh, n2, Ch, ldc, strideC, s);
+    }
+}
+
+namespace {
 
 }  // namespace
 
@@ -72,7 +126,9 @@ void star_q(const double* A, int64_t n1, int64_t m, int64_t n3, const double* B,
     mode3(A, n1 * m, n3, Q, p, true, ah.d(), 1.0, s);   // A x3 Q^T
     mode3(B, m * n2, n3, Q, p, true, bh.d(), 1.0, s);   // B x3 Q^T
     OzakiDigits bd;
-    if (!facewise_ozaki(ah.d(), n1, m, p, bh.d(), n2, ch.d(), bd, false, s))
+    bool b_ready = false;
+    double b_peak = 0.0;
+    if (!facewise_ozaki(ah.d(), n1, m, p, bh.d(), n2, ch.d(), bd, b_ready, b_peak, s))
         facewise(ah.d(), n1, m, p, bh.d(), n2, ch.d(), s);   // facewise
     mode3(ch.d(), n1 * n2, p, Q, n3, false, C, scale, s);  // x3 Q, scale in the epilogue
 }
@@ -119,9 +175,10 @@ void star_q_host(const double* hA, int64_t n1, int64_t m, int64_t n3, const doub
     }
     b.release();
     // 2. A row blocks: H2D (up) -> transforms + facewise (s) -> D2H (down)
-    const int64_t BI = std::min<int64_t>(n1, 128);
+    const int64_t BI = std::min<int64_t>(n1, kFaceRows);
     OzakiDigits bd;  // B's digits, split with the first block
     bool b_ready = false;
+    double b_peak = 0.0;
     DeviceBuffer ablk[2], ahblk[2], chblk[2], cblk[2];
     Event a_free[2], c_free[2];
     for (int u = 0; u < 2; ++u) {
@@ -143,9 +200,7 @@ void star_q_host(const double* hA, int64_t n1, int64_t m, int64_t n3, const doub
         landed.wait_on(s);
         mode3(ablk[u].d(), bi * m, n3, q.d(), p, true, ahblk[u].d(), 1.0, s);  // A_blk x3 Q^T
         a_free[u].record(s);
-        if (facewise_ozaki(ahblk[u].d(), bi, m, p, bh.d(), n2, chblk[u].d(), bd, b_ready, s))
-            b_ready = true;
-        else
+        if (!facewise_ozaki(ahblk[u].d(), bi, m, p, bh.d(), n2, chblk[u].d(), bd, b_ready, b_peak, s))
             facewise(ahblk[u].d(), bi, m, p, bh.d(), n2, chblk[u].d(), s);
         c_free[u].wait_on(s);  // block ib-2's C rows are down
         mode3(chblk[u].d(), bi * n2, p, q.d(), n3, false, cblk[u].d(), scale, s);  // x3 Q, scale

@@ -19,6 +19,13 @@ void mode3(const double* T, int64_t N, int64_t n3, const double* M, int64_t q, b
 // C(:,:,i) = A(:,:,i) B(:,:,i), i < p                     [tensor.cpp:149-156]
 void facewise(const double* A, int64_t n1, int64_t m, int64_t p, const double* B, int64_t n2,
               double* C, cudaStream_t s);
+// The transform-domain facewise product with a strided output (slice i of C
+// at C + i*strideC, leading dimension ldc): on the INT8 tensor cores where
+// the shapes and the operands' dynamic range allow (as star_q), else FP64
+// DMMA. A (n1 x m x p) and B (m x n2 x p) are contiguous slice stacks. Used
+// by the row-sharded multi-GPU star-Q, whose C rows are a strided view.
+void facewise_auto(const double* A, int64_t n1, int64_t m, int64_t p, const double* B, int64_t n2, double* C,
+                   int64_t ldc, int64_t strideC, cudaStream_t s);
 // star_products.cpp:51-59
 void star_q(const double* A, int64_t n1, int64_t m, int64_t n3, const double* B, int64_t n2,
             const double* Q, int64_t p, double scale, double* C, cudaStream_t s);

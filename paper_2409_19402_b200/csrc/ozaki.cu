@@ -35,6 +35,7 @@
 #include <atomic>
 #include <cstdlib>
 #include <mutex>
+#include <vector>
 
 #include "internal.h"
 #include "kernels.cuh"
@@ -687,6 +688,48 @@ void ozaki_gemm(const OzakiDigits& A, const OzakiDigits& B, int64_t nbatch, cons
 
 bool ozaki_path_on() { return ozaki_enabled(); }
 
+namespace {
+// out[g] = max over blocks b and columns c of group g (c / group == g) of
+// (sc/2) sqrt(K) / ||x||: sc/2 bounds max|x| from above (sc in (2, 4] max|x|),
+// so this is >= the column's peak ratio max|x| sqrt(K) / ||x||_2 and < twice
+// it; zero columns count 0.
+__global__ void peak_ratio_kernel(const double* __restrict__ sc, const double* __restrict__ sq, int64_t nblk,
+                                  int64_t cols, double sqrtK, int64_t group, double* __restrict__ out) {
+    const int64_t g = blockIdx.x;
+    const int64_t c0 = g * group, c1 = std::min<int64_t>(c0 + group, cols);
+    double mx = 0.0;
+    for (int64_t b = 0; b < nblk; ++b)
+        for (int64_t c = c0 + threadIdx.x; c < c1; c += blockDim.x) {
+            const double q = sq[b * cols + c];
+            if (q > 0.0) mx = fmax(mx, 0.5 * sc[b * cols + c] * sqrtK / sqrt(q));
+        }
+    __shared__ double red[8];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) mx = fmax(mx, red[w]);
+        out[g] = fmax(mx, red[0]);
+    }
+}
+}  // namespace
+
+std::vector<double> ozaki_peak_ratios(const OzakiDigits& d, int64_t K, int64_t group, cudaStream_t s) {
+    const int64_t ng = (d.cols + group - 1) / group;
+    std::vector<double> h((size_t)ng);
+    DeviceBuffer out(sizeof(double) * ng);
+    peak_ratio_kernel<<<(unsigned)ng, 256, 0, s>>>(d.sc.d(), d.sq.d(), d.nblk, d.cols, std::sqrt((double)K), group,
+                                                  out.d());
+    count_launch();
+    check_launch("peak_ratio");
+    PPC_CUDA_CHECK(cudaMemcpyAsync(h.data(), out.d(), sizeof(double) * ng, cudaMemcpyDeviceToHost, s));
+    PPC_CUDA_CHECK(cudaStreamSynchronize(s));
+    return h;
+}
+
+bool ozaki_gram_eligible(int64_t n3, int64_t chunk) { return ozaki_enabled() && n3 >= 128 && chunk >= 4096; }
+
 bool ozaki_gemm_eligible(int64_t M, int64_t K) { return ozaki_enabled() && M >= kBM && K >= 256 && K <= kKC; }
 
 namespace {
@@ -760,8 +803,13 @@ bool ozaki_gram_partials(const double* T, int64_t ldT, int64_t rows, int64_t n3,
                          double* parts, cudaStream_t s, int* nonfinite, OzakiDigits* keep, int64_t block_base,
                          int64_t total_blocks) {
     if (!ozaki_enabled()) return false;
-    // the integer path pays off once each output tile sees a long K range
-    if (n3 < 128 || chunk < 4096 || rows < 4096 * 4) return false;
+    // The integer path pays off once each output tile sees a long K range.
+    // The decision depends on the plan (n3, chunk) only, never on this
+    // call's row count: every row group of the host-streamed Gram and every
+    // rank's shard takes the same path, so Q is bitwise the same for host and
+    // device input and for 1..8 GPUs (gram_plan keeps chunks >= 4096 rows
+    // whenever N >= 16384 with the path on).
+    if (!ozaki_gram_eligible(n3, chunk)) return false;
     if (rows > chunk * nchunks) return false;
     // each plan chunk is split into ceil(chunk / 4096) blocks that never cross
     // a plan-chunk boundary, and its partial sums them in order inside one
@@ -859,6 +907,8 @@ extern "C" int ppc_set_ozaki(int mode) {
     ppc::g_ozaki.store(mode);
     return 0;
 }
+
+extern "C" int ppc_get_ozaki(void) { return ppc::ozaki_path_on() ? 1 : 0; }
 
 extern "C" int ppc_ozaki_syrk_batched(const double* A, int64_t lda, int64_t strideA, int64_t rows, int64_t n,
                                       int64_t batch, double* G) {

@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <vector>
 
 #include "internal.h"
 
@@ -39,6 +40,19 @@ struct OzakiDigits {
 // (fixed_max): A is streamed from its upper triangles only (half the reads).
 void ozaki_gemm(const OzakiDigits& A, const OzakiDigits& B, int64_t nbatch, const int* zmap, double* C, int64_t ldc,
                 int64_t strideC, cudaStream_t s, int levels = 6, bool sym_a = false);
+// Whether the Gram partials of a plan with chunks of `chunk` rows run on the
+// integer path (a function of the plan only, see ozaki_gram_partials).
+bool ozaki_gram_eligible(int64_t n3, int64_t chunk);
+// The cheap dynamic-range gate of the INT8 products. The split rounds every
+// value at ~2^-47 of its column's maximum, so an output C(a,b) carries an
+// error ~ sqrt(K) 2^-46 max|A(a,:)| max|B(:,b)|, against FP64's ~ sqrt(K)
+// 2^-53 |A(a,:)| |B(:,b)|: the two stay within a small factor while every
+// row/column's peak ratio max|x| sqrt(K) / ||x|| is small (~3-4 for Gaussian
+// data, sqrt(K) for a row dominated by one entry). Returns, per group of
+// `group` consecutive columns of d, an upper bound (< 2x) on the largest
+// peak ratio over all its blocks (one host sync).
+std::vector<double> ozaki_peak_ratios(const OzakiDigits& d, int64_t K, int64_t group, cudaStream_t s);
+constexpr double kOzakiPeakGate = 16.0;  // products whose operands exceed it run on FP64 DMMA
 // Whether the integer path applies to an output with M rows and K-length sums.
 bool ozaki_gemm_eligible(int64_t M, int64_t K);
 // the INT8 path is on (PPC_OZAKI / ppc_set_ozaki)

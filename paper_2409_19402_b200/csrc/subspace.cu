@@ -149,7 +149,7 @@ __global__ void residual_kernel(const double* GX, const double* X, const double*
 constexpr int kCholSlots = 5;  // x slots per lane: b <= 160
 __global__ void __launch_bounds__(1024, 1) chol_inv_kernel(const double* __restrict__ S, double* __restrict__ Rinv, int64_t b64,
                                 int shift_pass, int* fail, double* __restrict__ Rout,
-                                const int* __restrict__ zmap = nullptr) {
+                                const int* __restrict__ zmap = nullptr, int* __restrict__ weak = nullptr) {
     extern __shared__ __align__(16) double M[];
     __shared__ double dinv[160];  // 1 / R(i,i)
     __shared__ unsigned char badk[160];  // pivot k broke down (a zero column)
@@ -174,10 +174,18 @@ __global__ void __launch_bounds__(1024, 1) chol_inv_kernel(const double* __restr
         if (tid == 0 && fail) atomicExch(fail, 1);
         return;
     }
+    // weak (nullable, one int per slice): set when a pivot falls below
+    // 1e-12 of the largest diagonal, i.e. a column's residual after the
+    // earlier ones is below 1e-6 of the largest column: CholQR's squared
+    // condition number no longer yields an orthonormal factor there
+    double dmax = 0.0;
+    if (weak)
+        for (int i = 0; i < b; ++i) dmax = fmax(dmax, M[i + i * b]);  // every thread, same order
     double dprev = 1.0;
     for (int k = 0; k < b; ++k) {
         const double d = M[k + k * b];
         const bool ok = d > 0.0;
+        if (weak && tid == 0 && !(d > 1e-12 * dmax)) weak[sl] = 1;
         const double dk = ok ? d : 1.0;
         const double rinv = 1.0 / dk;
         // trailing lower triangle i >= j > k: warps over columns, lanes over rows
@@ -248,6 +256,110 @@ __global__ void __launch_bounds__(1024, 1) chol_inv_kernel(const double* __restr
         }
     }
     if (tid == 0 && bad && fail) atomicExch(fail, 1);
+}
+
+// Block-wide sum with a fixed order (warp butterflies, then warp 0 over the
+// per-warp partials); every thread gets the result. red: >= 33 doubles.
+__device__ double block_sum(double v, double* red) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    v = warp_sum(v);
+    __syncthreads();  // red is free (previous use finished)
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+        double a = lane < nw ? red[lane] : 0.0;
+        a = warp_sum(a);
+        if (lane == 0) red[32] = a;
+    }
+    __syncthreads();
+    return red[32];
+}
+
+// The polish's QR of W (o x k per slice) for slices whose CholQR2 hit a weak
+// pivot (rank-deficient slices, k above the slice rank, zero slices): CGS2
+// (two classical Gram-Schmidt passes per column, which stays orthonormal to
+// working precision at any condition number), one CTA per flagged slice.
+// A column whose twice-projected residual is below 1e-14 of the largest
+// column of W carries no content: it is replaced by an orthonormal
+// completion, e_t projected out of the earlier columns with t the row of
+// least captured mass (first on ties). Then R = Qw^T W (a general k x k; the
+// Jacobi SVD of R that follows does not need it triangular), so W = Qw R
+// holds to working precision and U = Qw Ur is orthonormal, as the
+// reference's JacobiSVD factors are (matrix_kernels.cpp:29-37).
+__global__ void __launch_bounds__(512) cgs2_fallback_kernel(const double* __restrict__ W, double* __restrict__ Qw,
+                                                            double* __restrict__ R, int64_t o, int k,
+                                                            const int* __restrict__ weak, double* __restrict__ dots) {
+    const int64_t sl = blockIdx.x;
+    if (!weak[sl]) return;
+    __shared__ double red[33];
+    __shared__ double c[160];
+    __shared__ int tmin;
+    const double* w = W + sl * o * k;
+    double* q = Qw + sl * o * k;
+    double* rowm = dots + sl * o;  // captured mass per row, sum_i q_i(t)^2
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
+    double wmax = 0.0;
+    for (int j = 0; j < k; ++j) {
+        double a = 0.0;
+        for (int64_t t = tid; t < o; t += nt) a = fma(w[t + j * o], w[t + j * o], a);
+        wmax = fmax(wmax, block_sum(a, red));
+    }
+    for (int64_t t = tid; t < o; t += nt) rowm[t] = 0.0;
+    for (int j = 0; j < k; ++j) {
+        double* v = q + (int64_t)j * o;
+        for (int64_t t = tid; t < o; t += nt) v[t] = w[t + (int64_t)j * o];
+        double nv = 0.0;
+        for (int attempt = 0; attempt < 2; ++attempt) {
+            for (int pass = 0; pass < 2; ++pass) {
+                __syncthreads();
+                // c_i = q_i^T v (one warp per i, lanes over rows, fixed order)
+                for (int i = warp; i < j; i += nw) {
+                    const double* qi = q + (int64_t)i * o;
+                    double a = 0.0;
+                    for (int64_t t = lane; t < o; t += 32) a = fma(qi[t], v[t], a);
+                    a = warp_sum(a);
+                    if (lane == 0) c[i] = a;
+                }
+                __syncthreads();
+                for (int64_t t = tid; t < o; t += nt) {
+                    double x = v[t];
+                    for (int i = 0; i < j; ++i) x = fma(-q[t + (int64_t)i * o], c[i], x);
+                    v[t] = x;
+                }
+            }
+            double a = 0.0;
+            for (int64_t t = tid; t < o; t += nt) a = fma(v[t], v[t], a);
+            nv = block_sum(a, red);
+            if (attempt == 1 || nv > 1e-28 * wmax) break;
+            // no content left: start over from e_t, t = the least captured row
+            if (tid == 0) {
+                int64_t best = 0;
+                for (int64_t t = 1; t < o; ++t)
+                    if (rowm[t] < rowm[best]) best = t;
+                tmin = (int)best;
+            }
+            __syncthreads();
+            for (int64_t t = tid; t < o; t += nt) v[t] = t == tmin ? 1.0 : 0.0;
+        }
+        const double inv = nv > 0.0 ? 1.0 / sqrt(nv) : 0.0;
+        for (int64_t t = tid; t < o; t += nt) {
+            const double x = v[t] * inv;
+            v[t] = x;
+            rowm[t] = fma(x, x, rowm[t]);
+        }
+    }
+    __syncthreads();
+    // R = Qw^T W: one warp per entry
+    double* r = R + sl * (int64_t)k * k;
+    for (int e = warp; e < k * k; e += nw) {
+        const int i = e % k, jj = e / k;
+        const double* qi = q + (int64_t)i * o;
+        const double* wj = w + (int64_t)jj * o;
+        double a = 0.0;
+        for (int64_t t = lane; t < o; t += 32) a = fma(qi[t], wj[t], a);
+        a = warp_sum(a);
+        if (lane == 0) r[e] = a;
+    }
 }
 
 // tail2[z] = sum of the pairs' first components of CTA partials in group z.
@@ -913,7 +1025,8 @@ void subspace_svd(const double* A, int64_t m, int64_t n, int64_t stride, int64_t
         T1(sizeof(double) * o * k * batch), Sk(sizeof(double) * k * k * batch),
         R1(sizeof(double) * k * k * batch), R2(sizeof(double) * k * k * batch),
         Ri(sizeof(double) * k * k * batch), R(sizeof(double) * k * k * batch),
-        Ur(sizeof(double) * k * k * batch), Vr(sizeof(double) * k * k * batch), flag(sizeof(int) * 2);
+        Ur(sizeof(double) * k * k * batch), Vr(sizeof(double) * k * k * batch), weak(sizeof(int) * batch);
+    PPC_CUDA_CHECK(cudaMemsetAsync(weak.d(), 0, sizeof(int) * batch, s));
     {
         GemmDesc d;
         d.M = o; d.N = k; d.K = r; d.batch = batch;
@@ -929,16 +1042,25 @@ void subspace_svd(const double* A, int64_t m, int64_t n, int64_t stride, int64_t
     if (ksm > 48 * 1024)
         PPC_CUDA_CHECK(cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ksm));
     g_AtB(Wb.d(), Wb.d(), Sk.d(), o, k, k, batch, o * k, o * k, s);
-    chol_inv_kernel<<<(unsigned)batch, k > 16 ? 1024 : 256, ksm, s>>>(Sk.d(), Ri.d(), k, 0, flag.as<int>(), R1.d());
+    chol_inv_kernel<<<(unsigned)batch, k > 16 ? 1024 : 256, ksm, s>>>(Sk.d(), Ri.d(), k, 0, nullptr, R1.d(), nullptr,
+                                                                         weak.as<int>());
     count_launch();
     check_launch("chol_inv");
     g_AB(Wb.d(), Ri.d(), T1.d(), o, k, k, batch, o * k, k * k, 1.0, nullptr, 0.0, s);
     g_AtB(T1.d(), T1.d(), Sk.d(), o, k, k, batch, o * k, o * k, s);
-    chol_inv_kernel<<<(unsigned)batch, k > 16 ? 1024 : 256, ksm, s>>>(Sk.d(), Ri.d(), k, 0, flag.as<int>(), R2.d());
+    chol_inv_kernel<<<(unsigned)batch, k > 16 ? 1024 : 256, ksm, s>>>(Sk.d(), Ri.d(), k, 0, nullptr, R2.d(), nullptr,
+                                                                         weak.as<int>());
     count_launch();
     check_launch("chol_inv");
     g_AB(T1.d(), Ri.d(), Qw.d(), o, k, k, batch, o * k, k * k, 1.0, nullptr, 0.0, s);
     g_AB(R2.d(), R1.d(), R.d(), k, k, k, batch, k * k, k * k, 1.0, nullptr, 0.0, s);
+    {  // slices with a weak pivot: Qw and R again by CGS2 (one CTA each; the rest return at once)
+        DeviceBuffer rowm(sizeof(double) * o * batch);
+        cgs2_fallback_kernel<<<(unsigned)batch, 512, 0, s>>>(Wb.d(), Qw.d(), R.d(), o, (int)k, weak.as<int>(),
+                                                             rowm.d());
+        count_launch();
+        check_launch("cgs2_fallback");
+    }
     // R = Ur diag(sigma) Vr^T (one-CTA Jacobi, high relative accuracy)
     jacobi_svd(R.d(), k, k, k * k, batch, k, Ur.d(), S, Vr.d(), nullptr, s);
     if (tall) {  // A ~ (Qw Ur) sigma (Xk Vr)^T

@@ -45,6 +45,7 @@ import torch
 import torch.distributed as dist
 
 from . import _lib
+from .projprod import NumericError
 
 
 def _check(rc):
@@ -81,9 +82,16 @@ class DeviceBackend:
         mode3_fwd_kept."""
         parts = torch.empty(nchunks * n3 * n3, dtype=torch.float64, device=self.device)
         h = C.c_int64(0)
-        _check(self.L.ppc_gram_partials_keep(_p(A_blk), rows, rows, n3, chunk, nchunks, _p(parts), C.byref(h)))
+        bad = C.c_int(0)
+        _check(self.L.ppc_gram_partials_keep(_p(A_blk), rows, rows, n3, chunk, nchunks, _p(parts), C.byref(h),
+                                             C.byref(bad)))
         self._kept = h.value
-        return parts.view(nchunks, n3 * n3)
+        return parts.view(nchunks, n3 * n3), bool(bad.value)
+
+    def release_kept(self):
+        h, self._kept = getattr(self, "_kept", 0), 0
+        if h:
+            _check(self.L.ppc_digits_release(h))
 
     def mode3_fwd_kept(self, A_blk, n1, nj, n3, Q, p):
         """A_blk x3 Q^T from the digits kept by gram_partials (INT8 tensor
@@ -99,6 +107,7 @@ class DeviceBackend:
         return self.mode3_fwd(A_blk, n1, nj, n3, Q, p)
 
     def tree_reduce(self, parts):
+        """Fixed pairwise tree over the rows of parts (in place); returns row 0."""
         parts = parts.contiguous()
         _check(self.L.ppc_tree_reduce(_p(parts), parts.shape[0], parts.shape[1], 1))
         return parts[0].clone()
@@ -116,12 +125,19 @@ class DeviceBackend:
 
     def facewise_into(self, Ah, Bb, Cv):
         """Cv(:, :, s) = Ah(:, :, s) Bb(:, :, s): Ah (a x m x ns) and Bb (m x b x ns)
-        Fortran, Cv a strided (a x b x ns) view into the C^ rows."""
+        Fortran with contiguous slices, Cv a strided (a x b x ns) view into the
+        C^ rows. INT8 tensor cores where the 1-GPU star_q's facewise runs there
+        (ppc_facewise_strided), else FP64 DMMA."""
         a, m, ns = Ah.shape
         b = Bb.shape[1]
-        _check(self.L.ppc_gemm_strided(a, b, m, ns, C.c_double(1.0), _p(Ah), Ah.stride(1), Ah.stride(2), 0,
-                                       _p(Bb), Bb.stride(1), Bb.stride(2), 0, _p(Cv), Cv.stride(1),
-                                       Cv.stride(2)))
+        assert Ah.stride(1) == a and Ah.stride(2) == a * m and Bb.stride(1) == m and Bb.stride(2) == m * b
+        _check(self.L.ppc_facewise_strided(_p(Ah), a, m, ns, _p(Bb), b, _p(Cv), Cv.stride(1), Cv.stride(2)))
+
+    def unpack_slices(self, recv, G, ps, nj, n1):
+        """recv (G, ps, nj, n1) -> (ps, G nj, n1) whole slices (ppc_reshard_slices)."""
+        out = torch.empty((ps, G * nj, n1), dtype=torch.float64, device=self.device)
+        _check(self.L.ppc_reshard_slices(_p(recv), G, ps, nj, n1, _p(out)))
+        return out
 
     def mode3_inv(self, Ch, d1, d2, p, Q, n3, scale):
         """(Ch x3 Q) * scale, the scale in the GEMM epilogue (star_products.cpp:56-58)."""
@@ -218,14 +234,21 @@ def sharded_compress(A_blk, plan: ShardPlan, k: int, backend, group=None):
     n1, n2, n3, p, nj, G = plan.n1, plan.n2, plan.n3, plan.p, plan.nj, plan.world
     rows = n1 * nj
     # 1-2. partial Grams of the local chunks, local subtree, global finish
-    parts = backend.gram_partials(A_blk, rows, n3, plan.chunk, plan.chunks_per_rank)
-    root = backend.tree_reduce(parts)
-    roots = [torch.empty_like(root) for _ in range(G)]
+    parts, bad = backend.gram_partials(A_blk, rows, n3, plan.chunk, plan.chunks_per_rank)
+    # matrix_kernels.cpp:32 on the whole tensor: any rank's NaN/Inf fails all
+    flag = torch.tensor([1.0 if bad else 0.0], dtype=torch.float64, device=parts.device)
     if G > 1:
-        dist.all_gather(roots, root, group=group)
+        dist.all_reduce(flag, op=dist.ReduceOp.MAX, group=group)
+    if float(flag.item()) != 0.0:
+        backend.release_kept()
+        raise NumericError("svd: input has non-finite entries")
+    root = backend.tree_reduce(parts)
+    if G > 1:  # the rank subtree roots, finished by the same pairwise tree
+        roots = torch.empty((G, root.numel()), dtype=root.dtype, device=root.device)
+        dist.all_gather_into_tensor(roots, root.reshape(1, -1), group=group)
+        Gm = backend.tree_reduce(roots)
     else:
-        roots = [root]
-    Gm = _tree_finish(roots)
+        Gm = root
     # 3. replicated eigensolve
     Q, _ = backend.sym_eig_top(Gm, n3, p)
     # 4. local forward transform (from the Gram's kept digits when it can)
@@ -240,24 +263,23 @@ def sharded_compress(A_blk, plan: ShardPlan, k: int, backend, group=None):
     else:
         recv.copy_(send)
     # recv[r] = rank r's lateral block (columns j0_r..) of my ps slices
-    blocks = recv.view(G, ps, nj, n1)                 # [r][slice][j][i]
-    full = blocks.permute(1, 0, 2, 3).reshape(ps, n2, n1)  # [slice][j][i], j ascending by rank
+    full = backend.unpack_slices(recv, G, ps, nj, n1) if G > 1 else recv.view(ps, nj, n1)  # [slice][j][i]
     S_loc = full.permute(2, 1, 0)                     # (n1, n2, ps) Fortran view
     # 6. slice SVDs, all-gather the factor stacks
     U, s, V = backend.svd_slices(S_loc, n1, n2, ps, k)
     # slice-space half of the error split, on the local slices (before the gather)
     st, sa2 = backend.slice_sums(S_loc, n1, n2, ps, k, U, s, V)
-    Uc = U.permute(2, 1, 0).contiguous()  # (ps, k, n1)
+    Uc = U.permute(2, 1, 0).contiguous()  # (ps, k, n1): no copy, U is Fortran (n1, k, ps)
     sc = s.permute(1, 0).contiguous()     # (ps, k)
     Vc = V.permute(2, 1, 0).contiguous()  # (ps, k, n2)
-    if G > 1:
-        Ug = [torch.empty_like(Uc) for _ in range(G)]
-        sg = [torch.empty_like(sc) for _ in range(G)]
-        Vg = [torch.empty_like(Vc) for _ in range(G)]
-        dist.all_gather(Ug, Uc, group=group)
-        dist.all_gather(sg, sc, group=group)
-        dist.all_gather(Vg, Vc, group=group)
-        Uc, sc, Vc = torch.cat(Ug), torch.cat(sg), torch.cat(Vg)
+    if G > 1:  # gathered straight into the (n, k, p) stacks, slices in rank order
+        Ug = torch.empty((G * ps,) + tuple(Uc.shape[1:]), dtype=Uc.dtype, device=Uc.device)
+        sg = torch.empty((G * ps,) + tuple(sc.shape[1:]), dtype=sc.dtype, device=sc.device)
+        Vg = torch.empty((G * ps,) + tuple(Vc.shape[1:]), dtype=Vc.dtype, device=Vc.device)
+        dist.all_gather_into_tensor(Ug, Uc, group=group)
+        dist.all_gather_into_tensor(sg, sc, group=group)
+        dist.all_gather_into_tensor(Vg, Vc, group=group)
+        Uc, sc, Vc = Ug, sg, Vg
     Uf, Sf, Vf = Uc.permute(2, 1, 0), sc.permute(1, 0), Vc.permute(2, 1, 0)  # (n1,k,p) (k,p) (n2,k,p)
     # 7. relative error. Q is orthonormal, so ||A - A_k||^2 =
     # (||A||^2 - ||Ahat||^2) + sum_i ||Ahat_i - U_i S_i V_i^T||^2 with ||A||^2 the

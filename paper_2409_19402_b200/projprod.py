@@ -31,7 +31,7 @@ __all__ = [
     "tsvdq2_error", "read_pt3", "write_pt3", "read_pt3_matrix", "write_pt3_matrix", "pt3_shape",
     "write_tsvdq_factors", "star_m", "star_m_product", "HosvdFactors", "hosvd", "hosvd_reconstruct",
     "MatrixSvdBaseline", "matrix_svd_baseline", "matrix_svd_error", "compress_tsvdq", "tsvdq_sweep", "to_device", "empty_device", "to_host",
-    "launch_count",
+    "launch_count", "set_fp64_only", "fp64_only",
 ]
 
 
@@ -164,6 +164,18 @@ def _call(args: _Args, fn, *cargs):
 
 def launch_count(reset: bool = False) -> int:
     return int(_lib.lib().ppc_launch_count(1 if reset else 0))
+
+
+def set_fp64_only(on: bool = True) -> None:
+    """Engine arithmetic (no counterpart in the reference, which is Eigen FP64
+    throughout): False (default) runs the large products on the INT8 tensor
+    cores as Ozaki FP64 emulation (~1e-14 relative to the operands' scale),
+    True runs every product on FP64 DMMA. Process-wide (ppc_set_ozaki)."""
+    _check(_lib.lib().ppc_set_ozaki(0 if on else 1))
+
+
+def fp64_only() -> bool:
+    return _lib.lib().ppc_get_ozaki() == 0
 
 
 # --------------------------------------------------------------- transforms

@@ -153,3 +153,28 @@ def cp_block_device(n1, n2, n3, j0, nj, rank=50, noise=1e-3, seed=0, device="cud
             slab.add_(torch.randn(slab.shape, dtype=torch.float64, device=device, generator=gn),
                       alpha=noise)
     return flat.view(n3, nj, n1).permute(2, 1, 0)
+
+
+def cp_block(n1, n2, n3, j0, nj, rank=50, noise=1e-3, seed=0):
+    """Host lateral block A[:, j0:j0+nj, :] of a cfg5-distributed tensor
+    (rank-R CP with N(0,1) factors + N(0, noise^2)): the CPU baseline's
+    pixel sample. Same distribution as cp_tensor_device, not the same bits."""
+    rng = np.random.default_rng([seed, 5])
+    f1 = rng.standard_normal((n1, rank))
+    f2 = rng.standard_normal((n2, rank))[j0:j0 + nj]
+    f3 = rng.standard_normal((n3, rank))
+    kr = (f1[:, None, :] * f2[None, :, :]).reshape(n1 * nj, rank, order="F")
+    T = kr @ f3.T
+    T += noise * np.random.default_rng([seed, 17, j0]).standard_normal(T.shape)
+    return np.asfortranarray(T.reshape(n1, nj, n3, order="F"))
+
+
+def cp_slice(n1, n2, rank=50, noise=1e-3, seed=0, i=0):
+    """Host n1 x n2 transform-domain slice of a cfg5-distributed tensor:
+    A x3 q for a unit q is sum_r c_r f1_r f2_r^T + N(0, noise^2) with
+    c_r = (F3^T q)_r ~ N(0, 1) (the CPU baseline's slice-SVD sample)."""
+    rng = np.random.default_rng([seed, 29, i])
+    f1 = rng.standard_normal((n1, rank))
+    f2 = rng.standard_normal((n2, rank))
+    c = rng.standard_normal(rank)
+    return np.asfortranarray((f1 * c) @ f2.T + noise * rng.standard_normal((n1, n2)))

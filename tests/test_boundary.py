@@ -64,3 +64,18 @@ def test_host_builders_match_oracle():
         pp.Transform.custom(np.eye(4)[:, :2], 0.0)
     with pytest.raises(pp.ArgumentError):
         pp.Transform("data", 4, 2)
+
+
+def test_fp64_only_switch_without_gpu():
+    """The arithmetic switch (ppc_set_ozaki / projprod.set_fp64_only) is host
+    state: it works, and round-trips, without a device."""
+    import paper_2409_19402_b200 as pp
+    was = pp.fp64_only()
+    try:
+        pp.set_fp64_only(True)
+        assert pp.fp64_only()
+        pp.set_fp64_only(False)
+        assert not pp.fp64_only()
+    finally:
+        pp.set_fp64_only(was)
+    assert _lib.lib().ppc_set_ozaki(2) == 3  # PPC_ARGUMENT

@@ -53,10 +53,16 @@ class NumpyBackend:
     def gram_partials(self, A_blk, rows, n3, chunk, nchunks):
         T = A_blk.permute(2, 1, 0).contiguous().numpy().reshape(n3, rows).T
         parts = [T[c * chunk:(c + 1) * chunk].T @ T[c * chunk:(c + 1) * chunk] for c in range(nchunks)]
-        return torch.from_numpy(np.stack([p.reshape(-1) for p in parts]))
+        return torch.from_numpy(np.stack([p.reshape(-1) for p in parts])), not bool(np.isfinite(T).all())
+
+    def release_kept(self):
+        pass
 
     def tree_reduce(self, parts):
         return pdist._tree_finish([parts[i].clone() for i in range(parts.shape[0])])
+
+    def unpack_slices(self, recv, G, ps, nj, n1):
+        return recv.view(G, ps, nj, n1).permute(1, 0, 2, 3).reshape(ps, G * nj, n1)
 
     def sym_eig_top(self, G, n3, p):
         w, V = np.linalg.eigh(G.numpy().reshape(n3, n3))
@@ -240,3 +246,35 @@ def test_star_plan_rejects_uneven_rows():
         pdist.make_star_plan(9, 4, 8, 5, 3, 2, 0)
     assert pdist._slice_groups(5, 3) == [(0, 2), (2, 4), (4, 5)]
     assert pdist._slice_groups(2, 8) == [(0, 1), (1, 2)]
+
+
+def _run_nonfinite(rank, world, port, out_dir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n1, n2, n3, p = 16, 64, 24, 4
+        a = _tensor(n1, n2, n3)
+        a[3, 50, 7] = np.nan  # in rank 1's lateral block only
+        be = NumpyBackend()
+        plan = pdist.make_plan(n1, n2, n3, p, world, rank, be)
+        blk = _ft(a[:, plan.j0:plan.j0 + plan.nj, :])
+        try:
+            pdist.sharded_compress(blk, plan, 3, be)
+            msg = "no error"
+        except pdist.NumericError as ex:
+            msg = "numeric: " + str(ex)
+        with open(os.path.join(out_dir, f"e{rank}.txt"), "w") as f:
+            f.write(msg)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_sharded_compress_nonfinite_fails_every_rank(tmp_path):
+    """matrix_kernels.cpp:32 (non-finite SVD input -> numeric_error) on the
+    whole tensor: a NaN in one rank's block raises NumericError on both."""
+    mp.spawn(_run_nonfinite, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True)
+    for r in range(2):
+        msg = (tmp_path / f"e{r}.txt").read_text()
+        assert msg.startswith("numeric:") and "non-finite" in msg, (r, msg)

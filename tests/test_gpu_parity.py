@@ -414,18 +414,24 @@ def test_large_slice_svd_direct_batched(engine, m, n, batch):
         assert np.linalg.norm(rec - ak) <= 1e-10 * np.linalg.norm(a[:, :, z])
 
 
-def test_large_slice_svd_direct_zero_and_repeated(engine):
-    """Batched direct path with a zero slice, a rank-2 slice (k = 6) and a
-    slice of exactly repeated singular values next to a generic one: values match LAPACK, factors are
-    finite and U, V orthonormal where the values are nonzero."""
+@pytest.mark.parametrize("m,n", [(300, 260), (301, 261), (260, 300)])
+def test_large_slice_svd_direct_zero_and_repeated(engine, m, n):
+    """Large-slice path (even order: batched direct eigensolver; odd: subspace
+    iteration; wide: A A^T) with a zero slice, a rank-2 slice (k = 6 > rank)
+    and a slice of exactly repeated singular values next to a generic one:
+    values match LAPACK and U, V are orthonormal for EVERY slice, as the
+    reference's JacobiSVD factors are (matrix_kernels.cpp:29-37) -- the
+    polish's CholQR2 breaks down on the zero / rank-deficient slices and
+    falls back to CGS2 with an orthonormal completion there."""
     rng = np.random.default_rng(5)
-    m, n, batch, k = 300, 260, 4, 6
+    batch, k = 4, 6
     a = np.zeros((m, n, batch))
     a[:, :, 3] = rng.standard_normal((m, 2)) @ rng.standard_normal((2, n))  # rank 2 < k
     a[:, :, 0] = rng.standard_normal((m, n))
-    qu, _ = np.linalg.qr(rng.standard_normal((m, n)))
-    qv, _ = np.linalg.qr(rng.standard_normal((n, n)))
-    sv = np.concatenate([np.full(10, 3.0), np.linspace(1.0, 0.1, n - 10)])
+    r = min(m, n)
+    qu, _ = np.linalg.qr(rng.standard_normal((m, r)))
+    qv, _ = np.linalg.qr(rng.standard_normal((n, r)))
+    sv = np.concatenate([np.full(10, 3.0), np.linspace(1.0, 0.1, r - 10)])
     a[:, :, 2] = (qu * sv) @ qv.T
     a = np.asfortranarray(a)
     U, s, V = engine.truncated_svd(a, k)
@@ -433,13 +439,16 @@ def test_large_slice_svd_direct_zero_and_repeated(engine):
     for z in range(batch):
         sn = np.linalg.svd(a[:, :, z], compute_uv=False)
         np.testing.assert_allclose(s[:, z], sn[:k], rtol=1e-10, atol=1e-12 * max(1.0, sn[0]))
-    for z in (0, 2):
-        assert np.linalg.norm(U[:, :, z].T @ U[:, :, z] - np.eye(k)) <= 1e-10 * k
-        assert np.linalg.norm(V[:, :, z].T @ V[:, :, z] - np.eye(k)) <= 1e-10 * k
-        rec = (U[:, :, z] * s[:, z]) @ V[:, :, z].T
-        u_, s_, vt_ = np.linalg.svd(a[:, :, z], full_matrices=False)
-        if z == 0:
-            assert np.linalg.norm(rec - (u_[:, :k] * s_[:k]) @ vt_[:k]) <= 1e-10 * np.linalg.norm(a[:, :, z])
+        assert np.linalg.norm(U[:, :, z].T @ U[:, :, z] - np.eye(k)) <= 1e-10 * k, z
+        assert np.linalg.norm(V[:, :, z].T @ V[:, :, z] - np.eye(k)) <= 1e-10 * k, z
+        for j in range(k):  # sign rule (matrix_kernels.cpp:16-25)
+            i = int(np.argmax(np.abs(U[:, j, z])))
+            assert U[i, j, z] >= 0, (z, j)
+        if z != 2:  # z = 2: the k/k+1 boundary sits inside a repeated cluster
+            rec = (U[:, :, z] * s[:, z]) @ V[:, :, z].T
+            u_, s_, vt_ = np.linalg.svd(a[:, :, z], full_matrices=False)
+            want = (u_[:, :k] * s_[:k]) @ vt_[:k]
+            assert np.linalg.norm(rec - want) <= 1e-10 * max(1.0, np.linalg.norm(a[:, :, z])), z
 
 
 @pytest.mark.parametrize("k", [1, 10, 20])
@@ -556,11 +565,21 @@ def test_ws_gram_and_residual_bitwise(engine, oracle):
     assert abs(r1 - re) <= 1e-12 * re
 
 
-def test_compress_host_streaming_matches_device(engine, oracle):
+@pytest.mark.parametrize("n3", [64, 128])
+def test_compress_host_streaming_matches_device(engine, oracle, n3):
     # ppc_tsvdq_compress with host buffers streams A in chunk groups and
     # overlaps the upload with the Gram SYRK; results must equal the
-    # device-resident call bitwise (same chunks, same tree).
-    a = synth.cp_tensor(256, 256, 64, rank=10, noise=1e-3, seed=9)
+    # device-resident call bitwise (same chunks, same tree). n3 = 128: the
+    # plan has 16 chunks of 4096 rows on the INT8 path, uploaded in groups of
+    # 4, 4, 4, 3 and 1 chunks -- every group takes the plan's path, also the
+    # short ones (fewer than 16384 rows).
+    a = synth.cp_tensor(256, 256, n3, rank=10, noise=1e-3, seed=9)
+    if n3 == 128:
+        import ctypes as C
+        from paper_2409_19402_b200 import _lib
+        c, ch = C.c_int64(), C.c_int64()
+        assert _lib.lib().ppc_gram_plan(256 * 256, n3, C.byref(c), C.byref(ch)) == 0
+        assert (c.value, ch.value) == (16, 4096)
     fh, reh = engine.compress_tsvdq(a, 16, 8)
     fd, red = engine.compress_tsvdq(engine.to_device(a), 16, 8)
     assert np.array_equal(fh.transform.q, engine.to_host(fd.transform.q))
@@ -744,15 +763,23 @@ def test_tsvdq2_device_arrays_and_zero(engine, oracle):
 
 
 # ------------------------------------------------------- sharded star-Q (cfg4 §8e)
-@pytest.mark.parametrize("world,groups", [(1, 4), (2, 3), (4, 1)])
-def test_sharded_star_q_rows_bitwise(engine, world, groups):
+CFG4 = (1024, 512, 1024, 256, 64)
+
+
+@pytest.mark.parametrize("world,groups,dims", [(1, 4, None), (2, 3, None), (4, 1, None), (2, 4, CFG4),
+                                              (8, 4, CFG4)])
+def test_sharded_star_q_rows_bitwise(engine, world, groups, dims):
     """Every rank's row block of the sharded product equals the 1-GPU
     ppc_star_q_product rows bitwise. Ranks run one after another on one GPU:
     phase 1 (local transforms) for all ranks, then each rank's finish with a
-    gather that hands back the precomputed B^ groups (no cross-rank waits)."""
+    gather that hands back the precomputed B^ groups (no cross-rank waits).
+    At the cfg4 shape both run the facewise on the INT8 tensor cores (the
+    rank's 128-row blocks and B's columns split exactly as in the 1-GPU
+    product)."""
     import torch
     from paper_2409_19402_b200 import dist as pdist
-    n1, m, n2, n3, p, scale = 96, 80, 128, 40, 12, 0.75
+    n1, m, n2, n3, p = dims or (96, 80, 128, 40, 12)
+    scale = 0.75
     A = synth.gaussian_device(n1, m, n3, 5, 1)
     B = synth.gaussian_device(m, n2, n3, 5, 2)
     Q = engine.to_device(engine.Transform("dct", n3, p).q)
@@ -1269,3 +1296,61 @@ def test_dist_single_rank_kept_digits_matches_fused(engine):
     assert np.array_equal(engine.to_host(Q), f.transform.q)  # same digits, same Gram tree
     np.testing.assert_allclose(engine.to_host(S), engine.to_host(f.s), rtol=1e-12)
     assert abs(re2 - re) <= 1e-12 * re
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_gram_int8_decision_bitwise(engine, world):
+    """the INT8-vs-DMMA choice of the Gram is the plan's, not the
+    call's. 128 x 256 x 128 has 8 chunks of 4096 rows; at 2 and 4 ranks each
+    shard holds 16384 / 8192 rows. Every shard's partials run on the INT8
+    path (as the whole-tensor call), and the rank roots finished by the
+    pairwise tree give Q bitwise equal to the 1-GPU data-driven basis
+    (emulated ranks, one after another, on one GPU)."""
+    import ctypes as C
+    import torch
+    from paper_2409_19402_b200 import _lib, dist as pdist
+    n1, n2, n3, p = 128, 256, 128, 16
+    a = synth.cp_tensor_device(n1, n2, n3, rank=10, noise=1e-3, seed=21)
+    want = engine.data_dependent_transform(a, p).q
+    be = pdist.DeviceBackend("cuda:0")
+    roots = []
+    L = _lib.lib()
+    for r in range(world):
+        plan = pdist.make_plan(n1, n2, n3, p, world, r, be)
+        blk = a[:, plan.j0:plan.j0 + plan.nj, :].permute(2, 1, 0).contiguous().permute(2, 1, 0)
+        buf = C.create_string_buffer(1 << 16)
+        L.ppc_timing_report(buf, len(buf), 1)
+        L.ppc_timing_enable(1)
+        parts, bad = be.gram_partials(blk, n1 * plan.nj, n3, plan.chunk, plan.chunks_per_rank)
+        torch.cuda.synchronize()
+        L.ppc_timing_report(buf, len(buf), 1)
+        L.ppc_timing_enable(0)
+        assert "gram_ozaki" in buf.value.decode(), (r, buf.value.decode())
+        assert not bad
+        be.release_kept()
+        roots.append(be.tree_reduce(parts))
+    Q, _ = be.sym_eig_top(pdist._tree_finish(roots), n3, p)
+    torch.cuda.synchronize()
+    assert np.array_equal(engine.to_host(Q), engine.to_host(want))
+
+
+@pytest.mark.gpu
+def test_sharded_gram_nonfinite_flag(engine):
+    """ppc_gram_partials_keep reports a shard's NaN / Inf (the caller combines
+    the flags over the ranks, matrix_kernels.cpp:32) on both the INT8 and the
+    DMMA Gram paths."""
+    import torch
+    from paper_2409_19402_b200 import dist as pdist
+    be = pdist.DeviceBackend("cuda:0")
+    for n3 in (128, 64):  # INT8 / DMMA partials
+        a = synth.cp_tensor_device(64, 256, n3, rank=5, noise=1e-3, seed=2)
+        chunks, chunk = be.gram_plan(64 * 256, n3)
+        _, bad = be.gram_partials(a, 64 * 256, n3, chunk, chunks)
+        be.release_kept()
+        assert not bad
+        a[5, 100, n3 - 1] = float("inf")
+        _, bad = be.gram_partials(a, 64 * 256, n3, chunk, chunks)
+        be.release_kept()
+        torch.cuda.synchronize()
+        assert bad, n3

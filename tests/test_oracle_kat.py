@@ -357,3 +357,25 @@ def test_matrix_svd_baseline_kats():
     for k in (0, 5):
         with pytest.raises(ValueError):
             ppo.matrix_svd_baseline(A, k)
+
+
+def test_lapack_baseline_matches_oracle():
+    """oracle/baseline.py (the CPU-baseline restatement of the compress chain
+    on LAPACK, bench.py's cpu_baseline / --impl reference for cfg5) is pinned
+    to the C oracle: same basis (captured energies, sign rule), same slice
+    singular values with a shared basis, same relative error."""
+    from oracle import baseline
+    from paper_2409_19402_b200 import synth
+    a = synth.cp_tensor(24, 20, 16, rank=3, noise=1e-2, seed=2)
+    q, U, S, V, re = baseline.compress(a, 6, 3)
+    qo, _, _ = ppo.data_dependent_q(a, 6)
+    T = a.reshape(-1, 16, order="F")
+    np.testing.assert_allclose(np.sum((T @ q) ** 2, axis=0), np.sum((T @ qo) ** 2, axis=0), rtol=1e-10)
+    np.testing.assert_allclose(np.abs(q.T @ qo), np.eye(6), atol=1e-8)  # well-separated spectrum
+    Uo, So, Vo = ppo.tsvdq(a, q, 3)
+    np.testing.assert_allclose(S, So, rtol=1e-10)
+    re_o = ppo.relative_error(a, ppo.tsvdq_reconstruct(Uo, So, Vo, q))
+    assert abs(re - re_o) <= 1e-10 * re_o
+    sec, det = baseline.compress_timed(lambda w: np.asfortranarray(a[:, :w, :]), 24, 20, 16, 6, 3, 5,
+                                       lambda i: np.asfortranarray(a[:, :, i]))
+    assert sec > 0 and det["n_linear_scale"] == 4.0
