@@ -74,18 +74,31 @@ bool facewise_ozaki(const double* Ah, int64_t n1, int64_t m, int64_t p, const do
     if (ldc <= 0) ldc = n1;
     if (strideC <= 0) strideC = n1 * n2;
     if (!ozaki_gemm_eligible(n1, m) || n2 < 64) return false;
+    if (b_ready && b_peak > kOzakiPeakGate) return false;
     StageTimer tm("facewise", s, 2.0 * n1 * m * n2 * p, 8.0 * p * (n1 * m + m * n2 + n1 * n2));
-    if (!b_ready) {
-        Bd.split(Bh, m, m * n2, m, n2, m, p, s);
-        b_peak = ozaki_peak_ratios(Bd, m, n2, s)[0];
-        b_ready = true;
-    }
-    if (b_peak > kOzakiPeakGate) return false;
+    // both operands split and their gate values computed on the device, then
+    // one host read for the decision (B's only with the first row block)
     DeviceBuffer at(sizeof(double) * n1 * m * p);
     launch_transpose(Ah, at.d(), n1, m, p, s);  // (m x n1) per slice
     OzakiDigits Ad;
     Ad.split(at.d(), m, m * n1, m, n1, m, p, s);
-    const std::vector<double> a_peak = ozaki_peak_ratios(Ad, m, kFaceRows, s);
+    const int64_t ng = ozaki_peak_groups(Ad, kFaceRows);
+    DeviceBuffer peaks(sizeof(double) * (ng + 1));
+    ozaki_peak_ratios_async(Ad, m, kFaceRows, peaks.d(), s);
+    if (!b_ready) {
+        Bd.split(Bh, m, m * n2, m, n2, m, p, s);
+        ozaki_peak_ratios_async(Bd, m, n2, peaks.d() + ng, s);
+    }
+    std::vector<double> a_peak((size_t)ng + 1);
+    PPC_CUDA_CHECK(cudaMemcpyAsync(a_peak.data(), peaks.d(), sizeof(double) * (b_ready ? ng : ng + 1),
+                                   cudaMemcpyDeviceToHost, s));
+    PPC_CUDA_CHECK(cudaStreamSynchronize(s));
+    if (!b_ready) {
+        b_peak = a_peak[ng];
+        b_ready = true;
+    }
+    a_peak.resize((size_t)ng);
+    if (b_peak > kOzakiPeakGate) return false;
     // a short last block runs on DMMA too, as it does as its own host-pipeline call
     auto int8_rows = [&](size_t g) {
         return a_peak[g] <= kOzakiPeakGate && n1 - (int64_t)g * kFaceRows >= kFaceRows;

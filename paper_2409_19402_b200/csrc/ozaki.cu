@@ -715,14 +715,21 @@ __global__ void peak_ratio_kernel(const double* __restrict__ sc, const double* _
 }
 }  // namespace
 
-std::vector<double> ozaki_peak_ratios(const OzakiDigits& d, int64_t K, int64_t group, cudaStream_t s) {
-    const int64_t ng = (d.cols + group - 1) / group;
-    std::vector<double> h((size_t)ng);
-    DeviceBuffer out(sizeof(double) * ng);
+int64_t ozaki_peak_groups(const OzakiDigits& d, int64_t group) { return (d.cols + group - 1) / group; }
+
+void ozaki_peak_ratios_async(const OzakiDigits& d, int64_t K, int64_t group, double* out, cudaStream_t s) {
+    const int64_t ng = ozaki_peak_groups(d, group);
     peak_ratio_kernel<<<(unsigned)ng, 256, 0, s>>>(d.sc.d(), d.sq.d(), d.nblk, d.cols, std::sqrt((double)K), group,
-                                                  out.d());
+                                                  out);
     count_launch();
     check_launch("peak_ratio");
+}
+
+std::vector<double> ozaki_peak_ratios(const OzakiDigits& d, int64_t K, int64_t group, cudaStream_t s) {
+    const int64_t ng = ozaki_peak_groups(d, group);
+    std::vector<double> h((size_t)ng);
+    DeviceBuffer out(sizeof(double) * ng);
+    ozaki_peak_ratios_async(d, K, group, out.d(), s);
     PPC_CUDA_CHECK(cudaMemcpyAsync(h.data(), out.d(), sizeof(double) * ng, cudaMemcpyDeviceToHost, s));
     PPC_CUDA_CHECK(cudaStreamSynchronize(s));
     return h;

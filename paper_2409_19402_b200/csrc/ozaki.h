@@ -52,6 +52,9 @@ bool ozaki_gram_eligible(int64_t n3, int64_t chunk);
 // `group` consecutive columns of d, an upper bound (< 2x) on the largest
 // peak ratio over all its blocks (one host sync).
 std::vector<double> ozaki_peak_ratios(const OzakiDigits& d, int64_t K, int64_t group, cudaStream_t s);
+// the same into device memory (out: ozaki_peak_groups(d, group) doubles), no sync
+int64_t ozaki_peak_groups(const OzakiDigits& d, int64_t group);
+void ozaki_peak_ratios_async(const OzakiDigits& d, int64_t K, int64_t group, double* out, cudaStream_t s);
 constexpr double kOzakiPeakGate = 16.0;  // products whose operands exceed it run on FP64 DMMA
 // Whether the integer path applies to an output with M rows and K-length sums.
 bool ozaki_gemm_eligible(int64_t M, int64_t K);

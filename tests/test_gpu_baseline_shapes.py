@@ -174,7 +174,9 @@ def test_cfg3_full_shared_q_vs_oracle(engine, blas_oracle):
     da = engine.to_device(a)
     with Stages() as st:
         f, re = engine.compress_tsvdq(da, 32, 16)
-    assert {"gram_ozaki", "ozaki_fwd", "ozaki_syrk_batched"} <= st.names, st.names
+    # at cfg3 only Q's Gram is INT8-eligible (n3 >= 128, 4096-row chunks): the
+    # forward transform needs p % 64 == 0 and the slice Grams >= 1024 rows
+    assert "gram_ozaki" in st.names and "eig.tridiag" in st.names, st.names
     q = engine.to_host(f.transform.q)
     T = a.reshape(-1, 224, order="F")
     lam = np.sort(np.linalg.eigvalsh(T.T @ T))[::-1][:32]
