@@ -74,15 +74,22 @@ static_assert(kBN / 2 == 40, "epilogue column split (32 + 8)");
 // [cp*chunk + u*KC, min(cp*chunk + (u+1)*KC, (cp+1)*chunk, rows)). Batched
 // mode: block b is the first min(KC, rows) rows of X + b*stride.
 // D layout: [(b*S + s)*cols + j][KCp] bytes; scale[b*cols + j].
-template <int ND>
+// CPB columns per CTA (CPB * KCp <= 4096): 256 / CPB threads per column, so
+// short blocks (the facewise / filter operands, K = 512 .. 2048) still keep
+// 16 loads per thread in flight.
+template <int ND, int CPB>
 __global__ void __launch_bounds__(256) ozaki_split_kernel(const double* __restrict__ X, int64_t ldx, int64_t stride,
                                                           int64_t rows, int64_t cols, int64_t KC, int64_t KCp,
                                                           int64_t chunk, int64_t per, int8_t* __restrict__ D,
                                                           double* __restrict__ scale, double* __restrict__ sumsq,
                                                           const int* __restrict__ zmap, int* __restrict__ nonfinite,
                                                           const double* __restrict__ fixed_max) {
+    constexpr int TPC = 256 / CPB;  // threads per column
+    constexpr int WPC = TPC / 32;   // warps per column
     __shared__ double stage[kKC];
-    const int64_t j = blockIdx.x;
+    const int cc = threadIdx.x / TPC, lt = threadIdx.x % TPC;
+    const int64_t j = (int64_t)blockIdx.x * CPB + cc;
+    const bool live = j < cols;
     const int64_t b = zmap ? zmap[blockIdx.y] : blockIdx.y;
     int64_t r0, len;
     if (stride) {
@@ -94,23 +101,26 @@ __global__ void __launch_bounds__(256) ozaki_split_kernel(const double* __restri
         const int64_t end = std::min<int64_t>(std::min<int64_t>(r0 + KC, (cp + 1) * chunk), rows);
         len = std::max<int64_t>(0, end - r0);
     }
-    const double* col = X + (stride ? b * stride : 0) + j * ldx + r0;
+    if (!live) len = 0;
+    const double* col = X + (stride ? b * stride : 0) + (live ? j : 0) * ldx + r0;
+    double* stg = stage + cc * (kKC / CPB);
     // all 16 loads of a thread in flight before any use (the kernel is
     // DRAM-latency bound); same per-thread summation order as a strided loop
     double mx = 0.0, ss = 0.0;
-    double v[kKC / 256];
+    constexpr int NL = kKC / 256;
+    double v[NL];
 #pragma unroll
-    for (int q = 0; q < kKC / 256; ++q) {
-        const int64_t i = threadIdx.x + 256 * q;
+    for (int q = 0; q < NL; ++q) {
+        const int64_t i = lt + TPC * q;
         v[q] = i < len ? __ldcs(col + i) : 0.0;
     }
 #pragma unroll
-    for (int q = 0; q < kKC / 256; ++q) {
-        stage[threadIdx.x + 256 * q] = v[q];
+    for (int q = 0; q < NL; ++q) {
+        stg[lt + TPC * q] = v[q];
         mx = fmax(mx, fabs(v[q]));
         ss = fma(v[q], v[q], ss);
     }
-    // block max and (fixed-order) sum of squares: the Gram diagonal in FP64
+    // column max and (fixed-order) sum of squares: the Gram diagonal in FP64
     __shared__ double red[8], red2[8];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -122,27 +132,29 @@ __global__ void __launch_bounds__(256) ozaki_split_kernel(const double* __restri
         red2[threadIdx.x >> 5] = ss;
     }
     __syncthreads();
-    if (threadIdx.x < 32) {
-        mx = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
-        ss = threadIdx.x < (blockDim.x >> 5) ? red2[threadIdx.x] : 0.0;
+    __shared__ double colmax[CPB];
+    if (lt < 32) {
+        mx = lt < WPC ? red[cc * WPC + lt] : 0.0;
+        ss = lt < WPC ? red2[cc * WPC + lt] : 0.0;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
             ss += __shfl_xor_sync(0xffffffffu, ss, o);
         }
-        if (threadIdx.x == 0) {
-            red[0] = mx;
-            sumsq[b * cols + j] = ss;
+        if (lt == 0) {
+            colmax[cc] = mx;
+            if (live) sumsq[b * cols + j] = ss;
             // the caller's finiteness check rides on this pass over the input:
             // an Inf makes the max Inf, a NaN makes the sum of squares NaN
-            if (nonfinite && (!(mx <= 1.7976931348623157e308) || isnan(ss))) *nonfinite = 1;
+            if (live && nonfinite && (!(mx <= 1.7976931348623157e308) || isnan(ss))) *nonfinite = 1;
         }
     }
     __syncthreads();
-    mx = fixed_max ? fixed_max[b] : red[0];  // a block-wide bound: one scale for every column
+    if (!live) return;
+    mx = fixed_max ? fixed_max[b] : colmax[cc];  // a block-wide bound: one scale for every column
     // sigma = 2^e > 2 max |x| (mx = 0: all digits zero)
     const int e = mx > 0.0 ? ilogb(mx) + 2 : 0;
-    if (threadIdx.x == 0) scale[b * cols + j] = mx > 0.0 ? ldexp(1.0, e) : 0.0;
+    if (lt == 0) scale[b * cols + j] = mx > 0.0 ? ldexp(1.0, e) : 0.0;
     int8_t* out = D + ((b * ND) * cols + j) * KCp;
     const int64_t plane = cols * KCp;
     // Integer digit extraction with SH = 8 (ND - 1): y = rint(2^SH * 128 x / sigma)
@@ -154,14 +166,14 @@ __global__ void __launch_bounds__(256) ozaki_split_kernel(const double* __restri
     // 2^(SH+7-e) as two finite factors: e may be near -1074 (subnormal columns)
     const int e1 = (SH + 7 - e) / 2;
     const double scl1 = mx > 0.0 ? ldexp(1.0, e1) : 0.0, scl2 = ldexp(1.0, SH + 7 - e - e1);
-    for (int64_t i4 = (int64_t)threadIdx.x * 4; i4 < KCp; i4 += (int64_t)blockDim.x * 4) {
+    for (int64_t i4 = (int64_t)lt * 4; i4 < KCp; i4 += (int64_t)TPC * 4) {
         uint32_t w[ND];
 #pragma unroll
         for (int s = 0; s < ND; ++s) w[s] = 0u;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const int64_t i = i4 + q;
-            const long long y = i < len ? __double2ll_rn(stage[i] * scl1 * scl2) : 0LL;
+            const long long y = i < len ? __double2ll_rn(stg[i] * scl1 * scl2) : 0LL;
             const long long U = y + (long long)C80;
             const uint64_t low = (uint64_t)U ^ C80;
             w[0] |= (uint32_t)(uint8_t)(int8_t)(U >> SH) << (8 * q);
@@ -622,16 +634,24 @@ void OzakiDigits::split(const double* X, int64_t ldx, int64_t stride, int64_t ro
     if (launched <= 0) return;
     const double total_rows = stride ? (double)std::min(KC, rows) * launched : (double)rows;
     StageTimer ts("ozaki_split", s, 0.0, 8.0 * total_rows * cols + (double)nd * total_rows * cols);
-    dim3 grid((unsigned)cols, (unsigned)launched);
     int8_t* D0 = D.as<int8_t>() + (size_t)block_base * nd * cols * KCp;
     double* sc0 = sc.d() + block_base * cols;
     double* sq0 = sq.d() + block_base * cols;
-    if (nd == kSmax)
-        ozaki_split_kernel<kSmax><<<grid, 256, 0, s>>>(X, ldx, stride, rows, cols, KC, KCp, chunk ? chunk : KC,
-                                                       per ? per : 1, D0, sc0, sq0, zmap, nonfinite, fixed_max);
-    else
-        ozaki_split_kernel<kS><<<grid, 256, 0, s>>>(X, ldx, stride, rows, cols, KC, KCp, chunk ? chunk : KC,
-                                                    per ? per : 1, D0, sc0, sq0, zmap, nonfinite, fixed_max);
+    // columns per CTA: as many KCp-long columns as fit the 4096-element stage
+    const int cpb = KCp <= 512 ? 8 : (KCp <= 1024 ? 4 : (KCp <= 2048 ? 2 : 1));
+    dim3 grid((unsigned)((cols + cpb - 1) / cpb), (unsigned)launched);
+    const int64_t ch = chunk ? chunk : KC, pr = per ? per : 1;
+#define PPC_SPLIT(ND_, CPB_)                                                                                         \
+    ozaki_split_kernel<ND_, CPB_><<<grid, 256, 0, s>>>(X, ldx, stride, rows, cols, KC, KCp, ch, pr, D0, sc0, sq0,    \
+                                                       zmap, nonfinite, fixed_max)
+    if (nd == kSmax) {
+        if (cpb == 8) PPC_SPLIT(kSmax, 8); else if (cpb == 4) PPC_SPLIT(kSmax, 4);
+        else if (cpb == 2) PPC_SPLIT(kSmax, 2); else PPC_SPLIT(kSmax, 1);
+    } else {
+        if (cpb == 8) PPC_SPLIT(kS, 8); else if (cpb == 4) PPC_SPLIT(kS, 4);
+        else if (cpb == 2) PPC_SPLIT(kS, 2); else PPC_SPLIT(kS, 1);
+    }
+#undef PPC_SPLIT
     count_launch();
     check_launch("ozaki_split");
 }
@@ -693,25 +713,20 @@ namespace {
 // (sc/2) sqrt(K) / ||x||: sc/2 bounds max|x| from above (sc in (2, 4] max|x|),
 // so this is >= the column's peak ratio max|x| sqrt(K) / ||x||_2 and < twice
 // it; zero columns count 0.
-__global__ void peak_ratio_kernel(const double* __restrict__ sc, const double* __restrict__ sq, int64_t nblk,
-                                  int64_t cols, double sqrtK, int64_t group, double* __restrict__ out) {
-    const int64_t g = blockIdx.x;
+__global__ void peak_ratio_kernel(const double* __restrict__ sc, const double* __restrict__ sq, int64_t cols,
+                                  double sqrtK, int64_t group, unsigned long long* __restrict__ out) {
+    // CTA (g, b): the columns of group g in block b; max over CTAs by an
+    // atomic max of the (non-negative) bit patterns: order-independent
+    const int64_t g = blockIdx.x, b = blockIdx.y;
     const int64_t c0 = g * group, c1 = std::min<int64_t>(c0 + group, cols);
     double mx = 0.0;
-    for (int64_t b = 0; b < nblk; ++b)
-        for (int64_t c = c0 + threadIdx.x; c < c1; c += blockDim.x) {
-            const double q = sq[b * cols + c];
-            if (q > 0.0) mx = fmax(mx, 0.5 * sc[b * cols + c] * sqrtK / sqrt(q));
-        }
-    __shared__ double red[8];
+    for (int64_t c = c0 + threadIdx.x; c < c1; c += blockDim.x) {
+        const double q = sq[b * cols + c];
+        if (q > 0.0) mx = fmax(mx, 0.5 * sc[b * cols + c] * sqrtK / sqrt(q));
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) mx = fmax(mx, red[w]);
-        out[g] = fmax(mx, red[0]);
-    }
+    if ((threadIdx.x & 31) == 0 && mx > 0.0) atomicMax(out + g, (unsigned long long)__double_as_longlong(mx));
 }
 }  // namespace
 
@@ -719,8 +734,9 @@ int64_t ozaki_peak_groups(const OzakiDigits& d, int64_t group) { return (d.cols 
 
 void ozaki_peak_ratios_async(const OzakiDigits& d, int64_t K, int64_t group, double* out, cudaStream_t s) {
     const int64_t ng = ozaki_peak_groups(d, group);
-    peak_ratio_kernel<<<(unsigned)ng, 256, 0, s>>>(d.sc.d(), d.sq.d(), d.nblk, d.cols, std::sqrt((double)K), group,
-                                                  out);
+    PPC_CUDA_CHECK(cudaMemsetAsync(out, 0, sizeof(double) * ng, s));  // +0.0
+    peak_ratio_kernel<<<dim3((unsigned)ng, (unsigned)d.nblk), 256, 0, s>>>(
+        d.sc.d(), d.sq.d(), d.cols, std::sqrt((double)K), group, reinterpret_cast<unsigned long long*>(out));
     count_launch();
     check_launch("peak_ratio");
 }

@@ -235,8 +235,15 @@ bool data_q(const double* T, int64_t N, int64_t n3, int64_t p, double* Q, double
 void slice_svd(const double* A, int64_t m, int64_t n, int64_t stride, int64_t batch, int64_t k,
                double* U, double* S, double* V, double* tail2, cudaStream_t s) {
     const int64_t r = std::min(m, n);
-    if (r <= kSubspaceMinN || jacobi_smem_bytes(m, n) <= 200 * 1024 || k > r / 2) {
+    if (r <= kSubspaceMinN || jacobi_smem_bytes(m, n) <= 200 * 1024) {
         jacobi_svd(A, m, n, stride, batch, k, U, S, V, tail2, s);
+        return;
+    }
+    if (k > r / 2) {  // most of the spectrum (tsvdq2: all of it): blocked one-sided Jacobi
+        if (block_jacobi_eligible(m, n, k))
+            block_jacobi_svd(A, m, n, stride, batch, k, U, S, V, tail2, s);
+        else
+            jacobi_svd(A, m, n, stride, batch, k, U, S, V, tail2, s);
         return;
     }
     subspace_svd(A, m, n, stride, batch, k, U, S, V, tail2, s);

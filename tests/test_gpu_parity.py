@@ -1312,7 +1312,9 @@ def test_sharded_gram_int8_decision_bitwise(engine, world):
     from paper_2409_19402_b200 import _lib, dist as pdist
     n1, n2, n3, p = 128, 256, 128, 16
     a = synth.cp_tensor_device(n1, n2, n3, rank=10, noise=1e-3, seed=21)
-    want = engine.data_dependent_transform(a, p).q
+    # the compress chain keeps the Gram's 7-digit split for the forward
+    # transform, as the shards' ppc_gram_partials_keep does
+    want = engine.compress_tsvdq(a, p, 4)[0].transform.q
     be = pdist.DeviceBackend("cuda:0")
     roots = []
     L = _lib.lib()
@@ -1354,3 +1356,98 @@ def test_sharded_gram_nonfinite_flag(engine):
         be.release_kept()
         torch.cuda.synchronize()
         assert bad, n3
+
+
+# ------------------------------------- block one-sided Jacobi (large k, K6b)
+def _graded(m, n, rng, lo):
+    r = min(m, n)
+    qu, _ = np.linalg.qr(rng.standard_normal((m, r)))
+    qv, _ = np.linalg.qr(rng.standard_normal((n, r)))
+    return (qu * np.geomspace(1.0, lo, r)) @ qv.T
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m,n,k", [(300, 260, 260), (260, 300, 200), (520, 500, 400)])
+def test_block_jacobi_vs_lapack(engine, m, n, k):
+    """Slices too large for the one-CTA Jacobi that keep k > r/2 triplets go to
+    the blocked one-sided Jacobi (block_jacobi.cu): singular values as LAPACK
+    (relative 1e-10 down to 1e-6 sigma_1, also on a graded spectrum), U and V
+    orthonormal, the rank-k reconstruction, the sign rule, and a zero and a
+    rank-deficient slice (orthonormal completion for zero values)."""
+    import ctypes as C
+    from paper_2409_19402_b200 import _lib
+    rng = np.random.default_rng(m + n + k)
+    batch = 4
+    a = np.zeros((m, n, batch))
+    a[:, :, 0] = rng.standard_normal((m, n))
+    a[:, :, 1] = _graded(m, n, rng, 1e-8)
+    a[:, :, 2] = rng.standard_normal((m, 7)) @ rng.standard_normal((7, n))  # rank 7 < k
+    a = np.asfortranarray(a)  # slice 3: zero
+    L = _lib.lib()
+    buf = C.create_string_buffer(1 << 16)
+    L.ppc_timing_report(buf, len(buf), 1)
+    L.ppc_timing_enable(1)
+    U, s, V = engine.truncated_svd(a, k)
+    L.ppc_timing_report(buf, len(buf), 1)
+    L.ppc_timing_enable(0)
+    assert "block_jacobi" in buf.value.decode(), buf.value.decode()
+    for z in range(batch):
+        u_, sn, vt_ = np.linalg.svd(a[:, :, z], full_matrices=False)
+        big = sn[:k] >= 1e-6 * max(sn[0], 1e-300)
+        np.testing.assert_allclose(s[big, z], sn[:k][big], rtol=1e-10)
+        assert np.all(np.abs(s[:, z] - sn[:k]) <= 1e-13 * max(1.0, sn[0])), z
+        assert np.linalg.norm(U[:, :, z].T @ U[:, :, z] - np.eye(k)) <= 1e-10 * k, z
+        assert np.linalg.norm(V[:, :, z].T @ V[:, :, z] - np.eye(k)) <= 1e-10 * k, z
+        rec = (U[:, :, z] * s[:, z]) @ V[:, :, z].T
+        want = (u_[:, :k] * sn[:k]) @ vt_[:k]
+        assert np.linalg.norm(rec - want) <= 1e-10 * max(1.0, np.linalg.norm(a[:, :, z])), z
+        for j in range(k):
+            i = int(np.argmax(np.abs(U[:, j, z])))
+            assert U[i, j, z] >= 0, (z, j)
+
+
+def _tsvdq2_select(s_all, gamma):
+    """decompositions.cpp:137-167 restated: values above 1e-12 of the global
+    max, sorted descending (ties: slice, then position), the shortest prefix
+    whose energy reaches gamma of the total."""
+    r, p = s_all.shape
+    cutoff = 1e-12 * s_all[0].max()
+    pool = sorted(((-s_all[j, i], i, j) for i in range(p) for j in range(r) if s_all[j, i] > cutoff))
+    e = np.cumsum([v * v for v, _, _ in pool])
+    K = min(int(np.searchsorted(e, gamma * e[-1], side="left")) + 1, len(pool))
+    mr = np.zeros(p, dtype=np.int64)
+    for _, i, _ in pool[:K]:
+        mr[i] += 1
+    return mr
+
+
+@pytest.mark.gpu
+def test_tsvdq2_large_slices_vs_lapack(engine):
+    """tsvdq2 (k = r for every slice) on 1024^2 slices finishes in seconds on
+    the blocked Jacobi and matches LAPACK: full spectra, the multirank
+    selection, and the reconstruction of the kept triplets."""
+    import time
+    rng = np.random.default_rng(77)
+    n1 = n2 = 1024
+    n3, p, gamma = 6, 4, 0.9
+    a = np.asfortranarray(rng.standard_normal((n1, n2, n3)) +
+                          np.einsum("ir,jr,kr->ijk", rng.standard_normal((n1, 20)), rng.standard_normal((n2, 20)),
+                                    rng.standard_normal((n3, 20))))
+    t = engine.Transform("dct", n3, p)
+    t0 = time.time()
+    f = engine.tsvdq2(engine.to_device(a), t, gamma)
+    s_all = engine.to_host(f.s)
+    assert time.time() - t0 < 60
+    ah = np.einsum("ijk,kl->ijl", a, t.q)
+    sn = np.stack([np.linalg.svd(ah[:, :, i], compute_uv=False) for i in range(p)], axis=1)
+    mr = np.asarray(f.multirank)
+    assert np.array_equal(mr, _tsvdq2_select(sn, gamma))
+    for i in range(p):  # kept values (the factors are zero beyond multirank[i])
+        np.testing.assert_allclose(s_all[:mr[i], i], sn[:mr[i], i], rtol=1e-10)
+        assert not s_all[mr[i]:, i].any()
+    u, v = engine.to_host(f.u), engine.to_host(f.v)
+    for i in range(p):
+        kk = int(f.multirank[i])
+        uu, ss, vt = np.linalg.svd(ah[:, :, i], full_matrices=False)
+        rec = (u[:, :kk, i] * s_all[:kk, i]) @ v[:, :kk, i].T
+        assert np.linalg.norm(rec - (uu[:, :kk] * ss[:kk]) @ vt[:kk]) <= 1e-10 * np.linalg.norm(ah[:, :, i])
