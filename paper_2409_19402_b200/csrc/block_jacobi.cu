@@ -266,7 +266,7 @@ __global__ void __launch_bounds__(256) complete_zero_kernel(double* __restrict__
     double* x = X + b * rows * k;
     double* rm = rowm + b * rows;
     __shared__ double red[33];
-    __shared__ double cf[1024];
+    extern __shared__ double cf[];  // k projection coefficients
     __shared__ int64_t tmin;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
     auto bsum = [&](double v) {
@@ -310,12 +310,12 @@ __global__ void __launch_bounds__(256) complete_zero_kernel(double* __restrict__
                     for (int64_t t = lane; t < rows; t += 32) a = fma(x[t + q * rows], v[t], a);
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-                if (lane == 0 && q < 1024) cf[q] = (q != j && (sb[q] > 0.0 || q < j)) ? a : 0.0;
+                if (lane == 0) cf[q] = (q != j && (sb[q] > 0.0 || q < j)) ? a : 0.0;
             }
             __syncthreads();
             for (int64_t t = tid; t < rows; t += blockDim.x) {
                 double y = v[t];
-                for (int64_t q = 0; q < k && q < 1024; ++q) y = fma(-x[t + q * rows], cf[q], y);
+                for (int64_t q = 0; q < k; ++q) y = fma(-x[t + q * rows], cf[q], y);
                 v[t] = y;
             }
         }
@@ -335,7 +335,7 @@ __global__ void __launch_bounds__(256) complete_zero_kernel(double* __restrict__
 
 bool block_jacobi_eligible(int64_t m, int64_t n, int64_t k) {
     const int64_t C = std::min(m, n);
-    return k <= 1024 && C >= 2 * kBW && C <= 8192;
+    return k <= C && C >= 2 * kBW && C <= 8192;
 }
 
 void block_jacobi_svd(const double* A, int64_t m, int64_t n, int64_t strideA, int64_t batch, int64_t k, double* U,
@@ -387,9 +387,13 @@ void block_jacobi_svd(const double* A, int64_t m, int64_t n, int64_t strideA, in
                                                       ord.as<int>(), m, n);
     count_launch();
     check_launch("bj_finalize");
-    complete_zero_kernel<<<(unsigned)batch, 256, 0, s>>>(U, m, k, S, rowm.d());
+    const size_t czs = sizeof(double) * (size_t)k;  // k <= 8192: <= 64 KB
+    if (czs > 48 * 1024)
+        PPC_CUDA_CHECK(cudaFuncSetAttribute(complete_zero_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)czs));
+    complete_zero_kernel<<<(unsigned)batch, 256, czs, s>>>(U, m, k, S, rowm.d());
     count_launch();
-    complete_zero_kernel<<<(unsigned)batch, 256, 0, s>>>(V, n, k, S, rowm.d());
+    complete_zero_kernel<<<(unsigned)batch, 256, czs, s>>>(V, n, k, S, rowm.d());
     count_launch();
     check_launch("complete_zero");
     sign_rule(U, m, k, batch, V, n, s);  // matrix_kernels.cpp:16-25

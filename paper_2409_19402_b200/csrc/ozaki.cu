@@ -212,11 +212,12 @@ struct OzParams {
 };
 
 // tile t (upper-triangle order) -> (mb, nb): column tile nb holds
-// min(floor((nb*kBN + kBN - 1) / kBM) + 1, mtiles) row tiles.
+// min(floor((nb*BN + BN - 1) / kBM) + 1, mtiles) row tiles.
+template <int BN>
 __device__ __forceinline__ void tri_tile(int64_t t, int64_t mtiles, int64_t& mb, int64_t& nb) {
     nb = 0;
     for (;;) {
-        const int64_t cnt = std::min<int64_t>((nb * kBN + kBN - 1) / kBM + 1, mtiles);
+        const int64_t cnt = std::min<int64_t>((nb * BN + BN - 1) / kBM + 1, mtiles);
         if (t < cnt) break;
         t -= cnt;
         ++nb;
@@ -226,12 +227,12 @@ __device__ __forceinline__ void tri_tile(int64_t t, int64_t mtiles, int64_t& mb,
 
 
 // Work item -> (output block ob, row tile mb, column tile nb).
-template <bool SYM>
+template <bool SYM, int BN = kBN>
 __device__ __forceinline__ void decode_item(const OzParams& P, int64_t item, int64_t& ob, int64_t& mb, int64_t& nb) {
     const int64_t bi = item / P.tiles;
     ob = P.zmap ? P.zmap[bi] : bi;
     if (SYM) {
-        tri_tile(item - bi * P.tiles, P.mtiles, mb, nb);
+        tri_tile<BN>(item - bi * P.tiles, P.mtiles, mb, nb);
     } else {
         const int64_t t = item - bi * P.tiles;
         mb = t % P.mtiles;
@@ -292,7 +293,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             int64_t g = 0;  // stage counter across items
             for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
                 int64_t ob, mb, nb;
-                decode_item<SYM>(P, item, ob, mb, nb);
+                decode_item<SYM, BN>(P, item, ob, mb, nb);
                 for (int64_t gl = 0; gl < per * nkc; ++gl, ++g) {
                     const int st = (int)(g % STG);
                     bar_wait(&empty[st], (uint32_t)(((g / STG) & 1) ^ 1));
@@ -336,7 +337,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             int64_t mb_item = 0;
             if (SYMA) {
                 int64_t ob_, nb_;
-                decode_item<SYM>(P, item, ob_, mb_item, nb_);
+                decode_item<SYM, BN>(P, item, ob_, mb_item, nb_);
             }
             for (int64_t cc = 0; cc < per; ++cc, ++cg) {
                 if (cg > 0) {  // the epilogue has drained the previous block's levels
@@ -387,7 +388,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         double rsd = 0.0, rsx = 0.0;  // RESID: this thread's residual sums
         for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
             int64_t ob, mb, nb;
-            decode_item<SYM>(P, item, ob, mb, nb);
+            decode_item<SYM, BN>(P, item, ob, mb, nb);
             const int64_t m = mb * kBM + q * 32 + lane;
             const int64_t n0 = nb * BN + h * NH;
             const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(h * NH);
@@ -569,11 +570,11 @@ void launch_mma(const CUtensorMap& ma, const CUtensorMap& mb, const OzParams& P,
     check_launch("ozaki_mma");
 }
 
-int64_t tri_tiles(int64_t n) {
+int64_t tri_tiles(int64_t n, int64_t bn = kBN) {
     const int64_t mtiles = (n + kBM - 1) / kBM;
     int64_t tiles = 0;
-    for (int64_t nb = 0; nb < (n + kBN - 1) / kBN; ++nb)
-        tiles += std::min<int64_t>((nb * kBN + kBN - 1) / kBM + 1, mtiles);
+    for (int64_t nb = 0; nb < (n + bn - 1) / bn; ++nb)
+        tiles += std::min<int64_t>((nb * bn + bn - 1) / kBM + 1, mtiles);
     return tiles;
 }
 
@@ -583,14 +584,17 @@ void ozaki_syrk(const OzakiDigits& d, int64_t nout, int64_t per, double* out, cu
                 double rows_total, int64_t block_base = 0) {
     // the nout * per blocks from block_base on
     const int8_t* D0 = d.D.as<int8_t>() + (size_t)block_base * d.nd * d.cols * d.KCp;
+    // output tile width: 80 (6 x 80 TMEM columns, 2 ring stages) or 64
+    // (3 stages; PPC_SYRK_BN=64)
+    static const int bn = (std::getenv("PPC_SYRK_BN") && std::atoi(std::getenv("PPC_SYRK_BN")) == 64) ? 64 : kBN;
     CUtensorMap ma, mb;
     if (!make_digit_map(&ma, D0, d.KCp, d.cols, nout * per * d.nd, kBM) ||
-        !make_digit_map(&mb, D0, d.KCp, d.cols, nout * per * d.nd, kBN))
+        !make_digit_map(&mb, D0, d.KCp, d.cols, nout * per * d.nd, bn))
         fail(PPC_CUDA, "ozaki: tensor map encoding failed");
     OzParams P;
     P.M = P.N = d.cols;
     P.mtiles = (d.cols + kBM - 1) / kBM;
-    P.tiles = tri_tiles(d.cols);
+    P.tiles = tri_tiles(d.cols, bn);
     P.KCp = d.KCp;
     P.per = per;
     P.nd = d.nd;
@@ -606,7 +610,10 @@ void ozaki_syrk(const OzakiDigits& d, int64_t nout, int64_t per, double* out, cu
     // int8 ops of the 21 digit-pair products over the upper triangle
     StageTimer tk(stage, s, 2.0 * kS * (kS + 1) / 2 * rows_total * d.cols * d.cols / 2,
                   (double)kS * rows_total * d.cols);
-    launch_mma<true>(ma, mb, P, nout * P.tiles, s);
+    if (bn == 64)
+        launch_mma<true, false, false, 64>(ma, mb, P, nout * P.tiles, s);
+    else
+        launch_mma<true>(ma, mb, P, nout * P.tiles, s);
 }
 
 }  // namespace

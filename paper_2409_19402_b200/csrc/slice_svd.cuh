@@ -40,7 +40,7 @@ void slice_tail_energy(const double* A, int64_t m, int64_t n, int64_t stride, in
                        int64_t k, const double* U, const double* S, const double* V, double* tail2,
                        cudaStream_t s);
 // Block one-sided Jacobi SVD (block_jacobi.cu) for large slices that keep
-// k > r/2 triplets (tsvdq2: k = r): C = min(m, n) in [64, 8192], k <= 1024.
+// k > r/2 triplets (tsvdq2: k = r): C = min(m, n) in [64, 8192].
 bool block_jacobi_eligible(int64_t m, int64_t n, int64_t k);
 void block_jacobi_svd(const double* A, int64_t m, int64_t n, int64_t strideA, int64_t batch, int64_t k, double* U,
                       double* S, double* V, double* tail2, cudaStream_t s);
