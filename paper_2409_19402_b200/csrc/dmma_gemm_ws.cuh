@@ -103,8 +103,17 @@ __device__ __forceinline__ void ws_tile(const WsParams& P, int64_t w, int64_t& b
     }
 }
 
+// EPI_TSTORE: the plain store (beta = 0, no split, no mirror) through shared
+// memory and a TMA bulk tensor store issued by a dedicated store warp, so the
+// consumers start the next tile's MMAs while the previous tile drains to HBM
+// (short-K products: the epilogue is a third of the tile's time otherwise).
+enum { EPI_TSTORE = 2 };
+
+template <int BM, int BN, int WARPS_M, int WARPS_N, int EPI>
+constexpr int ws_threads() { return (WARPS_M * WARPS_N + 1 + (EPI == EPI_TSTORE ? 1 : 0)) * 32; }
+
 template <int BM, int BN, int BK, int WARPS_M, int WARPS_N, int STAGES, bool AK, bool BNM, int EPI>
-__global__ void __launch_bounds__((WARPS_M * WARPS_N + 1) * 32, 1)
+__global__ void __launch_bounds__(ws_threads<BM, BN, WARPS_M, WARPS_N, EPI>(), 1)
     dmma_gemm_ws_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                         const __grid_constant__ CUtensorMap mapX, const WsParams P) {
     constexpr int NCW = WARPS_M * WARPS_N;  // consumer warps
@@ -115,8 +124,9 @@ __global__ void __launch_bounds__((WARPS_M * WARPS_N + 1) * 32, 1)
     double* As = reinterpret_cast<double*>(smem_raw);
     double* Bs = As + STAGES * BM * BK;
     // RESID: the tile's reference block X (BN columns of BM rows, [n][m])
-    // is staged by TMA right after the operand ring
-    constexpr bool XS = (EPI == EPI_RESID);
+    // is staged by TMA right after the operand ring; TSTORE: the output tile
+    // ([n][m]) on its way to the TMA store
+    constexpr bool XS = (EPI == EPI_RESID) || (EPI == EPI_TSTORE);
     double* Xs = Bs + STAGES * BK * BN;
     uint64_t* full = reinterpret_cast<uint64_t*>(Xs + (XS ? BM * BN : 0));
     uint64_t* empty = full + STAGES;
@@ -129,14 +139,44 @@ __global__ void __launch_bounds__((WARPS_M * WARPS_N + 1) * 32, 1)
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], NCW);
         }
-        if constexpr (XS) {
+        if constexpr (EPI == EPI_RESID) {
             mbar_init(xfull, 1);
             mbar_init(xempty, NCW);
+        }
+        if constexpr (EPI == EPI_TSTORE) {
+            mbar_init(xfull, NCW);  // consumers wrote the tile
+            mbar_init(xempty, 1);   // the store warp's TMA has read it
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
     }
     __syncthreads();
 
+    if constexpr (EPI == EPI_TSTORE) {
+        if (warp == NCW + 1) {
+            // -------------------------------------------- TMA store warp
+            if (lane == 0) {
+                asm volatile("prefetch.tensormap [%0];\n" ::"l"(&mapX));
+                unsigned ph = 0;
+                for (int64_t w = blockIdx.x; w < P.total_tiles; w += gridDim.x) {
+                    int64_t b, sp, mt, nt;
+                    ws_tile(P, w, b, sp, mt, nt);
+                    mbar_wait(xfull, ph);
+                    asm volatile(
+                        "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];\n" ::"l"(
+                            &mapX),
+                        "r"((int)(mt * BM)), "r"((int)(nt * BN)), "r"((int)b),
+                        "r"((unsigned)__cvta_generic_to_shared(Xs))
+                        : "memory");
+                    asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+                    asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");  // Xs may be rewritten
+                    mbar_arrive(xempty);
+                    ph ^= 1;
+                }
+                asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+            }
+            return;
+        }
+    }
     if (warp == NCW) {
         // ------------------------------------------------ TMA producer warp
         if (lane == 0) {
@@ -150,7 +190,7 @@ __global__ void __launch_bounds__((WARPS_M * WARPS_N + 1) * 32, 1)
                 int64_t b, sp, mt, nt;
                 ws_tile(P, w, b, sp, mt, nt);
                 const int64_t kb = sp * P.kchunk, ke = min(P.K, kb + P.kchunk);
-                if constexpr (XS) {
+                if constexpr (EPI == EPI_RESID) {
                     // reference block of this tile -> Xs (after the previous
                     // tile's epilogue released it); lands during the k-loop
                     mbar_wait(xempty, xphase ^ 1);
@@ -243,7 +283,24 @@ __global__ void __launch_bounds__((WARPS_M * WARPS_N + 1) * 32, 1)
         }
 
         const int64_t m0 = mt * BM, n0 = nt * BN;
-        if constexpr (EPI == EPI_STORE) {
+        if constexpr (EPI == EPI_TSTORE) {
+            // the store warp has read the previous tile out of Xs
+            mbar_wait(xempty, xph ^ 1);
+#pragma unroll
+            for (int i = 0; i < TM; ++i)
+#pragma unroll
+                for (int j = 0; j < TN; ++j)
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int ml = wm * WM + i * 8 + g;
+                        const int nl = wn * WN + j * 8 + 2 * t + e;
+                        Xs[nl * BM + ml] = P.alpha * acc[i][j][e];  // rows / columns past M, N: not stored by TMA
+                    }
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic writes -> async proxy
+            __syncwarp();
+            if (lane == 0) mbar_arrive(xfull);
+            xph ^= 1;
+        } else if constexpr (EPI == EPI_STORE) {
             double* C = P.C + b * P.strideC + sp * P.strideCsplit;
             const double* Cin = P.Cin ? P.Cin + b * P.strideCin : nullptr;
             const bool diag = P.tri && (mt == nt);

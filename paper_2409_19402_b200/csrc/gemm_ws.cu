@@ -77,19 +77,19 @@ bool make_map(CUtensorMap* map, const double* base, bool contiguous_is_k, int64_
 
 template <int BM, int BN, int WARPS_M, int WARPS_N, int STAGES>
 struct WsCfg {
+    static constexpr int bm = BM, bn = BN;
     static constexpr size_t smem = (size_t)STAGES * (BM * 16 + 16 * BN) * 8 + 2 * STAGES * 8 + 128;
-    static constexpr int threads = (WARPS_M * WARPS_N + 1) * 32;
     template <bool AK, bool BNM, int EPI>
     static void launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& x, const WsParams& P,
                        int grid, cudaStream_t s) {
         auto k = dmma_gemm_ws_kernel<BM, BN, 16, WARPS_M, WARPS_N, STAGES, AK, BNM, EPI>;
-        const size_t sm = smem + (EPI == EPI_RESID ? (size_t)BM * BN * 8 + 16 : 0);
+        const size_t sm = smem + (EPI != EPI_STORE ? (size_t)BM * BN * 8 + 16 : 0);
         static bool set = false;
         if (!set) {
             PPC_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
             set = true;
         }
-        k<<<grid, threads, sm, s>>>(a, b, x, P);
+        k<<<grid, ws_threads<BM, BN, WARPS_M, WARPS_N, EPI>(), sm, s>>>(a, b, x, P);
     }
 };
 using WsL = WsCfg<128, 128, 2, 4, 5>;
@@ -103,6 +103,16 @@ void dispatch(bool ak, bool bnm, int epi, const CUtensorMap& a, const CUtensorMa
     if (!ak && !bnm && epi == EPI_STORE) return Cfg::template launch<false, false, EPI_STORE>(a, b, x, P, grid, s);
     if (!ak && bnm && epi == EPI_STORE) return Cfg::template launch<false, true, EPI_STORE>(a, b, x, P, grid, s);
     if (ak && !bnm && epi == EPI_STORE) return Cfg::template launch<true, false, EPI_STORE>(a, b, x, P, grid, s);
+    fail(PPC_ARGUMENT, "gemm_ws: unsupported variant");
+}
+
+// the TMA-store epilogue (configurations whose operand ring leaves room for the output tile)
+template <class Cfg>
+void dispatch_tstore(bool ak, bool bnm, const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
+                     const WsParams& P, int grid, cudaStream_t s) {
+    if (!ak && !bnm) return Cfg::template launch<false, false, EPI_TSTORE>(a, b, c, P, grid, s);
+    if (!ak && bnm) return Cfg::template launch<false, true, EPI_TSTORE>(a, b, c, P, grid, s);
+    if (ak && !bnm) return Cfg::template launch<true, false, EPI_TSTORE>(a, b, c, P, grid, s);
     fail(PPC_ARGUMENT, "gemm_ws: unsupported variant");
 }
 
@@ -207,8 +217,19 @@ bool gemm_ws(const GemmDesc& d, int epi, const double* X, int64_t ldx, int64_t s
     }
     if (ctas_out) *ctas_out = grid;
     if (!partials && epi == EPI_RESID) return true;  // sizing query only
+    // plain stores of the 128 x 64 / 128 x 32 tiles drain through shared
+    // memory and a TMA store (the map clips rows / columns past M, N)
+    static const bool no_tstore = std::getenv("PPC_WS_NO_TSTORE") != nullptr;
+    const bool tstore = !no_tstore && epi == EPI_STORE && cfg != 0 && !d.symmetric && d.splits == 1 &&
+                        !(d.Cin && d.beta != 0.0) && al16(d.C) && !(d.ldc & 1) && !(d.strideC & 1) &&
+                        make_map_x(&mx_, d.C, d.M, d.N, d.ldc, map_batch, d.strideC, bm, bn);
     if (epi == EPI_RESID) {
         WsR::launch<false, true, EPI_RESID>(ma, mb, mx_, P, grid, s);
+    } else if (tstore) {
+        if (cfg == 1)
+            dispatch_tstore<WsM>(d.a_kmajor, d.b_nmajor, ma, mb, mx_, P, grid, s);
+        else
+            dispatch_tstore<WsT>(d.a_kmajor, d.b_nmajor, ma, mb, mx_, P, grid, s);
     } else {
         switch (cfg) {
             case 0: dispatch<WsL>(d.a_kmajor, d.b_nmajor, epi, ma, mb, ma, P, grid, s); break;
