@@ -61,14 +61,17 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblk, unsig
 
 // Fixed-order block sum (every CTA running the same code on the same data
 // gets the same bits): thread-strided partials, then a fixed tree.
-__device__ __forceinline__ double block_sum(double v, double* red) {
+// red: 2 x 32 doubles, used alternately (the parity flips per call), so the
+// next call's writes never race this call's reads: one barrier per sum.
+__device__ __forceinline__ double block_sum(double v, double* red, int& par) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    double* r = red + 32 * par;
+    par ^= 1;
+    if (lane == 0) r[warp] = v;
     __syncthreads();
-    if (lane == 0) red[warp] = v;
-    __syncthreads();
-    double t = lane < nw ? red[lane] : 0.0;
+    double t = lane < nw ? r[lane] : 0.0;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
     return t;  // every thread
@@ -97,11 +100,11 @@ constexpr size_t kTrdSmemMax = 200 * 1024;
 // computed redundantly by every CTA (same bits everywhere). Writes vn and
 // returns tau; the CTA's slice of V(:, jj) and (CTA 0) d, e, tau go out.
 __device__ __forceinline__ double make_reflector(const TrdParams& P, int jj, const double* xs, double* vn,
-                                                 double* red) {
+                                                 double* red, int& rpar) {
     const int n = P.n, tid = threadIdx.x, nt = blockDim.x;
     double s2 = 0.0;
     for (int i = jj + 2 + tid; i < n; i += nt) s2 = fma(xs[i], xs[i], s2);
-    s2 = block_sum(s2, red);
+    s2 = block_sum(s2, red, rpar);
     const double alpha = xs[jj + 1];
     double beta, tau, scal;
     if (s2 == 0.0) {
@@ -195,7 +198,8 @@ __global__ void __launch_bounds__(kTrdThreads, 1) sytrd_kernel(TrdParams P0) {
     double* vn = vs + n;               // reflector of step j+1
     double* ws = vn + n;               // w = p - K v
     double* xs = ws + n;               // pivot column
-    __shared__ double red[32];
+    __shared__ double red[64];
+    int rpar = 0;
     const int tid = threadIdx.x, nt = blockDim.x;
     unsigned target = 0;
 
@@ -211,7 +215,7 @@ __global__ void __launch_bounds__(kTrdThreads, 1) sytrd_kernel(TrdParams P0) {
     __syncthreads();
     // prologue: reflector 0, its products, column 1 published (an update
     // with v = w = 0 leaves A unchanged)
-    double tau = make_reflector(P, 0, xs, vn, red);
+    double tau = make_reflector(P, 0, xs, vn, red, rpar);
     for (int i = tid; i < n; i += nt) vs[i] = 0.0;
     __syncthreads();
     update_pass(P, A, -1, vs, ws, vn, tau, P.pg, P.colpub, false);
@@ -233,18 +237,21 @@ __global__ void __launch_bounds__(kTrdThreads, 1) sytrd_kernel(TrdParams P0) {
             xs[i] = __ldcg(cp + i);
             pv = fma(p, vs[i], pv);
         }
-        const double K = 0.5 * tau * block_sum(pv, red);
-        for (int i = j + 1 + tid; i < n; i += nt) ws[i] = fma(-K, vs[i], ws[i]);
+        const double K = 0.5 * tau * block_sum(pv, red, rpar);
+        // w = p - K v and the pivot column j+1 after the step-j update, in one
+        // pass (w(j+1) recomputed from p(j+1): no barrier between the two)
+        {
+            const double vc = vs[j + 1], wc = fma(-K, vc, __ldcg(pg + j + 1));
+            for (int i = j + 1 + tid; i < n; i += nt) {
+                const double w = fma(-K, vs[i], ws[i]);
+                ws[i] = w;
+                xs[i] = fma(-w, vc, fma(-vs[i], wc, xs[i]));
+            }
+        }
         if (tid == 0) ws[j] = 0.0;  // rows <= j of w stay zero (read by the paired-row pass)
         __syncthreads();
-        // ---- pivot column j+1 after the step-j update
-        {
-            const double vc = vs[j + 1], wc = ws[j + 1];
-            for (int i = j + 1 + tid; i < n; i += nt) xs[i] = fma(-ws[i], vc, fma(-vs[i], wc, xs[i]));
-        }
-        __syncthreads();
         if (j + 1 <= n - 3) {
-            const double taun = make_reflector(P, j + 1, xs, vn, red);
+            const double taun = make_reflector(P, j + 1, xs, vn, red, rpar);
             __syncthreads();
             update_pass(P, A, j, vs, ws, vn, taun, P.pg + (size_t)((j + 1) & 1) * n,
                         P.colpub + (size_t)((j + 1) & 1) * n, false);
@@ -252,7 +259,7 @@ __global__ void __launch_bounds__(kTrdThreads, 1) sytrd_kernel(TrdParams P0) {
         } else {
             update_pass(P, A, j, vs, ws, nullptr, 0.0, nullptr, P.colpub + (size_t)((j + 1) & 1) * n, false);
         }
-        __syncthreads();
+        // (the next step's grid barrier opens with a block barrier)
     }
     // trailing 2 x 2 block: columns n-2 and n-1 are final in their owners
     for (int t = 0; t < cpc; ++t) {
