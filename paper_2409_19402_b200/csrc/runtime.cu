@@ -139,6 +139,18 @@ void big_drop(BigCache& c, size_t i) {
 }
 }  // namespace
 
+// The pool keeps freed memory (release threshold: unlimited); under memory
+// pressure it is returned to the driver once the stream's frees are done.
+void release_pool_reserve(cudaStream_t s) {
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        cudaStreamSynchronize(s);
+        cudaMemPoolTrimTo(pool, 0);
+    }
+    cudaGetLastError();
+}
+
 void trim_workspace() {
     Context& c = ctx();
     BigCache& bc = t_big[c.device < 64 ? c.device : 63];
@@ -172,18 +184,30 @@ DeviceBuffer::DeviceBuffer(size_t bytes) : n_(bytes) {
             big_drop(c, 0);
             e = cudaMalloc(&p_, bytes);
         }
+        if (e == cudaErrorMemoryAllocation) {  // and from the stream-ordered pool's reserve
+            cudaGetLastError();
+            release_pool_reserve(s);
+            e = cudaMalloc(&p_, bytes);
+        }
         PPC_CUDA_CHECK(e);
         return;
     }
     static const bool trace = std::getenv("PPC_TRACE_ALLOC") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
+    cudaError_t e = cudaMallocAsync(&p_, bytes, s);
+    if (e == cudaErrorMemoryAllocation) {
+        // memory pressure (another allocator, or a caller's own buffers): the
+        // workspace cache gives its blocks back, then the allocation retries
+        cudaGetLastError();
+        trim_workspace();
+        release_pool_reserve(s);
+        e = cudaMallocAsync(&p_, bytes, s);
+    }
+    PPC_CUDA_CHECK(e);
     if (trace) {
-        const auto t0 = std::chrono::steady_clock::now();
-        PPC_CUDA_CHECK(cudaMallocAsync(&p_, bytes, s));
         const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
         if (ms > 2.0) fprintf(stderr, "[alloc] pool %.1f MB took %.1f ms\n", bytes / 1e6, ms);
-        return;
     }
-    PPC_CUDA_CHECK(cudaMallocAsync(&p_, bytes, s));
 }
 DeviceBuffer::~DeviceBuffer() { release(); }
 void DeviceBuffer::release() {
