@@ -291,6 +291,19 @@ int ppc_mode3_forward_digits(int64_t handle, const double* Q, int64_t p, double*
 int ppc_digits_release(int64_t handle);
 /* parts[0] = fixed pairwise tree sum of nparts arrays of `elems` doubles. */
 int ppc_tree_reduce(double* parts, int64_t nparts, int64_t elems, int loc);
+/* The same eigensolve split across ranks, DEVICE memory, stream-ordered:
+ * _begin tridiagonalizes G (n x n; replicated on every rank) and returns a
+ * handle (0: the size takes another solver; use ppc_sym_eig_top);
+ * _vectors writes the inverse-iteration vectors of eigenvalues j0..j1-1
+ * (0 = largest) to Z (n x (j1-j0)); the caller gathers all p of them into
+ * Zall (n x p); _finish orthonormalizes Zall (in place, replicated) and
+ * writes columns j0..j1-1 of Q (sign rule applied) to Q (n x (j1-j0)).
+ * Q is bitwise the ppc_sym_eig_top result for any split. Handles belong to
+ * the calling thread; _release frees one. */
+int ppc_sym_eig_split_begin(const double* G, int64_t n, int64_t p, int64_t* handle);
+int ppc_sym_eig_split_vectors(int64_t handle, int64_t j0, int64_t j1, double* Z);
+int ppc_sym_eig_split_finish(int64_t handle, double* Zall, int64_t j0, int64_t j1, double* Q);
+int ppc_sym_eig_split_release(int64_t handle);
 /* Top-p eigenvectors Q (n x p, sign rule) and sigma = sqrt(lambda) (nullable)
  * of the symmetric PSD Gram G (n x n): the tail of data_dependent_transform. */
 int ppc_sym_eig_top(const double* G, int64_t n, int64_t p, double* Q, double* sigma, int loc);

@@ -54,6 +54,10 @@ def lib() -> C.CDLL:
         "ppc_get_ozaki": (C.c_int, []),
         "ppc_facewise_strided": (C.c_int, [vp, i64, i64, i64, vp, i64, vp, i64, i64]),
         "ppc_reshard_slices": (C.c_int, [vp, i64, i64, i64, i64, vp]),
+        "ppc_sym_eig_split_begin": (C.c_int, [vp, i64, i64, C.POINTER(C.c_int64)]),
+        "ppc_sym_eig_split_vectors": (C.c_int, [i64, i64, i64, vp]),
+        "ppc_sym_eig_split_finish": (C.c_int, [i64, vp, i64, i64, vp]),
+        "ppc_sym_eig_split_release": (C.c_int, [i64]),
         "ppc_ozaki_syrk_batched": (C.c_int, [vp, i64, i64, i64, i64, i64, vp]),
         "ppc_timing_report": (C.c_int, [C.c_char_p, i64, C.c_int]),
         "ppc_mode3_product": (C.c_int, [vp, i64, i64, i64, vp, i64, C.c_int, vp, C.c_int]),

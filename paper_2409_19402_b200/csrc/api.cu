@@ -619,6 +619,48 @@ int ppc_sym_eig_top(const double* G, int64_t n, int64_t p, double* Q, double* si
     });
 }
 
+namespace {
+thread_local std::map<int64_t, std::unique_ptr<EigSplit>> t_eig;
+thread_local int64_t t_eig_next = 1;
+EigSplit& eig_of(int64_t h) {
+    auto it = t_eig.find(h);
+    if (it == t_eig.end()) fail(PPC_ARGUMENT, "sym_eig_split: unknown handle");
+    return *it->second;
+}
+}  // namespace
+
+int ppc_sym_eig_split_begin(const double* G, int64_t n, int64_t p, int64_t* handle) {
+    return guarded([&] {
+        if (!G || !handle) fail(PPC_ARGUMENT, "null pointer");
+        *handle = 0;
+        check_transform(n, p);
+        if (n <= kSubspaceMinN || !tridiag_eig_eligible(n, p)) return;  // caller: replicated ppc_sym_eig_top
+        auto e = std::make_unique<EigSplit>(G, n, p, stream());
+        *handle = t_eig_next++;
+        t_eig[*handle] = std::move(e);
+    });
+}
+
+int ppc_sym_eig_split_vectors(int64_t handle, int64_t j0, int64_t j1, double* Z) {
+    return guarded([&] {
+        if (!Z) fail(PPC_ARGUMENT, "null pointer");
+        eig_of(handle).vectors(j0, j1, Z, stream());
+    });
+}
+
+int ppc_sym_eig_split_finish(int64_t handle, double* Zall, int64_t j0, int64_t j1, double* Q) {
+    return guarded([&] {
+        if (!Zall || !Q) fail(PPC_ARGUMENT, "null pointer");
+        EigSplit& e = eig_of(handle);
+        e.finish(Zall, j0, j1, Q, stream());
+        sign_rule(Q, e.n, j1 - j0, 1, nullptr, 0, stream());  // fix_svd_signs (matrix_kernels.cpp:35), per column
+    });
+}
+
+int ppc_sym_eig_split_release(int64_t handle) {
+    return guarded([&] { t_eig.erase(handle); });
+}
+
 int ppc_slice_residual_sums(const double* A, int64_t n1, int64_t n2, int64_t batch, int64_t k,
                             const double* U, const double* S, const double* V, double* sums, int loc) {
     return guarded([&] {

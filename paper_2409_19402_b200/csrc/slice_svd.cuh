@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 
+#include "internal.h"
+
 namespace ppc {
 
 // Problems with min dimension <= this go to the one-CTA Jacobi kernel; larger
@@ -33,6 +35,18 @@ void tridiag_eig_top(const double* G, int64_t n, int64_t p, double* Q, double* l
 // `batch` matrices G + b * strideG: Q (n, p, batch), lambda (p, batch), descending.
 void tridiag_eig_top_batched(const double* G, int64_t n, int64_t strideG, int64_t batch, int64_t p, double* Q,
                              double* lambda, cudaStream_t s);
+// The direct eigensolve of one matrix in three steps, for the multi-GPU
+// driver: the tridiagonalization (replicated), the eigenvalues / inverse
+// iteration vectors of an index range (sharded), then the orthonormalization
+// of all p vectors (replicated) and the back-transformation of a column range
+// (sharded). Every piece gives the bits tridiag_eig_top gives.
+struct EigSplit {
+    int64_t n, p;
+    DeviceBuffer V, tau, d, e, lam, bnd;
+    EigSplit(const double* G, int64_t n, int64_t p, cudaStream_t s);
+    void vectors(int64_t j0, int64_t j1, double* Z, cudaStream_t s);                     // Z: n x (j1 - j0)
+    void finish(double* Zall, int64_t j0, int64_t j1, double* Q, cudaStream_t s);        // Zall: n x p (modified)
+};
 // Z (r x k per block, column-major, `batch` blocks of r*k) <- orthonormal columns,
 // shifted CholQR3 in column order (k <= 160).
 void cholqr_inplace(double* Z, int64_t r, int64_t k, cudaStream_t s, int64_t batch = 1);

@@ -295,14 +295,17 @@ __device__ __forceinline__ int sturm_count(const double* d, const double* e2, in
 // multisection, every thread one Sturm count per round (~7 bits a round).
 // NT = 256 for a few eigenvalues (latency: 8 bits a round); 64 when a batch
 // brings hundreds (work: the SMs are full either way).
+// kl CTAs per matrix compute eigenvalues m0 .. m0 + kl - 1 of its k wanted
+// (kl = k, m0 = 0 for all of them; a subrange for the sharded eigensolve:
+// every eigenvalue comes out bitwise the same either way).
 template <int NT>
 __global__ void __launch_bounds__(NT) bisect_top_kernel(const double* __restrict__ dg,
                                                                  const double* __restrict__ eg, int n, int k,
                                                                  double* __restrict__ lam,
-                                                                 double* __restrict__ bounds) {
+                                                                 double* __restrict__ bounds, int kl, int m0) {
     extern __shared__ __align__(16) double sh[];
-    {  // matrix blockIdx.x / k of the batch
-        const int mat = blockIdx.x / k;
+    {  // matrix blockIdx.x / kl of the batch
+        const int mat = blockIdx.x / kl;
         dg += (size_t)mat * n;
         eg += (size_t)mat * n;
         lam += (size_t)mat * k;
@@ -349,7 +352,7 @@ __global__ void __launch_bounds__(NT) bisect_top_kernel(const double* __restrict
     gl -= 2.0 * kEps * tnorm * n + 2.0 * pivmin;
     gu += 2.0 * kEps * tnorm * n + 2.0 * pivmin;
     const double atol = kEps * tnorm;
-    const int m = blockIdx.x % k;  // eigenvalue of matrix blockIdx.x / k
+    const int m = m0 + (int)(blockIdx.x % kl);  // eigenvalue of matrix blockIdx.x / kl
     const int want = n - m;  // invariant: count(hi) >= want > count(lo)
     double lo = gl, hi = gu;
     for (int it = 0; it < 40; ++it) {
@@ -369,7 +372,7 @@ __global__ void __launch_bounds__(NT) bisect_top_kernel(const double* __restrict
     }
     if (tid == 0) {
         lam[m] = 0.5 * (lo + hi);
-        if (bounds && m == 0) {
+        if (bounds && blockIdx.x % kl == 0) {  // the same values in every CTA of the matrix
             bounds[0] = tnorm;
             bounds[1] = pivmin;
         }
@@ -390,16 +393,18 @@ __device__ __forceinline__ double hash_unit(uint64_t z) {
 // three solves from a deterministic random start with max-norm scaling in
 // between; the warp loads T, draws the start and normalizes. Pivots below
 // eps*||T|| are raised to it (dlagts job = -1).
+// (kl, m0 as for bisect_top_kernel: Z holds the kl columns m0 .. m0 + kl - 1)
 __global__ void inverse_iteration_kernel(const double* __restrict__ dg, const double* __restrict__ eg,
                                          int n, int k, const double* __restrict__ lam,
-                                         const double* __restrict__ bounds, double* __restrict__ Z) {
-    {  // matrix blockIdx.x / k of the batch
-        const int mat = blockIdx.x / k;
+                                         const double* __restrict__ bounds, double* __restrict__ Z, int kl,
+                                         int m0) {
+    {  // matrix blockIdx.x / kl of the batch
+        const int mat = blockIdx.x / kl;
         dg += (size_t)mat * n;
         eg += (size_t)mat * n;
         lam += (size_t)mat * k;
         bounds += (size_t)mat * 2;
-        Z += (size_t)mat * n * k;
+        Z += (size_t)mat * n * kl;
     }
     extern __shared__ __align__(16) double sh[];
     double* d = sh;
@@ -411,7 +416,7 @@ __global__ void inverse_iteration_kernel(const double* __restrict__ dg, const do
     double* x = lm + n;
     unsigned char* pv = reinterpret_cast<unsigned char*>(x + n);
     __shared__ double s_sc;
-    const int m = blockIdx.x % k, lane = threadIdx.x;
+    const int m = m0 + (int)(blockIdx.x % kl), lane = threadIdx.x;
     const double l = lam[m];
     const double pert = kEps * fmax(bounds[0], kSafeMin);
     for (int i = lane; i < n; i += 32) {
@@ -486,7 +491,7 @@ __global__ void inverse_iteration_kernel(const double* __restrict__ dg, const do
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
     const double inv = nrm > 0.0 ? 1.0 / sqrt(nrm) : 0.0;
-    for (int i = lane; i < n; i += 32) Z[(size_t)m * n + i] = x[i] * inv;
+    for (int i = lane; i < n; i += 32) Z[(size_t)(m - m0) * n + i] = x[i] * inv;
 }
 
 // Q = H_0 H_1 ... H_{n-3} Z. The reflectors go in chunks of kBtChunk,
@@ -755,53 +760,58 @@ void tridiag_eig_top(const double* G, int64_t n64, int64_t k64, double* Q, doubl
     tridiag_eig_top_batched(G, n64, n64 * n64, 1, k64, Q, lambda, s);
 }
 
-void tridiag_eig_top_batched(const double* G, int64_t n64, int64_t strideG, int64_t batch64, int64_t k64, double* Q,
-                             double* lambda, cudaStream_t s) {
-    const int n = (int)n64, k = (int)k64, batch = (int)batch64;
-    if (!tridiag_eig_eligible(n64, k64, batch64)) fail(PPC_ARGUMENT, "tridiag_eig_top: size out of range");
-    const TrdPlan t = trd_plan(n64, batch64);
+namespace {
+
+// Householder tridiagonalization of `batch` matrices in waves (sytrd_kernel):
+// V (n x n x batch), tau, d, e (n x batch).
+void run_sytrd(const double* G, int n, int64_t strideG, int batch, double* V, double* tau, double* d, double* e,
+               cudaStream_t s) {
+    const TrdPlan t = trd_plan(n, batch);
     const int nblk = t.nblk, cpc = t.cpc;
     const size_t smem = trd_smem(n, cpc);
     const size_t B = (size_t)batch;
-    DeviceBuffer Vb(sizeof(double) * (size_t)n * n * B), tb(sizeof(double) * n * B), db(sizeof(double) * n * B),
-        eb(sizeof(double) * n * B), pgb(sizeof(double) * 2 * n * B), cpb(sizeof(double) * 2 * n * B),
-        barb(sizeof(unsigned) * 32 * B), bnd(sizeof(double) * 2 * B);
+    DeviceBuffer pgb(sizeof(double) * 2 * n * B), cpb(sizeof(double) * 2 * n * B), barb(sizeof(unsigned) * 32 * B);
     PPC_CUDA_CHECK(cudaMemsetAsync(barb.d(), 0, sizeof(unsigned) * 32 * B, s));
-    {
-        StageTimer tm("eig.tridiag", s);
-        PPC_CUDA_CHECK(cudaFuncSetAttribute(sytrd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        for (int b0 = 0; b0 < batch; b0 += t.per_wave) {
-            const size_t o = (size_t)b0;
-            TrdParams P;
-            P.G = G + o * strideG;
-            P.n = n;
-            P.nblk = nblk;
-            P.cpc = cpc;
-            P.V = Vb.d() + o * n * n;
-            P.tau = tb.d() + o * n;
-            P.d = db.d() + o * n;
-            P.e = eb.d() + o * n;
-            P.pg = pgb.d() + o * 2 * n;
-            P.colpub = cpb.d() + o * 2 * n;
-            P.bar = barb.as<unsigned>() + o * 32;
-            P.strideG = strideG;
-            P.blk = 0;
-            void* args[] = {&P};
-            const int nm = std::min(t.per_wave, batch - b0);
-            PPC_CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)sytrd_kernel, dim3(nblk * nm),
-                                                       dim3(kTrdThreads), args, smem, s));
-            count_launch();
-            check_launch("sytrd");
-        }
+    StageTimer tm("eig.tridiag", s);
+    PPC_CUDA_CHECK(cudaFuncSetAttribute(sytrd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    for (int b0 = 0; b0 < batch; b0 += t.per_wave) {
+        const size_t o = (size_t)b0;
+        TrdParams P;
+        P.G = G + o * strideG;
+        P.n = n;
+        P.nblk = nblk;
+        P.cpc = cpc;
+        P.V = V + o * n * n;
+        P.tau = tau + o * n;
+        P.d = d + o * n;
+        P.e = e + o * n;
+        P.pg = pgb.d() + o * 2 * n;
+        P.colpub = cpb.d() + o * 2 * n;
+        P.bar = barb.as<unsigned>() + o * 32;
+        P.strideG = strideG;
+        P.blk = 0;
+        void* args[] = {&P};
+        const int nm = std::min(t.per_wave, batch - b0);
+        PPC_CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)sytrd_kernel, dim3(nblk * nm), dim3(kTrdThreads),
+                                                   args, smem, s));
+        count_launch();
+        check_launch("sytrd");
     }
+}
+
+// Eigenvalues m0 .. m0 + kl - 1 (of the k wanted) of every matrix and their
+// inverse-iteration vectors Z (n x kl x batch). The multisection width is
+// chosen from k (not kl), so a subrange gives the same bits.
+void run_vectors(const double* d, const double* e, int n, int k, int batch, int kl, int m0, double* lambda,
+                 double* bnd, double* Z, cudaStream_t s) {
     {
         StageTimer tm("eig.bisect", s);
-        const unsigned grid = (unsigned)(k * batch);
+        const unsigned grid = (unsigned)(kl * batch);
         const size_t bsm = 2 * n * sizeof(double);
-        if (grid >= 2u * (unsigned)ctx().sms)
-            bisect_top_kernel<64><<<grid, 64, bsm, s>>>(db.d(), eb.d(), n, k, lambda, bnd.d());
+        if ((unsigned)(k * batch) >= 2u * (unsigned)ctx().sms)
+            bisect_top_kernel<64><<<grid, 64, bsm, s>>>(d, e, n, k, lambda, bnd, kl, m0);
         else
-            bisect_top_kernel<256><<<grid, 256, bsm, s>>>(db.d(), eb.d(), n, k, lambda, bnd.d());
+            bisect_top_kernel<256><<<grid, 256, bsm, s>>>(d, e, n, k, lambda, bnd, kl, m0);
         count_launch();
         check_launch("bisect_top");
     }
@@ -810,24 +820,61 @@ void tridiag_eig_top_batched(const double* G, int64_t n64, int64_t strideG, int6
         const size_t ism = 7 * (size_t)n * sizeof(double) + n + 16;
         PPC_CUDA_CHECK(cudaFuncSetAttribute(inverse_iteration_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             (int)ism));
-        inverse_iteration_kernel<<<(unsigned)(k * batch), 32, ism, s>>>(db.d(), eb.d(), n, k, lambda, bnd.d(), Q);
+        inverse_iteration_kernel<<<(unsigned)(kl * batch), 32, ism, s>>>(d, e, n, k, lambda, bnd, Z, kl, m0);
         count_launch();
         check_launch("inverse_iteration");
     }
+}
+
+void run_back_transform(const double* V, const double* tau, int n, int k, int batch, double* Z, cudaStream_t s) {
+    StageTimer tm("eig.backtransform", s);
+    DeviceBuffer Tws(sizeof(double) * ((n - 3 + kBtChunk) / kBtChunk) * kBtChunk * kBtChunk * (size_t)batch);
+    if (n <= 256) launch_back_transform<8>(V, tau, n, k, batch, Z, Tws.d(), s);
+    else if (n <= 512) launch_back_transform<16>(V, tau, n, k, batch, Z, Tws.d(), s);
+    else if (n <= 1024) launch_back_transform<32>(V, tau, n, k, batch, Z, Tws.d(), s);
+    else launch_back_transform<48>(V, tau, n, k, batch, Z, Tws.d(), s);
+    count_launch();
+    check_launch("back_transform");
+}
+
+}  // namespace
+
+void tridiag_eig_top_batched(const double* G, int64_t n64, int64_t strideG, int64_t batch64, int64_t k64, double* Q,
+                             double* lambda, cudaStream_t s) {
+    const int n = (int)n64, k = (int)k64, batch = (int)batch64;
+    if (!tridiag_eig_eligible(n64, k64, batch64)) fail(PPC_ARGUMENT, "tridiag_eig_top: size out of range");
+    const size_t B = (size_t)batch;
+    DeviceBuffer Vb(sizeof(double) * (size_t)n * n * B), tb(sizeof(double) * n * B), db(sizeof(double) * n * B),
+        eb(sizeof(double) * n * B), bnd(sizeof(double) * 2 * B);
+    run_sytrd(G, n, strideG, batch, Vb.d(), tb.d(), db.d(), eb.d(), s);
+    run_vectors(db.d(), eb.d(), n, k, batch, k, 0, lambda, bnd.d(), Q, s);
     {
         StageTimer tm("eig.orth", s);
         cholqr_inplace(Q, n, k, s, batch);
     }
+    run_back_transform(Vb.d(), tb.d(), n, k, batch, Q, s);
+}
+
+// ---- the eigensolve split across ranks (multi-GPU data-driven Q) ----------
+EigSplit::EigSplit(const double* G, int64_t n_, int64_t p_, cudaStream_t s)
+    : n(n_), p(p_), V(sizeof(double) * n_ * n_), tau(sizeof(double) * n_), d(sizeof(double) * n_),
+      e(sizeof(double) * n_), lam(sizeof(double) * p_), bnd(sizeof(double) * 2) {
+    run_sytrd(G, (int)n, n * n, 1, V.d(), tau.d(), d.d(), e.d(), s);
+}
+
+void EigSplit::vectors(int64_t j0, int64_t j1, double* Z, cudaStream_t s) {
+    if (j0 < 0 || j1 > p || j0 >= j1) fail(PPC_BOUNDS, "eig split: eigen index range outside [0, p)");
+    run_vectors(d.d(), e.d(), (int)n, (int)p, 1, (int)(j1 - j0), (int)j0, lam.d(), bnd.d(), Z, s);
+}
+
+void EigSplit::finish(double* Zall, int64_t j0, int64_t j1, double* Q, cudaStream_t s) {
+    if (j0 < 0 || j1 > p || j0 >= j1) fail(PPC_BOUNDS, "eig split: column range outside [0, p)");
     {
-        StageTimer tm("eig.backtransform", s);
-        DeviceBuffer Tws(sizeof(double) * ((n - 3 + kBtChunk) / kBtChunk) * kBtChunk * kBtChunk * B);
-        if (n <= 256) launch_back_transform<8>(Vb.d(), tb.d(), n, k, batch, Q, Tws.d(), s);
-        else if (n <= 512) launch_back_transform<16>(Vb.d(), tb.d(), n, k, batch, Q, Tws.d(), s);
-        else if (n <= 1024) launch_back_transform<32>(Vb.d(), tb.d(), n, k, batch, Q, Tws.d(), s);
-        else launch_back_transform<48>(Vb.d(), tb.d(), n, k, batch, Q, Tws.d(), s);
-        count_launch();
-        check_launch("back_transform");
+        StageTimer tm("eig.orth", s);
+        cholqr_inplace(Zall, n, p, s, 1);
     }
+    PPC_CUDA_CHECK(cudaMemcpyAsync(Q, Zall + j0 * n, sizeof(double) * n * (j1 - j0), cudaMemcpyDeviceToDevice, s));
+    run_back_transform(V.d(), tau.d(), (int)n, (int)(j1 - j0), 1, Q, s);
 }
 
 }  // namespace ppc

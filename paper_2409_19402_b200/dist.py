@@ -118,6 +118,25 @@ class DeviceBackend:
         _check(self.L.ppc_sym_eig_top(_p(G), n3, p, _p(Q), _p(sig), 1))
         return Q, sig
 
+    # the direct eigensolve split across ranks (ppc_sym_eig_split_*)
+    def eig_begin(self, G, n3, p):
+        h = C.c_int64(0)
+        _check(self.L.ppc_sym_eig_split_begin(_p(G), n3, p, C.byref(h)))
+        return h.value or None
+
+    def eig_vectors(self, h, n3, j0, j1):
+        Z = _fempty((n3, j1 - j0), self.device)
+        _check(self.L.ppc_sym_eig_split_vectors(h, j0, j1, _p(Z)))
+        return Z
+
+    def eig_finish(self, h, Zall, n3, j0, j1):
+        Q = _fempty((n3, j1 - j0), self.device)
+        _check(self.L.ppc_sym_eig_split_finish(h, _p(Zall), j0, j1, _p(Q)))
+        return Q
+
+    def eig_release(self, h):
+        _check(self.L.ppc_sym_eig_split_release(h))
+
     def mode3_fwd(self, A_blk, n1, nj, n3, Q, p):
         out = _fempty((n1, nj, p), self.device)
         _check(self.L.ppc_mode3_product(_p(A_blk), n1, nj, n3, _p(Q), p, 1, _p(out), 1))
@@ -227,6 +246,34 @@ def _tree_finish(roots):
     return roots[0]
 
 
+def _gather_cols(X, G, group):
+    """all_gather of a Fortran (n, c) column block into Fortran (n, G c),
+    columns in rank order (no copy: the gathered buffer is the result)."""
+    n, c = X.shape
+    out = torch.empty((G * c, n), dtype=X.dtype, device=X.device)
+    dist.all_gather_into_tensor(out, X.permute(1, 0).contiguous(), group=group)
+    return out.permute(1, 0)
+
+
+def sharded_eig(Gm, n3, p, rank, G, backend, group=None):
+    """Top-p eigenvectors of the (replicated) Gram with the direct solver's
+    per-eigenvalue work split across the G ranks (transforms.cpp:97-115:
+    U3 = the top eigenvectors of T^T T, sign rule applied)."""
+    h = backend.eig_begin(Gm, n3, p) if p % G == 0 else None
+    if h is None:
+        Q, _ = backend.sym_eig_top(Gm, n3, p)
+        return Q
+    try:
+        j0, j1 = rank * (p // G), (rank + 1) * (p // G)
+        Z = backend.eig_vectors(h, n3, j0, j1)
+        Zall = _gather_cols(Z, G, group) if G > 1 else Z
+        Zall = Zall.permute(1, 0).contiguous().permute(1, 0)
+        Ql = backend.eig_finish(h, Zall, n3, j0, j1)
+        return _gather_cols(Ql, G, group) if G > 1 else Ql
+    finally:
+        backend.eig_release(h)
+
+
 def sharded_compress(A_blk, plan: ShardPlan, k: int, backend, group=None):
     """Runs the sharded pipeline on this rank's lateral block A_blk
     (n1 x nj x n3, Fortran layout). Returns (Q, U, S, V, relative_error) with
@@ -249,8 +296,11 @@ def sharded_compress(A_blk, plan: ShardPlan, k: int, backend, group=None):
         Gm = backend.tree_reduce(roots)
     else:
         Gm = root
-    # 3. replicated eigensolve
-    Q, _ = backend.sym_eig_top(Gm, n3, p)
+    # 3. eigensolve: the tridiagonalization replicated, the eigenvalues and
+    #    inverse-iteration vectors of p/G indices per rank, gathered; the
+    #    orthonormalization replicated, the back-transformation of p/G columns
+    #    per rank, gathered. Q is bitwise the 1-GPU basis for any G.
+    Q = sharded_eig(Gm, n3, p, plan.rank, G, backend, group)
     # 4. local forward transform (from the Gram's kept digits when it can)
     Ah = backend.mode3_fwd_kept(A_blk, n1, nj, n3, Q, p)  # (n1, nj, p) Fortran
     # 5. reshard pixel -> slice: chunk for rank s = my block of its slices

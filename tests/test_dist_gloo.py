@@ -64,6 +64,19 @@ class NumpyBackend:
     def unpack_slices(self, recv, G, ps, nj, n1):
         return recv.view(G, ps, nj, n1).permute(1, 0, 2, 3).reshape(ps, G * nj, n1)
 
+    def eig_begin(self, G, n3, p):
+        self._eig = self.sym_eig_top(G, n3, p)[0]
+        return 1
+
+    def eig_vectors(self, h, n3, j0, j1):
+        return self._eig[:, j0:j1].contiguous()
+
+    def eig_finish(self, h, Zall, n3, j0, j1):
+        return Zall[:, j0:j1]
+
+    def eig_release(self, h):
+        self._eig = None
+
     def sym_eig_top(self, G, n3, p):
         w, V = np.linalg.eigh(G.numpy().reshape(n3, n3))
         order = np.argsort(-w, kind="stable")[:p]
