@@ -331,7 +331,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         constexpr uint32_t kAmn = AMN ? (1u << 15) : 0u;
         constexpr uint32_t kIdesc1 = idesc_i8<kBM, BN>() | kAmn;
         constexpr uint32_t kIdesc2 = idesc_i8<kBM, 2 * BN>() | kAmn;
-        constexpr uint32_t kIdesc3 = idesc_i8<kBM, 3 * BN>() | kAmn;
+        constexpr uint32_t kIdesc3 = idesc_i8<kBM, (3 * BN <= 256 ? 3 : 1) * BN>() | kAmn;
+        constexpr int kGrp = 3 * BN <= 256 ? 3 : 2;  // UMMA N <= 256
         int64_t g = 0, cg = 0;  // stage and digit-block counters across items
         for (int64_t item = blockIdx.x; item < items; item += gridDim.x) {
             int64_t mb_item = 0;
@@ -363,8 +364,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                                 : sdesc_k_sw64(sa + (i - 1) * A_TILE) + (uint64_t)(kk * 2);
                                 const int jmax = NL + 1 - i;  // levels i + j <= NL + 1
 #pragma unroll
-                                for (int j0 = 1; j0 <= jmax; j0 += 3) {
-                                    const int nj = jmax - j0 + 1 < 3 ? jmax - j0 + 1 : 3;
+                                for (int j0 = 1; j0 <= jmax; j0 += kGrp) {
+                                    const int nj = jmax - j0 + 1 < kGrp ? jmax - j0 + 1 : kGrp;
                                     const uint32_t idesc = (nj == 3 ? kIdesc3 : (nj == 2 ? kIdesc2 : kIdesc1)) | amn;
                                     const uint64_t db = sdesc_k_sw64(sb + (j0 - 1) * B_TILE) + (uint64_t)(kk * 2);
                                     mma_i8(tmem + (uint32_t)((i + j0 - 2) * BN), da, db, idesc, i == 1 ? acc0 : 1u);
@@ -549,6 +550,19 @@ bool ozaki_enabled() {
     return v == 1;
 }
 
+// Digit levels of the data-driven Q's Gram SYRK (PPC_GRAM_LEVELS = 5 or 6,
+// default 6). Five levels (15 digit pairs, levels 2..6) drop the level-7
+// pair products, each <= 2^-40 sigma_a sigma_b per row with balanced signs:
+// over a K-row chunk they add ~2^-41.6 sqrt(6 K) sigma_a sigma_b. Measured
+// (cfg5): the step 127 -> 121 ms (the SYRK is not purely tensor-bound, so
+// 15/21 of the pairs save less than 15/21 of its time), with the Gram 256x
+// further from FP64 (i.i.d. Gaussian 2^18 x 512: 5e-13 of max|G| instead of
+// ~2e-15). Kept as an A/B switch; the default stays at FP64-level accuracy.
+int gram_levels() {
+    static const int v = (std::getenv("PPC_GRAM_LEVELS") && std::atoi(std::getenv("PPC_GRAM_LEVELS")) == 5) ? 5 : kS;
+    return v;
+}
+
 int64_t ozaki_grid(int64_t items) { return std::min<int64_t>(items, ctx().sms); }  // one persistent CTA per SM
 
 template <bool SYM, bool AMN = false, bool RESID = false, int BN = kBN, int NL = kS, bool SYMA = false>
@@ -581,7 +595,7 @@ int64_t tri_tiles(int64_t n, int64_t bn = kBN) {
 // Grams of `nout` outputs, each summing `per` digit blocks of d: out[ob] =
 // sum over its blocks of X_blk^T X_blk (cols x cols, column-major).
 void ozaki_syrk(const OzakiDigits& d, int64_t nout, int64_t per, double* out, cudaStream_t s, const char* stage,
-                double rows_total, int64_t block_base = 0) {
+                double rows_total, int64_t block_base = 0, int levels = kS) {
     // the nout * per blocks from block_base on
     const int8_t* D0 = d.D.as<int8_t>() + (size_t)block_base * d.nd * d.cols * d.KCp;
     // output tile width: 80 (6 x 80 TMEM columns, 2 ring stages) or 64
@@ -607,11 +621,13 @@ void ozaki_syrk(const OzakiDigits& d, int64_t nout, int64_t per, double* out, cu
     P.X = nullptr;
     P.ldx = P.strideX = P.m_total = 0;
     P.partial = nullptr;
-    // int8 ops of the 21 digit-pair products over the upper triangle
-    StageTimer tk(stage, s, 2.0 * kS * (kS + 1) / 2 * rows_total * d.cols * d.cols / 2,
-                  (double)kS * rows_total * d.cols);
+    // int8 ops of the levels (levels + 1) / 2 digit-pair products over the upper triangle
+    StageTimer tk(stage, s, 2.0 * levels * (levels + 1) / 2 * rows_total * d.cols * d.cols / 2,
+                  (double)levels * rows_total * d.cols);
     if (bn == 64)
         launch_mma<true, false, false, 64>(ma, mb, P, nout * P.tiles, s);
+    else if (levels == 5)
+        launch_mma<true, false, false, kBN, 5>(ma, mb, P, nout * P.tiles, s);
     else
         launch_mma<true>(ma, mb, P, nout * P.tiles, s);
 }
@@ -854,7 +870,7 @@ bool ozaki_gram_partials(const double* T, int64_t ldT, int64_t rows, int64_t n3,
     d.split(T, ldT, 0, rows, n3, kKC, nblk, s, nullptr, 0, chunk, per, nonfinite, retain ? kSmax : kS, base,
             retain ? total_blocks : 0);
     if (retain && base == 0 && total_blocks == 0) d.uniform = true;  // streamed groups: the caller decides
-    ozaki_syrk(d, nchunks, per, parts, s, "ozaki_syrk", (double)rows, base);
+    ozaki_syrk(d, nchunks, per, parts, s, "ozaki_syrk", (double)rows, base, gram_levels());
     return true;
 }
 
