@@ -21,7 +21,8 @@ CfgId choose(const GemmDesc& d) {
     if (d.N <= 24) return T24;
     if (d.N <= 32) return T32;
     if (d.symmetric) return work_ctas_L >= 296 ? L : S;
-    if (d.N <= 64) return (((d.M + 127) / 128) * d.batch * d.splits >= 148) ? M : S;
+    // M <= 64: the 128-row tile would spend half its MMAs on padding rows
+    if (d.N <= 64) return (d.M > 64 && ((d.M + 127) / 128) * d.batch * d.splits >= 148) ? M : S;
     return work_ctas_L >= 148 ? L : S;
 }
 
@@ -99,6 +100,7 @@ int64_t kchunk_of(const GemmDesc& d) {
 }  // namespace
 
 void gemm(const GemmDesc& d, cudaStream_t s) {
+    HostProf hp_("gemm");
     validate(d);
     if (d.M == 0 || d.N == 0) return;
     if (d.allow_ws && gemm_ws(d, EPI_STORE, nullptr, 0, 0, nullptr, nullptr, s)) return;

@@ -144,6 +144,7 @@ bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 // Returns false (nothing launched) when the problem does not fit the TMA path.
 bool gemm_ws(const GemmDesc& d, int epi, const double* X, int64_t ldx, int64_t strideX, double* partials,
              int64_t* ctas_out, cudaStream_t s) {
+    HostProf hp_("gemm_ws");
     if (gemm_path() == 1) return false;  // forced classic cp.async kernel
     if (d.M < 1 || d.N < 1 || d.K < 1) return false;
     if (d.zmap && d.zmap_extent < 1) return false;

@@ -123,6 +123,19 @@ private:
     cudaEvent_t e0_ = nullptr;
 };
 
+// Host-side time per named scope (PPC_HOST_PROFILE=1; printed at exit):
+// finds the host work that starves the GPU in launch-bound sequences.
+class HostProf {
+public:
+    explicit HostProf(const char* name);
+    ~HostProf();
+    HostProf(const HostProf&) = delete;
+    HostProf& operator=(const HostProf&) = delete;
+private:
+    const char* name_;
+    long long t0_ = -1;
+};
+
 void validate_loc(int loc);
 void require_positive(int64_t v, const char* what);
 

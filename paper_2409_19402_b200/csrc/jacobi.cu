@@ -463,6 +463,7 @@ size_t jacobi_smem_bytes(int64_t m, int64_t n) {
 void jacobi_svd(const double* A, int64_t m, int64_t n, int64_t strideA, int64_t batch, int64_t k,
                 double* U, double* S, double* V, double* tail2, cudaStream_t s, double gtol_rel,
                 int sweep_cap, const int* zmap) {
+    HostProf hp_("jacobi_svd");
     if (batch == 0) return;
     static bool tol_set = false;
     if (!tol_set) {

@@ -83,7 +83,7 @@ __global__ void __launch_bounds__(256) ozaki_split_kernel(const double* __restri
                                                           int64_t chunk, int64_t per, int8_t* __restrict__ D,
                                                           double* __restrict__ scale, double* __restrict__ sumsq,
                                                           const int* __restrict__ zmap, int* __restrict__ nonfinite,
-                                                          const double* __restrict__ fixed_max) {
+                                                          const double* __restrict__ fixed_max, int nwrite) {
     constexpr int TPC = 256 / CPB;  // threads per column
     constexpr int WPC = TPC / 32;   // warps per column
     __shared__ double stage[kKC];
@@ -181,7 +181,8 @@ __global__ void __launch_bounds__(256) ozaki_split_kernel(const double* __restri
             for (int s = 1; s < ND; ++s) w[s] |= (uint32_t)((low >> (SH - 8 * s)) & 0xFFu) << (8 * q);
         }
 #pragma unroll
-        for (int s = 0; s < ND; ++s) *reinterpret_cast<uint32_t*>(out + s * plane + i4) = w[s];
+        for (int s = 0; s < ND; ++s)
+            if (s < nwrite) *reinterpret_cast<uint32_t*>(out + s * plane + i4) = w[s];
     }
 }
 
@@ -209,6 +210,12 @@ struct OzParams {
     const double* X;
     int64_t ldx, strideX, m_total;
     double* partial;
+    // Chebyshev step fused into the store (SYMA products only; cy nullable):
+    // C = a (A^T B) + b Y + c Yp with Y, Yp laid out as C and the output
+    // block's coefficients {a, b, c} at ccoef + 3 ob (subspace.cu's filter)
+    const double* cy = nullptr;
+    const double* cyp = nullptr;
+    const double* ccoef = nullptr;
 };
 
 // tile t (upper-triangle order) -> (mb, nb): column tile nb holds
@@ -403,6 +410,36 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                     for (int j = 0; j < NH; ++j) xv[j] = xrow && n0 + j < P.N ? __ldcs(X + (n0 + j) * P.ldx) : 0.0;
                 }
+                // fused Chebyshev step: b Y + c Yp in flight while the MMAs run
+                constexpr bool kCheb = SYMA && !RESID;
+                double pre[kCheb ? NH : 1];
+                double ca = 1.0;
+                const bool cheb = kCheb && P.cy != nullptr;
+                if constexpr (kCheb) {
+                    if (cheb) {
+                        const double* cf = P.ccoef + 3 * ob;
+                        ca = cf[0];
+                        const double cb = cf[1], cc = cf[2];
+                        const bool row = m < P.M;
+                        const double* y = P.cy + ob * P.strideC + m;
+                        const double* yp = P.cyp + ob * P.strideC + m;
+                        // 16 loads in flight per round (the first use of a load
+                        // waits for it: four DRAM round trips, not NH)
+#pragma unroll
+                        for (int c8 = 0; c8 < NH; c8 += 8) {
+                            double ya[8], yb[8];
+#pragma unroll
+                            for (int jj = 0; jj < 8; ++jj) {
+                                const int64_t n = n0 + c8 + jj;
+                                const bool ok = row && n < P.N;
+                                ya[jj] = ok ? __ldcs(y + n * P.ldc) : 0.0;
+                                yb[jj] = ok && cc != 0.0 ? __ldcs(yp + n * P.ldc) : 0.0;
+                            }
+#pragma unroll
+                            for (int jj = 0; jj < 8; ++jj) pre[c8 + jj] = fma(cc, yb[jj], cb * ya[jj]);
+                        }
+                    }
+                }
                 bar_wait(tfull, (uint32_t)(cg & 1));
                 fence_after_sync();
                 const double sm = m < P.M ? (P.sa ? P.sa[ob * P.M + m] : 1.0) : 0.0;
@@ -428,7 +465,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                             rsd = fma(r, r, rsd);
                             rsx = fma(xv[j], xv[j], rsx);
                         } else if (m < P.M && n < P.N && (P.m_total == 0 || ob * P.M + m < P.m_total)) {
-                            C[m + n * P.ldc] = val;  // (m, n), coalesced over the warp's rows
+                            if constexpr (kCheb)
+                                C[m + n * P.ldc] = cheb ? fma(ca, val, pre[j]) : val;
+                            else
+                                C[m + n * P.ldc] = val;  // (m, n), coalesced over the warp's rows
                         }
                     }
                 }
@@ -528,6 +568,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 // 3-D uint8 map over the digit planes: (k, row, plane), box (kBK, rows, 1),
 // SWIZZLE_64B (rows beyond `cols` read as zeros: they never reach another plane).
 bool make_digit_map(CUtensorMap* map, const int8_t* D, int64_t KCp, int64_t cols, int64_t planes, int box_rows) {
+    HostProf hp_("make_digit_map");
     auto fn = encode_fn();
     if (!fn) return false;
     cuuint64_t dims[3] = {(cuuint64_t)KCp, (cuuint64_t)cols, (cuuint64_t)planes};
@@ -637,7 +678,8 @@ void ozaki_syrk(const OzakiDigits& d, int64_t nout, int64_t per, double* out, cu
 void OzakiDigits::split(const double* X, int64_t ldx, int64_t stride, int64_t rows_, int64_t cols_, int64_t KC,
                         int64_t nblk_, cudaStream_t s, const int* zmap, int64_t nz, int64_t chunk, int64_t per,
                         int* nonfinite, int ndig, int64_t block_base, int64_t alloc_blocks,
-                        const double* fixed_max) {
+                        const double* fixed_max, int nwrite) {
+    HostProf hp_("ozaki_split");
     if (ndig != kS && ndig != kSmax) fail(PPC_ARGUMENT, "ozaki split: 6 or 7 digits");
     if (block_base < 0 || (block_base > 0 && block_base + nblk_ > alloc_blocks))
         fail(PPC_ARGUMENT, "ozaki split: block range outside the allocation");
@@ -656,7 +698,8 @@ void OzakiDigits::split(const double* X, int64_t ldx, int64_t stride, int64_t ro
     const int64_t launched = zmap ? nz : ncall;
     if (launched <= 0) return;
     const double total_rows = stride ? (double)std::min(KC, rows) * launched : (double)rows;
-    StageTimer ts("ozaki_split", s, 0.0, 8.0 * total_rows * cols + (double)nd * total_rows * cols);
+    StageTimer ts("ozaki_split", s, 0.0,
+                  8.0 * total_rows * cols + (double)((nwrite > 0 && nwrite < nd) ? nwrite : nd) * total_rows * cols);
     int8_t* D0 = D.as<int8_t>() + (size_t)block_base * nd * cols * KCp;
     double* sc0 = sc.d() + block_base * cols;
     double* sq0 = sq.d() + block_base * cols;
@@ -664,9 +707,10 @@ void OzakiDigits::split(const double* X, int64_t ldx, int64_t stride, int64_t ro
     const int cpb = KCp <= 512 ? 8 : (KCp <= 1024 ? 4 : (KCp <= 2048 ? 2 : 1));
     dim3 grid((unsigned)((cols + cpb - 1) / cpb), (unsigned)launched);
     const int64_t ch = chunk ? chunk : KC, pr = per ? per : 1;
+    const int nw = (nwrite > 0 && nwrite < nd) ? nwrite : nd;  // leading planes written
 #define PPC_SPLIT(ND_, CPB_)                                                                                         \
     ozaki_split_kernel<ND_, CPB_><<<grid, 256, 0, s>>>(X, ldx, stride, rows, cols, KC, KCp, ch, pr, D0, sc0, sq0,    \
-                                                       zmap, nonfinite, fixed_max)
+                                                       zmap, nonfinite, fixed_max, nw)
     if (nd == kSmax) {
         if (cpb == 8) PPC_SPLIT(kSmax, 8); else if (cpb == 4) PPC_SPLIT(kSmax, 4);
         else if (cpb == 2) PPC_SPLIT(kSmax, 2); else PPC_SPLIT(kSmax, 1);
@@ -680,7 +724,8 @@ void OzakiDigits::split(const double* X, int64_t ldx, int64_t stride, int64_t ro
 }
 
 void ozaki_gemm(const OzakiDigits& A, const OzakiDigits& B, int64_t nbatch, const int* zmap, double* C, int64_t ldc,
-                int64_t strideC, cudaStream_t s, int levels, bool sym_a) {
+                int64_t strideC, cudaStream_t s, int levels, bool sym_a, const ChebFuse* cheb) {
+    HostProf hp_("ozaki_gemm");
     if (A.KCp != B.KCp) fail(PPC_ARGUMENT, "ozaki_gemm: K mismatch");
     if (levels != kS && levels != 4 && levels != 3) fail(PPC_ARGUMENT, "ozaki_gemm: levels must be 6, 4 or 3");
     // 64-wide output tiles for panels of <= 64 columns (the 80-wide tile
@@ -711,6 +756,13 @@ void ozaki_gemm(const OzakiDigits& A, const OzakiDigits& B, int64_t nbatch, cons
     P.ldx = P.strideX = P.m_total = 0;
     P.partial = nullptr;
     const double K = (double)std::min(A.rows, kKC);
+    if (cheb) {
+        if (!(sym_a && bn == 64 && A.cols == A.rows && A.KCp == A.cols && A.nd == kS))
+            fail(PPC_ARGUMENT, "ozaki_gemm: the fused Chebyshev step needs a symmetric A");
+        P.cy = cheb->Y;
+        P.cyp = cheb->Yp;
+        P.ccoef = cheb->coef;
+    }
     StageTimer tk(levels == kS ? "ozaki_gemm" : (levels == 4 ? "ozaki_gemm_l4" : "ozaki_gemm_l3"), s,
                   2.0 * levels * (levels + 1) / 2 * (double)nbatch * P.M * P.N * K,
                   (double)levels * nbatch * (P.M + P.N) * K);

@@ -23,11 +23,13 @@ struct OzakiDigits {
     void split(const double* X, int64_t ldx, int64_t stride, int64_t rows, int64_t cols, int64_t KC, int64_t nblk,
                cudaStream_t s, const int* zmap = nullptr, int64_t nz = 0, int64_t chunk = 0, int64_t per = 0,
                int* nonfinite = nullptr, int ndig = 6, int64_t block_base = 0, int64_t alloc_blocks = 0,
-               const double* fixed_max = nullptr);
+               const double* fixed_max = nullptr, int nwrite = 0);
     // fixed_max (device, per block): a bound on max|x| over the whole block,
     // giving every column the same scale (symmetric operands, sym_a below).
     // block_base / alloc_blocks: this call's nblk_ blocks land at block_base of an
     // allocation of max(nblk_, alloc_blocks) blocks (streamed row groups).
+    // nwrite (0: all): only the leading nwrite digit planes are written, for
+    // operands of reduced-level products (levels <= nwrite read no others).
 };
 
 // C_b (A.cols x B.cols, (m, n) at m + n*ldc, b at blk*strideC) = A_blk^T B_blk
@@ -38,8 +40,16 @@ struct OzakiDigits {
 // that only steer an iteration (the Chebyshev filter far from convergence).
 // sym_a: A's blocks are symmetric and split with one scale per block
 // (fixed_max): A is streamed from its upper triangles only (half the reads).
+// cheb (nullable, sym_a only): C = a (A^T B) + b Y + c Yp instead of A^T B,
+// with Y and Yp laid out as C and the block's {a, b, c} at coef + 3 zmap[b]
+// (one Chebyshev filter step fused into the store).
+struct ChebFuse {
+    const double* Y;
+    const double* Yp;
+    const double* coef;
+};
 void ozaki_gemm(const OzakiDigits& A, const OzakiDigits& B, int64_t nbatch, const int* zmap, double* C, int64_t ldc,
-                int64_t strideC, cudaStream_t s, int levels = 6, bool sym_a = false);
+                int64_t strideC, cudaStream_t s, int levels = 6, bool sym_a = false, const ChebFuse* cheb = nullptr);
 // Whether the Gram partials of a plan with chunks of `chunk` rows run on the
 // integer path (a function of the plan only, see ozaki_gram_partials).
 bool ozaki_gram_eligible(int64_t n3, int64_t chunk);

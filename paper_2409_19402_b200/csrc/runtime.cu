@@ -2,11 +2,13 @@
 // workspace, host<->device staging. Replaces the reference's L2 runtime
 // (parallel.cpp:13-57: slice loops over std::threads) with CUDA grids on one
 // device per host thread.
+#include <algorithm>
 #include <chrono>
 #include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <string>
 #include <vector>
 
 #include "internal.h"
@@ -158,6 +160,7 @@ void trim_workspace() {
 }
 
 DeviceBuffer::DeviceBuffer(size_t bytes) : n_(bytes) {
+    HostProf hp_("DeviceBuffer");
     if (!bytes) return;
     cudaStream_t s = stream();
     if (bytes >= kBigBytes) {
@@ -211,6 +214,7 @@ DeviceBuffer::DeviceBuffer(size_t bytes) : n_(bytes) {
 }
 DeviceBuffer::~DeviceBuffer() { release(); }
 void DeviceBuffer::release() {
+    HostProf hp_("DeviceBuffer::release");
     if (p_) {
         if (dev_ >= 0) {
             BigCache& c = t_big[dev_];
@@ -286,6 +290,7 @@ thread_local std::map<std::string, StageRec> t_stages;
 
 StageTimer::StageTimer(const char* name, cudaStream_t s, double flops, double bytes)
     : name_(name), s_(s), flops_(flops), bytes_(bytes) {
+    HostProf hp_("StageTimer");
     if (!t_timing) return;
     cudaEventCreate(&e0_);
     cudaEventRecord(e0_, s_);
@@ -300,6 +305,43 @@ StageTimer::~StageTimer() {
     r.flops += flops_;
     r.bytes += bytes_;
     r.launches += 1;
+}
+
+namespace {
+struct HostProfTable {
+    std::map<std::string, std::pair<double, long long>> t;  // ms, calls
+    ~HostProfTable() {
+        if (t.empty()) return;
+        std::vector<std::pair<double, std::string>> v;
+        for (auto& kv : t) v.push_back({kv.second.first, kv.first});
+        std::sort(v.rbegin(), v.rend());
+        for (auto& e : v)
+            fprintf(stderr, "[host] %-28s %9.3f ms  %7lld calls  %8.2f us/call\n", e.second.c_str(), e.first,
+                    t[e.second].second, 1e3 * e.first / (double)t[e.second].second);
+    }
+};
+HostProfTable g_hostprof;
+std::mutex g_hostprof_mu;
+bool host_prof_on() {
+    static const bool on = std::getenv("PPC_HOST_PROFILE") != nullptr;
+    return on;
+}
+long long now_ns() {
+    return std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now().time_since_epoch())
+        .count();
+}
+}  // namespace
+
+HostProf::HostProf(const char* name) : name_(name) {
+    if (host_prof_on()) t0_ = now_ns();
+}
+HostProf::~HostProf() {
+    if (t0_ < 0) return;
+    const double ms = (now_ns() - t0_) / 1e6;
+    std::lock_guard<std::mutex> g(g_hostprof_mu);
+    auto& e = g_hostprof.t[name_];
+    e.first += ms;
+    e.second += 1;
 }
 
 void set_error(const std::string& m) { t_err = m; }

@@ -18,6 +18,7 @@
 // one CTA per slice. The host drives the iteration and reads back only the
 // b Ritz values and residual norms per slice per iteration.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -30,6 +31,7 @@
 #include "jacobi.cuh"
 #include "kernels.cuh"
 #include "ozaki.h"
+#include "panel.cuh"
 #include "slice_svd.cuh"
 
 namespace ppc {
@@ -86,11 +88,13 @@ __global__ void cheb_kernel(double* __restrict__ Yn, const double* __restrict__ 
 
 // P(i, j, s) *= w(i, s)   (rows of the lp x cols block scaled: Theta_L mask;
 // w has stride b per slice)
-__global__ void scale_rows_kernel(double* P, const double* w, int64_t lp, int64_t b, int64_t cols, int64_t total) {
+// coef (nullable): also times the slice's Chebyshev coefficient a = coef[3 s]
+__global__ void scale_rows_kernel(double* P, const double* w, int64_t lp, int64_t b, int64_t cols, int64_t total,
+                                  const double* __restrict__ coef) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
         const int64_t row = i % lp, s = i / (lp * cols);
-        P[i] *= w[row + s * b];
+        P[i] *= coef ? w[row + s * b] * coef[3 * s] : w[row + s * b];
     }
 }
 
@@ -147,9 +151,12 @@ __global__ void residual_kernel(const double* GX, const double* X, const double*
 // x(l + 32 t)), each back-substitution step is a lane-parallel dot with a
 // fixed butterfly reduction.
 constexpr int kCholSlots = 5;  // x slots per lane: b <= 160
+// nsplit > 1: S holds nsplit split-K partials at S + t*sstride, summed here
+// in split order (fixed: the same bits as one pass over K in that order).
 __global__ void __launch_bounds__(1024, 1) chol_inv_kernel(const double* __restrict__ S, double* __restrict__ Rinv, int64_t b64,
                                 int shift_pass, int* fail, double* __restrict__ Rout,
-                                const int* __restrict__ zmap = nullptr, int* __restrict__ weak = nullptr) {
+                                const int* __restrict__ zmap = nullptr, int* __restrict__ weak = nullptr,
+                                int nsplit = 1, int64_t sstride = 0) {
     extern __shared__ __align__(16) double M[];
     __shared__ double dinv[160];  // 1 / R(i,i)
     __shared__ unsigned char badk[160];  // pivot k broke down (a zero column)
@@ -159,7 +166,11 @@ __global__ void __launch_bounds__(1024, 1) chol_inv_kernel(const double* __restr
     const double* Sin = S + sl * b64 * b64;
     const int tid = threadIdx.x, nt = blockDim.x;
     const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
-    for (int i = tid; i < b * b; i += nt) M[i] = Sin[i];
+    for (int i = tid; i < b * b; i += nt) {
+        double v = Sin[i];
+        for (int t = 1; t < nsplit; ++t) v += Sin[t * sstride + i];
+        M[i] = v;
+    }
     if (tid == 0) bad = 0;
     __syncthreads();
     if (shift_pass) {  // shifted CholQR (Fukaya et al.): tiny diagonal shift ~ u * trace
@@ -454,7 +465,7 @@ void g_AB(const double* A, const double* B, double* C, int64_t m, int64_t kk, in
 struct Work {
     int64_t r, b, batch;
     bool basis = false;  // eigenbasis Q (data_q) rather than slice SVDs: stage names sq.*
-    DeviceBuffer X, Y, Yp, Yn, Z, W, P, S, Rinv, Hv, th, res, coef, wmask, nlock, fail, zmap, glist;
+    DeviceBuffer X, Y, Yp, Yn, Z, W, P, S, Rinv, Hv, th, res, coef, wmask, nlock, fail, zmap, glist, Ssplit;
     Work(int64_t r_, int64_t b_, int64_t batch_)
         : r(r_), b(b_), batch(batch_),
           X(sizeof(double) * r_ * b_ * batch_), Y(sizeof(double) * r_ * b_ * batch_),
@@ -464,7 +475,10 @@ struct Work {
           Rinv(sizeof(double) * b_ * b_ * batch_), Hv(sizeof(double) * b_ * b_ * batch_),
           th(sizeof(double) * b_ * batch_), res(sizeof(double) * b_ * batch_),
           coef(sizeof(double) * 3 * batch_), wmask(sizeof(double) * b_ * batch_),
-          nlock(sizeof(int) * batch_), fail(sizeof(int) * 2), zmap(sizeof(int) * batch_) {}
+          nlock(sizeof(int) * batch_), fail(sizeof(int) * 2), zmap(sizeof(int) * batch_),
+          Ssplit(panel_kernels_ok(r_, std::min<int64_t>(b_, 64))
+                     ? sizeof(double) * b_ * b_ * batch_ * panel_splits(r_)
+                     : 0) {}
 };
 
 // General strided-batch GEMM on column panels: C = alpha op(A) B + beta C.
@@ -488,6 +502,7 @@ void gg(const double* A, int64_t lda, int64_t sA, bool at, const double* B, int6
 // cond(Y) up to ~1e15, two plain passes restore orthogonality.
 void cholqr3(Work& w, double* Y, double* Xout, int64_t c0, cudaStream_t s, const int* zm = nullptr,
              int64_t na = -1) {
+    HostProf hp_("cholqr3");
     const int64_t r = w.r, b = w.b, bc = b - c0, per = r * b;
     const int64_t batch = na < 0 ? w.batch : na;  // launched slices (zm: which ones)
     const int64_t zx = w.batch;
@@ -506,14 +521,22 @@ void cholqr3(Work& w, double* Y, double* Xout, int64_t c0, cudaStream_t s, const
                                             (int)smem));
     double* src = Y + c0 * r;
     double* bufs[3] = {w.Yn.d() + c0 * r, w.Z.d() + c0 * r, Xout + c0 * r};
+    const bool small = panel_kernels_ok(r, bc);
     for (int pass = 0; pass < 3; ++pass) {
-        gg(src, r, per, true, src, r, per, w.S.d(), bc, bc * bc, bc, bc, r, batch, 1.0, 0.0, s, zm, zx);  // S = Y^T Y
-        chol_inv_kernel<<<(unsigned)batch, bc > 16 ? 1024 : 256, smem, s>>>(w.S.d(), w.Rinv.d(), bc,
-                                                                             pass == 0 ? 1 : 0,
-                                                                             w.fail.as<int>(), nullptr, zm);
-        count_launch();
-        check_launch("chol_inv");
-        gg(src, r, per, false, w.Rinv.d(), bc, bc * bc, bufs[pass], r, per, r, bc, bc, batch, 1.0, 0.0, s, zm, zx);
+        if (small) {
+            // S = Y^T Y as split-K partials (panel.cu), summed by the Cholesky
+            panel_gram(src, per, src, per, r, bc, batch, w.S.d(), w.Ssplit.d(), zx, zm, s);
+            chol_inv64(w.S.d(), bc, batch, pass == 0, w.Rinv.d(), w.fail.as<int>(), zm, nullptr, s);
+            panel_apply(src, per, w.Rinv.d(), bufs[pass], per, r, bc, batch, zm, s);
+        } else {
+            gg(src, r, per, true, src, r, per, w.S.d(), bc, bc * bc, bc, bc, r, batch, 1.0, 0.0, s, zm, zx);
+            chol_inv_kernel<<<(unsigned)batch, bc > 16 ? 1024 : 256, smem, s>>>(
+                w.S.d(), w.Rinv.d(), bc, pass == 0 ? 1 : 0, w.fail.as<int>(), nullptr, zm);
+            count_launch();
+            check_launch("chol_inv");
+            gg(src, r, per, false, w.Rinv.d(), bc, bc * bc, bufs[pass], r, per, r, bc, bc, batch, 1.0, 0.0, s, zm,
+               zx);
+        }
         src = bufs[pass];
     }
 }
@@ -556,6 +579,7 @@ namespace {
 void rayleigh_ritz(Work& w, const double* G, int64_t sG, double* Xn, int64_t c0, cudaStream_t s,
                    double gtol_rel, int sweep_cap, const int* zm = nullptr, int64_t na = -1,
                    const OzakiDigits* Gd = nullptr, OzakiDigits* Xd = nullptr) {
+    HostProf hp_("rayleigh_ritz");
     const int64_t r = w.r, b = w.b, bc = b - c0, per = r * b;
     const int64_t batch = na < 0 ? w.batch : na;  // launched slices (zm: which ones)
     const int64_t zx = w.batch;
@@ -571,8 +595,13 @@ void rayleigh_ritz(Work& w, const double* G, int64_t sG, double* Xn, int64_t c0,
         gg(G, r, sG, false, Xn + c0 * r, r, per, w.Z.d() + c0 * r, r, per, r, bc, r, batch, 1.0, 0.0, s, zm,
            zx);  // Z = G Xn
     }
-    gg(Xn + c0 * r, r, per, true, w.Z.d() + c0 * r, r, per, w.S.d(), bc, bc * bc, bc, bc, r, batch, 1.0, 0.0, s,
-       zm, zx);
+    const bool small = panel_kernels_ok(r, bc);
+    if (small) {  // H = Xn^T Z (= Xn^T G Xn): upper triangle, mirrored
+        panel_gram(Xn + c0 * r, per, w.Z.d() + c0 * r, per, r, bc, batch, w.S.d(), w.Ssplit.d(), zx, zm, s);
+    } else {
+        gg(Xn + c0 * r, r, per, true, w.Z.d() + c0 * r, r, per, w.S.d(), bc, bc * bc, bc, bc, r, batch, 1.0, 0.0, s,
+           zm, zx);
+    }
     {
         StageTimer tj(w.basis ? "sq.rr_eig" : "ss.rr_eig", s);
         // H (PSD) = Hv diag(theta) Hv^T by one-sided Jacobi (eigen mode)
@@ -582,10 +611,15 @@ void rayleigh_ritz(Work& w, const double* G, int64_t sG, double* Xn, int64_t c0,
     copy_theta_kernel<<<(unsigned)batch, 64, 0, s>>>(w.th.d(), w.P.d(), b, bc, c0, zm);
     count_launch();
     check_launch("copy_theta");
-    gg(Xn + c0 * r, r, per, false, w.Hv.d(), bc, bc * bc, w.X.d() + c0 * r, r, per, r, bc, bc, batch, 1.0, 0.0, s,
-       zm, zx);
-    gg(w.Z.d() + c0 * r, r, per, false, w.Hv.d(), bc, bc * bc, w.W.d() + c0 * r, r, per, r, bc, bc, batch, 1.0,
-       0.0, s, zm, zx);
+    if (small) {
+        panel_apply(Xn + c0 * r, per, w.Hv.d(), w.X.d() + c0 * r, per, r, bc, batch, zm, s);
+        panel_apply(w.Z.d() + c0 * r, per, w.Hv.d(), w.W.d() + c0 * r, per, r, bc, batch, zm, s);
+    } else {
+        gg(Xn + c0 * r, r, per, false, w.Hv.d(), bc, bc * bc, w.X.d() + c0 * r, r, per, r, bc, bc, batch, 1.0, 0.0,
+           s, zm, zx);
+        gg(w.Z.d() + c0 * r, r, per, false, w.Hv.d(), bc, bc * bc, w.W.d() + c0 * r, r, per, r, bc, bc, batch, 1.0,
+           0.0, s, zm, zx);
+    }
     dim3 grid((unsigned)((b + 7) / 8), (unsigned)batch);
     residual_kernel<<<grid, 256, 0, s>>>(w.W.d(), w.X.d(), w.th.d(), w.res.d(), r, b, zm);
     count_launch();
@@ -638,6 +672,7 @@ void slice_tail_energy(const double* A, int64_t m, int64_t n, int64_t stride, in
 // Xout (r, k, batch), lambda (k, batch). Deterministic.
 void subspace_eig_top(const double* G, int64_t r, int64_t batch, int64_t k, double* Xout,
                       double* lambda, cudaStream_t s, bool vectors_for_reconstruction) {
+    HostProf hp_("subspace_eig_top");
     static const bool dbg = std::getenv("PPC_SUBSPACE_DEBUG") != nullptr;
     static const int64_t guard_env = std::getenv("PPC_SUBSPACE_GUARD") ? std::atoll(std::getenv("PPC_SUBSPACE_GUARD")) : 0;
     int64_t b = k + (guard_env > 0 ? guard_env : std::max<int64_t>(k, 16));
@@ -689,10 +724,19 @@ void subspace_eig_top(const double* G, int64_t r, int64_t batch, int64_t k, doub
     std::vector<double> prev_rmin(batch, 1e300);
     std::vector<char> cap(batch, 2);
     const int max_iter = 100;
+    auto tprev = std::chrono::steady_clock::now();
     for (int it = 0; it < max_iter; ++it) {
         PPC_CUDA_CHECK(cudaMemcpyAsync(th.data(), w.th.d(), sizeof(double) * b * batch, cudaMemcpyDeviceToHost, s));
         PPC_CUDA_CHECK(cudaMemcpyAsync(res.data(), w.res.d(), sizeof(double) * b * batch, cudaMemcpyDeviceToHost, s));
+        const auto tq = std::chrono::steady_clock::now();
         PPC_CUDA_CHECK(cudaStreamSynchronize(s));
+        if (dbg) {  // host time of the last iteration (the pageable D2H above already waited for the GPU)
+            const auto tw = std::chrono::steady_clock::now();
+            fprintf(stderr, "[subspace] it %d host enqueue %.3f ms, wait %.3f ms\n", it,
+                    std::chrono::duration<double, std::milli>(tq - tprev).count(),
+                    std::chrono::duration<double, std::milli>(tw - tq).count());
+            tprev = tw;
+        }
         bool all_done = true;
         int dmax = 0;
         // ||A||^2 ~ sum of the slices' captured energies (top-b Ritz values)
@@ -889,19 +933,32 @@ void subspace_eig_top(const double* G, int64_t r, int64_t batch, int64_t k, doub
                 // only the slices still filtering at this degree (compacted batch)
                 const int na = nact[j];
                 const int* zm = w.zmap.as<int>() + (int64_t)j * batch;
+                const double* cfj = w.coef.d() + 3 * (int64_t)j * batch;
+                // INT8 filter: the Chebyshev step rides on the product's store
+                // (Yn = a (G Y) + b Y + c Yp straight from TMEM; columns below cf
+                // of Yn are never read: locked in every filtering slice, they are
+                // restored from X after the filter)
+                const bool fused = oz_filter && !near_floor && bf <= 64;
                 if (na > 0) {
                     // Z = G Y, P = X^T Y, Z -= X diag(theta_L) P   (columns [cf, b))
                     if (oz_filter && !near_floor) {
-                        Yd.split(Y + cf * r, r, per, r, bf, r, batch, s, zm, na);
+                        const bool split = bf <= 64 && nlo[j] + nl3[j] > 0;
+                        // only the digit planes this degree's products read
+                        const int planes = !split || nhi[j] > 0 ? 6 : (nlo[j] > 0 ? 4 : 3);
+                        Yd.split(Y + cf * r, r, per, r, bf, r, batch, s, zm, na, 0, 0, nullptr, 6, 0, 0, nullptr,
+                                 planes);
                         const int* zlo = w.zmap.as<int>() + (int64_t)(dmax + j) * batch;
                         const int* zhi = w.zmap.as<int>() + (int64_t)(2 * dmax + j) * batch;
                         const int* zl3 = w.zmap.as<int>() + (int64_t)(3 * dmax + j) * batch;
-                        if (bf <= 64 && nlo[j] + nl3[j] > 0) {
-                            if (nl3[j] > 0) ozaki_gemm(Gd, Yd, nl3[j], zl3, w.Z.d() + cf * r, r, per, s, 3, true);
-                            if (nlo[j] > 0) ozaki_gemm(Gd, Yd, nlo[j], zlo, w.Z.d() + cf * r, r, per, s, 4, true);
-                            if (nhi[j] > 0) ozaki_gemm(Gd, Yd, nhi[j], zhi, w.Z.d() + cf * r, r, per, s, 6, true);
+                        const ChebFuse cfu{Y + cf * r, Yp + cf * r, cfj};
+                        const ChebFuse* cp = fused ? &cfu : nullptr;
+                        double* out = fused ? Yn + cf * r : w.Z.d() + cf * r;
+                        if (split) {
+                            if (nl3[j] > 0) ozaki_gemm(Gd, Yd, nl3[j], zl3, out, r, per, s, 3, true, cp);
+                            if (nlo[j] > 0) ozaki_gemm(Gd, Yd, nlo[j], zlo, out, r, per, s, 4, true, cp);
+                            if (nhi[j] > 0) ozaki_gemm(Gd, Yd, nhi[j], zhi, out, r, per, s, 6, true, cp);
                         } else {
-                            ozaki_gemm(Gd, Yd, na, zm, w.Z.d() + cf * r, r, per, s, 6, true);
+                            ozaki_gemm(Gd, Yd, na, zm, out, r, per, s, 6, true, cp);
                         }
                     } else {
                         gg(G, r, r * r, false, Y + cf * r, r, per, w.Z.d() + cf * r, r, per, r, bf, r, na, 1.0, 0.0,
@@ -912,16 +969,17 @@ void subspace_eig_top(const double* G, int64_t r, int64_t batch, int64_t k, doub
                     if (lmax > 0) {
                         gg(w.X.d(), r, per, true, Y + cf * r, r, per, w.P.d(), lmax, lmax * bf, lmax, bf, r, na, 1.0,
                            0.0, s, zm, batch);
-                        scale_rows_kernel<<<grid1(lmax * bf * batch), 256, 0, s>>>(w.P.d(), w.wmask.d(), lmax, b, bf,
-                                                                                    lmax * bf * batch);
+                        // fused: the correction lands on Yn, scaled by the slice's a
+                        scale_rows_kernel<<<grid1(lmax * bf * batch), 256, 0, s>>>(
+                            w.P.d(), w.wmask.d(), lmax, b, bf, lmax * bf * batch, fused ? cfj : nullptr);
                         count_launch();
-                        gg(w.X.d(), r, per, false, w.P.d(), lmax, lmax * bf, w.Z.d() + cf * r, r, per, r, bf, lmax, na,
-                           -1.0, 1.0, s, zm, batch);
+                        gg(w.X.d(), r, per, false, w.P.d(), lmax, lmax * bf, (fused ? Yn : w.Z.d()) + cf * r, r, per,
+                           r, bf, lmax, na, -1.0, 1.0, s, zm, batch);
                     }
                 }
                 // only the slices still filtering at this degree; a slice that
                 // stops keeps its block in its own buffer of the rotation
-                if (na > 0) {
+                if (na > 0 && !fused) {
                     cheb_kernel<<<grid1(per * na), 256, 0, s>>>(Yn, w.Z.d(), Y, Yp, w.coef.d() + 3 * j * batch,
                                                                 per, per * na, r, cf, zm);
                     count_launch();
