@@ -776,7 +776,7 @@ int ppc_tsvdq_compress(const double* A, int64_t n1, int64_t n2, int64_t n3, int6
         } else {
             data_q(dA, N, n3, p, q.d, sigma ? sg.d : nullptr, s, true, est.d(), &tdig);
         }
-        tsvdq(dA, n1, n2, n3, q.d, p, k, u.d, sv.d, v.d, s, est.d() + 1, &tdig);
+        tsvdq(dA, n1, n2, n3, q.d, p, k, u.d, sv.d, v.d, s, est.d() + 1, &tdig, est.d());
         tdig = OzakiDigits();  // the 7-digit split of A (30 GB at cfg5) is not needed past the transform
         *re = compress_relative_error(dA, n1, n2, n3, u.d, sv.d, v.d, q.d, p, k, est.d(), s);
         q.finish();

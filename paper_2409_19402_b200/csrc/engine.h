@@ -106,12 +106,14 @@ double compress_relative_error(const double* A, int64_t n1, int64_t n2, int64_t 
 void slice_residual_sums(const double* Ah, int64_t n1, int64_t n2, int64_t p, int64_t k, const double* U,
                          const double* S, const double* V, double* out, cudaStream_t s);
 // slice_sums (device, nullable, 2 doubles): {sum_i ||Ahat_i - U_i S_i V_i^T||^2, ||Ahat||^2},
-// measured directly on the transform-domain slices (fused residual GEMM).
+// measured directly on the transform-domain slices (fused residual GEMM);
+// with a2 (device, ||A||^2) and ||A||^2 - sum s^2 >= 2e-2 ||A||^2 they are
+// {0, sum s^2} instead (Eckart-Young through the polish, no pass over Ahat).
 // tdig (nullable): A's retained 7-digit Gram split; the forward transform
 // then runs on the INT8 tensor cores (ozaki_mode3_forward).
 void tsvdq(const double* A, int64_t n1, int64_t n2, int64_t n3, const double* Q, int64_t p,
            int64_t k, double* U, double* S, double* V, cudaStream_t s, double* slice_sums = nullptr,
-           const OzakiDigits* tdig = nullptr);
+           const OzakiDigits* tdig = nullptr, const double* a2 = nullptr);
 // Chat (n1 x n2 x p) = U diag(S) V^T facewise             [decompositions.cpp:88-92]
 // over the leading k columns of factor stacks that carry kstride >= k
 // columns per slice (kstride 0 = k).

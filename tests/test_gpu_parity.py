@@ -1140,20 +1140,34 @@ def test_nonfinite_input_rejected(engine, shape, val):
 
 @pytest.mark.gpu
 def test_compress_re_identity_matches_direct(engine):
-    """ppc_tsvdq_compress takes RE from the orthogonal split
+    """ppc_tsvdq_compress takes RE from ||A||^2 - sum s_ij^2 (Eckart-Young
+    through the polish) when RE^2 >= 2e-2, from the orthogonal split
     ||A - A_k||^2 = (||A||^2 - ||Ahat||^2) + sum_i ||Ahat_i - U_i S_i V_i^T||^2
-    (Q orthonormal) when RE^2 >= 2e-3, and measures it against the
-    reconstruction otherwise; both must equal the directly measured
-    relative_error(A, tsvdq_reconstruct(F))."""
-    cases = [((256, 192, 128), 32, 8, 1e-3),   # RE ~ 0.3: identity
-             ((192, 160, 96), 64, 4, 1e-2),    # noisy, many noise slices: identity
-             ((128, 128, 64), 48, 24, 1e-9)]   # rank 20 < k: RE ~ 1e-9, direct fallback
-    for shape, p, k, noise in cases:
-        a = synth.cp_tensor(*shape, rank=20, noise=noise, seed=5)
+    (Q orthonormal; one fused residual pass over Ahat) when 2e-3 <= RE^2 <
+    2e-2, and measures it against the reconstruction below; all three must
+    equal the directly measured relative_error(A, tsvdq_reconstruct(F)), and
+    the slice residual pass runs exactly below RE^2 = 2e-2."""
+    import ctypes as C
+    from paper_2409_19402_b200 import _lib
+    L = _lib.lib()
+    cases = [((256, 192, 128), 32, 8, 1e-3, 20),   # RE ~ 0.3: singular values
+             ((192, 160, 96), 64, 4, 1e-2, 20),    # noisy, many noise slices: singular values
+             ((128, 128, 64), 48, 16, 1e-2, 20),   # RE^2 ~ 5.7e-3: slice residual pass
+             ((128, 96, 64), 32, 12, 1e-2, 16),    # RE^2 ~ 8.4e-3: slice residual pass
+             ((128, 128, 64), 48, 24, 1e-9, 20)]   # rank 20 < k: RE ~ 1e-9, direct fallback
+    buf = C.create_string_buffer(1 << 16)
+    for shape, p, k, noise, rank in cases:
+        a = synth.cp_tensor(*shape, rank=rank, noise=noise, seed=5)
         da = engine.to_device(a)
+        L.ppc_timing_report(buf, len(buf), 1)
+        L.ppc_timing_enable(1)
         f, re = engine.compress_tsvdq(da, p, k)
+        L.ppc_timing_report(buf, len(buf), 1)
+        L.ppc_timing_enable(0)
         red = engine.tsvdq_relative_error(da, f)
         assert abs(re - red) <= 1e-12 * red, (shape, re, red)
+        residual_pass = "slice_residual" in buf.value.decode()
+        assert residual_pass == (red * red < 2e-2), (shape, red, residual_pass)
 
 
 @pytest.mark.gpu
