@@ -380,11 +380,11 @@ void tsvdq(const double* A, int64_t n1, int64_t n2, int64_t n3, const double* Q,
     DeviceBuffer ah(sizeof(double) * N * p);
     if (!(tdig && ozaki_mode3_forward(*tdig, N, Q, p, ah.d(), s)))
         mode3(A, N, n3, Q, p, true, ah.d(), 1.0, s);  // decompositions.cpp:65
-    require_finite(ah.d(), N * p, "svd", s);       // matrix_kernels.cpp:32
     {
         StageTimer tm("slice_svd", s, (double)p * std::min(n1, n2) * std::min(n1, n2) * std::max(n1, n2) +
                                           4.0 * p * N * k, 8.0 * p * N);
-        slice_svd(ah.d(), n1, n2, N, p, k, U, S, V, nullptr, s);  // :75-81
+        // :75-81, with the input check of matrix_kernels.cpp:32
+        slice_svd(ah.d(), n1, n2, N, p, k, U, S, V, nullptr, s, "svd");
     }
     if (!slice_sums) return;
     // Eckart-Young through the polish: U_i S_i V_i^T = Ahat_i V_k V_k^T for the

@@ -45,8 +45,11 @@ void require_finite(const double* x, int64_t n, const char* who, cudaStream_t s)
 
 // Batched thin SVD (leading k triplets) of `batch` m x n blocks at `stride`.
 // tail2 (device, nullable, length batch): sum_{j>=k} s_j^2 per block.
+// finite_who (nullable): check the (contiguous) input for NaN/Inf first, as
+// the reference's SVD does (matrix_kernels.cpp:32): PPC_NUMERIC "<who>: input
+// has non-finite entries" (inside the INT8 slice-Gram split when it runs).
 void slice_svd(const double* A, int64_t m, int64_t n, int64_t stride, int64_t batch, int64_t k,
-               double* U, double* S, double* V, double* tail2, cudaStream_t s);
+               double* U, double* S, double* V, double* tail2, cudaStream_t s, const char* finite_who = nullptr);
 
 // Deterministic Gram G = T^T T (n3 x n3) over the N rows of T (SYRK).
 // nonfinite (nullable device int): when the Gram's own pass over T can also

@@ -988,12 +988,12 @@ bool ozaki_mode3_forward(const OzakiDigits& td, int64_t N, const double* Q, int6
 }
 
 bool ozaki_syrk_batched(const double* A, int64_t lda, int64_t strideA, int64_t rows, int64_t n, int64_t batch,
-                        double* G, cudaStream_t s) {
+                        double* G, cudaStream_t s, int* nonfinite) {
     if (!ozaki_enabled()) return false;
     if (n < 128 || rows < 1024 || rows > kKC || batch < 1) return false;
     if (strideA < lda * n) return false;
     OzakiDigits d;
-    d.split(A, lda, strideA, rows, n, rows, batch, s);
+    d.split(A, lda, strideA, rows, n, rows, batch, s, nullptr, 0, 0, 0, nonfinite);
     ozaki_syrk(d, batch, 1, G, s, "ozaki_syrk_batched", (double)rows * batch);
     return true;
 }

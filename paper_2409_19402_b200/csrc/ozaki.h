@@ -105,7 +105,9 @@ bool ozaki_mode3_forward(const OzakiDigits& td, int64_t N, const double* Q, int6
 // G_b (n x n, column-major, b < batch, stride n*n) = A_b^T A_b for A_b
 // (rows x n, leading dimension lda) at A + b*strideA: the batched slice
 // Grams. rows <= 4096. Returns false when not eligible.
+// nonfinite (nullable device int): set to 1 if any entry of the rows x n
+// blocks is NaN or Inf (the split reads every value once).
 bool ozaki_syrk_batched(const double* A, int64_t lda, int64_t strideA, int64_t rows, int64_t n, int64_t batch,
-                        double* G, cudaStream_t s);
+                        double* G, cudaStream_t s, int* nonfinite = nullptr);
 
 }  // namespace ppc

@@ -233,8 +233,14 @@ bool data_q(const double* T, int64_t N, int64_t n3, int64_t p, double* Q, double
 }
 
 void slice_svd(const double* A, int64_t m, int64_t n, int64_t stride, int64_t batch, int64_t k,
-               double* U, double* S, double* V, double* tail2, cudaStream_t s) {
+               double* U, double* S, double* V, double* tail2, cudaStream_t s, const char* finite_who) {
     const int64_t r = std::min(m, n);
+    const bool sub = !(r <= kSubspaceMinN || jacobi_smem_bytes(m, n) <= 200 * 1024) && !(k > r / 2);
+    if (finite_who && !(sub && m >= n && ozaki_path_on())) {  // no INT8 slice-Gram split to ride on
+        if (stride != m * n) fail(PPC_ARGUMENT, "slice_svd: the finiteness check needs contiguous slices");
+        require_finite(A, m * n * batch, finite_who, s);  // matrix_kernels.cpp:32
+        finite_who = nullptr;
+    }
     if (r <= kSubspaceMinN || jacobi_smem_bytes(m, n) <= 200 * 1024) {
         jacobi_svd(A, m, n, stride, batch, k, U, S, V, tail2, s);
         return;
@@ -246,7 +252,11 @@ void slice_svd(const double* A, int64_t m, int64_t n, int64_t stride, int64_t ba
             jacobi_svd(A, m, n, stride, batch, k, U, S, V, tail2, s);
         return;
     }
-    subspace_svd(A, m, n, stride, batch, k, U, S, V, tail2, s);
+    if (!subspace_svd(A, m, n, stride, batch, k, U, S, V, tail2, s, finite_who) && finite_who) {
+        // the INT8 split did not run after all (shape not eligible): its checks
+        // were skipped, so check now (results are discarded on failure)
+        require_finite(A, m * n * batch, finite_who, s);
+    }
 }
 
 }  // namespace ppc

@@ -58,7 +58,10 @@ void slice_tail_energy(const double* A, int64_t m, int64_t n, int64_t stride, in
 bool block_jacobi_eligible(int64_t m, int64_t n, int64_t k);
 void block_jacobi_svd(const double* A, int64_t m, int64_t n, int64_t strideA, int64_t batch, int64_t k, double* U,
                       double* S, double* V, double* tail2, cudaStream_t s);
-void subspace_svd(const double* A, int64_t m, int64_t n, int64_t stride, int64_t batch, int64_t k,
-                  double* U, double* S, double* V, double* tail2, cudaStream_t s);
+// finite_who (nullable): also check the input for NaN/Inf (PPC_NUMERIC
+// "<who>: input has non-finite entries"), inside the slice-Gram split when it
+// runs on the INT8 path (returns true then), else not at all (returns false).
+bool subspace_svd(const double* A, int64_t m, int64_t n, int64_t stride, int64_t batch, int64_t k,
+                  double* U, double* S, double* V, double* tail2, cudaStream_t s, const char* finite_who = nullptr);
 
 }  // namespace ppc

@@ -22,6 +22,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -1046,8 +1047,9 @@ void subspace_eig_top(const double* G, int64_t r, int64_t batch, int64_t k, doub
                                      sizeof(double) * k, batch, cudaMemcpyDeviceToDevice, s));
 }
 
-void subspace_svd(const double* A, int64_t m, int64_t n, int64_t stride, int64_t batch, int64_t k,
-                  double* U, double* S, double* V, double* tail2, cudaStream_t s) {
+bool subspace_svd(const double* A, int64_t m, int64_t n, int64_t stride, int64_t batch, int64_t k,
+                  double* U, double* S, double* V, double* tail2, cudaStream_t s, const char* finite_who) {
+    bool checked = false;
     const bool tall = m >= n;
     const int64_t r = tall ? n : m;  // Gram dimension
     DeviceBuffer G(sizeof(double) * r * r * batch);
@@ -1055,7 +1057,16 @@ void subspace_svd(const double* A, int64_t m, int64_t n, int64_t stride, int64_t
         StageTimer tg("ss.gram", s, (double)batch * r * r * (tall ? m : n), 8.0 * batch * m * n);
         // tall slices: G_b = A_b^T A_b is the Gram of an m-row tube matrix
         // (INT8 tensor-core Ozaki SYRK where eligible)
-        if (!(tall && ozaki_syrk_batched(A, m, stride, m, n, batch, G.d(), s))) {
+        // the split of the INT8 slice Grams reads every entry once: the
+        // input's finiteness check (matrix_kernels.cpp:32) rides on it
+        std::unique_ptr<FiniteFlag> ff;
+        if (finite_who && tall) ff.reset(new FiniteFlag(s));
+        const bool oz = tall && ozaki_syrk_batched(A, m, stride, m, n, batch, G.d(), s, ff ? ff->d() : nullptr);
+        if (oz && ff) {
+            ff->check(s, finite_who);
+            checked = true;
+        }
+        if (!oz) {
             GemmDesc d;
             d.M = r; d.N = r; d.batch = batch; d.symmetric = true;
             d.C = G.d(); d.ldc = r; d.strideC = r * r;
@@ -1130,6 +1141,7 @@ void subspace_svd(const double* A, int64_t m, int64_t n, int64_t stride, int64_t
     }
     sign_rule(U, m, k, batch, V, n, s);  // matrix_kernels.cpp:16-25
     if (tail2) slice_tail_energy(A, m, n, stride, batch, k, U, S, V, tail2, s);
+    return checked;
 }
 
 }  // namespace ppc

@@ -160,6 +160,23 @@ def test_svd_errors(engine):
         engine.svd(bad)
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("shape", [(1024, 1024, 8), (512, 1024, 8)])
+def test_tsvdq_nonfinite_slices_rejected(engine, shape):
+    """The svd guard on the transform-domain slices (matrix_kernels.cpp:32):
+    tall 1024^2 slices check inside the INT8 slice-Gram split, wide ones
+    through the plain scan; either way NumericError, and clean input passes."""
+    n1, n2, n3 = shape
+    a = synth.cp_tensor_device(n1, n2, n3, rank=5, noise=1e-3, seed=2)
+    t = engine.Transform("random", n3, n3, seed=3)
+    a[n1 - 7, n2 // 2, 3] = float("nan")
+    with pytest.raises(engine.NumericError):
+        engine.tsvdq(a, t, 4)
+    a[n1 - 7, n2 // 2, 3] = 0.0
+    f = engine.tsvdq(a, t, 4)
+    assert np.isfinite(engine.to_host(f.s)).all()
+
+
 def _slice_parity(engine, oracle, a, q, k, s_tol=1e-10, rec_tol=1e-10):
     t = engine.Transform.custom(q)
     f = engine.tsvdq(a, t, k)
