@@ -787,21 +787,40 @@ namespace {
 // out[g] = max over blocks b and columns c of group g (c / group == g) of
 // (sc/2) sqrt(K) / ||x||: sc/2 bounds max|x| from above (sc in (2, 4] max|x|),
 // so this is >= the column's peak ratio max|x| sqrt(K) / ||x||_2 and < twice
-// it; zero columns count 0.
-__global__ void peak_ratio_kernel(const double* __restrict__ sc, const double* __restrict__ sq, int64_t cols,
-                                  double sqrtK, int64_t group, unsigned long long* __restrict__ out) {
-    // CTA (g, b): the columns of group g in block b; max over CTAs by an
-    // atomic max of the (non-negative) bit patterns: order-independent
-    const int64_t g = blockIdx.x, b = blockIdx.y;
-    const int64_t c0 = g * group, c1 = std::min<int64_t>(c0 + group, cols);
+// it; zero columns count 0. CTA (g, y) scans blocks y, y + gridDim.y, ... of
+// group g (all loads of a thread issued before the max), one block-level
+// max, one atomic max of the (non-negative) bit patterns per CTA:
+// order-independent.
+__global__ void __launch_bounds__(256) peak_ratio_kernel(const double* __restrict__ sc, const double* __restrict__ sq,
+                                                         int64_t cols, int64_t nblk, double sqrtK, int64_t group,
+                                                         unsigned long long* __restrict__ out) {
+    const int64_t g = blockIdx.x;
+    const int64_t c0 = g * group, c1 = std::min<int64_t>(c0 + group, cols), gw = c1 - c0;
+    const int64_t n = gw * ((nblk - blockIdx.y + gridDim.y - 1) / gridDim.y);
     double mx = 0.0;
-    for (int64_t c = c0 + threadIdx.x; c < c1; c += blockDim.x) {
-        const double q = sq[b * cols + c];
-        if (q > 0.0) mx = fmax(mx, 0.5 * sc[b * cols + c] * sqrtK / sqrt(q));
+    for (int64_t e0 = threadIdx.x; e0 < n; e0 += 8 * blockDim.x) {
+        double qv[8], sv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int64_t e = e0 + u * blockDim.x;
+            const int64_t b = blockIdx.y + (e / gw) * gridDim.y, c = c0 + e % gw;
+            const bool ok = e < n;
+            qv[u] = ok ? sq[b * cols + c] : 0.0;
+            sv[u] = ok ? sc[b * cols + c] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+            if (qv[u] > 0.0) mx = fmax(mx, 0.5 * sv[u] * sqrtK / sqrt(qv[u]));
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    if ((threadIdx.x & 31) == 0 && mx > 0.0) atomicMax(out + g, (unsigned long long)__double_as_longlong(mx));
+    __shared__ double red[8];
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) mx = fmax(mx, red[w]);
+        if (mx > 0.0) atomicMax(out + g, (unsigned long long)__double_as_longlong(mx));
+    }
 }
 }  // namespace
 
@@ -810,8 +829,9 @@ int64_t ozaki_peak_groups(const OzakiDigits& d, int64_t group) { return (d.cols 
 void ozaki_peak_ratios_async(const OzakiDigits& d, int64_t K, int64_t group, double* out, cudaStream_t s) {
     const int64_t ng = ozaki_peak_groups(d, group);
     PPC_CUDA_CHECK(cudaMemsetAsync(out, 0, sizeof(double) * ng, s));  // +0.0
-    peak_ratio_kernel<<<dim3((unsigned)ng, (unsigned)d.nblk), 256, 0, s>>>(
-        d.sc.d(), d.sq.d(), d.cols, std::sqrt((double)K), group, reinterpret_cast<unsigned long long*>(out));
+    const int64_t ny = std::max<int64_t>(1, std::min<int64_t>(d.nblk, (4 * 148 + ng - 1) / ng));
+    peak_ratio_kernel<<<dim3((unsigned)ng, (unsigned)ny), 256, 0, s>>>(
+        d.sc.d(), d.sq.d(), d.cols, d.nblk, std::sqrt((double)K), group, reinterpret_cast<unsigned long long*>(out));
     count_launch();
     check_launch("peak_ratio");
 }
