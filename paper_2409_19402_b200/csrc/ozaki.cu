@@ -599,6 +599,26 @@ bool ozaki_enabled() {
 // 15/21 of the pairs save less than 15/21 of its time), with the Gram 256x
 // further from FP64 (i.i.d. Gaussian 2^18 x 512: 5e-13 of max|G| instead of
 // ~2e-15). Kept as an A/B switch; the default stays at FP64-level accuracy.
+// Sub-chunks per Gram plan chunk (PPC_GRAM_SUB, default 4; 1 = off); must
+// divide the chunk's 4096-row block count.
+int64_t gram_subchunks(int64_t per) {
+    static const int64_t v = std::getenv("PPC_GRAM_SUB") ? std::atoll(std::getenv("PPC_GRAM_SUB")) : 4;
+    return (v > 1 && per % v == 0) ? v : 1;
+}
+
+// out[g][e] = sum_{u < n} in[g n + u][e] in u order (fixed)
+__global__ void sum_groups_kernel(const double* __restrict__ in, int64_t n, int64_t elems, int64_t total,
+                                  double* __restrict__ out) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
+        const int64_t g = i / elems, e = i - g * elems;
+        const double* p = in + g * n * elems + e;
+        double v = p[0];
+        for (int64_t u = 1; u < n; ++u) v += p[u * elems];
+        out[i] = v;
+    }
+}
+
 int gram_levels() {
     static const int v = (std::getenv("PPC_GRAM_LEVELS") && std::atoi(std::getenv("PPC_GRAM_LEVELS")) == 5) ? 5 : kS;
     return v;
@@ -942,7 +962,23 @@ bool ozaki_gram_partials(const double* T, int64_t ldT, int64_t rows, int64_t n3,
     d.split(T, ldT, 0, rows, n3, kKC, nblk, s, nullptr, 0, chunk, per, nonfinite, retain ? kSmax : kS, base,
             retain ? total_blocks : 0);
     if (retain && base == 0 && total_blocks == 0) d.uniform = true;  // streamed groups: the caller decides
-    ozaki_syrk(d, nchunks, per, parts, s, "ozaki_syrk", (double)rows, base, gram_levels());
+    // Each chunk's partial as nsub sub-chunk partials (per / nsub blocks each),
+    // summed in sub-chunk order: the 62-odd tiles of a (sub-)chunk stream its
+    // rows side by side, and the shorter work items keep them closer together
+    // in K (better L2 reuse of the digit planes) and cut the last wave's idle
+    // tail. The sum order depends on the plan only (sharding-invariant).
+    const int64_t nsub = gram_subchunks(per);
+    if (nsub > 1) {
+        DeviceBuffer sub(sizeof(double) * nchunks * nsub * n3 * n3);
+        ozaki_syrk(d, nchunks * nsub, per / nsub, sub.d(), s, "ozaki_syrk", (double)rows, base, gram_levels());
+        const int64_t total = nchunks * n3 * n3;
+        sum_groups_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, 148 * 16), 256, 0, s>>>(
+            sub.d(), nsub, n3 * n3, total, parts);
+        count_launch();
+        check_launch("sum_groups");
+    } else {
+        ozaki_syrk(d, nchunks, per, parts, s, "ozaki_syrk", (double)rows, base, gram_levels());
+    }
     return true;
 }
 
