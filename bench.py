@@ -788,6 +788,12 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # functional check of the N-rank path on a one-GPU box: every rank on
+    # cuda:0, collectives over gloo (NCCL refuses two ranks on one device);
+    # the numbers of such a run are not a measurement
+    shared_gpu = os.environ.get("PPC_BENCH_SHARED_GPU") == "1"
+    if shared_gpu:
+        local = 0
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
@@ -798,7 +804,10 @@ def main():
     if dist_on:
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     import paper_2409_19402_b200 as pp  # noqa: F401
     from paper_2409_19402_b200 import _lib
@@ -874,7 +883,10 @@ def main():
         cfg["parallelism"] = (f"{'row' if isinstance(wl, StarQSharded) else 'pixel'}-sharded dp{world}" if sharded else
                               (f"replicas{world}" if world > 1 else "single"))
         if dist_on:
-            cfg["comm"] = {"backend": "nccl", "nccl": ".".join(map(str, torch.cuda.nccl.version()))}
+            cfg["comm"] = ({"backend": "gloo", "note": "PPC_BENCH_SHARED_GPU: all ranks on cuda:0, a functional "
+                                                   "check of the N-rank path, not a measurement"}
+                           if shared_gpu else
+                           {"backend": "nccl", "nccl": ".".join(map(str, torch.cuda.nccl.version()))})
         line = {"metric": wl.metric, "value": value, "unit": wl.unit, "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
                 "higher_is_better": True, "scaling": "strong" if sharded else "weak", "vs_baseline": None,
