@@ -88,6 +88,9 @@ struct TrdParams {
                      //        writes step j+1 while a slow one still reads step j)
     double* colpub;  // 2 x n  published next pivot column, by step parity
     unsigned* bar;   // arrival counter (one per matrix, 128 bytes apart)
+    double* Aw;      // hybrid variant: owned slots >= cps in global memory (L2),
+                     // [matrix][CTA][slot - cps][n]; nullptr: all in shared memory
+    int cps;         // slots held in shared memory (hybrid variant)
     // batch: matrix b is G + b * strideG; its nblk CTAs are blocks
     // [b * nblk, (b+1) * nblk) and every output above is per matrix
     int64_t strideG;
@@ -144,7 +147,50 @@ __device__ __forceinline__ void update_pass(const TrdParams& P, double* A, int j
     const int n = P.n, nblk = P.nblk, cpc = P.cpc, blk = P.blk;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     const int i0 = (j + 1) & ~1;
-    for (int t = warp; t < cpc; t += nw) {
+    if (P.Aw) {
+        // slots past cps live in L2: four row pairs of a lane in flight per
+        // round (a load-use loop would pay one L2 round trip per 64 rows)
+        for (int t = P.cps + warp; t < cpc; t += nw) {
+            const int c = blk + t * nblk;
+            if (c <= j || c >= n) continue;  // warp-uniform
+            const double vc = vs[c], wc = ws[c];
+            double* a = P.Aw + (size_t)(t - P.cps) * n;
+            const bool pub = (c == j + 2);
+            double acc = 0.0;
+            for (int ib = i0 + 2 * lane; ib < n; ib += 256) {
+                double2 av[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int i = ib + 64 * u;
+                    av[u] = i < n ? __ldcg(reinterpret_cast<const double2*>(a + i)) : make_double2(0.0, 0.0);
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int i = ib + 64 * u;
+                    if (i >= n) break;
+                    const double2 v2 = *reinterpret_cast<const double2*>(vs + i);
+                    const double2 w2 = *reinterpret_cast<const double2*>(ws + i);
+                    double2 nv;
+                    nv.x = fma(-w2.x, vc, fma(-v2.x, wc, av[u].x));
+                    nv.y = fma(-w2.y, vc, fma(-v2.y, wc, av[u].y));
+                    __stcg(reinterpret_cast<double2*>(a + i), nv);
+                    if (vn) {
+                        const double2 n2 = *reinterpret_cast<const double2*>(vn + i);
+                        acc = fma(nv.x, n2.x, acc);
+                        acc = fma(nv.y, n2.y, acc);
+                    }
+                    if (pub) *reinterpret_cast<double2*>(cp + i) = nv;
+                }
+            }
+            if (vn) {
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+                if (lane == 0 && c > j + 1) pgo[by_slot ? t : c] = taun * acc;
+            }
+        }
+    }
+    const int ts = P.Aw ? P.cps : cpc;  // the shared-memory slots
+    for (int t = warp; t < ts; t += nw) {
         const int c = blk + t * nblk;
         if (c <= j || c >= n) continue;  // warp-uniform
         const double vc = vs[c], wc = ws[c];
@@ -175,7 +221,8 @@ __device__ __forceinline__ void update_pass(const TrdParams& P, double* A, int j
 }
 
 // Column c is owned by CTA c % nblk, slot c / nblk.
-__global__ void __launch_bounds__(kTrdThreads, 1) sytrd_kernel(TrdParams P0) {
+template <int NT>
+__global__ void __launch_bounds__(NT, 1) sytrd_kernel(TrdParams P0) {
     extern __shared__ __align__(16) double sm[];
     // this CTA's matrix and rank, and the matrix's slices of every array
     TrdParams P = P0;
@@ -193,8 +240,12 @@ __global__ void __launch_bounds__(kTrdThreads, 1) sytrd_kernel(TrdParams P0) {
         P.bar += (size_t)mat * 32;
     }
     const int n = P.n, nblk = P.nblk, cpc = P.cpc, blk = P.blk;
-    double* A = sm;                    // cpc x n (slot t = column blk + t*nblk)
-    double* vs = A + (size_t)cpc * n;  // reflector of step j
+    // cpc x n (slot t = column blk + t*nblk): slots < cps in shared memory,
+    // the rest (hybrid variant) in this CTA's slice of the global working copy
+    if (P.Aw) P.Aw += ((size_t)mat * nblk + blk) * (size_t)(cpc - P.cps) * n;
+    double* A = sm;
+    const int ts = P.Aw ? P.cps : cpc;
+    double* vs = A + (size_t)ts * n;  // reflector of step j
     double* vn = vs + n;               // reflector of step j+1
     double* ws = vn + n;               // w = p - K v
     double* xs = ws + n;               // pivot column
@@ -206,7 +257,8 @@ __global__ void __launch_bounds__(kTrdThreads, 1) sytrd_kernel(TrdParams P0) {
     for (int t = 0; t < cpc; ++t) {
         const int c = blk + t * nblk;
         if (c < n)
-            for (int i = tid; i < n; i += nt) A[(size_t)t * n + i] = P.G[(size_t)c * n + i];
+            for (int i = tid; i < n; i += nt)
+                (t < ts ? A + (size_t)t * n : P.Aw + (size_t)(t - ts) * n)[i] = P.G[(size_t)c * n + i];
     }
     for (int i = tid; i < n; i += nt) {
         xs[i] = P.G[i];
@@ -265,12 +317,14 @@ __global__ void __launch_bounds__(kTrdThreads, 1) sytrd_kernel(TrdParams P0) {
     for (int t = 0; t < cpc; ++t) {
         const int c = blk + t * nblk;
         if (tid == 0 && c == n - 2) {
-            P.d[n - 2] = A[(size_t)t * n + n - 2];
-            P.e[n - 2] = A[(size_t)t * n + n - 1];
+            const double* a = t < ts ? A + (size_t)t * n : P.Aw + (size_t)(t - ts) * n;
+            P.d[n - 2] = a[n - 2];
+            P.e[n - 2] = a[n - 1];
             P.tau[n - 2] = 0.0;
         }
         if (tid == 0 && c == n - 1) {
-            P.d[n - 1] = A[(size_t)t * n + n - 1];
+            const double* a = t < ts ? A + (size_t)t * n : P.Aw + (size_t)(t - ts) * n;
+            P.d[n - 1] = a[n - 1];
             P.tau[n - 1] = 0.0;
         }
     }
@@ -723,6 +777,20 @@ size_t trd_smem(int n, int cpc) { return ((size_t)cpc * n + 4 * (size_t)n) * siz
 struct TrdPlan {
     int nblk = 0, cpc = 0, per_wave = 0;
 };
+// Batches that would need more than one wave with every column in shared
+// memory (cfg3: 32 Grams of order 512 at 13 CTAs each = 3 waves) run in ONE
+// wave with the owned columns in a global working copy instead (L2-resident:
+// 64 MB at cfg3): the step latency chain is paid once, not once per wave.
+TrdPlan trd_plan_gmem(int64_t n, int64_t batch) {
+    TrdPlan t;
+    const int sms = ctx().sms;
+    if (batch < 2 || batch > sms) return t;
+    t.per_wave = (int)batch;
+    t.nblk = (int)std::min<int64_t>(sms / batch, n);
+    t.cpc = (int)((n + t.nblk - 1) / t.nblk);
+    return t;
+}
+
 TrdPlan trd_plan(int64_t n, int64_t batch) {
     TrdPlan t;
     const int sms = ctx().sms;
@@ -766,14 +834,26 @@ namespace {
 // V (n x n x batch), tau, d, e (n x batch).
 void run_sytrd(const double* G, int n, int64_t strideG, int batch, double* V, double* tau, double* d, double* e,
                cudaStream_t s) {
-    const TrdPlan t = trd_plan(n, batch);
+    TrdPlan t = trd_plan(n, batch);
+    static const bool no_gmem = std::getenv("PPC_TRD_GMEM") && std::getenv("PPC_TRD_GMEM")[0] == '0';
+    const bool gmem = !no_gmem && t.per_wave < batch && trd_plan_gmem(n, batch).nblk >= 1;
+    if (gmem) t = trd_plan_gmem(n, batch);
     const int nblk = t.nblk, cpc = t.cpc;
-    const size_t smem = trd_smem(n, cpc);
+    // hybrid: as many slots in shared memory as fit, the rest in L2
+    // (a hybrid with part of the slots in shared memory measured slower at
+    // cfg3: 9.1 ms a step against 8.4 with every slot in L2, warps unevenly
+    // loaded between the two kinds of slots)
+    const int cps = gmem ? 0 : cpc;
+    const size_t smem = trd_smem(n, cps);
     const size_t B = (size_t)batch;
     DeviceBuffer pgb(sizeof(double) * 2 * n * B), cpb(sizeof(double) * 2 * n * B), barb(sizeof(unsigned) * 32 * B);
+    DeviceBuffer aw(gmem ? sizeof(double) * B * nblk * (cpc - cps) * n : 0);
     PPC_CUDA_CHECK(cudaMemsetAsync(barb.d(), 0, sizeof(unsigned) * 32 * B, s));
     StageTimer tm("eig.tridiag", s);
-    PPC_CUDA_CHECK(cudaFuncSetAttribute(sytrd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    // (1024 threads for the L2-resident variant measured no faster)
+    const void* kern = (const void*)sytrd_kernel<kTrdThreads>;
+    const int threads = kTrdThreads;
+    PPC_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     for (int b0 = 0; b0 < batch; b0 += t.per_wave) {
         const size_t o = (size_t)b0;
         TrdParams P;
@@ -788,11 +868,13 @@ void run_sytrd(const double* G, int n, int64_t strideG, int batch, double* V, do
         P.pg = pgb.d() + o * 2 * n;
         P.colpub = cpb.d() + o * 2 * n;
         P.bar = barb.as<unsigned>() + o * 32;
+        P.Aw = gmem ? aw.d() : nullptr;
+        P.cps = cps;
         P.strideG = strideG;
         P.blk = 0;
         void* args[] = {&P};
         const int nm = std::min(t.per_wave, batch - b0);
-        PPC_CUDA_CHECK(cudaLaunchCooperativeKernel((const void*)sytrd_kernel, dim3(nblk * nm), dim3(kTrdThreads),
+        PPC_CUDA_CHECK(cudaLaunchCooperativeKernel(kern, dim3(nblk * nm), dim3(threads),
                                                    args, smem, s));
         count_launch();
         check_launch("sytrd");
