@@ -152,12 +152,9 @@ __global__ void residual_kernel(const double* GX, const double* X, const double*
 // x(l + 32 t)), each back-substitution step is a lane-parallel dot with a
 // fixed butterfly reduction.
 constexpr int kCholSlots = 5;  // x slots per lane: b <= 160
-// nsplit > 1: S holds nsplit split-K partials at S + t*sstride, summed here
-// in split order (fixed: the same bits as one pass over K in that order).
 __global__ void __launch_bounds__(1024, 1) chol_inv_kernel(const double* __restrict__ S, double* __restrict__ Rinv, int64_t b64,
                                 int shift_pass, int* fail, double* __restrict__ Rout,
-                                const int* __restrict__ zmap = nullptr, int* __restrict__ weak = nullptr,
-                                int nsplit = 1, int64_t sstride = 0) {
+                                const int* __restrict__ zmap = nullptr, int* __restrict__ weak = nullptr) {
     extern __shared__ __align__(16) double M[];
     __shared__ double dinv[160];  // 1 / R(i,i)
     __shared__ unsigned char badk[160];  // pivot k broke down (a zero column)
@@ -167,11 +164,7 @@ __global__ void __launch_bounds__(1024, 1) chol_inv_kernel(const double* __restr
     const double* Sin = S + sl * b64 * b64;
     const int tid = threadIdx.x, nt = blockDim.x;
     const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
-    for (int i = tid; i < b * b; i += nt) {
-        double v = Sin[i];
-        for (int t = 1; t < nsplit; ++t) v += Sin[t * sstride + i];
-        M[i] = v;
-    }
+    for (int i = tid; i < b * b; i += nt) M[i] = Sin[i];
     if (tid == 0) bad = 0;
     __syncthreads();
     if (shift_pass) {  // shifted CholQR (Fukaya et al.): tiny diagonal shift ~ u * trace
@@ -525,7 +518,7 @@ void cholqr3(Work& w, double* Y, double* Xout, int64_t c0, cudaStream_t s, const
     const bool small = panel_kernels_ok(r, bc);
     for (int pass = 0; pass < 3; ++pass) {
         if (small) {
-            // S = Y^T Y as split-K partials (panel.cu), summed by the Cholesky
+            // S = Y^T Y (split-K partials summed in split order, panel.cu)
             panel_gram(src, per, src, per, r, bc, batch, w.S.d(), w.Ssplit.d(), zx, zm, s);
             chol_inv64(w.S.d(), bc, batch, pass == 0, w.Rinv.d(), w.fail.as<int>(), zm, nullptr, s);
             panel_apply(src, per, w.Rinv.d(), bufs[pass], per, r, bc, batch, zm, s);
