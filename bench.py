@@ -242,9 +242,11 @@ class StarQ:
 
     def dominant(self, stages):
         # the single longest kernel launch of the step: the inverse transform
-        # (FP64 DMMA, K = p = 64), the facewise product (INT8 Ozaki MMA when
-        # eligible) or a forward transform
-        cands = [("mode3_inv", "tensor"), ("ozaki_gemm", "int8") if "ozaki_gemm" in stages else ("facewise", "tensor"),
+        # (INT8 row-split kernel, bound by its 8-byte FP64 stores: HBM; FP64
+        # DMMA where not eligible), the facewise product (INT8 Ozaki MMA when
+        # eligible) or a forward transform (FP64 DMMA)
+        cands = [("ozaki_star_inv", "hbm") if "ozaki_star_inv" in stages else ("mode3_inv", "tensor"),
+                 ("ozaki_gemm", "int8") if "ozaki_gemm" in stages else ("facewise", "tensor"),
                  ("mode3_fwd", "tensor")]
         cands = [c for c in cands if c[0] in stages]
         if not cands:

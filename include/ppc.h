@@ -265,6 +265,13 @@ int ppc_gemm_strided(int64_t M, int64_t N, int64_t K, int64_t batch, double alph
  * tensor.cpp:149-156 for the rank's C rows. */
 int ppc_facewise_strided(const double* A, int64_t n1, int64_t m, int64_t batch, const double* B, int64_t n2,
                          double* C, int64_t ldc, int64_t strideC);
+/* The star product's inverse transform, DEVICE memory, stream-ordered:
+ * C (N x n3, column-major) = scale Ch Q^T for Ch (N x p) and Q (n3 x p) --
+ * what star_q runs for C^ x3 Q (star_products.cpp:56-58). On the INT8 tensor
+ * cores with one scale per row of Ch (rows are independent: a row shard gives
+ * the 1-GPU bits) when 32 <= p <= 64 and n3 <= 256 is a multiple of 32, else
+ * FP64 DMMA. The row-sharded star-Q's inverse transform. */
+int ppc_star_inverse(const double* Ch, int64_t N, int64_t p, const double* Q, int64_t n3, double scale, double* C);
 /* The pixel -> slice reshard's unpack, DEVICE memory, stream-ordered:
  * recv holds G blocks [r][slice][j][i] (rank r's nj lateral columns of my ps
  * slices, as all_to_all_single delivers them); out receives the ps whole

@@ -53,6 +53,7 @@ def lib() -> C.CDLL:
         "ppc_set_ozaki": (C.c_int, [C.c_int]),
         "ppc_get_ozaki": (C.c_int, []),
         "ppc_facewise_strided": (C.c_int, [vp, i64, i64, i64, vp, i64, vp, i64, i64]),
+        "ppc_star_inverse": (C.c_int, [vp, i64, i64, vp, i64, C.c_double, vp]),
         "ppc_reshard_slices": (C.c_int, [vp, i64, i64, i64, i64, vp]),
         "ppc_sym_eig_split_begin": (C.c_int, [vp, i64, i64, C.POINTER(C.c_int64)]),
         "ppc_sym_eig_split_vectors": (C.c_int, [i64, i64, i64, vp]),

@@ -429,6 +429,16 @@ int ppc_facewise_strided(const double* A, int64_t n1, int64_t m, int64_t batch, 
     });
 }
 
+int ppc_star_inverse(const double* Ch, int64_t N, int64_t p, const double* Q, int64_t n3, double scale, double* C) {
+    return guarded([&] {
+        require_positive(N, "N");
+        require_positive(p, "p");
+        require_positive(n3, "n3");
+        if (!Ch || !Q || !C) fail(PPC_ARGUMENT, "star_inverse: null operand");
+        star_inverse(Ch, N, p, Q, n3, scale, C, stream());
+    });
+}
+
 int ppc_reshard_slices(const double* recv, int64_t G, int64_t ps, int64_t nj, int64_t n1, double* out) {
     return guarded([&] {
         if (G < 1 || ps < 1 || nj < 1 || n1 < 1) fail(PPC_SHAPE, "reshard_slices: extents must be positive");

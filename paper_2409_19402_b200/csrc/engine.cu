@@ -132,6 +132,11 @@ namespace {
 
 }  // namespace
 
+void star_inverse(const double* Ch, int64_t N, int64_t p, const double* Q, int64_t n3, double scale, double* C,
+                  cudaStream_t s) {
+    if (!ozaki_star_inverse(Ch, N, p, Q, n3, scale, C, N, s)) mode3(Ch, N, p, Q, n3, false, C, scale, s);
+}
+
 void star_q(const double* A, int64_t n1, int64_t m, int64_t n3, const double* B, int64_t n2,
             const double* Q, int64_t p, double scale, double* C, cudaStream_t s) {
     DeviceBuffer ah(sizeof(double) * n1 * m * p), bh(sizeof(double) * m * n2 * p),
@@ -143,7 +148,7 @@ void star_q(const double* A, int64_t n1, int64_t m, int64_t n3, const double* B,
     double b_peak = 0.0;
     if (!facewise_ozaki(ah.d(), n1, m, p, bh.d(), n2, ch.d(), bd, b_ready, b_peak, s))
         facewise(ah.d(), n1, m, p, bh.d(), n2, ch.d(), s);   // facewise
-    mode3(ch.d(), n1 * n2, p, Q, n3, false, C, scale, s);  // x3 Q, scale in the epilogue
+    star_inverse(ch.d(), n1 * n2, p, Q, n3, scale, C, s);  // x3 Q, scaled
 }
 
 namespace {
@@ -216,7 +221,7 @@ void star_q_host(const double* hA, int64_t n1, int64_t m, int64_t n3, const doub
         if (!facewise_ozaki(ahblk[u].d(), bi, m, p, bh.d(), n2, chblk[u].d(), bd, b_ready, b_peak, s))
             facewise(ahblk[u].d(), bi, m, p, bh.d(), n2, chblk[u].d(), s);
         c_free[u].wait_on(s);  // block ib-2's C rows are down
-        mode3(chblk[u].d(), bi * n2, p, q.d(), n3, false, cblk[u].d(), scale, s);  // x3 Q, scale
+        star_inverse(chblk[u].d(), bi * n2, p, q.d(), n3, scale, cblk[u].d(), s);  // x3 Q, scaled
         Event done;
         done.record(s);
         done.wait_on(down);

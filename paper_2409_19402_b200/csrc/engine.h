@@ -16,6 +16,10 @@ namespace ppc {
 // trans_m=true: M is n3 x q (the basis Q itself).       [tensor.cpp:139-147]
 void mode3(const double* T, int64_t N, int64_t n3, const double* M, int64_t q, bool trans_m,
            double* out, double alpha, cudaStream_t s);
+// The star product's inverse transform C (N x n3) = scale Ch Q^T: the INT8
+// row-split kernel (ozaki_star_inverse) where eligible, else mode3 on DMMA.
+void star_inverse(const double* Ch, int64_t N, int64_t p, const double* Q, int64_t n3, double scale, double* C,
+                  cudaStream_t s);
 // C(:,:,i) = A(:,:,i) B(:,:,i), i < p                     [tensor.cpp:149-156]
 void facewise(const double* A, int64_t n1, int64_t m, int64_t p, const double* B, int64_t n2,
               double* C, cudaStream_t s);

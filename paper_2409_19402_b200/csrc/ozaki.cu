@@ -1043,6 +1043,347 @@ bool ozaki_mode3_forward(const OzakiDigits& td, int64_t N, const double* Q, int6
     return true;
 }
 
+// --------------------------------------------- star product inverse transform
+// C (M x N, leading dimension ldc) = A B with A (M x K) split row-wise (one
+// power-of-two scale per row over its K <= 64 values) and B (K x N, N <= 256,
+// a multiple of 32) split column-wise: the cfg4 inverse transform C^ x3 Q
+// (K = p, N = n3). Rows are independent (any row blocking gives the same
+// bits: the host pipeline and the row-sharded product equal the device call).
+//
+// Shape of the work: K is one 64-byte stage, so the generic persistent kernel
+// (one TMEM accumulator set, register stores) serialized MMA and epilogue and
+// lost to FP64 DMMA. Here B's digits stay resident in shared memory for the
+// whole launch (6 planes x N x 64 B <= 96 KB), each 128-row tile's A digits
+// take one 48 KB stage, the N columns run as 32-wide sub-tiles into two TMEM
+// buffers (6 levels x 32 columns each), and the epilogue drains one buffer
+// while the MMAs fill the other and streams every 128 x 32 FP64 sub-tile out
+// with a TMA store from a double-buffered staging tile. The kernel is bound
+// by the 8 bytes written per output.
+namespace {
+
+constexpr int kRowsPerSplit = 32;
+constexpr int kRgNB = 32;        // sub-tile width (output columns)
+constexpr int kRgMaxSub = 8;     // N <= 256
+constexpr int kRgEpiWarps = 8;   // two per TMEM lane quadrant (16 columns each)
+constexpr int kRgThreads = (2 + kRgEpiWarps) * 32;
+
+// Row-wise split: digit row j of D holds row j of X (rows x K, column-major,
+// leading dimension ldx) scaled by sigma_j > 2 max_k |X(j, k)| (a power of
+// two), cut into ND digits along k (D layout [plane][row][KCp], zero padded).
+// CTA: 32 rows; lane = row (coalesced column loads); warp w: k in runs of 4
+// (w, w + 8, ...); the digits are staged in shared memory and written out as
+// contiguous 32 KCp-byte runs per plane.
+template <int ND>
+__global__ void __launch_bounds__(256) ozaki_split_rows_kernel(const double* __restrict__ X, int64_t ldx, int64_t rows,
+                                                               int K, int KCp, int8_t* __restrict__ D,
+                                                               double* __restrict__ scale) {
+    extern __shared__ uint8_t tile[];  // ND x 32 rows x (KCp + 16)
+    __shared__ double rmx[8][32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t r0 = (int64_t)blockIdx.x * kRowsPerSplit, row = r0 + lane;
+    const bool live = row < rows;
+    const double* x = X + (live ? row : 0);
+    double mx = 0.0;
+    for (int k4 = w; 4 * k4 < K; k4 += 8) {
+        double v[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int k = 4 * k4 + q;
+            v[q] = (live && k < K) ? __ldg(x + (int64_t)k * ldx) : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) mx = fmax(mx, fabs(v[q]));
+    }
+    rmx[w][lane] = mx;
+    __syncthreads();
+    mx = 0.0;
+    for (int u = 0; u < 8; ++u) mx = fmax(mx, rmx[u][lane]);
+    if (w == 0 && live) scale[row] = mx > 0.0 ? ldexp(1.0, ilogb(mx) + 2) : 0.0;
+    const int e = mx > 0.0 ? ilogb(mx) + 2 : 0;
+    constexpr int SH = 8 * (ND - 1);
+    constexpr unsigned long long C80 = 0x8080808080808080ULL >> (64 - SH);
+    const int e1 = (SH + 7 - e) / 2;
+    const double scl1 = mx > 0.0 ? ldexp(1.0, e1) : 0.0, scl2 = ldexp(1.0, SH + 7 - e - e1);
+    const int RS = KCp + 16;
+    for (int k4 = w; 4 * k4 < KCp; k4 += 8) {
+        uint32_t wd[ND];
+#pragma unroll
+        for (int t = 0; t < ND; ++t) wd[t] = 0u;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int k = 4 * k4 + q;
+            const double v = (live && k < K) ? __ldg(x + (int64_t)k * ldx) : 0.0;
+            const long long y = __double2ll_rn(v * scl1 * scl2);
+            const long long U = y + (long long)C80;
+            const uint64_t low = (uint64_t)U ^ C80;
+            wd[0] |= (uint32_t)(uint8_t)(int8_t)(U >> SH) << (8 * q);
+#pragma unroll
+            for (int t = 1; t < ND; ++t) wd[t] |= (uint32_t)((low >> (SH - 8 * t)) & 0xFFu) << (8 * q);
+        }
+#pragma unroll
+        for (int t = 0; t < ND; ++t)
+            *reinterpret_cast<uint32_t*>(tile + ((size_t)t * kRowsPerSplit + lane) * RS + 4 * k4) = wd[t];
+    }
+    __syncthreads();
+    const int nr = (int)std::min<int64_t>(kRowsPerSplit, rows - r0);
+    const int per_plane = nr * KCp / 16;
+    for (int t = 0; t < ND; ++t) {
+        uint4* dst = reinterpret_cast<uint4*>(D + ((size_t)t * rows + r0) * KCp);
+        for (int c = threadIdx.x; c < per_plane; c += blockDim.x) {
+            const int i = (c * 16) / KCp, b = (c * 16) % KCp;
+            dst[c] = *reinterpret_cast<const uint4*>(tile + ((size_t)t * kRowsPerSplit + i) * RS + b);
+        }
+    }
+}
+
+struct RgParams {
+    int64_t M;          // rows
+    int N, nsub;        // columns, 32-wide sub-tiles
+    int64_t tiles;      // 128-row tiles
+    const double* sa;   // row scales [M]
+    const double* sb;   // column scales [N]
+};
+
+__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n)); }
+
+__global__ void __launch_bounds__(kRgThreads, 1)
+    ozaki_rowgemm_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+                         const __grid_constant__ CUtensorMap mapC, const RgParams P) {
+    constexpr int NL = kS;
+    constexpr int A_PLANE = kBM * kBK;         // 8 KB
+    constexpr int B_PLANE = kRgNB * kBK;       // 2 KB
+    constexpr int STG_TILE = kRgNB * kBM * 8;  // 32 KB of FP64
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sB = base;                                            // [sub][plane] 2 KB each
+    uint8_t* sA = sB + kRgMaxSub * NL * B_PLANE;                   // [plane] 8 KB each
+    double* stg = reinterpret_cast<double*>(sA + NL * A_PLANE);    // 2 x [32 cols][128 rows]
+    uint64_t* bfull = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(stg) + 2 * STG_TILE);
+    uint64_t* afull = bfull + 1;
+    uint64_t* aempty = afull + 1;
+    uint64_t* tfull = aempty + 1;   // [2]
+    uint64_t* tempty = tfull + 2;   // [2]
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        bar_init(bfull, 1);
+        bar_init(afull, 1);
+        bar_init(aempty, 1);
+        for (int u = 0; u < 2; ++u) {
+            bar_init(&tfull[u], 1);
+            bar_init(&tempty[u], kRgEpiWarps);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc<512>(tslot);
+    fence_before_sync();
+    __syncthreads();
+    fence_after_sync();
+    const uint32_t tmem = *tslot;
+    const int nsub = P.nsub;
+
+    if (warp == 0) {
+        if (elect_one()) {
+            bar_expect_tx(bfull, (uint32_t)(nsub * NL * B_PLANE));
+            for (int sb = 0; sb < nsub; ++sb)
+                for (int t = 0; t < NL; ++t) tma_load_3d(sB + (sb * NL + t) * B_PLANE, &mapB, bfull, 0, sb * kRgNB, t);
+            int64_t it = 0;
+            for (int64_t tile = blockIdx.x; tile < P.tiles; tile += gridDim.x, ++it) {
+                bar_wait(aempty, (uint32_t)((it & 1) ^ 1));
+                bar_expect_tx(afull, (uint32_t)(NL * A_PLANE));
+                for (int t = 0; t < NL; ++t) tma_load_3d(sA + t * A_PLANE, &mapA, afull, 0, (int)(tile * kBM), t);
+            }
+        }
+    } else if (warp == 1) {
+        bar_wait(bfull, 0u);
+        int64_t it = 0, gs = 0;
+        for (int64_t tile = blockIdx.x; tile < P.tiles; tile += gridDim.x, ++it) {
+            bar_wait(afull, (uint32_t)(it & 1));
+            fence_after_sync();
+            for (int sb = 0; sb < nsub; ++sb, ++gs) {
+                const int u = (int)(gs & 1);
+                bar_wait(&tempty[u], (uint32_t)(((gs >> 1) & 1) ^ 1));
+                fence_after_sync();
+                if (elect_one()) {
+#pragma unroll
+                    for (int kk = 0; kk < kBK / 32; ++kk) {
+#pragma unroll
+                        for (int i = 1; i <= NL; ++i) {
+                            const uint64_t da = sdesc_k_sw64(sA + (i - 1) * A_PLANE) + (uint64_t)(kk * 2);
+                            const int jmax = NL + 1 - i;
+#pragma unroll
+                            for (int j0 = 1; j0 <= jmax; j0 += 3) {
+                                const int nj = jmax - j0 + 1 < 3 ? jmax - j0 + 1 : 3;
+                                const uint32_t idesc = nj == 3 ? idesc_i8<kBM, 3 * kRgNB>()
+                                                               : (nj == 2 ? idesc_i8<kBM, 2 * kRgNB>()
+                                                                          : idesc_i8<kBM, kRgNB>());
+                                const uint64_t db = sdesc_k_sw64(sB + (sb * NL + j0 - 1) * B_PLANE) + (uint64_t)(kk * 2);
+                                mma_i8(tmem + (uint32_t)(u * NL * kRgNB + (i + j0 - 2) * kRgNB), da, db, idesc,
+                                       (i == 1 && kk == 0) ? 0u : 1u);
+                            }
+                        }
+                    }
+                    mma_commit(&tfull[u]);
+                }
+                __syncwarp();
+            }
+            if (elect_one()) mma_commit(aempty);  // every MMA of the tile has read A
+            __syncwarp();
+        }
+    } else {
+        // warp w reads TMEM lanes 32 (w % 4) .. + 31 (the rows of the tile),
+        // columns [16 h, 16 h + 16) of each sub-tile
+        const int q = warp & 3, h = (warp - 2) >> 2;
+        int64_t gs = 0;
+        for (int64_t tile = blockIdx.x; tile < P.tiles; tile += gridDim.x) {
+            const int64_t m = tile * kBM + q * 32 + lane;
+            const double sm = m < P.M ? P.sa[m] : 0.0;
+            for (int sb = 0; sb < nsub; ++sb, ++gs) {
+                const int u = (int)(gs & 1);
+                bar_wait(&tfull[u], (uint32_t)((gs >> 1) & 1));
+                fence_after_sync();
+                double* st = stg + (size_t)u * (kRgNB * kBM);
+                const uint32_t ta = tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(u * NL * kRgNB);
+                // levels 0-2 and 3-5 combined exactly in 64-bit integers
+                // (|v| < 2^31: |v0 2^16 + v1 2^8 + v2| < 2^48 converts to FP64
+                // exactly), so each output costs two conversions and one FMA
+                // instead of six of each: the FP64 pipe bounds this epilogue
+                static_assert(NL == 6, "two three-level groups");
+#pragma unroll
+                for (int c = 2 * h; c < 2 * h + 2; ++c) {
+                    int32_t v[NL][8];
+#pragma unroll
+                    for (int l = 0; l < NL; ++l) tmem_ld_32x32b_x8(ta + (uint32_t)(l * kRgNB + c * 8), v[l]);
+                    double scl[8];
+#pragma unroll
+                    for (int jj = 0; jj < 8; ++jj) scl[jj] = sm * P.sb[sb * kRgNB + c * 8 + jj] * 0x1.0p-30;
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int jj = 0; jj < 8; ++jj) {
+                        const long long g0 = ((long long)v[0][jj] << 16) + ((long long)v[1][jj] << 8) + v[2][jj];
+                        const long long g1 = ((long long)v[3][jj] << 16) + ((long long)v[4][jj] << 8) + v[5][jj];
+                        // sum_l v_l 2^(-14-8l) = 2^-30 (g0 + 2^-24 g1)
+                        const double t = fma((double)g1, 0x1.0p-24, (double)g0);
+                        st[(c * 8 + jj) * kBM + q * 32 + lane] = t * scl[jj];
+                    }
+                }
+                fence_before_sync();
+                __syncwarp();
+                if (lane == 0) bar_arrive(&tempty[u]);  // the MMAs may refill this TMEM buffer
+                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                named_bar(1, kRgEpiWarps * 32);
+                if (warp == 2 && lane == 0) {
+                    asm volatile(
+                        "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];\n" ::"l"(
+                            &mapC),
+                        "r"((int)(tile * kBM)), "r"(sb * kRgNB), "r"(0), "r"(smem_u32(st))
+                        : "memory");
+                    asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+                    // the other staging tile (stored one sub-tile ago) is read out
+                    asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+                }
+                named_bar(1, kRgEpiWarps * 32);
+            }
+        }
+        if (warp == 2 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+    }
+    fence_before_sync();
+    __syncthreads();
+    if (warp == 1) tmem_free<512>(tmem);
+}
+
+constexpr size_t rg_smem() {
+    return 1024 + (size_t)kRgMaxSub * kS * kRgNB * kBK + (size_t)kS * kBM * kBK + 2 * (size_t)kRgNB * kBM * 8 + 8 * 8 +
+           16;
+}
+
+// Bt (K x N) = alpha Q^T for Q (N x K, column-major): column n = alpha Q(n, :)
+__global__ void star_bt_kernel(const double* __restrict__ Q, int64_t N, int64_t K, double alpha, double* __restrict__ Bt) {
+    const int64_t total = K * N;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k = i % K, n = i / K;
+        Bt[i] = alpha * Q[n + k * N];
+    }
+}
+
+bool make_fp64_map(CUtensorMap* map, const double* X, int64_t M, int64_t N, int64_t ld, int bm, int bn) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[3] = {(cuuint64_t)M, (cuuint64_t)N, 1};
+    cuuint64_t strides[2] = {(cuuint64_t)ld * 8, (cuuint64_t)ld * N * 8};
+    cuuint32_t box[3] = {(cuuint32_t)bm, (cuuint32_t)bn, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    if (strides[0] % 16) return false;
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(X), dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+bool ozaki_star_inverse_eligible(int64_t K, int64_t N) {
+    static const bool off = std::getenv("PPC_OZAKI_STAR_INV") && std::getenv("PPC_OZAKI_STAR_INV")[0] == '0';
+    return !off && ozaki_enabled() && K >= 32 && K <= kBK && N >= kRgNB && N <= kRgMaxSub * kRgNB && N % kRgNB == 0;
+}
+
+bool ozaki_star_inverse(const double* A, int64_t M, int64_t K, const double* Q, int64_t N, double alpha, double* C,
+                        int64_t ldc, cudaStream_t s) {
+    // (an odd ldc cannot carry the TMA store: FP64 DMMA then, for that call only)
+    if (!ozaki_star_inverse_eligible(K, N) || M < 1 || (ldc & 1) || ldc < M) return false;
+    StageTimer tm("mode3_inv", s, 2.0 * M * K * N, 8.0 * (M * K + M * N + K * N));
+    // A (M x K, leading dimension M): row-wise digits
+    OzakiDigits ad;
+    ad.nd = kS;
+    ad.rows = K;
+    ad.cols = M;
+    ad.nblk = 1;
+    ad.KCp = kBK;
+    ad.D = DeviceBuffer(sizeof(int8_t) * kS * M * kBK);
+    ad.sc = DeviceBuffer(sizeof(double) * M);
+    {
+        const size_t smem = (size_t)kS * kRowsPerSplit * (kBK + 16);
+        StageTimer ts("ozaki_split", s, 0.0, 8.0 * M * K + (double)kS * M * kBK);
+        ozaki_split_rows_kernel<kS><<<(unsigned)((M + kRowsPerSplit - 1) / kRowsPerSplit), 256, smem, s>>>(
+            A, M, M, (int)K, (int)kBK, ad.D.as<int8_t>(), ad.sc.d());
+        count_launch();
+        check_launch("ozaki_split_rows");
+    }
+    // B = alpha Q^T (K x N): column-wise digits
+    DeviceBuffer bt(sizeof(double) * K * N);
+    star_bt_kernel<<<(unsigned)std::min<int64_t>((K * N + 255) / 256, 1024), 256, 0, s>>>(Q, N, K, alpha, bt.d());
+    count_launch();
+    check_launch("star_bt");
+    OzakiDigits bd;
+    bd.split(bt.d(), K, K * N, K, N, K, 1, s);
+    CUtensorMap ma, mb, mc;
+    if (!make_digit_map(&ma, ad.D.as<int8_t>(), kBK, M, kS, kBM) ||
+        !make_digit_map(&mb, bd.D.as<int8_t>(), bd.KCp, N, bd.nd, kRgNB) || !make_fp64_map(&mc, C, M, N, ldc, kBM, kRgNB))
+        fail(PPC_CUDA, "ozaki: tensor map encoding failed");
+    RgParams P;
+    P.M = M;
+    P.N = (int)N;
+    P.nsub = (int)(N / kRgNB);
+    P.tiles = (M + kBM - 1) / kBM;
+    P.sa = ad.sc.d();
+    P.sb = bd.sc.d();
+    static bool attr = false;
+    if (!attr) {
+        PPC_CUDA_CHECK(cudaFuncSetAttribute(ozaki_rowgemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)rg_smem()));
+        attr = true;
+    }
+    {
+        // bytes: the FP64 output written and A's digit planes read (HBM-bound: 8 B per output)
+        StageTimer tk("ozaki_star_inv", s, 2.0 * kS * (kS + 1) / 2 * (double)M * K * N,
+                      8.0 * M * N + (double)kS * M * kBK);
+        ozaki_rowgemm_kernel<<<(unsigned)std::min<int64_t>(P.tiles, ctx().sms), kRgThreads, rg_smem(), s>>>(ma, mb, mc,
+                                                                                                          P);
+        count_launch();
+        check_launch("ozaki_rowgemm");
+    }
+    return true;
+}
+
 bool ozaki_syrk_batched(const double* A, int64_t lda, int64_t strideA, int64_t rows, int64_t n, int64_t batch,
                         double* G, cudaStream_t s, int* nonfinite) {
     if (!ozaki_enabled()) return false;

@@ -66,6 +66,17 @@ std::vector<double> ozaki_peak_ratios(const OzakiDigits& d, int64_t K, int64_t g
 int64_t ozaki_peak_groups(const OzakiDigits& d, int64_t group);
 void ozaki_peak_ratios_async(const OzakiDigits& d, int64_t K, int64_t group, double* out, cudaStream_t s);
 constexpr double kOzakiPeakGate = 16.0;  // products whose operands exceed it run on FP64 DMMA
+// The star product's inverse transform on the INT8 tensor cores: C (M x N,
+// leading dimension ldc) = alpha A Q^T for A (M x K, leading dimension M) and
+// Q (N x K), 32 <= K <= 64, N <= 256 a multiple of 32. A is split row-wise
+// (one power-of-two scale per row over its K values: rows are independent,
+// so row blocks and shards give the device call's bits); 21 digit pairs,
+// error ~ sqrt(K) 2^-46 max|A(a,:)| max|Q(b,:)| <= 2^-43 |A(a,:)| |Q(b,:)|
+// (row scaling bounds the peak ratio by sqrt(K)). false when not eligible
+// (PPC_OZAKI_STAR_INV=0 disables).
+bool ozaki_star_inverse_eligible(int64_t K, int64_t N);
+bool ozaki_star_inverse(const double* A, int64_t M, int64_t K, const double* Q, int64_t N, double alpha, double* C,
+                        int64_t ldc, cudaStream_t s);
 // Whether the integer path applies to an output with M rows and K-length sums.
 bool ozaki_gemm_eligible(int64_t M, int64_t K);
 // the INT8 path is on (PPC_OZAKI / ppc_set_ozaki)

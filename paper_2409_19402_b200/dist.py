@@ -159,11 +159,11 @@ class DeviceBackend:
         return out
 
     def mode3_inv(self, Ch, d1, d2, p, Q, n3, scale):
-        """(Ch x3 Q) * scale, the scale in the GEMM epilogue (star_products.cpp:56-58)."""
+        """(Ch x3 Q) * scale with the 1-GPU star_q's inverse transform
+        (ppc_star_inverse: row-wise INT8 digits, so the rank's rows come out
+        as in the 1-GPU product) (star_products.cpp:56-58)."""
         out = _fempty((d1, d2, n3), self.device)
-        N = d1 * d2
-        _check(self.L.ppc_gemm_strided(N, n3, p, 1, C.c_double(scale), _p(Ch), N, 0, 0, _p(Q), n3, 0, 1,
-                                       _p(out), N, 0))
+        _check(self.L.ppc_star_inverse(_p(Ch), d1 * d2, p, _p(Q), n3, C.c_double(scale), _p(out)))
         return out
 
     def svd_slices(self, S_loc, n1, n2, ps, k):

@@ -1156,6 +1156,56 @@ def test_nonfinite_input_rejected(engine, shape, val):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("M,K,N,alpha", [(4096, 64, 256, 0.75), (1000, 40, 96, 1.0), (258, 33, 32, -2.0)])
+def test_star_inverse_vs_numpy(engine, M, K, N, alpha):
+    """ppc_star_inverse (the star product's inverse transform on the INT8
+    tensor cores, row-wise digit split, B resident in shared memory, TMA-store
+    epilogue) against numpy FP64: <= 1e-12 relative (Frobenius; the star
+    product's tolerance, DESIGN 5: the 6-digit split carries ~sqrt(K) 2^-45 of
+    a row's max, ~2e-13 here, against FP64's ~1e-15), partial last
+    tile, K < 64 (zero-padded digits), 1-8 sub-tiles; a row block of the
+    input gives those rows bit for bit (row-wise digits); rows with a wide
+    dynamic range stay accurate relative to their own norm."""
+    import ctypes as C
+    import torch
+    from paper_2409_19402_b200 import _lib
+    L = _lib.lib()
+    g = torch.Generator(device="cuda")
+    g.manual_seed(M + K + N)
+    A = torch.randn(K, M, dtype=torch.float64, device="cuda", generator=g).t()  # M x K, leading dimension M
+    A[3] *= 1e6          # a huge row
+    A[5] *= 1e-9         # a tiny row
+    A[7, 1] = 1e8        # one dominant entry in a row
+    Q = (torch.randn(K, N, dtype=torch.float64, device="cuda", generator=g) / K ** 0.5).t()  # N x K, column-major
+    Cout = torch.empty(N, M, dtype=torch.float64, device="cuda").t()
+    torch.cuda.synchronize()  # the engine runs on its own stream
+    L.ppc_timing_report(C.create_string_buffer(1 << 16), 1 << 16, 1)
+    L.ppc_timing_enable(1)
+    assert L.ppc_star_inverse(C.c_void_p(A.data_ptr()), M, K, C.c_void_p(Q.data_ptr()), N, C.c_double(alpha),
+                              C.c_void_p(Cout.data_ptr())) == 0, L.ppc_last_error()
+    buf = C.create_string_buffer(1 << 16)
+    L.ppc_timing_report(buf, len(buf), 1)
+    L.ppc_timing_enable(0)
+    assert L.ppc_synchronize() == 0
+    assert "ozaki_star_inv" in buf.value.decode()
+    want = alpha * (A.cpu().numpy() @ Q.cpu().numpy().T)
+    got = Cout.cpu().numpy()
+    assert np.linalg.norm(got - want) <= 1e-12 * np.linalg.norm(want)
+    # per row, relative to the row's own scale
+    rn = np.linalg.norm(A.cpu().numpy(), axis=1) * abs(alpha)
+    assert (np.abs(got - want).max(axis=1) <= 1e-12 * rn).all()
+    # a row block (as the host pipeline / a shard computes it): the same bits
+    r0, nr = 128, min(512, M - 128) & ~1
+    Ab = A[r0:r0 + nr].t().contiguous().t()
+    Cb = torch.empty(N, nr, dtype=torch.float64, device="cuda").t()
+    torch.cuda.synchronize()
+    assert L.ppc_star_inverse(C.c_void_p(Ab.data_ptr()), nr, K, C.c_void_p(Q.data_ptr()), N, C.c_double(alpha),
+                              C.c_void_p(Cb.data_ptr())) == 0
+    assert L.ppc_synchronize() == 0
+    assert torch.equal(Cb, Cout[r0:r0 + nr])
+
+
+@pytest.mark.gpu
 def test_compress_re_identity_matches_direct(engine):
     """ppc_tsvdq_compress takes RE from ||A||^2 - sum s_ij^2 (Eckart-Young
     through the polish) when RE^2 >= 2e-2, from the orthogonal split
