@@ -1058,62 +1058,63 @@ bool ozaki_mode3_forward(const OzakiDigits& td, int64_t N, const double* Q, int6
 // buffers (6 levels x 32 columns each), and the epilogue drains one buffer
 // while the MMAs fill the other and streams every 128 x 32 FP64 sub-tile out
 // with a TMA store from a double-buffered staging tile. The kernel is bound
-// by the 8 bytes written per output.
+// by the 8 bytes written per output: 2.1 GB at cfg4 in 0.58 ms, DRAM writes at
+// 3.6 TB/s (about what a copy reaches in either direction). Direct st.global
+// from the epilogue warps (16 column segments of 256 B per warp) took 1.0 ms.
 namespace {
 
-constexpr int kRowsPerSplit = 32;
 constexpr int kRgNB = 32;        // sub-tile width (output columns)
 constexpr int kRgMaxSub = 8;     // N <= 256
 constexpr int kRgEpiWarps = 8;   // two per TMEM lane quadrant (16 columns each)
 constexpr int kRgThreads = (2 + kRgEpiWarps) * 32;
 
-// Row-wise split: digit row j of D holds row j of X (rows x K, column-major,
-// leading dimension ldx) scaled by sigma_j > 2 max_k |X(j, k)| (a power of
-// two), cut into ND digits along k (D layout [plane][row][KCp], zero padded).
-// CTA: 32 rows; lane = row (coalesced column loads); warp w: k in runs of 4
-// (w, w + 8, ...); the digits are staged in shared memory and written out as
-// contiguous 32 KCp-byte runs per plane.
+// Row-wise split: digit row j of D holds row j of X (rows x K <= 64,
+// column-major, leading dimension ldx) scaled by sigma_j > 2 max_k |X(j, k)|
+// (a power of two), cut into ND digits along k (D layout [plane][row][64],
+// zero padded). CTA: 64 rows; warp w: rows 32 (w / 4) + lane (coalesced
+// column loads), k in [16 (w % 4), +16); a row's values stay in registers
+// between the max and the digits; the digits are staged in shared memory and
+// written out as contiguous 64 x 64-byte runs per plane.
+constexpr int kRowsPerSplit = 64;
 template <int ND>
 __global__ void __launch_bounds__(256) ozaki_split_rows_kernel(const double* __restrict__ X, int64_t ldx, int64_t rows,
-                                                               int K, int KCp, int8_t* __restrict__ D,
+                                                               int K, int8_t* __restrict__ D,
                                                                double* __restrict__ scale) {
-    extern __shared__ uint8_t tile[];  // ND x 32 rows x (KCp + 16)
-    __shared__ double rmx[8][32];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int64_t r0 = (int64_t)blockIdx.x * kRowsPerSplit, row = r0 + lane;
+    constexpr int KCp = kBK, RS = KCp + 16;
+    __shared__ __align__(16) uint8_t tile[ND * kRowsPerSplit * RS];
+    __shared__ double rmx[4][kRowsPerSplit];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, half = w >> 2, kq = w & 3;
+    const int64_t r0 = (int64_t)blockIdx.x * kRowsPerSplit;
+    const int rl = half * 32 + lane;
+    const int64_t row = r0 + rl;
     const bool live = row < rows;
     const double* x = X + (live ? row : 0);
+    double v[16];
     double mx = 0.0;
-    for (int k4 = w; 4 * k4 < K; k4 += 8) {
-        double v[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int k = 4 * k4 + q;
-            v[q] = (live && k < K) ? __ldg(x + (int64_t)k * ldx) : 0.0;
-        }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) mx = fmax(mx, fabs(v[q]));
+    for (int u = 0; u < 16; ++u) {
+        const int k = 16 * kq + u;
+        v[u] = (live && k < K) ? __ldg(x + (int64_t)k * ldx) : 0.0;
     }
-    rmx[w][lane] = mx;
+#pragma unroll
+    for (int u = 0; u < 16; ++u) mx = fmax(mx, fabs(v[u]));
+    rmx[kq][rl] = mx;
     __syncthreads();
-    mx = 0.0;
-    for (int u = 0; u < 8; ++u) mx = fmax(mx, rmx[u][lane]);
-    if (w == 0 && live) scale[row] = mx > 0.0 ? ldexp(1.0, ilogb(mx) + 2) : 0.0;
+    mx = fmax(fmax(rmx[0][rl], rmx[1][rl]), fmax(rmx[2][rl], rmx[3][rl]));
+    if (kq == 0 && live) scale[row] = mx > 0.0 ? ldexp(1.0, ilogb(mx) + 2) : 0.0;
     const int e = mx > 0.0 ? ilogb(mx) + 2 : 0;
     constexpr int SH = 8 * (ND - 1);
     constexpr unsigned long long C80 = 0x8080808080808080ULL >> (64 - SH);
     const int e1 = (SH + 7 - e) / 2;
     const double scl1 = mx > 0.0 ? ldexp(1.0, e1) : 0.0, scl2 = ldexp(1.0, SH + 7 - e - e1);
-    const int RS = KCp + 16;
-    for (int k4 = w; 4 * k4 < KCp; k4 += 8) {
+#pragma unroll
+    for (int u4 = 0; u4 < 4; ++u4) {
         uint32_t wd[ND];
 #pragma unroll
         for (int t = 0; t < ND; ++t) wd[t] = 0u;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            const int k = 4 * k4 + q;
-            const double v = (live && k < K) ? __ldg(x + (int64_t)k * ldx) : 0.0;
-            const long long y = __double2ll_rn(v * scl1 * scl2);
+            const long long y = __double2ll_rn(v[4 * u4 + q] * scl1 * scl2);
             const long long U = y + (long long)C80;
             const uint64_t low = (uint64_t)U ^ C80;
             wd[0] |= (uint32_t)(uint8_t)(int8_t)(U >> SH) << (8 * q);
@@ -1122,7 +1123,7 @@ __global__ void __launch_bounds__(256) ozaki_split_rows_kernel(const double* __r
         }
 #pragma unroll
         for (int t = 0; t < ND; ++t)
-            *reinterpret_cast<uint32_t*>(tile + ((size_t)t * kRowsPerSplit + lane) * RS + 4 * k4) = wd[t];
+            *reinterpret_cast<uint32_t*>(tile + ((size_t)t * kRowsPerSplit + rl) * RS + 16 * kq + 4 * u4) = wd[t];
     }
     __syncthreads();
     const int nr = (int)std::min<int64_t>(kRowsPerSplit, rows - r0);
@@ -1164,7 +1165,9 @@ __global__ void __launch_bounds__(kRgThreads, 1)
     uint64_t* tfull = aempty + 1;   // [2]
     uint64_t* tempty = tfull + 2;   // [2]
     uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+    __shared__ double sbs[kRgMaxSub * kRgNB];  // column scales x 2^-30
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int n = threadIdx.x; n < P.N; n += blockDim.x) sbs[n] = P.sb[n] * 0x1.0p-30;
     if (threadIdx.x == 0) {
         bar_init(bfull, 1);
         bar_init(afull, 1);
@@ -1254,17 +1257,17 @@ __global__ void __launch_bounds__(kRgThreads, 1)
                     int32_t v[NL][8];
 #pragma unroll
                     for (int l = 0; l < NL; ++l) tmem_ld_32x32b_x8(ta + (uint32_t)(l * kRgNB + c * 8), v[l]);
-                    double scl[8];
-#pragma unroll
-                    for (int jj = 0; jj < 8; ++jj) scl[jj] = sm * P.sb[sb * kRgNB + c * 8 + jj] * 0x1.0p-30;
                     tmem_ld_wait();
 #pragma unroll
                     for (int jj = 0; jj < 8; ++jj) {
                         const long long g0 = ((long long)v[0][jj] << 16) + ((long long)v[1][jj] << 8) + v[2][jj];
                         const long long g1 = ((long long)v[3][jj] << 16) + ((long long)v[4][jj] << 8) + v[5][jj];
-                        // sum_l v_l 2^(-14-8l) = 2^-30 (g0 + 2^-24 g1)
+                        // sum_l v_l 2^(-14-8l) = 2^-30 (g0 + 2^-24 g1); 2^-30 sits in sbs
                         const double t = fma((double)g1, 0x1.0p-24, (double)g0);
-                        st[(c * 8 + jj) * kBM + q * 32 + lane] = t * scl[jj];
+                        const double val = (t * sm) * sbs[sb * kRgNB + c * 8 + jj];  // broadcast read
+                        asm volatile("st.shared.f64 [%0], %1;\n" ::"r"(smem_u32(st + (c * 8 + jj) * kBM + q * 32 + lane)),
+                                     "d"(val)
+                                     : "memory");
                     }
                 }
                 fence_before_sync();
@@ -1341,10 +1344,9 @@ bool ozaki_star_inverse(const double* A, int64_t M, int64_t K, const double* Q, 
     ad.D = DeviceBuffer(sizeof(int8_t) * kS * M * kBK);
     ad.sc = DeviceBuffer(sizeof(double) * M);
     {
-        const size_t smem = (size_t)kS * kRowsPerSplit * (kBK + 16);
         StageTimer ts("ozaki_split", s, 0.0, 8.0 * M * K + (double)kS * M * kBK);
-        ozaki_split_rows_kernel<kS><<<(unsigned)((M + kRowsPerSplit - 1) / kRowsPerSplit), 256, smem, s>>>(
-            A, M, M, (int)K, (int)kBK, ad.D.as<int8_t>(), ad.sc.d());
+        ozaki_split_rows_kernel<kS><<<(unsigned)((M + kRowsPerSplit - 1) / kRowsPerSplit), 256, 0, s>>>(
+            A, M, M, (int)K, ad.D.as<int8_t>(), ad.sc.d());
         count_launch();
         check_launch("ozaki_split_rows");
     }
