@@ -169,7 +169,7 @@ def ncu_traffic(workload, stage):
     committed ncu --set full capture (profiles/<round>/ncu_<stage>_<workload>_raw.csv)."""
     import csv
     import glob
-    names = {"gram_syrk": "ws_syrk", "facewise": "cfg4_gemms", "ozaki_syrk": "ozaki_syrk"}
+    names = {"gram_syrk": "ws_syrk", "facewise": "cfg4_gemms", "ozaki_syrk": "ozaki_syrk", "ozaki_gemm": "ozaki_face"}
     key = names.get(stage, stage)
     for path in sorted(glob.glob(os.path.join(ROOT, "profiles", "*", f"ncu_{key}*raw.csv")), reverse=True):
         if workload not in os.path.basename(path) and stage != "facewise":
