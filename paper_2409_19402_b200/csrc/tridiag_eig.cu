@@ -148,44 +148,70 @@ __device__ __forceinline__ void update_pass(const TrdParams& P, double* A, int j
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     const int i0 = (j + 1) & ~1;
     if (P.Aw) {
-        // slots past cps live in L2: four row pairs of a lane in flight per
-        // round (a load-use loop would pay one L2 round trip per 64 rows)
-        for (int t = P.cps + warp; t < cpc; t += nw) {
-            const int c = blk + t * nblk;
-            if (c <= j || c >= n) continue;  // warp-uniform
-            const double vc = vs[c], wc = ws[c];
-            double* a = P.Aw + (size_t)(t - P.cps) * n;
-            const bool pub = (c == j + 2);
-            double acc = 0.0;
-            for (int ib = i0 + 2 * lane; ib < n; ib += 256) {
-                double2 av[4];
+        // slots past cps live in L2: a warp takes kCw of its columns at once,
+        // kU row pairs of each per lane per round, so kCw * kU loads are in
+        // flight (a column at a time paid one L2 round trip per column and
+        // 256 rows); every column's products keep the row order of a lane
+        constexpr int kCw = 2, kU = 4;
+        for (int t0 = P.cps + warp; t0 < cpc; t0 += kCw * nw) {
+            bool ok[kCw];
+            double vc[kCw], wc[kCw], acc[kCw];
+            double* a[kCw];
+            bool any = false;
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int i = ib + 64 * u;
-                    av[u] = i < n ? __ldcg(reinterpret_cast<const double2*>(a + i)) : make_double2(0.0, 0.0);
-                }
+            for (int q = 0; q < kCw; ++q) {
+                const int t = t0 + q * nw;
+                const int c = blk + t * nblk;
+                ok[q] = t < cpc && c > j && c < n;  // warp-uniform
+                any |= ok[q];
+                vc[q] = ok[q] ? vs[c] : 0.0;
+                wc[q] = ok[q] ? ws[c] : 0.0;
+                acc[q] = 0.0;
+                a[q] = P.Aw + (size_t)(t - P.cps) * n;
+            }
+            if (!any) continue;
+            for (int ib = i0 + 2 * lane; ib < n; ib += 64 * kU) {
+                double2 av[kCw][kU];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
+                for (int q = 0; q < kCw; ++q)
+#pragma unroll
+                    for (int u = 0; u < kU; ++u) {
+                        const int i = ib + 64 * u;
+                        av[q][u] = ok[q] && i < n ? __ldcg(reinterpret_cast<const double2*>(a[q] + i))
+                                                  : make_double2(0.0, 0.0);
+                    }
+#pragma unroll
+                for (int u = 0; u < kU; ++u) {
                     const int i = ib + 64 * u;
                     if (i >= n) break;
                     const double2 v2 = *reinterpret_cast<const double2*>(vs + i);
                     const double2 w2 = *reinterpret_cast<const double2*>(ws + i);
-                    double2 nv;
-                    nv.x = fma(-w2.x, vc, fma(-v2.x, wc, av[u].x));
-                    nv.y = fma(-w2.y, vc, fma(-v2.y, wc, av[u].y));
-                    __stcg(reinterpret_cast<double2*>(a + i), nv);
-                    if (vn) {
-                        const double2 n2 = *reinterpret_cast<const double2*>(vn + i);
-                        acc = fma(nv.x, n2.x, acc);
-                        acc = fma(nv.y, n2.y, acc);
+                    const double2 n2 = vn ? *reinterpret_cast<const double2*>(vn + i) : make_double2(0.0, 0.0);
+#pragma unroll
+                    for (int q = 0; q < kCw; ++q) {
+                        if (!ok[q]) continue;
+                        double2 nv;
+                        nv.x = fma(-w2.x, vc[q], fma(-v2.x, wc[q], av[q][u].x));
+                        nv.y = fma(-w2.y, vc[q], fma(-v2.y, wc[q], av[q][u].y));
+                        __stcg(reinterpret_cast<double2*>(a[q] + i), nv);
+                        if (vn) {
+                            acc[q] = fma(nv.x, n2.x, acc[q]);
+                            acc[q] = fma(nv.y, n2.y, acc[q]);
+                        }
+                        if (blk + (t0 + q * nw) * nblk == j + 2) *reinterpret_cast<double2*>(cp + i) = nv;
                     }
-                    if (pub) *reinterpret_cast<double2*>(cp + i) = nv;
                 }
             }
             if (vn) {
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-                if (lane == 0 && c > j + 1) pgo[by_slot ? t : c] = taun * acc;
+                for (int q = 0; q < kCw; ++q) {
+                    if (!ok[q]) continue;
+                    double r = acc[q];
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+                    const int t = t0 + q * nw, c = blk + t * nblk;
+                    if (lane == 0 && c > j + 1) pgo[by_slot ? t : c] = taun * r;
+                }
             }
         }
     }

@@ -431,6 +431,35 @@ def test_large_slice_svd_direct_batched(engine, m, n, batch):
         assert np.linalg.norm(rec - ak) <= 1e-10 * np.linalg.norm(a[:, :, z])
 
 
+_TRD_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+from paper_2409_19402_b200 import projprod as P
+rng = np.random.default_rng(5)
+a = np.asfortranarray(rng.standard_normal((512, 512, 24)) + 0.25)
+U, s, V = P.truncated_svd(a, 8)
+np.savez(sys.argv[2], U=U, s=s, V=V)
+"""
+
+
+def test_slice_tridiag_l2_copy_matches_shared_memory(tmp_path):
+    """The batched Householder reduction with the working copy in L2 (one
+    wave, several columns per warp in flight) against the shared-memory
+    variant (three waves): same per-lane row order, so the same bits."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = {}
+    for tag, env in (("l2", {}), ("smem", {"PPC_TRD_GMEM": "0"})):
+        f = str(tmp_path / f"{tag}.npz")
+        subprocess.run([sys.executable, "-c", _TRD_SCRIPT, root, f], check=True, env={**os.environ, **env},
+                       timeout=600)
+        out[tag] = np.load(f)
+    for key in ("U", "s", "V"):
+        assert np.array_equal(out["l2"][key], out["smem"][key]), key
+
+
 @pytest.mark.parametrize("m,n", [(300, 260), (301, 261), (260, 300)])
 def test_large_slice_svd_direct_zero_and_repeated(engine, m, n):
     """Large-slice path (even order: batched direct eigensolver; odd: subspace
