@@ -20,12 +20,11 @@ template <class Cfg, bool AK, bool BNM, int VEC, int EPI>
 void launch_variant(const GemmParams& P, dim3 grid, cudaStream_t s) {
     auto kern = dmma_gemm_kernel<Cfg::BM, Cfg::BN, Cfg::BK, Cfg::WARPS_M, Cfg::WARPS_N,
                                  Cfg::STAGES, AK, BNM, VEC, EPI>;
-    static bool attr_set = false;  // per instantiation, per process (one device type)
-    if (!attr_set) {
+    static std::atomic<uint64_t> attr_set{0};  // per instantiation, per device
+    once_per_device(attr_set, [&] {
         PPC_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             (int)Cfg::smem));
-        attr_set = true;
-    }
+    });
     kern<<<grid, Cfg::threads, Cfg::smem, s>>>(P);
 }
 

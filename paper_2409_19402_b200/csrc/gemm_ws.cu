@@ -84,11 +84,10 @@ struct WsCfg {
                        int grid, cudaStream_t s) {
         auto k = dmma_gemm_ws_kernel<BM, BN, 16, WARPS_M, WARPS_N, STAGES, AK, BNM, EPI>;
         const size_t sm = smem + (EPI != EPI_STORE ? (size_t)BM * BN * 8 + 16 : 0);
-        static bool set = false;
-        if (!set) {
+        static std::atomic<uint64_t> set{0};
+        once_per_device(set, [&] {
             PPC_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-            set = true;
-        }
+        });
         k<<<grid, ws_threads<BM, BN, WARPS_M, WARPS_N, EPI>(), sm, s>>>(a, b, x, P);
     }
 };

@@ -4,6 +4,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <cstdio>
 #include <stdexcept>
@@ -51,6 +52,14 @@ cudaStream_t copy_out_stream();  // this thread's D2H stream
 // tiny flag never splits the pool's cached multi-GB blocks.
 int* status_words();
 inline void count_launch(int n = 1) { ctx().launches += n; }
+// Per-device one-time setup (cudaFuncSetAttribute and the like): runs f the
+// first time for the current device; `done` holds one bit per device.
+template <class F> inline void once_per_device(std::atomic<uint64_t>& done, F&& f) {
+    const uint64_t bit = 1ull << (ctx().device & 63);
+    if (done.load(std::memory_order_acquire) & bit) return;
+    f();
+    done.fetch_or(bit, std::memory_order_release);
+}
 void check_launch(const char* name);  // cudaGetLastError -> PPC_CUDA
 
 // Stream-ordered device buffer (cudaMallocAsync on the current stream; the

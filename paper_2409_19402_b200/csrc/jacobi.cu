@@ -465,13 +465,12 @@ void jacobi_svd(const double* A, int64_t m, int64_t n, int64_t strideA, int64_t 
                 int sweep_cap, const int* zmap) {
     HostProf hp_("jacobi_svd");
     if (batch == 0) return;
-    static bool tol_set = false;
-    if (!tol_set) {
+    static std::atomic<uint64_t> tol_set{0};  // the symbol lives in each device's module
+    once_per_device(tol_set, [] {
         const char* e = std::getenv("PPC_JACOBI_TOL");
         const double v = e ? std::atof(e) : 1.0;
         PPC_CUDA_CHECK(cudaMemcpyToSymbol(c_tol_scale, &v, sizeof(double)));
-        tol_set = true;
-    }
+    });
     const int64_t R = m > n ? m : n, C = m > n ? n : m;
     if (k < 1 || k > C) fail(PPC_ARGUMENT, "jacobi_svd: k out of range");
     const size_t smem = jacobi_smem_bytes(m, n);

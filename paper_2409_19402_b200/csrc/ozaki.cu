@@ -32,6 +32,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cfloat>
 #include <atomic>
 #include <cstdlib>
 #include <mutex>
@@ -632,12 +633,11 @@ void launch_mma(const CUtensorMap& ma, const CUtensorMap& mb, const OzParams& P,
     // stages + barriers + TMEM slot + the epilogue warps' residual sums
     constexpr int STG = stages_for(BN, NL);
     const size_t smem = 1024 + (size_t)STG * NL * (kBM + BN) * kBK + (2 * STG + 2) * 8 + 16 + 16 * kEpiWarps;
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<uint64_t> attr{0};
+    once_per_device(attr, [&] {
         PPC_CUDA_CHECK(cudaFuncSetAttribute(ozaki_mma_kernel<SYM, AMN, RESID, BN, NL, SYMA>,
                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
-    }
+    });
     if (items == 0) return;
     ozaki_mma_kernel<SYM, AMN, RESID, BN, NL, SYMA><<<(unsigned)ozaki_grid(items), kThreads, smem, s>>>(
         ma, mb, ma2 ? *ma2 : ma, P, items);
@@ -830,7 +830,8 @@ __global__ void __launch_bounds__(256) peak_ratio_kernel(const double* __restric
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u)
-            if (qv[u] > 0.0) mx = fmax(mx, 0.5 * sv[u] * sqrtK / sqrt(qv[u]));
+            if (!(qv[u] <= DBL_MAX && sv[u] <= DBL_MAX)) mx = INFINITY;  // NaN / inf in the block column: fail the gate
+            else if (qv[u] > 0.0) mx = fmax(mx, 0.5 * sv[u] * sqrtK / sqrt(qv[u]));
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -1097,11 +1098,15 @@ __global__ void __launch_bounds__(256) ozaki_split_rows_kernel(const double* __r
         v[u] = (live && k < K) ? __ldg(x + (int64_t)k * ldx) : 0.0;
     }
 #pragma unroll
-    for (int u = 0; u < 16; ++u) mx = fmax(mx, fabs(v[u]));
+    for (int u = 0; u < 16; ++u) mx = fmax(mx, fabs(v[u]) <= DBL_MAX ? fabs(v[u]) : INFINITY);  // NaN -> inf
     rmx[kq][rl] = mx;
     __syncthreads();
     mx = fmax(fmax(rmx[0][rl], rmx[1][rl]), fmax(rmx[2][rl], rmx[3][rl]));
-    if (kq == 0 && live) scale[row] = mx > 0.0 ? ldexp(1.0, ilogb(mx) + 2) : 0.0;
+    // a row holding a NaN or an infinity: zero digits and a NaN scale, the
+    // mark star_inv_fixup_kernel recomputes the row by on FP64 FMAs
+    const bool bad = !(mx <= DBL_MAX);
+    if (bad) mx = 0.0;
+    if (kq == 0 && live) scale[row] = bad ? NAN : (mx > 0.0 ? ldexp(1.0, ilogb(mx) + 2) : 0.0);
     const int e = mx > 0.0 ? ilogb(mx) + 2 : 0;
     constexpr int SH = 8 * (ND - 1);
     constexpr unsigned long long C80 = 0x8080808080808080ULL >> (64 - SH);
@@ -1301,6 +1306,31 @@ constexpr size_t rg_smem() {
 }
 
 // Bt (K x N) = alpha Q^T for Q (N x K, column-major): column n = alpha Q(n, :)
+// Rows of the star inverse whose input holds a NaN or an infinity (scale
+// marked NaN by the row split): C(r, :) = A(r, :) Bt on FP64 FMAs, so the
+// non-finite pattern is the FP64 product's (its NaN / inf positions do not
+// depend on the summation order). One warp per 32 scanned rows, lanes over
+// the columns of each marked row.
+__global__ void star_inv_fixup_kernel(const double* __restrict__ A, int64_t M, int K, const double* __restrict__ Bt,
+                                      int N, const double* __restrict__ scale, double* __restrict__ C, int64_t ldc) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t r0 = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; r0 < M; r0 += warps * 32) {
+        const int64_t r = r0 + lane;
+        unsigned bad = __ballot_sync(0xffffffffu, r < M && isnan(scale[r]));
+        while (bad) {
+            const int b = __ffs(bad) - 1;
+            bad &= bad - 1;
+            const int64_t row = r0 + b;
+            for (int c = lane; c < N; c += 32) {
+                double acc = 0.0;
+                for (int k = 0; k < K; ++k) acc = fma(A[row + (int64_t)k * M], Bt[k + (int64_t)c * K], acc);
+                C[row + (int64_t)c * ldc] = acc;
+            }
+        }
+    }
+}
+
 __global__ void star_bt_kernel(const double* __restrict__ Q, int64_t N, int64_t K, double alpha, double* __restrict__ Bt) {
     const int64_t total = K * N;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
@@ -1368,12 +1398,11 @@ bool ozaki_star_inverse(const double* A, int64_t M, int64_t K, const double* Q, 
     P.tiles = (M + kBM - 1) / kBM;
     P.sa = ad.sc.d();
     P.sb = bd.sc.d();
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<uint64_t> attr{0};
+    once_per_device(attr, [] {
         PPC_CUDA_CHECK(cudaFuncSetAttribute(ozaki_rowgemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             (int)rg_smem()));
-        attr = true;
-    }
+    });
     {
         // bytes: the FP64 output written and A's digit planes read (HBM-bound: 8 B per output)
         StageTimer tk("ozaki_star_inv", s, 2.0 * kS * (kS + 1) / 2 * (double)M * K * N,
@@ -1383,6 +1412,11 @@ bool ozaki_star_inverse(const double* A, int64_t M, int64_t K, const double* Q, 
         count_launch();
         check_launch("ozaki_rowgemm");
     }
+    // non-finite rows (none in the common case: the kernel only scans the scales)
+    star_inv_fixup_kernel<<<(unsigned)std::min<int64_t>((M + 255) / 256, 8 * (int64_t)ctx().sms), 256, 0, s>>>(
+        A, M, (int)K, bt.d(), (int)N, ad.sc.d(), C, ldc);
+    count_launch();
+    check_launch("star_inv_fixup");
     return true;
 }
 

@@ -344,12 +344,11 @@ void panel_gram(const double* A, int64_t sA, const double* B, int64_t sB, int64_
     if (batch <= 0) return;
     const bool same = (A == B) && (sA == sB);
     const size_t smem = sizeof(double) * kBc * kGP * (same ? 1 : 2);
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<uint64_t> attr{0};
+    once_per_device(attr, [] {
         PPC_CUDA_CHECK(cudaFuncSetAttribute(panel_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             (int)(sizeof(double) * kBc * kGP * 2)));
-        attr = true;
-    }
+    });
     const int nt = (int)((bc + 15) / 16);
     const int ns = panel_splits(r);
     const int64_t zx = std::max<int64_t>(zext, batch);
@@ -369,12 +368,11 @@ void chol_inv64(const double* S, int64_t bc, int64_t batch, bool shift, double* 
     if (bc < 1 || bc > kBc) fail(PPC_ARGUMENT, "chol_inv64: bc out of range");
     if (batch <= 0) return;
     const size_t smem = sizeof(double) * 4 * kBc * (kBc + 1);
-    static bool attr = false;
-    if (!attr) {
+    static std::atomic<uint64_t> attr{0};
+    once_per_device(attr, [&] {
         PPC_CUDA_CHECK(
             cudaFuncSetAttribute(chol_inv64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
-    }
+    });
     chol_inv64_kernel<<<(unsigned)batch, 256, smem, s>>>(S, (int)bc, shift ? 1 : 0, Rinv, failed, zmap, weak);
     count_launch();
     check_launch("chol_inv64");

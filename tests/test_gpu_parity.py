@@ -1234,6 +1234,104 @@ def test_star_inverse_vs_numpy(engine, M, K, N, alpha):
     assert torch.equal(Cb, Cout[r0:r0 + nr])
 
 
+class _Stages:
+    """Records which engine stages ran (ppc_timing_report)."""
+
+    def __enter__(self):
+        import ctypes as C
+        from paper_2409_19402_b200 import _lib
+        self.L = _lib.lib()
+        self.L.ppc_timing_report(C.create_string_buffer(1 << 16), 1 << 16, 1)
+        self.L.ppc_timing_enable(1)
+        return self
+
+    def __exit__(self, *exc):
+        import ctypes as C
+        import json
+        self.L.ppc_synchronize()
+        buf = C.create_string_buffer(1 << 16)
+        self.L.ppc_timing_report(buf, len(buf), 1)
+        self.L.ppc_timing_enable(0)
+        self.names = set(json.loads(buf.value.decode()))
+        return False
+
+
+def _assert_nonfinite_match(got, want, rtol=1e-12):
+    """Same NaN and infinity positions (and infinity signs); the finite part
+    within rtol of the finite part's norm."""
+    assert np.array_equal(np.isnan(got), np.isnan(want))
+    assert np.array_equal(np.isposinf(got), np.isposinf(want))
+    assert np.array_equal(np.isneginf(got), np.isneginf(want))
+    f = np.isfinite(want)
+    assert np.linalg.norm(got[f] - want[f]) <= rtol * np.linalg.norm(want[f])
+
+
+@pytest.mark.gpu
+def test_star_inverse_nonfinite_rows(engine):
+    """ppc_star_inverse with NaN / infinity in some rows: those rows are
+    recomputed on FP64 FMAs (the row split marks them), so the output has the
+    FP64 product's NaN / infinity pattern; the other rows stay on the INT8
+    path at <= 1e-12."""
+    import ctypes as C
+    import torch
+    from paper_2409_19402_b200 import _lib
+    L = _lib.lib()
+    M, K, N, alpha = 1000, 64, 128, 0.5
+    g = torch.Generator(device="cuda")
+    g.manual_seed(11)
+    A = torch.randn(K, M, dtype=torch.float64, device="cuda", generator=g).t()
+    A[3, 5] = float("nan")
+    A[70, 0] = float("inf")
+    A[71, 9] = -float("inf")
+    A[72, 1], A[72, 2] = float("inf"), -float("inf")
+    A[999, 63] = float("nan")
+    Q = (torch.randn(K, N, dtype=torch.float64, device="cuda", generator=g) / K ** 0.5).t()
+    Cout = torch.empty(N, M, dtype=torch.float64, device="cuda").t()
+    torch.cuda.synchronize()
+    assert L.ppc_star_inverse(C.c_void_p(A.data_ptr()), M, K, C.c_void_p(Q.data_ptr()), N, C.c_double(alpha),
+                              C.c_void_p(Cout.data_ptr())) == 0, L.ppc_last_error()
+    assert L.ppc_synchronize() == 0
+    with np.errstate(invalid="ignore"):
+        want = A.cpu().numpy() @ (alpha * Q.cpu().numpy()).T
+    _assert_nonfinite_match(Cout.cpu().numpy(), want)
+    assert np.isnan(want[3]).all() and np.isnan(want[999]).all() and not np.isfinite(want[70:73]).any()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("b_inf", [False, True])
+def test_star_q_nonfinite_matches_fp64(engine, b_inf):
+    """star_q_product at a shape whose facewise and inverse take the INT8
+    paths, with a NaN in A (and an infinity in B): the dynamic-range gate
+    sends the row block holding the NaN (every block, for B's infinity) to
+    FP64 DMMA and the inverse recomputes the non-finite rows, so NaN /
+    infinity land where the FP64 chain (star_products.cpp:51-59) puts them;
+    device and host input agree."""
+    rng = np.random.default_rng(21)
+    n1, m, n2, n3, p = 384, 256, 128, 64, 32
+    a = np.asfortranarray(rng.standard_normal((n1, m, n3)))
+    b = np.asfortranarray(rng.standard_normal((m, n2, n3)))
+    a[5, 7, 3] = np.nan
+    if b_inf:
+        b[9, 11, 20] = np.inf
+    t = engine.Transform("dct", n3, p)
+    q = t.q
+    with _Stages() as st:
+        got = engine.to_host(engine.star_q_product(engine.to_device(a), engine.to_device(b), t))
+    assert "ozaki_star_inv" in st.names, st.names
+    assert ("ozaki_gemm" in st.names) == (not b_inf), st.names
+    with np.errstate(invalid="ignore"):
+        ah = np.einsum("ijt,tq->ijq", a, q)
+        bh = np.einsum("ijt,tq->ijq", b, q)
+        ch = np.einsum("ijq,jkq->ikq", ah, bh)
+        want = np.einsum("ikq,tq->ikt", ch, q) * t.scale
+    assert np.isnan(want[5]).all()
+    if b_inf:
+        assert not np.isfinite(want[:, 11]).any()
+    _assert_nonfinite_match(got, want)
+    host = engine.star_q_product(a, b, t)
+    assert np.array_equal(host, got, equal_nan=True)
+
+
 @pytest.mark.gpu
 def test_compress_re_identity_matches_direct(engine):
     """ppc_tsvdq_compress takes RE from ||A||^2 - sum s_ij^2 (Eckart-Young
