@@ -1361,8 +1361,11 @@ bool ozaki_star_inverse_eligible(int64_t K, int64_t N) {
 
 bool ozaki_star_inverse(const double* A, int64_t M, int64_t K, const double* Q, int64_t N, double alpha, double* C,
                         int64_t ldc, cudaStream_t s) {
-    // (an odd ldc cannot carry the TMA store: FP64 DMMA then, for that call only)
-    if (!ozaki_star_inverse_eligible(K, N) || M < 1 || (ldc & 1) || ldc < M) return false;
+    // (an odd ldc or a C not 16-byte aligned cannot carry the TMA store: FP64
+    // DMMA then, for that call only)
+    if (!ozaki_star_inverse_eligible(K, N) || M < 1 || (ldc & 1) || ldc < M ||
+        (reinterpret_cast<uintptr_t>(C) & 15))
+        return false;
     StageTimer tm("mode3_inv", s, 2.0 * M * K * N, 8.0 * (M * K + M * N + K * N));
     // A (M x K, leading dimension M): row-wise digits
     OzakiDigits ad;

@@ -1232,6 +1232,14 @@ def test_star_inverse_vs_numpy(engine, M, K, N, alpha):
                               C.c_void_p(Cb.data_ptr())) == 0
     assert L.ppc_synchronize() == 0
     assert torch.equal(Cb, Cout[r0:r0 + nr])
+    # an output 8 bytes off 16-byte alignment cannot take the TMA store: the
+    # call runs on FP64 DMMA instead, same tolerance
+    raw = torch.empty(M * N + 1, dtype=torch.float64, device="cuda")
+    assert L.ppc_star_inverse(C.c_void_p(A.data_ptr()), M, K, C.c_void_p(Q.data_ptr()), N, C.c_double(alpha),
+                              C.c_void_p(raw.data_ptr() + 8)) == 0, L.ppc_last_error()
+    assert L.ppc_synchronize() == 0
+    got2 = raw[1:].reshape(N, M).t().cpu().numpy()
+    assert np.linalg.norm(got2 - want) <= 1e-12 * np.linalg.norm(want)
 
 
 class _Stages:
