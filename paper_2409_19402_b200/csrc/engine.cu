@@ -78,10 +78,9 @@ bool facewise_ozaki(const double* Ah, int64_t n1, int64_t m, int64_t p, const do
     StageTimer tm("facewise", s, 2.0 * n1 * m * n2 * p, 8.0 * p * (n1 * m + m * n2 + n1 * n2));
     // both operands split and their gate values computed on the device, then
     // one host read for the decision (B's only with the first row block)
-    DeviceBuffer at(sizeof(double) * n1 * m * p);
-    launch_transpose(Ah, at.d(), n1, m, p, s);  // (m x n1) per slice
+    // A-hat's slices split as their transposes (m x n1, K-major), read in place
     OzakiDigits Ad;
-    Ad.split(at.d(), m, m * n1, m, n1, m, p, s);
+    Ad.split(Ah, n1, n1 * m, m, n1, m, p, s, nullptr, 0, 0, 0, nullptr, 6, 0, 0, nullptr, 0, true);
     const int64_t ng = ozaki_peak_groups(Ad, kFaceRows);
     DeviceBuffer peaks(sizeof(double) * (ng + 1));
     ozaki_peak_ratios_async(Ad, m, kFaceRows, peaks.d(), s);

@@ -78,7 +78,11 @@ static_assert(kBN / 2 == 40, "epilogue column split (32 + 8)");
 // CPB columns per CTA (CPB * KCp <= 4096): 256 / CPB threads per column, so
 // short blocks (the facewise / filter operands, K = 512 .. 2048) still keep
 // 16 loads per thread in flight.
-template <int ND, int CPB>
+// TRS: the source is transposed, element (k, c) of block b at
+// X[b stride + c + k ldx] (the facewise product's A-hat slices, read in place
+// of a transposed copy): loaded with the columns across the lanes (coalesced),
+// staged, then reduced and split exactly as a column-major source.
+template <int ND, int CPB, bool TRS = false>
 __global__ void __launch_bounds__(256) ozaki_split_kernel(const double* __restrict__ X, int64_t ldx, int64_t stride,
                                                           int64_t rows, int64_t cols, int64_t KC, int64_t KCp,
                                                           int64_t chunk, int64_t per, int8_t* __restrict__ D,
@@ -87,7 +91,8 @@ __global__ void __launch_bounds__(256) ozaki_split_kernel(const double* __restri
                                                           const double* __restrict__ fixed_max, int nwrite) {
     constexpr int TPC = 256 / CPB;  // threads per column
     constexpr int WPC = TPC / 32;   // warps per column
-    __shared__ double stage[kKC];
+    constexpr int SCOL = kKC / CPB + (TRS ? 1 : 0);  // staged column stride (+1: no bank conflicts)
+    __shared__ double stage[TRS ? SCOL * CPB : kKC];
     const int cc = threadIdx.x / TPC, lt = threadIdx.x % TPC;
     const int64_t j = (int64_t)blockIdx.x * CPB + cc;
     const bool live = j < cols;
@@ -103,21 +108,41 @@ __global__ void __launch_bounds__(256) ozaki_split_kernel(const double* __restri
         len = std::max<int64_t>(0, end - r0);
     }
     if (!live) len = 0;
-    const double* col = X + (stride ? b * stride : 0) + (live ? j : 0) * ldx + r0;
-    double* stg = stage + cc * (kKC / CPB);
+    double* stg = stage + cc * SCOL;
     // all 16 loads of a thread in flight before any use (the kernel is
     // DRAM-latency bound); same per-thread summation order as a strided loop
     double mx = 0.0, ss = 0.0;
     constexpr int NL = kKC / 256;
     double v[NL];
+    if (TRS) {
+        // lanes over the CPB columns, then over k; every column's full K
+        // extent is staged before the per-column reductions read it back
+        const int cl = threadIdx.x % CPB, kl = threadIdx.x / CPB;
+        const int64_t jc = (int64_t)blockIdx.x * CPB + cl;
+        const int64_t klen = jc < cols ? std::min<int64_t>(KC, rows) : 0;
+        const double* src = X + b * stride + (jc < cols ? jc : 0);
 #pragma unroll
-    for (int q = 0; q < NL; ++q) {
-        const int64_t i = lt + TPC * q;
-        v[q] = i < len ? __ldcs(col + i) : 0.0;
+        for (int q = 0; q < NL; ++q) {
+            const int64_t i = kl + TPC * q;
+            v[q] = i < klen ? __ldcs(src + i * ldx) : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < NL; ++q)
+            if (kl + TPC * q < kKC / CPB) stage[cl * SCOL + kl + TPC * q] = v[q];
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < NL; ++q) v[q] = stg[lt + TPC * q];
+    } else {
+        const double* col = X + (stride ? b * stride : 0) + (live ? j : 0) * ldx + r0;
+#pragma unroll
+        for (int q = 0; q < NL; ++q) {
+            const int64_t i = lt + TPC * q;
+            v[q] = i < len ? __ldcs(col + i) : 0.0;
+        }
     }
 #pragma unroll
     for (int q = 0; q < NL; ++q) {
-        stg[lt + TPC * q] = v[q];
+        if (!TRS) stg[lt + TPC * q] = v[q];
         mx = fmax(mx, fabs(v[q]));
         ss = fma(v[q], v[q], ss);
     }
@@ -698,8 +723,9 @@ void ozaki_syrk(const OzakiDigits& d, int64_t nout, int64_t per, double* out, cu
 void OzakiDigits::split(const double* X, int64_t ldx, int64_t stride, int64_t rows_, int64_t cols_, int64_t KC,
                         int64_t nblk_, cudaStream_t s, const int* zmap, int64_t nz, int64_t chunk, int64_t per,
                         int* nonfinite, int ndig, int64_t block_base, int64_t alloc_blocks,
-                        const double* fixed_max, int nwrite) {
+                        const double* fixed_max, int nwrite, bool trans_src) {
     HostProf hp_("ozaki_split");
+    if (trans_src && !stride) fail(PPC_ARGUMENT, "ozaki split: a transposed source needs batched blocks");
     if (ndig != kS && ndig != kSmax) fail(PPC_ARGUMENT, "ozaki split: 6 or 7 digits");
     if (block_base < 0 || (block_base > 0 && block_base + nblk_ > alloc_blocks))
         fail(PPC_ARGUMENT, "ozaki split: block range outside the allocation");
@@ -729,8 +755,14 @@ void OzakiDigits::split(const double* X, int64_t ldx, int64_t stride, int64_t ro
     const int64_t ch = chunk ? chunk : KC, pr = per ? per : 1;
     const int nw = (nwrite > 0 && nwrite < nd) ? nwrite : nd;  // leading planes written
 #define PPC_SPLIT(ND_, CPB_)                                                                                         \
-    ozaki_split_kernel<ND_, CPB_><<<grid, 256, 0, s>>>(X, ldx, stride, rows, cols, KC, KCp, ch, pr, D0, sc0, sq0,    \
-                                                       zmap, nonfinite, fixed_max, nw)
+    do {                                                                                                             \
+        if (trans_src)                                                                                               \
+            ozaki_split_kernel<ND_, CPB_, true><<<grid, 256, 0, s>>>(X, ldx, stride, rows, cols, KC, KCp, ch, pr,    \
+                                                                     D0, sc0, sq0, zmap, nonfinite, fixed_max, nw); \
+        else                                                                                                         \
+            ozaki_split_kernel<ND_, CPB_><<<grid, 256, 0, s>>>(X, ldx, stride, rows, cols, KC, KCp, ch, pr, D0, sc0, \
+                                                               sq0, zmap, nonfinite, fixed_max, nw);                 \
+    } while (0)
     if (nd == kSmax) {
         if (cpb == 8) PPC_SPLIT(kSmax, 8); else if (cpb == 4) PPC_SPLIT(kSmax, 4);
         else if (cpb == 2) PPC_SPLIT(kSmax, 2); else PPC_SPLIT(kSmax, 1);
