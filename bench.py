@@ -353,6 +353,15 @@ class Tsvdq:
     def value(self, sec):
         return self.in_bytes / sec / 1e9
 
+    def step_given_q(self, L):
+        """tsvdq(A, Q, k) alone (decompositions.cpp:62-83) with the basis the
+        last compress step left in self.Q: SURVEY 8(d) asks for the tSVDQ
+        time both with a given Q and including its construction."""
+        n1, n2, n3, p, k = self.dims
+        rc = L.ppc_tsvdq(ptr(self.A), n1, n2, n3, ptr(self.Q), p, k, ptr(self.U), ptr(self.S), ptr(self.V), 1)
+        if rc:
+            raise RuntimeError(L.ppc_last_error().decode())
+
     def dominant(self, stages):
         # the single most expensive kernel launch of the step (ncu launch
         # list: the Gram SYRK, on the INT8 tensor cores when the Ozaki path
@@ -844,6 +853,22 @@ def main():
 
     e2e = None if args.no_e2e else e2e_leg(wl, L, args.steps, world, dist_on)
 
+    # tSVDQ with a given Q (both timings): the Q of the last step
+    given_q = None
+    if hasattr(wl, "step_given_q") and args.workload in ("cfg5", "cfg3") and not args.no_fp64:
+        full_step = wl.step
+        wl.step = wl.step_given_q
+        try:
+            msq, stq, _ = timed_leg(wl, L, stream, args.steps, 1, dist_on)
+        finally:
+            wl.step = full_step
+        given_q = {"value": wl.value(msq / 1e3) * world, "unit": wl.unit, "ms_per_step": msq, "steps": args.steps,
+                   "warmup": 1, "step": "ppc_tsvdq(A, Q, k) = A x3 Q^T + facewise truncated SVDs "
+                                        "(decompositions.cpp:62-83), Q given (device-resident, from the last "
+                                        "compress step); the forward transform runs on FP64 DMMA here (no kept "
+                                        "Gram digits to reuse)",
+                   "stages": stage_summary(stq, msq * args.steps)}
+
     # the same step with every product on FP64 DMMA (no INT8 emulation)
     fp64 = None
     if args.workload == "cfg5" and not args.no_fp64:
@@ -899,6 +924,8 @@ def main():
                 "data": "synthetic", "config": cfg, "roofline": roof, "cpu_baseline": cpu,
                 "e2e": e2e, "gpu_launches": launches, "clocks": clk,
                 "stages": stage_summary(stages, ms_step * args.steps)}
+        if given_q is not None:
+            line["value_given_q"] = given_q
         if fp64 is not None:
             line["value_fp64_dmma"] = fp64
         if secondary is not None:

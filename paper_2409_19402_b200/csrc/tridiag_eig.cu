@@ -46,6 +46,11 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
 // Grid barrier over co-resident CTAs (cooperative launch) on a monotonic
 // arrival counter: barrier number b completes when the counter reaches
 // b * nblk, so nobody resets anything on the critical path.
+// (A flag per CTA, stored with release and polled by one warp with relaxed
+// vector loads and a closing acquire fence, measured slower: 6.3 against
+// 4.5 us a step at n = 1024 with 148 CTAs. The arrivals do not serialize in
+// L2 the way the same-address atomic model suggests; the second fence costs
+// more.)
 __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned nblk, unsigned& target) {
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -88,16 +93,26 @@ struct TrdParams {
                      //        writes step j+1 while a slow one still reads step j)
     double* colpub;  // 2 x n  published next pivot column, by step parity
     unsigned* bar;   // arrival counter (one per matrix, 128 bytes apart)
-    double* Aw;      // hybrid variant: owned slots >= cps in global memory (L2),
-                     // [matrix][CTA][slot - cps][n]; nullptr: all in shared memory
-    int cps;         // slots held in shared memory (hybrid variant)
+    double* Aw;      // hybrid variant: the owned slots < cpc - cps in global memory
+                     // (L2), [matrix][CTA][slot][n]; nullptr: all in shared memory
+    int cps;         // the last cps slots live in shared memory (hybrid variant):
+                     // the highest columns, which stay in the trailing matrix longest
     // batch: matrix b is G + b * strideG; its nblk CTAs are blocks
     // [b * nblk, (b+1) * nblk) and every output above is per matrix
     int64_t strideG;
     int blk;         // the CTA's rank within its matrix (set in the kernel)
+    long long* prof; // built with -DPPC_TRD_PROFILE and run with PPC_TRD_PROFILE=1: per-warp
+                     // clock sums of the step's phases (else nullptr)
 };
 
 constexpr size_t kTrdSmemMax = 200 * 1024;
+#ifndef PPC_TRD_KC
+#define PPC_TRD_KC 4
+#endif
+#ifndef PPC_TRD_KU
+#define PPC_TRD_KU 2
+#endif
+constexpr int kTrdKc = PPC_TRD_KC, kTrdKu = PPC_TRD_KU;  // columns per warp at once, row pairs per lane per round
 
 // Reflector of step jj from column jj (xs, rows jj+1..n-1), LAPACK dlarfg:
 // computed redundantly by every CTA (same bits everywhere). Writes vn and
@@ -133,116 +148,107 @@ __device__ __forceinline__ double make_reflector(const TrdParams& P, int jj, con
     return tau;
 }
 
-// One pass over the owned columns c > j: the step-j rank-2 update
-// A(j+1:, c) -= v w_c + w v_c, fused with the step-(j+1) products
-// p_c = tau' A(j+2:, c)^T v' of the updated columns (vn == nullptr: update
-// only). One warp per owned column, two rows per lane per iteration from an
-// even start (v, w and v' are zero in rows <= j, so the extra row is left
-// unchanged); the owner of column j+2 publishes it as it goes.
-// The products go to pgo[c] (pgo[slot] with by_slot) and the published
-// column to cp.
-__device__ __forceinline__ void update_pass(const TrdParams& P, double* A, int j, const double* vs,
-                                            const double* ws, const double* vn, double taun, double* pgo,
-                                            double* cp, bool by_slot) {
-    const int n = P.n, nblk = P.nblk, cpc = P.cpc, blk = P.blk;
+// Slots [ta, tb) of the owned columns, stored at base + (t - ta) * n (GM: in
+// the global working copy, read and written through L2 with ld/st.cg; else in
+// shared memory). A warp takes KC of its columns at once over the same rows,
+// KU row pairs of each per lane per round: v, w and v' are read from shared
+// memory once per KC columns (a column at a time spent 24 of every 40 bytes
+// of shared-memory traffic on them), and KC * KU loads are in flight (from L2
+// a column at a time paid one round trip per 256 rows). Every column's
+// products keep the row order of a lane, so the bits do not depend on KC, KU
+// or on where the column lives.
+template <bool GM, int KC, int KU>
+__device__ __forceinline__ void update_range(const TrdParams& P, double* base, int ta, int tb, int j,
+                                             const double* vs, const double* ws, const double* vn, double taun,
+                                             double* pgo, double* cp, bool by_slot) {
+    const int n = P.n, nblk = P.nblk, blk = P.blk;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     const int i0 = (j + 1) & ~1;
-    if (P.Aw) {
-        // slots past cps live in L2: a warp takes kCw of its columns at once,
-        // kU row pairs of each per lane per round, so kCw * kU loads are in
-        // flight (a column at a time paid one L2 round trip per column and
-        // 256 rows); every column's products keep the row order of a lane
-        constexpr int kCw = 2, kU = 4;
-        for (int t0 = P.cps + warp; t0 < cpc; t0 += kCw * nw) {
-            bool ok[kCw];
-            double vc[kCw], wc[kCw], acc[kCw];
-            double* a[kCw];
-            bool any = false;
+    for (int t0 = ta + warp; t0 < tb; t0 += KC * nw) {
+        bool ok[KC];
+        double vc[KC], wc[KC], acc[KC];
+        bool any = false;
 #pragma unroll
-            for (int q = 0; q < kCw; ++q) {
-                const int t = t0 + q * nw;
-                const int c = blk + t * nblk;
-                ok[q] = t < cpc && c > j && c < n;  // warp-uniform
-                any |= ok[q];
-                vc[q] = ok[q] ? vs[c] : 0.0;
-                wc[q] = ok[q] ? ws[c] : 0.0;
-                acc[q] = 0.0;
-                a[q] = P.Aw + (size_t)(t - P.cps) * n;
-            }
-            if (!any) continue;
-            for (int ib = i0 + 2 * lane; ib < n; ib += 64 * kU) {
-                double2 av[kCw][kU];
-#pragma unroll
-                for (int q = 0; q < kCw; ++q)
-#pragma unroll
-                    for (int u = 0; u < kU; ++u) {
-                        const int i = ib + 64 * u;
-                        av[q][u] = ok[q] && i < n ? __ldcg(reinterpret_cast<const double2*>(a[q] + i))
-                                                  : make_double2(0.0, 0.0);
-                    }
-#pragma unroll
-                for (int u = 0; u < kU; ++u) {
-                    const int i = ib + 64 * u;
-                    if (i >= n) break;
-                    const double2 v2 = *reinterpret_cast<const double2*>(vs + i);
-                    const double2 w2 = *reinterpret_cast<const double2*>(ws + i);
-                    const double2 n2 = vn ? *reinterpret_cast<const double2*>(vn + i) : make_double2(0.0, 0.0);
-#pragma unroll
-                    for (int q = 0; q < kCw; ++q) {
-                        if (!ok[q]) continue;
-                        double2 nv;
-                        nv.x = fma(-w2.x, vc[q], fma(-v2.x, wc[q], av[q][u].x));
-                        nv.y = fma(-w2.y, vc[q], fma(-v2.y, wc[q], av[q][u].y));
-                        __stcg(reinterpret_cast<double2*>(a[q] + i), nv);
-                        if (vn) {
-                            acc[q] = fma(nv.x, n2.x, acc[q]);
-                            acc[q] = fma(nv.y, n2.y, acc[q]);
-                        }
-                        if (blk + (t0 + q * nw) * nblk == j + 2) *reinterpret_cast<double2*>(cp + i) = nv;
-                    }
-                }
-            }
-            if (vn) {
-#pragma unroll
-                for (int q = 0; q < kCw; ++q) {
-                    if (!ok[q]) continue;
-                    double r = acc[q];
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
-                    const int t = t0 + q * nw, c = blk + t * nblk;
-                    if (lane == 0 && c > j + 1) pgo[by_slot ? t : c] = taun * r;
-                }
-            }
+        for (int q = 0; q < KC; ++q) {
+            const int t = t0 + q * nw;
+            const int c = blk + t * nblk;
+            ok[q] = t < tb && c > j && c < n;  // warp-uniform
+            any |= ok[q];
+            vc[q] = ok[q] ? vs[c] : 0.0;
+            wc[q] = ok[q] ? ws[c] : 0.0;
+            acc[q] = 0.0;
         }
-    }
-    const int ts = P.Aw ? P.cps : cpc;  // the shared-memory slots
-    for (int t = warp; t < ts; t += nw) {
-        const int c = blk + t * nblk;
-        if (c <= j || c >= n) continue;  // warp-uniform
-        const double vc = vs[c], wc = ws[c];
-        double* a = A + (size_t)t * n;
-        const bool pub = (c == j + 2);
-        double acc = 0.0;
-        for (int i = i0 + 2 * lane; i < n; i += 64) {
-            const double2 av = *reinterpret_cast<const double2*>(a + i);
-            const double2 v2 = *reinterpret_cast<const double2*>(vs + i);
-            const double2 w2 = *reinterpret_cast<const double2*>(ws + i);
-            double2 nv;
-            nv.x = fma(-w2.x, vc, fma(-v2.x, wc, av.x));
-            nv.y = fma(-w2.y, vc, fma(-v2.y, wc, av.y));
-            *reinterpret_cast<double2*>(a + i) = nv;
-            if (vn) {
-                const double2 n2 = *reinterpret_cast<const double2*>(vn + i);
-                acc = fma(nv.x, n2.x, acc);
-                acc = fma(nv.y, n2.y, acc);
+        if (!any) continue;
+        double* a0 = base + (size_t)(t0 - ta) * n;
+        const size_t astep = (size_t)nw * n;
+        for (int ib = i0 + 2 * lane; ib < n; ib += 64 * KU) {
+            double2 av[KC][KU];
+#pragma unroll
+            for (int q = 0; q < KC; ++q)
+#pragma unroll
+                for (int u = 0; u < KU; ++u) {
+                    const int i = ib + 64 * u;
+                    const double2* src = reinterpret_cast<const double2*>(a0 + q * astep + i);
+                    av[q][u] = ok[q] && i < n ? (GM ? __ldcg(src) : *src) : make_double2(0.0, 0.0);
+                }
+#pragma unroll
+            for (int u = 0; u < KU; ++u) {
+                const int i = ib + 64 * u;
+                if (i >= n) break;
+                const double2 v2 = *reinterpret_cast<const double2*>(vs + i);
+                const double2 w2 = *reinterpret_cast<const double2*>(ws + i);
+                const double2 n2 = vn ? *reinterpret_cast<const double2*>(vn + i) : make_double2(0.0, 0.0);
+#pragma unroll
+                for (int q = 0; q < KC; ++q) {
+                    if (!ok[q]) continue;
+                    double2 nv;
+                    nv.x = fma(-w2.x, vc[q], fma(-v2.x, wc[q], av[q][u].x));
+                    nv.y = fma(-w2.y, vc[q], fma(-v2.y, wc[q], av[q][u].y));
+                    double2* dst = reinterpret_cast<double2*>(a0 + q * astep + i);
+                    if (GM) __stcg(dst, nv);
+                    else *dst = nv;
+                    if (vn) {
+                        acc[q] = fma(nv.x, n2.x, acc[q]);
+                        acc[q] = fma(nv.y, n2.y, acc[q]);
+                    }
+                    if (blk + (t0 + q * nw) * nblk == j + 2) *reinterpret_cast<double2*>(cp + i) = nv;
+                }
             }
-            if (pub) *reinterpret_cast<double2*>(cp + i) = nv;
         }
         if (vn) {
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-            if (lane == 0 && c > j + 1) pgo[by_slot ? t : c] = taun * acc;
+            for (int q = 0; q < KC; ++q) {
+                if (!ok[q]) continue;
+                double r = acc[q];
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+                const int t = t0 + q * nw, c = blk + t * nblk;
+                if (lane == 0 && c > j + 1) pgo[by_slot ? t : c] = taun * r;
+            }
         }
+    }
+}
+
+// One pass over the owned columns c > j: the step-j rank-2 update
+// A(j+1:, c) -= v w_c + w v_c, fused with the step-(j+1) products
+// p_c = tau' A(j+2:, c)^T v' of the updated columns (vn == nullptr: update
+// only). Two rows per lane per iteration from an even start (v, w and v' are
+// zero in rows <= j, so the extra row is left unchanged); the owner of column
+// j+2 publishes it as it goes. The products go to pgo[c] (pgo[slot] with
+// by_slot) and the published column to cp.
+__device__ __forceinline__ void update_pass(const TrdParams& P, double* A, int j, const double* vs,
+                                            const double* ws, const double* vn, double taun, double* pgo,
+                                            double* cp, bool by_slot) {
+    const int cpc = P.cpc;
+    const int t1 = P.Aw ? cpc - P.cps : 0;  // slots [0, t1) in L2, [t1, cpc) in shared memory
+    if (t1 > 0) update_range<true, kTrdKc, kTrdKu>(P, P.Aw, 0, t1, j, vs, ws, vn, taun, pgo, cp, by_slot);
+    if (t1 < cpc) {
+        // few columns per warp (a single matrix spread over every SM): one at a
+        // time, or the chunk's empty columns would only cost predicates
+        if (cpc - t1 <= (int)(blockDim.x >> 5))
+            update_range<false, 1, 4>(P, A, t1, cpc, j, vs, ws, vn, taun, pgo, cp, by_slot);
+        else
+            update_range<false, kTrdKc, kTrdKu>(P, A, t1, cpc, j, vs, ws, vn, taun, pgo, cp, by_slot);
     }
 }
 
@@ -266,12 +272,13 @@ __global__ void __launch_bounds__(NT, 1) sytrd_kernel(TrdParams P0) {
         P.bar += (size_t)mat * 32;
     }
     const int n = P.n, nblk = P.nblk, cpc = P.cpc, blk = P.blk;
-    // cpc x n (slot t = column blk + t*nblk): slots < cps in shared memory,
-    // the rest (hybrid variant) in this CTA's slice of the global working copy
-    if (P.Aw) P.Aw += ((size_t)mat * nblk + blk) * (size_t)(cpc - P.cps) * n;
+    // cpc x n (slot t = column blk + t*nblk): the last cps slots in shared
+    // memory, the first cpc - cps (hybrid variant) in this CTA's slice of the
+    // global working copy
+    const int t1 = P.Aw ? cpc - P.cps : 0;  // first shared-memory slot
+    if (P.Aw) P.Aw += ((size_t)mat * nblk + blk) * (size_t)t1 * n;
     double* A = sm;
-    const int ts = P.Aw ? P.cps : cpc;
-    double* vs = A + (size_t)ts * n;  // reflector of step j
+    double* vs = A + (size_t)(cpc - t1) * n;  // reflector of step j
     double* vn = vs + n;               // reflector of step j+1
     double* ws = vn + n;               // w = p - K v
     double* xs = ws + n;               // pivot column
@@ -284,7 +291,7 @@ __global__ void __launch_bounds__(NT, 1) sytrd_kernel(TrdParams P0) {
         const int c = blk + t * nblk;
         if (c < n)
             for (int i = tid; i < n; i += nt)
-                (t < ts ? A + (size_t)t * n : P.Aw + (size_t)(t - ts) * n)[i] = P.G[(size_t)c * n + i];
+                (t >= t1 ? A + (size_t)(t - t1) * n : P.Aw + (size_t)t * n)[i] = P.G[(size_t)c * n + i];
     }
     for (int i = tid; i < n; i += nt) {
         xs[i] = P.G[i];
@@ -304,7 +311,14 @@ __global__ void __launch_bounds__(NT, 1) sytrd_kernel(TrdParams P0) {
             vs = vn;
             vn = t;
         }
+#ifdef PPC_TRD_PROFILE
+        long long c0 = 0, c1 = 0, c2 = 0, c3 = 0;
+        if (P.prof) c0 = clock64();
+#endif
         grid_barrier(P.bar, (unsigned)nblk, target);
+#ifdef PPC_TRD_PROFILE
+        if (P.prof) c1 = clock64();
+#endif
         // ---- p and the published column j+1 (both written before the barrier)
         const double* pg = P.pg + (size_t)(j & 1) * n;
         const double* cp = P.colpub + (size_t)(j & 1) * n;
@@ -328,12 +342,27 @@ __global__ void __launch_bounds__(NT, 1) sytrd_kernel(TrdParams P0) {
         }
         if (tid == 0) ws[j] = 0.0;  // rows <= j of w stay zero (read by the paired-row pass)
         __syncthreads();
+#ifdef PPC_TRD_PROFILE
+        if (P.prof) c2 = clock64();
+#endif
         if (j + 1 <= n - 3) {
             const double taun = make_reflector(P, j + 1, xs, vn, red, rpar);
             __syncthreads();
+#ifdef PPC_TRD_PROFILE
+            if (P.prof) c3 = clock64();
+#endif
             update_pass(P, A, j, vs, ws, vn, taun, P.pg + (size_t)((j + 1) & 1) * n,
                         P.colpub + (size_t)((j + 1) & 1) * n, false);
             tau = taun;
+#ifdef PPC_TRD_PROFILE
+            if (P.prof && (tid & 31) == 0) {  // per warp: barrier wait, p/w pass, reflector, update
+                long long* q = P.prof + ((size_t)blockIdx.x * (nt >> 5) + (tid >> 5)) * 4;
+                q[0] += c1 - c0;
+                q[1] += c2 - c1;
+                q[2] += c3 - c2;
+                q[3] += clock64() - c3;
+            }
+#endif
         } else {
             update_pass(P, A, j, vs, ws, nullptr, 0.0, nullptr, P.colpub + (size_t)((j + 1) & 1) * n, false);
         }
@@ -343,13 +372,13 @@ __global__ void __launch_bounds__(NT, 1) sytrd_kernel(TrdParams P0) {
     for (int t = 0; t < cpc; ++t) {
         const int c = blk + t * nblk;
         if (tid == 0 && c == n - 2) {
-            const double* a = t < ts ? A + (size_t)t * n : P.Aw + (size_t)(t - ts) * n;
+            const double* a = t >= t1 ? A + (size_t)(t - t1) * n : P.Aw + (size_t)t * n;
             P.d[n - 2] = a[n - 2];
             P.e[n - 2] = a[n - 1];
             P.tau[n - 2] = 0.0;
         }
         if (tid == 0 && c == n - 1) {
-            const double* a = t < ts ? A + (size_t)t * n : P.Aw + (size_t)(t - ts) * n;
+            const double* a = t >= t1 ? A + (size_t)(t - t1) * n : P.Aw + (size_t)t * n;
             P.d[n - 1] = a[n - 1];
             P.tau[n - 1] = 0.0;
         }
@@ -865,16 +894,34 @@ void run_sytrd(const double* G, int n, int64_t strideG, int batch, double* V, do
     const bool gmem = !no_gmem && t.per_wave < batch && trd_plan_gmem(n, batch).nblk >= 1;
     if (gmem) t = trd_plan_gmem(n, batch);
     const int nblk = t.nblk, cpc = t.cpc;
-    // hybrid: as many slots in shared memory as fit, the rest in L2
-    // (a hybrid with part of the slots in shared memory measured slower at
-    // cfg3: 9.1 ms a step against 8.4 with every slot in L2, warps unevenly
-    // loaded between the two kinds of slots)
-    const int cps = gmem ? 0 : cpc;
+    // hybrid (off by default, PPC_TRD_HYBRID_KB = shared memory for the slots):
+    // the last cps slots of every CTA (its highest columns, which stay in the
+    // trailing matrix longest) in shared memory, the rest in L2. Measured at
+    // cfg3 with 40% of the slots in shared memory: no faster than everything in
+    // L2 (8.0-8.2 ms a step either way). The update pass moves every trailing
+    // element through the SM's load/store path once in and once out wherever
+    // it lives; a per-warp clock profile (-DPPC_TRD_PROFILE) puts 55% of the
+    // kernel there, 24% in the grid barrier, 10% each in the p/w pass and
+    // the reflector.
+    static const int hyb_kb = std::getenv("PPC_TRD_HYBRID_KB") ? std::atoi(std::getenv("PPC_TRD_HYBRID_KB")) : 0;
+    int cps = cpc;
+    if (gmem) {
+        const int64_t room = (int64_t)hyb_kb * 1024 - (int64_t)trd_smem(n, 0);
+        cps = (int)std::max<int64_t>(0, std::min<int64_t>(cpc, room / ((int64_t)n * (int64_t)sizeof(double))));
+    }
     const size_t smem = trd_smem(n, cps);
     const size_t B = (size_t)batch;
     DeviceBuffer pgb(sizeof(double) * 2 * n * B), cpb(sizeof(double) * 2 * n * B), barb(sizeof(unsigned) * 32 * B);
-    DeviceBuffer aw(gmem ? sizeof(double) * B * nblk * (cpc - cps) * n : 0);
+    DeviceBuffer aw(gmem ? sizeof(double) * B * nblk * std::max(cpc - cps, 1) * n : 0);
     PPC_CUDA_CHECK(cudaMemsetAsync(barb.d(), 0, sizeof(unsigned) * 32 * B, s));
+#ifdef PPC_TRD_PROFILE
+    static const bool do_prof = std::getenv("PPC_TRD_PROFILE") != nullptr;
+#else
+    const bool do_prof = false;
+#endif
+    const size_t nprof = do_prof ? (size_t)nblk * t.per_wave * (kTrdThreads / 32) * 4 : 0;
+    DeviceBuffer prof(sizeof(long long) * nprof);
+    if (do_prof) PPC_CUDA_CHECK(cudaMemsetAsync(prof.d(), 0, sizeof(long long) * nprof, s));
     StageTimer tm("eig.tridiag", s);
     // (1024 threads for the L2-resident variant measured no faster)
     const void* kern = (const void*)sytrd_kernel<kTrdThreads>;
@@ -898,12 +945,27 @@ void run_sytrd(const double* G, int n, int64_t strideG, int batch, double* V, do
         P.cps = cps;
         P.strideG = strideG;
         P.blk = 0;
+        P.prof = prof.as<long long>();
         void* args[] = {&P};
         const int nm = std::min(t.per_wave, batch - b0);
         PPC_CUDA_CHECK(cudaLaunchCooperativeKernel(kern, dim3(nblk * nm), dim3(threads),
                                                    args, smem, s));
         count_launch();
         check_launch("sytrd");
+    }
+    if (do_prof) {
+        std::vector<long long> h(nprof);
+        PPC_CUDA_CHECK(cudaMemcpyAsync(h.data(), prof.d(), sizeof(long long) * nprof, cudaMemcpyDeviceToHost, s));
+        PPC_CUDA_CHECK(cudaStreamSynchronize(s));
+        const int nw = kTrdThreads / 32;
+        std::fprintf(stderr, "[trd profile] n=%d batch=%d nblk=%d cpc=%d cps=%d (last wave; kcycles per warp)\n", n, batch,
+                     nblk, cpc, cps);
+        for (int b = 0; b < std::min(nblk, 2); ++b)
+            for (int w = 0; w < nw; w += 5) {
+                const long long* q = h.data() + ((size_t)b * nw + w) * 4;
+                std::fprintf(stderr, "  cta %d warp %2d: barrier %7.0f  p/w %7.0f  reflector %7.0f  update %7.0f\n", b, w,
+                             q[0] * 1e-3, q[1] * 1e-3, q[2] * 1e-3, q[3] * 1e-3);
+            }
     }
 }
 
