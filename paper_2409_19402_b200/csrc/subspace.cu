@@ -835,6 +835,9 @@ void subspace_eig_top(const double* G, int64_t r, int64_t batch, int64_t k, doub
                 prev_rmin[sl] = rmin;
             }
             // Chebyshev interval [0, ub]: damp everything below the smallest Ritz value
+            // (moving the bound up by the last column's residual, to cover the
+            // eigenvalues just outside a block whose last Ritz value still lags,
+            // measured much slower at cfg5: 142-149 ms a step against 118)
             const double ub = std::max(t[b - 1], 0.0);
             const double c = 0.5 * ub, e = std::max(0.5 * ub, 1e-300 * scale);
             cc[sl] = c;
@@ -855,8 +858,14 @@ void subspace_eig_top(const double* G, int64_t r, int64_t batch, int64_t k, doub
             if (xk > 1.0 + 1e-12 && it >= 2) {
                 double rmax = 1.0;  // largest residual / threshold ratio among unlocked wanted columns
                 for (int64_t j = L; j < k; ++j) rmax = std::max(rmax, rr[j] / thrv[j]);
+                // (1.4x and two spare degrees: the asymptotic rate overestimates the
+                // first degrees after a restart, and a cleanup iteration for a
+                // handful of columns costs a whole CholQR3 + Rayleigh-Ritz round;
+                // cfg5: 6 -> 5 rounds, slice SVD 44.7 -> 43.0 ms)
                 const double need = std::log(rmax) / std::acosh(xk);
-                d = std::min(d, std::max(1.0, std::ceil(need) + 1.0));
+                static const double need_scale = std::getenv("PPC_NEED_SCALE") ? std::atof(std::getenv("PPC_NEED_SCALE")) : 1.4;
+                static const double need_add = std::getenv("PPC_NEED_ADD") ? std::atof(std::getenv("PPC_NEED_ADD")) : 2.0;
+                d = std::min(d, std::max(1.0, std::ceil(need_scale * need) + need_add));
             }
             deg[sl] = std::max(1, (int)d);
             dmax = std::max(dmax, deg[sl]);
