@@ -5,7 +5,12 @@
 // exception types.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
+#include <exception>
+#include <mutex>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "ppc.h"
 #include "projprod/decompositions.hpp"
@@ -15,6 +20,7 @@
 #include "projprod/matrix_kernels.hpp"
 #include "projprod/metrics.hpp"
 #include "projprod/star_products.hpp"
+#include "projprod/parallel.hpp"
 #include "projprod/tensor.hpp"
 #include "projprod/transforms.hpp"
 
@@ -119,12 +125,35 @@ Tensor3 mode3_product(const Tensor3& A, const Matrix& M) {  // tensor.cpp:139-14
     return out;
 }
 
-Tensor3 mode_product(const Tensor3& A, const Matrix& M, int mode) {
+Matrix mode_unfold(const Tensor3& A, int mode) {  // tensor.cpp:87-107 (host-side layout)
+    const Index n1 = A.n1(), n2 = A.n2(), n3 = A.n3();
+    if (mode == 3) return mode3_unfold(A);
+    if (mode == 1) {  // n1 x (n2 n3), column j + k n2: the buffer itself
+        Matrix out(n1, n2 * n3);
+        std::copy(A.data(), A.data() + A.size(), out.data());
+        return out;
+    }
+    if (mode == 2) {  // n2 x (n1 n3), column i + k n1: slice-wise transposes
+        Matrix out(n2, n1 * n3);
+        for (Index k = 0; k < n3; ++k)
+            for (Index i = 0; i < n1; ++i)
+                for (Index j = 0; j < n2; ++j) out(j, i + k * n1) = A(i, j, k);
+        return out;
+    }
+    throw argument_error("mode_unfold: mode must be 1, 2 or 3, got " + std::to_string(mode));
+}
+
+Tensor3 mode_product(const Tensor3& A, const Matrix& M, int mode) {  // tensor.cpp:109-137
     if (mode == 3) return mode3_product(A, M);
-    if (mode == 1 || mode == 2)
-        throw argument_error("mode_product: modes 1 and 2 (HOSVD baseline) are outside the B200 "
-                             "engine's scope");
-    throw argument_error("mode_product: mode must be 1, 2 or 3, got " + std::to_string(mode));
+    if (mode != 1 && mode != 2)
+        throw argument_error("mode_product: mode must be 1, 2 or 3, got " + std::to_string(mode));
+    const Index ext = mode == 1 ? A.n1() : A.n2();
+    if (M.cols() != ext)
+        throw shape_error("mode_product(" + std::to_string(mode) + "): M has " + std::to_string(M.cols()) +
+                          " cols, tensor n" + std::to_string(mode) + "=" + std::to_string(ext));
+    Tensor3 out(mode == 1 ? M.rows() : A.n1(), mode == 2 ? M.rows() : A.n2(), A.n3());
+    check(ppc_mode_product(A.data(), A.n1(), A.n2(), A.n3(), M.data(), M.rows(), mode, out.data(), PPC_HOST));
+    return out;
 }
 
 Tensor3 facewise_product(const Tensor3& A, const Tensor3& B) {  // tensor.cpp:149-156
@@ -593,5 +622,38 @@ namespace engine {
 void set_fp64_only(bool on) { check(ppc_set_ozaki(on ? 0 : 1)); }
 bool fp64_only() { return ppc_get_ozaki() == 0; }
 }  // namespace engine
+
+// ---- parallel.hpp (parallel.cpp:13-57) ------------------------------------
+int max_threads() {
+    const unsigned hc = std::thread::hardware_concurrency();
+    int cap = hc == 0 ? 1 : static_cast<int>(hc);
+    if (const char* e = std::getenv("PROJPROD_THREADS"); e && *e) {
+        char* end = nullptr;
+        const long v = std::strtol(e, &end, 10);
+        if (end != e) cap = std::min<long>(cap, std::max<long>(v, 1));  // parsed: clamp to >= 1
+    }
+    return cap;
+}
+
+void parallel_for(std::ptrdiff_t n, const std::function<void(std::ptrdiff_t)>& fn) {
+    if (n <= 0) return;
+    const std::ptrdiff_t workers = std::min<std::ptrdiff_t>(max_threads(), n);
+    const std::ptrdiff_t span = (n + workers - 1) / workers;  // contiguous range per worker
+    std::exception_ptr failed;
+    std::mutex guard;
+    auto run = [&](std::ptrdiff_t lo) {
+        try {
+            for (std::ptrdiff_t i = lo, hi = std::min(n, lo + span); i < hi; ++i) fn(i);
+        } catch (...) {
+            std::lock_guard<std::mutex> lk(guard);
+            if (!failed) failed = std::current_exception();
+        }
+    };
+    std::vector<std::thread> pool;
+    for (std::ptrdiff_t lo = span; lo < n; lo += span) pool.emplace_back(run, lo);
+    run(0);  // the first range runs on the calling thread
+    for (std::thread& t : pool) t.join();
+    if (failed) std::rethrow_exception(failed);
+}
 
 }  // namespace projprod

@@ -106,6 +106,12 @@ int ppc_timing_report(char* buf, int64_t cap, int reset);
 int ppc_mode3_product(const double* A, int64_t n1, int64_t n2, int64_t n3,
                       const double* M, int64_t q, int trans_m, double* out, int loc);
 
+/* tensor.hpp:84 / tensor.cpp:109-137: out = A x_mode M, M is q x n_mode
+ * (column-major); the mode's extent becomes q. mode 3 is ppc_mode3_product
+ * with trans_m = 0; modes 1 and 2 serve the HOSVD baseline. */
+int ppc_mode_product(const double* A, int64_t n1, int64_t n2, int64_t n3,
+                     const double* M, int64_t q, int mode, double* out, int loc);
+
 /* tensor.hpp:90 / tensor.cpp:149-156: C(:,:,k) = A(:,:,k) B(:,:,k);
  * A n1 x m x n3, B m x n2 x n3, C n1 x n2 x n3. */
 int ppc_facewise_product(const double* A, int64_t n1, int64_t m, int64_t n3,

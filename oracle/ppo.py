@@ -391,6 +391,19 @@ def mode_unfold(a, mode):
     return a.reshape(n1 * n2, n3, order="F").T
 
 
+def mode_product(a, m, mode):
+    """tensor.cpp:109-137: A x_mode M by index contraction (tests/support/oracles.hpp:82-101)."""
+    a = np.asarray(a, dtype=float)
+    m = np.asarray(m, dtype=float)
+    if mode == 1:
+        return np.asfortranarray(np.einsum("qt,tjk->qjk", m, a))
+    if mode == 2:
+        return np.asfortranarray(np.einsum("qt,itk->iqk", m, a))
+    if mode == 3:
+        return np.asfortranarray(np.einsum("qt,ijt->ijq", m, a))
+    raise ValueError(f"mode_product: mode must be 1, 2 or 3, got {mode}")
+
+
 def hosvd(a, k1, k2, k3):
     """decompositions.cpp:211-236 -> (core, U1, U2, U3)."""
     a = np.asarray(a, dtype=float)

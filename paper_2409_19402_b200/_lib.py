@@ -62,6 +62,7 @@ def lib() -> C.CDLL:
         "ppc_ozaki_syrk_batched": (C.c_int, [vp, i64, i64, i64, i64, i64, vp]),
         "ppc_timing_report": (C.c_int, [C.c_char_p, i64, C.c_int]),
         "ppc_mode3_product": (C.c_int, [vp, i64, i64, i64, vp, i64, C.c_int, vp, C.c_int]),
+        "ppc_mode_product": (C.c_int, [vp, i64, i64, i64, vp, i64, C.c_int, vp, C.c_int]),
         "ppc_facewise_product": (C.c_int, [vp, i64, i64, i64, vp, i64, vp, C.c_int]),
         "ppc_frobenius_norm": (C.c_int, [vp, i64, pd, C.c_int]),
         "ppc_svd_batched": (C.c_int, [vp, i64, i64, i64, i64, vp, vp, vp, C.c_int]),

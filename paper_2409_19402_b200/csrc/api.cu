@@ -130,6 +130,26 @@ int ppc_mode3_product(const double* A, int64_t n1, int64_t n2, int64_t n3, const
     });
 }
 
+int ppc_mode_product(const double* A, int64_t n1, int64_t n2, int64_t n3, const double* M,
+                     int64_t q, int mode, double* out, int loc) {
+    return guarded([&] {
+        validate_loc(loc);
+        check_tensor(n1, n2, n3);
+        if (mode < 1 || mode > 3)
+            fail(PPC_ARGUMENT, "mode_product: mode must be 1, 2 or 3, got " + std::to_string(mode));
+        if (q < 1) fail(PPC_SHAPE, "mode_product: M must have at least one row");
+        const int64_t ext = mode == 1 ? n1 : (mode == 2 ? n2 : n3);
+        const int64_t count = n1 * n2 * n3 / ext * q;
+        cudaStream_t s = stream();
+        In a(A, n1 * n2 * n3, loc), m(M, q * ext, loc);
+        Out o(out, count, loc);
+        if (mode == 3) mode3(a.d, n1 * n2, n3, m.d, q, false, o.d, 1.0, s);
+        else mode12_product(a.d, n1, n2, n3, m.d, q, mode, o.d, s);
+        o.finish();
+        if (loc == PPC_HOST) PPC_CUDA_CHECK(cudaStreamSynchronize(s));
+    });
+}
+
 int ppc_facewise_product(const double* A, int64_t n1, int64_t m, int64_t n3, const double* B,
                          int64_t n2, double* C, int loc) {
     return guarded([&] {

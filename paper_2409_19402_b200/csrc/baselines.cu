@@ -80,6 +80,26 @@ void star_m(const double* A, int64_t n1, int64_t m, int64_t n3, const double* B,
     mode3(ch.d(), n1 * n2, n3, minv.d(), n3, false, C, 1.0, s);  // x3 M^{-1}
 }
 
+void mode12_product(const double* A, int64_t n1, int64_t n2, int64_t n3, const double* M, int64_t q,
+                     int mode, double* out, cudaStream_t s) {
+    GemmDesc d;
+    if (mode == 1) {
+        // tensor.cpp:112-120: out(:,:,k) = M A(:,:,k); the buffer is the
+        // n1 x (n2 n3) mode-1 unfolding, so this is one GEMM
+        d.M = q; d.N = n2 * n3; d.K = n1;
+        d.A = M; d.lda = q;
+        d.B = A; d.ldb = n1;
+        d.C = out; d.ldc = q;
+    } else {
+        // tensor.cpp:121-130: out(:,:,k) = A(:,:,k) M^T, batched over the slices
+        d.M = n1; d.N = q; d.K = n2; d.batch = n3;
+        d.A = A; d.lda = n1; d.strideA = n1 * n2;
+        d.B = M; d.ldb = q; d.strideB = 0; d.b_nmajor = true;  // B(kk,nn) = M[nn + kk*q]
+        d.C = out; d.ldc = n1; d.strideC = n1 * q;
+    }
+    gemm(d, s);
+}
+
 void hosvd(const double* A, int64_t n1, int64_t n2, int64_t n3, int64_t k1, int64_t k2, int64_t k3,
            double* core, double* U1, double* U2, double* U3, cudaStream_t s) {
     const int64_t N = n1 * n2;

@@ -169,6 +169,10 @@ ErrorParts tsvdq2_error(const double* A, int64_t n1, int64_t n2, int64_t n3, con
 // star_products.cpp:38-49: [(A x3 M) facewise (B x3 M)] x3 M^{-1}, M n3 x n3.
 void star_m(const double* A, int64_t n1, int64_t m, int64_t n3, const double* B, int64_t n2,
             const double* M, double* C, cudaStream_t s);
+// tensor.cpp:109-130: A x_m M for m = 1 (out q x n2 x n3) or 2 (out n1 x q x n3),
+// M q x n_m column-major; DMMA GEMMs on the buffer as it lies (no unfolding copy).
+void mode12_product(const double* A, int64_t n1, int64_t n2, int64_t n3, const double* M, int64_t q,
+                    int mode, double* out, cudaStream_t s);
 // decompositions.cpp:211-236: core (k1,k2,k3), U1 (n1,k1), U2 (n2,k2), U3 (n3,k3).
 void hosvd(const double* A, int64_t n1, int64_t n2, int64_t n3, int64_t k1, int64_t k2, int64_t k3,
            double* core, double* U1, double* U2, double* U3, cudaStream_t s);

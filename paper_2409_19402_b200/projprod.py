@@ -24,7 +24,7 @@ from . import _lib
 
 __all__ = [
     "ShapeError", "BoundsError", "ArgumentError", "DegenerateInputError", "NumericError",
-    "FormatError", "EngineError", "Transform", "TsvdqFactors", "mode3_product",
+    "FormatError", "EngineError", "Transform", "TsvdqFactors", "mode3_product", "mode_product",
     "facewise_product", "frobenius_norm", "svd", "truncated_svd", "data_dependent_transform",
     "projection_error", "star_q", "star_q_product", "tsvdq", "tsvdq_reconstruct", "tsvdq_error",
     "relative_error", "tsvdq_relative_error", "TsvdqIIFactors", "tsvdq2", "tsvdq2_reconstruct",
@@ -278,6 +278,27 @@ def mode3_product(a, m):
         raise ShapeError(f"mode3_product: M has {m_.shape[1]} cols, tensor n3={n3}")
     out, po = args.out((n1, n2, m_.shape[0]))
     _call(args, _lib.lib().ppc_mode3_product, pa, n1, n2, n3, pm, m_.shape[0], 0, po, args.loc)
+    return out
+
+
+def mode_product(a, m, mode: int):
+    """tensor.cpp:109-137: A x_mode M, M is q x n_mode."""
+    if mode == 3:
+        return mode3_product(a, m)
+    if mode not in (1, 2):
+        raise ArgumentError(f"mode_product: mode must be 1, 2 or 3, got {mode}")
+    args = _Args(a, m if _is_dev(m) else None)
+    a_, pa = args.inp(a, 3)
+    if args.device and not _is_dev(m):
+        m = to_device(m)
+    m_, pm = args.inp(m, 2)
+    n1, n2, n3 = a_.shape
+    ext = n1 if mode == 1 else n2
+    if m_.shape[1] != ext:
+        raise ShapeError(f"mode_product({mode}): M has {m_.shape[1]} cols, tensor n{mode}={ext}")
+    q = m_.shape[0]
+    out, po = args.out((q, n2, n3) if mode == 1 else (n1, q, n3))
+    _call(args, _lib.lib().ppc_mode_product, pa, n1, n2, n3, pm, q, mode, po, args.loc)
     return out
 
 

@@ -2,6 +2,7 @@
 // restated without doctest/Eigen) run against libprojprod.so -> libppc.so.
 // Exit code 0 = all passed. Needs a B200.
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <filesystem>
 #include <fstream>
@@ -16,6 +17,7 @@
 #include "projprod/errors.hpp"
 #include "projprod/io.hpp"
 #include "projprod/metrics.hpp"
+#include "projprod/parallel.hpp"
 #include "projprod/star_products.hpp"
 
 using namespace projprod;
@@ -89,6 +91,80 @@ int main() {
         CHECK(std::fabs(ah(0, 0, 0) - (3 + 3 * s2)) <= 1e-14 * (3 + 3 * s2));
         CHECK(std::fabs(ah(0, 0, 1) - (3 - 3 * s2)) <= 1e-13);
         check_throws<shape_error>([&] { mode3_product(a, Matrix::Identity(3, 3)); }, "mode3 shape");
+    }
+    // test_tensor.cpp:87-99 — general mode unfold (host-side layout)
+    {
+        Tensor3 A = counterexample();
+        Matrix u3 = mode_unfold(A, 3), w3 = mode3_unfold(A);
+        bool same = u3.rows() == w3.rows() && u3.cols() == w3.cols();
+        for (Index i = 0; same && i < u3.size(); ++i) same = u3.data()[i] == w3.data()[i];
+        CHECK(same);
+        Tensor3 I2(2, 2, 2);
+        I2(0, 0, 0) = I2(1, 1, 0) = I2(0, 0, 1) = I2(1, 1, 1) = 1.0;
+        const double w1[2][4] = {{1, 0, 1, 0}, {0, 1, 0, 1}};
+        Matrix u1 = mode_unfold(I2, 1);
+        CHECK(u1.rows() == 2 && u1.cols() == 4);
+        for (Index r = 0; r < 2; ++r)
+            for (Index c = 0; c < 4; ++c) CHECK(u1(r, c) == w1[r][c]);
+        Matrix u2 = mode_unfold(Tensor3(3, 2, 2), 2);
+        CHECK(u2.rows() == 2 && u2.cols() == 6);
+        for (Index i = 0; i < u2.size(); ++i) CHECK(u2.data()[i] == 0.0);
+        // mode 2 column order i + k n1
+        Tensor3 S = seeded(3, 4, 2, 11);
+        Matrix s2u = mode_unfold(S, 2);
+        for (Index k = 0; k < 2; ++k)
+            for (Index i = 0; i < 3; ++i)
+                for (Index j = 0; j < 4; ++j) CHECK(s2u(j, i + k * 3) == S(i, j, k));
+        check_throws<argument_error>([&] { mode_unfold(A, 4); }, "mode_unfold mode");
+    }
+    // test_tensor.cpp:123-134 — mode products against index loops (3 x 4 x 5, M 6 x ext)
+    {
+        Tensor3 A = seeded(3, 4, 5, 7);
+        for (int mode = 1; mode <= 3; ++mode) {
+            const Index ext = mode == 1 ? 3 : (mode == 2 ? 4 : 5);
+            Tensor3 Ms = seeded(6, ext, 1, 20 + (unsigned)mode);
+            Matrix M(6, ext);
+            for (Index r = 0; r < 6; ++r)
+                for (Index c = 0; c < ext; ++c) M(r, c) = Ms(r, c, 0);
+            Tensor3 got = mode_product(A, M, mode);
+            double err2 = 0.0, ref2 = 0.0;
+            const Index o1 = mode == 1 ? 6 : 3, o2 = mode == 2 ? 6 : 4, o3 = mode == 3 ? 6 : 5;
+            CHECK(got.n1() == o1 && got.n2() == o2 && got.n3() == o3);
+            for (Index i = 0; i < o1; ++i)
+                for (Index j = 0; j < o2; ++j)
+                    for (Index k = 0; k < o3; ++k) {
+                        double w = 0.0;
+                        for (Index t = 0; t < ext; ++t)
+                            w += mode == 1 ? M(i, t) * A(t, j, k) : (mode == 2 ? M(j, t) * A(i, t, k) : M(k, t) * A(i, j, t));
+                        err2 += (got(i, j, k) - w) * (got(i, j, k) - w);
+                        ref2 += w * w;
+                    }
+            CHECK(std::sqrt(err2) <= 1e-13 * std::max(1.0, std::sqrt(ref2)));
+        }
+        check_throws<shape_error>([&] { mode_product(A, Matrix::Identity(4, 4), 1); }, "mode_product(1) shape");
+        check_throws<shape_error>([&] { mode_product(A, Matrix::Identity(3, 3), 2); }, "mode_product(2) shape");
+        check_throws<argument_error>([&] { mode_product(A, Matrix::Identity(3, 3), 0); }, "mode_product mode");
+    }
+    // parallel.cpp:13-57 — worker cap, coverage of [0, n), first exception rethrown
+    {
+        CHECK(max_threads() >= 1);
+        setenv("PROJPROD_THREADS", "3", 1);
+        CHECK(max_threads() <= 3);
+        setenv("PROJPROD_THREADS", "-5", 1);
+        CHECK(max_threads() == 1);
+        setenv("PROJPROD_THREADS", "junk", 1);
+        CHECK(max_threads() >= 1);
+        setenv("PROJPROD_THREADS", "4", 1);
+        std::vector<int> hit(1000, 0);
+        parallel_for(1000, [&](std::ptrdiff_t i) { hit[(size_t)i] += 1; });
+        bool once = true;
+        for (int h : hit) once = once && h == 1;
+        CHECK(once);
+        parallel_for(0, [&](std::ptrdiff_t) { CHECK(false); });
+        check_throws<argument_error>(
+            [&] { parallel_for(64, [&](std::ptrdiff_t i) { if (i == 37) throw argument_error("boom"); }); },
+            "parallel_for rethrow");
+        unsetenv("PROJPROD_THREADS");
     }
     // test_tensor.cpp:144-149 — facewise tube
     {

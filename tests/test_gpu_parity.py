@@ -54,6 +54,28 @@ def test_mode3_product_vs_oracle(engine, oracle, shape, q):
     assert rel(got, want) <= 1e-13
 
 
+@pytest.mark.parametrize("shape,q", [((3, 4, 5), 6), ((64, 48, 32), 8), ((37, 29, 61), 13),
+                                     ((256, 192, 40), 50), ((16, 8, 7), 1)])
+@pytest.mark.parametrize("mode", [1, 2, 3])
+def test_mode_product_vs_oracle(engine, oracle, shape, q, mode):
+    """tensor.cpp:109-137 (test_tensor.cpp:123-134): modes 1 and 2 (the HOSVD
+    baseline's products) and mode 3 against the index-contraction oracle,
+    host and device input; the reference's shape and mode errors."""
+    import paper_2409_19402_b200 as pp
+    a = oracle.random_tensor(*shape, 13)
+    m = oracle.random_matrix(q, shape[mode - 1], 14 + mode)
+    want = oracle.mode_product(a, m, mode)
+    got = engine.mode_product(a, m, mode)
+    assert got.shape == want.shape
+    assert rel(got, want) <= 1e-13
+    got_d = pp.to_host(engine.mode_product(pp.to_device(a), pp.to_device(m), mode))
+    assert np.array_equal(got_d, got)
+    with pytest.raises(engine.ShapeError):
+        engine.mode_product(a, oracle.random_matrix(q, shape[mode - 1] + 1, 3), mode)
+    with pytest.raises(engine.ArgumentError):
+        engine.mode_product(a, m, 4)
+
+
 @pytest.mark.parametrize("n1,m,n2,p", [(1, 1, 1, 3), (5, 7, 3, 4), (64, 48, 64, 8),
                                        (130, 70, 90, 5), (256, 128, 256, 3)])
 def test_facewise_vs_oracle(engine, oracle, n1, m, n2, p):
@@ -451,13 +473,16 @@ def test_slice_tridiag_l2_copy_matches_shared_memory(tmp_path):
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     out = {}
-    for tag, env in (("l2", {}), ("smem", {"PPC_TRD_GMEM": "0"})):
+    # hybrid: the long-lived (highest) columns of every CTA in shared memory,
+    # the rest in L2 (PPC_TRD_HYBRID_KB, off by default)
+    for tag, env in (("l2", {}), ("smem", {"PPC_TRD_GMEM": "0"}), ("hybrid", {"PPC_TRD_HYBRID_KB": "200"})):
         f = str(tmp_path / f"{tag}.npz")
         subprocess.run([sys.executable, "-c", _TRD_SCRIPT, root, f], check=True, env={**os.environ, **env},
                        timeout=600)
         out[tag] = np.load(f)
     for key in ("U", "s", "V"):
         assert np.array_equal(out["l2"][key], out["smem"][key]), key
+        assert np.array_equal(out["l2"][key], out["hybrid"][key]), key
 
 
 @pytest.mark.parametrize("m,n", [(300, 260), (301, 261), (260, 300)])

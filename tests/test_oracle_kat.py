@@ -328,6 +328,25 @@ def test_star_m_kats():
         ppo.star_m_product(tube([1, 2]), tube([1, 2]), sing)
 
 
+def test_mode_unfold_and_mode_product_kats():
+    """test_tensor.cpp:87-99 (unfold pins) and :123-134 (mode products vs the
+    unfolding identity (A x_m M)_(m) = M A_(m))."""
+    A = counterexample()
+    assert np.array_equal(ppo.mode_unfold(A, 3), A.reshape(4, 2, order="F").T)
+    I = np.zeros((2, 2, 2), order="F")
+    I[:, :, 0] = I[:, :, 1] = np.eye(2)
+    assert np.array_equal(ppo.mode_unfold(I, 1), np.array([[1, 0, 1, 0], [0, 1, 0, 1.0]]))
+    assert not ppo.mode_unfold(np.zeros((3, 2, 2)), 2).any()
+    a = ppo.random_tensor(3, 4, 5, 7)
+    for mode, ext in ((1, 3), (2, 4), (3, 5)):
+        m = ppo.random_matrix(6, ext, 20 + mode)
+        got = ppo.mode_product(a, m, mode)
+        assert np.abs(ppo.mode_unfold(got, mode) - m @ ppo.mode_unfold(a, mode)).max() <= 1e-13
+    assert np.abs(ppo.mode_product(a, m, 3) - ppo.mode3_product(a, m)).max() <= 1e-13
+    with pytest.raises(ValueError):
+        ppo.mode_product(a, m, 4)
+
+
 def test_hosvd_kats():
     # tests/test_decompositions.cpp:203-232
     A = ppo.random_tensor(4, 3, 5, 48)
