@@ -24,7 +24,8 @@ from . import _lib
 
 __all__ = [
     "ShapeError", "BoundsError", "ArgumentError", "DegenerateInputError", "NumericError",
-    "FormatError", "EngineError", "Transform", "TsvdqFactors", "mode3_product", "mode_product",
+    "FormatError", "EngineError", "Transform", "TsvdqFactors", "mode3_product", "mode_product", "star_q_transpose", "star_q_identity",
+    "star_q_rank",
     "facewise_product", "frobenius_norm", "svd", "truncated_svd", "data_dependent_transform",
     "projection_error", "star_q", "star_q_product", "tsvdq", "tsvdq_reconstruct", "tsvdq_error",
     "relative_error", "tsvdq_relative_error", "TsvdqIIFactors", "tsvdq2", "tsvdq2_reconstruct",
@@ -388,6 +389,58 @@ def star_q_product(a, b, t):
 
 
 star_q = star_q_product
+
+
+def _host_q(t):
+    q = t.q if isinstance(t, Transform) else t
+    return to_host(q) if _is_dev(q) else np.asfortranarray(q, dtype=np.float64)
+
+
+def star_q_transpose(a, t):
+    """star_products.cpp:74-85 (bindings.cpp:165-170): transform, transpose
+    every slice, transform back. Both mode-3 products run on the GPU."""
+    q = _host_q(t)
+    a_h = to_host(a) if _is_dev(a) else np.asfortranarray(a, dtype=np.float64)
+    if a_h.ndim != 3 or a_h.shape[2] != q.shape[0]:
+        raise ShapeError(f"star_q_transpose: mode-3 extent {a_h.shape[2] if a_h.ndim == 3 else '?'} "
+                         f"!= transform length {q.shape[0]}")
+    ahat = mode3_product(a_h, np.asfortranarray(q.T))
+    return mode3_product(np.asfortranarray(ahat.transpose(1, 0, 2)), q)
+
+
+def star_q_identity(m: int, t):
+    """star_products.cpp:61-72 (bindings.cpp:171-176): the m x m x n3 tensor
+    whose transform-domain slices are identities, divided by the scale."""
+    if m < 1:
+        raise ArgumentError("star_q_identity: m must be positive")
+    q = _host_q(t)
+    ihat = np.zeros((m, m, q.shape[1]), order="F")
+    ihat[np.arange(m), np.arange(m), :] = 1.0
+    out = mode3_product(ihat, q)
+    scale = t.scale if isinstance(t, Transform) else 1.0
+    return out if scale == 1.0 else np.asfortranarray(out / scale)
+
+
+def star_q_rank(a, t, tol_rel: float = 1e-12) -> int:
+    """decompositions.cpp:105-114 (bindings.cpp:177-182): the largest numerical
+    rank (matrix_kernels.cpp:93-101, s_j > tol_rel * s_0) over the slices of
+    A x3 Q^T; the slice SVDs are one batched GPU call."""
+    q = _host_q(t)
+    a_h = to_host(a) if _is_dev(a) else np.asfortranarray(a, dtype=np.float64)
+    if a_h.ndim != 3 or a_h.shape[2] != q.shape[0]:
+        raise ShapeError(f"star_q_rank: transform length {q.shape[0]} != tensor n3 "
+                         f"{a_h.shape[2] if a_h.ndim == 3 else '?'}")
+    ahat = mode3_product(a_h, np.asfortranarray(q.T))
+    _, s, _ = svd(ahat)
+    s = np.asarray(s).reshape(min(a_h.shape[0], a_h.shape[1]), -1)
+    rank = 0
+    for i in range(s.shape[1]):
+        col = s[:, i]
+        r = 0
+        while r < col.size and col[r] > tol_rel * col[0]:
+            r += 1
+        rank = max(rank, r)
+    return rank
 
 
 def star_m_product(a, b, m):

@@ -76,6 +76,40 @@ def test_mode_product_vs_oracle(engine, oracle, shape, q, mode):
         engine.mode_product(a, m, 4)
 
 
+def test_star_q_identity_transpose_rank_reference_cases(engine, oracle):
+    """test_star_products.cpp:103-149, test_decompositions.cpp:118-124 and
+    tests/python/test_smoke.py:24-44,77-78 through the Python mirror."""
+    pp = engine
+    a, t = tube([2, 4, 6, 8]), pp.Transform("haar", 4, 2)
+    ia = pp.star_q(pp.star_q_identity(1, t), a, t)
+    assert np.abs(ia.ravel() - [3, 3, 6, 0]).max() <= 1e-12
+    # full transform: a true identity
+    A = oracle.random_tensor(3, 4, 4, 9)
+    full = pp.Transform("dct", 4, 4)
+    assert rel(pp.star_q(pp.star_q_identity(3, full), A, full), A) <= 1e-12
+    with pytest.raises(pp.ArgumentError):
+        pp.star_q_identity(0, t)
+    # transpose rules: (A * B)^T = B^T * A^T; double transpose = the projected part
+    A = oracle.random_tensor(3, 2, 5, 10)
+    B = oracle.random_tensor(2, 4, 5, 11)
+    ctx = pp.Transform("random", 5, 3, seed=13)
+    lhs = pp.star_q_transpose(pp.star_q(A, B, ctx), ctx)
+    rhs = pp.star_q(pp.star_q_transpose(B, ctx), pp.star_q_transpose(A, ctx), ctx)
+    assert lhs.shape == (4, 3, 5)
+    assert rel(lhs, rhs) <= 1e-12
+    twice = pp.star_q_transpose(pp.star_q_transpose(A, ctx), ctx)
+    P = ctx.q @ ctx.q.T
+    assert np.linalg.norm(twice - oracle.mode3_product(A, P)) <= 1e-12 * np.linalg.norm(A)
+    assert np.linalg.norm(pp.star_q_transpose(np.zeros((2, 3, 5), order="F"), ctx)) == 0.0
+    with pytest.raises(pp.ShapeError):
+        pp.star_q_transpose(np.zeros((2, 3, 4), order="F"), ctx)
+    # star_q_rank
+    ce = counterexample()
+    assert pp.star_q_rank(ce, pp.Transform("identity", 2, 2)) == 2
+    assert pp.star_q_rank(ce, pp.Transform("haar", 2, 1)) == 1
+    assert pp.star_q_rank(np.zeros((3, 3, 4), order="F"), pp.Transform("dct", 4, 2)) == 0
+
+
 @pytest.mark.parametrize("n1,m,n2,p", [(1, 1, 1, 3), (5, 7, 3, 4), (64, 48, 64, 8),
                                        (130, 70, 90, 5), (256, 128, 256, 3)])
 def test_facewise_vs_oracle(engine, oracle, n1, m, n2, p):
