@@ -246,9 +246,17 @@ namespace {
 // Fused residual GEMM: {sum (X - alpha op(A)op(B))^2, sum X^2} as host doubles.
 std::array<double, 2> residual_sums(const GemmDesc& d, const double* X, int64_t ldx,
                                     int64_t strideX, cudaStream_t s) {
-    const int64_t ctas = gemm_residual_ctas(d, X, ldx, strideX);
+    // a tall product with a short inner dimension (the residual through Q at
+    // small p): streamed, one row per thread (kernels.cu smallk_residual)
+    static const bool no_smallk = std::getenv("PPC_NO_SMALLK") != nullptr;
+    const bool smallk = !no_smallk && d.batch == 1 && d.K >= 1 && d.K <= 32 && d.M >= 4096 && !d.a_kmajor &&
+                        d.b_nmajor && d.alpha == 1.0;
+    const int64_t ctas = smallk ? smallk_residual_ctas(d.M, d.N) : gemm_residual_ctas(d, X, ldx, strideX);
     DeviceBuffer part(sizeof(double) * 2 * (ctas + 1));
-    gemm_residual(d, X, ldx, strideX, part.d(), s);
+    if (smallk)
+        launch_smallk_residual(d.A, d.lda, d.B, d.ldb, X, ldx, d.M, d.N, d.K, part.d(), s);
+    else
+        gemm_residual(d, X, ldx, strideX, part.d(), s);
     double* fin = part.d() + 2 * ctas;
     launch_reduce_pairs(part.d(), ctas, fin, s);
     std::array<double, 2> out{};

@@ -147,7 +147,87 @@ unsigned grid_for(int64_t n, int threads) {
     return (unsigned)g;
 }
 
+// Residual sums of a tall product with a short inner dimension:
+// {sum (X - C B)^2, sum X^2} for C (M x K, column-major, lda), B(k, n) =
+// Bq[n + k * ldb] and X (M x Nn, ldx), K <= KMAX. One thread per row: its K
+// coefficients stay in registers, a CTA's column chunk of B sits in shared
+// memory (read as broadcasts), and X streams through once, coalesced along
+// the rows. HBM-bound (the residual GEMM's 128 x 128 tiles spend their time in
+// a latency-exposed epilogue when K is 16-32: 0.3 ms at cfg2 against 0.03).
+// Fixed grid and a fixed-order block sum: deterministic.
+constexpr int kSkRows = 128;  // rows per CTA = threads
+constexpr int kSkCols = 64;   // columns per CTA
+template <int KMAX>
+__global__ void __launch_bounds__(kSkRows) smallk_residual_kernel(
+    const double* __restrict__ Cm, int64_t lda, const double* __restrict__ Bq, int64_t ldb,
+    const double* __restrict__ X, int64_t ldx, int64_t M, int64_t Nn, int K, double* __restrict__ partials) {
+    __shared__ double bs[kSkCols * KMAX];  // bs[c * K + k] = B(k, n0 + c)
+    const int64_t r = (int64_t)blockIdx.x * kSkRows + threadIdx.x;
+    const int64_t n0 = (int64_t)blockIdx.y * kSkCols;
+    const int nc = (int)(Nn - n0 < kSkCols ? Nn - n0 : kSkCols);
+    for (int t = threadIdx.x; t < nc * K; t += kSkRows) {
+        const int c = t % nc, k = t / nc;  // consecutive threads: consecutive n (coalesced)
+        bs[c * K + k] = Bq[n0 + c + (int64_t)k * ldb];
+    }
+    double cr[KMAX];
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k) cr[k] = (k < K && r < M) ? Cm[r + (int64_t)k * lda] : 0.0;
+    __syncthreads();
+    double sd = 0.0, sa = 0.0;
+    if (r < M) {
+        const double* xp = X + r + n0 * ldx;
+        constexpr int U = 8;
+        int c = 0;
+        for (; c + U <= nc; c += U) {
+            double x[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) x[u] = xp[(int64_t)(c + u) * ldx];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                double d = x[u];
+                const double* b = bs + (c + u) * K;
+#pragma unroll
+                for (int k = 0; k < KMAX; ++k)
+                    if (k < K) d = fma(-cr[k], b[k], d);
+                sd = fma(d, d, sd);
+                sa = fma(x[u], x[u], sa);
+            }
+        }
+        for (; c < nc; ++c) {
+            const double xv = xp[(int64_t)c * ldx];
+            double d = xv;
+            const double* b = bs + c * K;
+#pragma unroll
+            for (int k = 0; k < KMAX; ++k)
+                if (k < K) d = fma(-cr[k], b[k], d);
+            sd = fma(d, d, sd);
+            sa = fma(xv, xv, sa);
+        }
+    }
+    block_sum2(sd, sa);
+    if (threadIdx.x == 0) {
+        const int64_t cta = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
+        partials[2 * cta] = sd;
+        partials[2 * cta + 1] = sa;
+    }
+}
+
 }  // namespace
+
+int64_t smallk_residual_ctas(int64_t M, int64_t Nn) {
+    return ((M + kSkRows - 1) / kSkRows) * ((Nn + kSkCols - 1) / kSkCols);
+}
+
+void launch_smallk_residual(const double* Cm, int64_t lda, const double* Bq, int64_t ldb, const double* X,
+                            int64_t ldx, int64_t M, int64_t Nn, int64_t K, double* partials, cudaStream_t s) {
+    const dim3 grid((unsigned)((M + kSkRows - 1) / kSkRows), (unsigned)((Nn + kSkCols - 1) / kSkCols));
+    if (K <= 16)
+        smallk_residual_kernel<16><<<grid, kSkRows, 0, s>>>(Cm, lda, Bq, ldb, X, ldx, M, Nn, (int)K, partials);
+    else
+        smallk_residual_kernel<32><<<grid, kSkRows, 0, s>>>(Cm, lda, Bq, ldb, X, ldx, M, Nn, (int)K, partials);
+    count_launch();
+    check_launch("smallk_residual");
+}
 
 void launch_sumsq_partials(const double* a, const double* b, int64_t count, double* partials,
                            cudaStream_t s) {

@@ -18,6 +18,12 @@ void launch_sumsq_partials(const double* a, const double* b, int64_t count, doub
                            cudaStream_t s);
 // out[0..1] = fixed-order sums of the pairs in partials[0..2n).
 void launch_reduce_pairs(const double* partials, int64_t n, double* out, cudaStream_t s);
+// {sum (X - C B)^2, sum X^2} per CTA for a tall product with K <= 32:
+// C (M x K, lda), B(k, n) = Bq[n + k * ldb], X (M x Nn, ldx); 2 doubles per
+// CTA into partials (smallk_residual_ctas of them), summed by launch_reduce_pairs.
+int64_t smallk_residual_ctas(int64_t M, int64_t Nn);
+void launch_smallk_residual(const double* Cm, int64_t lda, const double* Bq, int64_t ldb, const double* X,
+                            int64_t ldx, int64_t M, int64_t Nn, int64_t K, double* partials, cudaStream_t s);
 // out(:, j, b) = U(:, j, b) * S(j, b) for a stack of `batch` rows x k blocks.
 void launch_scale_columns(const double* U, const double* S, double* out, int64_t rows,
                           int64_t k, int64_t batch, cudaStream_t s);
