@@ -298,6 +298,24 @@ def test_projection_error_kat(engine, oracle):
         oracle.projection_error(a, q), rel=1e-12)
 
 
+@pytest.mark.parametrize("shape,p", [((67, 63, 37), 1), ((67, 63, 37), 5), ((67, 63, 37), 16), ((67, 63, 37), 17),
+                                     ((128, 64, 70), 32), ((129, 65, 130), 20), ((67, 63, 37), 33)])
+def test_projection_and_tsvdq_residuals_small_p(engine, oracle, shape, p):
+    """The streamed residual kernel (K = p <= 32, tall N >= 4096; p = 33 keeps
+    the residual GEMM): projection error and the fused tSVDQ relative error
+    against numpy, with ragged row and column tails."""
+    a = oracle.random_tensor(*shape, 21)
+    t = engine.Transform("random", shape[2], p, seed=3)
+    T = a.reshape(-1, shape[2], order="F")
+    want = np.linalg.norm(T - (T @ t.q) @ t.q.T)
+    assert engine.projection_error(a, t) == pytest.approx(want, rel=1e-12)
+    k = 3
+    f = engine.tsvdq(a, t, k)
+    re = engine.tsvdq_relative_error(a, f)
+    rec = oracle.tsvdq_reconstruct(f.u, f.s, f.v, t.q)
+    assert re == pytest.approx(np.linalg.norm(a - rec) / np.linalg.norm(a), rel=1e-11)
+
+
 def test_tsvdq_error_vs_oracle_and_ey_identity(engine, oracle):
     a = oracle.random_tensor(6, 5, 7, 7)
     t = engine.Transform("dct", 7, 4)
