@@ -89,9 +89,9 @@ bool facewise_ozaki(const double* Ah, int64_t n1, int64_t m, int64_t p, const do
         ozaki_peak_ratios_async(Bd, m, n2, peaks.d() + ng, s);
     }
     std::vector<double> a_peak((size_t)ng + 1);
-    PPC_CUDA_CHECK(cudaMemcpyAsync(a_peak.data(), peaks.d(), sizeof(double) * (b_ready ? ng : ng + 1),
-                                   cudaMemcpyDeviceToHost, s));
-    PPC_CUDA_CHECK(cudaStreamSynchronize(s));
+    // (not a cudaMemcpyAsync: in the host pipeline it would wait on the copy
+    // engine for the previous block's C rows to finish their way down)
+    read_small(peaks.d(), a_peak.data(), (size_t)(b_ready ? ng : ng + 1), s);
     if (!b_ready) {
         b_peak = a_peak[ng];
         b_ready = true;
@@ -166,6 +166,17 @@ void star_q_host(const double* hA, int64_t n1, int64_t m, int64_t n3, const doub
                  const double* hQ, int64_t p, double scale, double* hC, cudaStream_t s) {
     cudaStream_t up = copy_stream(), down = copy_out_stream();
     const int64_t NB = m * n2;
+    // PPC_STARQ_TRACE: timed events on the three streams, printed at the end
+    static const bool trace = std::getenv("PPC_STARQ_TRACE") != nullptr;
+    std::vector<std::pair<std::string, cudaEvent_t>> marks;
+    auto mark = [&](const char* what, int64_t idx, cudaStream_t st) {
+        if (!trace) return;
+        cudaEvent_t e;
+        PPC_CUDA_CHECK(cudaEventCreate(&e));
+        PPC_CUDA_CHECK(cudaEventRecord(e, st));
+        marks.emplace_back(std::string(what) + " " + std::to_string(idx), e);
+    };
+    mark("start", 0, s);
     DeviceBuffer q(sizeof(double) * n3 * p), b(sizeof(double) * NB * n3), bh(sizeof(double) * NB * p);
     Event ready;
     ready.record(s);  // buffers allocated on s
@@ -182,6 +193,7 @@ void star_q_host(const double* hA, int64_t n1, int64_t m, int64_t n3, const doub
             Event landed;
             landed.record(up);
             landed.wait_on(s);
+            mark("B chunk up", r0, up);
             GemmDesc d;  // Bh rows [r0, r0+nr) = B rows x Q
             d.M = nr; d.N = p; d.K = n3;
             d.A = b.d() + r0; d.lda = NB;
@@ -215,6 +227,7 @@ void star_q_host(const double* hA, int64_t n1, int64_t m, int64_t n3, const doub
         Event landed;
         landed.record(up);
         landed.wait_on(s);
+        mark("A block up", ib, up);
         mode3(ablk[u].d(), bi * m, n3, q.d(), p, true, ahblk[u].d(), 1.0, s);  // A_blk x3 Q^T
         a_free[u].record(s);
         if (!facewise_ozaki(ahblk[u].d(), bi, m, p, bh.d(), n2, chblk[u].d(), bd, b_ready, b_peak, s))
@@ -224,9 +237,21 @@ void star_q_host(const double* hA, int64_t n1, int64_t m, int64_t n3, const doub
         Event done;
         done.record(s);
         done.wait_on(down);
+        mark("block computed", ib, s);
         PPC_CUDA_CHECK(cudaMemcpy2DAsync(hC + i0, sizeof(double) * n1, cblk[u].d(), sizeof(double) * bi,
                                          sizeof(double) * bi, n2 * n3, cudaMemcpyDeviceToHost, down));
         c_free[u].record(down);
+        mark("C block down", ib, down);
+    }
+    if (trace) {
+        PPC_CUDA_CHECK(cudaStreamSynchronize(down));
+        PPC_CUDA_CHECK(cudaStreamSynchronize(s));
+        for (size_t i = 1; i < marks.size(); ++i) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, marks[0].second, marks[i].second);
+            std::fprintf(stderr, "[starq trace] %8.2f ms  %s\n", ms, marks[i].first.c_str());
+        }
+        for (auto& mk : marks) cudaEventDestroy(mk.second);
     }
     Event all_down;
     all_down.record(down);

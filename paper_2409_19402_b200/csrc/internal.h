@@ -47,6 +47,11 @@ Context& ctx();               // ensures a device is selected (throws PPC_NO_DEV
 cudaStream_t stream();        // current stream of this thread
 cudaStream_t copy_stream();   // this thread's H2D staging stream (overlap)
 cudaStream_t copy_out_stream();  // this thread's D2H stream
+// n doubles (n <= 4096, else a plain copy) from device memory to `out`, stream
+// ordered on s and synchronized: a one-CTA kernel stores them into mapped pinned
+// memory, so the read does not queue on the D2H copy engine behind a bulk
+// download in flight on another stream (a pageable cudaMemcpyAsync does).
+void read_small(const double* dev, double* out, size_t n, cudaStream_t s);
 // This thread's persistent 4-int device status scratch on the current device
 // (finiteness flags): allocated once outside the stream-ordered pool, so a
 // tiny flag never splits the pool's cached multi-GB blocks.

@@ -98,6 +98,39 @@ cudaStream_t copy_stream() {
     return c.copy;
 }
 
+namespace {
+constexpr size_t kSmallRead = 4096;
+__global__ void read_small_kernel(const double* __restrict__ src, double* __restrict__ dst, int n) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+}
+struct MappedScratch {
+    double* h = nullptr;
+    ~MappedScratch() {
+        if (h) cudaFreeHost(h);
+    }
+};
+thread_local MappedScratch t_scratch;
+}  // namespace
+
+void read_small(const double* dev, double* out, size_t n, cudaStream_t s) {
+    if (n == 0) return;
+    if (n > kSmallRead) {
+        PPC_CUDA_CHECK(cudaMemcpyAsync(out, dev, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+        PPC_CUDA_CHECK(cudaStreamSynchronize(s));
+        return;
+    }
+    if (!t_scratch.h)
+        PPC_CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&t_scratch.h), sizeof(double) * kSmallRead,
+                                     cudaHostAllocMapped | cudaHostAllocPortable));
+    double* dptr = nullptr;
+    PPC_CUDA_CHECK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dptr), t_scratch.h, 0));
+    read_small_kernel<<<1, 256, 0, s>>>(dev, dptr, (int)n);
+    count_launch();
+    check_launch("read_small");
+    PPC_CUDA_CHECK(cudaStreamSynchronize(s));
+    std::copy(t_scratch.h, t_scratch.h + n, out);
+}
+
 void check_launch(const char* name) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) fail(PPC_CUDA, std::string(name) + " launch: " + cudaGetErrorString(e));

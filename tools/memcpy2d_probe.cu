@@ -59,5 +59,33 @@ int main() {
     CK(cudaEventSynchronize(b));
     CK(cudaEventElapsedTime(&ms, a, b));
     printf("duplex 4 x 128 MiB each way: %.2f ms  %.1f GB/s per direction\n", ms, 4 * blk / ms * 1e-6);
+    // the star-Q host pipeline's shape: 128 MiB row blocks up (1 KB rows, pitch 8 KB)
+    // while 256 MiB row blocks come down (1 KB rows, pitch 8 KB)
+    {
+        char* h2; CK(cudaMallocHost(&h2, 2ull << 30));
+        char* d3; CK(cudaMalloc(&d3, 2 * blk));
+        const size_t w = 1024, pitch = 8 * w;
+        CK(cudaDeviceSynchronize());
+        CK(cudaEventRecord(a, s));
+        CK(cudaStreamWaitEvent(s2, a, 0));
+        for (int i = 0; i < 8; ++i) {
+            CK(cudaMemcpy2DAsync(d, w, h + i * w, pitch, w, blk / w, cudaMemcpyHostToDevice, s));
+            CK(cudaMemcpy2DAsync(h2 + i * w, pitch, d3, w, w, 2 * blk / w, cudaMemcpyDeviceToHost, s2));
+        }
+        CK(cudaEventRecord(c, s2));
+        CK(cudaStreamWaitEvent(s, c, 0));
+        CK(cudaEventRecord(b, s));
+        CK(cudaEventSynchronize(b));
+        CK(cudaEventElapsedTime(&ms, a, b));
+        printf("pipeline shape: 8 x (128 MiB up + 256 MiB down), strided: %.2f ms  down %.1f GB/s\n", ms,
+               16 * blk / ms * 1e-6);
+        CK(cudaEventRecord(a, s2));
+        for (int i = 0; i < 8; ++i)
+            CK(cudaMemcpy2DAsync(h2 + i * w, pitch, d3, w, w, 2 * blk / w, cudaMemcpyDeviceToHost, s2));
+        CK(cudaEventRecord(b, s2));
+        CK(cudaEventSynchronize(b));
+        CK(cudaEventElapsedTime(&ms, a, b));
+        printf("down only, 8 x 256 MiB strided: %.2f ms  %.1f GB/s\n", ms, 16 * blk / ms * 1e-6);
+    }
     return 0;
 }
