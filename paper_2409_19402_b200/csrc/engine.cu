@@ -3,6 +3,8 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <memory>
+#include <string>
 #include <vector>
 
 #include "dmma_gemm.cuh"
@@ -164,84 +166,189 @@ struct Event {
 
 void star_q_host(const double* hA, int64_t n1, int64_t m, int64_t n3, const double* hB, int64_t n2,
                  const double* hQ, int64_t p, double scale, double* hC, cudaStream_t s) {
+    // 2-D tiling: A in blocks of kFaceRows rows, B in blocks of kFaceRows
+    // lateral columns. Tile (I, J) of C needs only A block I and B block J, so
+    // the first rows of C start their way down after two blocks have come up,
+    // not after all of B (the row-block pipeline before this: 70 ms at cfg4,
+    // of which 22 before the first download).
+    //  - every upload is enqueued at once on the H2D stream, alternating A and
+    //    B blocks, each into its own device buffer;
+    //  - a block is transformed, split into digits and gated as it lands;
+    //  - each arrival enables the tiles it completes: facewise product, inverse
+    //    transform, one 3-D copy down (D2H stream), four tile buffers rotating.
+    // Same bits as star_q on device copies: the INT8 digits of a row / column,
+    // the exact integer sums, the row-wise inverse transform and the DMMA
+    // k-order do not depend on the tiling. B-hat's gate is one value over all
+    // of B (as in star_q): tiles run on the INT8 path until a B block fails it;
+    // then every tile so far is redone on FP64 DMMA, as star_q would have.
     cudaStream_t up = copy_stream(), down = copy_out_stream();
-    const int64_t NB = m * n2;
     // PPC_STARQ_TRACE: timed events on the three streams, printed at the end
     static const bool trace = std::getenv("PPC_STARQ_TRACE") != nullptr;
     std::vector<std::pair<std::string, cudaEvent_t>> marks;
-    auto mark = [&](const char* what, int64_t idx, cudaStream_t st) {
+    auto mark = [&](const char* what, int64_t i, int64_t j, cudaStream_t st) {
         if (!trace) return;
         cudaEvent_t e;
         PPC_CUDA_CHECK(cudaEventCreate(&e));
         PPC_CUDA_CHECK(cudaEventRecord(e, st));
-        marks.emplace_back(std::string(what) + " " + std::to_string(idx), e);
+        marks.emplace_back(std::string(what) + " " + std::to_string(i) + (j >= 0 ? "," + std::to_string(j) : ""), e);
     };
-    mark("start", 0, s);
-    DeviceBuffer q(sizeof(double) * n3 * p), b(sizeof(double) * NB * n3), bh(sizeof(double) * NB * p);
+    mark("start", 0, -1, s);
+    struct Block {
+        int64_t o = 0, n = 0;         // first row / column, extent
+        DeviceBuffer raw, hat;        // the block as uploaded; its transform (compact)
+        OzakiDigits dig;
+        double peak = 0.0;
+        std::unique_ptr<Event> landed;
+    };
+    auto blocks_of = [](int64_t n, bool merge_short) {
+        std::vector<Block> v;
+        for (int64_t o = 0; o < n;) {
+            int64_t len = std::min(kFaceRows, n - o);
+            // lateral blocks: a short tail joins the last block (the INT8 product wants >= 64 columns)
+            if (merge_short && n - o < kFaceRows + 64) len = n - o;
+            v.emplace_back();
+            v.back().o = o;
+            v.back().n = len;
+            o += len;
+        }
+        return v;
+    };
+    std::vector<Block> ab = blocks_of(n1, false), bb = blocks_of(n2, true);
+    const int64_t nI = (int64_t)ab.size(), nJ = (int64_t)bb.size();
+    const bool int8_ok = ozaki_gemm_eligible(n1, m) && n2 >= 64;  // star_q's shape test
+    DeviceBuffer q(sizeof(double) * n3 * p);
+    for (Block& x : ab) {
+        x.raw = DeviceBuffer(sizeof(double) * x.n * m * n3);
+        x.hat = DeviceBuffer(sizeof(double) * x.n * m * p);
+    }
+    DeviceBuffer bh(sizeof(double) * m * n2 * p);  // B-hat whole: slice i at i * m * n2 (star_q's layout)
+    for (Block& x : bb) x.raw = DeviceBuffer(sizeof(double) * m * x.n * n3);
     Event ready;
     ready.record(s);  // buffers allocated on s
     ready.wait_on(up);
     PPC_CUDA_CHECK(cudaMemcpyAsync(q.d(), hQ, sizeof(double) * n3 * p, cudaMemcpyHostToDevice, up));
-    // 1. B in pixel chunks: H2D (up) -> forward transform of those rows (s)
-    {
-        StageTimer tm("mode3_fwd", s, 2.0 * NB * n3 * p, 8.0 * (NB * n3 + NB * p + n3 * p));
-        const int64_t nch = 4, rows = (NB + nch - 1) / nch;
-        for (int64_t r0 = 0; r0 < NB; r0 += rows) {
-            const int64_t nr = std::min(rows, NB - r0);
-            PPC_CUDA_CHECK(cudaMemcpy2DAsync(b.d() + r0, sizeof(double) * NB, hB + r0, sizeof(double) * NB,
-                                             sizeof(double) * nr, n3, cudaMemcpyHostToDevice, up));
-            Event landed;
-            landed.record(up);
-            landed.wait_on(s);
-            mark("B chunk up", r0, up);
-            GemmDesc d;  // Bh rows [r0, r0+nr) = B rows x Q
-            d.M = nr; d.N = p; d.K = n3;
-            d.A = b.d() + r0; d.lda = NB;
-            d.B = q.d(); d.ldb = n3;
-            d.C = bh.d() + r0; d.ldc = NB;
-            gemm(d, s);
+    // 1. every upload, alternating A and B blocks
+    for (int64_t t = 0; t < std::max(nI, nJ); ++t) {
+        if (t < nI) {
+            Block& x = ab[(size_t)t];  // rows [o, o+n) of every lateral slice: n x (m n3), compact
+            PPC_CUDA_CHECK(cudaMemcpy2DAsync(x.raw.d(), sizeof(double) * x.n, hA + x.o, sizeof(double) * n1,
+                                             sizeof(double) * x.n, m * n3, cudaMemcpyHostToDevice, up));
+            x.landed = std::make_unique<Event>();
+            x.landed->record(up);
+            mark("A block up", t, -1, up);
+        }
+        if (t < nJ) {
+            Block& x = bb[(size_t)t];  // columns [o, o+n) of every frontal slice: (m n) x n3, compact
+            PPC_CUDA_CHECK(cudaMemcpy2DAsync(x.raw.d(), sizeof(double) * m * x.n, hB + x.o * m,
+                                             sizeof(double) * m * n2, sizeof(double) * m * x.n, n3,
+                                             cudaMemcpyHostToDevice, up));
+            x.landed = std::make_unique<Event>();
+            x.landed->record(up);
+            mark("B block up", t, -1, up);
         }
     }
-    b.release();
-    // 2. A row blocks: H2D (up) -> transforms + facewise (s) -> D2H (down)
-    const int64_t BI = std::min<int64_t>(n1, kFaceRows);
-    OzakiDigits bd;  // B's digits, split with the first block
-    bool b_ready = false;
-    double b_peak = 0.0;
-    DeviceBuffer ablk[2], ahblk[2], chblk[2], cblk[2];
-    Event a_free[2], c_free[2];
-    for (int u = 0; u < 2; ++u) {
-        ablk[u] = DeviceBuffer(sizeof(double) * BI * m * n3);
-        ahblk[u] = DeviceBuffer(sizeof(double) * BI * m * p);
-        chblk[u] = DeviceBuffer(sizeof(double) * BI * n2 * p);
-        cblk[u] = DeviceBuffer(sizeof(double) * BI * n2 * n3);
-        a_free[u].record(s);
+    // 2. tiles
+    constexpr int kBufs = 4;
+    int64_t maxn = 0;
+    for (const Block& x : bb) maxn = std::max(maxn, x.n);
+    const int64_t BI = ab.empty() ? 0 : ab[0].n;
+    DeviceBuffer chb[kBufs], cb[kBufs];
+    Event c_free[kBufs];
+    for (int u = 0; u < kBufs; ++u) {
+        chb[u] = DeviceBuffer(sizeof(double) * BI * maxn * p);
+        cb[u] = DeviceBuffer(sizeof(double) * BI * maxn * n3);
         c_free[u].record(s);
     }
-    for (int64_t i0 = 0, ib = 0; i0 < n1; i0 += BI, ++ib) {
-        const int u = (int)(ib & 1);
-        const int64_t bi = std::min(BI, n1 - i0);
-        a_free[u].wait_on(up);  // block ib-2's transform has read ablk[u]
-        PPC_CUDA_CHECK(cudaMemcpy2DAsync(ablk[u].d(), sizeof(double) * bi, hA + i0, sizeof(double) * n1,
-                                         sizeof(double) * bi, m * n3, cudaMemcpyHostToDevice, up));
-        Event landed;
-        landed.record(up);
-        landed.wait_on(s);
-        mark("A block up", ib, up);
-        mode3(ablk[u].d(), bi * m, n3, q.d(), p, true, ahblk[u].d(), 1.0, s);  // A_blk x3 Q^T
-        a_free[u].record(s);
-        if (!facewise_ozaki(ahblk[u].d(), bi, m, p, bh.d(), n2, chblk[u].d(), bd, b_ready, b_peak, s))
-            facewise(ahblk[u].d(), bi, m, p, bh.d(), n2, chblk[u].d(), s);
-        c_free[u].wait_on(s);  // block ib-2's C rows are down
-        star_inverse(chblk[u].d(), bi * n2, p, q.d(), n3, scale, cblk[u].d(), s);  // x3 Q, scaled
+    bool b_bad = !int8_ok;  // B-hat failed the gate (or the shape never qualified): DMMA everywhere
+    const bool inv_int8 = ((n1 * n2) & 1) == 0;
+    int64_t ntile = 0;
+    auto tile = [&](int64_t I, int64_t J, bool dmma) {
+        Block& a = ab[(size_t)I];
+        Block& b = bb[(size_t)J];
+        const int u = (int)(ntile++ % kBufs);
+        c_free[u].wait_on(s);  // this buffer's previous tile is down
+        // the INT8 path as in facewise_ozaki: whole kFaceRows row blocks passing the gate
+        const bool int8 = !dmma && a.n >= kFaceRows && a.peak <= kOzakiPeakGate;
+        {
+            StageTimer tm("facewise", s, 2.0 * a.n * m * b.n * p, 8.0 * p * (a.n * m + m * b.n + a.n * b.n));
+            if (int8) {
+                ozaki_gemm(a.dig, b.dig, p, nullptr, chb[u].d(), a.n, a.n * b.n, s);
+            } else {
+                GemmDesc d;
+                d.M = a.n; d.N = b.n; d.K = m; d.batch = p;
+                d.A = a.hat.d(); d.lda = a.n; d.strideA = a.n * m;
+                d.B = bh.d() + b.o * m; d.ldb = m; d.strideB = m * n2;
+                d.C = chb[u].d(); d.ldc = a.n; d.strideC = a.n * b.n;
+                gemm(d, s);
+            }
+        }
+        // x3 Q, scaled; on the path star_q takes for the whole product (its
+        // INT8 kernel wants an even leading dimension: n1 n2 there, the tile's
+        // row count here, which is even whenever n1 n2 is)
+        if (!(inv_int8 && ozaki_star_inverse(chb[u].d(), a.n * b.n, p, q.d(), n3, scale, cb[u].d(), a.n * b.n, s)))
+            mode3(chb[u].d(), a.n * b.n, p, q.d(), n3, false, cb[u].d(), scale, s);
         Event done;
         done.record(s);
         done.wait_on(down);
-        mark("block computed", ib, s);
-        PPC_CUDA_CHECK(cudaMemcpy2DAsync(hC + i0, sizeof(double) * n1, cblk[u].d(), sizeof(double) * bi,
-                                         sizeof(double) * bi, n2 * n3, cudaMemcpyDeviceToHost, down));
+        mark("tile computed", I, J, s);
+        cudaMemcpy3DParms cp{};
+        cp.srcPtr = make_cudaPitchedPtr(cb[u].d(), sizeof(double) * a.n, sizeof(double) * a.n, (size_t)b.n);
+        cp.dstPtr = make_cudaPitchedPtr(hC + a.o + b.o * n1, sizeof(double) * n1, sizeof(double) * n1, (size_t)n2);
+        cp.extent = make_cudaExtent(sizeof(double) * a.n, (size_t)b.n, (size_t)n3);
+        cp.kind = cudaMemcpyDeviceToHost;
+        PPC_CUDA_CHECK(cudaMemcpy3DAsync(&cp, down));
         c_free[u].record(down);
-        mark("C block down", ib, down);
+        mark("tile down", I, J, down);
+    };
+    DeviceBuffer peaks(sizeof(double) * 2);
+    for (int64_t t = 0; t < std::max(nI, nJ); ++t) {
+        const bool was_bad = b_bad;
+        if (t < nI) {
+            Block& x = ab[(size_t)t];
+            x.landed->wait_on(s);
+            mode3(x.raw.d(), x.n * m, n3, q.d(), p, true, x.hat.d(), 1.0, s);  // A_blk x3 Q^T
+            x.raw.release();
+            if (int8_ok && !b_bad && x.n >= kFaceRows) {
+                x.dig.split(x.hat.d(), x.n, x.n * m, m, x.n, m, p, s, nullptr, 0, 0, 0, nullptr, 6, 0, 0, nullptr, 0,
+                            true);
+                ozaki_peak_ratios_async(x.dig, m, kFaceRows, peaks.d(), s);
+            }
+        }
+        if (t < nJ) {
+            Block& x = bb[(size_t)t];
+            x.landed->wait_on(s);
+            StageTimer tm("mode3_fwd", s, 2.0 * m * x.n * n3 * p, 8.0 * (m * x.n * (n3 + p) + n3 * p));
+            GemmDesc d;  // B-hat rows [o m, (o + n) m) of every slice = those tubes x Q
+            d.M = m * x.n; d.N = p; d.K = n3;
+            d.A = x.raw.d(); d.lda = m * x.n;
+            d.B = q.d(); d.ldb = n3;
+            d.C = bh.d() + x.o * m; d.ldc = m * n2;
+            gemm(d, s);
+            x.raw.release();
+            if (int8_ok && !b_bad) {
+                x.dig.split(bh.d() + x.o * m, m, m * n2, m, x.n, m, p, s);
+                ozaki_peak_ratios_async(x.dig, m, x.n, peaks.d() + 1, s);
+            }
+        }
+        if (int8_ok && !b_bad) {
+            double h[2] = {0.0, 0.0};
+            read_small(peaks.d(), h, 2, s);
+            if (t < nI && ab[(size_t)t].n >= kFaceRows) ab[(size_t)t].peak = h[0];
+            if (t < nJ) {
+                bb[(size_t)t].peak = h[1];
+                if (h[1] > kOzakiPeakGate) b_bad = true;
+            }
+        }
+        if (b_bad && !was_bad) {
+            // a B block failed the gate: star_q runs the whole product on DMMA
+            for (int64_t I = 0; I < std::min(t, nI); ++I)
+                for (int64_t J = 0; J < std::min(t, nJ); ++J) tile(I, J, true);
+        }
+        // the tiles this step completes: row t against the columns so far, column t against the rows before
+        if (t < nI)
+            for (int64_t J = 0; J <= std::min(t, nJ - 1); ++J) tile(t, J, b_bad);
+        if (t < nJ)
+            for (int64_t I = 0; I < std::min(t, nI); ++I) tile(I, t, b_bad);
     }
     if (trace) {
         PPC_CUDA_CHECK(cudaStreamSynchronize(down));

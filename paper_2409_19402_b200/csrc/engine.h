@@ -33,10 +33,11 @@ void facewise_auto(const double* A, int64_t n1, int64_t m, int64_t p, const doub
 // star_products.cpp:51-59
 void star_q(const double* A, int64_t n1, int64_t m, int64_t n3, const double* B, int64_t n2,
             const double* Q, int64_t p, double scale, double* C, cudaStream_t s);
-// star_q on HOST buffers, pipelined: B is uploaded in pixel chunks and
-// transformed as they land; then A row blocks stream up while the finished C
-// row blocks stream down (separate H2D / D2H streams), so PCIe runs both
-// directions at once. Bitwise equal to star_q on device copies.
+// star_q on HOST buffers, pipelined in 2-D tiles: A's row blocks and B's
+// lateral blocks stream up alternately, each is transformed as it lands, and
+// every tile of C the arrivals complete is computed and sent down at once
+// (separate H2D / D2H streams: PCIe runs both directions from the second block
+// on). Bitwise equal to star_q on device copies (engine.cu for the argument).
 void star_q_host(const double* hA, int64_t n1, int64_t m, int64_t n3, const double* hB, int64_t n2,
                  const double* hQ, int64_t p, double scale, double* hC, cudaStream_t s);
 // host sums[0] = sum (a-b)^2 (or a^2 when b == nullptr), sums[1] = sum a^2.

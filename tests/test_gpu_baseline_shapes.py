@@ -131,6 +131,43 @@ def test_star_q_dynamic_range_gate(engine, blas_oracle):
     assert np.array_equal(engine.star_q(a, b, t), got)
 
 
+def test_star_q_host_tiles_redone_when_late_b_block_fails_gate(engine, blas_oracle):
+    """The host pipeline computes C in 2-D tiles as A's row blocks and B's
+    lateral blocks land, on the INT8 path until a B block fails the
+    dynamic-range gate (B-hat's gate is one value over all of B, as in the
+    device call). Here the third lateral block fails: the tiles already sent
+    down are redone on FP64 DMMA, and the result is bitwise the device call's
+    (which runs the whole product on DMMA) and matches the oracle."""
+    rng = np.random.default_rng(4)
+    n1, m, n2, n3, p = 256, 256, 384, 32, 16
+    a = np.asfortranarray(rng.standard_normal((n1, m, n3)))
+    b = np.asfortranarray(rng.standard_normal((m, n2, n3)))
+    b[9, 300, :] = 1e9 * rng.standard_normal(n3)  # lateral block 2 (columns 256..383)
+    t = engine.Transform("dct", n3, p)
+    with Stages() as st:
+        dev = engine.to_host(engine.star_q(engine.to_device(a), engine.to_device(b), t))
+    assert "ozaki_gemm" not in st.names, st.names  # the device call: all DMMA
+    with Stages() as st:
+        host = engine.star_q(a, b, t)
+    assert "ozaki_gemm" in st.names, st.names      # the first tiles ran on INT8 before block 2 landed
+    assert np.array_equal(host, dev)
+    want = blas_oracle.star_q_product(a, b, blas_oracle.dct_q(n3, p))
+    assert rel(host, want) <= 1e-12
+    # ragged extents: short last row block (DMMA), merged short lateral tail, odd n1
+    n1, n2 = 300, 450
+    a = np.asfortranarray(rng.standard_normal((n1, m, n3)))
+    b = np.asfortranarray(rng.standard_normal((m, n2, n3)))
+    dev = engine.to_host(engine.star_q(engine.to_device(a), engine.to_device(b), t))
+    assert np.array_equal(engine.star_q(a, b, t), dev)
+    assert rel(dev, blas_oracle.star_q_product(a, b, blas_oracle.dct_q(n3, p))) <= 1e-12
+    for n1o, n2o in ((257, 129), (129, 322)):  # n1 n2 odd: the device call's inverse runs on DMMA
+        a = np.asfortranarray(rng.standard_normal((n1o, m, n3)))
+        b = np.asfortranarray(rng.standard_normal((m, n2o, n3)))
+        t64 = engine.Transform("dct", n3, 32)
+        dev = engine.to_host(engine.star_q(engine.to_device(a), engine.to_device(b), t64))
+        assert np.array_equal(engine.star_q(a, b, t64), dev), (n1o, n2o)
+
+
 # ------------------------------------------------------------------ cfg2
 def test_cfg2_sweep_full_vs_oracle(engine, blas_oracle):
     """BASELINE configs[1]: the 240x320x200 video, data-driven Q p=20, tSVDQ at

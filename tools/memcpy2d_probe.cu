@@ -86,6 +86,27 @@ int main() {
         CK(cudaEventSynchronize(b));
         CK(cudaEventElapsedTime(&ms, a, b));
         printf("down only, 8 x 256 MiB strided: %.2f ms  %.1f GB/s\n", ms, 16 * blk / ms * 1e-6);
+        // the 2-D tiled pipeline's downloads: 3-D copies of 128 x 128 x 256 tiles
+        // (1 KB runs, 128 per plane, 256 planes) into an 8 KB-pitch, 1024-row slice layout
+        char* d4; CK(cudaMalloc(&d4, 32ull << 20));
+        for (int rows : {128, 256, 1024}) {
+            const size_t tile = (size_t)w * rows * 256;
+            const int nt = (int)((1ull << 30) / tile);
+            CK(cudaEventRecord(a, s2));
+            for (int i = 0; i < nt; ++i) {
+                cudaMemcpy3DParms cp = {};
+                cp.srcPtr = make_cudaPitchedPtr(d3, w, w, rows);
+                cp.dstPtr = make_cudaPitchedPtr(h2 + (i % 8) * w, pitch, pitch, 1024);
+                cp.extent = make_cudaExtent(w, rows, 256);
+                cp.kind = cudaMemcpyDeviceToHost;
+                CK(cudaMemcpy3DAsync(&cp, s2));
+            }
+            CK(cudaEventRecord(b, s2));
+            CK(cudaEventSynchronize(b));
+            CK(cudaEventElapsedTime(&ms, a, b));
+            printf("down only, 3-D tiles of 1 KB x %d x 256 (%zu MiB each), 1 GiB: %.2f ms  %.1f GB/s\n", rows,
+                   tile >> 20, ms, (double)nt * tile / ms * 1e-6);
+        }
     }
     return 0;
 }
