@@ -300,55 +300,51 @@ void star_q_host(const double* hA, int64_t n1, int64_t m, int64_t n3, const doub
         c_free[u].record(down);
         mark("tile down", I, J, down);
     };
-    DeviceBuffer peaks(sizeof(double) * 2);
+    DeviceBuffer peaks(sizeof(double));
+    // every tile among rows [0, ni) x columns [0, nj) again, on DMMA
+    auto redo = [&](int64_t ni, int64_t nj) {
+        for (int64_t I = 0; I < ni; ++I)
+            for (int64_t J = 0; J < nj; ++J) tile(I, J, true);
+    };
     for (int64_t t = 0; t < std::max(nI, nJ); ++t) {
-        const bool was_bad = b_bad;
-        if (t < nI) {
+        if (t < nI) {  // A block t: transform, digits, gate; then its tiles against the B blocks so far
             Block& x = ab[(size_t)t];
             x.landed->wait_on(s);
             mode3(x.raw.d(), x.n * m, n3, q.d(), p, true, x.hat.d(), 1.0, s);  // A_blk x3 Q^T
             x.raw.release();
-            if (int8_ok && !b_bad && x.n >= kFaceRows) {
+            if (!b_bad && x.n >= kFaceRows) {
                 x.dig.split(x.hat.d(), x.n, x.n * m, m, x.n, m, p, s, nullptr, 0, 0, 0, nullptr, 6, 0, 0, nullptr, 0,
                             true);
                 ozaki_peak_ratios_async(x.dig, m, kFaceRows, peaks.d(), s);
+                read_small(peaks.d(), &x.peak, 1, s);
             }
+            for (int64_t J = 0; J < std::min(t, nJ); ++J) tile(t, J, b_bad);
         }
-        if (t < nJ) {
+        if (t < nJ) {  // B block t: transform, digits, gate; then its tiles against the A blocks so far
             Block& x = bb[(size_t)t];
             x.landed->wait_on(s);
-            StageTimer tm("mode3_fwd", s, 2.0 * m * x.n * n3 * p, 8.0 * (m * x.n * (n3 + p) + n3 * p));
-            GemmDesc d;  // B-hat rows [o m, (o + n) m) of every slice = those tubes x Q
-            d.M = m * x.n; d.N = p; d.K = n3;
-            d.A = x.raw.d(); d.lda = m * x.n;
-            d.B = q.d(); d.ldb = n3;
-            d.C = bh.d() + x.o * m; d.ldc = m * n2;
-            gemm(d, s);
+            {
+                StageTimer tm("mode3_fwd", s, 2.0 * m * x.n * n3 * p, 8.0 * (m * x.n * (n3 + p) + n3 * p));
+                GemmDesc d;  // B-hat rows [o m, (o + n) m) of every slice = those tubes x Q
+                d.M = m * x.n; d.N = p; d.K = n3;
+                d.A = x.raw.d(); d.lda = m * x.n;
+                d.B = q.d(); d.ldb = n3;
+                d.C = bh.d() + x.o * m; d.ldc = m * n2;
+                gemm(d, s);
+            }
             x.raw.release();
-            if (int8_ok && !b_bad) {
+            if (!b_bad) {
                 x.dig.split(bh.d() + x.o * m, m, m * n2, m, x.n, m, p, s);
-                ozaki_peak_ratios_async(x.dig, m, x.n, peaks.d() + 1, s);
+                ozaki_peak_ratios_async(x.dig, m, x.n, peaks.d(), s);
+                read_small(peaks.d(), &x.peak, 1, s);
+                if (x.peak > kOzakiPeakGate) {
+                    // this B block fails the gate: star_q runs the whole product on DMMA
+                    b_bad = true;
+                    redo(std::min(t + 1, nI), t);
+                }
             }
+            for (int64_t I = 0; I < std::min(t + 1, nI); ++I) tile(I, t, b_bad);
         }
-        if (int8_ok && !b_bad) {
-            double h[2] = {0.0, 0.0};
-            read_small(peaks.d(), h, 2, s);
-            if (t < nI && ab[(size_t)t].n >= kFaceRows) ab[(size_t)t].peak = h[0];
-            if (t < nJ) {
-                bb[(size_t)t].peak = h[1];
-                if (h[1] > kOzakiPeakGate) b_bad = true;
-            }
-        }
-        if (b_bad && !was_bad) {
-            // a B block failed the gate: star_q runs the whole product on DMMA
-            for (int64_t I = 0; I < std::min(t, nI); ++I)
-                for (int64_t J = 0; J < std::min(t, nJ); ++J) tile(I, J, true);
-        }
-        // the tiles this step completes: row t against the columns so far, column t against the rows before
-        if (t < nI)
-            for (int64_t J = 0; J <= std::min(t, nJ - 1); ++J) tile(t, J, b_bad);
-        if (t < nJ)
-            for (int64_t I = 0; I < std::min(t, nI); ++I) tile(I, t, b_bad);
     }
     if (trace) {
         PPC_CUDA_CHECK(cudaStreamSynchronize(down));
