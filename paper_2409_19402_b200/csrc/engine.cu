@@ -195,7 +195,7 @@ void star_q_host(const double* hA, int64_t n1, int64_t m, int64_t n3, const doub
     mark("start", 0, -1, s);
     struct Block {
         int64_t o = 0, n = 0;         // first row / column, extent
-        DeviceBuffer raw, hat;        // the block as uploaded; its transform (compact)
+        DeviceBuffer hat;             // A blocks: the transform (compact); B's go into bh
         OzakiDigits dig;
         double peak = 0.0;
         std::unique_ptr<Event> landed;
@@ -217,21 +217,33 @@ void star_q_host(const double* hA, int64_t n1, int64_t m, int64_t n3, const doub
     const int64_t nI = (int64_t)ab.size(), nJ = (int64_t)bb.size();
     const bool int8_ok = ozaki_gemm_eligible(n1, m) && n2 >= 64;  // star_q's shape test
     DeviceBuffer q(sizeof(double) * n3 * p);
-    for (Block& x : ab) {
-        x.raw = DeviceBuffer(sizeof(double) * x.n * m * n3);
-        x.hat = DeviceBuffer(sizeof(double) * x.n * m * p);
-    }
+    for (Block& x : ab) x.hat = DeviceBuffer(sizeof(double) * x.n * m * p);
     DeviceBuffer bh(sizeof(double) * m * n2 * p);  // B-hat whole: slice i at i * m * n2 (star_q's layout)
-    for (Block& x : bb) x.raw = DeviceBuffer(sizeof(double) * m * x.n * n3);
+    // the blocks as uploaded: rings of kRing buffers per operand, so the uploads
+    // run kRing - 1 steps ahead of the transforms whatever the tensors' size
+    constexpr int kRing = 4;
+    int64_t maxn = 0;
+    for (const Block& x : bb) maxn = std::max(maxn, x.n);
+    const int64_t BI = ab.empty() ? 0 : ab[0].n;
+    DeviceBuffer araw[kRing], braw[kRing];
+    Event a_done[kRing], b_done[kRing];  // the transform reading the slot is enqueued
+    for (int r = 0; r < kRing; ++r) {
+        araw[r] = DeviceBuffer(sizeof(double) * BI * m * n3);
+        braw[r] = DeviceBuffer(sizeof(double) * m * maxn * n3);
+    }
     Event ready;
     ready.record(s);  // buffers allocated on s
     ready.wait_on(up);
     PPC_CUDA_CHECK(cudaMemcpyAsync(q.d(), hQ, sizeof(double) * n3 * p, cudaMemcpyHostToDevice, up));
-    // 1. every upload, alternating A and B blocks
-    for (int64_t t = 0; t < std::max(nI, nJ); ++t) {
+    // 1. uploads, alternating A and B blocks (step t: A block t, then B block t)
+    const int64_t steps = std::max(nI, nJ);
+    auto upload = [&](int64_t t) {
+        if (t >= steps) return;
+        const int r = (int)(t % kRing);
         if (t < nI) {
             Block& x = ab[(size_t)t];  // rows [o, o+n) of every lateral slice: n x (m n3), compact
-            PPC_CUDA_CHECK(cudaMemcpy2DAsync(x.raw.d(), sizeof(double) * x.n, hA + x.o, sizeof(double) * n1,
+            if (t >= kRing) a_done[r].wait_on(up);
+            PPC_CUDA_CHECK(cudaMemcpy2DAsync(araw[r].d(), sizeof(double) * x.n, hA + x.o, sizeof(double) * n1,
                                              sizeof(double) * x.n, m * n3, cudaMemcpyHostToDevice, up));
             x.landed = std::make_unique<Event>();
             x.landed->record(up);
@@ -239,19 +251,18 @@ void star_q_host(const double* hA, int64_t n1, int64_t m, int64_t n3, const doub
         }
         if (t < nJ) {
             Block& x = bb[(size_t)t];  // columns [o, o+n) of every frontal slice: (m n) x n3, compact
-            PPC_CUDA_CHECK(cudaMemcpy2DAsync(x.raw.d(), sizeof(double) * m * x.n, hB + x.o * m,
+            if (t >= kRing) b_done[r].wait_on(up);
+            PPC_CUDA_CHECK(cudaMemcpy2DAsync(braw[r].d(), sizeof(double) * m * x.n, hB + x.o * m,
                                              sizeof(double) * m * n2, sizeof(double) * m * x.n, n3,
                                              cudaMemcpyHostToDevice, up));
             x.landed = std::make_unique<Event>();
             x.landed->record(up);
             mark("B block up", t, -1, up);
         }
-    }
+    };
+    for (int64_t t = 0; t < kRing; ++t) upload(t);
     // 2. tiles
     constexpr int kBufs = 4;
-    int64_t maxn = 0;
-    for (const Block& x : bb) maxn = std::max(maxn, x.n);
-    const int64_t BI = ab.empty() ? 0 : ab[0].n;
     DeviceBuffer chb[kBufs], cb[kBufs];
     Event c_free[kBufs];
     for (int u = 0; u < kBufs; ++u) {
@@ -306,12 +317,14 @@ void star_q_host(const double* hA, int64_t n1, int64_t m, int64_t n3, const doub
         for (int64_t I = 0; I < ni; ++I)
             for (int64_t J = 0; J < nj; ++J) tile(I, J, true);
     };
-    for (int64_t t = 0; t < std::max(nI, nJ); ++t) {
+    for (int64_t t = 0; t < steps; ++t) {
+        const int r = (int)(t % kRing);
+        if (t > 0) upload(t - 1 + kRing);  // into the slots step t - 1's transforms have read
         if (t < nI) {  // A block t: transform, digits, gate; then its tiles against the B blocks so far
             Block& x = ab[(size_t)t];
             x.landed->wait_on(s);
-            mode3(x.raw.d(), x.n * m, n3, q.d(), p, true, x.hat.d(), 1.0, s);  // A_blk x3 Q^T
-            x.raw.release();
+            mode3(araw[r].d(), x.n * m, n3, q.d(), p, true, x.hat.d(), 1.0, s);  // A_blk x3 Q^T
+            a_done[r].record(s);
             if (!b_bad && x.n >= kFaceRows) {
                 x.dig.split(x.hat.d(), x.n, x.n * m, m, x.n, m, p, s, nullptr, 0, 0, 0, nullptr, 6, 0, 0, nullptr, 0,
                             true);
@@ -327,12 +340,12 @@ void star_q_host(const double* hA, int64_t n1, int64_t m, int64_t n3, const doub
                 StageTimer tm("mode3_fwd", s, 2.0 * m * x.n * n3 * p, 8.0 * (m * x.n * (n3 + p) + n3 * p));
                 GemmDesc d;  // B-hat rows [o m, (o + n) m) of every slice = those tubes x Q
                 d.M = m * x.n; d.N = p; d.K = n3;
-                d.A = x.raw.d(); d.lda = m * x.n;
+                d.A = braw[r].d(); d.lda = m * x.n;
                 d.B = q.d(); d.ldb = n3;
                 d.C = bh.d() + x.o * m; d.ldc = m * n2;
                 gemm(d, s);
             }
-            x.raw.release();
+            b_done[r].record(s);
             if (!b_bad) {
                 x.dig.split(bh.d() + x.o * m, m, m * n2, m, x.n, m, p, s);
                 ozaki_peak_ratios_async(x.dig, m, x.n, peaks.d(), s);
