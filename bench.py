@@ -628,8 +628,16 @@ def run_reference(args, rank, world):
     v = vals[len(vals) // 2]
     cpu = {"value": v, "unit": unit, "cores": threads, "kind": "port", "sample": info["sample"],
            "how": info["how"], "extrapolated": info["extrapolated"]}
+    if args.workload == "cfg4":
+        n1, m, n2, n3, p = shim.dims
+        work = 2.0 * p * (n1 * m * n3 + m * n2 * n3 + n1 * m * n2 + n1 * n2 * n3) / 1e12
+    else:
+        n1, n2, n3 = shim.dims[:3]
+        work = 8.0 * n1 * n2 * n3 / 1e9
     line = {"impl": "reference", "metric": metric, "value": v, "unit": unit, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * work / v,  # of the whole workload (extrapolated from the sample where it says so)
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": args.workload, "sample": info["sample"]},
             "cpu_baseline": cpu,
