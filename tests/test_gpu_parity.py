@@ -1778,3 +1778,44 @@ def test_sharded_eigensolve_bitwise(engine, n, p, world):
     lam = np.sort(np.linalg.eigvalsh(Gm.cpu().numpy()))[::-1][:p]
     cap = torch.sum(Q * (Gm @ Q), dim=0).cpu().numpy()
     assert np.max(np.abs(cap - lam)) <= 1e-12 * lam[0]
+
+
+def test_concurrent_host_threads_match_serial(engine, oracle):
+    """The engine keeps its device context, streams, workspace cache and stage
+    timers per host thread (the reference's slice loops run on worker threads,
+    parallel.cpp:29-57): four threads calling the C-ABI at once get the bits of
+    the same calls made one after another."""
+    import threading
+    pp = engine
+    t = pp.Transform("dct", 48, 12)
+    inputs = [oracle.random_tensor(96, 80, 48, 100 + i) for i in range(4)]
+
+    def work(a):
+        at = np.asfortranarray(a.transpose(1, 0, 2))
+        c = pp.star_q(a, at, t)
+        f = pp.tsvdq(a, t, 5)
+        fq, re = pp.compress_tsvdq(a, 12, 5)
+        return c, f.s, re, fq.transform.q
+
+    serial = [work(a) for a in inputs]
+    out = [None] * 4
+    errs = []
+
+    def run(i):
+        try:
+            for _ in range(3):
+                out[i] = work(inputs[i])
+        except Exception as e:  # noqa: BLE001
+            errs.append(e)
+
+    th = [threading.Thread(target=run, args=(i,)) for i in range(4)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+    assert not errs, errs
+    for got, want in zip(out, serial):
+        assert np.array_equal(got[0], want[0])
+        assert np.array_equal(got[1], want[1])
+        assert got[2] == want[2]
+        assert np.array_equal(got[3], want[3])
