@@ -1819,3 +1819,71 @@ def test_concurrent_host_threads_match_serial(engine, oracle):
         assert np.array_equal(got[1], want[1])
         assert got[2] == want[2]
         assert np.array_equal(got[3], want[3])
+
+
+def test_star_q_algebra_and_error_identities_random_instances(engine, oracle):
+    """Property checks in the spirit of the reference's verify suite
+    (src/verify.cpp:487-537, 581-726: star-Q algebra, projection tail,
+    Eckart-Young identity, recovery), on the GPU path over random instances
+    and all four transform kinds."""
+    pp = engine
+    rng = np.random.default_rng(11)
+    worst = 0.0
+    for inst in range(16):
+        n1, m, n2, l = (int(rng.integers(2, 9)) for _ in range(4))
+        n3 = int(rng.choice([4, 6, 8, 12]))
+        p = int(rng.integers(1, n3 + 1))
+        kind = ["dct", "haar", "random", "data"][inst % 4]
+        A = np.asfortranarray(rng.standard_normal((n1, m, n3)))
+        B = np.asfortranarray(rng.standard_normal((m, n2, n3)))
+        B2 = np.asfortranarray(rng.standard_normal((m, n2, n3)))
+        Cc = np.asfortranarray(rng.standard_normal((n2, l, n3)))
+        if kind == "haar":  # the reference's Haar basis exists for n3 = 2 and 4 only (transforms.cpp:45-60)
+            n3 = 4
+            p = min(p, n3)
+            A, B, B2, Cc = (np.asfortranarray(x[:, :, :4]) for x in (A, B, B2, Cc))
+        t = pp.data_dependent_transform(A, p) if kind == "data" else pp.Transform(kind, n3, p, seed=inst)
+        q = t.q
+        nrm = lambda x: float(np.linalg.norm(x))  # noqa: E731
+        AB = pp.star_q(A, B, t)
+        # associativity, distributivity
+        lhs, rhs = pp.star_q(AB, Cc, t), pp.star_q(A, pp.star_q(B, Cc, t), t)
+        worst = max(worst, nrm(lhs - rhs) / max(nrm(lhs), 1e-300))
+        worst = max(worst, nrm(pp.star_q(A, np.asfortranarray(B + B2), t) - AB - pp.star_q(A, B2, t)) / nrm(AB))
+        # transpose reversal, identity from both sides (the identity acts as the projection)
+        tr = pp.star_q_transpose(AB, t)
+        worst = max(worst, nrm(tr - pp.star_q(pp.star_q_transpose(B, t), pp.star_q_transpose(A, t), t)) / nrm(tr))
+        PA = oracle.mode3_product(A, q @ q.T)
+        worst = max(worst, nrm(pp.star_q(pp.star_q_identity(n1, t), A, t) - PA) / nrm(A))
+        worst = max(worst, nrm(pp.star_q(A, pp.star_q_identity(m, t), t) - PA) / nrm(A))
+        # projection form: the product only sees the projected parts of its factors
+        PB = oracle.mode3_product(B, q @ q.T)
+        worst = max(worst, nrm(pp.star_q(PA, PB, t) - AB) / nrm(AB))
+        # transform-domain slices of the product are the facewise products
+        worst = max(worst, nrm(oracle.mode3_product(AB, q.T) -
+                               pp.facewise_product(oracle.mode3_product(A, q.T), oracle.mode3_product(B, q.T))) /
+                    nrm(AB))
+        # Eckart-Young identity and projection tail for every k
+        T = A.reshape(-1, n3, order="F")
+        sv = np.linalg.svd(T, compute_uv=False)
+        for k in range(1, min(n1, m) + 1):
+            f = pp.tsvdq(A, t, k)
+            tot, ey, pr = pp.tsvdq_error(A, f)
+            worst = max(worst, abs(tot ** 2 - ey ** 2 - pr ** 2) / nrm(A) ** 2)
+            if kind == "data":
+                tail = float(np.sum(sv[p:] ** 2))
+                worst = max(worst, abs(pr ** 2 - tail) / nrm(A) ** 2)
+            # the kept slice spectra are the leading singular values of the transform-domain slices
+            ah = oracle.mode3_product(A, q.T)
+            for i in range(p):
+                si = np.linalg.svd(ah[:, :, i], compute_uv=False)[:k]
+                worst = max(worst, float(np.max(np.abs(f.s[:, i] - si))) / max(si[0], 1e-300))
+        # recovery: rank-r slices in the transform domain come back exactly at k = r
+        r = 1 + inst % 2
+        core = np.zeros((n1, m, p), order="F")
+        for i in range(p):
+            core[:, :, i] = rng.standard_normal((n1, r)) @ rng.standard_normal((r, m))
+        X = oracle.mode3_product(core, q)
+        fx = pp.tsvdq(X, t, min(r, n1, m))
+        worst = max(worst, pp.tsvdq_relative_error(X, fx) if min(n1, m) >= r else 0.0)
+    assert worst <= 1e-10, worst
