@@ -1887,3 +1887,32 @@ def test_star_q_algebra_and_error_identities_random_instances(engine, oracle):
         fx = pp.tsvdq(X, t, min(r, n1, m))
         worst = max(worst, pp.tsvdq_relative_error(X, fx) if min(n1, m) >= r else 0.0)
     assert worst <= 1e-10, worst
+
+
+def test_projection_and_truncation_optimality(engine, oracle):
+    """verify.cpp:513-537 and the Eckart-Young optimality check: the
+    data-driven Q's projection error is no larger than that of random Stiefel
+    samples of the same p, and tsvdq's rank-k truncation error no larger than
+    that of random facewise rank-k approximations in the transform domain."""
+    pp = engine
+    rng = np.random.default_rng(23)
+    for inst in range(4):
+        n1, n2, n3 = int(rng.integers(4, 10)), int(rng.integers(4, 10)), int(rng.integers(4, 10))
+        p, k = int(rng.integers(1, n3)), int(rng.integers(1, min(n1, n2)))
+        A = np.asfortranarray(rng.standard_normal((n1, n2, n3)))
+        t = pp.data_dependent_transform(A, p)
+        best = pp.projection_error(A, t)
+        for s in range(20):
+            tr = pp.Transform("random", n3, p, seed=1000 * inst + s)
+            assert best <= pp.projection_error(A, tr) * (1 + 1e-12)
+        f = pp.tsvdq(A, t, k)
+        _, ey, _ = pp.tsvdq_error(A, f)
+        ah = oracle.mode3_product(A, t.q.T)
+        for s in range(20):
+            err2 = 0.0
+            for i in range(p):
+                R = rng.standard_normal((k, n2))  # a random k-dimensional row space
+                # the best fit within it: least squares on the left factor
+                coef, *_ = np.linalg.lstsq(R.T, ah[:, :, i].T, rcond=None)
+                err2 += np.linalg.norm(ah[:, :, i] - coef.T @ R) ** 2
+            assert ey ** 2 <= err2 * (1 + 1e-12)
