@@ -34,3 +34,35 @@ def test_bench_default_arguments():
     assert '"--gpus", type=int, default=1' in src
     assert '"--warmup", type=int, default=3' in src
     assert '"--steps", type=int, default=5' in src
+
+
+import pytest  # noqa: E402
+
+
+@pytest.mark.gpu
+def test_bench_line_has_the_contract_keys_on_gpu():
+    """One short run of the engine arm (cfg2: small) prints one JSON line with
+    the contract's keys: metric / value / unit, the roofline and e2e objects,
+    the launch count and the sampled clocks."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--workload", "cfg2", "--steps", "2",
+                        "--warmup", "3"], capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+                "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e", "gpu_launches", "clocks"):
+        assert key in d, key
+    assert d["metric"] == "tsvdq_input_GBps" and d["unit"] == "GB/s" and d["n_gpus"] == 1
+    assert d["steps"] == 2 and d["warmup"] == 3 and d["value"] > 0 and d["gpu_launches"] > 0
+    assert d["dtype"] == "f64" and d["data"] == "synthetic" and "workload" in d["config"] and "model" not in d["config"]
+    rf = d["roofline"]
+    for key in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
+        assert key in rf, key
+    assert abs(rf["frac"] - rf["achieved"] / rf["peak"]) <= 1e-9
+    e = d["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] == 8 * 240 * 320 * 200 and e["d2h_bytes_per_step"] > 0
+    assert e["value"] < d["value"]  # host buffers and PCIe inside the step
+    cb = d["cpu_baseline"]
+    assert cb["kind"] == "port" and cb["cores"] >= 1 and cb["value"] > 0
+    assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
