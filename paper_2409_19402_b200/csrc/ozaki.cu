@@ -88,7 +88,11 @@ __global__ void __launch_bounds__(256) ozaki_split_kernel(const double* __restri
                                                           int64_t chunk, int64_t per, int8_t* __restrict__ D,
                                                           double* __restrict__ scale, double* __restrict__ sumsq,
                                                           const int* __restrict__ zmap, int* __restrict__ nonfinite,
-                                                          const double* __restrict__ fixed_max, int nwrite) {
+                                                          const double* __restrict__ fixed_max, int nwrite,
+                                                          const double* __restrict__ rowscale) {
+    // rowscale (nullable, batched blocks, not TRS): every block reads the SAME
+    // source X and scales row k by rowscale[b * rows + k] (the forward
+    // transform's diag(sigma_b) Q, without materializing it per block)
     constexpr int TPC = 256 / CPB;  // threads per column
     constexpr int WPC = TPC / 32;   // warps per column
     constexpr int SCOL = kKC / CPB + (TRS ? 1 : 0);  // staged column stride (+1: no bank conflicts)
@@ -133,11 +137,19 @@ __global__ void __launch_bounds__(256) ozaki_split_kernel(const double* __restri
 #pragma unroll
         for (int q = 0; q < NL; ++q) v[q] = stg[lt + TPC * q];
     } else {
-        const double* col = X + (stride ? b * stride : 0) + (live ? j : 0) * ldx + r0;
+        const double* col = X + (stride && !rowscale ? b * stride : 0) + (live ? j : 0) * ldx + r0;
 #pragma unroll
         for (int q = 0; q < NL; ++q) {
             const int64_t i = lt + TPC * q;
             v[q] = i < len ? __ldcs(col + i) : 0.0;
+        }
+        if (rowscale) {
+            const double* rs = rowscale + b * rows + r0;
+#pragma unroll
+            for (int q = 0; q < NL; ++q) {
+                const int64_t i = lt + TPC * q;
+                if (i < len) v[q] = rs[i] * v[q];
+            }
         }
     }
 #pragma unroll
@@ -739,8 +751,9 @@ void ozaki_syrk(const OzakiDigits& d, int64_t nout, int64_t per, double* out, cu
 void OzakiDigits::split(const double* X, int64_t ldx, int64_t stride, int64_t rows_, int64_t cols_, int64_t KC,
                         int64_t nblk_, cudaStream_t s, const int* zmap, int64_t nz, int64_t chunk, int64_t per,
                         int* nonfinite, int ndig, int64_t block_base, int64_t alloc_blocks,
-                        const double* fixed_max, int nwrite, bool trans_src) {
+                        const double* fixed_max, int nwrite, bool trans_src, const double* rowscale) {
     HostProf hp_("ozaki_split");
+    if (rowscale && (!stride || trans_src)) fail(PPC_ARGUMENT, "ozaki split: row scales need batched, untransposed blocks");
     if (trans_src && !stride) fail(PPC_ARGUMENT, "ozaki split: a transposed source needs batched blocks");
     if (ndig != kS && ndig != kSmax) fail(PPC_ARGUMENT, "ozaki split: 6 or 7 digits");
     if (block_base < 0 || (block_base > 0 && block_base + nblk_ > alloc_blocks))
@@ -774,10 +787,11 @@ void OzakiDigits::split(const double* X, int64_t ldx, int64_t stride, int64_t ro
     do {                                                                                                             \
         if (trans_src)                                                                                               \
             ozaki_split_kernel<ND_, CPB_, true><<<grid, 256, 0, s>>>(X, ldx, stride, rows, cols, KC, KCp, ch, pr,    \
-                                                                     D0, sc0, sq0, zmap, nonfinite, fixed_max, nw); \
+                                                                     D0, sc0, sq0, zmap, nonfinite, fixed_max, nw,  \
+                                                                     nullptr);                                       \
         else                                                                                                         \
             ozaki_split_kernel<ND_, CPB_><<<grid, 256, 0, s>>>(X, ldx, stride, rows, cols, KC, KCp, ch, pr, D0, sc0, \
-                                                               sq0, zmap, nonfinite, fixed_max, nw);                 \
+                                                               sq0, zmap, nonfinite, fixed_max, nw, rowscale);       \
     } while (0)
     if (nd == kSmax) {
         if (cpb == 8) PPC_SPLIT(kSmax, 8); else if (cpb == 4) PPC_SPLIT(kSmax, 4);
@@ -1031,37 +1045,19 @@ bool ozaki_gram_partials(const double* T, int64_t ldT, int64_t rows, int64_t n3,
     return true;
 }
 
-namespace {
-
-// Bq[b] (n3 x p, column-major) = diag(sigma_{b,.}) Q: the per-(row block,
-// column) scales of T's digits folded into the transform.
-__global__ void fold_q_kernel(const double* __restrict__ sc, const double* __restrict__ Q, int64_t n3, int64_t p,
-                              int64_t total, double* __restrict__ Bq) {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += stride) {
-        const int64_t b = i / (n3 * p), r = i - b * n3 * p, c = r % n3;
-        Bq[i] = sc[b * n3 + c] * Q[r];
-    }
-}
-
-}  // namespace
-
 bool ozaki_mode3_forward(const OzakiDigits& td, int64_t N, const double* Q, int64_t p, double* out, cudaStream_t s) {
     static const bool off = std::getenv("PPC_OZAKI_FWD") && std::getenv("PPC_OZAKI_FWD")[0] == '0';
     if (off || !ozaki_enabled() || !td.uniform || td.nd != kSmax || td.KCp != kKC) return false;
     const int64_t n3 = td.cols, nblk = std::min(td.nblk, (N + kKC - 1) / kKC);  // blocks holding rows < N
     if (p < 64 || p % 64 || n3 < 256 || n3 > kKC || nblk * kKC < N) return false;
     StageTimer tm("mode3_fwd", s, 2.0 * N * n3 * p, 8.0 * (N * n3 + N * p + n3 * p));
-    DeviceBuffer bq(sizeof(double) * nblk * n3 * p);
-    {
-        const int64_t total = nblk * n3 * p;
-        fold_q_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, 148 * 16), 256, 0, s>>>(td.sc.d(), Q, n3, p,
-                                                                                              total, bq.d());
-        count_launch();
-        check_launch("fold_q");
-    }
+    // B_b = diag(sigma_b) Q per 4096-row block b of T (its column scales vary
+    // along the contraction index, so they fold into Q's rows, not into the
+    // epilogue): split straight from Q with the block's row scales (the 1 GB of
+    // scaled copies at cfg5 used to be written by a fold kernel and read back)
     OzakiDigits bd;
-    bd.split(bq.d(), n3, n3 * p, n3, p, n3, nblk, s, nullptr, 0, 0, 0, nullptr, kSmax);
+    bd.split(Q, n3, n3 * p, n3, p, n3, nblk, s, nullptr, 0, 0, 0, nullptr, kSmax, 0, 0, nullptr, 0, false,
+             td.sc.d());
     CUtensorMap ma, mb;
     if (!make_digit_map(&ma, td.D.as<int8_t>(), td.KCp, n3, nblk * td.nd, 64) ||
         !make_digit_map(&mb, bd.D.as<int8_t>(), bd.KCp, p, nblk * bd.nd, 64))

@@ -23,13 +23,16 @@ struct OzakiDigits {
     void split(const double* X, int64_t ldx, int64_t stride, int64_t rows, int64_t cols, int64_t KC, int64_t nblk,
                cudaStream_t s, const int* zmap = nullptr, int64_t nz = 0, int64_t chunk = 0, int64_t per = 0,
                int* nonfinite = nullptr, int ndig = 6, int64_t block_base = 0, int64_t alloc_blocks = 0,
-               const double* fixed_max = nullptr, int nwrite = 0, bool trans_src = false);
+               const double* fixed_max = nullptr, int nwrite = 0, bool trans_src = false,
+               const double* rowscale = nullptr);
     // fixed_max (device, per block): a bound on max|x| over the whole block,
     // giving every column the same scale (symmetric operands, sym_a below).
     // block_base / alloc_blocks: this call's nblk_ blocks land at block_base of an
     // allocation of max(nblk_, alloc_blocks) blocks (streamed row groups).
     // nwrite (0: all): only the leading nwrite digit planes are written, for
     // operands of reduced-level products (levels <= nwrite read no others).
+    // rowscale (batched blocks only): every block reads the same source X
+    // (no b * stride) with row k scaled by rowscale[b * rows + k].
     // trans_src (batched blocks only): element (k, c) of block b is
     // X[b * stride + c + k * ldx], the transpose of the usual layout.
 };
